@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""SAA samples/sec for risk(z) + grad_risk(z) through the MR-DINO surrogate
+on B200 (BASELINE.json metric), default workload = BASELINE config 2:
+elliptic 2D 129x129, MLP 228->512x4->128 (ELU, residual), N=16384 samples
+per GPU, one step = mean+variance AND exact CVaR_0.95 risk + gradient.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N>1, NCCL); per-GPU work fixed (weak
+scaling); `value` = all ranks' samples / max-over-ranks device time.
+See DESIGN.md section "Measurement" for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SAA samples/sec for risk+grad_risk(z)"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--gemm", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-samples", type=int, default=768, help="bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def risks_for(cfg):
+    out = []
+    for r in cfg.risks:
+        d = dict(kind=r.kind, beta=r.beta, eps=r.eps, alpha=cfg.alpha)
+        out.append(d)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
+                 str(self.device), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.lines:
+            return None
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1", "0x1"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference algorithm (oracle port, forward-mode Jacobian as
+# ouukit's SurrogateEvaluator) on a bounded sample of the same workload
+
+
+def cpu_reference_rate(cfg, seed, n_cpu, reps=1):
+    from oracle import mrdino_ref as ref
+    from paper_2305_20053_b200 import workloads as wl
+    p = wl.make_problem(cfg.with_samples(n_cpu), seed=seed, count=n_cpu)
+    m = ref.as_oracle(p)
+    form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    z = p.z.astype(np.float64)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        Q, G = ref.evaluate_forward_mode(m, p.m_r, z, form)
+        for r in cfg.risks:
+            ref.saa_objective(Q, G, z, ref.Risk(r.kind, beta=r.beta, eps=r.eps, alpha=cfg.alpha),
+                              t=float(np.quantile(Q, r.beta)) if r.kind == "cvar" else None)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return n_cpu / best, best
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference's own CPU algorithm (oracle port)."""
+    if rank != 0:
+        return
+    n_step = 256
+    from oracle import mrdino_ref as ref
+    from paper_2305_20053_b200 import workloads as wl
+    p = wl.make_problem(cfg.with_samples(n_step), seed=args.seed, count=n_step)
+    m = ref.as_oracle(p)
+    form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    z = p.z.astype(np.float64)
+
+    def step():
+        Q, G = ref.evaluate_forward_mode(m, p.m_r, z, form)
+        for r in cfg.risks:
+            ref.saa_objective(Q, G, z, ref.Risk(r.kind, beta=r.beta, eps=r.eps, alpha=cfg.alpha),
+                              t=float(np.quantile(Q, r.beta)) if r.kind == "cvar" else None)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = n_step * args.steps / dt
+    sample = f"{n_step} samples of {cfg.name} per step (forward-mode z-Jacobian, fp64, numpy BLAS threads)"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": cfg.name, "description": cfg.description, "n_samples_per_step": n_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2305_20053_b200 import workloads as wl
+    cfg = wl.WORKLOADS[args.config]
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2305_20053_b200 import Engine
+    n_loc = cfg.n_samples
+    p = wl.make_problem(cfg, seed=args.seed, start=rank * n_loc, count=n_loc)
+    eng = Engine(p, max_samples=n_loc, device=local_rank, gemm=args.gemm)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    eng.set_tracking(p.c, p.q0)
+    eng.set_samples(torch.from_numpy(p.m_r).cuda(), global_offset=rank * n_loc)   # resident in HBM
+    risks = risks_for(cfg)
+    z = p.z.astype(np.float64)
+    sharded = None
+    if world > 1:
+        from paper_2305_20053_b200.distributed import ShardedObjective, TorchComm
+        sharded = ShardedObjective(eng, TorchComm(dist), n_global=n_loc * world)
+
+    def step():
+        if sharded is not None:
+            return sharded.eval_multi(z, risks)
+        return eng.eval_multi(z, risks)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+
+    # ---- timed region: device time per step (CUDA events on the engine's stream)
+    launches0 = eng.kernel_launches()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()                     # L2 flush between steps (untimed)
+            starts[i].record(stream)
+            res = step()
+            ends[i].record(stream)
+        barrier()
+    launches = eng.kernel_launches() - launches0
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_total = float(t_local.item())
+    ms_step = ms_total / args.steps
+    value = n_loc * world * args.steps / (ms_total / 1e3)
+
+    # ---- profiled pass (same steps, per-launch events by kernel class)
+    eng.profile(True)
+    for i in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    prof = eng.profile_read()
+    eng.profile(False)
+
+    # ---- e2e through the public API with host buffers (wall clock incl. H2D/D2H)
+    from paper_2305_20053_b200 import _lib
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        res = step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    t_e2e = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = n_loc * world * args.steps / float(t_e2e.item())
+    kmax = sum(max(int(np.ceil((1 - r["beta"]) * n_loc * world - 1e-9)), 1) for r in risks
+               if r["kind"] == "cvar_exact")
+    h2d = 8 * cfg.d_z
+    d2h = len(risks) * 8 * (_lib.STATS_LEN + eng.partial_len()) + 4 * kmax
+
+    # ---- roofline of the dominant kernel class
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_src = "measured bf16 sustained (MEASURED_PEAKS.json)" if peaks else "fallback"
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    step_ms_prof = sum(v["ms"] for v in prof.values())
+    if d["flops"] > 0:
+        achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": None, "kernel": dom,
+                "launches": d["launches"], "avg_launch_us": 1e3 * d["ms"] / max(d["launches"], 1),
+                "share_of_step": d["ms"] / step_ms_prof, "peak_source": peak_src,
+                "frac_of_bf16x3_effective": achieved / (peak_tf / 3.0)}
+    else:
+        bw = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        peak_bw = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": bw, "peak": peak_bw, "unit": "GB/s", "frac": bw / peak_bw,
+                "traffic": None, "kernel": dom, "launches": d["launches"],
+                "share_of_step": d["ms"] / step_ms_prof, "peak_source": peak_src}
+    tf_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf_path):
+        try:
+            roof["traffic"] = json.load(open(tf_path)).get(args.config, {}).get(dom)
+        except Exception:
+            pass
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, secs = cpu_reference_rate(cfg, args.seed, args.cpu_samples, reps=2)
+        cpu = {"value": rate, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+               "sample": f"{args.cpu_samples} samples of {cfg.name}, reference forward-mode algorithm "
+                         f"(oracle port, fp64 numpy), both risks, best of 2 ({secs:.1f} s)"}
+
+    if rank == 0:
+        per_class = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps}
+                     for k, v in prof.items() if v["launches"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "description": cfg.description, "n_samples_per_gpu": n_loc,
+                       "global_samples": n_loc * world,
+                       "risks": [f"{r['kind']}(beta={r['beta']})" for r in risks], "alpha": cfg.alpha,
+                       "gemm": args.gemm, "l2": "flushed between steps (256 MiB write, untimed)",
+                       "parallelism": f"dp{world} sample shards"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "Engine.eval_multi (host z in, host value/grad/indices out)"},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "kernel_classes": per_class,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,210 @@
+/*
+ * saadino.h -- C ABI of the B200 SAA risk / control-gradient engine for
+ * MR-DINO surrogates (arxiv 2305.20053).  Plain C: pointers, sizes, int
+ * status codes; no torch or C++ types.  Library: paper_2305_20053_b200/libsaadino.so
+ *
+ * One handle = one CUDA device = one shard of the SAA sample set.  Across
+ * processes (one per GPU) the caller combines the handle's small exchange
+ * buffers with its own collective; a single-process
+ * caller uses sdn_eval(), which chains every phase locally.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/ouukit):
+ *   sdn_set_model      <- SurrogateModel fields / init_model           surrogate.py:149-157, 241-256
+ *   sdn_set_tracking   <- build_tracking_form / ReducedTrackingForm     pod.py:46-62, 104-110
+ *   sdn_set_decoder    <- PODBasis.lift + TrackingTarget (full frame)   pod.py:36-40, riskopt.py:89-109
+ *   sdn_set_samples    <- SurrogateEvaluator.__init__ (m_r copy)        riskopt.py:166-172
+ *   sdn_encode_fields  <- KLEBasis.encode, pipeline's per-sample loop   randfield.py:67-72, pipeline.py:357-360
+ *   sdn_eval           <- saa_objective(prob, z, t) over the surrogate  riskopt.py:227-243 (+178-194)
+ *   sdn_eval_samples   <- SurrogateEvaluator.__call__ -> (Q, G)         riskopt.py:178-194
+ *   sdn_forward_batch  <- SurrogateModel.forward_batch                  surrogate.py:187-191
+ *   sdn_jacobian_batch <- SurrogateModel.z_jacobian_batch (+ decode)    surrogate.py:229-233, tests/test_acceptance.py:326
+ *   sdn_select_topk    <- mc_cvar / mc_var order statistics             riskopt.py:56-82
+ *
+ * Errors: every function returns SDN_OK (0) or a negative code; the message
+ * of the last failure on the calling thread is sdn_last_error().  Argument
+ * errors mirror the reference's ValueError cases (riskopt.py:28,64-67,
+ * 211-216,236-237; surrogate.py:188-189).  Non-finite samples propagate as
+ * NaN into the value and gradient, which minimize() treats as a rejected
+ * step (riskopt.py:341).
+ */
+#ifndef SAADINO_H
+#define SAADINO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDN_OK 0
+#define SDN_ERR_ARG (-1)     /* invalid argument (reference: ValueError) */
+#define SDN_ERR_CUDA (-2)    /* CUDA runtime failure */
+#define SDN_ERR_STATE (-3)   /* call order (e.g. eval before set_model) */
+#define SDN_ERR_NOMEM (-4)
+
+/* activations: identity/tanh/softplus/sigmoid as surrogate.py:42-63; elu (BASELINE) */
+#define SDN_ACT_IDENTITY 0
+#define SDN_ACT_TANH 1
+#define SDN_ACT_SOFTPLUS 2
+#define SDN_ACT_SIGMOID 3
+#define SDN_ACT_ELU 4
+
+/* risk kinds: mean / smoothed CVaR as RiskSpec (riskopt.py:204-216), plus
+ * mean + beta*variance and exact CVaR by device selection (BASELINE) */
+#define SDN_RISK_MEAN 0
+#define SDN_RISK_CVAR_SMOOTH 1
+#define SDN_RISK_MEANVAR 2
+#define SDN_RISK_CVAR_EXACT 3
+
+/* QoI frame: reduced (pod.py:46-62) or decoded full frame (riskopt.py:103-108) */
+#define SDN_QOI_REDUCED 0
+#define SDN_QOI_DECODED 1
+
+/* GEMM back end for the MLP chain */
+#define SDN_GEMM_AUTO 0
+#define SDN_GEMM_SIMT 1      /* fp32 FFMA */
+#define SDN_GEMM_TC 2        /* tcgen05 bf16x3 split, fp32 accumulate in TMEM */
+
+typedef struct sdn_handle sdn_handle;
+
+typedef struct sdn_config {
+  int32_t n_layers;          /* number of weight matrices (hidden + output) */
+  const int32_t* widths;     /* n_layers + 1 widths; widths[0] = r_m + r_z */
+  int32_t r_m;               /* field coefficients */
+  int32_t d_z;               /* controls (V_z is d_z x r_z, r_z = widths[0] - r_m) */
+  int32_t activation;        /* SDN_ACT_* */
+  int32_t residual;          /* 1: equal-width hidden layers add their input */
+  int32_t gemm;              /* SDN_GEMM_* */
+  int32_t device;            /* CUDA ordinal */
+  int64_t max_samples;       /* capacity of this shard */
+} sdn_config;
+
+typedef struct sdn_risk {
+  int32_t kind;              /* SDN_RISK_* */
+  int32_t qoi;               /* SDN_QOI_* */
+  double beta;               /* CVaR level / variance weight */
+  double eps;                /* smoothing width (smoothed CVaR) */
+  double t;                  /* auxiliary variable (smoothed CVaR) */
+  double alpha;              /* control cost alpha ||z||^2 */
+  int32_t need_grad;         /* 0: value only (line-search trials) */
+} sdn_risk;
+
+typedef struct sdn_result {
+  double value;
+  double grad_t;             /* smoothed CVaR only, else 0 */
+  int64_t n_samples;         /* global sample count */
+  int64_t n_selected;        /* CVaR exact: k; smoothed: active samples */
+  double q_mean, q_var;      /* sample moments of Q (for reporting) */
+} sdn_result;
+
+const char* sdn_last_error(void);
+int sdn_version(void);
+
+int sdn_create(const sdn_config* cfg, sdn_handle** out);
+int sdn_destroy(sdn_handle* h);
+
+/* Use an external CUDA stream (cudaStream_t) for all work; 0 = own stream. */
+int sdn_set_stream(sdn_handle* h, void* stream);
+int sdn_synchronize(sdn_handle* h);
+
+/* Weights W_l (n_out x n_in row-major, torch Linear layout) and biases;
+ * in_scale (r_m), out_mean/out_std (r_u), Vz (d_z x r_z row-major, NULL = I).
+ * All host pointers (float32). */
+int sdn_set_model(sdn_handle* h, const float* const* W, const float* const* b,
+                  const float* in_scale, const float* out_mean, const float* out_std,
+                  const float* Vz);
+
+/* Reduced tracking form c (r_u), q0. */
+int sdn_set_tracking(sdn_handle* h, const float* c, double q0);
+
+/* Decoder U (d_u x r_u row-major), bias (d_u), lumped mass diag (d_u),
+ * target (d_u): enables SDN_QOI_DECODED. */
+int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubias,
+                    const float* Mdiag, const float* u_target);
+
+/* Encoded samples m_r (n x r_m row-major).  on_device != 0: device pointer.
+ * global_offset = index of row 0 in the global sample set (CVaR tie-break). */
+int sdn_set_samples(sdn_handle* h, const float* m_r, int64_t n, int64_t global_offset,
+                    int32_t on_device);
+
+/* Encode nodal fields on the device: m_r = V_m^T diag(M) (m - m_mean).
+ * m (n x d_m), Vm (d_m x r_m), Mdiag (d_m); host pointers unless on_device.
+ * Stores the result as this shard's samples (like sdn_set_samples). */
+int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m,
+                      const float* Vm, const float* Mdiag, float m_mean,
+                      int64_t global_offset, int32_t on_device);
+
+/* Full single-process evaluation: value, grad_z (d_z), CVaR indices.
+ * z: host (d_z) float64.  grad_z: host (d_z) float64 or NULL.
+ * cvar_idx: host int64 (k) or NULL (exact CVaR). */
+int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* res,
+             double* grad_z, int64_t* cvar_idx);
+
+/* Several risk functionals sharing ONE forward pass (e.g. mean+variance and
+ * exact CVaR, BASELINE config 2).  res[n_risks]; grads (n_risks x d_z) or
+ * NULL; cvar_idx receives each exact-CVaR selection in order, or NULL. */
+int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks,
+                   sdn_result* res, double* grads, int64_t* cvar_idx);
+
+/* Per-sample evaluator protocol: Q (n) and G (n x d_z) as float64 host arrays. */
+int sdn_eval_samples(sdn_handle* h, const double* z, int32_t qoi, double* Q, double* G);
+
+/* Surrogate primal / Jacobian on arbitrary rows (host pointers, float32):
+ * m_r (n x r_m), z (n x d_z, one control per row as forward_batch takes it);
+ * phi (n x r_u); J (n x r_u x d_z), or decoded U J (n x d_u x d_z) when
+ * decoded != 0 (needs sdn_set_decoder). */
+int sdn_forward_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n,
+                      float* phi);
+int sdn_jacobian_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n,
+                       int32_t decoded, float* J);
+
+/* Decoded states u = U phi + b for the rows' phi (n x r_u) -> (n x d_u). */
+int sdn_lift(sdn_handle* h, const float* phi, int64_t n, float* u);
+
+/* Order statistics on device: indices of the k largest of values (n, float64,
+ * host or device), ordered by value desc then index asc.  idx: host int64. */
+int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k,
+                    int32_t on_device, int64_t* idx);
+
+/* ---- multi-process phases (one handle per rank) -------------------------
+ * The caller owns two device exchange buffers (float64) it can all-reduce /
+ * all-gather with its own collective on the handle's stream:
+ *   stats   : SDN_STATS_LEN doubles    (sum-reduce)
+ *   partial : sdn_partial_len(h) doubles (sum-reduce)
+ *   cand    : 2*k doubles per rank (exact CVaR candidates; all-gather)
+ * Sequence: eval_forward -> [allreduce stats] -> [cvar_exact: eval_candidates
+ * -> allgather cand -> eval_select] -> eval_backward -> [allreduce partial]
+ * -> eval_finish.  Every phase is asynchronous on the handle's stream. */
+#define SDN_STATS_LEN 8
+int sdn_partial_len(sdn_handle* h);
+int sdn_eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk,
+                     double* stats_dev);
+int sdn_eval_candidates(sdn_handle* h, int64_t k, double* cand_dev);
+int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, int64_t k);
+int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev);
+int sdn_eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev,
+                    sdn_result* res, double* grad_z);
+
+/* Local per-sample outputs of the last evaluation (device pointers, read-only;
+ * valid until the next call): Q (n, float64). */
+int sdn_last_q(sdn_handle* h, const double** q_dev, int64_t* n);
+
+/* Instrumentation.  sdn_profile(h, 1) starts CUDA-event timing of every
+ * launch by kernel class (0 fwd GEMM, 1 reverse GEMM, 2 QoI+moments,
+ * 3 top-k select, 4 compaction, 5 seeds, 6 column sums, 7 finalise,
+ * 8 zbias, 9 other); sdn_profile_read returns per-class device ms,
+ * algorithmic flops and bytes, and launch counts. */
+#define SDN_PROF_CLASSES 10
+int sdn_profile(sdn_handle* h, int32_t enable);
+int sdn_profile_read(sdn_handle* h, int32_t n_cls, double* ms, double* flops, double* bytes,
+                     int64_t* count);
+
+/* Number of kernels this handle has launched (lifetime). */
+int64_t sdn_kernel_launches(sdn_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAADINO_H */

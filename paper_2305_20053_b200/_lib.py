@@ -1,0 +1,116 @@
+"""ctypes binding of libsaadino.so (the C ABI in include/saadino.h).
+
+The product path has no CPU fallback: if the shared library is missing this
+module raises at import, naming the build command.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsaadino.so")
+
+SDN_OK = 0
+ACT = {"identity": 0, "tanh": 1, "softplus": 2, "sigmoid": 3, "elu": 4}
+RISK = {"mean": 0, "cvar": 1, "meanvar": 2, "cvar_exact": 3}
+QOI = {"reduced": 0, "decoded": 1}
+GEMM = {"auto": 0, "simt": 1, "tc": 2}
+STATS_LEN = 8
+PROF_CLASSES = ["fwd_gemm", "bwd_gemm", "qoi", "select", "compact", "seed", "colsum", "finalize", "zbias",
+                "other"]
+
+
+class Config(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("widths", C.POINTER(C.c_int32)), ("r_m", C.c_int32),
+                ("d_z", C.c_int32), ("activation", C.c_int32), ("residual", C.c_int32),
+                ("gemm", C.c_int32), ("device", C.c_int32), ("max_samples", C.c_int64)]
+
+
+class Risk(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("qoi", C.c_int32), ("beta", C.c_double), ("eps", C.c_double),
+                ("t", C.c_double), ("alpha", C.c_double), ("need_grad", C.c_int32)]
+
+
+class Result(C.Structure):
+    _fields_ = [("value", C.c_double), ("grad_t", C.c_double), ("n_samples", C.c_int64),
+                ("n_selected", C.c_int64), ("q_mean", C.c_double), ("q_var", C.c_double)]
+
+
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_F = C.POINTER(C.c_float)
+_I64 = C.POINTER(C.c_int64)
+
+# name -> (restype, argtypes); kept in sync with include/saadino.h
+SIGNATURES = {
+    "sdn_last_error": (C.c_char_p, []),
+    "sdn_version": (C.c_int, []),
+    "sdn_create": (C.c_int, [C.POINTER(Config), C.POINTER(_P)]),
+    "sdn_destroy": (C.c_int, [_P]),
+    "sdn_set_stream": (C.c_int, [_P, _P]),
+    "sdn_synchronize": (C.c_int, [_P]),
+    "sdn_set_model": (C.c_int, [_P, C.POINTER(_F), C.POINTER(_F), _F, _F, _F, _F]),
+    "sdn_set_tracking": (C.c_int, [_P, _F, C.c_double]),
+    "sdn_set_decoder": (C.c_int, [_P, C.c_int64, _F, _F, _F, _F]),
+    "sdn_set_samples": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int32]),
+    "sdn_encode_fields": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _F, _F, C.c_float, C.c_int64, C.c_int32]),
+    "sdn_eval": (C.c_int, [_P, _D, C.POINTER(Risk), C.POINTER(Result), _D, _I64]),
+    "sdn_eval_multi": (C.c_int, [_P, _D, C.POINTER(Risk), C.c_int32, C.POINTER(Result), _D, _I64]),
+    "sdn_eval_samples": (C.c_int, [_P, _D, C.c_int32, _D, _D]),
+    "sdn_forward_batch": (C.c_int, [_P, _F, _F, C.c_int64, _F]),
+    "sdn_jacobian_batch": (C.c_int, [_P, _F, _F, C.c_int64, C.c_int32, _F]),
+    "sdn_lift": (C.c_int, [_P, _F, C.c_int64, _F]),
+    "sdn_select_topk": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int32, _I64]),
+    "sdn_partial_len": (C.c_int, [_P]),
+    "sdn_eval_forward": (C.c_int, [_P, _D, C.POINTER(Risk), _P]),
+    "sdn_eval_candidates": (C.c_int, [_P, C.c_int64, _P]),
+    "sdn_eval_select": (C.c_int, [_P, _P, C.c_int32, C.c_int64]),
+    "sdn_eval_backward": (C.c_int, [_P, _P, _P]),
+    "sdn_eval_finish": (C.c_int, [_P, _P, _P, C.POINTER(Result), _D]),
+    "sdn_last_q": (C.c_int, [_P, C.POINTER(_P), _I64]),
+    "sdn_kernel_launches": (C.c_int64, [_P]),
+    "sdn_profile": (C.c_int, [_P, C.c_int32]),
+    "sdn_profile_read": (C.c_int, [_P, C.c_int32, _D, _D, _D, _I64]),
+}
+
+
+class SaadinoError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the SAA engine has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int, what: str = ""):
+    if rc != SDN_OK:
+        msg = lib.sdn_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise SaadinoError(f"{what} failed ({rc}): {msg}")
+
+
+def fptr(a):
+    return a.ctypes.data_as(_F)
+
+
+def dptr(a):
+    return a.ctypes.data_as(_D)
+
+
+def i64ptr(a):
+    return a.ctypes.data_as(_I64)

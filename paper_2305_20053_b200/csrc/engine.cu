@@ -1,0 +1,1247 @@
+// engine.cu -- sdn_handle and the C ABI declared in include/saadino.h.
+//
+// One handle owns one device's shard of the SAA sample set, the replicated
+// surrogate (weights, projections), the tracking form / decoder, and all
+// work buffers.  Per evaluation (reference saa_objective, riskopt.py:227-243,
+// over SurrogateEvaluator, riskopt.py:178-194) the device runs:
+//   zbias (W1_z V_z^T z + b1, once)  ->  forward GEMM chain with fused
+//   bias/activation/residual epilogues (derivatives kept for the sweep)  ->
+//   QoI + fp64 block moments  ->  [collective on the moments]  ->
+//   [exact CVaR: radix top-k selection]  ->  weighted seeds on the active
+//   rows  ->  reverse GEMM chain  ->  fp64 column sums of dL/dS_1  ->
+//   projection through V_z W1_z^T to the d_z gradient  ->  [collective].
+// The reverse sweep replaces the reference's forward-mode z-Jacobian
+// (surrogate.py:195-233, >=95% of its CPU time): sum_i w_i dQ_i/dz is
+// linear in the seeds, so one weighted sweep gives the risk gradient.
+#include "../../include/saadino.h"
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "kernels.cuh"
+#include "gemm_tc.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace sdn;
+
+static thread_local std::string g_err;
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(SDN_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+#define CHECK_LAUNCH(h)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(SDN_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != SDN_OK) return rc_; \
+  } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline int pad4(int x) { return (x + 3) & ~3; }
+
+struct sdn_handle {
+  // ---- configuration
+  int L = 0;                    // weight matrices (hidden + output)
+  std::vector<int> w;           // widths, L + 1
+  int r_m = 0, r_z = 0, d_z = 0, d_zp = 0, r_u = 0, h1 = 0, maxw = 0;
+  int act = ACT_ELU, residual = 1, gemm = SDN_GEMM_AUTO, device = 0;
+  int ldx = 0;                  // padded [r_m | d_z] input width for per-row z
+  int64_t cap = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<void*> allocs;
+  int64_t launches = 0;
+  int num_sms = 148;
+
+  // ---- model (device)
+  bool have_model = false;
+  std::vector<float*> W;        // W[0] = W1[:, :r_m] * in_scale (h1 x r_m); W[l] as given
+  std::vector<float*> b;
+  std::vector<char> res;        // residual flag per layer
+  float* Wx = nullptr;          // h1 x ldx : [W0m' | Pz32 | 0]
+  double* Pz = nullptr;         // h1 x d_z  = W0z V_z^T (fp64)
+  float* Pz32 = nullptr;        // h1 x d_zp
+  float* Pz32t = nullptr;       // d_z x h1
+  float* omean = nullptr;
+  float* ostd = nullptr;
+  TcWeights tcw;                // bf16x3 operand copies for the tensor-core path
+
+  // ---- QoI
+  bool have_form = false;
+  float* c = nullptr;
+  double q0 = 0.0;
+  bool have_dec = false;
+  int64_t d_u = 0;
+  float* U = nullptr;           // d_u x r_u
+  float* ub = nullptr;          // d_u
+  float* Kg = nullptr;          // r_u x r_u Gram U^T M U
+  float* cdec = nullptr;        // r_u
+  double q0dec = 0.0;
+
+  // ---- samples
+  float* MR = nullptr;
+  int64_t n = 0, goff = 0;
+
+  // ---- work buffers
+  float* H[2] = {nullptr, nullptr};
+  std::vector<float*> D;        // per hidden layer, cap x w[l+1]
+  float* Y = nullptr;           // cap x r_u (phi)
+  float* KPhi = nullptr;        // cap x r_u
+  double* Q = nullptr;          // cap
+  float* E = nullptr;           // cap x r_u (seeds, compacted)
+  float* G = nullptr;           // cap x maxw (residual gradient stream)
+  float* Ub[2] = {nullptr, nullptr};
+  float* Gz = nullptr;          // cap x d_zp (per-sample G)
+  int* rowidx = nullptr;
+  int* counts = nullptr;
+  int* offs = nullptr;
+  int* n_act_dev = nullptr;
+  uint8_t* sel = nullptr;
+  double* qpart = nullptr;      // qgrid x STATS_LEN
+  int qgrid = 0;
+  double* cpart = nullptr;      // crb x maxw
+  int crb = 0;
+  double* stats_loc = nullptr;  // STATS_LEN
+  double* partial_loc = nullptr;
+  double* zdev = nullptr;       // d_z
+  float* zb = nullptr;          // h1
+  double* cand_vals = nullptr;  // candidate scratch (exact CVaR, multi-rank)
+  double* cand_gidx = nullptr;
+  uint8_t* cand_mask = nullptr;
+  int64_t cand_cap = 0;
+  // pinned staging
+  double* hz = nullptr;         // d_z
+  double* hstats = nullptr;     // STATS_LEN
+  double* hpart = nullptr;      // partial len
+
+  // ---- profiling (per kernel class CUDA-event timing, sdn_profile)
+  bool prof = false;
+  int pcls = 9;                 // class of the next GEMM launch (PC_OTHER)
+  int64_t prows = 0;            // its true row count (-1: device-side n_act)
+  struct ProfRec { int cls; cudaEvent_t a, b; double flops; double bytes; int64_t rows; double per_row; };
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+
+  // ---- evaluation state
+  sdn_risk risk{};
+  double shift = 0.0;
+  bool have_mean = false;
+  double last_mean = 0.0;
+  bool fwd_done = false;
+  bool selected = false;        // exact CVaR selection done
+  int64_t kk = 0;               // exact CVaR k (global)
+  bool compacted = false;
+  double hzz = 0.0;             // z.z of the current evaluation
+  std::vector<double> zhost;
+
+  int plen() const { return d_z + 2; }
+};
+
+template <class T>
+static int dalloc(sdn_handle* h, T** p, size_t count) {
+  void* q = nullptr;
+  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) return fail(SDN_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  h->allocs.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return SDN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// profiling: events bracket each launch on the handle's stream
+
+enum ProfClass { PC_FWD_GEMM = 0, PC_BWD_GEMM, PC_QOI, PC_SELECT, PC_COMPACT, PC_SEED, PC_COLSUM, PC_FINAL,
+                 PC_ZBIAS, PC_OTHER, PC_N };
+
+static cudaEvent_t prof_event(sdn_handle* h) {
+  if (h->pool_used == h->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->pool.push_back(e);
+  }
+  return h->pool[h->pool_used++];
+}
+
+struct ProfScope {
+  sdn_handle* h; int cls; double flops, bytes; int64_t rows; double per_row; cudaEvent_t a = nullptr;
+  // flops/bytes are totals when rows >= 0; when rows < 0 the count is the
+  // device-side n_act and per_row scales it at read time
+  ProfScope(sdn_handle* h_, int cls_, double flops_, double bytes_, int64_t rows_ = 0, double per_row_ = 0.0)
+      : h(h_), cls(cls_), flops(flops_), bytes(bytes_), rows(rows_), per_row(per_row_) {
+    if (h->prof) { a = prof_event(h); cudaEventRecord(a, h->stream); }
+  }
+  ~ProfScope() {
+    if (!h->prof) return;
+    cudaEvent_t b = prof_event(h);
+    cudaEventRecord(b, h->stream);
+    h->recs.push_back({cls, a, b, flops, bytes, rows, per_row});
+  }
+};
+
+// ---------------------------------------------------------------------------
+// GEMM dispatch
+
+static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int BM, int BN, int TM, int TN, bool AT, bool BT, class Epi>
+static void launch_simt(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const float* A,
+                        int64_t lda, const float* B, int64_t ldb, Epi epi, bool vec) {
+  dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN));
+  dim3 block((BM / TM) * (BN / TN));
+  if (vec)
+    gemm_simt_kernel<BM, BN, 16, TM, TN, AT, BT, true, Epi>
+        <<<grid, block, 0, h->stream>>>(M, Mdev, N, K, A, lda, B, ldb, epi);
+  else
+    gemm_simt_kernel<BM, BN, 16, TM, TN, AT, BT, false, Epi>
+        <<<grid, block, 0, h->stream>>>(M, Mdev, N, K, A, lda, B, ldb, epi);
+  h->launches++;
+}
+
+// C = opA(A) opB(B) with a fused epilogue; M rows (Mdev: device row count
+// upper-bounded by M, for compacted sweeps).  Routes to tcgen05 when the
+// handle allows it and the shape qualifies.
+template <bool AT, bool BT, class Epi>
+static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const float* A, int64_t lda,
+                const float* B, int64_t ldb, Epi epi, const TcOperand* tcB = nullptr,
+                const TcOperand* tcA = nullptr) {
+  if (M <= 0 || N <= 0) return SDN_OK;
+  const int64_t rows = h->prows ? h->prows : M;
+  h->prows = 0;
+  ProfScope ps(h, h->pcls, rows >= 0 ? 2.0 * rows * N * K : 0.0, 0.0, rows, 2.0 * N * K);
+  h->pcls = PC_OTHER;
+  if (h->gemm != SDN_GEMM_SIMT && !AT && tcB && tcA &&
+      tc_gemm_supported(M, N, K)) {
+    int rc = tc_gemm<Epi>(h->stream, M, Mdev, N, K, *tcA, *tcB, epi);
+    h->launches += 2;
+    if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed");
+    CHECK_LAUNCH(h);
+    return SDN_OK;
+  }
+  bool vec = !AT && (K % 4 == 0) && (lda % 4 == 0) && (ldb % 4 == 0) && al16(A) && al16(B) &&
+             (BT || N % 4 == 0);
+  int64_t tiles128 = cdiv(M, 128) * cdiv(N, 128);
+  if (tiles128 >= 2 * h->num_sms)
+    launch_simt<128, 128, 8, 8, AT, BT>(h, M, Mdev, N, K, A, lda, B, ldb, epi, vec);
+  else
+    launch_simt<64, 64, 4, 4, AT, BT>(h, M, Mdev, N, K, A, lda, B, ldb, epi, vec);
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// forward / backward building blocks
+
+// layer chain on `nrows` rows.  Layer 0 input: X (ld0, K0) with weight W0 and
+// bias0 (either MR + zb, or [m_r | z] + b0).  store_D keeps act' for the sweep.
+static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0, int K0,
+                       const float* W0, int64_t ldW0, const float* bias0, bool store_D,
+                       float* phi_out, const TcOperand* tcX0) {
+  const int L = h->L;
+  int cur = 0;
+  const float* in = X;
+  int64_t ldin = ld0;
+  for (int l = 0; l < L; ++l) {
+    const int n_in = h->w[l], n_out = h->w[l + 1];
+    const float* Wl = (l == 0) ? W0 : h->W[l];
+    const int64_t ldW = (l == 0) ? ldW0 : n_in;
+    const int K = (l == 0) ? K0 : n_in;
+    const float* bl = (l == 0) ? bias0 : h->b[l];
+    const bool tc = h->tcw.enabled && (l > 0 || tcX0);
+    const TcOperand* tA = !tc ? nullptr : (l == 0) ? tcX0 : &h->tcw.act[cur];
+    const TcOperand* tB = !tc ? nullptr : &h->tcw.fwd[l];
+    h->pcls = PC_FWD_GEMM;
+    h->prows = nrows;
+    if (l == L - 1) {
+      EpiAffine e{bl, h->ostd, h->omean, phi_out, (int64_t)n_out};
+      TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA)));
+    } else {
+      float* out = h->H[(l == 0) ? 0 : 1 - cur];
+      EpiFwdHidden e{bl, (h->res[l] ? in : nullptr), out, store_D ? h->D[l] : nullptr,
+                     (int64_t)n_out, h->act};
+      TcEpiSplit split = h->tcw.enabled ? TcEpiSplit{&h->tcw.act[(l == 0) ? 0 : 1 - cur]} : TcEpiSplit{nullptr};
+      TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW,
+                             TcChain<EpiFwdHidden>{e, split}, tB, tA)));
+      cur = (l == 0) ? 0 : 1 - cur;
+      in = out;
+      ldin = n_out;
+    }
+  }
+  return SDN_OK;
+}
+
+// reverse sweep over `nmax` (device count n_act_dev) compacted rows from the
+// seeds E; leaves dL/dS_0 (rows x w[1]) in *u0_out.
+static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const int* rowidx,
+                        float** u0_out, int64_t rows_hint) {
+  const int L = h->L;
+  if (L == 1) { *u0_out = h->E; return SDN_OK; }
+  int cur = 0;
+  {
+    const int K = h->w[L], N = h->w[L - 1];
+    EpiBwd e{nullptr, h->res[L - 2] ? h->G : nullptr, h->D[L - 2], (int64_t)N, rowidx, h->Ub[cur],
+             (int64_t)N};
+    TcEpiSplit split = h->tcw.enabled ? TcEpiSplit{&h->tcw.act[cur]} : TcEpiSplit{nullptr};
+    h->pcls = PC_BWD_GEMM;
+    h->prows = rows_hint;
+    TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, h->E, K, h->W[L - 1], N,
+                            TcChain<EpiBwd>{e, split}, h->tcw.enabled ? &h->tcw.bwd[L - 1] : nullptr,
+                            h->tcw.enabled ? &h->tcw.seed : nullptr)));
+  }
+  for (int l = L - 2; l >= 1; --l) {
+    const int K = h->w[l + 1], N = h->w[l];
+    EpiBwd e{h->res[l] ? h->G : nullptr, h->res[l - 1] ? h->G : nullptr, h->D[l - 1], (int64_t)N,
+             rowidx, h->Ub[1 - cur], (int64_t)N};
+    TcEpiSplit split = h->tcw.enabled ? TcEpiSplit{&h->tcw.act[1 - cur]} : TcEpiSplit{nullptr};
+    h->pcls = PC_BWD_GEMM;
+    h->prows = rows_hint;
+    TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, h->Ub[cur], K, h->W[l], N,
+                            TcChain<EpiBwd>{e, split}, h->tcw.enabled ? &h->tcw.bwd[l] : nullptr,
+                            h->tcw.enabled ? &h->tcw.act[cur] : nullptr)));
+    cur = 1 - cur;
+  }
+  *u0_out = h->Ub[cur];
+  return SDN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char* sdn_last_error(void) { return g_err.c_str(); }
+int sdn_version(void) { return 1; }
+
+int sdn_create(const sdn_config* cfg, sdn_handle** out) {
+  if (!cfg || !out) return fail(SDN_ERR_ARG, "null argument");
+  if (cfg->n_layers < 1 || !cfg->widths) return fail(SDN_ERR_ARG, "need at least one layer");
+  for (int i = 0; i <= cfg->n_layers; ++i)
+    if (cfg->widths[i] < 1) return fail(SDN_ERR_ARG, "all widths must be positive");
+  if (cfg->r_m < 1 || cfg->d_z < 1 || cfg->r_m >= cfg->widths[0])
+    return fail(SDN_ERR_ARG, "need 1 <= r_m < widths[0] and d_z >= 1");
+  if (cfg->activation < 0 || cfg->activation > 4) return fail(SDN_ERR_ARG, "unknown activation");
+  if (cfg->max_samples < 1) return fail(SDN_ERR_ARG, "max_samples must be >= 1");
+  for (int i = 1; i <= cfg->n_layers; ++i)
+    if (cfg->widths[i] % 4 != 0) return fail(SDN_ERR_ARG, "layer output widths must be multiples of 4");
+  if (cfg->r_m % 4 != 0) return fail(SDN_ERR_ARG, "r_m must be a multiple of 4");
+
+  sdn_handle* h = new sdn_handle();
+  h->L = cfg->n_layers;
+  h->w.assign(cfg->widths, cfg->widths + cfg->n_layers + 1);
+  h->r_m = cfg->r_m;
+  h->r_z = h->w[0] - h->r_m;
+  h->d_z = cfg->d_z;
+  h->d_zp = pad4(cfg->d_z);
+  h->r_u = h->w[h->L];
+  h->h1 = h->w[1];
+  h->maxw = *std::max_element(h->w.begin() + 1, h->w.end());
+  h->act = cfg->activation;
+  h->residual = cfg->residual;
+  h->gemm = cfg->gemm;
+  h->device = cfg->device;
+  h->ldx = pad4(h->r_m + h->d_z);
+  h->cap = cfg->max_samples;
+  h->res.assign(h->L, 0);
+  for (int l = 1; l < h->L - 1; ++l) h->res[l] = (h->residual && h->w[l] == h->w[l + 1]) ? 1 : 0;
+
+  auto bail = [&](int rc) { sdn_destroy(h); return rc; };
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) { delete h; return fail(SDN_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete h; return fail(SDN_ERR_CUDA, "cudaStreamCreate failed"); }
+  h->own_stream = true;
+
+  const int64_t cap = h->cap;
+  int rc;
+  h->W.assign(h->L, nullptr);
+  h->b.assign(h->L, nullptr);
+  for (int l = 0; l < h->L; ++l) {
+    int n_in = (l == 0) ? h->r_m : h->w[l];
+    if ((rc = dalloc(h, &h->W[l], (size_t)h->w[l + 1] * n_in))) return bail(rc);
+    if ((rc = dalloc(h, &h->b[l], h->w[l + 1]))) return bail(rc);
+  }
+  if ((rc = dalloc(h, &h->Wx, (size_t)h->h1 * h->ldx))) return bail(rc);
+  if ((rc = dalloc(h, &h->Pz, (size_t)h->h1 * h->d_z))) return bail(rc);
+  if ((rc = dalloc(h, &h->Pz32, (size_t)h->h1 * h->d_zp))) return bail(rc);
+  if ((rc = dalloc(h, &h->Pz32t, (size_t)h->h1 * h->d_z))) return bail(rc);
+  if ((rc = dalloc(h, &h->omean, h->r_u))) return bail(rc);
+  if ((rc = dalloc(h, &h->ostd, h->r_u))) return bail(rc);
+  if ((rc = dalloc(h, &h->c, h->r_u))) return bail(rc);
+  if ((rc = dalloc(h, &h->MR, (size_t)cap * h->r_m))) return bail(rc);
+  for (int i = 0; i < 2; ++i) {
+    if ((rc = dalloc(h, &h->H[i], (size_t)cap * h->maxw))) return bail(rc);
+    if ((rc = dalloc(h, &h->Ub[i], (size_t)cap * h->maxw))) return bail(rc);
+  }
+  h->D.assign(std::max(h->L - 1, 0), nullptr);
+  for (int l = 0; l < h->L - 1; ++l)
+    if ((rc = dalloc(h, &h->D[l], (size_t)cap * h->w[l + 1]))) return bail(rc);
+  if ((rc = dalloc(h, &h->Y, (size_t)cap * h->r_u))) return bail(rc);
+  if ((rc = dalloc(h, &h->E, (size_t)cap * h->r_u))) return bail(rc);
+  if ((rc = dalloc(h, &h->G, (size_t)cap * h->maxw))) return bail(rc);
+  if ((rc = dalloc(h, &h->Q, cap))) return bail(rc);
+  if ((rc = dalloc(h, &h->rowidx, cap))) return bail(rc);
+  if ((rc = dalloc(h, &h->sel, cap))) return bail(rc);
+  const int nb1024 = (int)cdiv(cap, 1024);
+  if ((rc = dalloc(h, &h->counts, nb1024))) return bail(rc);
+  if ((rc = dalloc(h, &h->offs, nb1024))) return bail(rc);
+  if ((rc = dalloc(h, &h->n_act_dev, 1))) return bail(rc);
+  h->qgrid = (int)std::min<int64_t>(cdiv(cap, 8), 2 * h->num_sms);
+  if ((rc = dalloc(h, &h->qpart, (size_t)h->qgrid * STATS_LEN))) return bail(rc);
+  h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 256);
+  if ((rc = dalloc(h, &h->cpart, (size_t)h->crb * h->maxw))) return bail(rc);
+  if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
+  if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
+  if ((rc = dalloc(h, &h->zdev, h->d_z))) return bail(rc);
+  if ((rc = dalloc(h, &h->zb, h->h1))) return bail(rc);
+  if (cudaHostAlloc((void**)&h->hz, sizeof(double) * h->d_z, 0) != cudaSuccess ||
+      cudaHostAlloc((void**)&h->hstats, sizeof(double) * STATS_LEN, 0) != cudaSuccess ||
+      cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), 0) != cudaSuccess)
+    return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
+  h->tcw.enabled = false;
+  if (h->gemm != SDN_GEMM_SIMT) {
+    if ((rc = tc_alloc(h, h->tcw))) return bail(rc);
+  }
+  *out = h;
+  return SDN_OK;
+}
+
+int sdn_destroy(sdn_handle* h) {
+  if (!h) return SDN_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->U) cudaFree(h->U);
+  if (h->ub) cudaFree(h->ub);
+  if (h->Kg) cudaFree(h->Kg);
+  if (h->cdec) cudaFree(h->cdec);
+  if (h->KPhi) cudaFree(h->KPhi);
+  if (h->Gz) cudaFree(h->Gz);
+  if (h->cand_vals) cudaFree(h->cand_vals);
+  if (h->cand_gidx) cudaFree(h->cand_gidx);
+  if (h->cand_mask) cudaFree(h->cand_mask);
+  if (h->hz) cudaFreeHost(h->hz);
+  if (h->hstats) cudaFreeHost(h->hstats);
+  if (h->hpart) cudaFreeHost(h->hpart);
+  tc_free(h->tcw);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return SDN_OK;
+}
+
+int sdn_set_stream(sdn_handle* h, void* stream) {
+  if (!h) return fail(SDN_ERR_ARG, "null handle");
+  CU(cudaSetDevice(h->device));
+  if (stream) {
+    CU(cudaStreamSynchronize(h->stream));
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    h->stream = reinterpret_cast<cudaStream_t>(stream);
+    h->own_stream = false;
+  }
+  return SDN_OK;
+}
+
+int sdn_synchronize(sdn_handle* h) {
+  if (!h) return fail(SDN_ERR_ARG, "null handle");
+  CU(cudaStreamSynchronize(h->stream));
+  return SDN_OK;
+}
+
+int64_t sdn_kernel_launches(sdn_handle* h) { return h ? h->launches : -1; }
+
+int sdn_set_model(sdn_handle* h, const float* const* W, const float* const* b, const float* in_scale,
+                  const float* out_mean, const float* out_std, const float* Vz) {
+  if (!h || !W || !b || !in_scale || !out_mean || !out_std) return fail(SDN_ERR_ARG, "null argument");
+  CU(cudaSetDevice(h->device));
+  const int n0 = h->w[0], h1 = h->h1, r_m = h->r_m, r_z = h->r_z, d_z = h->d_z;
+  if (!Vz && r_z != d_z) return fail(SDN_ERR_ARG, "V_z = identity needs r_z == d_z");
+  // layer 0 split: W0m' = W0[:, :r_m] * in_scale ; Pz = W0[:, r_m:] V_z^T (fp64)
+  std::vector<float> w0m((size_t)h1 * r_m);
+  std::vector<double> pz((size_t)h1 * d_z, 0.0);
+  std::vector<float> pz32((size_t)h1 * h->d_zp, 0.0f), pz32t((size_t)d_z * h1), wx((size_t)h1 * h->ldx, 0.0f);
+  for (int c = 0; c < h1; ++c) {
+    const float* row = W[0] + (size_t)c * n0;
+    for (int j = 0; j < r_m; ++j) {
+      w0m[(size_t)c * r_m + j] = (float)((double)row[j] * (double)in_scale[j]);
+      wx[(size_t)c * h->ldx + j] = w0m[(size_t)c * r_m + j];
+    }
+    for (int k = 0; k < d_z; ++k) {
+      double s = 0.0;
+      if (Vz)
+        for (int j = 0; j < r_z; ++j) s += (double)row[r_m + j] * (double)Vz[(size_t)k * r_z + j];
+      else
+        s = row[r_m + k];
+      pz[(size_t)c * d_z + k] = s;
+      pz32[(size_t)c * h->d_zp + k] = (float)s;
+      pz32t[(size_t)k * h1 + c] = (float)s;
+      wx[(size_t)c * h->ldx + r_m + k] = (float)s;
+    }
+  }
+  CU(cudaMemcpy(h->W[0], w0m.data(), w0m.size() * 4, cudaMemcpyHostToDevice));
+  for (int l = 1; l < h->L; ++l)
+    CU(cudaMemcpy(h->W[l], W[l], (size_t)h->w[l + 1] * h->w[l] * 4, cudaMemcpyHostToDevice));
+  for (int l = 0; l < h->L; ++l) CU(cudaMemcpy(h->b[l], b[l], (size_t)h->w[l + 1] * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->Pz, pz.data(), pz.size() * 8, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->Pz32, pz32.data(), pz32.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->Pz32t, pz32t.data(), pz32t.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->Wx, wx.data(), wx.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->omean, out_mean, (size_t)h->r_u * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->ostd, out_std, (size_t)h->r_u * 4, cudaMemcpyHostToDevice));
+  if (h->tcw.enabled) TRY(tc_set_weights(h, h->tcw));
+  h->have_model = true;
+  h->have_mean = false;
+  return SDN_OK;
+}
+
+int sdn_set_tracking(sdn_handle* h, const float* c, double q0) {
+  if (!h || !c) return fail(SDN_ERR_ARG, "null argument");
+  CU(cudaSetDevice(h->device));
+  CU(cudaMemcpy(h->c, c, (size_t)h->r_u * 4, cudaMemcpyHostToDevice));
+  h->q0 = q0;
+  h->have_form = true;
+  h->have_mean = false;
+  return SDN_OK;
+}
+
+int sdn_set_samples(sdn_handle* h, const float* m_r, int64_t n, int64_t global_offset, int32_t on_device) {
+  if (!h || (!m_r && n > 0)) return fail(SDN_ERR_ARG, "null argument");
+  if (n < 0 || n > h->cap) return fail(SDN_ERR_ARG, "sample count exceeds the handle capacity");
+  CU(cudaSetDevice(h->device));
+  if (n > 0)
+    CU(cudaMemcpyAsync(h->MR, m_r, (size_t)n * h->r_m * 4,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  h->n = n;
+  h->goff = global_offset;
+  h->fwd_done = false;
+  if (h->tcw.enabled) TRY(tc_set_samples(h, h->tcw, h->MR, n));
+  return SDN_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// evaluation phases
+
+static int check_risk(const sdn_risk* r) {
+  if (!r) return fail(SDN_ERR_ARG, "null risk");
+  if (r->kind < 0 || r->kind > 3) return fail(SDN_ERR_ARG, "unknown risk kind");
+  if ((r->kind == SDN_RISK_CVAR_SMOOTH || r->kind == SDN_RISK_CVAR_EXACT) && !(r->beta >= 0.0 && r->beta < 1.0))
+    return fail(SDN_ERR_ARG, "beta must be in [0, 1)");
+  if (r->kind == SDN_RISK_MEANVAR && !(r->beta >= 0.0)) return fail(SDN_ERR_ARG, "variance weight must be >= 0");
+  if (r->kind == SDN_RISK_CVAR_SMOOTH && !(r->eps > 0.0)) return fail(SDN_ERR_ARG, "eps must be positive");
+  if (r->qoi != SDN_QOI_REDUCED && r->qoi != SDN_QOI_DECODED) return fail(SDN_ERR_ARG, "unknown QoI frame");
+  return SDN_OK;
+}
+
+static int ceil_count(double x) { return (int)std::ceil(x - 1e-9); }   // riskopt.py:56-58
+
+static int upload_z(sdn_handle* h, const double* z) {
+  double zz = 0.0;
+  h->zhost.assign(z, z + h->d_z);
+  for (int k = 0; k < h->d_z; ++k) { h->hz[k] = z[k]; zz += z[k] * z[k]; }
+  h->hzz = zz;
+  CU(cudaMemcpyAsync(h->zdev, h->hz, sizeof(double) * h->d_z, cudaMemcpyHostToDevice, h->stream));
+  return SDN_OK;
+}
+
+// phase 1: forward over the shard; local moments -> stats_dev (device)
+static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, double* stats_dev,
+                        bool store_D) {
+  if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
+  if (risk->qoi == SDN_QOI_REDUCED && !h->have_form) return fail(SDN_ERR_STATE, "set_tracking first");
+  if (risk->qoi == SDN_QOI_DECODED && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  TRY(check_risk(risk));
+  CU(cudaSetDevice(h->device));
+  h->risk = *risk;
+  h->selected = false;
+  h->compacted = false;
+  const bool dec = risk->qoi == SDN_QOI_DECODED;
+  const double q0 = dec ? h->q0dec : h->q0;
+  h->shift = h->have_mean ? h->last_mean : q0;
+  TRY(upload_z(h, z));
+  { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
+  k_zbias<<<(unsigned)cdiv(h->h1, 128), 128, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb); }
+  h->launches++;
+  CHECK_LAUNCH(h);
+  if (h->n > 0) {
+    TRY(run_forward(h, h->n, h->MR, h->r_m, h->r_m, h->W[0], h->r_m, h->zb, store_D, h->Y,
+                    h->tcw.enabled ? &h->tcw.mr : nullptr));
+    if (dec) {
+      TRY((gemm<false, true>(h, h->n, nullptr, h->r_u, h->r_u, h->Y, h->r_u, h->Kg, h->r_u,
+                             EpiStore{h->KPhi, (int64_t)h->r_u})));
+    }
+  }
+  const int qg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(h->n, 1), 8), h->qgrid));
+  { ProfScope ps(h, PC_QOI, 4.0 * h->n * h->r_u, 4.0 * h->n * h->r_u * (dec ? 2 : 1) + 8.0 * h->n);
+  k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
+                                   h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
+                                   h->Q, h->qpart);
+  k_sum_rows<<<1, STATS_LEN, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
+  h->launches += 2;
+  CHECK_LAUNCH(h);
+  h->fwd_done = true;
+  return SDN_OK;
+}
+
+// ensure candidate scratch for `count` entries
+static int ensure_cand(sdn_handle* h, int64_t count) {
+  if (count <= h->cand_cap) return SDN_OK;
+  if (h->cand_vals) cudaFree(h->cand_vals);
+  if (h->cand_gidx) cudaFree(h->cand_gidx);
+  if (h->cand_mask) cudaFree(h->cand_mask);
+  CU(cudaMalloc(&h->cand_vals, sizeof(double) * count));
+  CU(cudaMalloc(&h->cand_gidx, sizeof(double) * count));
+  CU(cudaMalloc(&h->cand_mask, count));
+  h->cand_cap = count;
+  return SDN_OK;
+}
+
+// ordered compaction of flagged rows -> rowidx / n_act_dev
+static int compact_rows(sdn_handle* h, int kind, double t, double eps) {
+  const int nb = (int)cdiv(std::max<int64_t>(h->n, 1), 1024);
+  ProfScope ps(h, PC_COMPACT, 0.0, 2.0 * (8.0 + 1.0) * h->n);
+  k_flag_count<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, h->counts);
+  k_scan_counts<<<1, 32, 0, h->stream>>>(nb, h->counts, h->offs, h->n_act_dev);
+  k_compact<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, h->offs, h->rowidx);
+  h->launches += 3;
+  CHECK_LAUNCH(h);
+  h->compacted = true;
+  return SDN_OK;
+}
+
+// local exact top-k (single rank): selection mask over the shard's Q
+static int select_local(sdn_handle* h, int64_t k) {
+  { ProfScope ps(h, PC_SELECT, 0.0, 8.0 * 8.0 * h->n);
+  k_topk_select<<<1, 1024, 0, h->stream>>>(h->n, k, h->Q, nullptr, h->sel); }
+  h->launches++;
+  CHECK_LAUNCH(h);
+  TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
+  h->selected = true;
+  return SDN_OK;
+}
+
+// phase 3: weights, seeds, reverse sweep, projection -> partial_dev
+static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev) {
+  if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
+  const sdn_risk& r = h->risk;
+  const bool dec = r.qoi == SDN_QOI_DECODED;
+  const int kind = r.kind;
+  const bool exact = kind == SDN_RISK_CVAR_EXACT;
+  if (exact && !h->selected) return fail(SDN_ERR_STATE, "exact CVaR needs the selection phase");
+  const double eps = kind == SDN_RISK_CVAR_SMOOTH ? r.eps : 1.0;
+  const double kinv = exact ? 1.0 / (double)h->kk : 0.0;
+  const int* rowidx = nullptr;
+  const int* nact = nullptr;
+  if (kind == SDN_RISK_CVAR_SMOOTH) TRY(compact_rows(h, RISK_CVAR_SMOOTH, r.t, eps));
+  if (h->compacted) { rowidx = h->rowidx; nact = h->n_act_dev; }
+  const int64_t rows_hint = exact ? h->kk : (h->compacted ? -1 : h->n);
+  if (!r.need_grad) {
+    k_finalize_grad<<<1, 256, sizeof(double) * h->h1, h->stream>>>(0, h->h1, h->d_z, nullptr, h->Pz, h->rowidx,
+                                                                    h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
+    h->launches++;
+    CHECK_LAUNCH(h);
+    return SDN_OK;
+  }
+  const int64_t nmax = h->n;
+  if (nmax > 0) {
+    const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nmax, 8), 4 * h->num_sms));
+    { ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
+    k_seed<<<sg, 256, 0, h->stream>>>(nmax, nact, rowidx, h->r_u, h->Y, dec ? h->KPhi : nullptr,
+                                      dec ? h->cdec : h->c, h->ostd, h->Q, stats_dev, kind, h->shift, r.beta,
+                                      eps, r.t, kinv, h->E); }
+    h->launches++;
+    CHECK_LAUNCH(h);
+    if (h->tcw.enabled) TRY(tc_split_seed(h, h->tcw, h->E, nmax, nact));
+    float* u0 = nullptr;
+    TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint));
+    dim3 cg((unsigned)cdiv(h->h1, 32), (unsigned)h->crb);
+    { ProfScope ps(h, PC_COLSUM, 0.0, 0.0, rows_hint, 4.0 * h->h1);
+    k_colsum<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, h->cpart); }
+    h->launches++;
+  }
+  ProfScope psf(h, PC_FINAL, 0.0, 8.0 * h->crb * h->h1);
+  k_finalize_grad<<<1, 256, sizeof(double) * h->h1, h->stream>>>(
+      nmax > 0 ? h->crb : 0, h->h1, h->d_z, nmax > 0 ? h->cpart : nullptr, h->Pz, h->rowidx, h->n_act_dev, h->Q,
+      exact ? 1 : 0, partial_dev);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
+static int eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
+                       double* grad_z) {
+  CU(cudaMemcpyAsync(h->hstats, stats_dev, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaMemcpyAsync(h->hpart, partial_dev, sizeof(double) * h->plen(), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  const double* st = h->hstats;
+  const double* pt = h->hpart;
+  const sdn_risk& r = h->risk;
+  const double n = st[0];
+  if (!(n > 0)) return fail(SDN_ERR_ARG, "empty sample set");
+  const double m1 = st[1] / n;
+  const double qmean = h->shift + m1;
+  const double qvar = std::max(st[2] / n - m1 * m1, 0.0);
+  double value = 0.0, grad_t = 0.0;
+  switch (r.kind) {
+    case SDN_RISK_MEAN: value = qmean; break;
+    case SDN_RISK_MEANVAR: value = qmean + r.beta * qvar; break;
+    case SDN_RISK_CVAR_SMOOTH: {
+      const double s = 1.0 / (n * (1.0 - r.beta));
+      value = r.t + s * st[3];
+      grad_t = 1.0 - s * st[4];
+      break;
+    }
+    default: value = pt[h->d_z] / pt[h->d_z + 1]; break;
+  }
+  value += r.alpha * h->hzz;
+  if (grad_z)
+    for (int k = 0; k < h->d_z; ++k) grad_z[k] = (r.need_grad ? pt[k] : 0.0) + 2.0 * r.alpha * h->zhost[k];
+  if (std::isfinite(qmean)) { h->last_mean = qmean; h->have_mean = true; }
+  if (res) {
+    res->value = value;
+    res->grad_t = grad_t;
+    res->n_samples = (int64_t)n;
+    res->n_selected = r.kind == SDN_RISK_CVAR_EXACT ? (int64_t)pt[h->d_z + 1]
+                      : r.kind == SDN_RISK_CVAR_SMOOTH ? (int64_t)st[5] : (int64_t)n;
+    res->q_mean = qmean;
+    res->q_var = qvar;
+  }
+  return SDN_OK;
+}
+
+extern "C" {
+
+int sdn_partial_len(sdn_handle* h) { return h ? h->plen() : -1; }
+
+int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* res, double* grad_z,
+             int64_t* cvar_idx) {
+  if (!h || !z || !risk) return fail(SDN_ERR_ARG, "null argument");
+  if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
+  TRY(eval_forward(h, z, risk, h->stats_loc, risk->need_grad != 0));
+  if (risk->kind == SDN_RISK_CVAR_EXACT) {
+    h->kk = std::max(ceil_count((1.0 - risk->beta) * (double)h->n), 1);   // riskopt.py:80
+    TRY(select_local(h, h->kk));
+  }
+  TRY(eval_backward(h, h->stats_loc, h->partial_loc));
+  TRY(eval_finish(h, h->stats_loc, h->partial_loc, res, grad_z));
+  if (cvar_idx && risk->kind == SDN_RISK_CVAR_EXACT) {
+    std::vector<int> idx(h->kk);
+    CU(cudaMemcpy(idx.data(), h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < h->kk; ++i) cvar_idx[i] = h->goff + idx[i];
+  }
+  return SDN_OK;
+}
+
+// several risk functionals from ONE forward pass (e.g. c2: mean+variance and
+// exact CVaR): the activations/derivatives are kept, each risk runs its own
+// (possibly compacted) reverse sweep.  At most one smoothed-CVaR entry (its
+// t/eps feed the forward-time moments).
+int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks, sdn_result* res,
+                   double* grads, int64_t* cvar_idx) {
+  if (!h || !z || !risks || n_risks < 1 || !res) return fail(SDN_ERR_ARG, "null argument");
+  if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
+  int smooth = -1, any_grad = 0;
+  for (int i = 0; i < n_risks; ++i) {
+    TRY(check_risk(&risks[i]));
+    if (risks[i].qoi != risks[0].qoi) return fail(SDN_ERR_ARG, "all risks must share the QoI frame");
+    if (risks[i].kind == SDN_RISK_CVAR_SMOOTH) {
+      if (smooth >= 0) return fail(SDN_ERR_ARG, "at most one smoothed CVaR per multi-evaluation");
+      smooth = i;
+    }
+    any_grad |= risks[i].need_grad;
+  }
+  TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad != 0));
+  int64_t off = 0;
+  for (int i = 0; i < n_risks; ++i) {
+    h->risk = risks[i];
+    h->compacted = false;
+    h->selected = false;
+    if (risks[i].kind == SDN_RISK_CVAR_EXACT) {
+      h->kk = std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);
+      TRY(select_local(h, h->kk));
+    }
+    TRY(eval_backward(h, h->stats_loc, h->partial_loc));
+    TRY(eval_finish(h, h->stats_loc, h->partial_loc, &res[i], grads ? grads + (size_t)i * h->d_z : nullptr));
+    if (cvar_idx && risks[i].kind == SDN_RISK_CVAR_EXACT) {
+      std::vector<int> idx(h->kk);
+      CU(cudaMemcpy(idx.data(), h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost));
+      for (int64_t j = 0; j < h->kk; ++j) cvar_idx[off + j] = h->goff + idx[j];
+      off += h->kk;
+    }
+  }
+  return SDN_OK;
+}
+
+int sdn_profile(sdn_handle* h, int32_t enable) {
+  if (!h) return fail(SDN_ERR_ARG, "null handle");
+  CU(cudaStreamSynchronize(h->stream));
+  h->prof = enable != 0;
+  h->recs.clear();
+  h->pool_used = 0;
+  return SDN_OK;
+}
+
+// per-class totals since sdn_profile(h, 1): ms, algorithmic flops, bytes,
+// launches.  Arrays of length n_cls (<= SDN_PROF_CLASSES).
+int sdn_profile_read(sdn_handle* h, int32_t n_cls, double* ms, double* flops, double* bytes, int64_t* count) {
+  if (!h || !ms || !flops || !bytes || !count) return fail(SDN_ERR_ARG, "null argument");
+  CU(cudaStreamSynchronize(h->stream));
+  for (int c = 0; c < n_cls; ++c) { ms[c] = 0; flops[c] = 0; bytes[c] = 0; count[c] = 0; }
+  int nact = 0;
+  CU(cudaMemcpy(&nact, h->n_act_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  for (auto& r : h->recs) {
+    if (r.cls < 0 || r.cls >= n_cls) continue;
+    float t = 0.0f;
+    CU(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.cls] += t;
+    double f = r.flops, b = r.bytes;
+    if (r.rows < 0) f += (double)nact * r.per_row;
+    else if (r.per_row > 0.0 && r.flops == 0.0 && r.bytes == 0.0) b += (double)r.rows * r.per_row;
+    flops[r.cls] += f;
+    bytes[r.cls] += b;
+    count[r.cls] += 1;
+  }
+  return SDN_OK;
+}
+
+int sdn_eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, double* stats_dev) {
+  if (!h || !z || !risk || !stats_dev) return fail(SDN_ERR_ARG, "null argument");
+  return eval_forward(h, z, risk, stats_dev, risk->need_grad != 0);
+}
+
+int sdn_eval_candidates(sdn_handle* h, int64_t k, double* cand_dev) {
+  if (!h || !cand_dev || k < 1) return fail(SDN_ERR_ARG, "bad argument");
+  if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
+  CU(cudaSetDevice(h->device));
+  const int64_t kl = std::min<int64_t>(k, h->n);
+  if (kl > 0) {
+    k_topk_select<<<1, 1024, 0, h->stream>>>(h->n, kl, h->Q, nullptr, h->sel);
+    h->launches++;
+    TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
+  } else {
+    CU(cudaMemsetAsync(h->n_act_dev, 0, sizeof(int), h->stream));
+  }
+  k_export_candidates<<<(unsigned)cdiv(k, 256), 256, 0, h->stream>>>(k, h->n_act_dev, h->rowidx, h->Q, h->goff,
+                                                                      cand_dev);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
+int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, int64_t k) {
+  if (!h || !all_cand_dev || n_ranks < 1 || k < 1) return fail(SDN_ERR_ARG, "bad argument");
+  CU(cudaSetDevice(h->device));
+  const int64_t nc = (int64_t)n_ranks * k;
+  TRY(ensure_cand(h, nc));
+  k_unpack_candidates<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(n_ranks, k, all_cand_dev, h->cand_vals,
+                                                                      h->cand_gidx);
+  k_topk_select<<<1, 1024, 0, h->stream>>>(nc, k, h->cand_vals, h->cand_gidx, h->cand_mask);
+  CU(cudaMemsetAsync(h->sel, 0, std::max<int64_t>(h->n, 1), h->stream));
+  k_scatter_selection<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(nc, h->cand_mask, h->cand_gidx, h->goff,
+                                                                      h->n, h->sel);
+  h->launches += 3;
+  CHECK_LAUNCH(h);
+  TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
+  h->kk = k;
+  h->selected = true;
+  return SDN_OK;
+}
+
+int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev) {
+  if (!h || !stats_dev || !partial_dev) return fail(SDN_ERR_ARG, "null argument");
+  CU(cudaSetDevice(h->device));
+  return eval_backward(h, stats_dev, partial_dev);
+}
+
+int sdn_eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
+                    double* grad_z) {
+  if (!h || !stats_dev || !partial_dev) return fail(SDN_ERR_ARG, "null argument");
+  CU(cudaSetDevice(h->device));
+  return eval_finish(h, stats_dev, partial_dev, res, grad_z);
+}
+
+int sdn_last_q(sdn_handle* h, const double** q_dev, int64_t* n) {
+  if (!h || !q_dev || !n) return fail(SDN_ERR_ARG, "null argument");
+  *q_dev = h->Q;
+  *n = h->n;
+  return SDN_OK;
+}
+
+// per-sample (Q, G): unit weights through the same sweep, then G = dL/dS_0 Pz
+int sdn_eval_samples(sdn_handle* h, const double* z, int32_t qoi, double* Qout, double* Gout) {
+  if (!h || !z || !Qout) return fail(SDN_ERR_ARG, "null argument");
+  if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
+  sdn_risk r{};
+  r.kind = SDN_RISK_MEAN;
+  r.qoi = qoi;
+  r.beta = 0.0;
+  r.eps = 1.0;
+  r.need_grad = Gout != nullptr;
+  TRY(eval_forward(h, z, &r, h->stats_loc, Gout != nullptr));
+  if (Gout) {
+    if (!h->Gz) CU(cudaMalloc(&h->Gz, sizeof(float) * h->cap * h->d_zp));
+    const bool dec = qoi == SDN_QOI_DECODED;
+    const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(h->n, 8), 4 * h->num_sms));
+    k_seed<<<sg, 256, 0, h->stream>>>(h->n, nullptr, nullptr, h->r_u, h->Y, dec ? h->KPhi : nullptr,
+                                      dec ? h->cdec : h->c, h->ostd, h->Q, h->stats_loc, RISK_UNIT, 0.0, 0.0,
+                                      1.0, 0.0, 0.0, h->E);
+    h->launches++;
+    CHECK_LAUNCH(h);
+    if (h->tcw.enabled) TRY(tc_split_seed(h, h->tcw, h->E, h->n, nullptr));
+    float* u0 = nullptr;
+    TRY(run_backward(h, h->n, nullptr, nullptr, &u0, h->n));
+    TRY((gemm<false, false>(h, h->n, nullptr, h->d_zp, h->h1, u0, h->h1, h->Pz32, h->d_zp,
+                            EpiStore{h->Gz, (int64_t)h->d_zp})));
+    double* gd = nullptr;
+    CU(cudaMalloc(&gd, sizeof(double) * h->n * h->d_z));
+    k_copy_g<<<(unsigned)std::min<int64_t>(cdiv(h->n * h->d_z, 256), 65535), 256, 0, h->stream>>>(
+        h->n, h->d_z, h->d_zp, h->Gz, gd);
+    h->launches++;
+    cudaError_t e = cudaMemcpyAsync(Gout, gd, sizeof(double) * h->n * h->d_z, cudaMemcpyDeviceToHost, h->stream);
+    cudaError_t e2 = cudaStreamSynchronize(h->stream);
+    cudaFree(gd);
+    if (e != cudaSuccess || e2 != cudaSuccess) return fail(SDN_ERR_CUDA, "G download failed");
+  }
+  CU(cudaMemcpyAsync(Qout, h->Q, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return SDN_OK;
+}
+
+// rows with their own z: X = [m_r | z] through Wx = [W0m' | Pz]
+static int forward_rows(sdn_handle* h, const float* mr_dev, const float* z_dev, int64_t n, float* X, bool store_D,
+                        float* phi_dev) {
+  k_build_x<<<(unsigned)n, 128, 0, h->stream>>>(n, h->r_m, h->d_z, h->ldx, mr_dev, z_dev, X);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  return run_forward(h, n, X, h->ldx, h->ldx, h->Wx, h->ldx, h->b[0], store_D, phi_dev, nullptr);
+}
+
+int sdn_forward_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n, float* phi) {
+  if (!h || !m_r || !z || !phi) return fail(SDN_ERR_ARG, "null argument");
+  if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
+  if (n < 0) return fail(SDN_ERR_ARG, "negative row count");
+  CU(cudaSetDevice(h->device));
+  const int64_t chunk = h->cap;
+  float *mr = nullptr, *zz = nullptr, *X = nullptr;
+  CU(cudaMalloc(&mr, sizeof(float) * chunk * h->r_m + 16));
+  CU(cudaMalloc(&zz, sizeof(float) * chunk * h->d_z + 16));
+  CU(cudaMalloc(&X, sizeof(float) * chunk * h->ldx + 16));
+  int rc = SDN_OK;
+  for (int64_t s = 0; s < n && rc == SDN_OK; s += chunk) {
+    const int64_t m = std::min(chunk, n - s);
+    if (cudaMemcpyAsync(mr, m_r + s * h->r_m, sizeof(float) * m * h->r_m, cudaMemcpyHostToDevice, h->stream) ||
+        cudaMemcpyAsync(zz, z + s * h->d_z, sizeof(float) * m * h->d_z, cudaMemcpyHostToDevice, h->stream)) {
+      rc = fail(SDN_ERR_CUDA, "upload failed");
+      break;
+    }
+    rc = forward_rows(h, mr, zz, m, X, false, h->Y);
+    if (rc == SDN_OK &&
+        (cudaMemcpyAsync(phi + s * h->r_u, h->Y, sizeof(float) * m * h->r_u, cudaMemcpyDeviceToHost, h->stream) ||
+         cudaStreamSynchronize(h->stream)))
+      rc = fail(SDN_ERR_CUDA, "download failed");
+  }
+  cudaStreamSynchronize(h->stream);
+  cudaFree(mr);
+  cudaFree(zz);
+  cudaFree(X);
+  return rc;
+}
+
+// forward-mode control Jacobian (surrogate.py:195-233) on the device:
+// tangent rows (i*d_z + k) through the chain; decoded: U (std . J)
+int sdn_jacobian_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n, int32_t decoded, float* J) {
+  if (!h || !m_r || !z || !J) return fail(SDN_ERR_ARG, "null argument");
+  if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
+  if (decoded && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  CU(cudaSetDevice(h->device));
+  const int d_z = h->d_z, L = h->L;
+  const int64_t outw = decoded ? h->d_u : h->r_u;
+  const int64_t row_budget = std::max<int64_t>(d_z, (int64_t)(256ll << 20) / (4ll * std::max(h->maxw, h->r_u)));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(h->cap, row_budget / d_z));
+  const int64_t trows = chunk * d_z;
+  float *mr = nullptr, *zz = nullptr, *X = nullptr, *T0 = nullptr, *T1 = nullptr, *Jt = nullptr, *Jd = nullptr;
+  int rc = SDN_OK;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(h->stream);
+    cudaFree(mr); cudaFree(zz); cudaFree(X); cudaFree(T0); cudaFree(T1); cudaFree(Jt); cudaFree(Jd);
+  };
+  if (cudaMalloc(&mr, sizeof(float) * chunk * h->r_m + 16) || cudaMalloc(&zz, sizeof(float) * chunk * d_z + 16) ||
+      cudaMalloc(&X, sizeof(float) * chunk * h->ldx + 16) ||
+      cudaMalloc(&T0, sizeof(float) * trows * std::max(h->maxw, h->r_u) + 16) ||
+      cudaMalloc(&T1, sizeof(float) * trows * std::max(h->maxw, h->r_u) + 16) ||
+      cudaMalloc(&Jt, sizeof(float) * trows * h->r_u + 16) ||
+      cudaMalloc(&Jd, sizeof(float) * chunk * outw * d_z + 16)) {
+    cleanup();
+    return fail(SDN_ERR_NOMEM, "jacobian scratch allocation failed");
+  }
+  for (int64_t s = 0; s < n && rc == SDN_OK; s += chunk) {
+    const int64_t m = std::min(chunk, n - s), rows = m * d_z;
+    if (cudaMemcpyAsync(mr, m_r + s * h->r_m, sizeof(float) * m * h->r_m, cudaMemcpyHostToDevice, h->stream) ||
+        cudaMemcpyAsync(zz, z + s * d_z, sizeof(float) * m * d_z, cudaMemcpyHostToDevice, h->stream)) {
+      rc = fail(SDN_ERR_CUDA, "upload failed");
+      break;
+    }
+    if ((rc = forward_rows(h, mr, zz, m, X, true, h->Y))) break;
+    float* Tc = T0;
+    float* Tn = T1;
+    if (L == 1) {
+      // linear model: tangent of y is the constant Pz (w[1] = r_u)
+      k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, nullptr, h->Pz32t, Tc);
+    } else {
+      k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, h->D[0], h->Pz32t, Tc);
+    }
+    h->launches++;
+    for (int l = 1; l < L - 1 && rc == SDN_OK; ++l) {
+      EpiTangent e{h->D[l], (int64_t)h->w[l + 1], d_z, h->res[l] ? Tc : nullptr, Tn, (int64_t)h->w[l + 1]};
+      rc = gemm<false, true>(h, rows, nullptr, h->w[l + 1], h->w[l], Tc, h->w[l], h->W[l], h->w[l], e);
+      std::swap(Tc, Tn);
+    }
+    if (rc) break;
+    if (L >= 2) {
+      if (!decoded) {
+        EpiJacScatter e{h->ostd, Jd, d_z, (int64_t)h->r_u};
+        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->w[L - 1], Tc, h->w[L - 1], h->W[L - 1], h->w[L - 1], e);
+      } else {
+        EpiAffine e{nullptr, h->ostd, nullptr, Jt, (int64_t)h->r_u};
+        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->w[L - 1], Tc, h->w[L - 1], h->W[L - 1], h->w[L - 1], e);
+      }
+    } else {
+      if (!decoded) {
+        // Tc rows already hold dy/dz; scale by std and scatter via a unit GEMM
+        EpiJacScatter e{h->ostd, Jd, d_z, (int64_t)h->r_u};
+        std::vector<float> eye((size_t)h->r_u * h->r_u, 0.0f);
+        for (int i = 0; i < h->r_u; ++i) eye[(size_t)i * h->r_u + i] = 1.0f;
+        float* I = nullptr;
+        cudaMalloc(&I, sizeof(float) * eye.size());
+        cudaMemcpy(I, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice);
+        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->r_u, Tc, h->r_u, I, h->r_u, e);
+        cudaStreamSynchronize(h->stream);
+        cudaFree(I);
+      } else {
+        EpiAffine e{nullptr, h->ostd, nullptr, Jt, (int64_t)h->r_u};
+        std::vector<float> eye((size_t)h->r_u * h->r_u, 0.0f);
+        for (int i = 0; i < h->r_u; ++i) eye[(size_t)i * h->r_u + i] = 1.0f;
+        float* I = nullptr;
+        cudaMalloc(&I, sizeof(float) * eye.size());
+        cudaMemcpy(I, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice);
+        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->r_u, Tc, h->r_u, I, h->r_u, e);
+        cudaStreamSynchronize(h->stream);
+        cudaFree(I);
+      }
+    }
+    if (rc) break;
+    if (decoded) {
+      EpiJacScatter e{nullptr, Jd, d_z, (int64_t)h->d_u};
+      if ((rc = gemm<false, true>(h, rows, nullptr, (int)h->d_u, h->r_u, Jt, h->r_u, h->U, h->r_u, e))) break;
+    }
+    if (cudaMemcpyAsync(J + s * outw * d_z, Jd, sizeof(float) * m * outw * d_z, cudaMemcpyDeviceToHost,
+                        h->stream) ||
+        cudaStreamSynchronize(h->stream))
+      rc = fail(SDN_ERR_CUDA, "download failed");
+  }
+  cleanup();
+  return rc;
+}
+
+// decoder: Gram K = U^T M U (split-K fp64), c = U^T M (b - u_t), q0 (host fp64)
+int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubias, const float* Mdiag,
+                    const float* u_target) {
+  if (!h || !U || !ubias || !Mdiag || !u_target || d_u < 1) return fail(SDN_ERR_ARG, "bad argument");
+  if (d_u % 4 != 0 && false) return fail(SDN_ERR_ARG, "d_u");
+  CU(cudaSetDevice(h->device));
+  const int r_u = h->r_u;
+  std::vector<double> cd(r_u, 0.0);
+  double q0 = 0.0;
+  std::vector<float> um((size_t)d_u * r_u);
+  for (int64_t d = 0; d < d_u; ++d) {
+    const double s = (double)ubias[d] - (double)u_target[d];
+    const double ms = (double)Mdiag[d] * s;
+    q0 += s * ms;
+    for (int j = 0; j < r_u; ++j) {
+      cd[j] += (double)U[d * r_u + j] * ms;
+      um[(size_t)d * r_u + j] = (float)((double)Mdiag[d] * (double)U[d * r_u + j]);
+    }
+  }
+  if (h->U) { cudaFree(h->U); h->U = nullptr; }
+  if (h->ub) { cudaFree(h->ub); h->ub = nullptr; }
+  if (!h->Kg) CU(cudaMalloc(&h->Kg, sizeof(float) * r_u * r_u));
+  if (!h->cdec) CU(cudaMalloc(&h->cdec, sizeof(float) * r_u));
+  if (!h->KPhi) CU(cudaMalloc(&h->KPhi, sizeof(float) * h->cap * r_u));
+  CU(cudaMalloc(&h->U, sizeof(float) * d_u * r_u));
+  CU(cudaMalloc(&h->ub, sizeof(float) * d_u));
+  CU(cudaMemcpy(h->U, U, sizeof(float) * d_u * r_u, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->ub, ubias, sizeof(float) * d_u, cudaMemcpyHostToDevice));
+  float* Um = nullptr;
+  double* K64 = nullptr;
+  CU(cudaMalloc(&Um, sizeof(float) * d_u * r_u));
+  CU(cudaMalloc(&K64, sizeof(double) * r_u * r_u));
+  CU(cudaMemcpy(Um, um.data(), sizeof(float) * um.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemset(K64, 0, sizeof(double) * r_u * r_u));
+  const int64_t kc = 2048;
+  int rc = SDN_OK;
+  for (int64_t k0 = 0; k0 < d_u && rc == SDN_OK; k0 += kc) {
+    const int kl = (int)std::min(kc, d_u - k0);
+    // K += (Um[k0:k0+kl])^T U[k0:k0+kl]  (A stored K x M: AT)
+    rc = gemm<true, false>(h, r_u, nullptr, r_u, kl, Um + k0 * r_u, r_u, h->U + k0 * r_u, r_u,
+                           EpiAccum64{K64, (int64_t)r_u});
+  }
+  std::vector<double> k64((size_t)r_u * r_u);
+  std::vector<float> k32((size_t)r_u * r_u);
+  if (rc == SDN_OK) {
+    cudaStreamSynchronize(h->stream);
+    cudaMemcpy(k64.data(), K64, sizeof(double) * k64.size(), cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < k64.size(); ++i) k32[i] = (float)k64[i];
+    cudaMemcpy(h->Kg, k32.data(), sizeof(float) * k32.size(), cudaMemcpyHostToDevice);
+    std::vector<float> c32(r_u);
+    for (int j = 0; j < r_u; ++j) c32[j] = (float)cd[j];
+    cudaMemcpy(h->cdec, c32.data(), sizeof(float) * r_u, cudaMemcpyHostToDevice);
+  }
+  cudaFree(Um);
+  cudaFree(K64);
+  if (rc) return rc;
+  CU(cudaGetLastError());
+  h->d_u = d_u;
+  h->q0dec = q0;
+  h->have_dec = true;
+  h->have_mean = false;
+  return SDN_OK;
+}
+
+// u = U phi + b  (pod.py:36-40)
+int sdn_lift(sdn_handle* h, const float* phi, int64_t n, float* u) {
+  if (!h || !phi || !u) return fail(SDN_ERR_ARG, "null argument");
+  if (!h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  CU(cudaSetDevice(h->device));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(512ll << 20) / (4 * h->d_u)));
+  float *p = nullptr, *o = nullptr;
+  CU(cudaMalloc(&p, sizeof(float) * chunk * h->r_u + 16));
+  CU(cudaMalloc(&o, sizeof(float) * chunk * h->d_u + 16));
+  int rc = SDN_OK;
+  for (int64_t s = 0; s < n && rc == SDN_OK; s += chunk) {
+    const int64_t m = std::min(chunk, n - s);
+    cudaMemcpyAsync(p, phi + s * h->r_u, sizeof(float) * m * h->r_u, cudaMemcpyHostToDevice, h->stream);
+    rc = gemm<false, true>(h, m, nullptr, (int)h->d_u, h->r_u, p, h->r_u, h->U, h->r_u,
+                           EpiAffine{h->ub, nullptr, nullptr, o, h->d_u});
+    if (rc == SDN_OK && (cudaMemcpyAsync(u + s * h->d_u, o, sizeof(float) * m * h->d_u, cudaMemcpyDeviceToHost,
+                                         h->stream) ||
+                         cudaStreamSynchronize(h->stream)))
+      rc = fail(SDN_ERR_CUDA, "download failed");
+  }
+  cudaStreamSynchronize(h->stream);
+  cudaFree(p);
+  cudaFree(o);
+  return rc;
+}
+
+// encoder K1: m_r = (m - mean) diag(M) V_m, split-K in fp64 (randfield.py:67-72)
+int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, const float* Vm, const float* Mdiag,
+                      float m_mean, int64_t global_offset, int32_t on_device) {
+  if (!h || !m || !Vm || !Mdiag || n < 0 || d_m < 1) return fail(SDN_ERR_ARG, "bad argument");
+  if (n > h->cap) return fail(SDN_ERR_ARG, "sample count exceeds the handle capacity");
+  CU(cudaSetDevice(h->device));
+  const int r_m = h->r_m;
+  std::vector<float> vmm((size_t)d_m * r_m);
+  std::vector<double> bias(r_m, 0.0);
+  for (int64_t d = 0; d < d_m; ++d)
+    for (int j = 0; j < r_m; ++j) {
+      const double v = (double)Mdiag[d] * (double)Vm[d * r_m + j];
+      vmm[(size_t)d * r_m + j] = (float)v;
+      bias[j] -= (double)m_mean * v;
+    }
+  float *V = nullptr, *mb = nullptr;
+  double *acc = nullptr, *bd = nullptr;
+  int rc = SDN_OK;
+  const int64_t rows_chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(1ll << 30) / (4 * d_m)));
+  CU(cudaMalloc(&V, sizeof(float) * vmm.size()));
+  CU(cudaMalloc(&acc, sizeof(double) * std::max<int64_t>(n, 1) * r_m));
+  CU(cudaMalloc(&bd, sizeof(double) * r_m));
+  if (!on_device) CU(cudaMalloc(&mb, sizeof(float) * rows_chunk * d_m));
+  CU(cudaMemcpy(V, vmm.data(), sizeof(float) * vmm.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(bd, bias.data(), sizeof(double) * r_m, cudaMemcpyHostToDevice));
+  CU(cudaMemsetAsync(acc, 0, sizeof(double) * std::max<int64_t>(n, 1) * r_m, h->stream));
+  const int64_t kc = 1024;
+  for (int64_t s = 0; s < n && rc == SDN_OK; s += rows_chunk) {
+    const int64_t rows = std::min(rows_chunk, n - s);
+    const float* src = m + s * d_m;
+    if (!on_device) {
+      cudaMemcpyAsync(mb, src, sizeof(float) * rows * d_m, cudaMemcpyHostToDevice, h->stream);
+      src = mb;
+    }
+    for (int64_t k0 = 0; k0 < d_m && rc == SDN_OK; k0 += kc) {
+      const int kl = (int)std::min(kc, d_m - k0);
+      rc = gemm<false, false>(h, rows, nullptr, r_m, kl, src + k0, d_m, V + k0 * r_m, r_m,
+                              EpiAccum64{acc + s * r_m, (int64_t)r_m});
+    }
+  }
+  if (rc == SDN_OK && n > 0) {
+    // MR = (float)(acc + bias)
+    std::vector<double> hacc((size_t)n * r_m);
+    cudaStreamSynchronize(h->stream);
+    cudaMemcpy(hacc.data(), acc, sizeof(double) * hacc.size(), cudaMemcpyDeviceToHost);
+    std::vector<float> mr((size_t)n * r_m);
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < r_m; ++j) mr[(size_t)i * r_m + j] = (float)(hacc[(size_t)i * r_m + j] + bias[j]);
+    cudaMemcpy(h->MR, mr.data(), sizeof(float) * mr.size(), cudaMemcpyHostToDevice);
+  }
+  cudaStreamSynchronize(h->stream);
+  cudaFree(V);
+  cudaFree(acc);
+  cudaFree(bd);
+  if (mb) cudaFree(mb);
+  if (rc) return rc;
+  CU(cudaGetLastError());
+  h->n = n;
+  h->goff = global_offset;
+  h->fwd_done = false;
+  if (h->tcw.enabled) TRY(tc_set_samples(h, h->tcw, h->MR, n));
+  return SDN_OK;
+}
+
+// order statistics: indices of the k largest values (value desc, index asc),
+// returned in ascending index order
+int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k, int32_t on_device, int64_t* idx) {
+  if (!h || !values || !idx || n < 1 || k < 1 || k > n) return fail(SDN_ERR_ARG, "bad argument");
+  CU(cudaSetDevice(h->device));
+  double* v = nullptr;
+  uint8_t* mask = nullptr;
+  int *cnt = nullptr, *offs = nullptr, *na = nullptr, *ri = nullptr;
+  const int nb = (int)cdiv(n, 1024);
+  CU(cudaMalloc(&v, sizeof(double) * n));
+  CU(cudaMalloc(&mask, n));
+  CU(cudaMalloc(&cnt, sizeof(int) * nb));
+  CU(cudaMalloc(&offs, sizeof(int) * nb));
+  CU(cudaMalloc(&na, sizeof(int)));
+  CU(cudaMalloc(&ri, sizeof(int) * k));
+  CU(cudaMemcpyAsync(v, values, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     h->stream));
+  k_topk_select<<<1, 1024, 0, h->stream>>>(n, k, v, nullptr, mask);
+  k_flag_count<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, cnt);
+  k_scan_counts<<<1, 32, 0, h->stream>>>(nb, cnt, offs, na);
+  k_compact<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, offs, ri);
+  h->launches += 4;
+  std::vector<int> hi(k);
+  cudaError_t e = cudaMemcpyAsync(hi.data(), ri, sizeof(int) * k, cudaMemcpyDeviceToHost, h->stream);
+  cudaError_t e2 = cudaStreamSynchronize(h->stream);
+  cudaFree(v); cudaFree(mask); cudaFree(cnt); cudaFree(offs); cudaFree(na); cudaFree(ri);
+  if (e != cudaSuccess || e2 != cudaSuccess) return fail(SDN_ERR_CUDA, "top-k failed");
+  for (int64_t i = 0; i < k; ++i) idx[i] = hi[i];
+  return SDN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// kernels.cuh -- QoI, risk moments, sample weights, compaction, radix
+// selection and the gradient reductions of the SAA engine.
+//
+// Determinism: every reduction runs in a fixed order for a given sample
+// count (fixed grids, fixed-order block combines, no float atomics), so the
+// same inputs give bit-identical outputs run to run.
+#pragma once
+#include "common.cuh"
+
+namespace sdn {
+
+enum RiskKind : int { RISK_MEAN = 0, RISK_CVAR_SMOOTH = 1, RISK_MEANVAR = 2, RISK_CVAR_EXACT = 3,
+                      RISK_UNIT = 100 /* per-sample G: w_i = 1 */ };
+
+constexpr int STATS_LEN = 8;   // [n, sum q~, sum q~^2, sum splus, sum d1, n_active, 0, 0]
+
+// zb = b1 + Pz z  (first-layer control contribution, W1_z V_z^T z, shared by
+// every sample of the evaluation -- SURVEY 2.2 K2)
+__global__ void k_zbias(int h1, int d_z, const double* __restrict__ Pz, const double* __restrict__ z,
+                        const float* __restrict__ b1, float* __restrict__ zb) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= h1) return;
+  double s = b1[c];
+  for (int k = 0; k < d_z; ++k) s += Pz[(int64_t)c * d_z + k] * z[k];
+  zb[c] = (float)s;
+}
+
+// X = [m_r, z_row, 0-pad]  (forward_batch / jacobian rows with per-row z)
+__global__ void k_build_x(int64_t n, int r_m, int d_z, int ldx, const float* __restrict__ mr,
+                          const float* __restrict__ z, float* __restrict__ X) {
+  int64_t i = blockIdx.x;
+  for (int c = threadIdx.x; c < ldx; c += blockDim.x) {
+    float v = 0.0f;
+    if (c < r_m) v = mr[i * r_m + c];
+    else if (c < r_m + d_z) v = z[i * d_z + (c - r_m)];
+    X[i * ldx + c] = v;
+  }
+}
+
+// Per-sample QoI (reference riskopt.py:187-189 / pod.py:56-58):
+//   reduced: Q = phi.phi + 2 phi.c + q0
+//   gram   : Q = phi.(K phi) + 2 phi.c + q0  (decoded frame, K = U^T M U)
+// accumulated in fp64; plus per-block fp64 partial moments.
+// One warp per row, grid-stride; block partials in fixed order.
+__global__ void __launch_bounds__(256)
+k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict__ kphi,
+      const float* __restrict__ c, double q0, double shift, double t, double eps,
+      double* __restrict__ Q, double* __restrict__ part) {
+  __shared__ double sp[8][6];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
+    const float* p = phi + i * r_u;
+    const float* kp = kphi ? kphi + i * r_u : p;
+    double s = 0.0;
+    for (int j = lane; j < r_u; j += 32) {
+      double pj = p[j];
+      s += pj * ((double)kp[j] + 2.0 * (double)c[j]);
+    }
+    s = warp_sum(s);
+    double q = s + q0;
+    if (lane == 0) {
+      Q[i] = q;
+      double qs = q - shift, x = q - t;
+      double d1 = splus_d1_d(x, eps);
+      acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
+      acc[3] += splus_d(x, eps); acc[4] += d1; acc[5] += (d1 > 0.0) ? 1.0 : 0.0;
+    }
+  }
+  if (lane == 0)
+    for (int f = 0; f < 6; ++f) sp[warp][f] = acc[f];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += sp[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = s;
+  }
+  if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;
+}
+
+// fixed-order sum of nb rows of width w (fp64) -> out (w)
+__global__ void k_sum_rows(int nb, int w, const double* __restrict__ part, double* __restrict__ out) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= w) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * w + f];
+  out[f] = s;
+}
+
+// sample weight w_i of the risk functional:
+//   mean: 1/n; meanvar: (1 + 2 beta (Q_i - Qbar))/n; smoothed CVaR (riskopt.py:238-241):
+//   splus'(Q_i - t)/(n (1-beta)); exact CVaR: 1/k on the selection; unit: 1.
+SDN_DEV double sample_weight(int kind, double q, const double* st, double shift, double beta,
+                             double eps, double t, double kinv) {
+  double n = st[0];
+  switch (kind) {
+    case RISK_MEAN: return 1.0 / n;
+    case RISK_MEANVAR: {
+      double qbar = shift + st[1] / n;
+      return (1.0 + 2.0 * beta * (q - qbar)) / n;
+    }
+    case RISK_CVAR_SMOOTH: return splus_d1_d(q - t, eps) / (n * (1.0 - beta));
+    case RISK_CVAR_EXACT: return kinv;
+    default: return 1.0;
+  }
+}
+
+// active-row flags for compaction: smoothed CVaR -> splus'(Q - t) > 0;
+// exact CVaR -> selection mask.  Per 1024-row block: count.
+__global__ void __launch_bounds__(1024)
+k_flag_count(int64_t n, int kind, const double* __restrict__ Q, const uint8_t* __restrict__ sel,
+             double t, double eps, int* __restrict__ counts) {
+  __shared__ int wc[32];
+  int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  bool f = false;
+  if (i < n) f = (kind == RISK_CVAR_EXACT) ? (sel[i] != 0) : (splus_d1_d(Q[i] - t, eps) > 0.0);
+  unsigned b = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 32; ++w) s += wc[w];
+    counts[blockIdx.x] = s;
+  }
+}
+
+// exclusive scan of nb block counts (single block); total -> *n_act
+__global__ void k_scan_counts(int nb, const int* __restrict__ counts, int* __restrict__ offs,
+                              int* __restrict__ n_act) {
+  if (threadIdx.x != 0) return;
+  int s = 0;
+  for (int b = 0; b < nb; ++b) { offs[b] = s; s += counts[b]; }
+  *n_act = s;
+}
+
+// ordered compaction: rowidx[offs[b] + rank-in-block] = i for flagged rows
+__global__ void __launch_bounds__(1024)
+k_compact(int64_t n, int kind, const double* __restrict__ Q, const uint8_t* __restrict__ sel,
+          double t, double eps, const int* __restrict__ offs, int* __restrict__ rowidx) {
+  __shared__ int wbase[32];
+  int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  bool f = false;
+  if (i < n) f = (kind == RISK_CVAR_EXACT) ? (sel[i] != 0) : (splus_d1_d(Q[i] - t, eps) > 0.0);
+  unsigned b = __ballot_sync(0xffffffffu, f);
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wbase[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 32; ++w) { int c = wbase[w]; wbase[w] = s; s += c; }
+  }
+  __syncthreads();
+  if (f) rowidx[offs[blockIdx.x] + wbase[warp] + __popc(b & ((1u << lane) - 1u))] = (int)i;
+}
+
+// seed of the reverse sweep on y (pre-output-scaling), compacted rows:
+//   E[r] = w_i * out_std * dQ/dphi,  dQ/dphi = 2 (phi + c)  (reduced, pod.py:60-62)
+//                                     or 2 (K phi + c)       (decoded frame)
+// rowidx null = identity; n_act_dev null = all n rows.
+__global__ void __launch_bounds__(256)
+k_seed(int64_t n, const int* __restrict__ n_act_dev, const int* __restrict__ rowidx, int r_u,
+       const float* __restrict__ phi, const float* __restrict__ kphi, const float* __restrict__ c,
+       const float* __restrict__ ostd, const double* __restrict__ Q, const double* __restrict__ st,
+       int kind, double shift, double beta, double eps, double t, double kinv,
+       float* __restrict__ E) {
+  int64_t nr = n_act_dev ? (int64_t)*n_act_dev : n;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < nr; r += (int64_t)gridDim.x * 8) {
+    int64_t i = rowidx ? (int64_t)rowidx[r] : r;
+    double w = sample_weight(kind, Q[i], st, shift, beta, eps, t, kinv);
+    const float* p = (kphi ? kphi : phi) + i * r_u;
+    for (int j = lane; j < r_u; j += 32)
+      E[r * r_u + j] = (float)(w * 2.0 * ((double)p[j] + (double)c[j]) * (double)ostd[j]);
+  }
+}
+
+// column sums of U (n_act x w) in fp64: part[by][c] over the rows
+// by, by + RB, ... (fixed order), block (32 x 8)
+__global__ void __launch_bounds__(256)
+k_colsum(int64_t n, const int* __restrict__ n_act_dev, int w, const float* __restrict__ U,
+         double* __restrict__ part) {
+  __shared__ double s[8][33];
+  int64_t nr = n_act_dev ? (int64_t)*n_act_dev : n;
+  int c = blockIdx.x * 32 + threadIdx.x;
+  double acc = 0.0;
+  if (c < w)
+    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < nr; r += (int64_t)gridDim.y * 8)
+      acc += (double)U[r * w + c];
+  s[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < w) {
+    double t = 0.0;
+    for (int y = 0; y < 8; ++y) t += s[y][threadIdx.x];
+    part[(int64_t)blockIdx.y * w + c] = t;
+  }
+}
+
+// gradient finalisation on one block:
+//   A[c] = sum_rb part[rb][c]; out[k] = sum_c Pz[c][k] A[c]  (V_z W1_z^T A)
+//   exact CVaR extras: out[d_z] = sum_{selected} Q_i, out[d_z+1] = #selected
+__global__ void __launch_bounds__(256)
+k_finalize_grad(int nrb, int h1, int d_z, const double* __restrict__ part, const double* __restrict__ Pz,
+                const int* __restrict__ rowidx, const int* __restrict__ n_act_dev,
+                const double* __restrict__ Q, int with_qsum, double* __restrict__ out) {
+  extern __shared__ double A[];   // h1
+  for (int c = threadIdx.x; c < h1; c += blockDim.x) {
+    double s = 0.0;
+    if (part)
+      for (int b = 0; b < nrb; ++b) s += part[(int64_t)b * h1 + c];
+    A[c] = s;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < d_z; k += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < h1; ++c) s += Pz[(int64_t)c * d_z + k] * A[c];
+    out[k] = s;
+  }
+  if (with_qsum && threadIdx.x < 32) {
+    int na = *n_act_dev;
+    double s = 0.0;
+    for (int r = threadIdx.x; r < na; r += 32) s += Q[rowidx[r]];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) { out[d_z] = s; out[d_z + 1] = (double)na; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact top-k selection (value desc, then global index asc).
+// Single-CTA 8-pass MSD radix select over order-preserving 64-bit keys,
+// then an index-ordered tie resolution at the threshold key.  `gidx` (double,
+// may be null = position) supplies the global index used for ordering and
+// marks padding (gidx < 0 -> never selected).  Output: mask (n).
+__global__ void __launch_bounds__(1024)
+k_topk_select(int64_t n, int64_t k, const double* __restrict__ vals, const double* __restrict__ gidx,
+              uint8_t* __restrict__ mask) {
+  __shared__ unsigned hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ long long s_krem;
+  __shared__ int wsum[32];
+  __shared__ long long s_run;
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_prefix = 0; s_krem = k; }
+  uint64_t himask = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    for (int d = tid; d < 256; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      if (gidx && gidx[i] < 0.0) continue;
+      uint64_t key = dkey(vals[i]);
+      if ((key & himask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long krem = s_krem, cum = 0;
+      int d = 255;
+      for (; d > 0; --d) {
+        if (cum + (long long)hist[d] >= krem) break;
+        cum += hist[d];
+      }
+      s_krem = krem - cum;
+      s_prefix = prefix | ((uint64_t)d << shift);
+    }
+    himask |= (0xFFull << shift);
+    __syncthreads();
+  }
+  const uint64_t T = s_prefix;
+  const long long need = s_krem;       // how many threshold-equal keys to take
+  if (tid == 0) s_run = 0;
+  __syncthreads();
+  // rows in ascending global index order: positions are index-ordered for
+  // the local case; candidate arrays are concatenated in rank order, and each
+  // rank's candidates are index-ordered, so position order == global order.
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    int64_t i = base + tid;
+    bool valid = i < n && !(gidx && gidx[i] < 0.0);
+    uint64_t key = valid ? dkey(vals[i]) : 0;
+    bool eq = valid && key == T;
+    unsigned b = __ballot_sync(0xffffffffu, eq);
+    int lane = tid & 31, warp = tid >> 5;
+    if (lane == 0) wsum[warp] = __popc(b);
+    __syncthreads();
+    if (tid == 0) {
+      int s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { int c = wsum[w]; wsum[w] = s; s += c; }
+    }
+    __syncthreads();
+    long long rank = s_run + wsum[warp] + __popc(b & ((1u << lane) - 1u));
+    if (i < n) mask[i] = (valid && (key > T || (eq && rank < need))) ? 1 : 0;
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_run += wsum[warp] + __popc(b);
+    __syncthreads();
+  }
+}
+
+// candidate export: the selected local rows as (value, global index) pairs,
+// index-ordered, padded with (0, -1) up to k.  cand layout: [k values][k idx]
+__global__ void k_export_candidates(int64_t k, const int* __restrict__ n_act_dev,
+                                    const int* __restrict__ rowidx, const double* __restrict__ Q,
+                                    int64_t goff, double* __restrict__ cand) {
+  int na = *n_act_dev;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < k;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (r < na) { cand[r] = Q[rowidx[r]]; cand[k + r] = (double)(goff + rowidx[r]); }
+    else { cand[r] = 0.0; cand[k + r] = -1.0; }
+  }
+}
+
+// gathered candidates [rank][2k] -> contiguous values / indices (rank order)
+__global__ void k_unpack_candidates(int n_ranks, int64_t k, const double* __restrict__ all,
+                                    double* __restrict__ vals, double* __restrict__ gidx) {
+  int64_t tot = (int64_t)n_ranks * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / k, j = e % k;
+    vals[e] = all[r * 2 * k + j];
+    gidx[e] = all[r * 2 * k + k + j];
+  }
+}
+
+// global selection mask over candidates -> local selection mask
+__global__ void k_scatter_selection(int64_t ncand, const uint8_t* __restrict__ cmask,
+                                    const double* __restrict__ gidx, int64_t goff, int64_t n,
+                                    uint8_t* __restrict__ sel) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncand;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (!cmask[e]) continue;
+    int64_t g = (int64_t)gidx[e] - goff;
+    if (g >= 0 && g < n) sel[g] = 1;
+  }
+}
+
+// fp64 -> fp32 / fp32 -> fp64 conversions and small helpers
+__global__ void k_f32_to_f64(int64_t n, const float* __restrict__ a, double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+// strided copy of G (n x ldg) -> dense (n x d_z) fp64
+__global__ void k_copy_g(int64_t n, int d_z, int ldg, const float* __restrict__ G, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * d_z;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / d_z; int k = (int)(e % d_z);
+    out[e] = G[i * ldg + k];
+  }
+}
+
+// forward-mode layer-1 tangent: T[(i,k), c] = D0[i, c] * Pz[c, k]  (the
+// tangent of x_z = V_z^T z through W1_z is the constant W1_z V_z^T)
+__global__ void k_tangent_seed(int64_t rows, int d_z, int h1, const float* __restrict__ D0,
+                               const float* __restrict__ Pz32t /* d_z x h1 */, float* __restrict__ T) {
+  int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  int64_t i = r / d_z; int k = (int)(r % d_z);
+  for (int c = threadIdx.x; c < h1; c += blockDim.x)
+    T[r * h1 + c] = D0[i * h1 + c] * Pz32t[(int64_t)k * h1 + c];
+}
+
+}  // namespace sdn

@@ -1,0 +1,272 @@
+"""`Engine`: one libsaadino handle (one device, one shard of SAA samples).
+
+Thin Python over the C ABI (include/saadino.h).  Host arrays are numpy;
+device exchange buffers for multi-process runs are torch CUDA tensors
+(torch is plumbing here: memory, streams, torch.distributed).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, fptr, i64ptr, lib
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+@dataclass
+class EvalResult:
+    value: float
+    grad_z: Optional[np.ndarray]
+    grad_t: Optional[float]
+    idx: Optional[np.ndarray]      # exact CVaR selection (global indices, ascending)
+    n_samples: int
+    n_selected: int
+    q_mean: float
+    q_var: float
+
+
+class Engine:
+    """Device-resident surrogate + sample shard.
+
+    model: any object with weights/biases/input_scale/output_mean/output_std
+    (+ activation, residual, Vz) -- see model.SurrogateModel."""
+
+    def __init__(self, model, max_samples: int, device: int = 0, gemm: str = "auto"):
+        w = [int(np.asarray(model.weights[0]).shape[1])] + [int(np.asarray(W).shape[0]) for W in model.weights]
+        self.widths = w
+        self.r_m = int(np.asarray(model.input_scale).shape[0])
+        Vz = getattr(model, "Vz", None)
+        self.d_z = int(np.asarray(Vz).shape[0]) if Vz is not None else w[0] - self.r_m
+        self.r_u = w[-1]
+        self.device = int(device)
+        self.max_samples = int(max_samples)
+        self._widths_c = (C.c_int32 * len(w))(*w)
+        cfg = _lib.Config(n_layers=len(model.weights), widths=self._widths_c, r_m=self.r_m, d_z=self.d_z,
+                          activation=_lib.ACT[model.activation], residual=int(bool(model.residual)),
+                          gemm=_lib.GEMM[gemm], device=self.device, max_samples=self.max_samples)
+        h = C.c_void_p()
+        check(lib.sdn_create(C.byref(cfg), C.byref(h)), "sdn_create")
+        self.h = h
+        self.n = 0
+        self.global_offset = 0
+        self.d_u = None
+        self.set_model(model)
+
+    # -- lifetime --------------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sdn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def kernel_launches(self) -> int:
+        return int(lib.sdn_kernel_launches(self.h))
+
+    def synchronize(self):
+        check(lib.sdn_synchronize(self.h), "sdn_synchronize")
+
+    def set_stream(self, stream_handle: int):
+        check(lib.sdn_set_stream(self.h, C.c_void_p(stream_handle)), "sdn_set_stream")
+
+    # -- setup -------------------------------------------------------------------
+    def set_model(self, model):
+        Ws = [_f32(W) for W in model.weights]
+        bs = [_f32(b) for b in model.biases]
+        self._keep = (Ws, bs)
+        Wp = (_lib._F * len(Ws))(*[fptr(W) for W in Ws])
+        bp = (_lib._F * len(bs))(*[fptr(b) for b in bs])
+        Vz = getattr(model, "Vz", None)
+        vz = _f32(Vz) if Vz is not None else None
+        check(lib.sdn_set_model(self.h, Wp, bp, fptr(_f32(model.input_scale)), fptr(_f32(model.output_mean)),
+                                fptr(_f32(model.output_std)), fptr(vz) if vz is not None else None),
+              "sdn_set_model")
+
+    def set_tracking(self, c, q0: float):
+        check(lib.sdn_set_tracking(self.h, fptr(_f32(c)), float(q0)), "sdn_set_tracking")
+
+    def set_decoder(self, U, ubias, Mdiag, u_target):
+        U = _f32(U)
+        self.d_u = U.shape[0]
+        check(lib.sdn_set_decoder(self.h, U.shape[0], fptr(U), fptr(_f32(ubias)), fptr(_f32(Mdiag)),
+                                  fptr(_f32(u_target))), "sdn_set_decoder")
+
+    def set_samples(self, m_r, global_offset: int = 0):
+        """m_r: (n, r_m) numpy array, or a torch CUDA tensor on this device."""
+        if hasattr(m_r, "data_ptr") and getattr(m_r, "is_cuda", False):
+            t = m_r.contiguous().float()
+            n = t.shape[0]
+            check(lib.sdn_set_samples(self.h, C.c_void_p(t.data_ptr()), n, int(global_offset), 1), "sdn_set_samples")
+        else:
+            a = _f32(m_r)
+            if a.ndim != 2 or a.shape[1] != self.r_m:
+                raise ValueError("samples must be (n, r_m)")
+            n = a.shape[0]
+            check(lib.sdn_set_samples(self.h, a.ctypes.data_as(C.c_void_p), n, int(global_offset), 0),
+                  "sdn_set_samples")
+        self.n = int(n)
+        self.global_offset = int(global_offset)
+
+    def encode_fields(self, m, Vm, Mdiag, m_mean: float, global_offset: int = 0):
+        a = _f32(m)
+        check(lib.sdn_encode_fields(self.h, a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1], fptr(_f32(Vm)),
+                                    fptr(_f32(Mdiag)), float(m_mean), int(global_offset), 0), "sdn_encode_fields")
+        self.n = a.shape[0]
+        self.global_offset = int(global_offset)
+
+    # -- evaluation ----------------------------------------------------------------
+    @staticmethod
+    def make_risk(kind: str, beta: float = 0.95, eps: float = 1e-4, t: Optional[float] = None,
+                  alpha: float = 0.0, qoi: str = "reduced", need_grad: bool = True) -> _lib.Risk:
+        if kind not in _lib.RISK:
+            raise ValueError(f"unknown risk kind {kind!r}")
+        if kind == "cvar" and t is None:
+            raise ValueError("CVaR objective needs the auxiliary variable t")
+        return _lib.Risk(kind=_lib.RISK[kind], qoi=_lib.QOI[qoi], beta=float(beta), eps=float(eps),
+                         t=float(t) if t is not None else 0.0, alpha=float(alpha), need_grad=int(bool(need_grad)))
+
+    def eval(self, z, kind: str, beta: float = 0.95, eps: float = 1e-4, t: Optional[float] = None,
+             alpha: float = 0.0, qoi: str = "reduced", need_grad: bool = True) -> EvalResult:
+        risk = self.make_risk(kind, beta, eps, t, alpha, qoi, need_grad)
+        z = _f64(z)
+        if z.shape != (self.d_z,):
+            raise ValueError(f"control must have shape ({self.d_z},)")
+        res = _lib.Result()
+        grad = np.zeros(self.d_z)
+        idx = None
+        if kind == "cvar_exact":
+            k = max(int(np.ceil((1.0 - beta) * self.n - 1e-9)), 1)
+            idx = np.zeros(k, np.int64)
+        check(lib.sdn_eval(self.h, dptr(z), C.byref(risk), C.byref(res), dptr(grad),
+                           i64ptr(idx) if idx is not None else None), "sdn_eval")
+        return EvalResult(value=res.value, grad_z=grad if need_grad else None,
+                          grad_t=res.grad_t if kind == "cvar" else None, idx=idx,
+                          n_samples=int(res.n_samples), n_selected=int(res.n_selected),
+                          q_mean=res.q_mean, q_var=res.q_var)
+
+    def eval_samples(self, z, qoi: str = "reduced", need_grad: bool = True):
+        z = _f64(z)
+        Q = np.empty(self.n)
+        G = np.empty((self.n, self.d_z)) if need_grad else None
+        check(lib.sdn_eval_samples(self.h, dptr(z), _lib.QOI[qoi], dptr(Q), dptr(G) if G is not None else None),
+              "sdn_eval_samples")
+        return Q, G
+
+    def forward_batch(self, m_r, z) -> np.ndarray:
+        m_r = np.atleast_2d(_f32(m_r))
+        z = np.atleast_2d(_f32(z))
+        if m_r.shape[1] != self.r_m or z.shape[1] != self.d_z:
+            raise ValueError("input widths do not match the network spec")
+        z = _f32(np.broadcast_to(z, (m_r.shape[0], self.d_z)))
+        phi = np.empty((m_r.shape[0], self.r_u), np.float32)
+        check(lib.sdn_forward_batch(self.h, fptr(m_r), fptr(z), m_r.shape[0], fptr(phi)), "sdn_forward_batch")
+        return phi
+
+    def jacobian_batch(self, m_r, z, decoded: bool = False) -> np.ndarray:
+        m_r = np.atleast_2d(_f32(m_r))
+        z = _f32(np.broadcast_to(np.atleast_2d(_f32(z)), (m_r.shape[0], self.d_z)))
+        if m_r.shape[1] != self.r_m:
+            raise ValueError("input widths do not match the network spec")
+        outw = self.d_u if decoded else self.r_u
+        if decoded and self.d_u is None:
+            raise RuntimeError("set_decoder first")
+        J = np.empty((m_r.shape[0], outw, self.d_z), np.float32)
+        check(lib.sdn_jacobian_batch(self.h, fptr(m_r), fptr(z), m_r.shape[0], int(decoded), fptr(J)),
+              "sdn_jacobian_batch")
+        return J
+
+    def lift(self, phi) -> np.ndarray:
+        phi = np.atleast_2d(_f32(phi))
+        u = np.empty((phi.shape[0], self.d_u), np.float32)
+        check(lib.sdn_lift(self.h, fptr(phi), phi.shape[0], fptr(u)), "sdn_lift")
+        return u
+
+    def select_topk(self, values, k: int) -> np.ndarray:
+        v = _f64(values)
+        idx = np.zeros(int(k), np.int64)
+        check(lib.sdn_select_topk(self.h, v.ctypes.data_as(C.c_void_p), v.size, int(k), 0, i64ptr(idx)),
+              "sdn_select_topk")
+        return idx
+
+    def eval_multi(self, z, risks) -> list:
+        """Several risks from one forward pass.  risks: list of dicts with
+        keys of `eval` (kind, beta, eps, t, alpha, qoi, need_grad)."""
+        rs = [self.make_risk(**r) for r in risks]
+        arr = (_lib.Risk * len(rs))(*rs)
+        res = (_lib.Result * len(rs))()
+        z = _f64(z)
+        if z.shape != (self.d_z,):
+            raise ValueError(f"control must have shape ({self.d_z},)")
+        grads = np.zeros((len(rs), self.d_z))
+        ks = [max(int(np.ceil((1.0 - r["beta"]) * self.n - 1e-9)), 1) if r["kind"] == "cvar_exact" else 0
+              for r in risks]
+        idx = np.zeros(max(sum(ks), 1), np.int64)
+        check(lib.sdn_eval_multi(self.h, dptr(z), arr, len(rs), res, dptr(grads), i64ptr(idx)), "sdn_eval_multi")
+        out, off = [], 0
+        for i, r in enumerate(risks):
+            sel = None
+            if ks[i]:
+                sel = idx[off:off + ks[i]].copy()
+                off += ks[i]
+            out.append(EvalResult(value=res[i].value, grad_z=grads[i] if r.get("need_grad", True) else None,
+                                  grad_t=res[i].grad_t if r["kind"] == "cvar" else None, idx=sel,
+                                  n_samples=int(res[i].n_samples), n_selected=int(res[i].n_selected),
+                                  q_mean=res[i].q_mean, q_var=res[i].q_var))
+        return out
+
+    # -- instrumentation ---------------------------------------------------------------
+    def profile(self, enable: bool = True):
+        check(lib.sdn_profile(self.h, int(bool(enable))), "sdn_profile")
+
+    def profile_read(self) -> dict:
+        n = len(_lib.PROF_CLASSES)
+        ms, fl, by = np.zeros(n), np.zeros(n), np.zeros(n)
+        cnt = np.zeros(n, np.int64)
+        check(lib.sdn_profile_read(self.h, n, dptr(ms), dptr(fl), dptr(by), i64ptr(cnt)), "sdn_profile_read")
+        return {name: dict(ms=float(ms[i]), flops=float(fl[i]), bytes=float(by[i]), launches=int(cnt[i]))
+                for i, name in enumerate(_lib.PROF_CLASSES)}
+
+    # -- multi-process phases (exchange buffers: torch CUDA float64 tensors) ------------
+    def partial_len(self) -> int:
+        return int(lib.sdn_partial_len(self.h))
+
+    def phase_forward(self, z, risk: _lib.Risk, stats_dev):
+        z = _f64(z)
+        self._phase_z = z
+        self._phase_risk = risk
+        check(lib.sdn_eval_forward(self.h, dptr(z), C.byref(risk), C.c_void_p(stats_dev.data_ptr())),
+              "sdn_eval_forward")
+
+    def phase_candidates(self, k: int, cand_dev):
+        check(lib.sdn_eval_candidates(self.h, int(k), C.c_void_p(cand_dev.data_ptr())), "sdn_eval_candidates")
+
+    def phase_select(self, all_cand_dev, n_ranks: int, k: int):
+        check(lib.sdn_eval_select(self.h, C.c_void_p(all_cand_dev.data_ptr()), int(n_ranks), int(k)),
+              "sdn_eval_select")
+
+    def phase_backward(self, stats_dev, partial_dev):
+        check(lib.sdn_eval_backward(self.h, C.c_void_p(stats_dev.data_ptr()), C.c_void_p(partial_dev.data_ptr())),
+              "sdn_eval_backward")
+
+    def phase_finish(self, stats_dev, partial_dev):
+        res = _lib.Result()
+        grad = np.zeros(self.d_z)
+        check(lib.sdn_eval_finish(self.h, C.c_void_p(stats_dev.data_ptr()), C.c_void_p(partial_dev.data_ptr()),
+                                  C.byref(res), dptr(grad)), "sdn_eval_finish")
+        return res, grad

@@ -1,0 +1,209 @@
+"""GPU parity: libsaadino kernels vs the float64 oracle on the same seeded
+float32 inputs.  Tolerances (BASELINE north_star): 1e-4 relative for the
+risk value and the gradient (float32 path); CVaR selection indices
+bit-exact against the oracle's selection run on the GPU's own Q."""
+
+import numpy as np
+import pytest
+
+from oracle import mrdino_ref as ref
+from paper_2305_20053_b200 import Engine, workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+def _engine(p, gemm="auto", cap=None):
+    eng = Engine(p, max_samples=cap or p.m_r.shape[0], device=0, gemm=gemm)
+    eng.set_tracking(p.c, p.q0)
+    eng.set_samples(p.m_r)
+    return eng
+
+
+def _oracle(p, risk, t=None, decoded=False):
+    m = ref.as_oracle(p)
+    if decoded:
+        return ref.risk_and_grad(m, p.m_r, p.z, risk, t=t,
+                                 decoded=(p.U, p.ubias, p.Mdiag_u, p.u_target))
+    return ref.risk_and_grad(m, p.m_r, p.z, risk, t=t, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _problem(name, n, seed=0, **kw):
+    cfg = wl.WORKLOADS[name].with_samples(n)
+    return wl.make_problem(cfg, seed=seed, count=n, **kw)
+
+
+@pytest.mark.parametrize("gemm", ["simt", "auto"])
+def test_c1_meanvar_value_and_grad(gemm):
+    p = _problem("c1", 256)
+    r = _engine(p, gemm).eval(p.z, "meanvar", beta=0.5, alpha=1e-2)
+    o = _oracle(p, ref.Risk("meanvar", beta=0.5, alpha=1e-2))
+    assert abs(r.value - o["value"]) <= RTOL * abs(o["value"])
+    assert _rel(r.grad_z, o["grad_z"]) <= RTOL
+
+
+@pytest.mark.parametrize("kind", ["mean", "meanvar", "cvar", "cvar_exact"])
+def test_c2_shapes_all_risks(kind):
+    p = _problem("c2", 2048, bias_variant=True)
+    eng = _engine(p)
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    t = ref.mc_var(Qo, 0.95) if kind == "cvar" else None
+    beta = 1.0 if kind == "meanvar" else 0.95
+    r = eng.eval(p.z, kind, beta=beta, eps=1e-4 if kind != "cvar" else 1e-1, t=t, alpha=1e-2)
+    o = _oracle(p, ref.Risk(kind, beta=beta, eps=1e-4 if kind != "cvar" else 1e-1, alpha=1e-2), t=t)
+    assert abs(r.value - o["value"]) <= RTOL * abs(o["value"])
+    assert _rel(r.grad_z, o["grad_z"]) <= RTOL
+    if kind == "cvar":
+        assert abs(r.grad_t - o["grad_t"]) <= 1e-3
+    if kind == "cvar_exact":
+        # bit-exact selection: the oracle's rule applied to the GPU's own Q
+        Qg, _ = eng.eval_samples(p.z, need_grad=False)
+        np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qg, 0.95)))
+        # and near-ties aside, the same set as the fp64 oracle's Q
+        assert len(set(r.idx) ^ set(o["idx"])) <= 2
+
+
+def test_eval_samples_protocol_matches_forward_mode_reference():
+    """evaluator(z) -> (Q, G): per-sample gradients vs the reference's
+    forward-mode algorithm (riskopt.py:178-194)."""
+    p = _problem("c1", 300)
+    Q, G = _engine(p).eval_samples(p.z)
+    Qo, Go = ref.evaluate_forward_mode(ref.as_oracle(p), p.m_r, p.z, ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    np.testing.assert_allclose(Q, Qo, rtol=RTOL)
+    assert _rel(G, Go) <= RTOL
+    assert np.abs(G - Go).max() <= RTOL * np.abs(Go).max() * 10
+
+
+@pytest.mark.parametrize("act,residual", [("tanh", False), ("elu", True), ("softplus", True), ("sigmoid", False)])
+def test_forward_batch_and_jacobian_rowwise_z(act, residual):
+    p = _problem("c1", 64)
+    p.activation, p.residual = act, residual
+    g = np.random.default_rng(5)
+    Z = g.uniform(-4, 4, size=(64, p.cfg.d_z)).astype(np.float32)
+    eng = _engine(p)
+    phi = eng.forward_batch(p.m_r, Z)
+    J = eng.jacobian_batch(p.m_r, Z)
+    m = ref.as_oracle(p)
+    np.testing.assert_allclose(phi, ref.forward_batch(m, p.m_r, Z), rtol=1e-4, atol=1e-4)
+    Jo = ref.z_jacobian_batch(m, p.m_r, Z)
+    assert _rel(J, Jo) <= RTOL
+
+
+def test_decoded_frame_and_jacobian():
+    p = _problem("c1", 128, with_decoder=True)
+    eng = _engine(p)
+    eng.set_decoder(p.U, p.ubias, p.Mdiag_u, p.u_target)
+    r = eng.eval(p.z, "meanvar", beta=0.5, alpha=1e-2, qoi="decoded")
+    o = _oracle(p, ref.Risk("meanvar", beta=0.5, alpha=1e-2), decoded=True)
+    assert abs(r.value - o["value"]) <= RTOL * abs(o["value"])
+    assert _rel(r.grad_z, o["grad_z"]) <= RTOL
+    # decoded control Jacobian U J (tests/test_acceptance.py:326)
+    Z = np.broadcast_to(p.z, (16, p.cfg.d_z))
+    Jd = eng.jacobian_batch(p.m_r[:16], Z, decoded=True)
+    Jo = ref.z_jacobian_batch(ref.as_oracle(p), p.m_r[:16], Z)
+    Jod = np.einsum("du,iuk->idk", p.U.astype(np.float64), Jo)
+    assert _rel(Jd, Jod) <= RTOL
+    # lift (pod.py:36-40)
+    phi = eng.forward_batch(p.m_r[:8], Z[:8])
+    u = eng.lift(phi)
+    np.testing.assert_allclose(u, phi.astype(np.float64) @ p.U.T.astype(np.float64) + p.ubias, rtol=1e-4, atol=1e-5)
+
+
+def test_reference_kats_on_gpu():
+    """tests/test_surrogate.py:64-84, 106-112, 132-137 through the GPU."""
+    from paper_2305_20053_b200 import NetworkSpec, init_model
+    g = np.random.default_rng(0)
+    spec = NetworkSpec(r_m=4, d_z=4, r_u=8, hidden=(8,), activation="tanh")
+    mean = g.normal(size=8)
+    model = init_model(spec, seed=0, output_mean=mean)
+    for W in model.weights:
+        W[:] = 0.0
+    np.testing.assert_allclose(model.forward(g.normal(size=4), g.normal(size=4)), mean, rtol=1e-6, atol=1e-6)
+    np.testing.assert_array_equal(model.z_jacobian(g.normal(size=4), g.normal(size=4)), np.zeros((8, 4)))
+    # linear network -> constant Jacobian
+    spec = NetworkSpec(r_m=4, d_z=4, r_u=8, hidden=(8,), activation="identity")
+    model = init_model(spec, seed=4)
+    J1 = model.z_jacobian(g.normal(size=4), g.normal(size=4))
+    J2 = model.z_jacobian(g.normal(size=4), g.normal(size=4))
+    np.testing.assert_allclose(J1, J2, atol=1e-6)
+    # single affine layer (no hidden): phi = mean + std * (W [m_r*s, z] + b)
+    spec = NetworkSpec(r_m=4, d_z=4, r_u=8, hidden=(), activation="identity")
+    scale, std = g.uniform(0.5, 2, 4), g.uniform(0.5, 2, 8)
+    model = init_model(spec, seed=1, input_scale=scale, output_mean=mean, output_std=std)
+    m_r, z = g.normal(size=4), g.normal(size=4)
+    expect = mean + std * (model.weights[0] @ np.concatenate([m_r * scale, z]) + model.biases[0])
+    np.testing.assert_allclose(model.forward(m_r, z), expect, rtol=1e-5, atol=1e-5)
+    with pytest.raises(ValueError):
+        model.forward(g.normal(size=3), z)
+
+
+def test_gpu_evaluator_in_reference_protocol():
+    from paper_2305_20053_b200 import (RiskSpec, SAAProblem, SurrogateEvaluator, ReducedTrackingForm,
+                                       saa_objective)
+    p = _problem("c1", 512)
+    ev = SurrogateEvaluator(p, p.m_r, ReducedTrackingForm(p.c.astype(np.float64), p.q0))
+    t = 0.5 * (ev(p.z)[0].mean() + ev(p.z)[0].max())
+    prob = SAAProblem(ev, np.full(25, -4.0), np.full(25, 4.0), RiskSpec(kind="cvar", beta=0.9, eps=1e-2))
+    v, gz, gt = saa_objective(prob, p.z, t)
+    o = _oracle(p, ref.Risk("cvar", beta=0.9, eps=1e-2), t=t)
+    assert abs(v - o["value"]) <= RTOL * abs(o["value"])
+    assert _rel(gz, o["grad_z"]) <= RTOL
+    assert ev.counts["batched_evals"] == 3 and ev.counts["samples_evaluated"] == 3 * 512
+
+
+def test_select_topk_matches_oracle_with_ties():
+    eng = _engine(_problem("c1", 16))
+    g = np.random.default_rng(3)
+    v = np.round(g.normal(size=50000), 2)      # many exact ties
+    for k in (1, 7, 2500, 49999):
+        idx = eng.select_topk(v, k)
+        expect = np.lexsort((np.arange(v.size), -v))[:k]
+        np.testing.assert_array_equal(np.sort(idx), np.sort(expect))
+
+
+def test_encoder_matches_oracle():
+    cfg = wl.WORKLOADS["c1"].with_samples(96)
+    p = wl.make_problem(cfg, seed=0, count=96)
+    psi, lam, mdiag = wl.kl_modes(cfg, 0)
+    m = wl.fields(cfg, 0, 0, 96).astype(np.float32)
+    eng = Engine(p, max_samples=96)
+    eng.set_tracking(p.c, p.q0)
+    eng.encode_fields(m, psi[:, :cfg.r_m].astype(np.float32), mdiag.astype(np.float32), wl.M_MEAN)
+    Q, _ = eng.eval_samples(p.z, need_grad=False)
+    enc = ref.encode(m, psi[:, :cfg.r_m].astype(np.float32), mdiag.astype(np.float32), wl.M_MEAN)
+    p.m_r = enc.astype(np.float32)
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), enc, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    np.testing.assert_allclose(Q, Qo, rtol=1e-4)
+
+
+def test_determinism_bitwise():
+    p = _problem("c2", 4096)
+    eng = _engine(p)
+    a = eng.eval(p.z, "meanvar", beta=1.0)
+    b = eng.eval(p.z, "meanvar", beta=1.0)
+    assert a.value == b.value
+    np.testing.assert_array_equal(a.grad_z, b.grad_z)
+
+
+def test_nan_sample_propagates():
+    p = _problem("c1", 64)
+    p.m_r[5, 3] = np.nan
+    r = _engine(p).eval(p.z, "mean")
+    assert np.isnan(r.value) and np.all(np.isnan(r.grad_z))
+
+
+def test_errors_mirror_reference():
+    p = _problem("c1", 32)
+    eng = _engine(p)
+    with pytest.raises(ValueError):
+        eng.eval(p.z, "cvar")                      # riskopt.py:236-237: needs t
+    with pytest.raises(ValueError):
+        eng.eval(p.z, "cvar_exact", beta=1.5)
+    with pytest.raises(ValueError):
+        eng.eval(p.z[:3], "mean")
