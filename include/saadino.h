@@ -201,6 +201,10 @@ int sdn_profile(sdn_handle* h, int32_t enable);
 int sdn_profile_read(sdn_handle* h, int32_t n_cls, double* ms, double* flops, double* bytes,
                      int64_t* count);
 
+/* Kernel tuning: average ms of one layer-1 forward GEMM over M rows
+ * (mode 0 tcgen05 + null epilogue, 1 tcgen05 + fused epilogue, 2 SIMT). */
+int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t reps, double* ms);
+
 /* Number of kernels this handle has launched (lifetime). */
 int64_t sdn_kernel_launches(sdn_handle* h);
 

@@ -72,6 +72,7 @@ SIGNATURES = {
     "sdn_last_q": (C.c_int, [_P, C.POINTER(_P), _I64]),
     "sdn_kernel_launches": (C.c_int64, [_P]),
     "sdn_profile": (C.c_int, [_P, C.c_int32]),
+    "sdn_debug_gemm": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _D]),
     "sdn_profile_read": (C.c_int, [_P, C.c_int32, _D, _D, _D, _I64]),
 }
 

@@ -225,11 +225,18 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
   h->prows = 0;
   ProfScope ps(h, h->pcls, rows >= 0 ? 2.0 * rows * N * K : 0.0, 0.0, rows, 2.0 * N * K);
   h->pcls = PC_OTHER;
-  if (h->gemm != SDN_GEMM_SIMT && !AT && tcB && tcA &&
-      tc_gemm_supported(M, N, K)) {
-    int rc = tc_gemm<Epi>(h->stream, M, Mdev, N, K, *tcA, *tcB, epi);
-    h->launches += 2;
-    if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed");
+  bool use_tc = h->gemm != SDN_GEMM_SIMT && !AT && tcB && tcA && h->tcw.enabled && tc_gemm_supported(M, N, K) &&
+                tcA->ld % 8 == 0 && tcB->ld % 8 == 0;
+  if (use_tc && h->gemm == SDN_GEMM_AUTO) {
+    // small GEMMs (c1, CVaR tails) fill more SMs with 64x64 SIMT tiles
+    const int64_t mrows = rows >= 0 ? rows : M;
+    const int64_t tiles = cdiv(mrows, 128) * cdiv(N, N <= 128 ? 128 : 256);
+    if (tiles < h->num_sms / 2) use_tc = false;
+  }
+  if (use_tc) {
+    int rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, Mdev, N, K, *tcA, *tcB, epi);
+    h->launches++;
+    if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");
     CHECK_LAUNCH(h);
     return SDN_OK;
   }
@@ -403,7 +410,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->n_act_dev, 1))) return bail(rc);
   h->qgrid = (int)std::min<int64_t>(cdiv(cap, 8), 2 * h->num_sms);
   if ((rc = dalloc(h, &h->qpart, (size_t)h->qgrid * STATS_LEN))) return bail(rc);
-  h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 256);
+  h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 64);
   if ((rc = dalloc(h, &h->cpart, (size_t)h->crb * h->maxw))) return bail(rc);
   if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
@@ -573,7 +580,9 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   h->compacted = false;
   const bool dec = risk->qoi == SDN_QOI_DECODED;
   const double q0 = dec ? h->q0dec : h->q0;
-  h->shift = h->have_mean ? h->last_mean : q0;
+  // moments accumulate (Q - shift) in fp64; shift = q0 keeps every evaluation
+  // stateless and deterministic (cancellation ~1e-16 (Qbar - q0)^2 / var)
+  h->shift = q0;
   TRY(upload_z(h, z));
   { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
   k_zbias<<<(unsigned)cdiv(h->h1, 128), 128, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb); }
@@ -652,7 +661,7 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
   if (h->compacted) { rowidx = h->rowidx; nact = h->n_act_dev; }
   const int64_t rows_hint = exact ? h->kk : (h->compacted ? -1 : h->n);
   if (!r.need_grad) {
-    k_finalize_grad<<<1, 256, sizeof(double) * h->h1, h->stream>>>(0, h->h1, h->d_z, nullptr, h->Pz, h->rowidx,
+    k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(0, h->h1, h->d_z, nullptr, h->Pz, h->rowidx,
                                                                     h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
     h->launches++;
     CHECK_LAUNCH(h);
@@ -676,7 +685,7 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
     h->launches++;
   }
   ProfScope psf(h, PC_FINAL, 0.0, 8.0 * h->crb * h->h1);
-  k_finalize_grad<<<1, 256, sizeof(double) * h->h1, h->stream>>>(
+  k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(
       nmax > 0 ? h->crb : 0, h->h1, h->d_z, nmax > 0 ? h->cpart : nullptr, h->Pz, h->rowidx, h->n_act_dev, h->Q,
       exact ? 1 : 0, partial_dev);
   h->launches++;
@@ -1245,3 +1254,37 @@ int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k, i
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// kernel-tuning entry: time one layer-1 forward GEMM (A = activation operand,
+// B = W_1) `reps` times.  mode 0: tcgen05 mainloop with a null epilogue;
+// 1: tcgen05 with the fused hidden-layer epilogue; 2: SIMT with the same
+// epilogue.  ms[0] = average device ms per launch.
+extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t reps, double* ms) {
+  if (!h || !ms || h->L < 3 || M < 1 || M > h->cap) return fail(SDN_ERR_ARG, "bad argument");
+  if (mode != 2 && !h->tcw.enabled) return fail(SDN_ERR_STATE, "tensor-core path unavailable");
+  CU(cudaSetDevice(h->device));
+  const int K = h->w[1], N = h->w[2];
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  EpiFwdHidden e{h->b[1], h->res[1] ? h->H[0] : nullptr, h->H[1], h->D[1], (int64_t)N, h->act};
+  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{&h->tcw.act[1]}};
+  h->tcw.act[0].rows = M;
+  int rc = 0;
+  for (int it = 0; it <= reps && rc == 0; ++it) {
+    if (it == 1) cudaEventRecord(a, h->stream);
+    if (mode == 0) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], EpiNull{});
+    else if (mode == 1) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], ch);
+    else { launch_simt<128, 128, 8, 8, false, true>(h, M, nullptr, N, K, h->H[0], K, h->W[1], K, ch, true); }
+  }
+  cudaEventRecord(b, h->stream);
+  cudaError_t err = cudaEventSynchronize(b);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (rc || err != cudaSuccess) return fail(SDN_ERR_CUDA, std::string("debug gemm: ") + cudaGetErrorString(cudaGetLastError()));
+  ms[0] = t / std::max(reps, 1);
+  return SDN_OK;
+}

@@ -14,6 +14,14 @@
 
 namespace sdn {
 
+// output widths that are not a multiple of 4 (d_u, d_z): the last float4
+// group is written column by column through Epi::col
+template <class Epi>
+SDN_DEV void epi_tail(const Epi& epi, int64_t r, int c, int nv, float a, float b, float d) {
+  float v[3] = {a, b, d};
+  for (int j = 0; j < nv; ++j) epi.col(r, c + j, v[j]);
+}
+
 template <int BM, int BN, int BK, int TM, int TN, bool AT, bool BT, bool VEC, class Epi>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 gemm_simt_kernel(int64_t M, const int* __restrict__ Mdev, int N, int K, const float* __restrict__ A,
@@ -122,7 +130,8 @@ gemm_simt_kernel(int64_t M, const int* __restrict__ Mdev, int N, int K, const fl
 #pragma unroll
     for (int j = 0; j < TN; j += 4) {
       int c = n0 + tx * TN + j;
-      if (c < N) epi(r, c, make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]));
+      if (c + 4 <= N) epi(r, c, make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]));
+      else if (c < N) epi_tail(epi, r, c, N - c, acc[i][j], acc[i][j + 1], acc[i][j + 2]);
     }
   }
 }
@@ -135,8 +144,11 @@ gemm_simt_kernel(int64_t M, const int* __restrict__ Mdev, int N, int K, const fl
 struct EpiStore {
   float* C; int64_t ldc;
   SDN_DEV void operator()(int64_t r, int c, float4 v) const {
-    *reinterpret_cast<float4*>(C + r * ldc + c) = v;
+    float* p = C + r * ldc + c;
+    if ((ldc & 3) == 0) *reinterpret_cast<float4*>(p) = v;
+    else { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
   }
+  SDN_DEV void col(int64_t r, int c, float v) const { C[r * ldc + c] = v; }
 };
 
 // fp64 accumulate (split-K setup GEMMs): C64[r, c] += acc
@@ -146,6 +158,7 @@ struct EpiAccum64 {
     double* p = C + r * ldc + c;
     p[0] += v.x; p[1] += v.y; p[2] += v.z; p[3] += v.w;
   }
+  SDN_DEV void col(int64_t r, int c, float v) const { C[r * ldc + c] += v; }
 };
 
 // store with bias add and an optional per-column scale/shift:
@@ -161,7 +174,15 @@ struct EpiAffine {
       if (shift) y += shift[c + j];
       x[j] = y;
     }
-    *reinterpret_cast<float4*>(C + r * ldc + c) = make_float4(x[0], x[1], x[2], x[3]);
+    float* p = C + r * ldc + c;
+    if ((ldc & 3) == 0) *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    else { p[0] = x[0]; p[1] = x[1]; p[2] = x[2]; p[3] = x[3]; }
+  }
+  SDN_DEV void col(int64_t r, int c, float v) const {
+    float y = v + (bias ? bias[c] : 0.0f);
+    if (scale) y *= scale[c];
+    if (shift) y += shift[c];
+    C[r * ldc + c] = y;
   }
 };
 
@@ -184,6 +205,7 @@ struct EpiFwdHidden {
     return h;
   }
   SDN_DEV void operator()(int64_t r, int c, float4 v) const { (void)apply(r, c, v); }
+  SDN_DEV void col(int64_t, int, float) const {}   // widths are multiples of 4 (sdn_create)
 };
 
 // backward step: g = acc [+ resid]; U = D[row] * g; G = g (optional).
@@ -207,6 +229,7 @@ struct EpiBwd {
     return u;
   }
   SDN_DEV void operator()(int64_t r, int c, float4 v) const { (void)apply(r, c, v); }
+  SDN_DEV void col(int64_t, int, float) const {}   // widths are multiples of 4 (sdn_create)
 };
 
 // forward-mode tangent step (surrogate.py:208-223 with residual):
@@ -222,6 +245,7 @@ struct EpiTangent {
     }
     *reinterpret_cast<float4*>(tout + r * ld + c) = o;
   }
+  SDN_DEV void col(int64_t, int, float) const {}   // widths are multiples of 4 (sdn_create)
 };
 
 // Jacobian scatter: tangent row (i*d_z + k), column u -> J[i, u, k] * scale[u]
@@ -234,6 +258,10 @@ struct EpiJacScatter {
     float* base = J + i * ncol * d_z + k;
 #pragma unroll
     for (int j = 0; j < 4; ++j) base[(int64_t)(c + j) * d_z] = scale ? x[j] * scale[c + j] : x[j];
+  }
+  SDN_DEV void col(int64_t r, int c, float v) const {
+    int64_t i = r / d_z; int k = (int)(r % d_z);
+    J[i * ncol * d_z + (int64_t)c * d_z + k] = scale ? v * scale[c] : v;
   }
 };
 

@@ -198,7 +198,7 @@ k_colsum(int64_t n, const int* __restrict__ n_act_dev, int w, const float* __res
 // gradient finalisation on one block:
 //   A[c] = sum_rb part[rb][c]; out[k] = sum_c Pz[c][k] A[c]  (V_z W1_z^T A)
 //   exact CVaR extras: out[d_z] = sum_{selected} Q_i, out[d_z+1] = #selected
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 k_finalize_grad(int nrb, int h1, int d_z, const double* __restrict__ part, const double* __restrict__ Pz,
                 const int* __restrict__ rowidx, const int* __restrict__ n_act_dev,
                 const double* __restrict__ Q, int with_qsum, double* __restrict__ out) {
@@ -210,17 +210,19 @@ k_finalize_grad(int nrb, int h1, int d_z, const double* __restrict__ part, const
     A[c] = s;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < d_z; k += blockDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k = warp; k < d_z; k += nw) {          // one warp per output, lanes over c
     double s = 0.0;
-    for (int c = 0; c < h1; ++c) s += Pz[(int64_t)c * d_z + k] * A[c];
-    out[k] = s;
+    for (int c = lane; c < h1; c += 32) s += Pz[(int64_t)c * d_z + k] * A[c];
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
   }
-  if (with_qsum && threadIdx.x < 32) {
+  if (with_qsum && warp == nw - 1) {
     int na = *n_act_dev;
     double s = 0.0;
-    for (int r = threadIdx.x; r < na; r += 32) s += Q[rowidx[r]];
+    for (int r = lane; r < na; r += 32) s += Q[rowidx[r]];
     s = warp_sum(s);
-    if (threadIdx.x == 0) { out[d_z] = s; out[d_z + 1] = (double)na; }
+    if (lane == 0) { out[d_z] = s; out[d_z + 1] = (double)na; }
   }
 }
 
