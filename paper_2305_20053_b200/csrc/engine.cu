@@ -23,6 +23,8 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 using namespace sdn;
@@ -74,6 +76,7 @@ struct sdn_handle {
   std::vector<char> res;        // residual flag per layer
   float* Wx = nullptr;          // h1 x ldx : [W0m' | Pz32 | 0]
   double* Pz = nullptr;         // h1 x d_z  = W0z V_z^T (fp64)
+  double* PzT = nullptr;        // d_z x h1  (transposed, for the gradient projection)
   float* Pz32 = nullptr;        // h1 x d_zp
   float* Pz32t = nullptr;       // d_z x h1
   float* omean = nullptr;
@@ -242,7 +245,9 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
   }
   bool vec = !AT && (K % 4 == 0) && (lda % 4 == 0) && (ldb % 4 == 0) && al16(A) && al16(B) &&
              (BT || N % 4 == 0);
-  int64_t tiles128 = cdiv(M, 128) * cdiv(N, 128);
+  // tile size from the rows that will actually run (compacted sweeps pass
+  // the device count in Mdev and the known count as the row hint)
+  int64_t tiles128 = cdiv(rows >= 0 ? rows : M, 128) * cdiv(N, 128);
   if (tiles128 >= 2 * h->num_sms)
     launch_simt<128, 128, 8, 8, AT, BT>(h, M, Mdev, N, K, A, lda, B, ldb, epi, vec);
   else
@@ -385,6 +390,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   }
   if ((rc = dalloc(h, &h->Wx, (size_t)h->h1 * h->ldx))) return bail(rc);
   if ((rc = dalloc(h, &h->Pz, (size_t)h->h1 * h->d_z))) return bail(rc);
+  if ((rc = dalloc(h, &h->PzT, (size_t)h->h1 * h->d_z))) return bail(rc);
   if ((rc = dalloc(h, &h->Pz32, (size_t)h->h1 * h->d_zp))) return bail(rc);
   if ((rc = dalloc(h, &h->Pz32t, (size_t)h->h1 * h->d_z))) return bail(rc);
   if ((rc = dalloc(h, &h->omean, h->r_u))) return bail(rc);
@@ -410,7 +416,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->n_act_dev, 1))) return bail(rc);
   h->qgrid = (int)std::min<int64_t>(cdiv(cap, 8), 2 * h->num_sms);
   if ((rc = dalloc(h, &h->qpart, (size_t)h->qgrid * STATS_LEN))) return bail(rc);
-  h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 64);
+  h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 16);
   if ((rc = dalloc(h, &h->cpart, (size_t)h->crb * h->maxw))) return bail(rc);
   if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
@@ -504,6 +510,12 @@ int sdn_set_model(sdn_handle* h, const float* const* W, const float* const* b, c
     CU(cudaMemcpy(h->W[l], W[l], (size_t)h->w[l + 1] * h->w[l] * 4, cudaMemcpyHostToDevice));
   for (int l = 0; l < h->L; ++l) CU(cudaMemcpy(h->b[l], b[l], (size_t)h->w[l + 1] * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->Pz, pz.data(), pz.size() * 8, cudaMemcpyHostToDevice));
+  {
+    std::vector<double> pzt((size_t)d_z * h1);
+    for (int c = 0; c < h1; ++c)
+      for (int k = 0; k < d_z; ++k) pzt[(size_t)k * h1 + c] = pz[(size_t)c * d_z + k];
+    CU(cudaMemcpy(h->PzT, pzt.data(), pzt.size() * 8, cudaMemcpyHostToDevice));
+  }
   CU(cudaMemcpy(h->Pz32, pz32.data(), pz32.size() * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->Pz32t, pz32t.data(), pz32t.size() * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->Wx, wx.data(), wx.size() * 4, cudaMemcpyHostToDevice));
@@ -585,7 +597,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   h->shift = q0;
   TRY(upload_z(h, z));
   { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
-  k_zbias<<<(unsigned)cdiv(h->h1, 128), 128, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb); }
+  k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb); }
   h->launches++;
   CHECK_LAUNCH(h);
   if (h->n > 0) {
@@ -601,7 +613,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
                                    h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
                                    h->Q, h->qpart);
-  k_sum_rows<<<1, STATS_LEN, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
+  k_sum_rows<<<(unsigned)cdiv(STATS_LEN, 8), 256, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
   h->launches += 2;
   CHECK_LAUNCH(h);
   h->fwd_done = true;
@@ -634,12 +646,28 @@ static int compact_rows(sdn_handle* h, int kind, double t, double eps) {
   return SDN_OK;
 }
 
+// exact top-k selection mask (value desc, global index asc); SMEM-resident
+// keys when they fit, else the global-memory radix select
+static int launch_topk(sdn_handle* h, int64_t n, int64_t k, const double* vals, const double* gidx, uint8_t* mask) {
+  if (n <= TOPK_SMEM_MAX) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_topk_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, TOPK_SMEM_MAX * 8);
+      attr = true;
+    }
+    k_topk_select_smem<<<1, 1024, (size_t)std::max<int64_t>(n, 1) * 8, h->stream>>>((int)n, k, vals, gidx, mask);
+  } else {
+    k_topk_select<<<1, 1024, 0, h->stream>>>(n, k, vals, gidx, mask);
+  }
+  h->launches++;
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
 // local exact top-k (single rank): selection mask over the shard's Q
 static int select_local(sdn_handle* h, int64_t k) {
   { ProfScope ps(h, PC_SELECT, 0.0, 8.0 * 8.0 * h->n);
-  k_topk_select<<<1, 1024, 0, h->stream>>>(h->n, k, h->Q, nullptr, h->sel); }
-  h->launches++;
-  CHECK_LAUNCH(h);
+  TRY(launch_topk(h, h->n, k, h->Q, nullptr, h->sel)); }
   TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
   h->selected = true;
   return SDN_OK;
@@ -661,7 +689,7 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
   if (h->compacted) { rowidx = h->rowidx; nact = h->n_act_dev; }
   const int64_t rows_hint = exact ? h->kk : (h->compacted ? -1 : h->n);
   if (!r.need_grad) {
-    k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(0, h->h1, h->d_z, nullptr, h->Pz, h->rowidx,
+    k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(0, h->h1, h->d_z, nullptr, h->PzT, h->rowidx,
                                                                     h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
     h->launches++;
     CHECK_LAUNCH(h);
@@ -686,7 +714,7 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
   }
   ProfScope psf(h, PC_FINAL, 0.0, 8.0 * h->crb * h->h1);
   k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(
-      nmax > 0 ? h->crb : 0, h->h1, h->d_z, nmax > 0 ? h->cpart : nullptr, h->Pz, h->rowidx, h->n_act_dev, h->Q,
+      nmax > 0 ? h->crb : 0, h->h1, h->d_z, nmax > 0 ? h->cpart : nullptr, h->PzT, h->rowidx, h->n_act_dev, h->Q,
       exact ? 1 : 0, partial_dev);
   h->launches++;
   CHECK_LAUNCH(h);
@@ -840,7 +868,7 @@ int sdn_eval_candidates(sdn_handle* h, int64_t k, double* cand_dev) {
   CU(cudaSetDevice(h->device));
   const int64_t kl = std::min<int64_t>(k, h->n);
   if (kl > 0) {
-    k_topk_select<<<1, 1024, 0, h->stream>>>(h->n, kl, h->Q, nullptr, h->sel);
+    TRY(launch_topk(h, h->n, kl, h->Q, nullptr, h->sel));
     h->launches++;
     TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
   } else {
@@ -860,7 +888,7 @@ int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, 
   TRY(ensure_cand(h, nc));
   k_unpack_candidates<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(n_ranks, k, all_cand_dev, h->cand_vals,
                                                                       h->cand_gidx);
-  k_topk_select<<<1, 1024, 0, h->stream>>>(nc, k, h->cand_vals, h->cand_gidx, h->cand_mask);
+  TRY(launch_topk(h, nc, k, h->cand_vals, h->cand_gidx, h->cand_mask));
   CU(cudaMemsetAsync(h->sel, 0, std::max<int64_t>(h->n, 1), h->stream));
   k_scatter_selection<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(nc, h->cand_mask, h->cand_gidx, h->goff,
                                                                       h->n, h->sel);
@@ -1239,7 +1267,7 @@ int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k, i
   CU(cudaMalloc(&ri, sizeof(int) * k));
   CU(cudaMemcpyAsync(v, values, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      h->stream));
-  k_topk_select<<<1, 1024, 0, h->stream>>>(n, k, v, nullptr, mask);
+  if (int rc = launch_topk(h, n, k, v, nullptr, mask)) { cudaFree(v); cudaFree(mask); return rc; }
   k_flag_count<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, cnt);
   k_scan_counts<<<1, 32, 0, h->stream>>>(nb, cnt, offs, na);
   k_compact<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, offs, ri);
@@ -1268,18 +1296,43 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  EpiFwdHidden e{h->b[1], h->res[1] ? h->H[0] : nullptr, h->H[1], h->D[1], (int64_t)N, h->act};
-  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{&h->tcw.act[1]}};
+  // modes 3..6 drop parts of the fused epilogue: 3 no D, 4 no split, 5 no
+  // residual input, 6 only the fp32 H store
+  const bool keepD = mode < 3 || (mode != 3 && mode < 6), keepS = mode < 4 || (mode != 4 && mode < 6);
+  const bool keepP = mode < 5, keepH = mode != 7;
+  EpiFwdHidden e{h->b[1], (h->res[1] && keepP) ? h->H[0] : nullptr, keepH ? h->H[1] : nullptr, keepD ? h->D[1] : nullptr,
+                 (int64_t)N, h->act};
+  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{keepS ? &h->tcw.act[1] : nullptr}};
   h->tcw.act[0].rows = M;
   int rc = 0;
   for (int it = 0; it <= reps && rc == 0; ++it) {
     if (it == 1) cudaEventRecord(a, h->stream);
     if (mode == 0) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], EpiNull{});
-    else if (mode == 1) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], ch);
+    else if (mode != 2) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], ch);
     else { launch_simt<128, 128, 8, 8, false, true>(h, M, nullptr, N, K, h->H[0], K, h->W[1], K, ch, true); }
   }
   cudaEventRecord(b, h->stream);
   cudaError_t err = cudaEventSynchronize(b);
+  if (getenv("SDN_TRACE") && mode != 2 && rc == 0) {
+    // one more launch with per-phase clock64 stamps of CTA 0 (stderr)
+    unsigned long long* tr = nullptr;
+    cudaMalloc(&tr, 64 * sizeof(unsigned long long));
+    cudaMemset(tr, 0, 64 * sizeof(unsigned long long));
+    g_tc_trace = tr;
+    if (mode == 0) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], EpiNull{});
+    else rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], ch);
+    g_tc_trace = nullptr;
+    cudaStreamSynchronize(h->stream);
+    unsigned long long ht[64];
+    cudaMemcpy(ht, tr, sizeof(ht), cudaMemcpyDeviceToHost);
+    cudaFree(tr);
+    fprintf(stderr, "trace mode %d M %lld: tma[kb0..3] %lld %lld %lld %lld | mma_done %lld | epi_start %lld |", mode,
+            (long long)M, (long long)(ht[1] - ht[0]), (long long)(ht[2] - ht[0]), (long long)(ht[3] - ht[0]),
+            (long long)(ht[4] - ht[0]), (long long)(ht[5] - ht[0]), (long long)(ht[8] - ht[0]));
+    for (int i = 0; i < 8; ++i)
+      if (ht[9 + 2 * i]) fprintf(stderr, " c%d[%lld,%lld]", i, (long long)(ht[9 + 2 * i] - ht[0]), (long long)(ht[10 + 2 * i] - ht[0]));
+    fprintf(stderr, "\n");
+  }
   float t = 0.f;
   cudaEventElapsedTime(&t, a, b);
   cudaEventDestroy(a);

@@ -195,6 +195,15 @@ SDN_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: 
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms of
 // 1024 B (SBO), version 1 (sm_100), LBO unused for swizzled K-major (= 16 B)
+// K-major, 64B swizzle (32 bf16 per row), 8-row atoms of 512 B (SBO)
+SDN_DEV uint64_t sdesc_k64(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
 SDN_DEV uint64_t sdesc_k128(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)1 << 16;
@@ -212,19 +221,21 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 }  // namespace tcx
 
 constexpr int TC_BM = 128;
-constexpr int TC_BK = 64;   // 64 bf16 = one 128-byte swizzle row
+// optional device trace buffer (sdn_debug_gemm): per-phase clock64 stamps of CTA 0
+static unsigned long long* g_tc_trace = nullptr;
+constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 
 // per epilogue warp: two fp32 32x16 tiles + two bf16 32x16 tiles (6 KB)
-constexpr uint32_t TC_EPI_WARP_BYTES = 4096;   // fp32 32x16 tile + two bf16 32x16 tiles (the
-                                               // bf16 pair doubles as a second fp32 tile)
-constexpr int TC_EPI_WARPS = 8;                // two per TMEM lane quarter
+constexpr uint32_t TC_EPI_WARP_BYTES = 6144;
+constexpr int TC_EPI_WARPS = 12;               // three per TMEM lane quarter
+constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
 
 template <int BN>
 struct TcCfg {
   static constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;
   static constexpr uint32_t B_BYTES = BN * TC_BK * 2;
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 2 : 3;
+  static constexpr int STAGES = (BN == 256) ? 3 : 4;
   static constexpr uint32_t EPI_BYTES = TC_EPI_WARPS * TC_EPI_WARP_BYTES;
   static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -265,6 +276,7 @@ SDN_DEV void tile_in(float* buf, const float* src, int64_t ld, const TileRows& t
 // tile_in), parked in smem once the current chunk has released it
 struct EpiPre {
   float4 a[4], b[4];
+  float4 c[4];           // per-column constants of the chunk (bias), lane-uniform
 };
 SDN_DEV void tile_fetch(float4 (&p)[4], const float* src, int64_t ld, const TileRows& tr, bool gathered, int c0,
                         int N, int lane) {
@@ -381,17 +393,26 @@ struct TileEpi<EpiNull> {
 // output layer: phi = shift + scale * (acc + bias)
 template <>
 struct TileEpi<EpiAffine> {
-  static SDN_DEV void load(const EpiAffine&, const TileRows&, int, int, int, EpiPre&) {}
+  static SDN_DEV void load(const EpiAffine& e, const TileRows&, int c0, int N, int, EpiPre& p) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f), o = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = min(c0 + 4 * j, N - 4);
+      p.c[j] = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + c)) : z;
+      p.b[j] = e.scale ? __ldg(reinterpret_cast<const float4*>(e.scale + c)) : o;
+      p.a[j] = e.shift ? __ldg(reinterpret_cast<const float4*>(e.shift + c)) : z;
+    }
+  }
   static SDN_DEV void chunk(const EpiAffine& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const EpiPre&) {
+                            const uint32_t (&v)[16], const EpiPre& pre) {
     float x[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int c = min(c0 + j, N - 1);
-      float y = __uint_as_float(v[j]) + (e.bias ? __ldg(e.bias + c) : 0.0f);
-      if (e.scale) y *= __ldg(e.scale + c);
-      if (e.shift) y += __ldg(e.shift + c);
-      x[j] = y;
+    for (int j = 0; j < 16; j += 4) {
+      const float4 b = pre.c[j / 4], sc = pre.b[j / 4], sh = pre.a[j / 4];
+      x[j] = sh.x + sc.x * (__uint_as_float(v[j]) + b.x);
+      x[j + 1] = sh.y + sc.y * (__uint_as_float(v[j + 1]) + b.y);
+      x[j + 2] = sh.z + sc.z * (__uint_as_float(v[j + 2]) + b.z);
+      x[j + 3] = sh.w + sc.w * (__uint_as_float(v[j + 3]) + b.w);
     }
     row_put(s.f0, lane, x);
     __syncwarp();
@@ -405,6 +426,8 @@ template <>
 struct TileEpi<TcChain<EpiFwdHidden>> {
   static SDN_DEV void load(const TcChain<EpiFwdHidden>& ch, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
     if (ch.base.prev) tile_fetch(p.a, ch.base.prev, ch.base.ld, tr, false, c0, N, lane);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p.c[j] = __ldg(reinterpret_cast<const float4*>(ch.base.bias + min(c0 + 4 * j, N - 4)));
   }
   static SDN_DEV void chunk(const TcChain<EpiFwdHidden>& ch, const EpiSmem& s, const TileRows& tr, int c0, int N,
                             int lane, const uint32_t (&v)[16], const EpiPre& pre) {
@@ -418,23 +441,21 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
     float bias[16];
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
-      const float4 b4 = __ldg(reinterpret_cast<const float4*>(e.bias + min(c0 + j, N - 4)));
+      const float4 b4 = pre.c[j / 4];
       bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
     }
     if (e.act == ACT_ELU) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
+        // branch-free (selects only) so the 16 elements interleave
         const float x = __uint_as_float(v[j]) + bias[j];
-        float y, dy;
-        if (x > 0.0f) { y = x; dy = 1.0f; }
-        else {
-          dy = __expf(x);
-          // e^x - 1 without cancellation near 0
-          y = (x > -0.0625f) ? x * (1.0f + x * (0.5f + x * (0.16666667f + x * (0.041666668f + x * 0.008333334f))))
-                             : dy - 1.0f;
-        }
+        const float xn = fminf(x, 0.0f);
+        const float ex = __expf(xn);
+        // e^x - 1 without cancellation near 0 (Taylor to x^5 on (-1/16, 0])
+        const float pm = xn * (1.0f + xn * (0.5f + xn * (0.16666667f + xn * (0.041666668f + xn * 0.008333334f))));
+        const float y = x > 0.0f ? x : (xn > -0.0625f ? pm : ex - 1.0f);
         a[j] = e.prev ? a[j] + y : y;
-        d[j] = dy;
+        d[j] = x > 0.0f ? 1.0f : ex;
       }
     } else {
 #pragma unroll
@@ -449,7 +470,7 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
     row_put(s.f0, lane, a);
     if (ch.split.hi) row_put_split(s.h, s.l, lane, a);
     __syncwarp();
-    tile_out(s.f0, e.H, e.ld, tr, c0, N, lane);
+    if (e.H) tile_out(s.f0, e.H, e.ld, tr, c0, N, lane);
     if (ch.split.hi) {
       tile_out_h(s.h, ch.split.hi, ch.split.ld, tr, c0, N, lane);
       tile_out_h(s.l, ch.split.lo, ch.split.ld, tr, c0, N, lane);
@@ -510,10 +531,11 @@ struct TileEpi<TcChain<EpiBwd>> {
 };
 
 template <int BN, class Epi>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
-               const int* __restrict__ Mdev, int N, int K, Epi epi) {
+               const int* __restrict__ Mdev, int N, int K, Epi epi,
+               unsigned long long* __restrict__ trace = nullptr) {
   using C = TcCfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -552,10 +574,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      if (trace && blockIdx.x == 0) trace[0] = clock64();
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int mb = tile / n_tiles, nb = tile % n_tiles;
         for (int kb = 0; kb < kblocks; ++kb) {
           tcx::mbar_wait(&empty[stage], phase ^ 1);
+          if (trace && blockIdx.x == 0 && tile == (int)blockIdx.x && kb < 4) trace[1 + kb] = clock64();
           uint8_t* st = smem + stage * C::STAGE_BYTES;
           tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           tcx::tma_load_2d(st, &tAh, &full[stage], kb * TC_BK, mb * TC_BM);
@@ -581,10 +605,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
           const uint32_t base = tcx::smem_u32(smem + stage * C::STAGE_BYTES);
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 16; ++kk) {
-            const uint64_t ah = tcx::sdesc_k128(base + kk * 32);
-            const uint64_t al = tcx::sdesc_k128(base + C::A_BYTES + kk * 32);
-            const uint64_t bh = tcx::sdesc_k128(base + 2 * C::A_BYTES + kk * 32);
-            const uint64_t bl = tcx::sdesc_k128(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
+            const uint64_t ah = tcx::sdesc_k64(base + kk * 32);
+            const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
+            const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
+            const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
             tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
             tcx::mma_bf16(d, ah, bl, idesc, 1);
             tcx::mma_bf16(d, al, bh, idesc, 1);
@@ -592,16 +616,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
           tcx::commit(&empty[stage]);            // frees the smem slot when these MMAs finish
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (trace && blockIdx.x == 0 && tile == (int)blockIdx.x) trace[5] = clock64();
         tcx::commit(&tfull[acc]);                // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;                      // TMEM lane quarter of this warp
-    const int half = (warp - 4) >> 2;            // which 16-column chunks (even / odd)
+    const int third = (warp - 4) >> 2;           // which 16-column chunks (mod 3)
     uint8_t* ep = smem + STAGES * C::STAGE_BYTES + (warp - 4) * TC_EPI_WARP_BYTES;
     const EpiSmem es{reinterpret_cast<float*>(ep), reinterpret_cast<float*>(ep + 2048),
-                     reinterpret_cast<uint32_t*>(ep + 2048), reinterpret_cast<uint32_t*>(ep + 3072)};
+                     reinterpret_cast<uint32_t*>(ep + 4096), reinterpret_cast<uint32_t*>(ep + 5120)};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -610,17 +635,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       tcx::fence_after();
       const TileRows tr{(int64_t)mb * TC_BM + q * 32, M, nullptr};
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
-#pragma unroll 1
+      const bool tr0 = trace && blockIdx.x == 0 && warp == 4 && lane == 0 && tile == (int)blockIdx.x;
+      if (tr0) trace[8] = clock64();
       EpiPre cur;
-      if (nb * BN + 16 * half < N) TileEpi<Epi>::load(epi, tr, nb * BN + 16 * half, N, lane, cur);
-      for (int c0 = 16 * half; c0 < BN; c0 += 32) {
+      if (nb * BN + 16 * third < N) TileEpi<Epi>::load(epi, tr, nb * BN + 16 * third, N, lane, cur);
+      int ci = 0;
+#pragma unroll 1
+      for (int c0 = 16 * third; c0 < BN; c0 += 48, ++ci) {
         if (nb * BN + c0 >= N) break;            // warp-uniform
         EpiPre nxt;                              // prefetch the next chunk's inputs
-        if (c0 + 32 < BN && nb * BN + c0 + 32 < N) TileEpi<Epi>::load(epi, tr, nb * BN + c0 + 32, N, lane, nxt);
+        if (c0 + 48 < BN && nb * BN + c0 + 48 < N) TileEpi<Epi>::load(epi, tr, nb * BN + c0 + 48, N, lane, nxt);
         uint32_t v[16];
         tcx::tmem_ld16(tbase + c0, v);
         tcx::tmem_ld_wait();
+        if (tr0 && ci < 10) trace[9 + 2 * ci] = clock64();
         TileEpi<Epi>::chunk(epi, es, tr, nb * BN + c0, N, lane, v, cur);
+        if (tr0 && ci < 10) trace[10 + 2 * ci] = clock64();
         cur = nxt;
       }
       tcx::fence_before();
@@ -665,7 +695,7 @@ static int tc_map(TcWeights& t, const __nv_bfloat16* base, int64_t rows, int col
   cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -2;
   t.maps[key] = m;
@@ -691,7 +721,7 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   }
   const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
-  tc_gemm_kernel<BN, Epi><<<grid, 384, TcCfg<BN>::SMEM, st>>>(ah, al, bh, bl, M, Mdev, N, K, epi);
+  tc_gemm_kernel<BN, Epi><<<grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ah, al, bh, bl, M, Mdev, N, K, epi, g_tc_trace);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

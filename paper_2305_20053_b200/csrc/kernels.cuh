@@ -16,13 +16,16 @@ constexpr int STATS_LEN = 8;   // [n, sum q~, sum q~^2, sum splus, sum d1, n_act
 
 // zb = b1 + Pz z  (first-layer control contribution, W1_z V_z^T z, shared by
 // every sample of the evaluation -- SURVEY 2.2 K2)
-__global__ void k_zbias(int h1, int d_z, const double* __restrict__ Pz, const double* __restrict__ z,
-                        const float* __restrict__ b1, float* __restrict__ zb) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+// one warp per output c, lanes over k (row c of Pz is contiguous)
+__global__ void __launch_bounds__(256)
+k_zbias(int h1, int d_z, const double* __restrict__ Pz, const double* __restrict__ z,
+        const float* __restrict__ b1, float* __restrict__ zb) {
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= h1) return;
-  double s = b1[c];
-  for (int k = 0; k < d_z; ++k) s += Pz[(int64_t)c * d_z + k] * z[k];
-  zb[c] = (float)s;
+  double s = 0.0;
+  for (int k = lane; k < d_z; k += 32) s += Pz[(int64_t)c * d_z + k] * z[k];
+  s = warp_sum(s);
+  if (lane == 0) zb[c] = (float)(s + (double)b1[c]);
 }
 
 // X = [m_r, z_row, 0-pad]  (forward_batch / jacobian rows with per-row z)
@@ -78,13 +81,16 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
   if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;
 }
 
-// fixed-order sum of nb rows of width w (fp64) -> out (w)
-__global__ void k_sum_rows(int nb, int w, const double* __restrict__ part, double* __restrict__ out) {
-  int f = blockIdx.x * blockDim.x + threadIdx.x;
+// fixed-order sum of nb rows of width w (fp64) -> out (w): one warp per
+// column, lanes stride the rows, then a fixed butterfly (deterministic)
+__global__ void __launch_bounds__(256)
+k_sum_rows(int nb, int w, const double* __restrict__ part, double* __restrict__ out) {
+  const int f = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (f >= w) return;
   double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * w + f];
-  out[f] = s;
+  for (int b = lane; b < nb; b += 32) s += part[(int64_t)b * w + f];
+  s = warp_sum(s);
+  if (lane == 0) out[f] = s;
 }
 
 // sample weight w_i of the risk functional:
@@ -205,15 +211,17 @@ k_finalize_grad(int nrb, int h1, int d_z, const double* __restrict__ part, const
   extern __shared__ double A[];   // h1
   for (int c = threadIdx.x; c < h1; c += blockDim.x) {
     double s = 0.0;
-    if (part)
+    if (part) {
+#pragma unroll 8
       for (int b = 0; b < nrb; ++b) s += part[(int64_t)b * h1 + c];
+    }
     A[c] = s;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int k = warp; k < d_z; k += nw) {          // one warp per output, lanes over c
-    double s = 0.0;
-    for (int c = lane; c < h1; c += 32) s += Pz[(int64_t)c * d_z + k] * A[c];
+    double s = 0.0;                               // PzT is d_z x h1: contiguous in c
+    for (int c = lane; c < h1; c += 32) s += Pz[(int64_t)k * h1 + c] * A[c];
     s = warp_sum(s);
     if (lane == 0) out[k] = s;
   }
@@ -290,6 +298,89 @@ k_topk_select(int64_t n, int64_t k, const double* __restrict__ vals, const doubl
     }
     __syncthreads();
     long long rank = s_run + wsum[warp] + __popc(b & ((1u << lane) - 1u));
+    if (i < n) mask[i] = (valid && (key > T || (eq && rank < need))) ? 1 : 0;
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_run += wsum[warp] + __popc(b);
+    __syncthreads();
+  }
+}
+
+// Same selection with the keys resident in shared memory (n <= TOPK_SMEM_MAX):
+// one global read, 8 histogram passes over SMEM, a warp-parallel digit search.
+constexpr int TOPK_SMEM_MAX = 24576;   // 192 KB of uint64 keys
+
+__global__ void __launch_bounds__(1024)
+k_topk_select_smem(int n, int64_t k, const double* __restrict__ vals, const double* __restrict__ gidx,
+                   uint8_t* __restrict__ mask) {
+  extern __shared__ uint64_t keys[];
+  __shared__ unsigned hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ long long s_krem;
+  __shared__ int wsum[32];
+  __shared__ long long s_run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < n; i += blockDim.x)
+    keys[i] = (gidx && gidx[i] < 0.0) ? 0ull : dkey(vals[i]);   // padding: key 0, below every value
+  if (tid == 0) { s_prefix = 0; s_krem = k; }
+  uint64_t himask = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const uint64_t key = keys[i];
+      if ((key & himask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // lane l owns digits 255-8l .. 248-8l (descending)
+      unsigned c[8], tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { c[i] = hist[255 - 8 * lane - i]; tot += c[i]; }
+      unsigned incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const long long krem = s_krem;
+      const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= krem);
+      const int L = hit ? __ffs(hit) - 1 : 31;
+      if (lane == L) {
+        long long cum = (long long)(incl - tot);
+        int d = 255 - 8 * lane;
+        for (int i = 0; i < 8; ++i) {
+          d = 255 - 8 * lane - i;
+          if (cum + (long long)c[i] >= krem || i == 7) break;
+          cum += c[i];
+        }
+        s_krem = krem - cum;
+        s_prefix = prefix | ((uint64_t)d << shift);
+      }
+    }
+    himask |= (0xFFull << shift);
+    __syncthreads();
+  }
+  const uint64_t T = s_prefix;
+  const long long need = s_krem;
+  if (tid == 0) s_run = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + tid;
+    const uint64_t key = i < n ? keys[i] : 0ull;
+    const bool valid = i < n && key != 0ull;
+    const bool eq = valid && key == T;
+    const unsigned b = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) wsum[warp] = __popc(b);
+    __syncthreads();
+    if (tid == 0) {
+      int s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { int cc = wsum[w]; wsum[w] = s; s += cc; }
+    }
+    __syncthreads();
+    const long long rank = s_run + wsum[warp] + __popc(b & ((1u << lane) - 1u));
     if (i < n) mask[i] = (valid && (key > T || (eq && rank < need))) ? 1 : 0;
     __syncthreads();
     if (tid == blockDim.x - 1) s_run += wsum[warp] + __popc(b);

@@ -1,17 +1,25 @@
-"""Time the layer-1 forward GEMM: tcgen05 (null / fused epilogue) vs SIMT."""
-import sys, os, ctypes as C
+"""Time the layer-1 forward GEMM: tcgen05 with null / fused / partial
+epilogues vs SIMT, at full M and at one tile per SM (latency view)."""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2305_20053_b200 import Engine, workloads as wl, _lib
-for name in sys.argv[1:] or ["c2"]:
+
+MODES = {0: "tc-null-epi", 1: "tc-fused-epi", 2: "simt-fused-epi", 3: "tc-no-D", 4: "tc-no-split", 7: "tc-no-stores",
+         5: "tc-no-residual", 6: "tc-H-only"}
+names = [a for a in sys.argv[1:] if not a.startswith("-")] or ["c2"]
+modes = [0, 1, 3, 4, 5, 6, 7] + ([2] if "--simt" in sys.argv else [])
+for name in names:
     cfg = wl.WORKLOADS[name]
     p = wl.make_problem(cfg.with_samples(256), seed=0, count=256)
-    n = cfg.n_samples
-    eng = Engine(p, max_samples=n, gemm="tc")
+    eng = Engine(p, max_samples=cfg.n_samples, gemm="tc")
     K, N = cfg.widths[1], cfg.widths[2]
-    for mode, label in ((0, "tc-null-epi"), (1, "tc-fused-epi"), (2, "simt-fused-epi")):
-        ms = np.zeros(1)
-        _lib.check(_lib.lib.sdn_debug_gemm(eng.h, n, mode, 20, _lib.dptr(ms)), "debug")
-        fl = 2.0 * n * K * N
-        print(f"{name} M={n} N={N} K={K} {label:16s} {ms[0]*1e3:8.1f} us  {fl/ms[0]/1e9:7.1f} TFLOP/s (algorithmic)  "
-              f"{3*fl/ms[0]/1e9:7.1f} TFLOP/s (bf16 issued)")
+    for M in (cfg.n_samples, 128 * 148 // (N // 256 if N >= 256 else 1)):
+        for mode in modes:
+            ms = np.zeros(1)
+            _lib.check(_lib.lib.sdn_debug_gemm(eng.h, M, mode, 20, _lib.dptr(ms)), "debug")
+            fl = 2.0 * M * K * N
+            print(f"{name} M={M:6d} N={N} K={K} {MODES[mode]:16s} {ms[0]*1e3:8.1f} us  "
+                  f"{3*fl/ms[0]/1e9:7.1f} TFLOP/s bf16 issued")
