@@ -184,6 +184,8 @@ int sdn_eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk,
 int sdn_eval_candidates(sdn_handle* h, int64_t k, double* cand_dev);
 int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, int64_t k);
 int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev);
+/* Switch the risk for the next sweep sharing the last forward (multi-risk). */
+int sdn_eval_set_risk(sdn_handle* h, const sdn_risk* risk);
 int sdn_eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev,
                     sdn_result* res, double* grad_z);
 

@@ -900,6 +900,22 @@ int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, 
   return SDN_OK;
 }
 
+// next reverse sweep after one forward (multi-risk): same QoI frame; a
+// smoothed CVaR must be the forward's own risk (its t/eps fed the moments)
+int sdn_eval_set_risk(sdn_handle* h, const sdn_risk* risk) {
+  if (!h || !risk) return fail(SDN_ERR_ARG, "null argument");
+  TRY(check_risk(risk));
+  if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
+  if (risk->qoi != h->risk.qoi) return fail(SDN_ERR_ARG, "risk must keep the forward's QoI frame");
+  if (risk->kind == SDN_RISK_CVAR_SMOOTH &&
+      (h->risk.kind != SDN_RISK_CVAR_SMOOTH || risk->t != h->risk.t || risk->eps != h->risk.eps))
+    return fail(SDN_ERR_ARG, "smoothed CVaR must be the forward's risk");
+  h->risk = *risk;
+  h->compacted = false;
+  h->selected = false;
+  return SDN_OK;
+}
+
 int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev) {
   if (!h || !stats_dev || !partial_dev) return fail(SDN_ERR_ARG, "null argument");
   CU(cudaSetDevice(h->device));

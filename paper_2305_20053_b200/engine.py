@@ -260,6 +260,15 @@ class Engine:
         check(lib.sdn_eval_select(self.h, C.c_void_p(all_cand_dev.data_ptr()), int(n_ranks), int(k)),
               "sdn_eval_select")
 
+    def phase_set_risk(self, risk: _lib.Risk):
+        self._phase_risk = risk
+        check(lib.sdn_eval_set_risk(self.h, C.byref(risk)), "sdn_eval_set_risk")
+
+    def new_buffer(self, n: int):
+        """float64 exchange buffer on this engine's device (torch tensor)."""
+        import torch
+        return torch.zeros(int(n), dtype=torch.float64, device=f"cuda:{self.device}")
+
     def phase_backward(self, stats_dev, partial_dev):
         check(lib.sdn_eval_backward(self.h, C.c_void_p(stats_dev.data_ptr()), C.c_void_p(partial_dev.data_ptr())),
               "sdn_eval_backward")

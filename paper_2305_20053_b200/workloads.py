@@ -21,6 +21,7 @@ input_scale = 1/sqrt(lam[:r_m]) (pipeline.py:280).
 
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass, field, replace
 from typing import Optional
 
@@ -239,10 +240,25 @@ def sample_xi(cfg: Workload, seed: int, start: int, count: int) -> np.ndarray:
 M_MEAN = -1.0   # MaternSpec default mean (randfield.py:27)
 
 
+@functools.lru_cache(maxsize=8)
 def kl_modes(cfg: Workload, seed: int):
+    """(Psi, lambda, mass diag) -- cached: shards of one run share them."""
     mdiag = field_mass(cfg)
     psi = m_orthonormal(substream(seed, STREAM_KL_MODES), cfg.d_m, cfg.n_kl, mdiag)
     return psi, kl_eigvals(cfg.n_kl), mdiag
+
+
+@functools.lru_cache(maxsize=8)
+def _state_bases(cfg: Workload, seed: int):
+    mdiag_u = state_mass(cfg)
+    U = m_orthonormal(substream(seed, STREAM_DECODER), cfg.d_u, cfg.r_u, mdiag_u)
+    ubias = 0.1 * substream(seed, STREAM_DECODER_BIAS).standard_normal(cfg.d_u)
+    if cfg.state_mass == "grid":
+        xy = grid_coords(cfg.field_shape[1], cfg.field_shape[2])
+        u_t = np.sin(2 * np.pi * xy[:, 0]) * np.sin(2 * np.pi * xy[:, 1])   # config.py:157-158
+    else:
+        u_t = 0.1 * substream(seed, STREAM_TARGET).standard_normal(cfg.d_u)
+    return f32(U), f32(ubias), f32(u_t), f32(mdiag_u)
 
 
 def fields(cfg: Workload, seed: int, start: int, count: int) -> np.ndarray:
@@ -270,17 +286,9 @@ def make_problem(cfg: Workload, seed: int = 0, start: int = 0, count: Optional[i
     Vz = np.linalg.qr(substream(seed, STREAM_VZ).standard_normal((cfg.d_z, cfg.r_z)))[0]
     z = substream(seed, STREAM_CONTROL).uniform(-4.0, 4.0, cfg.d_z)   # config.py:43-45
 
-    mdiag_u = state_mass(cfg)
-    U = m_orthonormal(substream(seed, STREAM_DECODER), cfg.d_u, cfg.r_u, mdiag_u)
-    ubias = 0.1 * substream(seed, STREAM_DECODER_BIAS).standard_normal(cfg.d_u)
-    if cfg.state_mass == "grid":
-        xy = grid_coords(cfg.field_shape[1], cfg.field_shape[2])
-        u_t = np.sin(2 * np.pi * xy[:, 0]) * np.sin(2 * np.pi * xy[:, 1])   # config.py:157-158
-    else:
-        u_t = 0.1 * substream(seed, STREAM_TARGET).standard_normal(cfg.d_u)
-    # round the bases to f32 first so the reduced form is exact for the
+    # bases rounded to f32 first so the reduced form is exact for the
     # arrays the device actually holds
-    U32, b32, t32, M32 = f32(U), f32(ubias), f32(u_t), f32(mdiag_u)
+    U32, b32, t32, M32 = _state_bases(cfg, seed)
     shift = b32.astype(np.float64) - t32.astype(np.float64)
     Md = M32.astype(np.float64)
     c = U32.astype(np.float64).T @ (Md * shift)
