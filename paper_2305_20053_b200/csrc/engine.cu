@@ -117,6 +117,8 @@ struct sdn_handle {
   double* qpart = nullptr;      // qgrid x STATS_LEN
   int qgrid = 0;
   double* cpart = nullptr;      // crb x maxw
+  double* tsum = nullptr;       // (cap/128 * 4) x maxw: fused column-sum partials (TC chains)
+  double* csum = nullptr;       // maxw: summed columns
   int crb = 0;
   double* stats_loc = nullptr;  // STATS_LEN
   double* partial_loc = nullptr;
@@ -219,25 +221,27 @@ static void launch_simt(sdn_handle* h, int64_t M, const int* Mdev, int N, int K,
 // C = opA(A) opB(B) with a fused epilogue; M rows (Mdev: device row count
 // upper-bounded by M, for compacted sweeps).  Routes to tcgen05 when the
 // handle allows it and the shape qualifies.
+// route: -1 per-GEMM policy, 0 SIMT, 1 tcgen05 (a chain decided up front)
 template <bool AT, bool BT, class Epi>
 static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const float* A, int64_t lda,
                 const float* B, int64_t ldb, Epi epi, const TcOperand* tcB = nullptr,
-                const TcOperand* tcA = nullptr) {
+                const TcOperand* tcA = nullptr, int route = -1) {
   if (M <= 0 || N <= 0) return SDN_OK;
   const int64_t rows = h->prows ? h->prows : M;
   h->prows = 0;
   ProfScope ps(h, h->pcls, rows >= 0 ? 2.0 * rows * N * K : 0.0, 0.0, rows, 2.0 * N * K);
   h->pcls = PC_OTHER;
-  bool use_tc = h->gemm != SDN_GEMM_SIMT && !AT && tcB && tcA && h->tcw.enabled && tc_gemm_supported(M, N, K) &&
-                tcA->ld % 8 == 0 && tcB->ld % 8 == 0;
-  if (use_tc && h->gemm == SDN_GEMM_AUTO) {
+  bool use_tc = route != 0 && h->gemm != SDN_GEMM_SIMT && !AT && tcB && tcA && h->tcw.enabled &&
+                tc_gemm_supported(M, N, K) && tcA->ld % 8 == 0 && tcB->ld % 8 == 0;
+  if (route == 1 && !use_tc) return fail(SDN_ERR_STATE, "tensor-core chain without a tensor-core GEMM");
+  if (use_tc && route < 0 && h->gemm == SDN_GEMM_AUTO) {
     // small GEMMs (c1, CVaR tails) fill more SMs with 64x64 SIMT tiles
     const int64_t mrows = rows >= 0 ? rows : M;
     const int64_t tiles = cdiv(mrows, 128) * cdiv(N, N <= 128 ? 128 : 256);
     if (tiles < h->num_sms / 2) use_tc = false;
   }
   if (use_tc) {
-    int rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, Mdev, N, K, *tcA, *tcB, epi);
+    int rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, Mdev, N, K, *tcA, *tcB, epi, rows);
     h->launches++;
     if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");
     CHECK_LAUNCH(h);
@@ -259,12 +263,29 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
 // ---------------------------------------------------------------------------
 // forward / backward building blocks
 
+// Whether a whole layer chain over `rows` rows runs on the tensor cores.  A
+// chain is routed as one unit so that intermediates only the SIMT path reads
+// (fp32 H for residuals, fp32 U) are skipped when every GEMM is tcgen05.
+static bool chain_tc(sdn_handle* h, int64_t rows) {
+  if (!h->tcw.enabled || h->gemm == SDN_GEMM_SIMT || rows < 1) return false;
+  for (int l = 0; l < h->L; ++l) {
+    const int n_out = h->w[l + 1], n_in = (l == 0) ? h->r_m : h->w[l];
+    if (!tc_gemm_supported(rows, n_out, n_in) || n_in % 8 || n_out % 8) return false;
+    if (l >= 1 && !tc_gemm_supported(rows, n_in, n_out)) return false;
+  }
+  if (h->gemm == SDN_GEMM_TC) return true;
+  // auto: small chains (c1, CVaR tails) fill more SMs with 64x64 SIMT tiles
+  // (the tcgen05 kernel narrows its N tile for short chains)
+  return rows >= 512;
+}
+
 // layer chain on `nrows` rows.  Layer 0 input: X (ld0, K0) with weight W0 and
 // bias0 (either MR + zb, or [m_r | z] + b0).  store_D keeps act' for the sweep.
 static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0, int K0,
                        const float* W0, int64_t ldW0, const float* bias0, bool store_D,
                        float* phi_out, const TcOperand* tcX0) {
   const int L = h->L;
+  const bool tcc = chain_tc(h, nrows);
   int cur = 0;
   const float* in = X;
   int64_t ldin = ld0;
@@ -274,21 +295,25 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
     const int64_t ldW = (l == 0) ? ldW0 : n_in;
     const int K = (l == 0) ? K0 : n_in;
     const float* bl = (l == 0) ? bias0 : h->b[l];
-    const bool tc = h->tcw.enabled && (l > 0 || tcX0);
+    const bool tc = tcc && (l > 0 || tcX0);      // layer 0 of per-row-z inputs stays SIMT
     const TcOperand* tA = !tc ? nullptr : (l == 0) ? tcX0 : &h->tcw.act[cur];
     const TcOperand* tB = !tc ? nullptr : &h->tcw.fwd[l];
     h->pcls = PC_FWD_GEMM;
     h->prows = nrows;
     if (l == L - 1) {
       EpiAffine e{bl, h->ostd, h->omean, phi_out, (int64_t)n_out};
-      TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA)));
+      TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA, tc ? 1 : 0)));
     } else {
       float* out = h->H[(l == 0) ? 0 : 1 - cur];
-      EpiFwdHidden e{bl, (h->res[l] ? in : nullptr), out, store_D ? h->D[l] : nullptr,
-                     (int64_t)n_out, h->act};
-      TcEpiSplit split = h->tcw.enabled ? TcEpiSplit{&h->tcw.act[(l == 0) ? 0 : 1 - cur]} : TcEpiSplit{nullptr};
+      // in a tensor-core chain the residual is read from the bf16 split of the
+      // layer input (the A operand), and the fp32 H is never needed
+      const bool split_prev = tc && h->res[l];
+      EpiFwdHidden e{bl, (h->res[l] && !split_prev ? in : nullptr), tcc ? nullptr : out,
+                     store_D ? h->D[l] : nullptr, (int64_t)n_out, h->act};
+      TcEpiSplit split = tcc ? TcEpiSplit{&h->tcw.act[(l == 0) ? 0 : 1 - cur]} : TcEpiSplit{nullptr};
+      TcEpiSplit prev = split_prev ? TcEpiSplit{&h->tcw.act[cur]} : TcEpiSplit{nullptr};
       TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW,
-                             TcChain<EpiFwdHidden>{e, split}, tB, tA)));
+                             TcChain<EpiFwdHidden>{e, split, prev}, tB, tA, tc ? 1 : 0)));
       cur = (l == 0) ? 0 : 1 - cur;
       in = out;
       ldin = n_out;
@@ -298,33 +323,39 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
 }
 
 // reverse sweep over `nmax` (device count n_act_dev) compacted rows from the
-// seeds E; leaves dL/dS_0 (rows x w[1]) in *u0_out.
+// seeds E.  SIMT chains (or want_u0) leave dL/dS_0 (rows x w[1]) in *u0_out;
+// tensor-core chains fuse the sample sum into the last GEMM and leave fp64
+// column-sum partials in h->tsum (*u0_out = nullptr, *nrb = partial rows,
+// device-bounded by n_act_dev).
 static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const int* rowidx,
-                        float** u0_out, int64_t rows_hint) {
+                        float** u0_out, int64_t rows_hint, bool want_u0 = false, int64_t* nrb = nullptr) {
   const int L = h->L;
   if (L == 1) { *u0_out = h->E; return SDN_OK; }
+  const bool tcc = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
+  const int route = tcc ? 1 : 0;
   int cur = 0;
-  {
-    const int K = h->w[L], N = h->w[L - 1];
-    EpiBwd e{nullptr, h->res[L - 2] ? h->G : nullptr, h->D[L - 2], (int64_t)N, rowidx, h->Ub[cur],
-             (int64_t)N};
-    TcEpiSplit split = h->tcw.enabled ? TcEpiSplit{&h->tcw.act[cur]} : TcEpiSplit{nullptr};
-    h->pcls = PC_BWD_GEMM;
-    h->prows = rows_hint;
-    TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, h->E, K, h->W[L - 1], N,
-                            TcChain<EpiBwd>{e, split}, h->tcw.enabled ? &h->tcw.bwd[L - 1] : nullptr,
-                            h->tcw.enabled ? &h->tcw.seed : nullptr)));
-  }
-  for (int l = L - 2; l >= 1; --l) {
+  for (int l = L - 1; l >= 1; --l) {
+    // GEMM l: g_{l-1} = (res[l] ? g_l : 0) + u_l W_l, u_{l-1} = D_{l-1} g_{l-1}
     const int K = h->w[l + 1], N = h->w[l];
-    EpiBwd e{h->res[l] ? h->G : nullptr, h->res[l - 1] ? h->G : nullptr, h->D[l - 1], (int64_t)N,
-             rowidx, h->Ub[1 - cur], (int64_t)N};
-    TcEpiSplit split = h->tcw.enabled ? TcEpiSplit{&h->tcw.act[1 - cur]} : TcEpiSplit{nullptr};
+    const float* A = (l == L - 1) ? h->E : h->Ub[cur];
+    const TcOperand* tA = !tcc ? nullptr : (l == L - 1) ? &h->tcw.seed : &h->tcw.act[cur];
+    const TcOperand* tB = tcc ? &h->tcw.bwd[l] : nullptr;
+    const float* resid = (l < L - 1 && h->res[l]) ? h->G : nullptr;
     h->pcls = PC_BWD_GEMM;
     h->prows = rows_hint;
-    TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, h->Ub[cur], K, h->W[l], N,
-                            TcChain<EpiBwd>{e, split}, h->tcw.enabled ? &h->tcw.bwd[l] : nullptr,
-                            h->tcw.enabled ? &h->tcw.act[cur] : nullptr)));
+    if (l == 1 && tcc && !want_u0) {
+      EpiBwdSum e{resid, h->D[0], (int64_t)N, rowidx, (int64_t)N, h->tsum, (int64_t)N};
+      TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, e, tB, tA, route)));
+      *u0_out = nullptr;
+      if (nrb) *nrb = cdiv(nmax, 128) * 4;
+      return SDN_OK;
+    }
+    const bool last = (l == 1);
+    EpiBwd e{resid, h->res[l - 1] ? h->G : nullptr, h->D[l - 1], (int64_t)N, rowidx,
+             (!tcc || last) ? h->Ub[1 - cur] : nullptr, (int64_t)N};
+    TcEpiSplit split = (tcc && !last) ? TcEpiSplit{&h->tcw.act[1 - cur]} : TcEpiSplit{nullptr};
+    TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, TcChain<EpiBwd>{e, split}, tB, tA,
+                            route)));
     cur = 1 - cur;
   }
   *u0_out = h->Ub[cur];
@@ -418,6 +449,8 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->qpart, (size_t)h->qgrid * STATS_LEN))) return bail(rc);
   h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 16);
   if ((rc = dalloc(h, &h->cpart, (size_t)h->crb * h->maxw))) return bail(rc);
+  if ((rc = dalloc(h, &h->tsum, (size_t)cdiv(cap, 128) * 4 * h->maxw))) return bail(rc);
+  if ((rc = dalloc(h, &h->csum, (size_t)h->maxw))) return bail(rc);
   if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
   if ((rc = dalloc(h, &h->zdev, h->d_z))) return bail(rc);
@@ -698,24 +731,34 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
   const int64_t nmax = h->n;
   if (nmax > 0) {
     const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nmax, 8), 4 * h->num_sms));
+    const bool tcs = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
     { ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
     k_seed<<<sg, 256, 0, h->stream>>>(nmax, nact, rowidx, h->r_u, h->Y, dec ? h->KPhi : nullptr,
                                       dec ? h->cdec : h->c, h->ostd, h->Q, stats_dev, kind, h->shift, r.beta,
-                                      eps, r.t, kinv, h->E); }
+                                      eps, r.t, kinv, h->E, tcs ? h->tcw.seed.hi : nullptr,
+                                      tcs ? h->tcw.seed.lo : nullptr); }
     h->launches++;
     CHECK_LAUNCH(h);
-    if (h->tcw.enabled) TRY(tc_split_seed(h, h->tcw, h->E, nmax, nact));
     float* u0 = nullptr;
-    TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint));
-    dim3 cg((unsigned)cdiv(h->h1, 32), (unsigned)h->crb);
-    { ProfScope ps(h, PC_COLSUM, 0.0, 0.0, rows_hint, 4.0 * h->h1);
-    k_colsum<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, h->cpart); }
+    int64_t nrb = 0;
+    TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint, false, &nrb));
+    if (u0) {
+      dim3 cg((unsigned)cdiv(h->h1, 32), (unsigned)h->crb);
+      { ProfScope ps(h, PC_COLSUM, 0.0, 0.0, rows_hint, 4.0 * h->h1);
+      k_colsum<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, h->cpart); }
+    } else {
+      // tensor-core chain: the last GEMM left per-(tile, quarter) fp64 partials
+      ProfScope ps(h, PC_COLSUM, 0.0, 8.0 * nrb * h->h1);
+      k_colsum64<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>((int)nrb, nact, h->h1, h->tsum,
+                                                                            h->csum);
+    }
     h->launches++;
   }
   ProfScope psf(h, PC_FINAL, 0.0, 8.0 * h->crb * h->h1);
-  k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(
-      nmax > 0 ? h->crb : 0, h->h1, h->d_z, nmax > 0 ? h->cpart : nullptr, h->PzT, h->rowidx, h->n_act_dev, h->Q,
-      exact ? 1 : 0, partial_dev);
+  const bool summed = nmax > 0 && chain_tc(h, rows_hint >= 0 ? rows_hint : nmax) && h->L > 1;
+  k_finalize_grad<<<(unsigned)cdiv(h->d_z, 8), 256, sizeof(double) * h->h1, h->stream>>>(
+      nmax > 0 ? (summed ? 1 : h->crb) : 0, h->h1, h->d_z, nmax > 0 ? (summed ? h->csum : h->cpart) : nullptr,
+      h->PzT, h->rowidx, h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
   h->launches++;
   CHECK_LAUNCH(h);
   return SDN_OK;
@@ -958,7 +1001,7 @@ int sdn_eval_samples(sdn_handle* h, const double* z, int32_t qoi, double* Qout, 
     CHECK_LAUNCH(h);
     if (h->tcw.enabled) TRY(tc_split_seed(h, h->tcw, h->E, h->n, nullptr));
     float* u0 = nullptr;
-    TRY(run_backward(h, h->n, nullptr, nullptr, &u0, h->n));
+    TRY(run_backward(h, h->n, nullptr, nullptr, &u0, h->n, /*want_u0=*/true));
     TRY((gemm<false, false>(h, h->n, nullptr, h->d_zp, h->h1, u0, h->h1, h->Pz32, h->d_zp,
                             EpiStore{h->Gz, (int64_t)h->d_zp})));
     double* gd = nullptr;

@@ -200,7 +200,7 @@ struct EpiFwdHidden {
       a[0] += p.x; a[1] += p.y; a[2] += p.z; a[3] += p.w;
     }
     float4 h = make_float4(a[0], a[1], a[2], a[3]);
-    *reinterpret_cast<float4*>(H + r * ld + c) = h;
+    if (H) *reinterpret_cast<float4*>(H + r * ld + c) = h;
     if (D) *reinterpret_cast<float4*>(D + r * ld + c) = make_float4(d[0], d[1], d[2], d[3]);
     return h;
   }
@@ -225,7 +225,7 @@ struct EpiBwd {
     int64_t rd = rowidx ? (int64_t)rowidx[r] : r;
     float4 d = *reinterpret_cast<const float4*>(D + rd * ldD + c);
     float4 u = make_float4(d.x * g[0], d.y * g[1], d.z * g[2], d.w * g[3]);
-    *reinterpret_cast<float4*>(U + r * ld + c) = u;
+    if (U) *reinterpret_cast<float4*>(U + r * ld + c) = u;
     return u;
   }
   SDN_DEV void operator()(int64_t r, int c, float4 v) const { (void)apply(r, c, v); }

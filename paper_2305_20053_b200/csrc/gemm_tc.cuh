@@ -20,6 +20,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -46,6 +48,7 @@ struct TcWeights {
   TcOperand mr;                      // encoded samples (layer-0 A operand)
   std::vector<void*> allocs;
   std::map<std::tuple<const void*, int64_t, int, int>, CUtensorMap> maps;
+  std::map<std::tuple<const void*, int64_t, int64_t, int64_t>, CUtensorMap> omaps;   // epilogue outputs
 };
 
 SDN_DEV void split_bf16(float x, __nv_bfloat16& h, __nv_bfloat16& l) {
@@ -58,7 +61,8 @@ struct TcEpiSplit {
   __nv_bfloat16* hi;
   __nv_bfloat16* lo;
   int64_t ld;
-  TcEpiSplit(const TcOperand* op) : hi(op ? op->hi : nullptr), lo(op ? op->lo : nullptr), ld(op ? op->ld : 0) {}
+  TcEpiSplit(const TcOperand* op = nullptr)
+      : hi(op ? op->hi : nullptr), lo(op ? op->lo : nullptr), ld(op ? op->ld : 0) {}
   SDN_DEV void store(int64_t r, int c, float4 v) const {
     __nv_bfloat16 h0, h1, h2, h3, l0, l1, l2, l3;
     split_bf16(v.x, h0, l0); split_bf16(v.y, h1, l1);
@@ -74,6 +78,9 @@ template <class Epi>
 struct TcChain {
   Epi base;
   TcEpiSplit split;
+  // tensor-core chains: the residual input read from its bf16 split (the
+  // previous layer's GEMM operand) instead of a separate fp32 copy
+  TcEpiSplit prev;
   SDN_DEV void operator()(int64_t r, int c, float4 v) const {
     float4 o = base.apply(r, c, v);
     if (split.hi) split.store(r, c, o);
@@ -148,6 +155,18 @@ SDN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// TMA store smem tile -> global (bulk-group completion); the staging layout
+// must match the map's swizzle (64B for 16 fp32, 32B for 16 bf16 per row)
+SDN_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+SDN_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+SDN_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+SDN_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+SDN_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 SDN_DEV void tmem_alloc(uint32_t* dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
                : "memory");
@@ -223,6 +242,8 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 constexpr int TC_BM = 128;
 // optional device trace buffer (sdn_debug_gemm): per-phase clock64 stamps of CTA 0
 static unsigned long long* g_tc_trace = nullptr;
+// tuning switch: thread-issued coalesced stores instead of TMA stores
+static bool g_tc_thread_stores = getenv("SDN_TC_THREAD_STORES") != nullptr;
 constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 
 // per epilogue warp: two fp32 32x16 tiles + two bf16 32x16 tiles (6 KB)
@@ -276,6 +297,7 @@ SDN_DEV void tile_in(float* buf, const float* src, int64_t ld, const TileRows& t
 // tile_in), parked in smem once the current chunk has released it
 struct EpiPre {
   float4 a[4], b[4];
+  uint4 ph[2], pl[2];    // bf16 split residual input (hi / lo)
   float4 c[4];           // per-column constants of the chunk (bias), lane-uniform
 };
 SDN_DEV void tile_fetch(float4 (&p)[4], const float* src, int64_t ld, const TileRows& tr, bool gathered, int c0,
@@ -293,6 +315,37 @@ SDN_DEV void tile_stash(float* buf, const float4 (&p)[4], int lane) {
   const int rr = lane >> 2, j = lane & 3;
 #pragma unroll
   for (int it = 0; it < 4; ++it) *reinterpret_cast<float4*>(buf + sw_f(it * 8 + rr, j)) = p[it];
+}
+// bf16 32x16 tile (hi or lo half of a split operand): coalesced fetch into
+// registers (2 rows x 32 B per lane pair), stash into the sw_h layout
+SDN_DEV void tile_fetch_h(uint4 (&p)[2], const __nv_bfloat16* src, int64_t ld, const TileRows& tr, int c0, int N,
+                          int lane) {
+  const int rr = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int64_t g = tr.r0 + it * 16 + rr;
+    p[it] = make_uint4(0u, 0u, 0u, 0u);
+    if (g < tr.M && c0 + 8 * h < N) p[it] = __ldg(reinterpret_cast<const uint4*>(src + g * ld + c0 + 8 * h));
+  }
+}
+SDN_DEV void tile_stash_h(uint32_t* buf, const uint4 (&p)[2], int lane) {
+  const int rr = lane >> 1, h = lane & 1;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) *reinterpret_cast<uint4*>(buf + sw_h(it * 16 + rr, h)) = p[it];
+}
+// row-per-thread read of hi + lo (fp32 reconstruction, exact to 2^-17 relative)
+SDN_DEV void row_get_split(const uint32_t* bh, const uint32_t* bl, int lane, float (&x)[16]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint4 a = *reinterpret_cast<const uint4*>(bh + sw_h(lane, h));
+    const uint4 b = *reinterpret_cast<const uint4*>(bl + sw_h(lane, h));
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[8 * h + 2 * k] = __uint_as_float(av[k] << 16) + __uint_as_float(bv[k] << 16);
+      x[8 * h + 2 * k + 1] = __uint_as_float(av[k] & 0xFFFF0000u) + __uint_as_float(bv[k] & 0xFFFF0000u);
+    }
+  }
 }
 
 // smem (swizzled) -> global, coalesced
@@ -350,12 +403,39 @@ SDN_DEV void row_put_split(uint32_t* bh, uint32_t* bl, int lane, const float (&x
   }
 }
 
+// output tensor maps of a TMA-store epilogue (slot meaning per epilogue:
+// fwd hidden H, D, hi, lo; reverse G, U, hi, lo; affine C)
+struct TcOutMaps {
+  CUtensorMap m[4];
+};
+
 struct EpiSmem {
   float* f0;
   float* f1;
   uint32_t* h;
   uint32_t* l;
+  const TcOutMaps* om;   // null: thread stores (tile_out)
 };
+
+// the warp's staged tiles -> TMA bulk stores (one elected lane)
+SDN_DEV void epi_issue(const EpiSmem& s, int lane, int64_t r0, int c0, bool s0, bool s1, bool s2, bool s3) {
+  tcx::fence_proxy_async();          // generic-proxy smem writes -> visible to the async proxy
+  __syncwarp();
+  if (lane == 0) {
+    if (s0) tcx::tma_store_2d(&s.om->m[0], s.f0, c0, (int)r0);
+    if (s1) tcx::tma_store_2d(&s.om->m[1], s.f1, c0, (int)r0);
+    if (s2) tcx::tma_store_2d(&s.om->m[2], s.h, c0, (int)r0);
+    if (s3) tcx::tma_store_2d(&s.om->m[3], s.l, c0, (int)r0);
+    tcx::bulk_commit();
+  }
+}
+// before the staging is rewritten: the previous chunk's stores have read it
+SDN_DEV void epi_reclaim(const EpiSmem& s, int lane) {
+  if (s.om) {
+    if (lane == 0) tcx::bulk_wait_read0();
+    __syncwarp();
+  }
+}
 
 // generic path: row-per-thread functor calls (setup GEMMs, Jacobian scatter).
 // Every TileEpi has load() (register prefetch of the next chunk's inputs)
@@ -414,26 +494,45 @@ struct TileEpi<EpiAffine> {
       x[j + 2] = sh.z + sc.z * (__uint_as_float(v[j + 2]) + b.z);
       x[j + 3] = sh.w + sc.w * (__uint_as_float(v[j + 3]) + b.w);
     }
+    epi_reclaim(s, lane);
     row_put(s.f0, lane, x);
+    if (s.om) {
+      epi_issue(s, lane, tr.r0, c0, true, false, false, false);
+      return;
+    }
     __syncwarp();
     tile_out(s.f0, e.C, e.ldc, tr, c0, N, lane);
     __syncwarp();
   }
 };
 
-// hidden layer forward: H = [prev +] act(acc + b), D = act'(.), split(H)
+// hidden layer forward: H = [prev +] act(acc + b), D = act'(.), split(H).
+// In a tensor-core chain prev comes from the previous layer's bf16 split
+// (ch.prev) and the fp32 H is not written (e.H == nullptr).
 template <>
 struct TileEpi<TcChain<EpiFwdHidden>> {
   static SDN_DEV void load(const TcChain<EpiFwdHidden>& ch, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
-    if (ch.base.prev) tile_fetch(p.a, ch.base.prev, ch.base.ld, tr, false, c0, N, lane);
+    if (ch.prev.hi) {
+      tile_fetch_h(p.ph, ch.prev.hi, ch.prev.ld, tr, c0, N, lane);
+      tile_fetch_h(p.pl, ch.prev.lo, ch.prev.ld, tr, c0, N, lane);
+    } else if (ch.base.prev) {
+      tile_fetch(p.a, ch.base.prev, ch.base.ld, tr, false, c0, N, lane);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) p.c[j] = __ldg(reinterpret_cast<const float4*>(ch.base.bias + min(c0 + 4 * j, N - 4)));
   }
   static SDN_DEV void chunk(const TcChain<EpiFwdHidden>& ch, const EpiSmem& s, const TileRows& tr, int c0, int N,
                             int lane, const uint32_t (&v)[16], const EpiPre& pre) {
     const EpiFwdHidden& e = ch.base;
+    const bool has_prev = ch.prev.hi || e.prev;
     float a[16], d[16];
-    if (e.prev) {
+    epi_reclaim(s, lane);
+    if (ch.prev.hi) {
+      tile_stash_h(s.h, pre.ph, lane);
+      tile_stash_h(s.l, pre.pl, lane);
+      __syncwarp();
+      row_get_split(s.h, s.l, lane, a);
+    } else if (e.prev) {
       tile_stash(s.f0, pre.a, lane);
       __syncwarp();
       row_get(s.f0, lane, a);
@@ -454,7 +553,7 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
         // e^x - 1 without cancellation near 0 (Taylor to x^5 on (-1/16, 0])
         const float pm = xn * (1.0f + xn * (0.5f + xn * (0.16666667f + xn * (0.041666668f + xn * 0.008333334f))));
         const float y = x > 0.0f ? x : (xn > -0.0625f ? pm : ex - 1.0f);
-        a[j] = e.prev ? a[j] + y : y;
+        a[j] = has_prev ? a[j] + y : y;
         d[j] = x > 0.0f ? 1.0f : ex;
       }
     } else {
@@ -462,30 +561,31 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
       for (int j = 0; j < 16; ++j) {
         float y, dy;
         act_eval(e.act, __uint_as_float(v[j]) + bias[j], y, dy);
-        a[j] = e.prev ? a[j] + y : y;
+        a[j] = has_prev ? a[j] + y : y;
         d[j] = dy;
       }
     }
     __syncwarp();
-    row_put(s.f0, lane, a);
+    if (e.H) row_put(s.f0, lane, a);
+    if (e.D) row_put(s.f1, lane, d);
     if (ch.split.hi) row_put_split(s.h, s.l, lane, a);
+    if (s.om) {
+      epi_issue(s, lane, tr.r0, c0, e.H, e.D, ch.split.hi, ch.split.hi);
+      return;
+    }
     __syncwarp();
     if (e.H) tile_out(s.f0, e.H, e.ld, tr, c0, N, lane);
+    if (e.D) tile_out(s.f1, e.D, e.ld, tr, c0, N, lane);
     if (ch.split.hi) {
       tile_out_h(s.h, ch.split.hi, ch.split.ld, tr, c0, N, lane);
       tile_out_h(s.l, ch.split.lo, ch.split.ld, tr, c0, N, lane);
-    }
-    if (e.D) {
-      __syncwarp();
-      row_put(s.f0, lane, d);
-      __syncwarp();
-      tile_out(s.f0, e.D, e.ld, tr, c0, N, lane);
     }
     __syncwarp();
   }
 };
 
-// reverse step: g = acc [+ resid]; U = D[row] g; G = g (optional); split(U)
+// reverse step: g = acc [+ resid]; U = D[row] g; G = g (optional); split(U).
+// In a tensor-core chain the fp32 U is not written (e.U == nullptr).
 template <>
 struct TileEpi<TcChain<EpiBwd>> {
   static SDN_DEV void load(const TcChain<EpiBwd>& ch, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
@@ -498,6 +598,7 @@ struct TileEpi<TcChain<EpiBwd>> {
   static SDN_DEV void chunk(const TcChain<EpiBwd>& ch, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
                             const uint32_t (&v)[16], const EpiPre& pre) {
     const EpiBwd& e = ch.base;
+    epi_reclaim(s, lane);
     if (e.resid) tile_stash(s.f0, pre.a, lane);
     tile_stash(s.f1, pre.b, lane);
     __syncwarp();
@@ -515,16 +616,68 @@ struct TileEpi<TcChain<EpiBwd>> {
     for (int j = 0; j < 16; ++j) dd[j] *= g[j];
     __syncwarp();
     if (e.G) row_put(s.f0, lane, g);
-    row_put(s.f1, lane, dd);
+    if (e.U) row_put(s.f1, lane, dd);
+    if (ch.split.hi) row_put_split(s.h, s.l, lane, dd);
+    if (s.om) {
+      epi_issue(s, lane, tr.r0, c0, e.G, e.U, ch.split.hi, ch.split.hi);
+      return;
+    }
     __syncwarp();
     if (e.G) tile_out(s.f0, e.G, e.ld, tr, c0, N, lane);
-    tile_out(s.f1, e.U, e.ld, tr, c0, N, lane);
+    if (e.U) tile_out(s.f1, e.U, e.ld, tr, c0, N, lane);
     if (ch.split.hi) {
-      __syncwarp();
-      row_put_split(s.h, s.l, lane, dd);
-      __syncwarp();
       tile_out_h(s.h, ch.split.hi, ch.split.ld, tr, c0, N, lane);
       tile_out_h(s.l, ch.split.lo, ch.split.ld, tr, c0, N, lane);
+    }
+    __syncwarp();
+  }
+};
+
+// last reverse step with the sample reduction fused: u = D[row] (acc + resid)
+// is never stored; each (M tile, lane quarter) writes fp64 column sums of its
+// 32 rows to part[(tile_m * 4 + quarter) * ldp + c] (fixed order, no atomics)
+struct EpiBwdSum {
+  const float* resid; const float* D; int64_t ldD; const int* rowidx; int64_t ld;
+  double* part; int64_t ldp;
+  SDN_DEV void operator()(int64_t, int, float4) const {}
+  SDN_DEV void col(int64_t, int, float) const {}
+};
+template <>
+struct TileEpi<EpiBwdSum> {
+  static SDN_DEV void load(const EpiBwdSum& e, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
+    TileRows tg = tr;
+    tg.gather = e.rowidx;
+    if (e.resid) tile_fetch(p.a, e.resid, e.ld, tr, false, c0, N, lane);
+    tile_fetch(p.b, e.D, e.ldD, tg, true, c0, N, lane);
+  }
+  static SDN_DEV void chunk(const EpiBwdSum& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
+                            const uint32_t (&v)[16], const EpiPre& pre) {
+    if (e.resid) tile_stash(s.f0, pre.a, lane);
+    tile_stash(s.f1, pre.b, lane);
+    __syncwarp();
+    float g[16], dd[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) g[j] = __uint_as_float(v[j]);
+    if (e.resid) {
+      float r[16];
+      row_get(s.f0, lane, r);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) g[j] += r[j];
+    }
+    row_get(s.f1, lane, dd);
+    const bool live = tr.r0 + lane < tr.M;        // rows past M hold stale operand data
+#pragma unroll
+    for (int j = 0; j < 16; ++j) dd[j] = live ? dd[j] * g[j] : 0.0f;
+    __syncwarp();
+    row_put(s.f1, lane, dd);
+    __syncwarp();
+    if (lane < 16 && c0 + lane < N) {
+      const int j = lane;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) acc += (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
+      const int64_t prow = (tr.r0 >> 7) * 4 + ((tr.r0 >> 5) & 3);
+      e.part[prow * e.ldp + c0 + j] = acc;
     }
     __syncwarp();
   }
@@ -534,8 +687,8 @@ template <int BN, class Epi>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
-               const int* __restrict__ Mdev, int N, int K, Epi epi,
-               unsigned long long* __restrict__ trace = nullptr) {
+               const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
+               int use_om, unsigned long long* __restrict__ trace = nullptr) {
   using C = TcCfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -626,7 +779,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
     const int third = (warp - 4) >> 2;           // which 16-column chunks (mod 3)
     uint8_t* ep = smem + STAGES * C::STAGE_BYTES + (warp - 4) * TC_EPI_WARP_BYTES;
     const EpiSmem es{reinterpret_cast<float*>(ep), reinterpret_cast<float*>(ep + 2048),
-                     reinterpret_cast<uint32_t*>(ep + 4096), reinterpret_cast<uint32_t*>(ep + 5120)};
+                     reinterpret_cast<uint32_t*>(ep + 4096), reinterpret_cast<uint32_t*>(ep + 5120),
+                     use_om ? &om : nullptr};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -658,6 +812,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (use_om && lane == 0) tcx::bulk_wait0();    // this warp's TMA stores are complete
   }
   __syncthreads();
   if (warp == 2) {
@@ -703,6 +858,70 @@ static int tc_map(TcWeights& t, const __nv_bfloat16* base, int64_t rows, int col
   return 0;
 }
 
+// output map for the TMA-store epilogue: (rows x cols) of fp32 or bf16 with
+// row pitch ld; box = 32 rows x 16 columns, swizzle matching the staging
+// layout (sw_f = 64B for fp32 rows of 64 B, sw_h = 32B for bf16 rows of 32 B)
+static int tc_out_map(TcWeights& t, const void* base, bool bf16, int64_t rows, int cols, int64_t ld,
+                      CUtensorMap* out) {
+  auto key = std::make_tuple(base, rows, (int64_t)cols * 2 + (bf16 ? 1 : 0), ld);
+  auto it = t.omaps.find(key);
+  if (it != t.omaps.end()) { *out = it->second; return 0; }
+  auto fn = tc_encode_fn();
+  if (!fn) return -1;
+  const int es = bf16 ? 2 : 4;
+  if (((uintptr_t)base & 15) || (ld * es) % 16) return -2;
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * es};
+  cuuint32_t box[2] = {16, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  bf16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -3;
+  t.omaps[key] = m;
+  *out = m;
+  return 0;
+}
+
+// which epilogues store through TMA, and their output maps (slot order as in
+// TcOutMaps); returns 1 when every output got a map
+template <class Epi>
+struct EpiOut {
+  static int build(TcWeights&, const Epi&, int64_t, int, TcOutMaps&) { return 0; }
+};
+template <>
+struct EpiOut<EpiAffine> {
+  static int build(TcWeights& t, const EpiAffine& e, int64_t M, int N, TcOutMaps& om) {
+    return tc_out_map(t, e.C, false, M, N, e.ldc, &om.m[0]) == 0 ? 1 : 0;
+  }
+};
+template <>
+struct EpiOut<TcChain<EpiFwdHidden>> {
+  static int build(TcWeights& t, const TcChain<EpiFwdHidden>& ch, int64_t M, int N, TcOutMaps& om) {
+    const EpiFwdHidden& e = ch.base;
+    if (e.H && tc_out_map(t, e.H, false, M, N, e.ld, &om.m[0])) return 0;
+    if (e.D && tc_out_map(t, e.D, false, M, N, e.ld, &om.m[1])) return 0;
+    if (ch.split.hi && (tc_out_map(t, ch.split.hi, true, M, N, ch.split.ld, &om.m[2]) ||
+                        tc_out_map(t, ch.split.lo, true, M, N, ch.split.ld, &om.m[3])))
+      return 0;
+    return 1;
+  }
+};
+template <>
+struct EpiOut<TcChain<EpiBwd>> {
+  static int build(TcWeights& t, const TcChain<EpiBwd>& ch, int64_t M, int N, TcOutMaps& om) {
+    const EpiBwd& e = ch.base;
+    if (e.G && tc_out_map(t, e.G, false, M, N, e.ld, &om.m[0])) return 0;
+    if (e.U && tc_out_map(t, e.U, false, M, N, e.ld, &om.m[1])) return 0;
+    if (ch.split.hi && (tc_out_map(t, ch.split.hi, true, M, N, ch.split.ld, &om.m[2]) ||
+                        tc_out_map(t, ch.split.lo, true, M, N, ch.split.ld, &om.m[3])))
+      return 0;
+    return 1;
+  }
+};
+
 inline bool tc_gemm_supported(int64_t M, int N, int K) {
   return M >= 1 && K >= 8 && K % 8 == 0 && N >= 16 && N % 16 == 0 && tc_encode_fn() != nullptr;
 }
@@ -721,15 +940,23 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   }
   const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
-  tc_gemm_kernel<BN, Epi><<<grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ah, al, bh, bl, M, Mdev, N, K, epi, g_tc_trace);
+  TcOutMaps om;
+  memset(&om, 0, sizeof(om));
+  const int use_om = g_tc_thread_stores ? 0 : EpiOut<Epi>::build(t, epi, std::max<int64_t>(M, 1), N, om);
+  tc_gemm_kernel<BN, Epi><<<grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ah, al, bh, bl, M, Mdev, N, K, epi, om, use_om,
+                                                                     g_tc_trace);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
 template <class Epi>
 static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const int* Mdev, int N, int K,
-                   const TcOperand& A, const TcOperand& B, Epi epi) {
-  if (N <= 128) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
-  return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
+                   const TcOperand& A, const TcOperand& B, Epi epi, int64_t rows_est = -1) {
+  // widest N tile that still gives every SM work; narrower tiles for the
+  // short compacted sweeps (CVaR tails) and small shards
+  const int64_t mt = ((rows_est > 0 ? rows_est : M) + TC_BM - 1) / TC_BM;
+  if (N > 128 && mt * ((N + 255) / 256) >= num_sms / 2) return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
+  if (N > 64 && mt * ((N + 127) / 128) >= num_sms / 4) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
+  return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
 }
 
 // allocation / refresh of the split operands -------------------------------
@@ -774,6 +1001,7 @@ static void tc_free(TcWeights& t) {
   for (void* p : t.allocs) cudaFree(p);
   t.allocs.clear();
   t.maps.clear();
+  t.omaps.clear();
   t.enabled = false;
 }
 

@@ -6,6 +6,7 @@
 // same inputs give bit-identical outputs run to run.
 #pragma once
 #include "common.cuh"
+#include <cuda_bf16.h>
 
 namespace sdn {
 
@@ -168,7 +169,7 @@ k_seed(int64_t n, const int* __restrict__ n_act_dev, const int* __restrict__ row
        const float* __restrict__ phi, const float* __restrict__ kphi, const float* __restrict__ c,
        const float* __restrict__ ostd, const double* __restrict__ Q, const double* __restrict__ st,
        int kind, double shift, double beta, double eps, double t, double kinv,
-       float* __restrict__ E) {
+       float* __restrict__ E, __nv_bfloat16* __restrict__ Ehi = nullptr, __nv_bfloat16* __restrict__ Elo = nullptr) {
   int64_t nr = n_act_dev ? (int64_t)*n_act_dev : n;
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < nr; r += (int64_t)gridDim.x * 8) {
@@ -176,7 +177,15 @@ k_seed(int64_t n, const int* __restrict__ n_act_dev, const int* __restrict__ row
     double w = sample_weight(kind, Q[i], st, shift, beta, eps, t, kinv);
     const float* p = (kphi ? kphi : phi) + i * r_u;
     for (int j = lane; j < r_u; j += 32)
-      E[r * r_u + j] = (float)(w * 2.0 * ((double)p[j] + (double)c[j]) * (double)ostd[j]);
+    {
+      const float e = (float)(w * 2.0 * ((double)p[j] + (double)c[j]) * (double)ostd[j]);
+      E[r * r_u + j] = e;
+      if (Ehi) {   // bf16x3 split for the tensor-core sweep (its first A operand)
+        const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+        Ehi[r * r_u + j] = hi;
+        Elo[r * r_u + j] = __float2bfloat16_rn(e - __bfloat162float(hi));
+      }
+    }
   }
 }
 
@@ -201,6 +210,26 @@ k_colsum(int64_t n, const int* __restrict__ n_act_dev, int w, const float* __res
   }
 }
 
+// column sums of fp64 partial rows (nrb rows, bounded by the device row count
+// for compacted sweeps: 4 partial rows per 128-row tile), fixed order
+__global__ void __launch_bounds__(1024)
+k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __restrict__ part,
+           double* __restrict__ out) {
+  __shared__ double s[32][33];
+  if (n_act_dev) nrb = min(nrb, ((*n_act_dev + 127) / 128) * 4);
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  double acc = 0.0;
+  if (c < w)
+    for (int r = threadIdx.y; r < nrb; r += 32) acc += part[(int64_t)r * w + c];
+  s[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < w) {
+    double t = 0.0;
+    for (int y = 0; y < 32; ++y) t += s[y][threadIdx.x];
+    out[c] = t;
+  }
+}
+
 // gradient finalisation on one block:
 //   A[c] = sum_rb part[rb][c]; out[k] = sum_c Pz[c][k] A[c]  (V_z W1_z^T A)
 //   exact CVaR extras: out[d_z] = sum_{selected} Q_i, out[d_z+1] = #selected
@@ -219,13 +248,14 @@ k_finalize_grad(int nrb, int h1, int d_z, const double* __restrict__ part, const
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int k = warp; k < d_z; k += nw) {          // one warp per output, lanes over c
+  // blocks share the outputs (the d_z x h1 projection is read by many SMs)
+  for (int k = blockIdx.x * nw + warp; k < d_z; k += gridDim.x * nw) {   // one warp per output
     double s = 0.0;                               // PzT is d_z x h1: contiguous in c
     for (int c = lane; c < h1; c += 32) s += Pz[(int64_t)k * h1 + c] * A[c];
     s = warp_sum(s);
     if (lane == 0) out[k] = s;
   }
-  if (with_qsum && warp == nw - 1) {
+  if (with_qsum && blockIdx.x == 0 && warp == nw - 1) {
     int na = *n_act_dev;
     double s = 0.0;
     for (int r = lane; r < na; r += 32) s += Q[rowidx[r]];
