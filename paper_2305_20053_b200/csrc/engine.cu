@@ -117,6 +117,11 @@ struct sdn_handle {
   double* qpart = nullptr;      // qgrid x STATS_LEN
   int qgrid = 0;
   double* cpart = nullptr;      // crb x maxw
+  double* partial_multi = nullptr;   // per-risk partials of sdn_eval_multi (device)
+  double* hpart_multi = nullptr;     // pinned host copy
+  int* hidx = nullptr;               // pinned CVaR indices
+  int multi_cap = 0;
+  int64_t hidx_cap = 0;
   double* tsum = nullptr;       // (cap/128 * 4) x maxw: fused column-sum partials (TC chains)
   double* csum = nullptr;       // maxw: summed columns
   int crb = 0;
@@ -484,6 +489,9 @@ int sdn_destroy(sdn_handle* h) {
   if (h->hz) cudaFreeHost(h->hz);
   if (h->hstats) cudaFreeHost(h->hstats);
   if (h->hpart) cudaFreeHost(h->hpart);
+  if (h->partial_multi) cudaFree(h->partial_multi);
+  if (h->hpart_multi) cudaFreeHost(h->hpart_multi);
+  if (h->hidx) cudaFreeHost(h->hidx);
   tc_free(h->tcw);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -764,14 +772,9 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
   return SDN_OK;
 }
 
-static int eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
+// host combination of the (global) moments and partials of one risk
+static int finish_host(sdn_handle* h, const sdn_risk& r, const double* st, const double* pt, sdn_result* res,
                        double* grad_z) {
-  CU(cudaMemcpyAsync(h->hstats, stats_dev, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaMemcpyAsync(h->hpart, partial_dev, sizeof(double) * h->plen(), cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaStreamSynchronize(h->stream));
-  const double* st = h->hstats;
-  const double* pt = h->hpart;
-  const sdn_risk& r = h->risk;
   const double n = st[0];
   if (!(n > 0)) return fail(SDN_ERR_ARG, "empty sample set");
   const double m1 = st[1] / n;
@@ -803,6 +806,14 @@ static int eval_finish(sdn_handle* h, const double* stats_dev, const double* par
     res->q_var = qvar;
   }
   return SDN_OK;
+}
+
+static int eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
+                       double* grad_z) {
+  CU(cudaMemcpyAsync(h->hstats, stats_dev, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaMemcpyAsync(h->hpart, partial_dev, sizeof(double) * h->plen(), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return finish_host(h, h->risk, h->hstats, h->hpart, res, grad_z);
 }
 
 extern "C" {
@@ -846,8 +857,24 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     }
     any_grad |= risks[i].need_grad;
   }
+  // device work of every risk is queued back to back; one host sync at the end
+  const int plen = h->plen();
+  int64_t ktot = 0;
+  for (int i = 0; i < n_risks; ++i)
+    if (risks[i].kind == SDN_RISK_CVAR_EXACT) ktot += std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);
+  if (n_risks > h->multi_cap || ktot > h->hidx_cap) {
+    if (h->partial_multi) cudaFree(h->partial_multi);
+    if (h->hpart_multi) cudaFreeHost(h->hpart_multi);
+    if (h->hidx) cudaFreeHost(h->hidx);
+    h->multi_cap = std::max(n_risks, 4);
+    h->hidx_cap = std::max<int64_t>(ktot, 1);
+    CU(cudaMalloc(&h->partial_multi, sizeof(double) * h->multi_cap * plen));
+    CU(cudaHostAlloc((void**)&h->hpart_multi, sizeof(double) * h->multi_cap * plen, 0));
+    CU(cudaHostAlloc((void**)&h->hidx, sizeof(int) * h->hidx_cap, 0));
+  }
   TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad != 0));
   int64_t off = 0;
+  std::vector<int64_t> koff(n_risks, -1);
   for (int i = 0; i < n_risks; ++i) {
     h->risk = risks[i];
     h->compacted = false;
@@ -856,15 +883,22 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       h->kk = std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);
       TRY(select_local(h, h->kk));
     }
-    TRY(eval_backward(h, h->stats_loc, h->partial_loc));
-    TRY(eval_finish(h, h->stats_loc, h->partial_loc, &res[i], grads ? grads + (size_t)i * h->d_z : nullptr));
+    TRY(eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen));
     if (cvar_idx && risks[i].kind == SDN_RISK_CVAR_EXACT) {
-      std::vector<int> idx(h->kk);
-      CU(cudaMemcpy(idx.data(), h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost));
-      for (int64_t j = 0; j < h->kk; ++j) cvar_idx[off + j] = h->goff + idx[j];
+      CU(cudaMemcpyAsync(h->hidx + off, h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream));
+      koff[i] = off;
       off += h->kk;
     }
   }
+  CU(cudaMemcpyAsync(h->hstats, h->stats_loc, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaMemcpyAsync(h->hpart_multi, h->partial_multi, sizeof(double) * n_risks * plen, cudaMemcpyDeviceToHost,
+                     h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < n_risks; ++i)
+    TRY(finish_host(h, risks[i], h->hstats, h->hpart_multi + (size_t)i * plen, &res[i],
+                    grads ? grads + (size_t)i * h->d_z : nullptr));
+  if (cvar_idx)
+    for (int64_t j = 0; j < off; ++j) cvar_idx[j] = h->goff + h->hidx[j];
   return SDN_OK;
 }
 
@@ -1358,10 +1392,14 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   // modes 3..6 drop parts of the fused epilogue: 3 no D, 4 no split, 5 no
   // residual input, 6 only the fp32 H store
   const bool keepD = mode < 3 || (mode != 3 && mode < 6), keepS = mode < 4 || (mode != 4 && mode < 6);
-  const bool keepP = mode < 5, keepH = mode != 7;
-  EpiFwdHidden e{h->b[1], (h->res[1] && keepP) ? h->H[0] : nullptr, keepH ? h->H[1] : nullptr, keepD ? h->D[1] : nullptr,
-                 (int64_t)N, h->act};
-  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{keepS ? &h->tcw.act[1] : nullptr}};
+  const bool keepP = mode < 5, keepH = mode != 7 && mode != 8;
+  // mode 8: the production tensor-core chain epilogue (no fp32 H, residual
+  // read from the input's bf16 split, D + split outputs)
+  const bool chainm = mode == 8;
+  EpiFwdHidden e{h->b[1], (h->res[1] && keepP && !chainm) ? h->H[0] : nullptr, keepH ? h->H[1] : nullptr,
+                 (keepD || chainm) ? h->D[1] : nullptr, (int64_t)N, h->act};
+  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{(keepS || chainm) ? &h->tcw.act[1] : nullptr},
+                           TcEpiSplit{(chainm && h->res[1]) ? &h->tcw.act[0] : nullptr}};
   h->tcw.act[0].rows = M;
   int rc = 0;
   for (int it = 0; it <= reps && rc == 0; ++it) {

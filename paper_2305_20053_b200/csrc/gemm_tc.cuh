@@ -294,11 +294,19 @@ SDN_DEV void tile_in(float* buf, const float* src, int64_t ld, const TileRows& t
   }
 }
 // register prefetch of the next chunk's inputs (same coalesced pattern as
-// tile_in), parked in smem once the current chunk has released it
-struct EpiPre {
-  float4 a[4], b[4];
-  uint4 ph[2], pl[2];    // bf16 split residual input (hi / lo)
-  float4 c[4];           // per-column constants of the chunk (bias), lane-uniform
+// tile_in), parked in smem once the current chunk has released it.  Each
+// epilogue keeps only what it needs: two chunks of prefetch state must stay
+// well inside the 128-register budget of a 512-thread CTA (no spills).
+struct PreNone {};
+struct PreAff {
+  float4 b[4], s[4];     // folded bias (shift + scale*bias) and scale, lane-uniform
+};
+struct PreFwd {
+  uint4 u[4];            // residual input: 4 fp32 float4 (bit-cast) or bf16 split hi[0..1] / lo[2..3]
+  float4 c[4];           // bias, lane-uniform
+};
+struct PreBwd {
+  float4 a[4], b[4];     // residual gradient, gathered derivative
 };
 SDN_DEV void tile_fetch(float4 (&p)[4], const float* src, int64_t ld, const TileRows& tr, bool gathered, int c0,
                         int N, int lane) {
@@ -318,7 +326,7 @@ SDN_DEV void tile_stash(float* buf, const float4 (&p)[4], int lane) {
 }
 // bf16 32x16 tile (hi or lo half of a split operand): coalesced fetch into
 // registers (2 rows x 32 B per lane pair), stash into the sw_h layout
-SDN_DEV void tile_fetch_h(uint4 (&p)[2], const __nv_bfloat16* src, int64_t ld, const TileRows& tr, int c0, int N,
+SDN_DEV void tile_fetch_h(uint4* p, const __nv_bfloat16* src, int64_t ld, const TileRows& tr, int c0, int N,
                           int lane) {
   const int rr = lane >> 1, h = lane & 1;
 #pragma unroll
@@ -328,7 +336,7 @@ SDN_DEV void tile_fetch_h(uint4 (&p)[2], const __nv_bfloat16* src, int64_t ld, c
     if (g < tr.M && c0 + 8 * h < N) p[it] = __ldg(reinterpret_cast<const uint4*>(src + g * ld + c0 + 8 * h));
   }
 }
-SDN_DEV void tile_stash_h(uint32_t* buf, const uint4 (&p)[2], int lane) {
+SDN_DEV void tile_stash_h(uint32_t* buf, const uint4* p, int lane) {
   const int rr = lane >> 1, h = lane & 1;
 #pragma unroll
   for (int it = 0; it < 2; ++it) *reinterpret_cast<uint4*>(buf + sw_h(it * 16 + rr, h)) = p[it];
@@ -442,9 +450,10 @@ SDN_DEV void epi_reclaim(const EpiSmem& s, int lane) {
 // and chunk() (process one 32x16 chunk given its accumulator values).
 template <class Epi>
 struct TileEpi {
-  static SDN_DEV void load(const Epi&, const TileRows&, int, int, int, EpiPre&) {}
+  using Pre = PreNone;
+  static SDN_DEV void load(const Epi&, const TileRows&, int, int, int, Pre&) {}
   static SDN_DEV void chunk(const Epi& epi, const EpiSmem&, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const EpiPre&) {
+                            const uint32_t (&v)[16], const Pre&) {
     const int64_t row = tr.r0 + lane;
     if (row >= tr.M) return;
 #pragma unroll
@@ -465,34 +474,38 @@ struct EpiNull {
 };
 template <>
 struct TileEpi<EpiNull> {
-  static SDN_DEV void load(const EpiNull&, const TileRows&, int, int, int, EpiPre&) {}
+  using Pre = PreNone;
+  static SDN_DEV void load(const EpiNull&, const TileRows&, int, int, int, Pre&) {}
   static SDN_DEV void chunk(const EpiNull&, const EpiSmem&, const TileRows&, int, int, int, const uint32_t (&)[16],
-                            const EpiPre&) {}
+                            const Pre&) {}
 };
 
 // output layer: phi = shift + scale * (acc + bias)
 template <>
 struct TileEpi<EpiAffine> {
-  static SDN_DEV void load(const EpiAffine& e, const TileRows&, int c0, int N, int, EpiPre& p) {
+  using Pre = PreAff;
+  static SDN_DEV void load(const EpiAffine& e, const TileRows&, int c0, int N, int, Pre& p) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f), o = make_float4(1.f, 1.f, 1.f, 1.f);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = min(c0 + 4 * j, N - 4);
-      p.c[j] = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + c)) : z;
-      p.b[j] = e.scale ? __ldg(reinterpret_cast<const float4*>(e.scale + c)) : o;
-      p.a[j] = e.shift ? __ldg(reinterpret_cast<const float4*>(e.shift + c)) : z;
+      const float4 b = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + c)) : z;
+      const float4 s = e.scale ? __ldg(reinterpret_cast<const float4*>(e.scale + c)) : o;
+      const float4 h = e.shift ? __ldg(reinterpret_cast<const float4*>(e.shift + c)) : z;
+      p.s[j] = s;
+      p.b[j] = make_float4(h.x + s.x * b.x, h.y + s.y * b.y, h.z + s.z * b.z, h.w + s.w * b.w);
     }
   }
   static SDN_DEV void chunk(const EpiAffine& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const EpiPre& pre) {
+                            const uint32_t (&v)[16], const Pre& pre) {
     float x[16];
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
-      const float4 b = pre.c[j / 4], sc = pre.b[j / 4], sh = pre.a[j / 4];
-      x[j] = sh.x + sc.x * (__uint_as_float(v[j]) + b.x);
-      x[j + 1] = sh.y + sc.y * (__uint_as_float(v[j + 1]) + b.y);
-      x[j + 2] = sh.z + sc.z * (__uint_as_float(v[j + 2]) + b.z);
-      x[j + 3] = sh.w + sc.w * (__uint_as_float(v[j + 3]) + b.w);
+      const float4 b = pre.b[j / 4], sc = pre.s[j / 4];
+      x[j] = fmaf(sc.x, __uint_as_float(v[j]), b.x);
+      x[j + 1] = fmaf(sc.y, __uint_as_float(v[j + 1]), b.y);
+      x[j + 2] = fmaf(sc.z, __uint_as_float(v[j + 2]), b.z);
+      x[j + 3] = fmaf(sc.w, __uint_as_float(v[j + 3]), b.w);
     }
     epi_reclaim(s, lane);
     row_put(s.f0, lane, x);
@@ -511,29 +524,30 @@ struct TileEpi<EpiAffine> {
 // (ch.prev) and the fp32 H is not written (e.H == nullptr).
 template <>
 struct TileEpi<TcChain<EpiFwdHidden>> {
-  static SDN_DEV void load(const TcChain<EpiFwdHidden>& ch, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
+  using Pre = PreFwd;
+  static SDN_DEV void load(const TcChain<EpiFwdHidden>& ch, const TileRows& tr, int c0, int N, int lane, Pre& p) {
     if (ch.prev.hi) {
-      tile_fetch_h(p.ph, ch.prev.hi, ch.prev.ld, tr, c0, N, lane);
-      tile_fetch_h(p.pl, ch.prev.lo, ch.prev.ld, tr, c0, N, lane);
+      tile_fetch_h(p.u, ch.prev.hi, ch.prev.ld, tr, c0, N, lane);
+      tile_fetch_h(p.u + 2, ch.prev.lo, ch.prev.ld, tr, c0, N, lane);
     } else if (ch.base.prev) {
-      tile_fetch(p.a, ch.base.prev, ch.base.ld, tr, false, c0, N, lane);
+      tile_fetch(reinterpret_cast<float4(&)[4]>(p.u), ch.base.prev, ch.base.ld, tr, false, c0, N, lane);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) p.c[j] = __ldg(reinterpret_cast<const float4*>(ch.base.bias + min(c0 + 4 * j, N - 4)));
   }
   static SDN_DEV void chunk(const TcChain<EpiFwdHidden>& ch, const EpiSmem& s, const TileRows& tr, int c0, int N,
-                            int lane, const uint32_t (&v)[16], const EpiPre& pre) {
+                            int lane, const uint32_t (&v)[16], const Pre& pre) {
     const EpiFwdHidden& e = ch.base;
     const bool has_prev = ch.prev.hi || e.prev;
     float a[16], d[16];
     epi_reclaim(s, lane);
     if (ch.prev.hi) {
-      tile_stash_h(s.h, pre.ph, lane);
-      tile_stash_h(s.l, pre.pl, lane);
+      tile_stash_h(s.h, pre.u, lane);
+      tile_stash_h(s.l, pre.u + 2, lane);
       __syncwarp();
       row_get_split(s.h, s.l, lane, a);
     } else if (e.prev) {
-      tile_stash(s.f0, pre.a, lane);
+      tile_stash(s.f0, reinterpret_cast<const float4(&)[4]>(pre.u), lane);
       __syncwarp();
       row_get(s.f0, lane, a);
     }
@@ -588,7 +602,8 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
 // In a tensor-core chain the fp32 U is not written (e.U == nullptr).
 template <>
 struct TileEpi<TcChain<EpiBwd>> {
-  static SDN_DEV void load(const TcChain<EpiBwd>& ch, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
+  using Pre = PreBwd;
+  static SDN_DEV void load(const TcChain<EpiBwd>& ch, const TileRows& tr, int c0, int N, int lane, Pre& p) {
     const EpiBwd& e = ch.base;
     TileRows tg = tr;
     tg.gather = e.rowidx;
@@ -596,7 +611,7 @@ struct TileEpi<TcChain<EpiBwd>> {
     tile_fetch(p.b, e.D, e.ldD, tg, true, c0, N, lane);
   }
   static SDN_DEV void chunk(const TcChain<EpiBwd>& ch, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const EpiPre& pre) {
+                            const uint32_t (&v)[16], const Pre& pre) {
     const EpiBwd& e = ch.base;
     epi_reclaim(s, lane);
     if (e.resid) tile_stash(s.f0, pre.a, lane);
@@ -644,14 +659,15 @@ struct EpiBwdSum {
 };
 template <>
 struct TileEpi<EpiBwdSum> {
-  static SDN_DEV void load(const EpiBwdSum& e, const TileRows& tr, int c0, int N, int lane, EpiPre& p) {
+  using Pre = PreBwd;
+  static SDN_DEV void load(const EpiBwdSum& e, const TileRows& tr, int c0, int N, int lane, Pre& p) {
     TileRows tg = tr;
     tg.gather = e.rowidx;
     if (e.resid) tile_fetch(p.a, e.resid, e.ld, tr, false, c0, N, lane);
     tile_fetch(p.b, e.D, e.ldD, tg, true, c0, N, lane);
   }
   static SDN_DEV void chunk(const EpiBwdSum& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const EpiPre& pre) {
+                            const uint32_t (&v)[16], const Pre& pre) {
     if (e.resid) tile_stash(s.f0, pre.a, lane);
     tile_stash(s.f1, pre.b, lane);
     __syncwarp();
@@ -791,13 +807,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
       const bool tr0 = trace && blockIdx.x == 0 && warp == 4 && lane == 0 && tile == (int)blockIdx.x;
       if (tr0) trace[8] = clock64();
-      EpiPre cur;
+      typename TileEpi<Epi>::Pre cur;
       if (nb * BN + 16 * third < N) TileEpi<Epi>::load(epi, tr, nb * BN + 16 * third, N, lane, cur);
       int ci = 0;
 #pragma unroll 1
       for (int c0 = 16 * third; c0 < BN; c0 += 48, ++ci) {
         if (nb * BN + c0 >= N) break;            // warp-uniform
-        EpiPre nxt;                              // prefetch the next chunk's inputs
+        typename TileEpi<Epi>::Pre nxt;          // prefetch the next chunk's inputs
         if (c0 + 48 < BN && nb * BN + c0 + 48 < N) TileEpi<Epi>::load(epi, tr, nb * BN + c0 + 48, N, lane, nxt);
         uint32_t v[16];
         tcx::tmem_ld16(tbase + c0, v);
