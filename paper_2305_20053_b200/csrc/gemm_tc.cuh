@@ -970,6 +970,9 @@ static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const 
   // widest N tile that still gives every SM work; narrower tiles for the
   // short compacted sweeps (CVaR tails) and small shards
   const int64_t mt = ((rows_est > 0 ? rows_est : M) + TC_BM - 1) / TC_BM;
+  static const int bn_force = getenv("SDN_TC_BN") ? atoi(getenv("SDN_TC_BN")) : 0;   // tuning override
+  if (bn_force == 64) return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
+  if (bn_force == 128) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
   if (N > 128 && mt * ((N + 255) / 256) >= num_sms / 2) return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
   if (N > 64 && mt * ((N + 127) / 128) >= num_sms / 4) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
   return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi);

@@ -1,0 +1,97 @@
+"""BASELINE configs 3-5 on the GPU: parity at reduced N against the float64
+oracle, and size-independent properties at full N (c4: 131072 samples)."""
+
+import numpy as np
+import pytest
+
+from oracle import mrdino_ref as ref
+from paper_2305_20053_b200 import Engine, workloads as wl
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-4
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _setup(name, n, gemm="auto", seed=0):
+    cfg = wl.WORKLOADS[name].with_samples(n)
+    p = wl.make_problem(cfg, seed=seed, count=n)
+    eng = Engine(p, max_samples=n, gemm=gemm)
+    eng.set_tracking(p.c, p.q0)
+    eng.set_samples(p.m_r)
+    return p, eng
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_ns_shapes_meanvar_and_exact_cvar(name):
+    """width-1024 chains (depth 4 / 6), r_u 256 / 400, exact CVaR 0.99."""
+    p, eng = _setup(name, 2048, gemm="tc")
+    form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=form)
+    res = eng.eval_multi(p.z, [dict(kind="meanvar", beta=1.0, alpha=1e-2),
+                               dict(kind="cvar_exact", beta=0.99, alpha=1e-2)])
+    o = ref.saa_objective(Qo, Go, p.z, ref.Risk("meanvar", beta=1.0, alpha=1e-2))
+    assert abs(res[0].value - o[0]) <= RTOL * abs(o[0])
+    assert _rel(res[0].grad_z, o[1]) <= RTOL
+    # exact CVaR: indices bit-exact on the GPU's own Q; value/grad on that selection
+    Qg, _ = eng.eval_samples(p.z, need_grad=False)
+    np.testing.assert_array_equal(np.sort(res[1].idx), np.sort(ref.cvar_select(Qg, 0.99)))
+    sel = res[1].idx
+    v = Qo[sel].mean() + 1e-2 * float(p.z.astype(np.float64) @ p.z)
+    g = Go[sel].mean(0) + 2e-2 * p.z.astype(np.float64)
+    assert abs(res[1].value - v) <= RTOL * abs(v)
+    assert _rel(res[1].grad_z, g) <= RTOL
+
+
+def test_c3_smoothed_cvar_simt_exact_fp32():
+    """BASELINE c3 risk (smoothed CVaR, the reference's eps = 1e-4, t from
+    mc_var of Q(z0) as minimize does) on the exact-fp32 path."""
+    p, eng = _setup("c3", 1024, gemm="simt")
+    form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=form)
+    t = ref.mc_var(Qo, 0.95)
+    r = eng.eval(p.z, "cvar", beta=0.95, eps=1e-4, t=t)
+    o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar", beta=0.95, eps=1e-4), t)
+    assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+    assert _rel(r.grad_z, o[1]) <= RTOL
+    assert abs(r.grad_t - o[2]) <= 1e-6
+
+
+def test_c5_decoded_jacobian_batch():
+    """c5: batched dq/dz decoded to d_u x d_z (tests/test_acceptance.py:326)."""
+    cfg = wl.WORKLOADS["c5"].with_samples(64)
+    p = wl.make_problem(cfg, seed=0, count=64, with_decoder=True)
+    eng = Engine(p, max_samples=64)
+    eng.set_decoder(p.U, p.ubias, p.Mdiag_u, p.u_target)
+    Z = np.broadcast_to(p.z, (64, cfg.d_z))
+    Jd = eng.jacobian_batch(p.m_r, Z, decoded=True)
+    Jo = ref.z_jacobian_batch(ref.as_oracle(p), p.m_r, Z)
+    assert Jd.shape == (64, cfg.d_u, cfg.d_z)
+    assert _rel(Jd, np.einsum("du,iuk->idk", p.U.astype(np.float64), Jo)) <= RTOL
+
+
+def test_c4_full_n_properties():
+    """N = 131072 (BASELINE c4): the exact-CVaR objective returned by the
+    fused path equals the mean over its own selection of the per-sample
+    evaluator protocol (Q, G) -- a size-independent consistency check -- and
+    the selection is the oracle's rule on the GPU's Q."""
+    cfg = wl.WORKLOADS["c4"]
+    n = cfg.n_samples
+    p = wl.make_problem(cfg, seed=0, count=n)
+    eng = Engine(p, max_samples=n)
+    eng.set_tracking(p.c, p.q0)
+    eng.set_samples(p.m_r)
+    r = eng.eval(p.z, "cvar_exact", beta=0.99)
+    assert r.idx.size == 1311                      # ceil(0.01 * 131072)
+    Q, G = eng.eval_samples(p.z)
+    np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Q, 0.99)))
+    assert abs(r.value - Q[r.idx].mean()) <= 1e-9 * abs(r.value)
+    assert _rel(r.grad_z, G[r.idx].mean(0)) <= 1e-5
+    # and a 2048-sample slice against the float64 oracle
+    sl = slice(5000, 7048)
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), p.m_r[sl], p.z,
+                                 form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    assert _rel(Q[sl], Qo) <= 2e-5
