@@ -3,14 +3,14 @@
 surface (ouukit/__init__.py:5-22); the compute runs in libsaadino.so
 (hand-written sm_100a CUDA, include/saadino.h)."""
 
-from .api import (Decoder, NetworkSpec, ReducedTrackingForm, RiskSpec, SAAProblem,
+from .api import (Decoder, NetworkSpec, OptResult, ReducedTrackingForm, RiskSpec, SAAProblem,
                   SurrogateEvaluator, SurrogateModel, build_tracking_form, init_model,
-                  mc_cvar, mc_var, saa_objective, splus, splus_d1)
+                  mc_cvar, mc_var, minimize, saa_objective, splus, splus_d1)
 from .engine import Engine, EvalResult
 from . import workloads
 
 __version__ = "0.1.0"
 
-__all__ = ["Decoder", "Engine", "EvalResult", "NetworkSpec", "ReducedTrackingForm", "RiskSpec",
+__all__ = ["Decoder", "Engine", "EvalResult", "NetworkSpec", "OptResult", "ReducedTrackingForm", "RiskSpec", "minimize",
            "SAAProblem", "SurrogateEvaluator", "SurrogateModel", "build_tracking_form", "init_model",
            "mc_cvar", "mc_var", "saa_objective", "splus", "splus_d1", "workloads"]

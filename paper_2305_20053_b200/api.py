@@ -320,6 +320,111 @@ class SurrogateEvaluator:
         return r
 
 
+@dataclass
+class OptResult:
+    """riskopt.py:250-260."""
+    z_star: np.ndarray
+    t_star: Optional[float]
+    objective: float
+    objective_history: list
+    pg_norm_history: list
+    iterations: int
+    converged: bool
+    line_search_failed: bool
+    evaluator_counts: dict
+
+
+def _lbfgs_direction(g, pairs):
+    """Two-loop recursion (riskopt.py:263-276) with the s.y/y.y initial scaling."""
+    q = g.copy()
+    alphas = []
+    for s, y, rho in reversed(pairs):
+        a = rho * float(s @ q)
+        alphas.append(a)
+        q -= a * y
+    if pairs:
+        s, y, _ = pairs[-1]
+        q *= float(s @ y) / float(y @ y)
+    for (s, y, rho), a in zip(pairs, reversed(alphas)):
+        q += (a - rho * float(y @ q)) * s
+    return -q
+
+
+def minimize(prob: SAAProblem, z0, t0: Optional[float] = None, max_iter: int = 500, pg_tol: float = 1e-6,
+             memory: int = 10) -> OptResult:
+    """Projected L-BFGS over (z, t) with Armijo backtracking along the
+    projection arc (riskopt.py:279-373); t exists for the smoothed CVaR and
+    starts at the beta-quantile of Q(z0) (mc_var) when t0 is omitted.  Every
+    objective call goes through saa_objective, i.e. the fused GPU path for
+    a SurrogateEvaluator."""
+    z0 = np.asarray(z0, float)
+    lo = np.asarray(prob.bounds_lo, float)
+    hi = np.asarray(prob.bounds_hi, float)
+    if np.any(z0 < lo - 1e-12) or np.any(z0 > hi + 1e-12):
+        raise ValueError("initial control violates the bounds")
+    use_t = prob.risk.kind == "cvar"
+    if use_t and t0 is None:
+        ev = prob.evaluator
+        Q0 = ev.values_only(z0) if hasattr(ev, "values_only") else ev(z0)[0]
+        t0 = mc_var(Q0, prob.risk.beta)
+    if use_t:
+        x = np.append(z0, float(t0))
+        xlo, xhi = np.append(lo, -np.inf), np.append(hi, np.inf)
+    else:
+        x, xlo, xhi = z0.copy(), lo, hi
+
+    def fg(xv):
+        if use_t:
+            v, gz, gt = saa_objective(prob, xv[:-1], xv[-1])
+            return float(v), np.append(gz, gt)
+        v, gz, _ = saa_objective(prob, xv)
+        return float(v), np.asarray(gz, float)
+
+    f, g = fg(x)
+    pairs: list = []
+    history, pg_history = [f], []
+    converged = ls_failed = False
+    best_f, best_x = f, x.copy()
+    it = 0
+    for it in range(1, max_iter + 1):
+        pgnorm = float(np.abs(x - np.clip(x - g, xlo, xhi)).max())
+        pg_history.append(pgnorm)
+        if pgnorm <= pg_tol * max(1.0, abs(f)):
+            converged = True
+            break
+        d = _lbfgs_direction(g, pairs)
+        if g @ d > -1e-12 * np.linalg.norm(g) * np.linalg.norm(d):
+            d = -g                                   # not a descent direction
+        step, accepted = 1.0, False
+        for _ in range(40):
+            x_new = np.clip(x + step * d, xlo, xhi)
+            dx = x_new - x
+            if not np.any(dx):
+                break
+            f_new, g_new = fg(x_new)
+            if np.isfinite(f_new) and f_new <= f + 1e-4 * float(g @ dx):
+                accepted = True
+                break
+            step *= 0.5
+        if not accepted:
+            ls_failed = True
+            break
+        s_vec, y_vec = x_new - x, g_new - g
+        sy = float(s_vec @ y_vec)
+        if sy > 1e-12 * np.linalg.norm(s_vec) * np.linalg.norm(y_vec):
+            pairs.append((s_vec, y_vec, 1.0 / sy))
+            del pairs[:-memory]
+        x, f, g = x_new, f_new, g_new
+        history.append(f)
+        if f < best_f:
+            best_f, best_x = f, x.copy()
+    if ls_failed and best_f < f:
+        f, x = best_f, best_x.copy()
+    return OptResult(z_star=x[:-1] if use_t else x, t_star=float(x[-1]) if use_t else None, objective=float(f),
+                     objective_history=history, pg_norm_history=pg_history, iterations=it, converged=converged,
+                     line_search_failed=ls_failed, evaluator_counts=dict(getattr(prob.evaluator, "counts", {})))
+
+
 def saa_objective(prob: SAAProblem, z, t: Optional[float] = None):
     """Value and exact gradients of the SAA risk objective; returns
     (value, grad_z, grad_t) with grad_t None unless kind == "cvar"
