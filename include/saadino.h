@@ -97,6 +97,8 @@ typedef struct sdn_result {
   int64_t n_samples;         /* global sample count */
   int64_t n_selected;        /* CVaR exact: k; smoothed: active samples */
   double q_mean, q_var;      /* sample moments of Q (for reporting) */
+  int64_t n_refined;         /* rows of this rank re-evaluated in exact fp32
+                                (smoothed CVaR on tensor-core chains) */
 } sdn_result;
 
 const char* sdn_last_error(void);
@@ -183,6 +185,13 @@ int sdn_eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk,
                      double* stats_dev);
 int sdn_eval_candidates(sdn_handle* h, int64_t k, double* cand_dev);
 int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, int64_t k);
+
+/* Multi-rank exact CVaR, optional: after sdn_eval_select, re-evaluate in fp64
+ * the rows of this shard whose Q lies within refinement error of the global
+ * threshold (Q refined in place); then repeat sdn_eval_candidates ->
+ * all-gather -> sdn_eval_select.  Single-rank sdn_eval / sdn_eval_multi do
+ * the equivalent internally. */
+int sdn_eval_refine_band(sdn_handle* h);
 int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev);
 /* Switch the risk for the next sweep sharing the last forward (multi-risk). */
 int sdn_eval_set_risk(sdn_handle* h, const sdn_risk* risk);
@@ -196,9 +205,9 @@ int sdn_last_q(sdn_handle* h, const double** q_dev, int64_t* n);
 /* Instrumentation.  sdn_profile(h, 1) starts CUDA-event timing of every
  * launch by kernel class (0 fwd GEMM, 1 reverse GEMM, 2 QoI+moments,
  * 3 top-k select, 4 compaction, 5 seeds, 6 column sums, 7 finalise,
- * 8 zbias, 9 other); sdn_profile_read returns per-class device ms,
+ * 8 zbias, 9 other, 10 fp64 Q refinement); sdn_profile_read returns per-class device ms,
  * algorithmic flops and bytes, and launch counts. */
-#define SDN_PROF_CLASSES 10
+#define SDN_PROF_CLASSES 11
 int sdn_profile(sdn_handle* h, int32_t enable);
 int sdn_profile_read(sdn_handle* h, int32_t n_cls, double* ms, double* flops, double* bytes,
                      int64_t* count);

@@ -19,7 +19,7 @@ QOI = {"reduced": 0, "decoded": 1}
 GEMM = {"auto": 0, "simt": 1, "tc": 2}
 STATS_LEN = 8
 PROF_CLASSES = ["fwd_gemm", "bwd_gemm", "qoi", "select", "compact", "seed", "colsum", "finalize", "zbias",
-                "other"]
+                "other", "refine"]
 
 
 class Config(C.Structure):
@@ -35,7 +35,8 @@ class Risk(C.Structure):
 
 class Result(C.Structure):
     _fields_ = [("value", C.c_double), ("grad_t", C.c_double), ("n_samples", C.c_int64),
-                ("n_selected", C.c_int64), ("q_mean", C.c_double), ("q_var", C.c_double)]
+                ("n_selected", C.c_int64), ("q_mean", C.c_double), ("q_var", C.c_double),
+                ("n_refined", C.c_int64)]
 
 
 _P = C.c_void_p
@@ -67,6 +68,7 @@ SIGNATURES = {
     "sdn_eval_forward": (C.c_int, [_P, _D, C.POINTER(Risk), _P]),
     "sdn_eval_candidates": (C.c_int, [_P, C.c_int64, _P]),
     "sdn_eval_select": (C.c_int, [_P, _P, C.c_int32, C.c_int64]),
+    "sdn_eval_refine_band": (C.c_int, [_P]),
     "sdn_eval_backward": (C.c_int, [_P, _P, _P]),
     "sdn_eval_set_risk": (C.c_int, [_P, C.POINTER(Risk)]),
     "sdn_eval_finish": (C.c_int, [_P, _P, _P, C.POINTER(Result), _D]),

@@ -70,4 +70,21 @@ SDN_DEV uint64_t dkey(double v) {
   return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// inverse of dkey (the NaN key maps back to a NaN)
+SDN_DEV double dkey_inv(uint64_t k) {
+  uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// activations in fp64 (Q refinement chain; oracle act_value)
+SDN_DEV double act64(int act, double s) {
+  switch (act) {
+    case ACT_TANH: return tanh(s);
+    case ACT_SOFTPLUS: return fmax(s, 0.0) + log1p(exp(-fabs(s)));
+    case ACT_SIGMOID: return 1.0 / (1.0 + exp(-s));
+    case ACT_ELU: return s > 0.0 ? s : expm1(s);
+    default: return s;
+  }
+}
+
 }  // namespace sdn

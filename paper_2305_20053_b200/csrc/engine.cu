@@ -18,6 +18,10 @@
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
+#include "refine.cuh"
+
+// SMs left to side-stream work while the main stream's GEMMs run (sdn_eval_multi)
+constexpr int SDN_SIDE_SMS = 8;
 
 #include <algorithm>
 #include <cmath>
@@ -153,6 +157,31 @@ struct sdn_handle {
   bool have_mean = false;
   double last_mean = 0.0;
   bool fwd_done = false;
+  // Q refinement (fp64 re-evaluation of decision-boundary rows)
+  float* W0raw = nullptr;       // h1 x r_m : W1[:, :r_m] as given (fp32)
+  float* iscale = nullptr;      // r_m input scale
+  double* zb64 = nullptr;       // h1 : b1 + Pz z in fp64
+  double* ref64[2] = {nullptr, nullptr};   // ref_rows x maxw ping-pong
+  int ref_rows = 0;
+  double* thr_dev = nullptr;    // exact-CVaR threshold value (top-k output)
+  int* ref_blockcnt = nullptr;  // k_refine grid scratch
+  unsigned* ref_bar = nullptr;  // k_refine grid barrier
+  int ref_grid = 0;
+  bool ref_ok = false;          // every layer input width <= REF_KC
+  // side stream (overlapped exact-CVaR selection in sdn_eval_multi)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_side = nullptr;
+  double* Qx = nullptr;
+  int* x_counts = nullptr;
+  int* x_offs = nullptr;
+  std::vector<int*> x_rowidx, x_nact;
+  int sm_avail = 0;             // SMs the persistent GEMMs may use
+  int* band_log = nullptr;      // band row counts: [0] forward window, [1 + i] exact risk i
+  int* hband = nullptr;         // pinned mirror
+  int band_cap = 0;
+  double* K64 = nullptr;        // decoded-frame Gram / c in fp64
+  double* c64dec = nullptr;
+  bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
   bool selected = false;        // exact CVaR selection done
   int64_t kk = 0;               // exact CVaR k (global)
   bool compacted = false;
@@ -177,7 +206,7 @@ static int dalloc(sdn_handle* h, T** p, size_t count) {
 // profiling: events bracket each launch on the handle's stream
 
 enum ProfClass { PC_FWD_GEMM = 0, PC_BWD_GEMM, PC_QOI, PC_SELECT, PC_COMPACT, PC_SEED, PC_COLSUM, PC_FINAL,
-                 PC_ZBIAS, PC_OTHER, PC_N };
+                 PC_ZBIAS, PC_OTHER, PC_REFINE, PC_N };
 
 static cudaEvent_t prof_event(sdn_handle* h) {
   if (h->pool_used == h->pool.size()) {
@@ -246,7 +275,7 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
     if (tiles < h->num_sms / 2) use_tc = false;
   }
   if (use_tc) {
-    int rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, Mdev, N, K, *tcA, *tcB, epi, rows);
+    int rc = tc_gemm(h->tcw, h->stream, h->sm_avail, M, Mdev, N, K, *tcA, *tcB, epi, rows);
     h->launches++;
     if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");
     CHECK_LAUNCH(h);
@@ -286,11 +315,15 @@ static bool chain_tc(sdn_handle* h, int64_t rows) {
 
 // layer chain on `nrows` rows.  Layer 0 input: X (ld0, K0) with weight W0 and
 // bias0 (either MR + zb, or [m_r | z] + b0).  store_D keeps act' for the sweep.
+// Hs (optional) replaces the hidden ping-pong buffers; simt forces the exact
+// fp32 SIMT chain (Q refinement).
 static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0, int K0,
                        const float* W0, int64_t ldW0, const float* bias0, bool store_D,
-                       float* phi_out, const TcOperand* tcX0) {
+                       float* phi_out, const TcOperand* tcX0, float* const* Hs = nullptr,
+                       bool simt = false) {
   const int L = h->L;
-  const bool tcc = chain_tc(h, nrows);
+  const bool tcc = !simt && chain_tc(h, nrows);
+  float* const* Hb = Hs ? Hs : h->H;
   int cur = 0;
   const float* in = X;
   int64_t ldin = ld0;
@@ -309,7 +342,7 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
       EpiAffine e{bl, h->ostd, h->omean, phi_out, (int64_t)n_out};
       TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA, tc ? 1 : 0)));
     } else {
-      float* out = h->H[(l == 0) ? 0 : 1 - cur];
+      float* out = Hb[(l == 0) ? 0 : 1 - cur];
       // in a tensor-core chain the residual is read from the bf16 split of the
       // layer input (the A operand), and the fp32 H is never needed
       const bool split_prev = tc && h->res[l];
@@ -411,6 +444,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   cudaError_t e = cudaSetDevice(h->device);
   if (e != cudaSuccess) { delete h; return fail(SDN_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  h->sm_avail = h->num_sms;
   e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) { delete h; return fail(SDN_ERR_CUDA, "cudaStreamCreate failed"); }
   h->own_stream = true;
@@ -460,10 +494,34 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
   if ((rc = dalloc(h, &h->zdev, h->d_z))) return bail(rc);
   if ((rc = dalloc(h, &h->zb, h->h1))) return bail(rc);
+  if ((rc = dalloc(h, &h->zb64, h->h1))) return bail(rc);
+  if ((rc = dalloc(h, &h->W0raw, (size_t)h->h1 * h->r_m))) return bail(rc);
+  if ((rc = dalloc(h, &h->iscale, h->r_m))) return bail(rc);
+  if ((rc = dalloc(h, &h->thr_dev, 1))) return bail(rc);
+  h->ref_rows = (int)std::min<int64_t>(cap, REFINE_ROWS);
+  {
+    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(double) * REF_RB * REF_KC);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, REF_THREADS, sizeof(double) * REF_RB * REF_KC);
+    h->ref_grid = h->num_sms;                     // one block per SM, all co-resident
+    h->ref_ok = per_sm >= 1 && h->L <= REF_MAX_LAYERS && h->r_m <= REF_KC;
+    for (int l = 1; l < h->L; ++l) h->ref_ok = h->ref_ok && h->w[l] <= REF_KC;
+  }
+  if ((rc = dalloc(h, &h->ref_blockcnt, h->num_sms))) return bail(rc);
+  if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);
+  if (cudaMemset(h->ref_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
+  for (int i = 0; i < 2; ++i)
+    if ((rc = dalloc(h, &h->ref64[i], (size_t)h->ref_rows * h->maxw))) return bail(rc);
+  h->band_cap = 8;
+  if ((rc = dalloc(h, &h->band_log, h->band_cap))) return bail(rc);
+  if (cudaHostAlloc((void**)&h->hband, sizeof(int) * h->band_cap, 0) != cudaSuccess)
+    return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
   if (cudaHostAlloc((void**)&h->hz, sizeof(double) * h->d_z, 0) != cudaSuccess ||
       cudaHostAlloc((void**)&h->hstats, sizeof(double) * STATS_LEN, 0) != cudaSuccess ||
       cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), 0) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
+  { const char* e = getenv("SDN_NO_REFINE"); h->no_refine = e && e[0] == '1'; }
   h->tcw.enabled = false;
   if (h->gemm != SDN_GEMM_SIMT) {
     if ((rc = tc_alloc(h, h->tcw))) return bail(rc);
@@ -489,10 +547,16 @@ int sdn_destroy(sdn_handle* h) {
   if (h->hz) cudaFreeHost(h->hz);
   if (h->hstats) cudaFreeHost(h->hstats);
   if (h->hpart) cudaFreeHost(h->hpart);
+  if (h->hband) cudaFreeHost(h->hband);
+  if (h->K64) cudaFree(h->K64);
+  if (h->c64dec) cudaFree(h->c64dec);
   if (h->partial_multi) cudaFree(h->partial_multi);
   if (h->hpart_multi) cudaFreeHost(h->hpart_multi);
   if (h->hidx) cudaFreeHost(h->hidx);
   tc_free(h->tcw);
+  if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
+  if (h->ev_fwd) cudaEventDestroy(h->ev_fwd);
+  if (h->ev_side) cudaEventDestroy(h->ev_side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return SDN_OK;
@@ -547,6 +611,13 @@ int sdn_set_model(sdn_handle* h, const float* const* W, const float* const* b, c
     }
   }
   CU(cudaMemcpy(h->W[0], w0m.data(), w0m.size() * 4, cudaMemcpyHostToDevice));
+  {
+    std::vector<float> raw((size_t)h1 * r_m);
+    for (int c = 0; c < h1; ++c)
+      for (int j = 0; j < r_m; ++j) raw[(size_t)c * r_m + j] = W[0][(size_t)c * n0 + j];
+    CU(cudaMemcpy(h->W0raw, raw.data(), raw.size() * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->iscale, in_scale, (size_t)r_m * 4, cudaMemcpyHostToDevice));
+  }
   for (int l = 1; l < h->L; ++l)
     CU(cudaMemcpy(h->W[l], W[l], (size_t)h->w[l + 1] * h->w[l] * 4, cudaMemcpyHostToDevice));
   for (int l = 0; l < h->L; ++l) CU(cudaMemcpy(h->b[l], b[l], (size_t)h->w[l + 1] * 4, cudaMemcpyHostToDevice));
@@ -620,6 +691,53 @@ static int upload_z(sdn_handle* h, const double* z) {
   return SDN_OK;
 }
 
+static int compact_rows(sdn_handle* h, int kind, double t, double eps, const double* tdev = nullptr,
+                        int* count_out = nullptr);
+
+// Q refinement.  Rows whose chain Q (bf16x3 or fp32, ~1e-5
+// relative) lies within REFINE_REL |Q| of a decision boundary -- the
+// smoothed-CVaR window [t, t + eps] (kind RISK_BAND) or the exact-CVaR
+// threshold (RISK_BAND_EXACT, value in thr_dev) -- are compacted and
+// re-evaluated by an fp64 chain on the same fp32 weights (the oracle's
+// arithmetic), and their Q replaced in place.  No host round trip: the band
+// count stays on the device (*count); more than ref_rows band rows skips the
+// refinement for that evaluation (reported as a negative n_refined).
+static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, int* count,
+                       uint8_t* mask = nullptr) {
+  if (!h->ref_ok) return SDN_OK;
+  RefineArgs a{};
+  a.n = h->n; a.kind = kind; a.t = t; a.eps = eps; a.tdev = h->thr_dev;
+  a.rowidx = h->rowidx; a.count = count; a.blockcnt = h->ref_blockcnt; a.bar = h->ref_bar;
+  a.L = h->L;
+  for (int l = 0; l < h->L; ++l) {
+    const bool first = l == 0;
+    a.layer[l] = RefineLayer{first ? h->W0raw : h->W[l], h->b[l], first ? h->r_m : h->w[l], h->w[l + 1],
+                             (l > 0 && l < h->L - 1 && h->res[l]) ? 1 : 0};
+  }
+  a.MR = h->MR; a.iscale = h->iscale; a.zb64 = h->zb64; a.act = h->act; a.omean = h->omean; a.ostd = h->ostd;
+  a.buf[0] = h->ref64[0]; a.buf[1] = h->ref64[1]; a.cap_rows = h->ref_rows;
+  a.r_u = h->r_u; a.c32 = h->c; a.K64 = dec ? h->K64 : nullptr; a.c64 = dec ? h->c64dec : nullptr;
+  a.q0 = dec ? h->q0dec : h->q0; a.Q = h->Q; a.mask = mask;
+  void* args[] = {&a};
+  ProfScope ps(h, PC_REFINE, 0.0, 0.0);
+  CU(cudaLaunchCooperativeKernel((const void*)k_refine, dim3(h->ref_grid), dim3(REF_THREADS), args,
+                                 sizeof(double) * REF_RB * REF_KC, h->stream));
+  h->launches++;
+  return SDN_OK;
+}
+
+// smoothed CVaR: refine the window rows, then retake the moments from Q
+static int refine_window(sdn_handle* h, const sdn_risk* risk, bool dec, int qg, double* stats_dev) {
+  if (risk->kind != SDN_RISK_CVAR_SMOOTH || h->n == 0 || h->no_refine || !h->ref_ok) return SDN_OK;
+  TRY(refine_band(h, RISK_BAND, risk->t, risk->eps, dec, h->band_log));
+  { ProfScope ps(h, PC_QOI, 0.0, 8.0 * h->n);
+  k_moments<<<qg, 256, 0, h->stream>>>(h->n, h->Q, h->shift, risk->t, risk->eps, h->qpart);
+  k_sum_rows<<<(unsigned)cdiv(STATS_LEN, 8), 256, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
+  h->launches += 2;
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
 // phase 1: forward over the shard; local moments -> stats_dev (device)
 static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, double* stats_dev,
                         bool store_D) {
@@ -638,7 +756,8 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   h->shift = q0;
   TRY(upload_z(h, z));
   { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
-  k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb); }
+  k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb,
+                                                             h->zb64); }
   h->launches++;
   CHECK_LAUNCH(h);
   if (h->n > 0) {
@@ -657,6 +776,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   k_sum_rows<<<(unsigned)cdiv(STATS_LEN, 8), 256, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
   h->launches += 2;
   CHECK_LAUNCH(h);
+  TRY(refine_window(h, risk, dec, qg, stats_dev));
   h->fwd_done = true;
   return SDN_OK;
 }
@@ -675,12 +795,12 @@ static int ensure_cand(sdn_handle* h, int64_t count) {
 }
 
 // ordered compaction of flagged rows -> rowidx / n_act_dev
-static int compact_rows(sdn_handle* h, int kind, double t, double eps) {
+static int compact_rows(sdn_handle* h, int kind, double t, double eps, const double* tdev, int* count_out) {
   const int nb = (int)cdiv(std::max<int64_t>(h->n, 1), 1024);
   ProfScope ps(h, PC_COMPACT, 0.0, 2.0 * (8.0 + 1.0) * h->n);
-  k_flag_count<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, h->counts);
-  k_scan_counts<<<1, 32, 0, h->stream>>>(nb, h->counts, h->offs, h->n_act_dev);
-  k_compact<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, h->offs, h->rowidx);
+  k_flag_count<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, tdev, h->counts);
+  k_scan_counts<<<1, 32, 0, h->stream>>>(nb, h->counts, h->offs, count_out ? count_out : h->n_act_dev);
+  k_compact<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, tdev, h->offs, h->rowidx);
   h->launches += 3;
   CHECK_LAUNCH(h);
   h->compacted = true;
@@ -689,26 +809,32 @@ static int compact_rows(sdn_handle* h, int kind, double t, double eps) {
 
 // exact top-k selection mask (value desc, global index asc); SMEM-resident
 // keys when they fit, else the global-memory radix select
-static int launch_topk(sdn_handle* h, int64_t n, int64_t k, const double* vals, const double* gidx, uint8_t* mask) {
+static int launch_topk(sdn_handle* h, int64_t n, int64_t k, const double* vals, const double* gidx, uint8_t* mask,
+                       double* thr = nullptr) {
   if (n <= TOPK_SMEM_MAX) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_topk_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, TOPK_SMEM_MAX * 8);
       attr = true;
     }
-    k_topk_select_smem<<<1, 1024, (size_t)std::max<int64_t>(n, 1) * 8, h->stream>>>((int)n, k, vals, gidx, mask);
+    k_topk_select_smem<<<1, 1024, (size_t)std::max<int64_t>(n, 1) * 8, h->stream>>>((int)n, k, vals, gidx, mask,
+                                                                                     thr);
   } else {
-    k_topk_select<<<1, 1024, 0, h->stream>>>(n, k, vals, gidx, mask);
+    k_topk_select<<<1, 1024, 0, h->stream>>>(n, k, vals, gidx, mask, thr);
   }
   h->launches++;
   CHECK_LAUNCH(h);
   return SDN_OK;
 }
 
-// local exact top-k (single rank): selection mask over the shard's Q
-static int select_local(sdn_handle* h, int64_t k) {
+// local exact top-k (single rank): selection mask over the shard's Q.  With
+// band_count, the rows within refinement error of the threshold are
+// re-evaluated in fp64 and reselected among themselves.
+static int select_local(sdn_handle* h, int64_t k, int* band_count = nullptr) {
+  const bool refine = band_count && !h->no_refine;
   { ProfScope ps(h, PC_SELECT, 0.0, 8.0 * 8.0 * h->n);
-  TRY(launch_topk(h, h->n, k, h->Q, nullptr, h->sel)); }
+  TRY(launch_topk(h, h->n, k, h->Q, nullptr, h->sel, refine ? h->thr_dev : nullptr)); }
+  if (refine) TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, band_count, h->sel));
   TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
   h->selected = true;
   return SDN_OK;
@@ -804,16 +930,82 @@ static int finish_host(sdn_handle* h, const sdn_risk& r, const double* st, const
                       : r.kind == SDN_RISK_CVAR_SMOOTH ? (int64_t)st[5] : (int64_t)n;
     res->q_mean = qmean;
     res->q_var = qvar;
+    res->n_refined = 0;
   }
   return SDN_OK;
 }
 
+// side-stream buffers for overlapped exact-CVaR selections (sdn_eval_multi)
+static int ensure_side(sdn_handle* h, int n_exact) {
+  if (!h->side) {
+    CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
+    const int nb1024 = (int)cdiv(h->cap, 1024);
+    int rc;
+    if ((rc = dalloc(h, &h->Qx, h->cap))) return rc;
+    if ((rc = dalloc(h, &h->x_counts, nb1024))) return rc;
+    if ((rc = dalloc(h, &h->x_offs, nb1024))) return rc;
+  }
+  while ((int)h->x_rowidx.size() < n_exact) {
+    int* r = nullptr;
+    int* c = nullptr;
+    int rc;
+    if ((rc = dalloc(h, &r, h->cap))) return rc;
+    if ((rc = dalloc(h, &c, 1))) return rc;
+    h->x_rowidx.push_back(r);
+    h->x_nact.push_back(c);
+  }
+  return SDN_OK;
+}
+
+// enqueue on the side stream with the side copies of Q and the compaction
+// scratch (the helpers below read these handle fields)
+struct SideScope {
+  sdn_handle* h;
+  cudaStream_t s0;
+  double* Qmain;
+  int *c0, *o0, *r0, *n0;
+  int g0;
+  explicit SideScope(sdn_handle* h_) : h(h_), s0(h_->stream), Qmain(h_->Q), c0(h_->counts), o0(h_->offs),
+                                       r0(h_->rowidx), n0(h_->n_act_dev), g0(h_->ref_grid) {
+    h->stream = h->side;
+    h->Q = h->Qx;
+    h->counts = h->x_counts;
+    h->offs = h->x_offs;
+    h->ref_grid = SDN_SIDE_SMS;
+  }
+  ~SideScope() {
+    h->stream = s0;
+    h->Q = Qmain;
+    h->counts = c0;
+    h->offs = o0;
+    h->rowidx = r0;
+    h->n_act_dev = n0;
+    h->ref_grid = g0;
+  }
+};
+
+// refined-row count of a risk from the band log (read back with the
+// results): smoothed CVaR -> the forward window (slot 0), exact CVaR -> its
+// threshold band (exact_slot, -1 = none); > ref_rows means skipped (negative)
+static int64_t refined_count(sdn_handle* h, const sdn_risk& r, int exact_slot) {
+  if (h->no_refine || !h->ref_ok) return 0;
+  int64_t v = 0;
+  if (r.kind == SDN_RISK_CVAR_SMOOTH) v = h->hband[0];
+  else if (r.kind == SDN_RISK_CVAR_EXACT && exact_slot > 0) v = h->hband[exact_slot];
+  return v > h->ref_rows ? -v : v;
+}
+
 static int eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
-                       double* grad_z) {
+                       double* grad_z, int exact_slot = -1) {
   CU(cudaMemcpyAsync(h->hstats, stats_dev, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaMemcpyAsync(h->hpart, partial_dev, sizeof(double) * h->plen(), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaMemcpyAsync(h->hband, h->band_log, sizeof(int) * 2, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  return finish_host(h, h->risk, h->hstats, h->hpart, res, grad_z);
+  TRY(finish_host(h, h->risk, h->hstats, h->hpart, res, grad_z));
+  res->n_refined = refined_count(h, h->risk, exact_slot);
+  return SDN_OK;
 }
 
 extern "C" {
@@ -827,10 +1019,10 @@ int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* r
   TRY(eval_forward(h, z, risk, h->stats_loc, risk->need_grad != 0));
   if (risk->kind == SDN_RISK_CVAR_EXACT) {
     h->kk = std::max(ceil_count((1.0 - risk->beta) * (double)h->n), 1);   // riskopt.py:80
-    TRY(select_local(h, h->kk));
+    TRY(select_local(h, h->kk, h->band_log + 1));
   }
   TRY(eval_backward(h, h->stats_loc, h->partial_loc));
-  TRY(eval_finish(h, h->stats_loc, h->partial_loc, res, grad_z));
+  TRY(eval_finish(h, h->stats_loc, h->partial_loc, res, grad_z, 1));
   if (cvar_idx && risk->kind == SDN_RISK_CVAR_EXACT) {
     std::vector<int> idx(h->kk);
     CU(cudaMemcpy(idx.data(), h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost));
@@ -872,31 +1064,102 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     CU(cudaHostAlloc((void**)&h->hpart_multi, sizeof(double) * h->multi_cap * plen, 0));
     CU(cudaHostAlloc((void**)&h->hidx, sizeof(int) * h->hidx_cap, 0));
   }
+  if (n_risks + 1 > h->band_cap) {
+    int* bl = nullptr;
+    int* hb = nullptr;
+    CU(cudaMalloc(&bl, sizeof(int) * (n_risks + 1)));
+    CU(cudaHostAlloc((void**)&hb, sizeof(int) * (n_risks + 1), 0));
+    h->allocs.push_back(bl);
+    if (h->hband) cudaFreeHost(h->hband);
+    h->band_log = bl;                // (the old block stays in allocs until destroy)
+    h->hband = hb;
+    h->band_cap = n_risks + 1;
+  }
   TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad != 0));
+  // CVaR index offsets in risk order
+  std::vector<int64_t> koff(n_risks, -1), kks(n_risks, 0);
   int64_t off = 0;
-  std::vector<int64_t> koff(n_risks, -1);
-  for (int i = 0; i < n_risks; ++i) {
-    h->risk = risks[i];
-    h->compacted = false;
-    h->selected = false;
+  int n_exact = 0;
+  for (int i = 0; i < n_risks; ++i)
     if (risks[i].kind == SDN_RISK_CVAR_EXACT) {
-      h->kk = std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);
-      TRY(select_local(h, h->kk));
-    }
-    TRY(eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen));
-    if (cvar_idx && risks[i].kind == SDN_RISK_CVAR_EXACT) {
-      CU(cudaMemcpyAsync(h->hidx + off, h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream));
+      kks[i] = std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);   // riskopt.py:80
       koff[i] = off;
-      off += h->kk;
+      off += kks[i];
+      ++n_exact;
+    }
+  // Overlap: the exact-CVaR selections (top-k, fp64 refinement of the
+  // threshold band, compaction) only read Q, so they run on the side stream
+  // -- on a copy Qx, over SDN_SIDE_SMS SMs kept free of the persistent GEMMs --
+  // while the other risks' reverse sweeps run on the main stream.  Every
+  // exact sweep waits for the whole side chain, so results do not depend on
+  // the interleaving.  (Profiling runs serialise: its class timers are
+  // stream-ordered.)
+  const bool overlap = n_exact > 0 && n_exact < n_risks && !h->prof;
+  if (overlap) {
+    TRY(ensure_side(h, n_exact));
+    CU(cudaEventRecord(h->ev_fwd, h->stream));
+    CU(cudaStreamWaitEvent(h->side, h->ev_fwd, 0));
+    {
+      SideScope ss(h);
+      CU(cudaMemcpyAsync(h->Q, ss.Qmain, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->stream));
+      for (int i = 0, e = 0; i < n_risks; ++i) {
+        if (risks[i].kind != SDN_RISK_CVAR_EXACT) continue;
+        h->risk = risks[i];
+        h->rowidx = h->x_rowidx[e];
+        h->n_act_dev = h->x_nact[e];
+        TRY(select_local(h, kks[i], h->band_log + 1 + i));
+        ++e;
+      }
+    }
+    CU(cudaEventRecord(h->ev_side, h->side));
+    h->sm_avail = h->num_sms - SDN_SIDE_SMS;
+  }
+  for (int pass = 0; pass < (overlap ? 2 : 1); ++pass) {
+    if (overlap && pass == 1) {
+      h->sm_avail = h->num_sms;
+      CU(cudaStreamWaitEvent(h->stream, h->ev_side, 0));
+    }
+    for (int i = 0, e = 0; i < n_risks; ++i) {
+      const bool exact = risks[i].kind == SDN_RISK_CVAR_EXACT;
+      if (overlap && (exact != (pass == 1))) { e += exact; continue; }
+      h->risk = risks[i];
+      h->compacted = false;
+      h->selected = false;
+      double* Qm = h->Q;
+      int* rm = h->rowidx;
+      int* nm = h->n_act_dev;
+      if (exact) {
+        h->kk = kks[i];
+        if (overlap) {                       // selection made on the side stream
+          h->Q = h->Qx;
+          h->rowidx = h->x_rowidx[e];
+          h->n_act_dev = h->x_nact[e];
+          h->compacted = h->selected = true;
+        } else {
+          TRY(select_local(h, h->kk, h->band_log + 1 + i));
+        }
+      }
+      int rc = eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen);
+      if (rc == SDN_OK && cvar_idx && exact &&
+          cudaMemcpyAsync(h->hidx + koff[i], h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream))
+        rc = fail(SDN_ERR_CUDA, "index download failed");
+      h->Q = Qm;
+      h->rowidx = rm;
+      h->n_act_dev = nm;
+      if (rc) return rc;
+      e += exact;
     }
   }
   CU(cudaMemcpyAsync(h->hstats, h->stats_loc, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaMemcpyAsync(h->hpart_multi, h->partial_multi, sizeof(double) * n_risks * plen, cudaMemcpyDeviceToHost,
                      h->stream));
+  CU(cudaMemcpyAsync(h->hband, h->band_log, sizeof(int) * (n_risks + 1), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  for (int i = 0; i < n_risks; ++i)
+  for (int i = 0; i < n_risks; ++i) {
     TRY(finish_host(h, risks[i], h->hstats, h->hpart_multi + (size_t)i * plen, &res[i],
                     grads ? grads + (size_t)i * h->d_z : nullptr));
+    res[i].n_refined = refined_count(h, risks[i], 1 + i);
+  }
   if (cvar_idx)
     for (int64_t j = 0; j < off; ++j) cvar_idx[j] = h->goff + h->hidx[j];
   return SDN_OK;
@@ -965,7 +1228,7 @@ int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, 
   TRY(ensure_cand(h, nc));
   k_unpack_candidates<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(n_ranks, k, all_cand_dev, h->cand_vals,
                                                                       h->cand_gidx);
-  TRY(launch_topk(h, nc, k, h->cand_vals, h->cand_gidx, h->cand_mask));
+  TRY(launch_topk(h, nc, k, h->cand_vals, h->cand_gidx, h->cand_mask, h->thr_dev));
   CU(cudaMemsetAsync(h->sel, 0, std::max<int64_t>(h->n, 1), h->stream));
   k_scatter_selection<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(nc, h->cand_mask, h->cand_gidx, h->goff,
                                                                       h->n, h->sel);
@@ -974,6 +1237,20 @@ int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, 
   TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
   h->kk = k;
   h->selected = true;
+  return SDN_OK;
+}
+
+// multi-rank exact CVaR: after a global selection (sdn_eval_select, which
+// leaves the global threshold on the device), re-evaluate this shard's rows
+// within refinement error of it in fp64 (Q updated in place).  The caller
+// then repeats candidates -> all-gather -> select on the refined Q.
+int sdn_eval_refine_band(sdn_handle* h) {
+  if (!h) return fail(SDN_ERR_ARG, "null handle");
+  if (!h->fwd_done || !h->selected) return fail(SDN_ERR_STATE, "eval_select first");
+  CU(cudaSetDevice(h->device));
+  if (h->no_refine || h->n == 0) return SDN_OK;
+  TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, h->band_log + 1));
+  h->selected = false;
   return SDN_OK;
 }
 
@@ -1241,9 +1518,12 @@ int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubi
     std::vector<float> c32(r_u);
     for (int j = 0; j < r_u; ++j) c32[j] = (float)cd[j];
     cudaMemcpy(h->cdec, c32.data(), sizeof(float) * r_u, cudaMemcpyHostToDevice);
+    if (!h->c64dec) CU(cudaMalloc(&h->c64dec, sizeof(double) * r_u));
+    cudaMemcpy(h->c64dec, cd.data(), sizeof(double) * r_u, cudaMemcpyHostToDevice);
   }
   cudaFree(Um);
-  cudaFree(K64);
+  if (h->K64) cudaFree(h->K64);
+  h->K64 = K64;                 // kept (fp64) for the refinement chain's decoded QoI
   if (rc) return rc;
   CU(cudaGetLastError());
   h->d_u = d_u;
@@ -1361,9 +1641,9 @@ int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k, i
   CU(cudaMemcpyAsync(v, values, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      h->stream));
   if (int rc = launch_topk(h, n, k, v, nullptr, mask)) { cudaFree(v); cudaFree(mask); return rc; }
-  k_flag_count<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, cnt);
+  k_flag_count<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, nullptr, cnt);
   k_scan_counts<<<1, 32, 0, h->stream>>>(nb, cnt, offs, na);
-  k_compact<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, offs, ri);
+  k_compact<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, nullptr, offs, ri);
   h->launches += 4;
   std::vector<int> hi(k);
   cudaError_t e = cudaMemcpyAsync(hi.data(), ri, sizeof(int) * k, cudaMemcpyDeviceToHost, h->stream);

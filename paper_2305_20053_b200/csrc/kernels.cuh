@@ -11,7 +11,8 @@
 namespace sdn {
 
 enum RiskKind : int { RISK_MEAN = 0, RISK_CVAR_SMOOTH = 1, RISK_MEANVAR = 2, RISK_CVAR_EXACT = 3,
-                      RISK_UNIT = 100 /* per-sample G: w_i = 1 */ };
+                      RISK_UNIT = 100 /* per-sample G: w_i = 1 */,
+                      RISK_BAND = 101, RISK_BAND_EXACT = 102 /* refinement band flags */ };
 
 constexpr int STATS_LEN = 8;   // [n, sum q~, sum q~^2, sum splus, sum d1, n_active, 0, 0]
 
@@ -20,13 +21,16 @@ constexpr int STATS_LEN = 8;   // [n, sum q~, sum q~^2, sum splus, sum d1, n_act
 // one warp per output c, lanes over k (row c of Pz is contiguous)
 __global__ void __launch_bounds__(256)
 k_zbias(int h1, int d_z, const double* __restrict__ Pz, const double* __restrict__ z,
-        const float* __restrict__ b1, float* __restrict__ zb) {
+        const float* __restrict__ b1, float* __restrict__ zb, double* __restrict__ zb64 = nullptr) {
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= h1) return;
   double s = 0.0;
   for (int k = lane; k < d_z; k += 32) s += Pz[(int64_t)c * d_z + k] * z[k];
   s = warp_sum(s);
-  if (lane == 0) zb[c] = (float)(s + (double)b1[c]);
+  if (lane == 0) {
+    zb[c] = (float)(s + (double)b1[c]);
+    if (zb64) zb64[c] = s + (double)b1[c];
+  }
 }
 
 // X = [m_r, z_row, 0-pad]  (forward_batch / jacobian rows with per-row z)
@@ -94,6 +98,47 @@ k_sum_rows(int nb, int w, const double* __restrict__ part, double* __restrict__ 
   if (lane == 0) out[f] = s;
 }
 
+// ---- Q refinement band (the fp64 re-evaluation is refine.cuh).
+// REFINE_REL bounds the chain's Q error with ~6x margin over the largest
+// measured (1.7e-5 relative at c3).
+constexpr double REFINE_REL = 1e-4;
+constexpr int REFINE_ROWS = 4096;     // band rows per evaluation (k_refine reselect: <= 16 x 256)
+SDN_DEV bool in_band(double q, double t, double eps) {       // smoothed CVaR window
+  double d = REFINE_REL * fabs(q) + 1e-300;
+  double x = q - t;
+  return x >= -d && x <= eps + d;
+}
+SDN_DEV bool in_band_exact(double q, double thr) {            // exact-CVaR threshold
+  return fabs(q - thr) <= 2.0 * REFINE_REL * fabs(q) + 1e-300 || q != q || thr != thr;
+}
+
+// block moments of k_qoi recomputed from Q (after refinement)
+__global__ void __launch_bounds__(256)
+k_moments(int64_t n, const double* __restrict__ Q, double shift, double t, double eps,
+          double* __restrict__ part) {
+  __shared__ double sp[8][6];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  // same row -> (block, warp) assignment and per-lane-0 order as k_qoi
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
+    if (lane == 0) {
+      double q = Q[i], qs = q - shift, x = q - t;
+      double d1 = splus_d1_d(x, eps);
+      acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
+      acc[3] += splus_d(x, eps); acc[4] += d1; acc[5] += (d1 > 0.0) ? 1.0 : 0.0;
+    }
+  }
+  if (lane == 0)
+    for (int f = 0; f < 6; ++f) sp[warp][f] = acc[f];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += sp[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = s;
+  }
+  if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;
+}
+
 // sample weight w_i of the risk functional:
 //   mean: 1/n; meanvar: (1 + 2 beta (Q_i - Qbar))/n; smoothed CVaR (riskopt.py:238-241):
 //   splus'(Q_i - t)/(n (1-beta)); exact CVaR: 1/k on the selection; unit: 1.
@@ -113,14 +158,22 @@ SDN_DEV double sample_weight(int kind, double q, const double* st, double shift,
 }
 
 // active-row flags for compaction: smoothed CVaR -> splus'(Q - t) > 0;
-// exact CVaR -> selection mask.  Per 1024-row block: count.
+// exact CVaR -> selection mask; RISK_BAND -> Q within the refinement band.
+SDN_DEV bool row_flag(int kind, const double* Q, const uint8_t* sel, int64_t i, double t, double eps,
+                      const double* tdev) {
+  if (kind == RISK_CVAR_EXACT) return sel[i] != 0;
+  if (kind == RISK_BAND) return in_band(Q[i], t, eps);
+  if (kind == RISK_BAND_EXACT) return in_band_exact(Q[i], *tdev);
+  return splus_d1_d(Q[i] - t, eps) > 0.0;
+}
+// Per 1024-row block: count.
 __global__ void __launch_bounds__(1024)
 k_flag_count(int64_t n, int kind, const double* __restrict__ Q, const uint8_t* __restrict__ sel,
-             double t, double eps, int* __restrict__ counts) {
+             double t, double eps, const double* __restrict__ tdev, int* __restrict__ counts) {
   __shared__ int wc[32];
   int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
   bool f = false;
-  if (i < n) f = (kind == RISK_CVAR_EXACT) ? (sel[i] != 0) : (splus_d1_d(Q[i] - t, eps) > 0.0);
+  if (i < n) f = row_flag(kind, Q, sel, i, t, eps, tdev);
   unsigned b = __ballot_sync(0xffffffffu, f);
   if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = __popc(b);
   __syncthreads();
@@ -143,11 +196,12 @@ __global__ void k_scan_counts(int nb, const int* __restrict__ counts, int* __res
 // ordered compaction: rowidx[offs[b] + rank-in-block] = i for flagged rows
 __global__ void __launch_bounds__(1024)
 k_compact(int64_t n, int kind, const double* __restrict__ Q, const uint8_t* __restrict__ sel,
-          double t, double eps, const int* __restrict__ offs, int* __restrict__ rowidx) {
+          double t, double eps, const double* __restrict__ tdev, const int* __restrict__ offs,
+          int* __restrict__ rowidx) {
   __shared__ int wbase[32];
   int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
   bool f = false;
-  if (i < n) f = (kind == RISK_CVAR_EXACT) ? (sel[i] != 0) : (splus_d1_d(Q[i] - t, eps) > 0.0);
+  if (i < n) f = row_flag(kind, Q, sel, i, t, eps, tdev);
   unsigned b = __ballot_sync(0xffffffffu, f);
   int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) wbase[warp] = __popc(b);
@@ -278,7 +332,7 @@ SDN_DEV void hist_add(unsigned* hist, bool m, unsigned d) {
 // marks padding (gidx < 0 -> never selected).  Output: mask (n).
 __global__ void __launch_bounds__(1024)
 k_topk_select(int64_t n, int64_t k, const double* __restrict__ vals, const double* __restrict__ gidx,
-              uint8_t* __restrict__ mask) {
+              uint8_t* __restrict__ mask, double* __restrict__ thr) {
   __shared__ unsigned hist[256];
   __shared__ uint64_t s_prefix;
   __shared__ long long s_krem;
@@ -320,6 +374,7 @@ k_topk_select(int64_t n, int64_t k, const double* __restrict__ vals, const doubl
   }
   const uint64_t T = s_prefix;
   const long long need = s_krem;       // how many threshold-equal keys to take
+  if (thr && tid == 0) *thr = dkey_inv(T);
   if (tid == 0) s_run = 0;
   __syncthreads();
   // rows in ascending global index order: positions are index-ordered for
@@ -353,7 +408,7 @@ constexpr int TOPK_SMEM_MAX = 24576;   // 192 KB of uint64 keys
 
 __global__ void __launch_bounds__(1024)
 k_topk_select_smem(int n, int64_t k, const double* __restrict__ vals, const double* __restrict__ gidx,
-                   uint8_t* __restrict__ mask) {
+                   uint8_t* __restrict__ mask, double* __restrict__ thr) {
   extern __shared__ uint64_t keys[];
   __shared__ unsigned hist[256];
   __shared__ uint64_t s_prefix;
@@ -408,6 +463,7 @@ k_topk_select_smem(int n, int64_t k, const double* __restrict__ vals, const doub
   }
   const uint64_t T = s_prefix;
   const long long need = s_krem;
+  if (thr && tid == 0) *thr = dkey_inv(T);
   if (tid == 0) s_run = 0;
   __syncthreads();
   for (int base = 0; base < n; base += blockDim.x) {

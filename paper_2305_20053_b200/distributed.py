@@ -140,9 +140,14 @@ class ShardedObjective:
             if r["kind"] == "cvar_exact":
                 k = cvar_count(self.n_global, r.get("beta", 0.95))
                 cand = self.b.new_buffer(2 * k)
-                self.b.phase_candidates(k, cand)
-                allc = self.comm.allgather(cand)
-                self.b.phase_select(allc.contiguous(), self.comm.world, k)
+                for rnd in range(2):
+                    # round 2 reselects after the rows near the global
+                    # threshold were re-evaluated in fp64 (sdn_eval_refine_band)
+                    self.b.phase_candidates(k, cand)
+                    allc = self.comm.allgather(cand)
+                    self.b.phase_select(allc.contiguous(), self.comm.world, k)
+                    if rnd == 0:
+                        self.b.phase_refine_band()
             partial = self.b.new_buffer(self.b.partial_len())
             self.b.phase_backward(stats, partial)
             self.comm.allreduce_(partial)

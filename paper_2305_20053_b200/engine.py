@@ -35,6 +35,7 @@ class EvalResult:
     n_selected: int
     q_mean: float
     q_var: float
+    n_refined: int = 0             # rows re-evaluated in exact fp32 (smoothed CVaR, TC chains)
 
 
 class Engine:
@@ -158,7 +159,7 @@ class Engine:
         return EvalResult(value=res.value, grad_z=grad if need_grad else None,
                           grad_t=res.grad_t if kind == "cvar" else None, idx=idx,
                           n_samples=int(res.n_samples), n_selected=int(res.n_selected),
-                          q_mean=res.q_mean, q_var=res.q_var)
+                          q_mean=res.q_mean, q_var=res.q_var, n_refined=int(res.n_refined))
 
     def eval_samples(self, z, qoi: str = "reduced", need_grad: bool = True):
         z = _f64(z)
@@ -227,7 +228,8 @@ class Engine:
             out.append(EvalResult(value=res[i].value, grad_z=grads[i] if r.get("need_grad", True) else None,
                                   grad_t=res[i].grad_t if r["kind"] == "cvar" else None, idx=sel,
                                   n_samples=int(res[i].n_samples), n_selected=int(res[i].n_selected),
-                                  q_mean=res[i].q_mean, q_var=res[i].q_var))
+                                  q_mean=res[i].q_mean, q_var=res[i].q_var,
+                                  n_refined=int(res[i].n_refined)))
         return out
 
     # -- instrumentation ---------------------------------------------------------------
@@ -260,9 +262,27 @@ class Engine:
         check(lib.sdn_eval_select(self.h, C.c_void_p(all_cand_dev.data_ptr()), int(n_ranks), int(k)),
               "sdn_eval_select")
 
+    def phase_refine_band(self):
+        check(lib.sdn_eval_refine_band(self.h), "sdn_eval_refine_band")
+
     def phase_set_risk(self, risk: _lib.Risk):
         self._phase_risk = risk
         check(lib.sdn_eval_set_risk(self.h, C.byref(risk)), "sdn_eval_set_risk")
+
+    def last_q(self) -> np.ndarray:
+        """Per-sample Q of the last evaluation as the engine used it (after
+        Q refinement), copied to the host (sdn_last_q)."""
+        import torch
+        ptr, n = C.c_void_p(), C.c_int64()
+        check(lib.sdn_last_q(self.h, C.byref(ptr), C.byref(n)), "sdn_last_q")
+        self.synchronize()
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(n.value),), "typestr": "<f8",
+                                        "data": (int(ptr.value or 0), False), "version": 3}
+        if n.value == 0:
+            return np.zeros(0)
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}").cpu().numpy().copy()
 
     def new_buffer(self, n: int):
         """float64 exchange buffer on this engine's device (torch tensor)."""

@@ -73,6 +73,9 @@ class OracleBackend:
         self.sel = np.sort(top[(top >= 0) & (top < self.n)])
         self.k = k
 
+    def phase_refine_band(self):
+        pass                       # Q is already float64 here
+
     def phase_backward(self, stats, partial):
         st = stats.numpy()
         n = st[0]

@@ -36,10 +36,9 @@ def test_ns_shapes_meanvar_and_exact_cvar(name):
     o = ref.saa_objective(Qo, Go, p.z, ref.Risk("meanvar", beta=1.0, alpha=1e-2))
     assert abs(res[0].value - o[0]) <= RTOL * abs(o[0])
     assert _rel(res[0].grad_z, o[1]) <= RTOL
-    # exact CVaR: indices bit-exact on the GPU's own Q; value/grad on that selection
-    Qg, _ = eng.eval_samples(p.z, need_grad=False)
-    np.testing.assert_array_equal(np.sort(res[1].idx), np.sort(ref.cvar_select(Qg, 0.99)))
-    sel = res[1].idx
+    # exact CVaR: indices bit-exact vs the fp64 oracle; value/grad on that selection
+    sel = ref.cvar_select(Qo, 0.99)
+    np.testing.assert_array_equal(np.sort(res[1].idx), np.sort(sel))
     v = Qo[sel].mean() + 1e-2 * float(p.z.astype(np.float64) @ p.z)
     g = Go[sel].mean(0) + 2e-2 * p.z.astype(np.float64)
     assert abs(res[1].value - v) <= RTOL * abs(v)
@@ -55,6 +54,23 @@ def test_c3_smoothed_cvar_simt_exact_fp32():
     t = ref.mc_var(Qo, 0.95)
     r = eng.eval(p.z, "cvar", beta=0.95, eps=1e-4, t=t)
     o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar", beta=0.95, eps=1e-4), t)
+    assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+    assert _rel(r.grad_z, o[1]) <= RTOL
+    assert abs(r.grad_t - o[2]) <= 1e-6
+
+
+@pytest.mark.parametrize("n", [2048, 8192])
+def test_c3_smoothed_cvar_tc_refined(n):
+    """Same risk on the default tensor-core chain: the rows whose bf16x3 Q
+    lies within error of the splus' window are re-evaluated in exact fp32
+    (Q refinement), so the 1e-4 tolerance holds at eps = 1e-4."""
+    p, eng = _setup("c3", n, gemm="tc")
+    form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=form)
+    t = ref.mc_var(Qo, 0.95)
+    r = eng.eval(p.z, "cvar", beta=0.95, eps=1e-4, t=t)
+    o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar", beta=0.95, eps=1e-4), t)
+    assert 1 <= r.n_refined <= max(8, n // 100)
     assert abs(r.value - o[0]) <= RTOL * abs(o[0])
     assert _rel(r.grad_z, o[1]) <= RTOL
     assert abs(r.grad_t - o[2]) <= 1e-6
@@ -86,9 +102,11 @@ def test_c4_full_n_properties():
     eng.set_samples(p.m_r)
     r = eng.eval(p.z, "cvar_exact", beta=0.99)
     assert r.idx.size == 1311                      # ceil(0.01 * 131072)
+    Qr = eng.last_q()                              # Q as used (threshold band refined in fp64)
+    assert r.n_refined >= 1
+    np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qr, 0.99)))
+    assert abs(r.value - Qr[r.idx].mean()) <= 1e-9 * abs(r.value)
     Q, G = eng.eval_samples(p.z)
-    np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Q, 0.99)))
-    assert abs(r.value - Q[r.idx].mean()) <= 1e-9 * abs(r.value)
     assert _rel(r.grad_z, G[r.idx].mean(0)) <= 1e-5
     # and a 2048-sample slice against the float64 oracle
     sl = slice(5000, 7048)
