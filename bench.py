@@ -216,6 +216,16 @@ def main():
     eng.set_samples(torch.from_numpy(p.m_r).cuda(), global_offset=rank * n_loc)   # resident in HBM
     risks = risks_for(cfg)
     z = p.z.astype(np.float64)
+    for d in risks:
+        if d["kind"] == "cvar":
+            # smoothed CVaR: t starts at the beta-VaR of Q(z0), as the reference's
+            # minimize initialises it (riskopt.py:295-297); rank 0's value for all
+            from paper_2305_20053_b200.api import mc_var
+            q0, _ = eng.eval_samples(z, need_grad=False)
+            tt = torch.tensor([mc_var(q0, d["beta"])], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.broadcast(tt, 0)
+            d["t"] = float(tt.item())
     sharded = None
     if world > 1:
         from paper_2305_20053_b200.distributed import ShardedObjective, TorchComm

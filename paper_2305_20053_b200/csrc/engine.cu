@@ -20,8 +20,9 @@
 #include "gemm_tc.cuh"
 #include "refine.cuh"
 
-// SMs left to side-stream work while the main stream's GEMMs run (sdn_eval_multi)
-constexpr int SDN_SIDE_SMS = 8;
+// SMs left to side-stream work while the main stream's GEMMs run (sdn_eval_multi).
+// 40 measured best at c2 (34-48 plateau; the side chain is latency-bound).
+constexpr int SDN_SIDE_SMS_DEFAULT = 40;
 
 #include <algorithm>
 #include <cmath>
@@ -58,6 +59,20 @@ static int fail(int code, const std::string& msg) {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int pad4(int x) { return (x + 3) & ~3; }
+
+// reverse-sweep work buffers; a second set (sized for the CVaR tail) lets the
+// exact-CVaR sweep run on the side stream while the main set is in use
+struct SweepBufs {
+  float* E = nullptr;           // seeds (rows x r_u)
+  float* G = nullptr;           // residual gradient stream (rows x maxw)
+  float* Ub[2] = {nullptr, nullptr};
+  double* tsum = nullptr;       // fused column-sum partials (TC chains)
+  double* cpart = nullptr;      // SIMT column-sum partials (crb x maxw)
+  double* csum = nullptr;
+  TcOperand act[2];             // bf16x3 split of the sweep operand (ping-pong)
+  TcOperand seed;
+  int64_t rows = 0;
+};
 
 struct sdn_handle {
   // ---- configuration
@@ -176,6 +191,10 @@ struct sdn_handle {
   int* x_offs = nullptr;
   std::vector<int*> x_rowidx, x_nact;
   int sm_avail = 0;             // SMs the persistent GEMMs may use
+  int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS
+  bool no_overlap = false;               // env SDN_NO_OVERLAP=1
+  SweepBufs sw0, sw1;           // main / side sweep buffers
+  SweepBufs* sw = &sw0;
   int* band_log = nullptr;      // band row counts: [0] forward window, [1 + i] exact risk i
   int* hband = nullptr;         // pinned mirror
   int band_cap = 0;
@@ -368,35 +387,35 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
 static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const int* rowidx,
                         float** u0_out, int64_t rows_hint, bool want_u0 = false, int64_t* nrb = nullptr) {
   const int L = h->L;
-  if (L == 1) { *u0_out = h->E; return SDN_OK; }
+  if (L == 1) { *u0_out = h->sw->E; return SDN_OK; }
   const bool tcc = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
   const int route = tcc ? 1 : 0;
   int cur = 0;
   for (int l = L - 1; l >= 1; --l) {
     // GEMM l: g_{l-1} = (res[l] ? g_l : 0) + u_l W_l, u_{l-1} = D_{l-1} g_{l-1}
     const int K = h->w[l + 1], N = h->w[l];
-    const float* A = (l == L - 1) ? h->E : h->Ub[cur];
-    const TcOperand* tA = !tcc ? nullptr : (l == L - 1) ? &h->tcw.seed : &h->tcw.act[cur];
+    const float* A = (l == L - 1) ? h->sw->E : h->sw->Ub[cur];
+    const TcOperand* tA = !tcc ? nullptr : (l == L - 1) ? &h->sw->seed : &h->sw->act[cur];
     const TcOperand* tB = tcc ? &h->tcw.bwd[l] : nullptr;
-    const float* resid = (l < L - 1 && h->res[l]) ? h->G : nullptr;
+    const float* resid = (l < L - 1 && h->res[l]) ? h->sw->G : nullptr;
     h->pcls = PC_BWD_GEMM;
     h->prows = rows_hint;
     if (l == 1 && tcc && !want_u0) {
-      EpiBwdSum e{resid, h->D[0], (int64_t)N, rowidx, (int64_t)N, h->tsum, (int64_t)N};
+      EpiBwdSum e{resid, h->D[0], (int64_t)N, rowidx, (int64_t)N, h->sw->tsum, (int64_t)N};
       TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, e, tB, tA, route)));
       *u0_out = nullptr;
       if (nrb) *nrb = cdiv(nmax, 128) * 4;
       return SDN_OK;
     }
     const bool last = (l == 1);
-    EpiBwd e{resid, h->res[l - 1] ? h->G : nullptr, h->D[l - 1], (int64_t)N, rowidx,
-             (!tcc || last) ? h->Ub[1 - cur] : nullptr, (int64_t)N};
-    TcEpiSplit split = (tcc && !last) ? TcEpiSplit{&h->tcw.act[1 - cur]} : TcEpiSplit{nullptr};
+    EpiBwd e{resid, h->res[l - 1] ? h->sw->G : nullptr, h->D[l - 1], (int64_t)N, rowidx,
+             (!tcc || last) ? h->sw->Ub[1 - cur] : nullptr, (int64_t)N};
+    TcEpiSplit split = (tcc && !last) ? TcEpiSplit{&h->sw->act[1 - cur]} : TcEpiSplit{nullptr};
     TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, TcChain<EpiBwd>{e, split}, tB, tA,
                             route)));
     cur = 1 - cur;
   }
-  *u0_out = h->Ub[cur];
+  *u0_out = h->sw->Ub[cur];
   return SDN_OK;
 }
 
@@ -522,10 +541,25 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
       cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), 0) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
   { const char* e = getenv("SDN_NO_REFINE"); h->no_refine = e && e[0] == '1'; }
+  { const char* e = getenv("SDN_NO_OVERLAP"); h->no_overlap = e && e[0] == '1'; }
+  { const char* e = getenv("SDN_SIDE_SMS");
+    if (e) h->side_sms = std::max(1, std::min(atoi(e), h->num_sms / 2)); }
   h->tcw.enabled = false;
   if (h->gemm != SDN_GEMM_SIMT) {
     if ((rc = tc_alloc(h, h->tcw))) return bail(rc);
   }
+  h->sw0.E = h->E;
+  h->sw0.G = h->G;
+  h->sw0.Ub[0] = h->Ub[0];
+  h->sw0.Ub[1] = h->Ub[1];
+  h->sw0.tsum = h->tsum;
+  h->sw0.cpart = h->cpart;
+  h->sw0.csum = h->csum;
+  h->sw0.act[0] = h->tcw.act[0];
+  h->sw0.act[1] = h->tcw.act[1];
+  h->sw0.seed = h->tcw.seed;
+  h->sw0.rows = cap;
+  h->sw = &h->sw0;
   *out = h;
   return SDN_OK;
 }
@@ -862,15 +896,18 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
     CHECK_LAUNCH(h);
     return SDN_OK;
   }
-  const int64_t nmax = h->n;
+  // exact CVaR: k selected rows (device count <= k on a multi-rank shard)
+  const int64_t nmax = exact ? std::min<int64_t>(h->kk, h->n) : h->n;
+  SweepBufs& sw = *h->sw;
+  if (nmax > sw.rows) return fail(SDN_ERR_STATE, "sweep buffers too small");
   if (nmax > 0) {
     const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nmax, 8), 4 * h->num_sms));
     const bool tcs = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
     { ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
     k_seed<<<sg, 256, 0, h->stream>>>(nmax, nact, rowidx, h->r_u, h->Y, dec ? h->KPhi : nullptr,
                                       dec ? h->cdec : h->c, h->ostd, h->Q, stats_dev, kind, h->shift, r.beta,
-                                      eps, r.t, kinv, h->E, tcs ? h->tcw.seed.hi : nullptr,
-                                      tcs ? h->tcw.seed.lo : nullptr); }
+                                      eps, r.t, kinv, sw.E, tcs ? sw.seed.hi : nullptr,
+                                      tcs ? sw.seed.lo : nullptr); }
     h->launches++;
     CHECK_LAUNCH(h);
     float* u0 = nullptr;
@@ -879,19 +916,19 @@ static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial
     if (u0) {
       dim3 cg((unsigned)cdiv(h->h1, 32), (unsigned)h->crb);
       { ProfScope ps(h, PC_COLSUM, 0.0, 0.0, rows_hint, 4.0 * h->h1);
-      k_colsum<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, h->cpart); }
+      k_colsum<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, sw.cpart); }
     } else {
       // tensor-core chain: the last GEMM left per-(tile, quarter) fp64 partials
       ProfScope ps(h, PC_COLSUM, 0.0, 8.0 * nrb * h->h1);
-      k_colsum64<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>((int)nrb, nact, h->h1, h->tsum,
-                                                                            h->csum);
+      k_colsum64<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>((int)nrb, nact, h->h1, sw.tsum,
+                                                                            sw.csum);
     }
     h->launches++;
   }
   ProfScope psf(h, PC_FINAL, 0.0, 8.0 * h->crb * h->h1);
   const bool summed = nmax > 0 && chain_tc(h, rows_hint >= 0 ? rows_hint : nmax) && h->L > 1;
   k_finalize_grad<<<(unsigned)cdiv(h->d_z, 8), 256, sizeof(double) * h->h1, h->stream>>>(
-      nmax > 0 ? (summed ? 1 : h->crb) : 0, h->h1, h->d_z, nmax > 0 ? (summed ? h->csum : h->cpart) : nullptr,
+      nmax > 0 ? (summed ? 1 : h->crb) : 0, h->h1, h->d_z, nmax > 0 ? (summed ? sw.csum : sw.cpart) : nullptr,
       h->PzT, h->rowidx, h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
   h->launches++;
   CHECK_LAUNCH(h);
@@ -936,13 +973,13 @@ static int finish_host(sdn_handle* h, const sdn_risk& r, const double* st, const
 }
 
 // side-stream buffers for overlapped exact-CVaR selections (sdn_eval_multi)
-static int ensure_side(sdn_handle* h, int n_exact) {
+static int ensure_side(sdn_handle* h, int n_exact, int64_t kmax) {
+  int rc;
   if (!h->side) {
     CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
     const int nb1024 = (int)cdiv(h->cap, 1024);
-    int rc;
     if ((rc = dalloc(h, &h->Qx, h->cap))) return rc;
     if ((rc = dalloc(h, &h->x_counts, nb1024))) return rc;
     if ((rc = dalloc(h, &h->x_offs, nb1024))) return rc;
@@ -950,11 +987,27 @@ static int ensure_side(sdn_handle* h, int n_exact) {
   while ((int)h->x_rowidx.size() < n_exact) {
     int* r = nullptr;
     int* c = nullptr;
-    int rc;
     if ((rc = dalloc(h, &r, h->cap))) return rc;
     if ((rc = dalloc(h, &c, 1))) return rc;
     h->x_rowidx.push_back(r);
     h->x_nact.push_back(c);
+  }
+  if (kmax > h->sw1.rows) {           // side sweep buffers for the CVaR tail
+    SweepBufs& b = h->sw1;
+    const int64_t rows = std::max<int64_t>(cdiv(kmax, 128) * 128, 128);
+    if ((rc = dalloc(h, &b.E, (size_t)rows * h->r_u))) return rc;
+    if ((rc = dalloc(h, &b.G, (size_t)rows * h->maxw))) return rc;
+    for (int i = 0; i < 2; ++i)
+      if ((rc = dalloc(h, &b.Ub[i], (size_t)rows * h->maxw))) return rc;
+    if ((rc = dalloc(h, &b.tsum, (size_t)cdiv(rows, 128) * 4 * h->maxw))) return rc;
+    if ((rc = dalloc(h, &b.cpart, (size_t)h->crb * h->maxw))) return rc;
+    if ((rc = dalloc(h, &b.csum, (size_t)h->maxw))) return rc;
+    if (h->tcw.enabled) {
+      for (int i = 0; i < 2; ++i)
+        if (tc_buf(h, h->tcw, b.act[i], rows, h->maxw)) return fail(SDN_ERR_NOMEM, "side sweep operands");
+      if (tc_buf(h, h->tcw, b.seed, rows, h->r_u)) return fail(SDN_ERR_NOMEM, "side sweep operands");
+    }
+    b.rows = rows;
   }
   return SDN_OK;
 }
@@ -966,14 +1019,16 @@ struct SideScope {
   cudaStream_t s0;
   double* Qmain;
   int *c0, *o0, *r0, *n0;
-  int g0;
+  int g0, a0;
   explicit SideScope(sdn_handle* h_) : h(h_), s0(h_->stream), Qmain(h_->Q), c0(h_->counts), o0(h_->offs),
-                                       r0(h_->rowidx), n0(h_->n_act_dev), g0(h_->ref_grid) {
+                                       r0(h_->rowidx), n0(h_->n_act_dev), g0(h_->ref_grid), a0(h_->sm_avail) {
     h->stream = h->side;
     h->Q = h->Qx;
     h->counts = h->x_counts;
     h->offs = h->x_offs;
-    h->ref_grid = SDN_SIDE_SMS;
+    h->ref_grid = h->side_sms;
+    h->sm_avail = h->side_sms;
+    h->sw = &h->sw1;
   }
   ~SideScope() {
     h->stream = s0;
@@ -983,6 +1038,8 @@ struct SideScope {
     h->rowidx = r0;
     h->n_act_dev = n0;
     h->ref_grid = g0;
+    h->sm_avail = a0;
+    h->sw = &h->sw0;
   }
 };
 
@@ -1087,16 +1144,19 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       off += kks[i];
       ++n_exact;
     }
-  // Overlap: the exact-CVaR selections (top-k, fp64 refinement of the
-  // threshold band, compaction) only read Q, so they run on the side stream
-  // -- on a copy Qx, over SDN_SIDE_SMS SMs kept free of the persistent GEMMs --
-  // while the other risks' reverse sweeps run on the main stream.  Every
-  // exact sweep waits for the whole side chain, so results do not depend on
-  // the interleaving.  (Profiling runs serialise: its class timers are
-  // stream-ordered.)
-  const bool overlap = n_exact > 0 && n_exact < n_risks && !h->prof;
+  // Overlap: each exact-CVaR risk (top-k, fp64 refinement of the threshold
+  // band, compaction, and its k-row reverse sweep) only reads Q and the
+  // forward's act' arrays, so it runs on the side stream -- on a copy Qx,
+  // with its own sweep buffers (sw1), over side_sms SMs kept free of the
+  // main stream's persistent GEMMs -- while the other risks' sweeps run on
+  // the main stream.  The two chains share no written buffer, so results do
+  // not depend on the interleaving.  (Profiling runs serialise: its class
+  // timers are stream-ordered.)
+  const bool overlap = n_exact > 0 && n_exact < n_risks && !h->prof && !h->no_overlap;
   if (overlap) {
-    TRY(ensure_side(h, n_exact));
+    int64_t kmax = 0;
+    for (int i = 0; i < n_risks; ++i) kmax = std::max(kmax, kks[i]);
+    TRY(ensure_side(h, n_exact, kmax));
     CU(cudaEventRecord(h->ev_fwd, h->stream));
     CU(cudaStreamWaitEvent(h->side, h->ev_fwd, 0));
     {
@@ -1107,48 +1167,34 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
         h->risk = risks[i];
         h->rowidx = h->x_rowidx[e];
         h->n_act_dev = h->x_nact[e];
-        TRY(select_local(h, kks[i], h->band_log + 1 + i));
+        h->kk = kks[i];
+        TRY(select_local(h, h->kk, h->band_log + 1 + i));
+        TRY(eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen));
+        if (cvar_idx)
+          CU(cudaMemcpyAsync(h->hidx + koff[i], h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream));
         ++e;
       }
     }
     CU(cudaEventRecord(h->ev_side, h->side));
-    h->sm_avail = h->num_sms - SDN_SIDE_SMS;
+    h->sm_avail = h->num_sms - h->side_sms;
   }
-  for (int pass = 0; pass < (overlap ? 2 : 1); ++pass) {
-    if (overlap && pass == 1) {
-      h->sm_avail = h->num_sms;
-      CU(cudaStreamWaitEvent(h->stream, h->ev_side, 0));
+  for (int i = 0; i < n_risks; ++i) {
+    const bool exact = risks[i].kind == SDN_RISK_CVAR_EXACT;
+    if (overlap && exact) continue;          // done on the side stream
+    h->risk = risks[i];
+    h->compacted = false;
+    h->selected = false;
+    if (exact) {
+      h->kk = kks[i];
+      TRY(select_local(h, h->kk, h->band_log + 1 + i));
     }
-    for (int i = 0, e = 0; i < n_risks; ++i) {
-      const bool exact = risks[i].kind == SDN_RISK_CVAR_EXACT;
-      if (overlap && (exact != (pass == 1))) { e += exact; continue; }
-      h->risk = risks[i];
-      h->compacted = false;
-      h->selected = false;
-      double* Qm = h->Q;
-      int* rm = h->rowidx;
-      int* nm = h->n_act_dev;
-      if (exact) {
-        h->kk = kks[i];
-        if (overlap) {                       // selection made on the side stream
-          h->Q = h->Qx;
-          h->rowidx = h->x_rowidx[e];
-          h->n_act_dev = h->x_nact[e];
-          h->compacted = h->selected = true;
-        } else {
-          TRY(select_local(h, h->kk, h->band_log + 1 + i));
-        }
-      }
-      int rc = eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen);
-      if (rc == SDN_OK && cvar_idx && exact &&
-          cudaMemcpyAsync(h->hidx + koff[i], h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream))
-        rc = fail(SDN_ERR_CUDA, "index download failed");
-      h->Q = Qm;
-      h->rowidx = rm;
-      h->n_act_dev = nm;
-      if (rc) return rc;
-      e += exact;
-    }
+    TRY(eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen));
+    if (cvar_idx && exact)
+      CU(cudaMemcpyAsync(h->hidx + koff[i], h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream));
+  }
+  if (overlap) {
+    h->sm_avail = h->num_sms;
+    CU(cudaStreamWaitEvent(h->stream, h->ev_side, 0));
   }
   CU(cudaMemcpyAsync(h->hstats, h->stats_loc, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaMemcpyAsync(h->hpart_multi, h->partial_multi, sizeof(double) * n_risks * plen, cudaMemcpyDeviceToHost,
