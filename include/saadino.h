@@ -201,6 +201,10 @@ int sdn_eval_finish(sdn_handle* h, const double* stats_dev, const double* partia
 /* Local per-sample outputs of the last evaluation (device pointers, read-only;
  * valid until the next call): Q (n, float64). */
 int sdn_last_q(sdn_handle* h, const double** q_dev, int64_t* n);
+/* Q as used by the last exact-CVaR selection: the chain's Q with the rows
+ * near the threshold re-evaluated in fp64; = sdn_last_q when
+ * no exact selection ran since the last forward. */
+int sdn_last_qsel(sdn_handle* h, const double** q_dev, int64_t* n);
 
 /* Instrumentation.  sdn_profile(h, 1) starts CUDA-event timing of every
  * launch by kernel class (0 fwd GEMM, 1 reverse GEMM, 2 QoI+moments,

@@ -73,6 +73,7 @@ SIGNATURES = {
     "sdn_eval_set_risk": (C.c_int, [_P, C.POINTER(Risk)]),
     "sdn_eval_finish": (C.c_int, [_P, _P, _P, C.POINTER(Result), _D]),
     "sdn_last_q": (C.c_int, [_P, C.POINTER(_P), _I64]),
+    "sdn_last_qsel": (C.c_int, [_P, C.POINTER(_P), _I64]),
     "sdn_kernel_launches": (C.c_int64, [_P]),
     "sdn_profile": (C.c_int, [_P, C.c_int32]),
     "sdn_debug_gemm": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _D]),

@@ -20,9 +20,10 @@
 #include "gemm_tc.cuh"
 #include "refine.cuh"
 
-// SMs left to side-stream work while the main stream's GEMMs run (sdn_eval_multi).
-// 40 measured best at c2 (34-48 plateau; the side chain is latency-bound).
-constexpr int SDN_SIDE_SMS_DEFAULT = 40;
+// SMs left to side-stream work (the exact-CVaR selections) while the main
+// stream's persistent GEMMs run (sdn_eval_multi).  20 keeps the c2 sweep GEMMs
+// (256 tiles) at two full waves on the other 128.
+constexpr int SDN_SIDE_SMS_DEFAULT = 20;
 
 #include <algorithm>
 #include <cmath>
@@ -30,6 +31,7 @@ constexpr int SDN_SIDE_SMS_DEFAULT = 40;
 #include <string>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <vector>
 
 using namespace sdn;
@@ -60,8 +62,7 @@ static int fail(int code, const std::string& msg) {
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int pad4(int x) { return (x + 3) & ~3; }
 
-// reverse-sweep work buffers; a second set (sized for the CVaR tail) lets the
-// exact-CVaR sweep run on the side stream while the main set is in use
+// reverse-sweep work buffers (one set per handle)
 struct SweepBufs {
   float* E = nullptr;           // seeds (rows x r_u)
   float* G = nullptr;           // residual gradient stream (rows x maxw)
@@ -72,6 +73,8 @@ struct SweepBufs {
   TcOperand act[2];             // bf16x3 split of the sweep operand (ping-pong)
   TcOperand seed;
   int64_t rows = 0;
+  double* W = nullptr;          // per-row risk weights (rows x planes)
+  int planes = 0;               // risks the partial buffers hold
 };
 
 struct sdn_handle {
@@ -135,14 +138,11 @@ struct sdn_handle {
   uint8_t* sel = nullptr;
   double* qpart = nullptr;      // qgrid x STATS_LEN
   int qgrid = 0;
-  double* cpart = nullptr;      // crb x maxw
   double* partial_multi = nullptr;   // per-risk partials of sdn_eval_multi (device)
   double* hpart_multi = nullptr;     // pinned host copy
   int* hidx = nullptr;               // pinned CVaR indices
   int multi_cap = 0;
   int64_t hidx_cap = 0;
-  double* tsum = nullptr;       // (cap/128 * 4) x maxw: fused column-sum partials (TC chains)
-  double* csum = nullptr;       // maxw: summed columns
   int crb = 0;
   double* stats_loc = nullptr;  // STATS_LEN
   double* partial_loc = nullptr;
@@ -180,20 +180,27 @@ struct sdn_handle {
   int ref_rows = 0;
   double* thr_dev = nullptr;    // exact-CVaR threshold value (top-k output)
   int* ref_blockcnt = nullptr;  // k_refine grid scratch
+  int* ref_rowidx = nullptr;    // k_refine band rows
+  unsigned* ref_ghist = nullptr;           // k_refine selection histograms (2 x grid x 256)
+  unsigned long long* ref_gmm = nullptr;   // k_refine selection min / max keys (2 x grid)
+  double* Qr = nullptr;         // exact-CVaR selection copy of Q (threshold band refined in fp64)
+  bool qr_valid = false;
+  double* wpart = nullptr;      // k_weights block partials (qgrid x 2 SDN_RMAX)
+  double* vsum = nullptr;       // 2 SDN_RMAX: per-risk sum_{w != 0} Q, count
   unsigned* ref_bar = nullptr;  // k_refine grid barrier
   int ref_grid = 0;
   bool ref_ok = false;          // every layer input width <= REF_KC
   // side stream (overlapped exact-CVaR selection in sdn_eval_multi)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fwd = nullptr, ev_side = nullptr;
-  double* Qx = nullptr;
   int* x_counts = nullptr;
   int* x_offs = nullptr;
   std::vector<int*> x_rowidx, x_nact;
+  std::vector<uint8_t*> x_mask;
   int sm_avail = 0;             // SMs the persistent GEMMs may use
   int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS
   bool no_overlap = false;               // env SDN_NO_OVERLAP=1
-  SweepBufs sw0, sw1;           // main / side sweep buffers
+  SweepBufs sw0;                // sweep buffers
   SweepBufs* sw = &sw0;
   int* band_log = nullptr;      // band row counts: [0] forward window, [1 + i] exact risk i
   int* hband = nullptr;         // pinned mirror
@@ -201,6 +208,8 @@ struct sdn_handle {
   double* K64 = nullptr;        // decoded-frame Gram / c in fp64
   double* c64dec = nullptr;
   bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
+  bool ref_trace = false;       // env SDN_REFINE_TRACE=1
+  unsigned long long* ref_trace_dev = nullptr;
   bool selected = false;        // exact CVaR selection done
   int64_t kk = 0;               // exact CVaR k (global)
   bool compacted = false;
@@ -379,15 +388,30 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
   return SDN_OK;
 }
 
+// weighted column sums of the unified sweep (backward_multi): per-row risk
+// weights W (sweep rows x R), partial plane stride, and a hook run right
+// before the last GEMM (where the weights are first needed)
+struct SweepSum {
+  const double* W = nullptr;
+  int R = 1;
+  int64_t plane = 0;
+  std::function<int()> before_last;
+};
+
 // reverse sweep over `nmax` (device count n_act_dev) compacted rows from the
 // seeds E.  SIMT chains (or want_u0) leave dL/dS_0 (rows x w[1]) in *u0_out;
-// tensor-core chains fuse the sample sum into the last GEMM and leave fp64
-// column-sum partials in h->tsum (*u0_out = nullptr, *nrb = partial rows,
-// device-bounded by n_act_dev).
+// tensor-core chains fuse the (weighted) sample sum into the last GEMM and
+// leave fp64 column-sum partials in h->sw->tsum (*u0_out = nullptr, *nrb =
+// partial rows, device-bounded by n_act_dev).
 static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const int* rowidx,
-                        float** u0_out, int64_t rows_hint, bool want_u0 = false, int64_t* nrb = nullptr) {
+                        float** u0_out, int64_t rows_hint, bool want_u0 = false, int64_t* nrb = nullptr,
+                        const SweepSum* ss = nullptr) {
   const int L = h->L;
-  if (L == 1) { *u0_out = h->sw->E; return SDN_OK; }
+  if (L == 1) {
+    if (ss && ss->before_last) TRY(ss->before_last());
+    *u0_out = h->sw->E;
+    return SDN_OK;
+  }
   const bool tcc = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
   const int route = tcc ? 1 : 0;
   int cur = 0;
@@ -398,10 +422,12 @@ static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const
     const TcOperand* tA = !tcc ? nullptr : (l == L - 1) ? &h->sw->seed : &h->sw->act[cur];
     const TcOperand* tB = tcc ? &h->tcw.bwd[l] : nullptr;
     const float* resid = (l < L - 1 && h->res[l]) ? h->sw->G : nullptr;
+    if (l == 1 && ss && ss->before_last) TRY(ss->before_last());
     h->pcls = PC_BWD_GEMM;
     h->prows = rows_hint;
     if (l == 1 && tcc && !want_u0) {
       EpiBwdSum e{resid, h->D[0], (int64_t)N, rowidx, (int64_t)N, h->sw->tsum, (int64_t)N};
+      if (ss) { e.W = ss->W; e.R = ss->R; e.plane = ss->plane; }
       TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, e, tB, tA, route)));
       *u0_out = nullptr;
       if (nrb) *nrb = cdiv(nmax, 128) * 4;
@@ -506,9 +532,6 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   h->qgrid = (int)std::min<int64_t>(cdiv(cap, 8), 2 * h->num_sms);
   if ((rc = dalloc(h, &h->qpart, (size_t)h->qgrid * STATS_LEN))) return bail(rc);
   h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 16);
-  if ((rc = dalloc(h, &h->cpart, (size_t)h->crb * h->maxw))) return bail(rc);
-  if ((rc = dalloc(h, &h->tsum, (size_t)cdiv(cap, 128) * 4 * h->maxw))) return bail(rc);
-  if ((rc = dalloc(h, &h->csum, (size_t)h->maxw))) return bail(rc);
   if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
   if ((rc = dalloc(h, &h->zdev, h->d_z))) return bail(rc);
@@ -528,6 +551,12 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
     for (int l = 1; l < h->L; ++l) h->ref_ok = h->ref_ok && h->w[l] <= REF_KC;
   }
   if ((rc = dalloc(h, &h->ref_blockcnt, h->num_sms))) return bail(rc);
+  if ((rc = dalloc(h, &h->ref_rowidx, cap))) return bail(rc);
+  if ((rc = dalloc(h, &h->ref_ghist, (size_t)2 * h->num_sms * 256))) return bail(rc);
+  if ((rc = dalloc(h, &h->ref_gmm, (size_t)2 * h->num_sms))) return bail(rc);
+  if ((rc = dalloc(h, &h->Qr, cap))) return bail(rc);
+  if ((rc = dalloc(h, &h->wpart, (size_t)h->qgrid * 2 * SDN_RMAX))) return bail(rc);
+  if ((rc = dalloc(h, &h->vsum, 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);
   if (cudaMemset(h->ref_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
   for (int i = 0; i < 2; ++i)
@@ -542,6 +571,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
   { const char* e = getenv("SDN_NO_REFINE"); h->no_refine = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_OVERLAP"); h->no_overlap = e && e[0] == '1'; }
+  { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
   { const char* e = getenv("SDN_SIDE_SMS");
     if (e) h->side_sms = std::max(1, std::min(atoi(e), h->num_sms / 2)); }
   h->tcw.enabled = false;
@@ -552,9 +582,6 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   h->sw0.G = h->G;
   h->sw0.Ub[0] = h->Ub[0];
   h->sw0.Ub[1] = h->Ub[1];
-  h->sw0.tsum = h->tsum;
-  h->sw0.cpart = h->cpart;
-  h->sw0.csum = h->csum;
   h->sw0.act[0] = h->tcw.act[0];
   h->sw0.act[1] = h->tcw.act[1];
   h->sw0.seed = h->tcw.seed;
@@ -582,6 +609,7 @@ int sdn_destroy(sdn_handle* h) {
   if (h->hstats) cudaFreeHost(h->hstats);
   if (h->hpart) cudaFreeHost(h->hpart);
   if (h->hband) cudaFreeHost(h->hband);
+  if (h->ref_trace_dev) cudaFree(h->ref_trace_dev);
   if (h->K64) cudaFree(h->K64);
   if (h->c64dec) cudaFree(h->c64dec);
   if (h->partial_multi) cudaFree(h->partial_multi);
@@ -726,7 +754,7 @@ static int upload_z(sdn_handle* h, const double* z) {
 }
 
 static int compact_rows(sdn_handle* h, int kind, double t, double eps, const double* tdev = nullptr,
-                        int* count_out = nullptr);
+                        int* count_out = nullptr, const uint8_t* sel = nullptr, int* rowidx_out = nullptr);
 
 // Q refinement.  Rows whose chain Q (bf16x3 or fp32, ~1e-5
 // relative) lies within REFINE_REL |Q| of a decision boundary -- the
@@ -737,13 +765,14 @@ static int compact_rows(sdn_handle* h, int kind, double t, double eps, const dou
 // count stays on the device (*count); more than ref_rows band rows skips the
 // refinement for that evaluation (reported as a negative n_refined).
 static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, int* count,
-                       uint8_t* mask = nullptr) {
-  if (!h->ref_ok) return SDN_OK;
+                       uint8_t* mask = nullptr, double* Qt = nullptr, int64_t k = 0, bool do_refine = true) {
+  do_refine = do_refine && h->ref_ok;
+  if (!do_refine && k == 0) return SDN_OK;
   RefineArgs a{};
   a.n = h->n; a.kind = kind; a.t = t; a.eps = eps; a.tdev = h->thr_dev;
-  a.rowidx = h->rowidx; a.count = count; a.blockcnt = h->ref_blockcnt; a.bar = h->ref_bar;
+  a.rowidx = h->ref_rowidx; a.count = count; a.blockcnt = h->ref_blockcnt; a.bar = h->ref_bar;
   a.L = h->L;
-  for (int l = 0; l < h->L; ++l) {
+  for (int l = 0; l < h->L && l < REF_MAX_LAYERS; ++l) {
     const bool first = l == 0;
     a.layer[l] = RefineLayer{first ? h->W0raw : h->W[l], h->b[l], first ? h->r_m : h->w[l], h->w[l + 1],
                              (l > 0 && l < h->L - 1 && h->res[l]) ? 1 : 0};
@@ -751,12 +780,27 @@ static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, 
   a.MR = h->MR; a.iscale = h->iscale; a.zb64 = h->zb64; a.act = h->act; a.omean = h->omean; a.ostd = h->ostd;
   a.buf[0] = h->ref64[0]; a.buf[1] = h->ref64[1]; a.cap_rows = h->ref_rows;
   a.r_u = h->r_u; a.c32 = h->c; a.K64 = dec ? h->K64 : nullptr; a.c64 = dec ? h->c64dec : nullptr;
-  a.q0 = dec ? h->q0dec : h->q0; a.Q = h->Q; a.mask = mask;
+  a.q0 = dec ? h->q0dec : h->q0; a.Q = Qt ? Qt : h->Q; a.mask = mask;
+  a.k = k; a.ghist = h->ref_ghist; a.gmm = h->ref_gmm; a.refine = do_refine ? 1 : 0;
   void* args[] = {&a};
-  ProfScope ps(h, PC_REFINE, 0.0, 0.0);
+  ProfScope ps(h, k > 0 ? PC_SELECT : PC_REFINE, 0.0, k > 0 ? 8.0 * 8.0 * h->n : 0.0);
+  if (h->ref_trace) {
+    if (!h->ref_trace_dev) CU(cudaMalloc(&h->ref_trace_dev, 64 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(h->ref_trace_dev, 0, 64 * sizeof(unsigned long long), h->stream));
+    a.trace = h->ref_trace_dev;
+  }
   CU(cudaLaunchCooperativeKernel((const void*)k_refine, dim3(h->ref_grid), dim3(REF_THREADS), args,
                                  sizeof(double) * REF_RB * REF_KC, h->stream));
   h->launches++;
+  if (h->ref_trace) {                 // debug: phase timestamps of block 0 (env SDN_REFINE_TRACE=1)
+    unsigned long long tr[64];
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaMemcpy(tr, h->ref_trace_dev, sizeof(tr), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "k_refine grid %d k %lld:", h->ref_grid, (long long)k);
+    for (int i = 1; i < 64; ++i)
+      if (tr[i]) fprintf(stderr, " [%d]%.1f", i, (tr[i] - tr[0]) * 1e-3);
+    fprintf(stderr, " us\n");
+  }
   return SDN_OK;
 }
 
@@ -783,6 +827,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   h->risk = *risk;
   h->selected = false;
   h->compacted = false;
+  h->qr_valid = false;
   const bool dec = risk->qoi == SDN_QOI_DECODED;
   const double q0 = dec ? h->q0dec : h->q0;
   // moments accumulate (Q - shift) in fp64; shift = q0 keeps every evaluation
@@ -829,15 +874,18 @@ static int ensure_cand(sdn_handle* h, int64_t count) {
 }
 
 // ordered compaction of flagged rows -> rowidx / n_act_dev
-static int compact_rows(sdn_handle* h, int kind, double t, double eps, const double* tdev, int* count_out) {
+static int compact_rows(sdn_handle* h, int kind, double t, double eps, const double* tdev, int* count_out,
+                        const uint8_t* sel, int* rowidx_out) {
   const int nb = (int)cdiv(std::max<int64_t>(h->n, 1), 1024);
+  if (!sel) sel = h->sel;
   ProfScope ps(h, PC_COMPACT, 0.0, 2.0 * (8.0 + 1.0) * h->n);
-  k_flag_count<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, tdev, h->counts);
+  k_flag_count<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, sel, t, eps, tdev, h->counts);
   k_scan_counts<<<1, 32, 0, h->stream>>>(nb, h->counts, h->offs, count_out ? count_out : h->n_act_dev);
-  k_compact<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, h->sel, t, eps, tdev, h->offs, h->rowidx);
+  k_compact<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, sel, t, eps, tdev, h->offs,
+                                        rowidx_out ? rowidx_out : h->rowidx);
   h->launches += 3;
   CHECK_LAUNCH(h);
-  h->compacted = true;
+  if (!rowidx_out) h->compacted = true;
   return SDN_OK;
 }
 
@@ -848,11 +896,10 @@ static int launch_topk(sdn_handle* h, int64_t n, int64_t k, const double* vals, 
   if (n <= TOPK_SMEM_MAX) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_topk_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, TOPK_SMEM_MAX * 8);
+      cudaFuncSetAttribute(k_topk_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TOPK_SMEM_BYTES);
       attr = true;
     }
-    k_topk_select_smem<<<1, 1024, (size_t)std::max<int64_t>(n, 1) * 8, h->stream>>>((int)n, k, vals, gidx, mask,
-                                                                                     thr);
+    k_topk_select_smem<<<1, 1024, TOPK_SMEM_BYTES, h->stream>>>((int)n, k, vals, gidx, mask, thr);
   } else {
     k_topk_select<<<1, 1024, 0, h->stream>>>(n, k, vals, gidx, mask, thr);
   }
@@ -864,75 +911,175 @@ static int launch_topk(sdn_handle* h, int64_t n, int64_t k, const double* vals, 
 // local exact top-k (single rank): selection mask over the shard's Q.  With
 // band_count, the rows within refinement error of the threshold are
 // re-evaluated in fp64 and reselected among themselves.
-static int select_local(sdn_handle* h, int64_t k, int* band_count = nullptr) {
+// The exact-CVaR selection works on its own copy of Q, so that the fp64
+// refinement of the threshold band decides the selection only: every weight
+// and value (and the other risks of the evaluation) use the chain's Q.
+static double* sel_q(sdn_handle* h) {
+  if (!h->qr_valid) {
+    cudaMemcpyAsync(h->Qr, h->Q, sizeof(double) * std::max<int64_t>(h->n, 1), cudaMemcpyDeviceToDevice, h->stream);
+    h->qr_valid = true;
+  }
+  return h->Qr;
+}
+
+static int select_local(sdn_handle* h, int64_t k, int* band_count = nullptr, uint8_t* mask = nullptr,
+                        int* rowidx_out = nullptr, int* count_out = nullptr) {
   const bool refine = band_count && !h->no_refine;
-  { ProfScope ps(h, PC_SELECT, 0.0, 8.0 * 8.0 * h->n);
-  TRY(launch_topk(h, h->n, k, h->Q, nullptr, h->sel, refine ? h->thr_dev : nullptr)); }
-  if (refine) TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, band_count, h->sel));
-  TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
+  if (!mask) mask = h->sel;
+  double* Qs = sel_q(h);
+  // one cooperative launch: top-k, then (refine) the fp64 threshold band and
+  // the reselection among it
+  TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, band_count, mask, Qs, k,
+                  refine));
+  TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0, nullptr, count_out, mask, rowidx_out));
   h->selected = true;
   return SDN_OK;
 }
 
-// phase 3: weights, seeds, reverse sweep, projection -> partial_dev
-static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev) {
+// per-handle buffers of the unified sweep for R risks: weights, weight
+// partials, and R partial planes of the column sums (grown on demand)
+static int ensure_sweep(sdn_handle* h, SweepBufs& b, int R) {
+  if (R <= b.planes) return SDN_OK;
+  const int64_t rows = b.rows;
+  int rc;
+  if ((rc = dalloc(h, &b.tsum, (size_t)R * cdiv(rows, 128) * 4 * h->maxw))) return rc;
+  if ((rc = dalloc(h, &b.cpart, (size_t)R * h->crb * h->maxw))) return rc;
+  if ((rc = dalloc(h, &b.csum, (size_t)R * h->maxw))) return rc;
+  if ((rc = dalloc(h, &b.W, (size_t)R * std::max<int64_t>(rows, 1)))) return rc;
+  b.planes = R;
+  return SDN_OK;
+}
+
+// One reverse sweep for R risks.  Unit seeds over the union of
+// the risks' active rows (all rows when a mean / mean+variance risk is
+// present, else the ordered union of the CVaR rows), per-row weights
+// w_i^(r), weighted fp64 column sums per risk, projection through PzT ->
+// partials[r * plen] = [grad (d_z) | sum_{w != 0} Q | #{w != 0}].
+// `join` runs before the first use of the exact-CVaR masks (side-stream
+// selections, sdn_eval_multi): before the union compaction, or -- dense --
+// right before the last GEMM, so the selections overlap the sweep.
+static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uint8_t* const* masks,
+                          const int64_t* ks, const double* stats_dev, double* partials,
+                          const std::function<int()>& join = {}) {
   if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
-  const sdn_risk& r = h->risk;
-  const bool dec = r.qoi == SDN_QOI_DECODED;
-  const int kind = r.kind;
-  const bool exact = kind == SDN_RISK_CVAR_EXACT;
-  if (exact && !h->selected) return fail(SDN_ERR_STATE, "exact CVaR needs the selection phase");
-  const double eps = kind == SDN_RISK_CVAR_SMOOTH ? r.eps : 1.0;
-  const double kinv = exact ? 1.0 / (double)h->kk : 0.0;
+  if (R < 1 || R > SDN_RMAX) return fail(SDN_ERR_ARG, "1..8 risks per sweep");
+  RiskSet rs{};
+  rs.R = R;
+  bool dense = false, all_exact = true, any_grad = false;
+  int64_t ksum = 0;
+  for (int r = 0; r < R; ++r) {
+    const sdn_risk& k = risks[r];
+    const bool exact = k.kind == SDN_RISK_CVAR_EXACT;
+    if (exact && (!masks || !masks[r])) return fail(SDN_ERR_STATE, "exact CVaR needs the selection phase");
+    rs.kind[r] = k.kind;
+    rs.beta[r] = k.beta;
+    rs.eps[r] = k.kind == SDN_RISK_CVAR_SMOOTH ? k.eps : 1.0;
+    rs.t[r] = k.t;
+    rs.kinv[r] = exact ? 1.0 / (double)ks[r] : 0.0;
+    rs.mask[r] = exact ? masks[r] : nullptr;
+    dense |= k.kind == SDN_RISK_MEAN || k.kind == SDN_RISK_MEANVAR;
+    all_exact &= exact;
+    ksum += exact ? ks[r] : 0;
+    any_grad |= k.need_grad != 0;
+  }
+  const bool dec = risks[0].qoi == SDN_QOI_DECODED;
+  SweepBufs& sw = *h->sw;
+  TRY(ensure_sweep(h, sw, R));
+  // sweep rows
   const int* rowidx = nullptr;
   const int* nact = nullptr;
-  if (kind == SDN_RISK_CVAR_SMOOTH) TRY(compact_rows(h, RISK_CVAR_SMOOTH, r.t, eps));
-  if (h->compacted) { rowidx = h->rowidx; nact = h->n_act_dev; }
-  const int64_t rows_hint = exact ? h->kk : (h->compacted ? -1 : h->n);
-  if (!r.need_grad) {
-    k_finalize_grad<<<1, 1024, sizeof(double) * h->h1, h->stream>>>(0, h->h1, h->d_z, nullptr, h->PzT, h->rowidx,
-                                                                    h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
+  int64_t nmax = h->n, rows_hint = h->n;
+  if (!dense && h->n > 0) {
+    if (join) TRY(join());
+    const int nb = (int)cdiv(h->n, 1024);
+    { ProfScope ps(h, PC_COMPACT, 0.0, 9.0 * h->n);
+    k_union_count<<<nb, 1024, 0, h->stream>>>(h->n, rs, h->Q, h->counts);
+    k_scan_counts<<<1, 32, 0, h->stream>>>(nb, h->counts, h->offs, h->n_act_dev);
+    k_union_compact<<<nb, 1024, 0, h->stream>>>(h->n, rs, h->Q, h->offs, h->rowidx); }
+    h->launches += 3;
+    CHECK_LAUNCH(h);
+    rowidx = h->rowidx;
+    nact = h->n_act_dev;
+    h->compacted = true;
+    nmax = all_exact ? std::min<int64_t>(h->n, ksum) : h->n;
+    rows_hint = all_exact ? nmax : -1;
+  }
+  if (nmax > sw.rows) return fail(SDN_ERR_STATE, "sweep buffers too small");
+  // weights + value partials (the first read of the masks and of Q)
+  const int wg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(nmax, 1), 256), h->qgrid));
+  auto weights = [&]() -> int {
+    ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * (1 + R));
+    k_weights<<<wg, 256, 0, h->stream>>>(nmax, nact, rowidx, rs, h->Q, stats_dev, h->shift, sw.W, h->wpart);
+    k_sum_rows<<<(unsigned)cdiv(2 * SDN_RMAX, 8), 256, 0, h->stream>>>(wg, 2 * SDN_RMAX, h->wpart, h->vsum);
+    h->launches += 2;
+    CHECK_LAUNCH(h);
+    return SDN_OK;
+  };
+  const size_t fsm = sizeof(double) * h->h1;
+  if (!any_grad || h->n == 0) {
+    if (dense && join) TRY(join());
+    TRY(weights());
+    k_finalize_multi<<<dim3(1, R), 256, fsm, h->stream>>>(0, 0, h->h1, h->d_z, nullptr, h->PzT, h->vsum, h->plen(),
+                                                          partials);
     h->launches++;
     CHECK_LAUNCH(h);
     return SDN_OK;
   }
-  // exact CVaR: k selected rows (device count <= k on a multi-rank shard)
-  const int64_t nmax = exact ? std::min<int64_t>(h->kk, h->n) : h->n;
-  SweepBufs& sw = *h->sw;
-  if (nmax > sw.rows) return fail(SDN_ERR_STATE, "sweep buffers too small");
-  if (nmax > 0) {
-    const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nmax, 8), 4 * h->num_sms));
-    const bool tcs = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
-    { ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
-    k_seed<<<sg, 256, 0, h->stream>>>(nmax, nact, rowidx, h->r_u, h->Y, dec ? h->KPhi : nullptr,
-                                      dec ? h->cdec : h->c, h->ostd, h->Q, stats_dev, kind, h->shift, r.beta,
-                                      eps, r.t, kinv, sw.E, tcs ? sw.seed.hi : nullptr,
-                                      tcs ? sw.seed.lo : nullptr); }
-    h->launches++;
-    CHECK_LAUNCH(h);
-    float* u0 = nullptr;
-    int64_t nrb = 0;
-    TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint, false, &nrb));
-    if (u0) {
-      dim3 cg((unsigned)cdiv(h->h1, 32), (unsigned)h->crb);
-      { ProfScope ps(h, PC_COLSUM, 0.0, 0.0, rows_hint, 4.0 * h->h1);
-      k_colsum<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, sw.cpart); }
-    } else {
-      // tensor-core chain: the last GEMM left per-(tile, quarter) fp64 partials
-      ProfScope ps(h, PC_COLSUM, 0.0, 8.0 * nrb * h->h1);
-      k_colsum64<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>((int)nrb, nact, h->h1, sw.tsum,
-                                                                            sw.csum);
-    }
-    h->launches++;
+  const bool tcs = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
+  { ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
+  const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nmax, 8), 4 * h->num_sms));
+  k_seed<<<sg, 256, 0, h->stream>>>(nmax, nact, rowidx, h->r_u, h->Y, dec ? h->KPhi : nullptr,
+                                    dec ? h->cdec : h->c, h->ostd, nullptr, nullptr, RISK_UNIT, 0.0, 0.0, 1.0,
+                                    0.0, 0.0, sw.E, tcs ? sw.seed.hi : nullptr, tcs ? sw.seed.lo : nullptr); }
+  h->launches++;
+  CHECK_LAUNCH(h);
+  const int64_t tplane = cdiv(sw.rows, 128) * 4 * h->maxw;
+  SweepSum ssum;
+  ssum.W = sw.W;
+  ssum.R = R;
+  ssum.plane = tplane;
+  ssum.before_last = [&]() -> int {
+    if (dense && join) TRY(join());
+    return weights();
+  };
+  float* u0 = nullptr;
+  int64_t nrb = 0;
+  TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint, false, &nrb, &ssum));
+  const double* part;
+  int nrb_fin;
+  int64_t plane;
+  if (u0) {
+    ProfScope ps(h, PC_COLSUM, 0.0, 0.0, rows_hint, 4.0 * h->h1);
+    dim3 cg((unsigned)cdiv(h->h1, 32), (unsigned)h->crb);
+    k_colsum_w<<<cg, dim3(32, 8), 0, h->stream>>>(nmax, nact, h->h1, u0, sw.W, R, sw.cpart);
+    part = sw.cpart;
+    nrb_fin = h->crb;
+    plane = (int64_t)h->crb * h->h1;
+  } else {
+    ProfScope ps(h, PC_COLSUM, 0.0, 8.0 * nrb * h->h1 * R);
+    k_colsum64<<<dim3((unsigned)cdiv(h->h1, 32), R), dim3(32, 32), 0, h->stream>>>((int)nrb, nact, h->h1, sw.tsum,
+                                                                                sw.csum, tplane);
+    part = sw.csum;
+    nrb_fin = 1;
+    plane = h->h1;
   }
-  ProfScope psf(h, PC_FINAL, 0.0, 8.0 * h->crb * h->h1);
-  const bool summed = nmax > 0 && chain_tc(h, rows_hint >= 0 ? rows_hint : nmax) && h->L > 1;
-  k_finalize_grad<<<(unsigned)cdiv(h->d_z, 8), 256, sizeof(double) * h->h1, h->stream>>>(
-      nmax > 0 ? (summed ? 1 : h->crb) : 0, h->h1, h->d_z, nmax > 0 ? (summed ? sw.csum : sw.cpart) : nullptr,
-      h->PzT, h->rowidx, h->n_act_dev, h->Q, exact ? 1 : 0, partial_dev);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  { ProfScope ps(h, PC_FINAL, 0.0, 8.0 * nrb_fin * h->h1 * R);
+  k_finalize_multi<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(
+      nrb_fin, plane, h->h1, h->d_z, part, h->PzT, h->vsum, h->plen(), partials); }
   h->launches++;
   CHECK_LAUNCH(h);
   return SDN_OK;
+}
+
+// phase 3 for the current risk (sdn_eval, multi-rank phases)
+static int eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev) {
+  const uint8_t* m = h->sel;
+  const int64_t k = h->kk;
+  if (h->risk.kind == SDN_RISK_CVAR_EXACT && !h->selected)
+    return fail(SDN_ERR_STATE, "exact CVaR needs the selection phase");
+  return backward_multi(h, &h->risk, 1, &m, &k, stats_dev, partial_dev);
 }
 
 // host combination of the (global) moments and partials of one risk
@@ -972,74 +1119,54 @@ static int finish_host(sdn_handle* h, const sdn_risk& r, const double* st, const
   return SDN_OK;
 }
 
-// side-stream buffers for overlapped exact-CVaR selections (sdn_eval_multi)
-static int ensure_side(sdn_handle* h, int n_exact, int64_t kmax) {
+// per-exact-risk selection buffers (sdn_eval_multi)
+static int ensure_xsel(sdn_handle* h, int n_exact) {
   int rc;
-  if (!h->side) {
-    CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
-    CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
-    const int nb1024 = (int)cdiv(h->cap, 1024);
-    if ((rc = dalloc(h, &h->Qx, h->cap))) return rc;
-    if ((rc = dalloc(h, &h->x_counts, nb1024))) return rc;
-    if ((rc = dalloc(h, &h->x_offs, nb1024))) return rc;
-  }
   while ((int)h->x_rowidx.size() < n_exact) {
     int* r = nullptr;
     int* c = nullptr;
+    uint8_t* m = nullptr;
     if ((rc = dalloc(h, &r, h->cap))) return rc;
     if ((rc = dalloc(h, &c, 1))) return rc;
+    if ((rc = dalloc(h, &m, h->cap))) return rc;
     h->x_rowidx.push_back(r);
     h->x_nact.push_back(c);
-  }
-  if (kmax > h->sw1.rows) {           // side sweep buffers for the CVaR tail
-    SweepBufs& b = h->sw1;
-    const int64_t rows = std::max<int64_t>(cdiv(kmax, 128) * 128, 128);
-    if ((rc = dalloc(h, &b.E, (size_t)rows * h->r_u))) return rc;
-    if ((rc = dalloc(h, &b.G, (size_t)rows * h->maxw))) return rc;
-    for (int i = 0; i < 2; ++i)
-      if ((rc = dalloc(h, &b.Ub[i], (size_t)rows * h->maxw))) return rc;
-    if ((rc = dalloc(h, &b.tsum, (size_t)cdiv(rows, 128) * 4 * h->maxw))) return rc;
-    if ((rc = dalloc(h, &b.cpart, (size_t)h->crb * h->maxw))) return rc;
-    if ((rc = dalloc(h, &b.csum, (size_t)h->maxw))) return rc;
-    if (h->tcw.enabled) {
-      for (int i = 0; i < 2; ++i)
-        if (tc_buf(h, h->tcw, b.act[i], rows, h->maxw)) return fail(SDN_ERR_NOMEM, "side sweep operands");
-      if (tc_buf(h, h->tcw, b.seed, rows, h->r_u)) return fail(SDN_ERR_NOMEM, "side sweep operands");
-    }
-    b.rows = rows;
+    h->x_mask.push_back(m);
   }
   return SDN_OK;
 }
 
-// enqueue on the side stream with the side copies of Q and the compaction
-// scratch (the helpers below read these handle fields)
+// side stream for overlapped selections (sdn_eval_multi)
+static int ensure_side(sdn_handle* h) {
+  if (h->side) return SDN_OK;
+  CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
+  const int nb1024 = (int)cdiv(h->cap, 1024);
+  int rc;
+  if ((rc = dalloc(h, &h->x_counts, nb1024))) return rc;
+  if ((rc = dalloc(h, &h->x_offs, nb1024))) return rc;
+  return SDN_OK;
+}
+
+// enqueue on the side stream with its own compaction scratch (the helpers
+// read these handle fields); the refinement grid fits the reserved SMs
 struct SideScope {
   sdn_handle* h;
   cudaStream_t s0;
-  double* Qmain;
-  int *c0, *o0, *r0, *n0;
-  int g0, a0;
-  explicit SideScope(sdn_handle* h_) : h(h_), s0(h_->stream), Qmain(h_->Q), c0(h_->counts), o0(h_->offs),
-                                       r0(h_->rowidx), n0(h_->n_act_dev), g0(h_->ref_grid), a0(h_->sm_avail) {
+  int *c0, *o0;
+  int g0;
+  explicit SideScope(sdn_handle* h_) : h(h_), s0(h_->stream), c0(h_->counts), o0(h_->offs), g0(h_->ref_grid) {
     h->stream = h->side;
-    h->Q = h->Qx;
     h->counts = h->x_counts;
     h->offs = h->x_offs;
     h->ref_grid = h->side_sms;
-    h->sm_avail = h->side_sms;
-    h->sw = &h->sw1;
   }
   ~SideScope() {
     h->stream = s0;
-    h->Q = Qmain;
     h->counts = c0;
     h->offs = o0;
-    h->rowidx = r0;
-    h->n_act_dev = n0;
     h->ref_grid = g0;
-    h->sm_avail = a0;
-    h->sw = &h->sw0;
   }
 };
 
@@ -1144,58 +1271,56 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       off += kks[i];
       ++n_exact;
     }
-  // Overlap: each exact-CVaR risk (top-k, fp64 refinement of the threshold
-  // band, compaction, and its k-row reverse sweep) only reads Q and the
-  // forward's act' arrays, so it runs on the side stream -- on a copy Qx,
-  // with its own sweep buffers (sw1), over side_sms SMs kept free of the
-  // main stream's persistent GEMMs -- while the other risks' sweeps run on
-  // the main stream.  The two chains share no written buffer, so results do
-  // not depend on the interleaving.  (Profiling runs serialise: its class
-  // timers are stream-ordered.)
-  const bool overlap = n_exact > 0 && n_exact < n_risks && !h->prof && !h->no_overlap;
+  // exact-CVaR selections: a mask and an ordered index list per exact risk
+  TRY(ensure_xsel(h, n_exact));
+  bool dense = false;
+  for (int i = 0; i < n_risks; ++i)
+    dense |= risks[i].kind == SDN_RISK_MEAN || risks[i].kind == SDN_RISK_MEANVAR;
+  std::vector<const uint8_t*> masks(n_risks, nullptr);
+  auto select_all = [&]() -> int {
+    for (int i = 0, e = 0; i < n_risks; ++i) {
+      if (risks[i].kind != SDN_RISK_CVAR_EXACT) continue;
+      h->risk = risks[i];
+      TRY(select_local(h, kks[i], h->band_log + 1 + i, h->x_mask[e], h->x_rowidx[e], h->x_nact[e]));
+      masks[i] = h->x_mask[e];
+      if (cvar_idx)
+        CU(cudaMemcpyAsync(h->hidx + koff[i], h->x_rowidx[e], sizeof(int) * kks[i], cudaMemcpyDeviceToHost,
+                           h->stream));
+      ++e;
+    }
+    return SDN_OK;
+  };
+  // Overlap (a dense risk present): the selections (top-k, fp64 refinement
+  // of the threshold band, index compaction) only read Q, and the one sweep
+  // first needs the masks at its last GEMM -- so they run on the side stream
+  // (side_sms SMs kept free of the persistent GEMMs meanwhile) while the main
+  // stream seeds and runs the first L-2 sweep GEMMs.  The sweep's seeds are
+  // unit weights (no Q read), so the in-place refinement of Q cannot race.
+  // (Profiling runs serialise: its class timers are stream-ordered.)
+  const bool overlap = dense && n_exact > 0 && !h->prof && !h->no_overlap;
+  std::function<int()> join;
   if (overlap) {
-    int64_t kmax = 0;
-    for (int i = 0; i < n_risks; ++i) kmax = std::max(kmax, kks[i]);
-    TRY(ensure_side(h, n_exact, kmax));
+    TRY(ensure_side(h));
     CU(cudaEventRecord(h->ev_fwd, h->stream));
     CU(cudaStreamWaitEvent(h->side, h->ev_fwd, 0));
     {
       SideScope ss(h);
-      CU(cudaMemcpyAsync(h->Q, ss.Qmain, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->stream));
-      for (int i = 0, e = 0; i < n_risks; ++i) {
-        if (risks[i].kind != SDN_RISK_CVAR_EXACT) continue;
-        h->risk = risks[i];
-        h->rowidx = h->x_rowidx[e];
-        h->n_act_dev = h->x_nact[e];
-        h->kk = kks[i];
-        TRY(select_local(h, h->kk, h->band_log + 1 + i));
-        TRY(eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen));
-        if (cvar_idx)
-          CU(cudaMemcpyAsync(h->hidx + koff[i], h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream));
-        ++e;
-      }
+      TRY(select_all());
     }
     CU(cudaEventRecord(h->ev_side, h->side));
     h->sm_avail = h->num_sms - h->side_sms;
+    join = [h]() -> int {
+      h->sm_avail = h->num_sms;
+      CU(cudaStreamWaitEvent(h->stream, h->ev_side, 0));
+      return SDN_OK;
+    };
+  } else {
+    TRY(select_all());
   }
-  for (int i = 0; i < n_risks; ++i) {
-    const bool exact = risks[i].kind == SDN_RISK_CVAR_EXACT;
-    if (overlap && exact) continue;          // done on the side stream
-    h->risk = risks[i];
-    h->compacted = false;
-    h->selected = false;
-    if (exact) {
-      h->kk = kks[i];
-      TRY(select_local(h, h->kk, h->band_log + 1 + i));
-    }
-    TRY(eval_backward(h, h->stats_loc, h->partial_multi + (size_t)i * plen));
-    if (cvar_idx && exact)
-      CU(cudaMemcpyAsync(h->hidx + koff[i], h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost, h->stream));
-  }
-  if (overlap) {
-    h->sm_avail = h->num_sms;
-    CU(cudaStreamWaitEvent(h->stream, h->ev_side, 0));
-  }
+  h->risk = risks[0];
+  int rc = backward_multi(h, risks, n_risks, masks.data(), kks.data(), h->stats_loc, h->partial_multi, join);
+  h->sm_avail = h->num_sms;
+  if (rc) return rc;
   CU(cudaMemcpyAsync(h->hstats, h->stats_loc, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaMemcpyAsync(h->hpart_multi, h->partial_multi, sizeof(double) * n_risks * plen, cudaMemcpyDeviceToHost,
                      h->stream));
@@ -1254,13 +1379,12 @@ int sdn_eval_candidates(sdn_handle* h, int64_t k, double* cand_dev) {
   CU(cudaSetDevice(h->device));
   const int64_t kl = std::min<int64_t>(k, h->n);
   if (kl > 0) {
-    TRY(launch_topk(h, h->n, kl, h->Q, nullptr, h->sel));
-    h->launches++;
+    TRY(launch_topk(h, h->n, kl, sel_q(h), nullptr, h->sel));
     TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0));
   } else {
     CU(cudaMemsetAsync(h->n_act_dev, 0, sizeof(int), h->stream));
   }
-  k_export_candidates<<<(unsigned)cdiv(k, 256), 256, 0, h->stream>>>(k, h->n_act_dev, h->rowidx, h->Q, h->goff,
+  k_export_candidates<<<(unsigned)cdiv(k, 256), 256, 0, h->stream>>>(k, h->n_act_dev, h->rowidx, sel_q(h), h->goff,
                                                                       cand_dev);
   h->launches++;
   CHECK_LAUNCH(h);
@@ -1295,7 +1419,8 @@ int sdn_eval_refine_band(sdn_handle* h) {
   if (!h->fwd_done || !h->selected) return fail(SDN_ERR_STATE, "eval_select first");
   CU(cudaSetDevice(h->device));
   if (h->no_refine || h->n == 0) return SDN_OK;
-  TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, h->band_log + 1));
+  TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, h->band_log + 1, nullptr,
+                  sel_q(h)));
   h->selected = false;
   return SDN_OK;
 }
@@ -1332,6 +1457,13 @@ int sdn_eval_finish(sdn_handle* h, const double* stats_dev, const double* partia
 int sdn_last_q(sdn_handle* h, const double** q_dev, int64_t* n) {
   if (!h || !q_dev || !n) return fail(SDN_ERR_ARG, "null argument");
   *q_dev = h->Q;
+  *n = h->n;
+  return SDN_OK;
+}
+
+int sdn_last_qsel(sdn_handle* h, const double** q_dev, int64_t* n) {
+  if (!h || !q_dev || !n) return fail(SDN_ERR_ARG, "null argument");
+  *q_dev = h->qr_valid ? h->Qr : h->Q;
   *n = h->n;
   return SDN_OK;
 }

@@ -654,6 +654,9 @@ struct TileEpi<TcChain<EpiBwd>> {
 struct EpiBwdSum {
   const float* resid; const float* D; int64_t ldD; const int* rowidx; int64_t ld;
   double* part; int64_t ldp;
+  // unified sweep: per-row risk weights W[row * R + r] (sweep rows), one
+  // partial plane per risk (plane stride); W null = unit weights, R = 1
+  const double* W = nullptr; int R = 1; int64_t plane = 0;
   SDN_DEV void operator()(int64_t, int, float4) const {}
   SDN_DEV void col(int64_t, int, float) const {}
 };
@@ -686,14 +689,28 @@ struct TileEpi<EpiBwdSum> {
     for (int j = 0; j < 16; ++j) dd[j] = live ? dd[j] * g[j] : 0.0f;
     __syncwarp();
     row_put(s.f1, lane, dd);
+    // unified sweep: each lane stages its row's risk weights (fp64) in the
+    // residual staging buffer, free at this point
+    double* ws = reinterpret_cast<double*>(s.f0);
+    if (e.W)
+      for (int q = 0; q < e.R; ++q) ws[q * 32 + lane] = live ? e.W[(tr.r0 + lane) * e.R + q] : 0.0;
     __syncwarp();
     if (lane < 16 && c0 + lane < N) {
       const int j = lane;
-      double acc = 0.0;
-#pragma unroll 8
-      for (int r = 0; r < 32; ++r) acc += (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
       const int64_t prow = (tr.r0 >> 7) * 4 + ((tr.r0 >> 5) & 3);
-      e.part[prow * e.ldp + c0 + j] = acc;
+      if (!e.W) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) acc += (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
+        e.part[prow * e.ldp + c0 + j] = acc;
+      } else {
+        for (int q = 0; q < e.R; ++q) {
+          double acc = 0.0;
+#pragma unroll 8
+          for (int r = 0; r < 32; ++r) acc += ws[q * 32 + r] * (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
+          e.part[q * e.plane + prow * e.ldp + c0 + j] = acc;
+        }
+      }
     }
     __syncwarp();
   }

@@ -228,7 +228,7 @@ k_seed(int64_t n, const int* __restrict__ n_act_dev, const int* __restrict__ row
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < nr; r += (int64_t)gridDim.x * 8) {
     int64_t i = rowidx ? (int64_t)rowidx[r] : r;
-    double w = sample_weight(kind, Q[i], st, shift, beta, eps, t, kinv);
+    const double w = (kind == RISK_UNIT) ? 1.0 : sample_weight(kind, Q[i], st, shift, beta, eps, t, kinv);
     const float* p = (kphi ? kphi : phi) + i * r_u;
     for (int j = lane; j < r_u; j += 32)
     {
@@ -243,24 +243,158 @@ k_seed(int64_t n, const int* __restrict__ n_act_dev, const int* __restrict__ row
   }
 }
 
-// column sums of U (n_act x w) in fp64: part[by][c] over the rows
-// by, by + RB, ... (fixed order), block (32 x 8)
-__global__ void __launch_bounds__(256)
-k_colsum(int64_t n, const int* __restrict__ n_act_dev, int w, const float* __restrict__ U,
-         double* __restrict__ part) {
-  __shared__ double s[8][33];
-  int64_t nr = n_act_dev ? (int64_t)*n_act_dev : n;
-  int c = blockIdx.x * 32 + threadIdx.x;
-  double acc = 0.0;
-  if (c < w)
-    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < nr; r += (int64_t)gridDim.y * 8)
-      acc += (double)U[r * w + c];
-  s[threadIdx.y][threadIdx.x] = acc;
+// ---------------------------------------------------------------------------
+// Unified reverse sweep: one sweep with unit seeds gives the
+// per-sample VJPs u0_i = dQ_i/dS1; every risk's gradient is the weighted
+// column sum sum_i w_i^(r) u0_i (fp64), so all risks of an evaluation share
+// one sweep and the weights are only needed at the last reduction.
+constexpr int SDN_RMAX = 8;
+
+struct RiskSet {
+  int R;
+  int kind[SDN_RMAX];
+  double beta[SDN_RMAX], eps[SDN_RMAX], t[SDN_RMAX], kinv[SDN_RMAX];
+  const uint8_t* mask[SDN_RMAX];     // exact CVaR selection masks (sample rows)
+};
+
+SDN_DEV double risk_weight(const RiskSet& rs, int r, int64_t i, double q, const double* st, double shift) {
+  if (rs.kind[r] == RISK_CVAR_EXACT) return rs.mask[r][i] ? rs.kinv[r] : 0.0;
+  return sample_weight(rs.kind[r], q, st, shift, rs.beta[r], rs.eps[r], rs.t[r], 0.0);
+}
+
+SDN_DEV bool risk_active(const RiskSet& rs, int64_t i, double q) {
+  bool a = false;
+  for (int r = 0; r < rs.R; ++r) {
+    if (rs.kind[r] == RISK_CVAR_EXACT) a |= rs.mask[r][i] != 0;
+    else if (rs.kind[r] == RISK_CVAR_SMOOTH) a |= splus_d1_d(q - rs.t[r], rs.eps[r]) > 0.0;
+    else a = true;
+  }
+  return a;
+}
+
+// ordered compaction of the union of the risks' active rows (same scheme as
+// k_flag_count / k_compact)
+__global__ void __launch_bounds__(1024)
+k_union_count(int64_t n, RiskSet rs, const double* __restrict__ Q, int* __restrict__ counts) {
+  __shared__ int wc[32];
+  int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const bool f = i < n && risk_active(rs, i, Q[i]);
+  unsigned b = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = __popc(b);
   __syncthreads();
-  if (threadIdx.y == 0 && c < w) {
-    double t = 0.0;
-    for (int y = 0; y < 8; ++y) t += s[y][threadIdx.x];
-    part[(int64_t)blockIdx.y * w + c] = t;
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 32; ++w) s += wc[w];
+    counts[blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+k_union_compact(int64_t n, RiskSet rs, const double* __restrict__ Q, const int* __restrict__ offs,
+                int* __restrict__ rowidx) {
+  __shared__ int wbase[32];
+  int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const bool f = i < n && risk_active(rs, i, Q[i]);
+  unsigned b = __ballot_sync(0xffffffffu, f);
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wbase[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 32; ++w) { int c = wbase[w]; wbase[w] = s; s += c; }
+  }
+  __syncthreads();
+  if (f) rowidx[offs[blockIdx.x] + wbase[warp] + __popc(b & ((1u << lane) - 1u))] = (int)i;
+}
+
+// per-row risk weights of the sweep rows, W[j * R + r] (j = sweep row, i =
+// rowidx ? rowidx[j] : j), and per-block fixed-order partials of
+// sum_{w != 0} Q_i and #{w != 0} per risk (exact CVaR: the selection sum)
+__global__ void __launch_bounds__(256)
+k_weights(int64_t nsw, const int* __restrict__ n_act_dev, const int* __restrict__ rowidx, RiskSet rs,
+          const double* __restrict__ Q, const double* __restrict__ st, double shift, double* __restrict__ W,
+          double* __restrict__ part) {
+  __shared__ double sp[8][2 * SDN_RMAX];
+  const int64_t nr = n_act_dev ? (int64_t)*n_act_dev : nsw;
+  double acc[2 * SDN_RMAX];
+#pragma unroll
+  for (int f = 0; f < 2 * SDN_RMAX; ++f) acc[f] = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x; j < nr; j += (int64_t)gridDim.x * 256) {
+    const int64_t i = rowidx ? (int64_t)rowidx[j] : j;
+    const double q = Q[i];
+#pragma unroll
+    for (int r = 0; r < SDN_RMAX; ++r) {
+      if (r < rs.R) {
+        const double w = risk_weight(rs, r, i, q, st, shift);
+        W[j * rs.R + r] = w;
+        if (w != 0.0) { acc[2 * r] += q; acc[2 * r + 1] += 1.0; }
+      }
+    }
+  }
+  // fixed-order block reduction: lanes (butterfly), then warps in order
+#pragma unroll
+  for (int f = 0; f < 2 * SDN_RMAX; ++f) acc[f] = warp_sum(acc[f]);
+  if (lane == 0)
+    for (int f = 0; f < 2 * SDN_RMAX; ++f) sp[warp][f] = acc[f];
+  __syncthreads();
+  if (threadIdx.x < 2 * SDN_RMAX) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += sp[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * 2 * SDN_RMAX + threadIdx.x] = s;
+  }
+}
+
+// weighted column sums of U (n_act x w): part[r][by][c] = sum_rows W[row][r] U[row][c]
+__global__ void __launch_bounds__(256)
+k_colsum_w(int64_t n, const int* __restrict__ n_act_dev, int w, const float* __restrict__ U,
+           const double* __restrict__ Wt, int R, double* __restrict__ part) {
+  __shared__ double s[8][33];
+  const int64_t nr = n_act_dev ? (int64_t)*n_act_dev : n;
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  for (int r = 0; r < R; ++r) {
+    double acc = 0.0;
+    if (c < w)
+      for (int64_t j = (int64_t)blockIdx.y * 8 + threadIdx.y; j < nr; j += (int64_t)gridDim.y * 8)
+        acc += Wt[j * R + r] * (double)U[j * w + c];
+    s[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < w) {
+      double t = 0.0;
+      for (int y = 0; y < 8; ++y) t += s[y][threadIdx.x];
+      part[((int64_t)r * gridDim.y + blockIdx.y) * w + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// per-risk finalisation (blockIdx.y = risk): A = sum_rb part_r[rb][:];
+// out_r[k] = sum_c PzT[k][c] A[c]; out_r[d_z], out_r[d_z+1] = vsum[2r], vsum[2r+1]
+__global__ void __launch_bounds__(256)
+k_finalize_multi(int nrb, int64_t plane, int h1, int d_z, const double* __restrict__ part,
+                 const double* __restrict__ PzT, const double* __restrict__ vsum, int plen,
+                 double* __restrict__ out) {
+  extern __shared__ double A[];
+  const int r = blockIdx.y;
+  const double* pr = part ? part + (int64_t)r * plane : nullptr;
+  for (int c = threadIdx.x; c < h1; c += blockDim.x) {
+    double s = 0.0;
+    if (pr)
+      for (int b = 0; b < nrb; ++b) s += pr[(int64_t)b * h1 + c];
+    A[c] = s;
+  }
+  __syncthreads();
+  double* o = out + (int64_t)r * plen;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k = blockIdx.x * nw + warp; k < d_z; k += gridDim.x * nw) {
+    double s = 0.0;
+    for (int c = lane; c < h1; c += 32) s += PzT[(int64_t)k * h1 + c] * A[c];
+    s = warp_sum(s);
+    if (lane == 0) o[k] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    o[d_z] = vsum[2 * r];
+    o[d_z + 1] = vsum[2 * r + 1];
   }
 }
 
@@ -268,8 +402,10 @@ k_colsum(int64_t n, const int* __restrict__ n_act_dev, int w, const float* __res
 // for compacted sweeps: 4 partial rows per 128-row tile), fixed order
 __global__ void __launch_bounds__(1024)
 k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __restrict__ part,
-           double* __restrict__ out) {
+           double* __restrict__ out, int64_t plane = 0) {
   __shared__ double s[32][33];
+  part += blockIdx.y * plane;          // gridDim.y = risks (one partial plane each)
+  out += (int64_t)blockIdx.y * w;
   if (n_act_dev) nrb = min(nrb, ((*n_act_dev + 127) / 128) * 4);
   const int c = blockIdx.x * 32 + threadIdx.x;
   double acc = 0.0;
@@ -281,40 +417,6 @@ k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __re
     double t = 0.0;
     for (int y = 0; y < 32; ++y) t += s[y][threadIdx.x];
     out[c] = t;
-  }
-}
-
-// gradient finalisation on one block:
-//   A[c] = sum_rb part[rb][c]; out[k] = sum_c Pz[c][k] A[c]  (V_z W1_z^T A)
-//   exact CVaR extras: out[d_z] = sum_{selected} Q_i, out[d_z+1] = #selected
-__global__ void __launch_bounds__(1024)
-k_finalize_grad(int nrb, int h1, int d_z, const double* __restrict__ part, const double* __restrict__ Pz,
-                const int* __restrict__ rowidx, const int* __restrict__ n_act_dev,
-                const double* __restrict__ Q, int with_qsum, double* __restrict__ out) {
-  extern __shared__ double A[];   // h1
-  for (int c = threadIdx.x; c < h1; c += blockDim.x) {
-    double s = 0.0;
-    if (part) {
-#pragma unroll 8
-      for (int b = 0; b < nrb; ++b) s += part[(int64_t)b * h1 + c];
-    }
-    A[c] = s;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  // blocks share the outputs (the d_z x h1 projection is read by many SMs)
-  for (int k = blockIdx.x * nw + warp; k < d_z; k += gridDim.x * nw) {   // one warp per output
-    double s = 0.0;                               // PzT is d_z x h1: contiguous in c
-    for (int c = lane; c < h1; c += 32) s += Pz[(int64_t)k * h1 + c] * A[c];
-    s = warp_sum(s);
-    if (lane == 0) out[k] = s;
-  }
-  if (with_qsum && blockIdx.x == 0 && warp == nw - 1) {
-    int na = *n_act_dev;
-    double s = 0.0;
-    for (int r = lane; r < na; r += 32) s += Q[rowidx[r]];
-    s = warp_sum(s);
-    if (lane == 0) { out[d_z] = s; out[d_z + 1] = (double)na; }
   }
 }
 
@@ -403,33 +505,66 @@ k_topk_select(int64_t n, int64_t k, const double* __restrict__ vals, const doubl
 }
 
 // Same selection with the keys resident in shared memory (n <= TOPK_SMEM_MAX):
-// one global read, 8 histogram passes over SMEM, a warp-parallel digit search.
-constexpr int TOPK_SMEM_MAX = 24576;   // 192 KB of uint64 keys
+// one global read, then radix passes over SMEM only from the first byte in
+// which the keys differ (min/max common prefix skipped: Q values share sign,
+// exponent and leading mantissa bits), per-warp histograms (no cross-warp
+// atomic contention on the hot bins), a warp-parallel digit search.
+constexpr int TOPK_SMEM_MAX = 24576;   // 192 KB of uint64 keys (+ 32 KB warp histograms)
+constexpr size_t TOPK_SMEM_BYTES = (size_t)TOPK_SMEM_MAX * 8 + 32 * 256 * 4;
 
 __global__ void __launch_bounds__(1024)
 k_topk_select_smem(int n, int64_t k, const double* __restrict__ vals, const double* __restrict__ gidx,
                    uint8_t* __restrict__ mask, double* __restrict__ thr) {
   extern __shared__ uint64_t keys[];
+  unsigned* whist = reinterpret_cast<unsigned*>(keys + TOPK_SMEM_MAX);   // [32][256]
   __shared__ unsigned hist[256];
-  __shared__ uint64_t s_prefix;
+  __shared__ uint64_t s_prefix, s_min[32], s_max[32];
   __shared__ long long s_krem;
   __shared__ int wsum[32];
-  __shared__ long long s_run;
+  __shared__ int s_first;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < n; i += blockDim.x)
-    keys[i] = (gidx && gidx[i] < 0.0) ? 0ull : dkey(vals[i]);   // padding: key 0, below every value
-  if (tid == 0) { s_prefix = 0; s_krem = k; }
-  uint64_t himask = 0;
+  uint64_t kmin = ~0ull, kmax = 0ull;
+#pragma unroll 4
+  for (int i = tid; i < n; i += blockDim.x) {
+    const uint64_t key = (gidx && gidx[i] < 0.0) ? 0ull : dkey(vals[i]);   // padding: key 0, below every value
+    keys[i] = key;
+    kmin = min(kmin, key);
+    kmax = max(kmax, key);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) { s_min[warp] = kmin; s_max[warp] = kmax; }
   __syncthreads();
-  for (int pass = 0; pass < 8; ++pass) {
+  if (tid == 0) {
+    uint64_t a = ~0ull, b = 0ull;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a = min(a, s_min[w]); b = max(b, s_max[w]); }
+    const int cp = (a == b) ? 8 : __clzll((long long)(a ^ b)) / 8;      // common leading bytes
+    s_first = cp;
+    s_prefix = (cp == 0) ? 0ull : (cp >= 8 ? a : (a & (~0ull << (64 - 8 * cp))));
+    s_krem = k;
+  }
+  __syncthreads();
+  const int first = s_first;
+  uint64_t himask = (first == 0) ? 0ull : (first >= 8 ? ~0ull : (~0ull << (64 - 8 * first)));
+  for (int pass = first; pass < 8; ++pass) {
     const int shift = 56 - 8 * pass;
-    if (tid < 256) hist[tid] = 0;
+    for (int d = tid; d < 32 * 256; d += blockDim.x) whist[d] = 0;
     __syncthreads();
     const uint64_t prefix = s_prefix;
+    unsigned* wh = whist + warp * 256;
     for (int base = 0; base < n; base += blockDim.x) {
       const int i = base + tid;
       const uint64_t key = i < n ? keys[i] : 0ull;
-      hist_add(hist, i < n && (key & himask) == prefix, (unsigned)(key >> shift) & 255u);
+      if (i < n && (key & himask) == prefix) atomicAdd(&wh[(unsigned)(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int d = tid; d < 256; d += blockDim.x) {
+      unsigned c = 0;
+#pragma unroll 8
+      for (int w = 0; w < 32; ++w) c += whist[w * 256 + d];
+      hist[d] = c;
     }
     __syncthreads();
     if (warp == 0) {
@@ -462,28 +597,39 @@ k_topk_select_smem(int n, int64_t k, const double* __restrict__ vals, const doub
     __syncthreads();
   }
   const uint64_t T = s_prefix;
-  const long long need = s_krem;
+  const long long need = s_krem;       // how many threshold-equal keys to take
   if (thr && tid == 0) *thr = dkey_inv(T);
-  if (tid == 0) s_run = 0;
+  // tie resolution in index order: each thread owns a contiguous run of
+  // keys; one block-wide exclusive scan of the threshold-equal counts
+  const int per = (n + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int i0 = tid * per, i1 = min(i0 + per, n);
+  int cnt = 0;
+  for (int i = i0; i < i1; ++i) cnt += (keys[i] != 0ull && keys[i] == T) ? 1 : 0;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
   __syncthreads();
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int i = base + tid;
-    const uint64_t key = i < n ? keys[i] : 0ull;
-    const bool valid = i < n && key != 0ull;
-    const bool eq = valid && key == T;
-    const unsigned b = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) wsum[warp] = __popc(b);
-    __syncthreads();
-    if (tid == 0) {
-      int s = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { int cc = wsum[w]; wsum[w] = s; s += cc; }
+  if (warp == 0) {
+    int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0, x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
     }
-    __syncthreads();
-    const long long rank = s_run + wsum[warp] + __popc(b & ((1u << lane) - 1u));
-    if (i < n) mask[i] = (valid && (key > T || (eq && rank < need))) ? 1 : 0;
-    __syncthreads();
-    if (tid == blockDim.x - 1) s_run += wsum[warp] + __popc(b);
-    __syncthreads();
+    wsum[lane] = x - v;               // exclusive warp offsets
+  }
+  __syncthreads();
+  long long rank = wsum[warp] + (incl - cnt);
+  for (int i = i0; i < i1; ++i) {
+    const uint64_t key = keys[i];
+    const bool valid = key != 0ull;
+    const bool eq = valid && key == T;
+    mask[i] = (valid && (key > T || (eq && rank < need))) ? 1 : 0;
+    rank += eq ? 1 : 0;
   }
 }
 
@@ -522,12 +668,6 @@ __global__ void k_scatter_selection(int64_t ncand, const uint8_t* __restrict__ c
     int64_t g = (int64_t)gidx[e] - goff;
     if (g >= 0 && g < n) sel[g] = 1;
   }
-}
-
-// fp64 -> fp32 / fp32 -> fp64 conversions and small helpers
-__global__ void k_f32_to_f64(int64_t n, const float* __restrict__ a, double* __restrict__ b) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = a[i];
 }
 
 // strided copy of G (n x ldg) -> dense (n x d_z) fp64

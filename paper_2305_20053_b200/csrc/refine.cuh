@@ -59,7 +59,21 @@ struct RefineArgs {
   double* Q;
   // exact CVaR: reselect among the band rows (null = no reselection)
   uint8_t* mask;
+  // phase 0 (k > 0): the exact top-k selection itself (value desc, index
+  // asc) over Q -> mask and the threshold (written to *tdev), cooperative
+  int64_t k;
+  unsigned* ghist;              // 2 x gridDim.x x 256 scratch
+  unsigned long long* gmm;      // 2 x gridDim.x scratch (min / max keys)
+  int refine;                   // 0: selection only
+  unsigned long long* trace;    // optional phase timestamps (block 0, %globaltimer)
 };
+
+SDN_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define REF_STAMP(slot) do { if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[(slot)] = gtime(); } while (0)
 
 // Data written inside this kernel by other blocks (rowidx, the layer
 // ping-pong, Q) is read with ld.global.cg (L2): L1 is not coherent across SMs.
@@ -108,19 +122,220 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   __shared__ int s_w[REF_THREADS / 32], s_m[REF_THREADS / 32];
   __shared__ unsigned s_gen;
   __shared__ int s_need;
+  __shared__ unsigned s_hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ long long s_krem;
+  __shared__ unsigned long long s_mm[2][REF_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned G = gridDim.x;
+  REF_STAMP(0);
   if (tid == 0) s_gen = *(volatile unsigned*)&a.bar[1];
   __syncthreads();
   unsigned gen = s_gen;
-
-  // ---- 1. band flags and ordered compaction (contiguous slice per block)
-  const int64_t per = (a.n + G - 1) / G;
+  const int64_t per = (a.n + G - 1) / G;          // contiguous slice per block (index order)
   const int64_t lo = min((int64_t)blockIdx.x * per, a.n), hi = min(lo + per, a.n);
+  const int gw = blockIdx.x * (REF_THREADS / 32) + warp, nw = G * (REF_THREADS / 32);
+  if (a.refine) {                                 // W rows of every layer -> L2 now (overlaps phases 0-1)
+    for (int l = 0; l < a.L; ++l) {
+      const RefineLayer& ly = a.layer[l];
+      for (int c = gw; c < ly.N; c += nw) {
+        const char* row = reinterpret_cast<const char*>(ly.W + (int64_t)c * ly.K);
+        for (int o = lane * 128; o < ly.K * 4; o += 32 * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+      }
+    }
+  }
+
+  // ---- 0. exact top-k (k > 0): cooperative MSD radix select on order-
+  // preserving keys, from the first byte in which the keys differ; per-block
+  // 256-bin histograms summed by every block (identical decisions), ties
+  // taken in index order via per-block counts of threshold-equal keys
+  double thr = 0.0;
+  if (a.k > 0) {
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
+      const unsigned long long key = dkey(a.Q[i]);
+      kmin = min(kmin, key);
+      kmax = max(kmax, key);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) { s_mm[0][warp] = kmin; s_mm[1][warp] = kmax; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < REF_THREADS / 32; ++w) { kmin = min(kmin, s_mm[0][w]); kmax = max(kmax, s_mm[1][w]); }
+      a.gmm[blockIdx.x] = kmin;
+      a.gmm[G + blockIdx.x] = kmax;
+    }
+    grid_barrier(a.bar, gen);
+    REF_STAMP(1);
+    {                                              // parallel loads, warp reductions
+      unsigned long long x = ~0ull, y = 0ull;
+      for (unsigned b = tid; b < G; b += REF_THREADS) { x = min(x, __ldcg(a.gmm + b)); y = max(y, __ldcg(a.gmm + G + b)); }
+      for (int o = 16; o > 0; o >>= 1) {
+        x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+        y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
+      }
+      __syncthreads();
+      if (lane == 0) { s_mm[0][warp] = x; s_mm[1][warp] = y; }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      unsigned long long x = s_mm[0][0], y = s_mm[1][0];
+      for (int w = 1; w < REF_THREADS / 32; ++w) { x = min(x, s_mm[0][w]); y = max(y, s_mm[1][w]); }
+      const int cp = (x == y) ? 8 : __clzll((long long)(x ^ y)) / 8;
+      s_w[0] = cp;
+      s_prefix = (cp == 0) ? 0ull : (cp >= 8 ? x : (x & (~0ull << (64 - 8 * cp))));
+      s_krem = a.k;
+    }
+    __syncthreads();
+    const int first = s_w[0];
+    unsigned long long himask = (first == 0) ? 0ull : (first >= 8 ? ~0ull : (~0ull << (64 - 8 * first)));
+    bool early = false;
+    unsigned long long tmin = 0ull;
+    if (tid == 0) s_need = 0;
+    __syncthreads();
+    for (int pass = first; pass < 8; ++pass) {
+      const int shift = 56 - 8 * pass;
+      const unsigned long long prefix = s_prefix;
+      for (int d = tid; d < 256; d += REF_THREADS) s_hist[d] = 0;
+      __syncthreads();
+      for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
+        const unsigned long long key = dkey(a.Q[i]);
+        if ((key & himask) == prefix) atomicAdd(&s_hist[(unsigned)(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      unsigned* gh = a.ghist + (size_t)(pass & 1) * G * 256;
+      for (int d = tid; d < 256; d += REF_THREADS) gh[blockIdx.x * 256 + d] = s_hist[d];
+      grid_barrier(a.bar, gen);
+      for (int d = tid; d < 256; d += REF_THREADS) {
+        unsigned c = 0;
+#pragma unroll 16
+        for (unsigned b = 0; b < G; ++b) c += __ldcg(gh + b * 256 + d);   // unrolled: loads in flight
+        s_hist[d] = c;
+      }
+      __syncthreads();
+      if (warp == 0) {                             // lane l owns digits 255-8l .. 248-8l
+        unsigned c[8], t8 = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { c[i] = s_hist[255 - 8 * lane - i]; t8 += c[i]; }
+        unsigned incl = t8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const long long krem = s_krem;
+        const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= krem);
+        const int L = hit ? __ffs(hit) - 1 : 31;
+        if (lane == L) {
+          long long cum = (long long)(incl - t8);
+          int d = 255 - 8 * lane;
+          for (int i = 0; i < 8; ++i) {
+            d = 255 - 8 * lane - i;
+            if (cum + (long long)c[i] >= krem || i == 7) break;
+            cum += c[i];
+          }
+          s_krem = krem - cum;
+          s_prefix = prefix | ((unsigned long long)d << shift);
+          s_need = (krem - cum == (long long)c[(255 - 8 * lane) - d]) ? 1 : 0;   // whole bucket taken
+        }
+      }
+      himask |= (0xFFull << shift);
+      __syncthreads();
+      REF_STAMP(2 + pass);
+      if (s_need && pass < 7) {
+        // early exit: the k-th falls at the bottom of a bucket that is taken
+        // whole, so the selection is {key >= Tlow}; the threshold value (the
+        // band centre) is the smallest selected key
+        const unsigned long long Tlow = s_prefix;
+        unsigned long long mn = ~0ull;
+        for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
+          const unsigned long long key = dkey(a.Q[i]);
+          a.mask[i] = key >= Tlow ? 1 : 0;
+          if (key >= Tlow) mn = min(mn, key);
+        }
+        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        __syncthreads();
+        if (lane == 0) s_mm[0][warp] = mn;
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 1; w < REF_THREADS / 32; ++w) mn = min(mn, s_mm[0][w]);
+          a.gmm[blockIdx.x] = mn;
+        }
+        grid_barrier(a.bar, gen);
+        mn = ~0ull;
+        for (unsigned b = tid; b < G; b += REF_THREADS) mn = min(mn, __ldcg(a.gmm + b));
+        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        __syncthreads();
+        if (lane == 0) s_mm[0][warp] = mn;
+        __syncthreads();
+        for (int w = 0; w < REF_THREADS / 32; ++w) mn = min(mn, s_mm[0][w]);
+        early = true;
+        tmin = mn;
+        break;
+      }
+    }
+    if (early) {
+      thr = dkey_inv(tmin);
+      if (blockIdx.x == 0 && tid == 0) *const_cast<double*>(a.tdev) = thr;
+      REF_STAMP(10);
+      if (!a.refine) return;
+    } else {
+    const unsigned long long T = s_prefix;
+    const long long need = s_krem;                 // threshold-equal keys to take, lowest index first
+    thr = dkey_inv(T);
+    if (blockIdx.x == 0 && tid == 0) *const_cast<double*>(a.tdev) = thr;
+    int eq = 0;
+    for (int64_t i = lo + tid; i < hi; i += REF_THREADS) eq += (dkey(a.Q[i]) == T) ? 1 : 0;
+    eq = warp_sum_i(eq);
+    if (lane == 0) s_w[warp] = eq;
+    __syncthreads();
+    if (tid == 0) {
+      int e = 0;
+      for (int w = 0; w < REF_THREADS / 32; ++w) e += s_w[w];
+      a.blockcnt[blockIdx.x] = e;
+    }
+    grid_barrier(a.bar, gen);
+    long long run = 0;                             // threshold-equal keys in earlier blocks
+    {
+      int pr = 0;
+      for (unsigned b = tid; b < blockIdx.x; b += REF_THREADS) pr += __ldcg(a.blockcnt + b);
+      pr = warp_sum_i(pr);
+      __syncthreads();
+      if (lane == 0) s_w[warp] = pr;
+      __syncthreads();
+      for (int w = 0; w < REF_THREADS / 32; ++w) run += s_w[w];
+      __syncthreads();
+    }
+    for (int64_t base = lo; base < hi; base += REF_THREADS) {
+      const int64_t i = base + tid;
+      const unsigned long long key = i < hi ? dkey(a.Q[i]) : 0ull;
+      const bool e = i < hi && key == T;
+      const unsigned bal = __ballot_sync(0xffffffffu, e);
+      int t2;
+      const int wb = block_excl(s_w, warp, lane, __popc(bal), t2);
+      const long long rank = run + wb + __popc(bal & ((1u << lane) - 1u));
+      if (i < hi) a.mask[i] = (key > T || (e && rank < need)) ? 1 : 0;
+      run += t2;
+    }
+    REF_STAMP(10);
+    if (!a.refine) return;
+    grid_barrier(a.bar, gen);                      // blockcnt is reused below
+    }
+  }
+
+  // ---- 1. band flags and ordered compaction
+  auto band = [&](int64_t i) -> bool {
+    return a.kind == RISK_BAND_EXACT ? in_band_exact(a.Q[i], a.k > 0 ? thr : *a.tdev)
+                                     : row_flag(a.kind, a.Q, nullptr, i, a.t, a.eps, a.tdev);
+  };
   int mine = 0;
   for (int64_t base = lo; base < hi; base += REF_THREADS) {
     const int64_t i = base + tid;
-    const bool f = i < hi && row_flag(a.kind, a.Q, nullptr, i, a.t, a.eps, a.tdev);
+    const bool f = i < hi && band(i);
     const unsigned b = __ballot_sync(0xffffffffu, f);
     mine += (lane == 0) ? __popc(b) : 0;
   }
@@ -146,7 +361,7 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   }
   for (int64_t base = lo; base < hi; base += REF_THREADS) {
     const int64_t i = base + tid;
-    const bool f = i < hi && row_flag(a.kind, a.Q, nullptr, i, a.t, a.eps, a.tdev);
+    const bool f = i < hi && band(i);
     const unsigned b = __ballot_sync(0xffffffffu, f);
     int t2;
     const int wb = block_excl(s_w, warp, lane, __popc(b), t2);
@@ -154,19 +369,12 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     off += t2;
   }
   if (blockIdx.x == 0 && tid == 0) *a.count = m;
+  REF_STAMP(11);
   if (m == 0 || m > a.cap_rows) return;          // uniform: every block computed the same m
   grid_barrier(a.bar, gen);
+  REF_STAMP(12);
 
   // ---- 2. fp64 chain over the m band rows
-  const int gw = blockIdx.x * (REF_THREADS / 32) + warp, nw = G * (REF_THREADS / 32);
-  for (int l = 0; l < a.L; ++l) {                // W rows of every layer -> L2 now
-    const RefineLayer& ly = a.layer[l];
-    for (int c = gw; c < ly.N; c += nw) {
-      const char* row = reinterpret_cast<const char*>(ly.W + (int64_t)c * ly.K);
-      for (int o = lane * 128; o < ly.K * 4; o += 32 * 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
-    }
-  }
   for (int l = 0; l < a.L; ++l) {
     const RefineLayer& ly = a.layer[l];
     const int K = ly.K, N = ly.N;
@@ -236,7 +444,9 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
       }
       __syncthreads();
     }
+    REF_STAMP(13 + 2 * l);
     grid_barrier(a.bar, gen);
+    REF_STAMP(14 + 2 * l);
   }
 
   // ---- 3. QoI of the band rows -> Q (reduced: phi.(phi + 2c); decoded: phi.(K phi + 2c))
@@ -257,8 +467,10 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     s = warp_sum(s);
     if (lane == 0) a.Q[__ldcg(a.rowidx + r)] = s + a.q0;
   }
+  REF_STAMP(40);
   if (!a.mask) return;
   grid_barrier(a.bar, gen);
+  REF_STAMP(41);
 
   // ---- 4. exact CVaR: the band holds `need` selected rows (rows outside keep
   // their side of the threshold); take the top `need` band rows by
@@ -267,7 +479,7 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   if (tid == 0) s_need = 0;
   __syncthreads();
   int cnt = 0;
-  for (int r = tid; r < m; r += REF_THREADS) cnt += a.mask[__ldcg(a.rowidx + r)] ? 1 : 0;
+  for (int r = tid; r < m; r += REF_THREADS) cnt += __ldcg(a.mask + __ldcg(a.rowidx + r)) ? 1 : 0;
   atomicAdd(&s_need, cnt);
   __syncthreads();
   const int need = s_need;
@@ -287,6 +499,7 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   __syncthreads();                               // every rank computed from the pre-update mask
   t = 0;
   for (int r = tid; r < m && t < 16; r += REF_THREADS, ++t) a.mask[__ldcg(a.rowidx + r)] = selr[t] ? 1 : 0;
+  REF_STAMP(42);
 }
 
 }  // namespace sdn

@@ -269,12 +269,14 @@ class Engine:
         self._phase_risk = risk
         check(lib.sdn_eval_set_risk(self.h, C.byref(risk)), "sdn_eval_set_risk")
 
-    def last_q(self) -> np.ndarray:
-        """Per-sample Q of the last evaluation as the engine used it (after
-        Q refinement), copied to the host (sdn_last_q)."""
+    def last_q(self, selection: bool = False) -> np.ndarray:
+        """Per-sample Q of the last evaluation, copied to the host: the chain's
+        Q (smoothed-CVaR window rows refined), or with selection=True the copy
+        the exact-CVaR selection used (threshold band refined in fp64)."""
         import torch
         ptr, n = C.c_void_p(), C.c_int64()
-        check(lib.sdn_last_q(self.h, C.byref(ptr), C.byref(n)), "sdn_last_q")
+        fn = lib.sdn_last_qsel if selection else lib.sdn_last_q
+        check(fn(self.h, C.byref(ptr), C.byref(n)), "sdn_last_q")
         self.synchronize()
 
         class _View:

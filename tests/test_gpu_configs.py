@@ -102,10 +102,11 @@ def test_c4_full_n_properties():
     eng.set_samples(p.m_r)
     r = eng.eval(p.z, "cvar_exact", beta=0.99)
     assert r.idx.size == 1311                      # ceil(0.01 * 131072)
-    Qr = eng.last_q()                              # Q as used (threshold band refined in fp64)
+    Qr = eng.last_q(selection=True)                # Q the selection used (threshold band in fp64)
     assert r.n_refined >= 1
     np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qr, 0.99)))
-    assert abs(r.value - Qr[r.idx].mean()) <= 1e-9 * abs(r.value)
+    Qc = eng.last_q()                              # chain Q: the value is its mean over the selection
+    assert abs(r.value - Qc[r.idx].mean()) <= 1e-9 * abs(r.value)
     Q, G = eng.eval_samples(p.z)
     assert _rel(r.grad_z, G[r.idx].mean(0)) <= 1e-5
     # and a 2048-sample slice against the float64 oracle

@@ -65,7 +65,7 @@ def test_c2_shapes_all_risks(kind):
         # bit-exact selection vs the fp64 oracle (rows near the threshold are
         # re-evaluated in fp64), and the oracle's rule on the engine's own Q
         np.testing.assert_array_equal(np.sort(r.idx), np.sort(o["idx"]))
-        np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(eng.last_q(), 0.95)))
+        np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(eng.last_q(selection=True), 0.95)))
         assert r.n_refined >= 1
 
 
