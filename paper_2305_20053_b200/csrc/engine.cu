@@ -209,6 +209,12 @@ struct sdn_handle {
   double* c64dec = nullptr;
   bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
   bool ref_trace = false;       // env SDN_REFINE_TRACE=1
+  // CUDA graph of the last evaluation configuration (sdn_eval_multi)
+  bool use_graphs = true;       // env SDN_NO_GRAPH=1 disables
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<double> gkey;
+  int64_t glaunches = 0;
+  int64_t gen = 0;              // bumped by every set_* call (invalidates the graph)
   unsigned long long* ref_trace_dev = nullptr;
   bool selected = false;        // exact CVaR selection done
   int64_t kk = 0;               // exact CVaR k (global)
@@ -572,6 +578,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   { const char* e = getenv("SDN_NO_REFINE"); h->no_refine = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_OVERLAP"); h->no_overlap = e && e[0] == '1'; }
   { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
+  { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
   { const char* e = getenv("SDN_SIDE_SMS");
     if (e) h->side_sms = std::max(1, std::min(atoi(e), h->num_sms / 2)); }
   h->tcw.enabled = false;
@@ -616,6 +623,7 @@ int sdn_destroy(sdn_handle* h) {
   if (h->hpart_multi) cudaFreeHost(h->hpart_multi);
   if (h->hidx) cudaFreeHost(h->hidx);
   tc_free(h->tcw);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->ev_fwd) cudaEventDestroy(h->ev_fwd);
   if (h->ev_side) cudaEventDestroy(h->ev_side);
@@ -698,6 +706,7 @@ int sdn_set_model(sdn_handle* h, const float* const* W, const float* const* b, c
   if (h->tcw.enabled) TRY(tc_set_weights(h, h->tcw));
   h->have_model = true;
   h->have_mean = false;
+  h->gen++;
   return SDN_OK;
 }
 
@@ -708,6 +717,7 @@ int sdn_set_tracking(sdn_handle* h, const float* c, double q0) {
   h->q0 = q0;
   h->have_form = true;
   h->have_mean = false;
+  h->gen++;
   return SDN_OK;
 }
 
@@ -722,6 +732,7 @@ int sdn_set_samples(sdn_handle* h, const float* m_r, int64_t n, int64_t global_o
   h->n = n;
   h->goff = global_offset;
   h->fwd_done = false;
+  h->gen++;
   if (h->tcw.enabled) TRY(tc_set_samples(h, h->tcw, h->MR, n));
   return SDN_OK;
 }
@@ -1200,82 +1211,30 @@ int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* r
              int64_t* cvar_idx) {
   if (!h || !z || !risk) return fail(SDN_ERR_ARG, "null argument");
   if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
-  TRY(eval_forward(h, z, risk, h->stats_loc, risk->need_grad != 0));
-  if (risk->kind == SDN_RISK_CVAR_EXACT) {
-    h->kk = std::max(ceil_count((1.0 - risk->beta) * (double)h->n), 1);   // riskopt.py:80
-    TRY(select_local(h, h->kk, h->band_log + 1));
-  }
-  TRY(eval_backward(h, h->stats_loc, h->partial_loc));
-  TRY(eval_finish(h, h->stats_loc, h->partial_loc, res, grad_z, 1));
-  if (cvar_idx && risk->kind == SDN_RISK_CVAR_EXACT) {
-    std::vector<int> idx(h->kk);
-    CU(cudaMemcpy(idx.data(), h->rowidx, sizeof(int) * h->kk, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < h->kk; ++i) cvar_idx[i] = h->goff + idx[i];
-  }
-  return SDN_OK;
+  return sdn_eval_multi(h, z, risk, 1, res, grad_z, risk->kind == SDN_RISK_CVAR_EXACT ? cvar_idx : nullptr);
 }
 
-// several risk functionals from ONE forward pass (e.g. c2: mean+variance and
-// exact CVaR): the activations/derivatives are kept, each risk runs its own
-// (possibly compacted) reverse sweep.  At most one smoothed-CVaR entry (its
-// t/eps feed the forward-time moments).
-int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks, sdn_result* res,
-                   double* grads, int64_t* cvar_idx) {
-  if (!h || !z || !risks || n_risks < 1 || !res) return fail(SDN_ERR_ARG, "null argument");
-  if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
-  int smooth = -1, any_grad = 0;
-  for (int i = 0; i < n_risks; ++i) {
-    TRY(check_risk(&risks[i]));
-    if (risks[i].qoi != risks[0].qoi) return fail(SDN_ERR_ARG, "all risks must share the QoI frame");
-    if (risks[i].kind == SDN_RISK_CVAR_SMOOTH) {
-      if (smooth >= 0) return fail(SDN_ERR_ARG, "at most one smoothed CVaR per multi-evaluation");
-      smooth = i;
-    }
-    any_grad |= risks[i].need_grad;
-  }
-  // device work of every risk is queued back to back; one host sync at the end
+// several risk functionals from ONE forward pass and ONE reverse sweep (e.g.
+// c2: mean+variance and exact CVaR).  At most one smoothed-CVaR entry (its
+// t/eps feed the forward-time moments and window refinement).
+//
+// The device work is enqueued by enqueue_multi (no host sync inside); for a
+// repeated configuration without a smoothed CVaR (whose t changes every
+// optimizer step) it is captured once into a CUDA graph and replayed: one
+// launch per evaluation instead of ~30, which is what bounds small
+// problems (c1).  Host-side per-call state (z and its norm) is refreshed on
+// every call; the graph's memcpy node reads z from the pinned staging buffer.
+static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks, bool want_idx,
+                         const std::vector<int64_t>& kks, const std::vector<int64_t>& koff, int smooth,
+                         bool any_grad) {
   const int plen = h->plen();
-  int64_t ktot = 0;
-  for (int i = 0; i < n_risks; ++i)
-    if (risks[i].kind == SDN_RISK_CVAR_EXACT) ktot += std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);
-  if (n_risks > h->multi_cap || ktot > h->hidx_cap) {
-    if (h->partial_multi) cudaFree(h->partial_multi);
-    if (h->hpart_multi) cudaFreeHost(h->hpart_multi);
-    if (h->hidx) cudaFreeHost(h->hidx);
-    h->multi_cap = std::max(n_risks, 4);
-    h->hidx_cap = std::max<int64_t>(ktot, 1);
-    CU(cudaMalloc(&h->partial_multi, sizeof(double) * h->multi_cap * plen));
-    CU(cudaHostAlloc((void**)&h->hpart_multi, sizeof(double) * h->multi_cap * plen, 0));
-    CU(cudaHostAlloc((void**)&h->hidx, sizeof(int) * h->hidx_cap, 0));
-  }
-  if (n_risks + 1 > h->band_cap) {
-    int* bl = nullptr;
-    int* hb = nullptr;
-    CU(cudaMalloc(&bl, sizeof(int) * (n_risks + 1)));
-    CU(cudaHostAlloc((void**)&hb, sizeof(int) * (n_risks + 1), 0));
-    h->allocs.push_back(bl);
-    if (h->hband) cudaFreeHost(h->hband);
-    h->band_log = bl;                // (the old block stays in allocs until destroy)
-    h->hband = hb;
-    h->band_cap = n_risks + 1;
-  }
-  TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad != 0));
-  // CVaR index offsets in risk order
-  std::vector<int64_t> koff(n_risks, -1), kks(n_risks, 0);
-  int64_t off = 0;
   int n_exact = 0;
-  for (int i = 0; i < n_risks; ++i)
-    if (risks[i].kind == SDN_RISK_CVAR_EXACT) {
-      kks[i] = std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);   // riskopt.py:80
-      koff[i] = off;
-      off += kks[i];
-      ++n_exact;
-    }
-  // exact-CVaR selections: a mask and an ordered index list per exact risk
-  TRY(ensure_xsel(h, n_exact));
   bool dense = false;
-  for (int i = 0; i < n_risks; ++i)
+  for (int i = 0; i < n_risks; ++i) {
+    n_exact += risks[i].kind == SDN_RISK_CVAR_EXACT;
     dense |= risks[i].kind == SDN_RISK_MEAN || risks[i].kind == SDN_RISK_MEANVAR;
+  }
+  TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad));
   std::vector<const uint8_t*> masks(n_risks, nullptr);
   auto select_all = [&]() -> int {
     for (int i = 0, e = 0; i < n_risks; ++i) {
@@ -1283,7 +1242,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       h->risk = risks[i];
       TRY(select_local(h, kks[i], h->band_log + 1 + i, h->x_mask[e], h->x_rowidx[e], h->x_nact[e]));
       masks[i] = h->x_mask[e];
-      if (cvar_idx)
+      if (want_idx)
         CU(cudaMemcpyAsync(h->hidx + koff[i], h->x_rowidx[e], sizeof(int) * kks[i], cudaMemcpyDeviceToHost,
                            h->stream));
       ++e;
@@ -1300,7 +1259,6 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   const bool overlap = dense && n_exact > 0 && !h->prof && !h->no_overlap;
   std::function<int()> join;
   if (overlap) {
-    TRY(ensure_side(h));
     CU(cudaEventRecord(h->ev_fwd, h->stream));
     CU(cudaStreamWaitEvent(h->side, h->ev_fwd, 0));
     {
@@ -1325,6 +1283,126 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   CU(cudaMemcpyAsync(h->hpart_multi, h->partial_multi, sizeof(double) * n_risks * plen, cudaMemcpyDeviceToHost,
                      h->stream));
   CU(cudaMemcpyAsync(h->hband, h->band_log, sizeof(int) * (n_risks + 1), cudaMemcpyDeviceToHost, h->stream));
+  return SDN_OK;
+}
+
+// graph cache key of an evaluation configuration
+static std::vector<double> graph_key(sdn_handle* h, const sdn_risk* risks, int n_risks, bool want_idx) {
+  std::vector<double> k{(double)h->gen, (double)h->n, (double)n_risks, want_idx ? 1.0 : 0.0};
+  for (int i = 0; i < n_risks; ++i) {
+    k.push_back(risks[i].kind);
+    k.push_back(risks[i].qoi);
+    k.push_back(risks[i].beta);
+    k.push_back(risks[i].eps);
+    k.push_back(risks[i].need_grad);
+  }
+  return k;
+}
+
+static void drop_graph(sdn_handle* h) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  h->gexec = nullptr;
+  h->gkey.clear();
+}
+
+int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks, sdn_result* res,
+                   double* grads, int64_t* cvar_idx) {
+  if (!h || !z || !risks || n_risks < 1 || !res) return fail(SDN_ERR_ARG, "null argument");
+  if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
+  if (n_risks > SDN_RMAX) return fail(SDN_ERR_ARG, "at most 8 risks per evaluation");
+  int smooth = -1, any_grad = 0;
+  for (int i = 0; i < n_risks; ++i) {
+    TRY(check_risk(&risks[i]));
+    if (risks[i].qoi != risks[0].qoi) return fail(SDN_ERR_ARG, "all risks must share the QoI frame");
+    if (risks[i].kind == SDN_RISK_CVAR_SMOOTH) {
+      if (smooth >= 0) return fail(SDN_ERR_ARG, "at most one smoothed CVaR per multi-evaluation");
+      smooth = i;
+    }
+    any_grad |= risks[i].need_grad;
+  }
+  if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
+  if (risks[0].qoi == SDN_QOI_REDUCED && !h->have_form) return fail(SDN_ERR_STATE, "set_tracking first");
+  if (risks[0].qoi == SDN_QOI_DECODED && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  CU(cudaSetDevice(h->device));
+  // host-side buffers (never allocated while a graph is being captured)
+  const int plen = h->plen();
+  std::vector<int64_t> koff(n_risks, -1), kks(n_risks, 0);
+  int64_t ktot = 0;
+  int n_exact = 0;
+  bool dense = false;
+  for (int i = 0; i < n_risks; ++i) {
+    dense |= risks[i].kind == SDN_RISK_MEAN || risks[i].kind == SDN_RISK_MEANVAR;
+    if (risks[i].kind == SDN_RISK_CVAR_EXACT) {
+      kks[i] = std::max(ceil_count((1.0 - risks[i].beta) * (double)h->n), 1);   // riskopt.py:80
+      koff[i] = ktot;
+      ktot += kks[i];
+      ++n_exact;
+    }
+  }
+  if (n_risks > h->multi_cap || ktot > h->hidx_cap) {
+    drop_graph(h);
+    if (h->partial_multi) cudaFree(h->partial_multi);
+    if (h->hpart_multi) cudaFreeHost(h->hpart_multi);
+    if (h->hidx) cudaFreeHost(h->hidx);
+    h->multi_cap = std::max(n_risks, 4);
+    h->hidx_cap = std::max<int64_t>(ktot, 1);
+    CU(cudaMalloc(&h->partial_multi, sizeof(double) * h->multi_cap * plen));
+    CU(cudaHostAlloc((void**)&h->hpart_multi, sizeof(double) * h->multi_cap * plen, 0));
+    CU(cudaHostAlloc((void**)&h->hidx, sizeof(int) * h->hidx_cap, 0));
+  }
+  if (n_risks + 1 > h->band_cap) {
+    drop_graph(h);
+    int* bl = nullptr;
+    int* hb = nullptr;
+    CU(cudaMalloc(&bl, sizeof(int) * (n_risks + 1)));
+    CU(cudaHostAlloc((void**)&hb, sizeof(int) * (n_risks + 1), 0));
+    h->allocs.push_back(bl);
+    if (h->hband) cudaFreeHost(h->hband);
+    h->band_log = bl;                // (the old block stays in allocs until destroy)
+    h->hband = hb;
+    h->band_cap = n_risks + 1;
+  }
+  TRY(ensure_xsel(h, n_exact));
+  if (dense && n_exact > 0) TRY(ensure_side(h));
+  TRY(ensure_sweep(h, *h->sw, n_risks));
+  // graph path: not for a smoothed CVaR (t changes per call), nor when
+  // profiling / tracing (host-side timers and syncs)
+  const bool use_graph = h->use_graphs && smooth < 0 && !h->prof && !h->ref_trace;
+  const bool want_idx = cvar_idx != nullptr;
+  if (use_graph) {
+    const std::vector<double> key = graph_key(h, risks, n_risks, want_idx);
+    if (!h->gexec || key != h->gkey) {
+      drop_graph(h);
+      const int64_t l0 = h->launches;
+      CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+      int rc = enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+      if (rc != SDN_OK) { if (g) cudaGraphDestroy(g); return rc; }
+      if (ce != cudaSuccess) return fail(SDN_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&h->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) { h->gexec = nullptr; return fail(SDN_ERR_CUDA, "graph instantiate failed"); }
+      h->gkey = key;
+      h->glaunches = h->launches - l0;
+      h->launches = l0;
+    } else {
+      // per-call host state of eval_forward / upload_z
+      h->risk = risks[0];
+      h->selected = h->compacted = h->qr_valid = false;
+      h->shift = risks[0].qoi == SDN_QOI_DECODED ? h->q0dec : h->q0;
+      double zz = 0.0;
+      h->zhost.assign(z, z + h->d_z);
+      for (int k = 0; k < h->d_z; ++k) { h->hz[k] = z[k]; zz += z[k] * z[k]; }
+      h->hzz = zz;
+      h->fwd_done = true;
+      h->qr_valid = n_exact > 0;
+    }
+    CU(cudaGraphLaunch(h->gexec, h->stream));
+    h->launches += h->glaunches;
+  } else {
+    TRY(enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0));
+  }
   CU(cudaStreamSynchronize(h->stream));
   for (int i = 0; i < n_risks; ++i) {
     TRY(finish_host(h, risks[i], h->hstats, h->hpart_multi + (size_t)i * plen, &res[i],
@@ -1332,7 +1410,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     res[i].n_refined = refined_count(h, risks[i], 1 + i);
   }
   if (cvar_idx)
-    for (int64_t j = 0; j < off; ++j) cvar_idx[j] = h->goff + h->hidx[j];
+    for (int64_t j = 0; j < ktot; ++j) cvar_idx[j] = h->goff + h->hidx[j];
   return SDN_OK;
 }
 
@@ -1708,6 +1786,7 @@ int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubi
   h->q0dec = q0;
   h->have_dec = true;
   h->have_mean = false;
+  h->gen++;
   return SDN_OK;
 }
 
@@ -1797,6 +1876,7 @@ int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, con
   h->n = n;
   h->goff = global_offset;
   h->fwd_done = false;
+  h->gen++;
   if (h->tcw.enabled) TRY(tc_set_samples(h, h->tcw, h->MR, n));
   return SDN_OK;
 }
