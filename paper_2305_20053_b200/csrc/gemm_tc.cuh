@@ -695,21 +695,22 @@ struct TileEpi<EpiBwdSum> {
     if (e.W)
       for (int q = 0; q < e.R; ++q) ws[q * 32 + lane] = live ? e.W[(tr.r0 + lane) * e.R + q] : 0.0;
     __syncwarp();
-    if (lane < 16 && c0 + lane < N) {
-      const int j = lane;
-      const int64_t prow = (tr.r0 >> 7) * 4 + ((tr.r0 >> 5) & 3);
-      if (!e.W) {
+    const int64_t prow = (tr.r0 >> 7) * 4 + ((tr.r0 >> 5) & 3);
+    const int j = lane & 15;                      // column of the chunk
+    if (!e.W) {
+      if (lane < 16 && c0 + j < N) {
         double acc = 0.0;
 #pragma unroll 8
         for (int r = 0; r < 32; ++r) acc += (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
         e.part[prow * e.ldp + c0 + j] = acc;
-      } else {
-        for (int q = 0; q < e.R; ++q) {
-          double acc = 0.0;
+      }
+    } else if (c0 + j < N) {
+      // half-warps take alternate risks: lanes 0-15 risk q, lanes 16-31 risk q+1
+      for (int q = lane >> 4; q < e.R; q += 2) {
+        double acc = 0.0;
 #pragma unroll 8
-          for (int r = 0; r < 32; ++r) acc += ws[q * 32 + r] * (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
-          e.part[q * e.plane + prow * e.ldp + c0 + j] = acc;
-        }
+        for (int r = 0; r < 32; ++r) acc += ws[q * 32 + r] * (double)s.f1[sw_f(r, j >> 2) + (j & 3)];
+        e.part[q * e.plane + prow * e.ldp + c0 + j] = acc;
       }
     }
     __syncwarp();

@@ -388,7 +388,8 @@ k_finalize_multi(int nrb, int64_t plane, int h1, int d_z, const double* __restri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int k = blockIdx.x * nw + warp; k < d_z; k += gridDim.x * nw) {
     double s = 0.0;
-    for (int c = lane; c < h1; c += 32) s += PzT[(int64_t)k * h1 + c] * A[c];
+#pragma unroll 8
+    for (int c = lane; c < h1; c += 32) s += __ldg(PzT + (int64_t)k * h1 + c) * A[c];
     s = warp_sum(s);
     if (lane == 0) o[k] = s;
   }
@@ -409,8 +410,10 @@ k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __re
   if (n_act_dev) nrb = min(nrb, ((*n_act_dev + 127) / 128) * 4);
   const int c = blockIdx.x * 32 + threadIdx.x;
   double acc = 0.0;
-  if (c < w)
+  if (c < w) {
+#pragma unroll 8
     for (int r = threadIdx.y; r < nrb; r += 32) acc += part[(int64_t)r * w + c];
+  }
   s[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && c < w) {
