@@ -562,7 +562,7 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
       for (int j = 0; j < 16; ++j) {
         // branch-free (selects only) so the 16 elements interleave
         const float x = __uint_as_float(v[j]) + bias[j];
-        const float xn = fminf(x, 0.0f);
+        const float xn = x > 0.0f ? 0.0f : x;     // (not fminf: a NaN must propagate, as in the oracle)
         const float ex = __expf(xn);
         // e^x - 1 without cancellation near 0 (Taylor to x^5 on (-1/16, 0])
         const float pm = xn * (1.0f + xn * (0.5f + xn * (0.16666667f + xn * (0.041666668f + xn * 0.008333334f))));

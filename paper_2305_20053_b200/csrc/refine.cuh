@@ -117,6 +117,46 @@ SDN_DEV int block_excl(int* s_w, int warp, int lane, int v, int& total) {
   return base;
 }
 
+// one W row slice into registers: unconditional loads at clamped addresses so
+// all are in flight at once (a branch per load would serialise the round trips)
+SDN_DEV void ref_load_w(const float* w, int K, int lane, float (&wf)[REF_KC / 32]) {
+#pragma unroll
+  for (int u = 0; u < REF_KC / 32; ++u) wf[u] = __ldg(w + min(lane + 32 * u, K - 1));
+}
+
+// dot products of RB staged rows with one W row; transposed butterfly so that
+// lanes 4j..4j+3 end with row j's total (9 double shuffles instead of 8 x 5)
+template <int RB>
+SDN_DEV double ref_column(const double* xs, const float (&wf)[REF_KC / 32], int K, int lane) {
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+  for (int u = 0; u < REF_KC / 32; ++u) {
+    if (lane + 32 * u < K) {
+      const double wk = (double)wf[u];
+#pragma unroll
+      for (int j = 0; j < RB; ++j) acc[j] = fma(xs[j * REF_KC + lane + 32 * u], wk, acc[j]);
+    }
+  }
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  double b[4], c2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = h16 ? acc[i] : acc[i + 4], keep = h16 ? acc[i + 4] : acc[i];
+    b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = h8 ? b[i] : b[i + 2], keep = h8 ? b[i + 2] : b[i];
+    c2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double d = (h4 ? c2[1] : c2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? c2[0] : c2[1], 4);
+  d += __shfl_xor_sync(0xffffffffu, d, 2);
+  d += __shfl_xor_sync(0xffffffffu, d, 1);
+  return d;                                      // total of row (lane >> 2)
+}
+
 __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   extern __shared__ double xs[];                  // REF_RB x REF_KC
   __shared__ int s_w[REF_THREADS / 32], s_m[REF_THREADS / 32];
@@ -385,14 +425,17 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
       const int rb = min(REF_RB, m - r0);
       {                                          // warp j stages row r0 + j (clamped)
         const int rj = r0 + min(warp, rb - 1);
-        if (first) {
+        if (first) {                              // x = m_r * in_scale (exact in fp64, as the oracle)
           const float* src = a.MR + (int64_t)__ldcg(a.rowidx + rj) * K;
-          float v[REF_KC / 32];
+          float v[REF_KC / 32], sc[REF_KC / 32];
 #pragma unroll
-          for (int u = 0; u < REF_KC / 32; ++u) v[u] = __ldg(src + min(lane + 32 * u, K - 1));
+          for (int u = 0; u < REF_KC / 32; ++u) {
+            v[u] = __ldg(src + min(lane + 32 * u, K - 1));
+            sc[u] = __ldg(a.iscale + min(lane + 32 * u, K - 1));
+          }
 #pragma unroll
           for (int u = 0; u < REF_KC / 32; ++u)
-            if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = (double)v[u];
+            if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = (double)v[u] * (double)sc[u];
         } else {
           const double* src = in64 + (int64_t)rj * K;
           double v[REF_KC / 32];
@@ -404,43 +447,32 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
         }
       }
       __syncthreads();
-      for (int c = gw; c < N; c += nw) {
-        const float* w = ly.W + (int64_t)c * K;
-        float wf[REF_KC / 32], sf[REF_KC / 32];   // unconditional clamped loads: all in flight
-#pragma unroll
-        for (int u = 0; u < REF_KC / 32; ++u) {
-          const int k = min(lane + 32 * u, K - 1);
-          wf[u] = __ldg(w + k);
-          sf[u] = first ? __ldg(a.iscale + k) : 1.0f;
-        }
-        double acc[REF_RB];
-#pragma unroll
-        for (int j = 0; j < REF_RB; ++j) acc[j] = 0.0;
-#pragma unroll
-        for (int u = 0; u < REF_KC / 32; ++u) {
-          if (lane + 32 * u < K) {
-            const double wk = (double)wf[u] * (double)sf[u];
-#pragma unroll
-            for (int j = 0; j < REF_RB; ++j) acc[j] = fma(xs[j * REF_KC + lane + 32 * u], wk, acc[j]);
-          }
-        }
-        double v = 0.0;
-#pragma unroll
-        for (int j = 0; j < REF_RB; ++j) {
-          const double s = warp_sum(acc[j]);
-          if (lane == j) v = s;
-        }
-        if (lane < rb) {
+      // columns of this warp: c = gw, gw + nw, ...; the next column's W row is
+      // loaded while the current one is reduced (software pipeline)
+      float wf[REF_KC / 32];
+      int c = gw;
+      if (c < N) ref_load_w(ly.W + (int64_t)c * K, K, lane, wf);
+      for (; c < N; c += nw) {
+        float wn[REF_KC / 32];
+        if (c + nw < N) ref_load_w(ly.W + (int64_t)(c + nw) * K, K, lane, wn);
+        double v;
+        if (rb <= 2) v = ref_column<2>(xs, wf, K, lane);
+        else if (rb <= 4) v = ref_column<4>(xs, wf, K, lane);
+        else v = ref_column<8>(xs, wf, K, lane);
+        const int j = lane >> 2;                 // row whose total this lane holds
+        if ((lane & 3) == 0 && j < rb) {
           const double S = v + (first ? a.zb64[c] : (double)ly.b[c]);
           double o;
           if (last) {
             o = (double)a.omean[c] + (double)a.ostd[c] * S;
           } else {
             o = act64(a.act, S);
-            if (ly.resid) o += xs[lane * REF_KC + c];     // resid: K == N
+            if (ly.resid) o += xs[j * REF_KC + c];       // resid: K == N
           }
-          out[(int64_t)(r0 + lane) * N + c] = o;
+          out[(int64_t)(r0 + j) * N + c] = o;
         }
+#pragma unroll
+        for (int u = 0; u < REF_KC / 32; ++u) wf[u] = wn[u];
       }
       __syncthreads();
     }

@@ -225,3 +225,68 @@ def test_errors_mirror_reference():
         eng.eval(p.z, "cvar_exact", beta=1.5)
     with pytest.raises(ValueError):
         eng.eval(p.z[:3], "mean")
+
+
+@pytest.mark.parametrize("gemm", ["simt", "tc"])
+def test_exact_cvar_ties_at_threshold(gemm):
+    """Duplicated samples give bit-identical Q (row-independent GEMMs), so the
+    k-th value is tied across copies: the selection must take the lowest
+    indices of the tied group (riskopt.py:74-82 order: value desc, index asc),
+    in the cooperative select of k_refine and after the fp64 band refinement."""
+    p = _problem("c2", 4096, seed=4)
+    p.m_r = np.ascontiguousarray(p.m_r[np.arange(4096) % 512])
+    eng = _engine(p, gemm)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    for beta in (0.95, 0.99, 0.999):
+        r = eng.eval(p.z, "cvar_exact", beta=beta)
+        np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qo, beta)))
+        np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(eng.last_q(selection=True), beta)))
+
+
+def test_exact_cvar_nan_sample_selected_first():
+    p = _problem("c2", 2048, seed=5)
+    p.m_r[77, 0] = np.nan
+    eng = _engine(p)
+    r = eng.eval(p.z, "cvar_exact", beta=0.95)
+    assert 77 in set(r.idx.tolist()) and np.isnan(r.value)
+    Qs = eng.last_q(selection=True)
+    np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qs, 0.95)))
+
+
+@pytest.mark.parametrize("n", [1, 3, 20])
+def test_exact_cvar_tiny_sets(n):
+    """k = ceil((1-beta) n) down to the whole set (n = 1)."""
+    p = _problem("c1", n, seed=6)
+    eng = _engine(p)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    for beta in (0.0, 0.5, 0.9):
+        r = eng.eval(p.z, "cvar_exact", beta=beta)
+        sel = ref.cvar_select(Qo, beta)
+        np.testing.assert_array_equal(np.sort(r.idx), np.sort(sel))
+        assert abs(r.value - Qo[sel].mean()) <= RTOL * abs(Qo[sel].mean())
+        assert _rel(r.grad_z, Go[sel].mean(0)) <= RTOL
+
+
+@pytest.mark.parametrize("gemm", ["tc", "auto"])
+def test_multi_risk_graph_replay_tracks_z(gemm):
+    """Repeated multi-risk evaluations replay one captured graph; each call's z
+    must be the one used (values/gradients vs fresh single-risk evaluations).
+    Forced tensor-core chains make the per-row sweep values identical between
+    the dense multi-risk sweep and the compacted single-risk one (only the fp64
+    summation order differs); under auto routing the short CVaR-only sweep may
+    take the fp32 SIMT path, so the two agree to the fp32-path tolerance."""
+    p = _problem("c2", 4096, seed=7)
+    eng = _engine(p, gemm)
+    tol = 1e-9 if gemm == "tc" else RTOL
+    risks = [dict(kind="meanvar", beta=1.0, alpha=1e-2), dict(kind="cvar_exact", beta=0.95, alpha=1e-2),
+             dict(kind="mean")]
+    g = np.random.default_rng(0)
+    for it in range(4):
+        z = p.z + 0.1 * it * g.standard_normal(p.z.shape)
+        multi = eng.eval_multi(z, risks)
+        for rm, spec in zip(multi, risks):
+            single = eng.eval(z, spec["kind"], beta=spec.get("beta", 0.95), alpha=spec.get("alpha", 0.0))
+            assert rm.value == pytest.approx(single.value, rel=1e-12)
+            np.testing.assert_allclose(rm.grad_z, single.grad_z, rtol=tol, atol=tol * np.abs(single.grad_z).max())
+            if spec["kind"] == "cvar_exact":
+                np.testing.assert_array_equal(np.sort(rm.idx), np.sort(single.idx))
