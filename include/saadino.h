@@ -192,6 +192,17 @@ int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, 
  * all-gather -> sdn_eval_select.  Single-rank sdn_eval / sdn_eval_multi do
  * the equivalent internally. */
 int sdn_eval_refine_band(sdn_handle* h);
+
+/* Several risks over one forward (multi-rank): after the final sdn_eval_select
+ * of each exact-CVaR risk, sdn_eval_keep_selection(h, slot) keeps it (slots in
+ * the order the exact risks appear in the list); sdn_eval_backward_multi then
+ * runs ONE reverse sweep for all risks (unit seeds, per-risk weighted column
+ * sums) into partials_dev = n_risks x sdn_partial_len(h) doubles, all-reduced
+ * together; finish each risk with sdn_eval_set_risk + sdn_eval_finish on its
+ * slice.  (sdn_eval_multi does the same on one handle.) */
+int sdn_eval_keep_selection(sdn_handle* h, int32_t slot);
+int sdn_eval_backward_multi(sdn_handle* h, const sdn_risk* risks, int32_t n_risks, const double* stats_dev,
+                            double* partials_dev);
 int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev);
 /* Switch the risk for the next sweep sharing the last forward (multi-risk). */
 int sdn_eval_set_risk(sdn_handle* h, const sdn_risk* risk);

@@ -69,6 +69,8 @@ SIGNATURES = {
     "sdn_eval_candidates": (C.c_int, [_P, C.c_int64, _P]),
     "sdn_eval_select": (C.c_int, [_P, _P, C.c_int32, C.c_int64]),
     "sdn_eval_refine_band": (C.c_int, [_P]),
+    "sdn_eval_keep_selection": (C.c_int, [_P, C.c_int32]),
+    "sdn_eval_backward_multi": (C.c_int, [_P, C.POINTER(Risk), C.c_int32, _P, _P]),
     "sdn_eval_backward": (C.c_int, [_P, _P, _P]),
     "sdn_eval_set_risk": (C.c_int, [_P, C.POINTER(Risk)]),
     "sdn_eval_finish": (C.c_int, [_P, _P, _P, C.POINTER(Result), _D]),

@@ -168,6 +168,7 @@ struct sdn_handle {
 
   // ---- evaluation state
   sdn_risk risk{};
+  sdn_risk fwd_risk{};          // the risk the last forward ran with (its t / eps fed the moments)
   double shift = 0.0;
   bool have_mean = false;
   double last_mean = 0.0;
@@ -197,6 +198,7 @@ struct sdn_handle {
   int* x_offs = nullptr;
   std::vector<int*> x_rowidx, x_nact;
   std::vector<uint8_t*> x_mask;
+  std::vector<int64_t> x_k;     // k of each kept selection (multi-rank phases)
   int sm_avail = 0;             // SMs the persistent GEMMs may use
   int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS
   bool no_overlap = false;               // env SDN_NO_OVERLAP=1
@@ -836,6 +838,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   TRY(check_risk(risk));
   CU(cudaSetDevice(h->device));
   h->risk = *risk;
+  h->fwd_risk = *risk;
   h->selected = false;
   h->compacted = false;
   h->qr_valid = false;
@@ -1389,6 +1392,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     } else {
       // per-call host state of eval_forward / upload_z
       h->risk = risks[0];
+      h->fwd_risk = risks[smooth >= 0 ? smooth : 0];
       h->selected = h->compacted = h->qr_valid = false;
       h->shift = risks[0].qoi == SDN_QOI_DECODED ? h->q0dec : h->q0;
       double zz = 0.0;
@@ -1503,6 +1507,43 @@ int sdn_eval_refine_band(sdn_handle* h) {
   return SDN_OK;
 }
 
+// multi-rank, several risks: keep the current exact-CVaR selection (after
+// its final sdn_eval_select) in slot `slot` for sdn_eval_backward_multi
+int sdn_eval_keep_selection(sdn_handle* h, int32_t slot) {
+  if (!h || slot < 0 || slot >= SDN_RMAX) return fail(SDN_ERR_ARG, "bad argument");
+  if (!h->fwd_done || !h->selected) return fail(SDN_ERR_STATE, "eval_select first");
+  CU(cudaSetDevice(h->device));
+  TRY(ensure_xsel(h, slot + 1));
+  if ((int)h->x_k.size() < slot + 1) h->x_k.resize(slot + 1, 0);
+  CU(cudaMemcpyAsync(h->x_mask[slot], h->sel, std::max<int64_t>(h->n, 1), cudaMemcpyDeviceToDevice, h->stream));
+  h->x_k[slot] = h->kk;
+  return SDN_OK;
+}
+
+// multi-rank, several risks: ONE reverse sweep for all of them (the i-th
+// exact-CVaR risk in the list uses kept selection slot i); partials_dev holds
+// n_risks x sdn_partial_len(h) doubles (one all-reduce for all risks)
+int sdn_eval_backward_multi(sdn_handle* h, const sdn_risk* risks, int32_t n_risks, const double* stats_dev,
+                            double* partials_dev) {
+  if (!h || !risks || !stats_dev || !partials_dev || n_risks < 1 || n_risks > SDN_RMAX)
+    return fail(SDN_ERR_ARG, "bad argument");
+  if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
+  CU(cudaSetDevice(h->device));
+  std::vector<const uint8_t*> masks(n_risks, nullptr);
+  std::vector<int64_t> ks(n_risks, 0);
+  for (int i = 0, e = 0; i < n_risks; ++i) {
+    TRY(check_risk(&risks[i]));
+    if (risks[i].qoi != h->risk.qoi) return fail(SDN_ERR_ARG, "risks must keep the forward's QoI frame");
+    if (risks[i].kind != SDN_RISK_CVAR_EXACT) continue;
+    if (e >= (int)h->x_k.size() || h->x_k[e] < 1) return fail(SDN_ERR_STATE, "exact CVaR needs a kept selection");
+    masks[i] = h->x_mask[e];
+    ks[i] = h->x_k[e];
+    ++e;
+  }
+  TRY(ensure_sweep(h, *h->sw, n_risks));
+  return backward_multi(h, risks, n_risks, masks.data(), ks.data(), stats_dev, partials_dev);
+}
+
 // next reverse sweep after one forward (multi-risk): same QoI frame; a
 // smoothed CVaR must be the forward's own risk (its t/eps fed the moments)
 int sdn_eval_set_risk(sdn_handle* h, const sdn_risk* risk) {
@@ -1511,7 +1552,7 @@ int sdn_eval_set_risk(sdn_handle* h, const sdn_risk* risk) {
   if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
   if (risk->qoi != h->risk.qoi) return fail(SDN_ERR_ARG, "risk must keep the forward's QoI frame");
   if (risk->kind == SDN_RISK_CVAR_SMOOTH &&
-      (h->risk.kind != SDN_RISK_CVAR_SMOOTH || risk->t != h->risk.t || risk->eps != h->risk.eps))
+      (h->fwd_risk.kind != SDN_RISK_CVAR_SMOOTH || risk->t != h->fwd_risk.t || risk->eps != h->fwd_risk.eps))
     return fail(SDN_ERR_ARG, "smoothed CVaR must be the forward's risk");
   h->risk = *risk;
   h->compacted = false;

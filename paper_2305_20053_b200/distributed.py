@@ -114,7 +114,7 @@ class ShardedObjective:
 
     backend: object with the Engine phase API (make_risk, new_buffer,
     partial_len, phase_forward / _set_risk / _candidates / _select /
-    _backward / _finish, d_z)."""
+    _refine_band / _keep_selection / _backward_multi / _finish, d_z)."""
 
     def __init__(self, backend, comm, n_global: int):
         self.b = backend
@@ -132,26 +132,32 @@ class ShardedObjective:
         stats = self.b.new_buffer(STATS_LEN)
         self.b.phase_forward(z, rs[first], stats)
         self.comm.allreduce_(stats)
+        # exact-CVaR selections (two candidate rounds each: the second after
+        # the fp64 refinement of the band around the global threshold), kept
+        # in slots; then ONE sweep for all risks and ONE all-reduce
+        slot = 0
+        for r, rr in zip(risks, rs):
+            if r["kind"] != "cvar_exact":
+                continue
+            self.b.phase_set_risk(rr)
+            k = cvar_count(self.n_global, r.get("beta", 0.95))
+            cand = self.b.new_buffer(2 * k)
+            for rnd in range(2):
+                self.b.phase_candidates(k, cand)
+                allc = self.comm.allgather(cand)
+                self.b.phase_select(allc.contiguous(), self.comm.world, k)
+                if rnd == 0:
+                    self.b.phase_refine_band()
+            self.b.phase_keep_selection(slot)
+            slot += 1
+        plen = self.b.partial_len()
+        partials = self.b.new_buffer(plen * len(rs))
+        self.b.phase_backward_multi(rs, stats, partials)
+        self.comm.allreduce_(partials)
         out = []
         for i, (r, rr) in enumerate(zip(risks, rs)):
-            if i != first or len(rs) > 1:
-                self.b.phase_set_risk(rr)
-            k = 0
-            if r["kind"] == "cvar_exact":
-                k = cvar_count(self.n_global, r.get("beta", 0.95))
-                cand = self.b.new_buffer(2 * k)
-                for rnd in range(2):
-                    # round 2 reselects after the rows near the global
-                    # threshold were re-evaluated in fp64 (sdn_eval_refine_band)
-                    self.b.phase_candidates(k, cand)
-                    allc = self.comm.allgather(cand)
-                    self.b.phase_select(allc.contiguous(), self.comm.world, k)
-                    if rnd == 0:
-                        self.b.phase_refine_band()
-            partial = self.b.new_buffer(self.b.partial_len())
-            self.b.phase_backward(stats, partial)
-            self.comm.allreduce_(partial)
-            res, grad = self.b.phase_finish(stats, partial)
+            self.b.phase_set_risk(rr)
+            res, grad = self.b.phase_finish(stats, partials[i * plen:(i + 1) * plen])
             out.append(EvalResult(value=res.value, grad_z=grad if r.get("need_grad", True) else None,
                                   grad_t=res.grad_t if r["kind"] == "cvar" else None, idx=None,
                                   n_samples=int(res.n_samples), n_selected=int(res.n_selected),

@@ -265,6 +265,14 @@ class Engine:
     def phase_refine_band(self):
         check(lib.sdn_eval_refine_band(self.h), "sdn_eval_refine_band")
 
+    def phase_keep_selection(self, slot: int):
+        check(lib.sdn_eval_keep_selection(self.h, int(slot)), "sdn_eval_keep_selection")
+
+    def phase_backward_multi(self, risks, stats_dev, partials_dev):
+        arr = (_lib.Risk * len(risks))(*risks)
+        check(lib.sdn_eval_backward_multi(self.h, arr, len(risks), C.c_void_p(stats_dev.data_ptr()),
+                                          C.c_void_p(partials_dev.data_ptr())), "sdn_eval_backward_multi")
+
     def phase_set_risk(self, risk: _lib.Risk):
         self._phase_risk = risk
         check(lib.sdn_eval_set_risk(self.h, C.byref(risk)), "sdn_eval_set_risk")

@@ -76,6 +76,22 @@ class OracleBackend:
     def phase_refine_band(self):
         pass                       # Q is already float64 here
 
+    def phase_keep_selection(self, slot):
+        if not hasattr(self, "kept"):
+            self.kept = {}
+        self.kept[slot] = (self.sel.copy(), self.k)
+
+    def phase_backward_multi(self, risks, stats, partials):
+        """One call for all risks: the i-th exact risk uses kept slot i."""
+        plen = self.partial_len()
+        slot = 0
+        for i, r in enumerate(risks):
+            self.risk = r
+            if KIND[r.kind] == "cvar_exact":
+                self.sel, self.k = self.kept[slot]
+                slot += 1
+            self.phase_backward(stats, partials[i * plen:(i + 1) * plen])
+
     def phase_backward(self, stats, partial):
         st = stats.numpy()
         n = st[0]
