@@ -191,6 +191,7 @@ struct sdn_handle {
   unsigned* ref_bar = nullptr;  // k_refine grid barrier
   int ref_grid = 0;
   bool ref_ok = false;          // every layer input width <= REF_KC
+  const double* ref_tp = nullptr;  // device-side t of the refinement window (set by refine_window)
   // side stream (overlapped exact-CVaR selection in sdn_eval_multi)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fwd = nullptr, ev_side = nullptr;
@@ -542,7 +543,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 16);
   if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
-  if ((rc = dalloc(h, &h->zdev, h->d_z))) return bail(rc);
+  if ((rc = dalloc(h, &h->zdev, h->d_z + SDN_RMAX))) return bail(rc);   // [z | per-risk t]
   if ((rc = dalloc(h, &h->zb, h->h1))) return bail(rc);
   if ((rc = dalloc(h, &h->zb64, h->h1))) return bail(rc);
   if ((rc = dalloc(h, &h->W0raw, (size_t)h->h1 * h->r_m))) return bail(rc);
@@ -573,7 +574,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->band_log, h->band_cap))) return bail(rc);
   if (cudaHostAlloc((void**)&h->hband, sizeof(int) * h->band_cap, 0) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
-  if (cudaHostAlloc((void**)&h->hz, sizeof(double) * h->d_z, 0) != cudaSuccess ||
+  if (cudaHostAlloc((void**)&h->hz, sizeof(double) * (h->d_z + SDN_RMAX), 0) != cudaSuccess ||
       cudaHostAlloc((void**)&h->hstats, sizeof(double) * STATS_LEN, 0) != cudaSuccess ||
       cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), 0) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
@@ -757,12 +758,18 @@ static int check_risk(const sdn_risk* r) {
 
 static int ceil_count(double x) { return (int)std::ceil(x - 1e-9); }   // riskopt.py:56-58
 
-static int upload_z(sdn_handle* h, const double* z) {
+// z and the risks' t values -> pinned staging -> device (one copy; a captured
+// graph replays it, so z and t are per-call parameters of the graph)
+static void stage_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks) {
   double zz = 0.0;
   h->zhost.assign(z, z + h->d_z);
   for (int k = 0; k < h->d_z; ++k) { h->hz[k] = z[k]; zz += z[k] * z[k]; }
+  for (int r = 0; r < SDN_RMAX; ++r) h->hz[h->d_z + r] = r < n_risks ? risks[r].t : 0.0;
   h->hzz = zz;
-  CU(cudaMemcpyAsync(h->zdev, h->hz, sizeof(double) * h->d_z, cudaMemcpyHostToDevice, h->stream));
+}
+static int upload_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks) {
+  stage_z(h, z, risks, n_risks);
+  CU(cudaMemcpyAsync(h->zdev, h->hz, sizeof(double) * (h->d_z + SDN_RMAX), cudaMemcpyHostToDevice, h->stream));
   return SDN_OK;
 }
 
@@ -782,7 +789,7 @@ static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, 
   do_refine = do_refine && h->ref_ok;
   if (!do_refine && k == 0) return SDN_OK;
   RefineArgs a{};
-  a.n = h->n; a.kind = kind; a.t = t; a.eps = eps; a.tdev = h->thr_dev;
+  a.n = h->n; a.kind = kind; a.t = t; a.eps = eps; a.tdev = h->thr_dev; a.tp = h->ref_tp;
   a.rowidx = h->ref_rowidx; a.count = count; a.blockcnt = h->ref_blockcnt; a.bar = h->ref_bar;
   a.L = h->L;
   for (int l = 0; l < h->L && l < REF_MAX_LAYERS; ++l) {
@@ -818,11 +825,15 @@ static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, 
 }
 
 // smoothed CVaR: refine the window rows, then retake the moments from Q
-static int refine_window(sdn_handle* h, const sdn_risk* risk, bool dec, int qg, double* stats_dev) {
+static int refine_window(sdn_handle* h, const sdn_risk* risk, bool dec, int qg, double* stats_dev,
+                         const double* tp) {
   if (risk->kind != SDN_RISK_CVAR_SMOOTH || h->n == 0 || h->no_refine || !h->ref_ok) return SDN_OK;
-  TRY(refine_band(h, RISK_BAND, risk->t, risk->eps, dec, h->band_log));
+  h->ref_tp = tp;
+  int rc = refine_band(h, RISK_BAND, risk->t, risk->eps, dec, h->band_log);
+  h->ref_tp = nullptr;
+  TRY(rc);
   { ProfScope ps(h, PC_QOI, 0.0, 8.0 * h->n);
-  k_moments<<<qg, 256, 0, h->stream>>>(h->n, h->Q, h->shift, risk->t, risk->eps, h->qpart);
+  k_moments<<<qg, 256, 0, h->stream>>>(h->n, h->Q, h->shift, risk->t, risk->eps, h->qpart, tp);
   k_sum_rows<<<(unsigned)cdiv(STATS_LEN, 8), 256, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
   h->launches += 2;
   CHECK_LAUNCH(h);
@@ -830,8 +841,11 @@ static int refine_window(sdn_handle* h, const sdn_risk* risk, bool dec, int qg, 
 }
 
 // phase 1: forward over the shard; local moments -> stats_dev (device)
+// (all, n_all): the evaluation's risks, whose t values travel with z (graph
+// parameters); slot: this forward's risk among them
 static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, double* stats_dev,
-                        bool store_D) {
+                        bool store_D, const sdn_risk* all = nullptr, int n_all = 0, int slot = 0) {
+  if (!all) { all = risk; n_all = 1; slot = 0; }
   if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
   if (risk->qoi == SDN_QOI_REDUCED && !h->have_form) return fail(SDN_ERR_STATE, "set_tracking first");
   if (risk->qoi == SDN_QOI_DECODED && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
@@ -847,7 +861,8 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   // moments accumulate (Q - shift) in fp64; shift = q0 keeps every evaluation
   // stateless and deterministic (cancellation ~1e-16 (Qbar - q0)^2 / var)
   h->shift = q0;
-  TRY(upload_z(h, z));
+  TRY(upload_z(h, z, all, n_all));
+  const double* tp = h->zdev + h->d_z + slot;
   { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
   k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb,
                                                              h->zb64); }
@@ -865,11 +880,11 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   { ProfScope ps(h, PC_QOI, 4.0 * h->n * h->r_u, 4.0 * h->n * h->r_u * (dec ? 2 : 1) + 8.0 * h->n);
   k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
                                    h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
-                                   h->Q, h->qpart);
+                                   h->Q, h->qpart, tp);
   k_sum_rows<<<(unsigned)cdiv(STATS_LEN, 8), 256, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
   h->launches += 2;
   CHECK_LAUNCH(h);
-  TRY(refine_window(h, risk, dec, qg, stats_dev));
+  TRY(refine_window(h, risk, dec, qg, stats_dev, tp));
   h->fwd_done = true;
   return SDN_OK;
 }
@@ -974,11 +989,12 @@ static int ensure_sweep(sdn_handle* h, SweepBufs& b, int R) {
 // right before the last GEMM, so the selections overlap the sweep.
 static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uint8_t* const* masks,
                           const int64_t* ks, const double* stats_dev, double* partials,
-                          const std::function<int()>& join = {}) {
+                          const std::function<int()>& join = {}, const double* tdev = nullptr) {
   if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
   if (R < 1 || R > SDN_RMAX) return fail(SDN_ERR_ARG, "1..8 risks per sweep");
   RiskSet rs{};
   rs.R = R;
+  rs.tdev = tdev;                     // per-risk t on the device, in list order (sdn_eval_multi)
   bool dense = false, all_exact = true, any_grad = false;
   int64_t ksum = 0;
   for (int r = 0; r < R; ++r) {
@@ -1222,11 +1238,11 @@ int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* r
 // t/eps feed the forward-time moments and window refinement).
 //
 // The device work is enqueued by enqueue_multi (no host sync inside); for a
-// repeated configuration without a smoothed CVaR (whose t changes every
-// optimizer step) it is captured once into a CUDA graph and replayed: one
-// launch per evaluation instead of ~30, which is what bounds small
-// problems (c1).  Host-side per-call state (z and its norm) is refreshed on
-// every call; the graph's memcpy node reads z from the pinned staging buffer.
+// repeated risk configuration it is captured once into a CUDA graph and
+// replayed: one launch per evaluation instead of ~30, which is what bounds
+// small problems (c1) and the optimizer loop.  z and each risk's t (the
+// smoothed-CVaR variable changes every optimizer step) are staged in pinned
+// memory on every call and read by the graph's first copy node.
 static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks, bool want_idx,
                          const std::vector<int64_t>& kks, const std::vector<int64_t>& koff, int smooth,
                          bool any_grad) {
@@ -1237,7 +1253,8 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     n_exact += risks[i].kind == SDN_RISK_CVAR_EXACT;
     dense |= risks[i].kind == SDN_RISK_MEAN || risks[i].kind == SDN_RISK_MEANVAR;
   }
-  TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad));
+  TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad, risks, n_risks,
+                   smooth >= 0 ? smooth : 0));
   std::vector<const uint8_t*> masks(n_risks, nullptr);
   auto select_all = [&]() -> int {
     for (int i = 0, e = 0; i < n_risks; ++i) {
@@ -1279,7 +1296,8 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     TRY(select_all());
   }
   h->risk = risks[0];
-  int rc = backward_multi(h, risks, n_risks, masks.data(), kks.data(), h->stats_loc, h->partial_multi, join);
+  int rc = backward_multi(h, risks, n_risks, masks.data(), kks.data(), h->stats_loc, h->partial_multi, join,
+                          h->zdev + h->d_z);
   h->sm_avail = h->num_sms;
   if (rc) return rc;
   CU(cudaMemcpyAsync(h->hstats, h->stats_loc, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
@@ -1368,9 +1386,9 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   TRY(ensure_xsel(h, n_exact));
   if (dense && n_exact > 0) TRY(ensure_side(h));
   TRY(ensure_sweep(h, *h->sw, n_risks));
-  // graph path: not for a smoothed CVaR (t changes per call), nor when
-  // profiling / tracing (host-side timers and syncs)
-  const bool use_graph = h->use_graphs && smooth < 0 && !h->prof && !h->ref_trace;
+  // graph path (z and every risk's t are per-call graph parameters, staged
+  // in pinned memory); not when profiling / tracing (host timers and syncs)
+  const bool use_graph = h->use_graphs && !h->prof && !h->ref_trace;
   const bool want_idx = cvar_idx != nullptr;
   if (use_graph) {
     const std::vector<double> key = graph_key(h, risks, n_risks, want_idx);
@@ -1395,10 +1413,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       h->fwd_risk = risks[smooth >= 0 ? smooth : 0];
       h->selected = h->compacted = h->qr_valid = false;
       h->shift = risks[0].qoi == SDN_QOI_DECODED ? h->q0dec : h->q0;
-      double zz = 0.0;
-      h->zhost.assign(z, z + h->d_z);
-      for (int k = 0; k < h->d_z; ++k) { h->hz[k] = z[k]; zz += z[k] * z[k]; }
-      h->hzz = zz;
+      stage_z(h, z, risks, n_risks);
       h->fwd_done = true;
       h->qr_valid = n_exact > 0;
     }
@@ -1971,12 +1986,13 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   // modes 3..6 drop parts of the fused epilogue: 3 no D, 4 no split, 5 no
   // residual input, 6 only the fp32 H store
   const bool keepD = mode < 3 || (mode != 3 && mode < 6), keepS = mode < 4 || (mode != 4 && mode < 6);
-  const bool keepP = mode < 5, keepH = mode != 7 && mode != 8;
+  const bool keepP = mode < 5, keepH = mode != 7 && mode != 8 && mode != 9;
   // mode 8: the production tensor-core chain epilogue (no fp32 H, residual
   // read from the input's bf16 split, D + split outputs)
-  const bool chainm = mode == 8;
+  // mode 9: the chain epilogue with the identity activation (arithmetic share of ELU)
+  const bool chainm = mode == 8 || mode == 9;
   EpiFwdHidden e{h->b[1], (h->res[1] && keepP && !chainm) ? h->H[0] : nullptr, keepH ? h->H[1] : nullptr,
-                 (keepD || chainm) ? h->D[1] : nullptr, (int64_t)N, h->act};
+                 (keepD || chainm) ? h->D[1] : nullptr, (int64_t)N, mode == 9 ? (int)ACT_IDENTITY : h->act};
   TcChain<EpiFwdHidden> ch{e, TcEpiSplit{(keepS || chainm) ? &h->tcw.act[1] : nullptr},
                            TcEpiSplit{(chainm && h->res[1]) ? &h->tcw.act[0] : nullptr}};
   h->tcw.act[0].rows = M;

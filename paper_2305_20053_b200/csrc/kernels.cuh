@@ -53,7 +53,8 @@ __global__ void k_build_x(int64_t n, int r_m, int d_z, int ldx, const float* __r
 __global__ void __launch_bounds__(256)
 k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict__ kphi,
       const float* __restrict__ c, double q0, double shift, double t, double eps,
-      double* __restrict__ Q, double* __restrict__ part) {
+      double* __restrict__ Q, double* __restrict__ part, const double* __restrict__ tp = nullptr) {
+  if (tp) t = *tp;                     // device-side t (graph replay)
   __shared__ double sp[8][6];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -115,7 +116,8 @@ SDN_DEV bool in_band_exact(double q, double thr) {            // exact-CVaR thre
 // block moments of k_qoi recomputed from Q (after refinement)
 __global__ void __launch_bounds__(256)
 k_moments(int64_t n, const double* __restrict__ Q, double shift, double t, double eps,
-          double* __restrict__ part) {
+          double* __restrict__ part, const double* __restrict__ tp = nullptr) {
+  if (tp) t = *tp;
   __shared__ double sp[8][6];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -255,18 +257,20 @@ struct RiskSet {
   int kind[SDN_RMAX];
   double beta[SDN_RMAX], eps[SDN_RMAX], t[SDN_RMAX], kinv[SDN_RMAX];
   const uint8_t* mask[SDN_RMAX];     // exact CVaR selection masks (sample rows)
+  const double* tdev;                // per-risk t on the device (graph replay), else t[] by value
 };
+SDN_DEV double risk_t(const RiskSet& rs, int r) { return rs.tdev ? rs.tdev[r] : rs.t[r]; }
 
 SDN_DEV double risk_weight(const RiskSet& rs, int r, int64_t i, double q, const double* st, double shift) {
   if (rs.kind[r] == RISK_CVAR_EXACT) return rs.mask[r][i] ? rs.kinv[r] : 0.0;
-  return sample_weight(rs.kind[r], q, st, shift, rs.beta[r], rs.eps[r], rs.t[r], 0.0);
+  return sample_weight(rs.kind[r], q, st, shift, rs.beta[r], rs.eps[r], risk_t(rs, r), 0.0);
 }
 
 SDN_DEV bool risk_active(const RiskSet& rs, int64_t i, double q) {
   bool a = false;
   for (int r = 0; r < rs.R; ++r) {
     if (rs.kind[r] == RISK_CVAR_EXACT) a |= rs.mask[r][i] != 0;
-    else if (rs.kind[r] == RISK_CVAR_SMOOTH) a |= splus_d1_d(q - rs.t[r], rs.eps[r]) > 0.0;
+    else if (rs.kind[r] == RISK_CVAR_SMOOTH) a |= splus_d1_d(q - risk_t(rs, r), rs.eps[r]) > 0.0;
     else a = true;
   }
   return a;

@@ -34,6 +34,7 @@ struct RefineArgs {
   int64_t n;
   int kind;                     // RISK_BAND (t, eps) or RISK_BAND_EXACT (*tdev)
   double t, eps;
+  const double* tp;             // device-side t of the window (graph replay), else t
   const double* tdev;
   int* rowidx;
   int* count;                   // band row count (read back by the host)
@@ -368,9 +369,10 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   }
 
   // ---- 1. band flags and ordered compaction
+  const double tw = a.tp ? *a.tp : a.t;
   auto band = [&](int64_t i) -> bool {
     return a.kind == RISK_BAND_EXACT ? in_band_exact(a.Q[i], a.k > 0 ? thr : *a.tdev)
-                                     : row_flag(a.kind, a.Q, nullptr, i, a.t, a.eps, a.tdev);
+                                     : row_flag(a.kind, a.Q, nullptr, i, tw, a.eps, a.tdev);
   };
   int mine = 0;
   for (int64_t base = lo; base < hi; base += REF_THREADS) {

@@ -290,3 +290,18 @@ def test_multi_risk_graph_replay_tracks_z(gemm):
             np.testing.assert_allclose(rm.grad_z, single.grad_z, rtol=tol, atol=tol * np.abs(single.grad_z).max())
             if spec["kind"] == "cvar_exact":
                 np.testing.assert_array_equal(np.sort(rm.idx), np.sort(single.idx))
+
+
+def test_smoothed_cvar_graph_replay_tracks_t():
+    """Smoothed-CVaR evaluations at a moving t (as in minimize) replay one
+    captured graph: t is a device-side graph parameter."""
+    p = _problem("c2", 2048, seed=8)
+    eng = _engine(p)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    for beta, q in ((0.9, 0.85), (0.9, 0.9), (0.9, 0.97), (0.9, 0.5)):
+        t = float(np.quantile(Qo, q))
+        r = eng.eval(p.z, "cvar", beta=beta, eps=1e-2, t=t)
+        o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar", beta=beta, eps=1e-2), t)
+        assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+        assert _rel(r.grad_z, o[1]) <= RTOL
+        assert abs(r.grad_t - o[2]) <= 1e-6
