@@ -345,9 +345,10 @@ static bool chain_tc(sdn_handle* h, int64_t rows) {
     if (l >= 1 && !tc_gemm_supported(rows, n_in, n_out)) return false;
   }
   if (h->gemm == SDN_GEMM_TC) return true;
-  // auto: small chains (c1, CVaR tails) fill more SMs with 64x64 SIMT tiles
-  // (the tcgen05 kernel narrows its N tile for short chains)
-  return rows >= 512;
+  // auto: the tcgen05 chain (narrow N tiles for short chains) beats the SIMT
+  // tiles down to a single 128-row tile (c1: 113 vs 176 us per evaluation);
+  // only a handful of rows stays on the exact-fp32 SIMT path
+  return rows >= 64;
 }
 
 // layer chain on `nrows` rows.  Layer 0 input: X (ld0, K0) with weight W0 and
