@@ -54,6 +54,7 @@ class Engine:
         self.device = int(device)
         self.max_samples = int(max_samples)
         self._widths_c = (C.c_int32 * len(w))(*w)
+        self._multi_cache = {}
         cfg = _lib.Config(n_layers=len(model.weights), widths=self._widths_c, r_m=self.r_m, d_z=self.d_z,
                           activation=_lib.ACT[model.activation], residual=int(bool(model.residual)),
                           gemm=_lib.GEMM[gemm], device=self.device, max_samples=self.max_samples)
@@ -208,24 +209,39 @@ class Engine:
     def eval_multi(self, z, risks) -> list:
         """Several risks from one forward pass.  risks: list of dicts with
         keys of `eval` (kind, beta, eps, t, alpha, qoi, need_grad)."""
-        rs = [self.make_risk(**r) for r in risks]
-        arr = (_lib.Risk * len(rs))(*rs)
-        res = (_lib.Result * len(rs))()
+        # the ctypes argument blocks of a risk configuration are built once and
+        # reused (repeated calls replay one device graph; keep the host side lean)
+        key = (self.n, tuple(tuple(sorted((k, v) for k, v in r.items() if k != "t")) for r in risks))
+        cached = self._multi_cache.get(key)
+        if cached is None:
+            rs = [self.make_risk(**r) for r in risks]
+            arr = (_lib.Risk * len(rs))(*rs)
+            res = (_lib.Result * len(rs))()
+            grads = np.zeros((len(rs), self.d_z))
+            ks = [max(int(np.ceil((1.0 - r["beta"]) * self.n - 1e-9)), 1) if r["kind"] == "cvar_exact" else 0
+                  for r in risks]
+            idx = np.zeros(max(sum(ks), 1), np.int64)
+            cached = (arr, res, grads, ks, idx, dptr(grads), i64ptr(idx))
+            if len(self._multi_cache) > 16:
+                self._multi_cache.clear()
+            self._multi_cache[key] = cached
+        arr, res, grads, ks, idx, gptr, iptr = cached
+        for i, r in enumerate(risks):           # t is per call (the optimizer's auxiliary variable)
+            if r["kind"] == "cvar":
+                if r.get("t") is None:
+                    raise ValueError("CVaR objective needs the auxiliary variable t")
+                arr[i].t = float(r["t"])
         z = _f64(z)
         if z.shape != (self.d_z,):
             raise ValueError(f"control must have shape ({self.d_z},)")
-        grads = np.zeros((len(rs), self.d_z))
-        ks = [max(int(np.ceil((1.0 - r["beta"]) * self.n - 1e-9)), 1) if r["kind"] == "cvar_exact" else 0
-              for r in risks]
-        idx = np.zeros(max(sum(ks), 1), np.int64)
-        check(lib.sdn_eval_multi(self.h, dptr(z), arr, len(rs), res, dptr(grads), i64ptr(idx)), "sdn_eval_multi")
+        check(lib.sdn_eval_multi(self.h, dptr(z), arr, len(risks), res, gptr, iptr), "sdn_eval_multi")
         out, off = [], 0
         for i, r in enumerate(risks):
             sel = None
             if ks[i]:
                 sel = idx[off:off + ks[i]].copy()
                 off += ks[i]
-            out.append(EvalResult(value=res[i].value, grad_z=grads[i] if r.get("need_grad", True) else None,
+            out.append(EvalResult(value=res[i].value, grad_z=grads[i].copy() if r.get("need_grad", True) else None,
                                   grad_t=res[i].grad_t if r["kind"] == "cvar" else None, idx=sel,
                                   n_samples=int(res[i].n_samples), n_selected=int(res[i].n_selected),
                                   q_mean=res[i].q_mean, q_var=res[i].q_var,
