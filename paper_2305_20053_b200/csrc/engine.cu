@@ -185,6 +185,9 @@ struct sdn_handle {
   unsigned* ref_ghist = nullptr;           // k_refine selection histograms (2 x grid x 256)
   unsigned long long* ref_gmm = nullptr;   // k_refine selection min / max keys (2 x grid)
   double* Qr = nullptr;         // exact-CVaR selection copy of Q (threshold band refined in fp64)
+  float* seed_a2 = nullptr;     // r_u: 2 sigma        (fused output-layer seeds)
+  float* seed_b2 = nullptr;     // r_u: 2 sigma c
+  bool seed_fused = false;      // the last forward wrote the sweep's unit seeds
   bool qr_valid = false;
   double* wpart = nullptr;      // k_weights block partials (qgrid x 2 SDN_RMAX)
   double* vsum = nullptr;       // 2 SDN_RMAX: per-risk sum_{w != 0} Q, count
@@ -358,7 +361,7 @@ static bool chain_tc(sdn_handle* h, int64_t rows) {
 static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0, int K0,
                        const float* W0, int64_t ldW0, const float* bias0, bool store_D,
                        float* phi_out, const TcOperand* tcX0, float* const* Hs = nullptr,
-                       bool simt = false) {
+                       bool simt = false, bool fuse_seed = false) {
   const int L = h->L;
   const bool tcc = !simt && chain_tc(h, nrows);
   float* const* Hb = Hs ? Hs : h->H;
@@ -378,7 +381,13 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
     h->prows = nrows;
     if (l == L - 1) {
       EpiAffine e{bl, h->ostd, h->omean, phi_out, (int64_t)n_out};
-      TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA, tc ? 1 : 0)));
+      if (fuse_seed && tc && L > 1) {      // + the reverse sweep's unit seeds (bf16x3 split)
+        EpiAffineSeed es{e, h->seed_a2, h->seed_b2, TcEpiSplit{&h->sw->seed}};
+        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, es, tB, tA, 1)));
+        h->seed_fused = true;
+      } else {
+        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA, tc ? 1 : 0)));
+      }
     } else {
       float* out = Hb[(l == 0) ? 0 : 1 - cur];
       // in a tensor-core chain the residual is read from the bf16 split of the
@@ -565,6 +574,8 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->ref_ghist, (size_t)2 * h->num_sms * 256))) return bail(rc);
   if ((rc = dalloc(h, &h->ref_gmm, (size_t)2 * h->num_sms))) return bail(rc);
   if ((rc = dalloc(h, &h->Qr, cap))) return bail(rc);
+  if ((rc = dalloc(h, &h->seed_a2, h->r_u))) return bail(rc);
+  if ((rc = dalloc(h, &h->seed_b2, h->r_u))) return bail(rc);
   if ((rc = dalloc(h, &h->wpart, (size_t)h->qgrid * 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->vsum, 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);
@@ -708,6 +719,10 @@ int sdn_set_model(sdn_handle* h, const float* const* W, const float* const* b, c
   CU(cudaMemcpy(h->omean, out_mean, (size_t)h->r_u * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->ostd, out_std, (size_t)h->r_u * 4, cudaMemcpyHostToDevice));
   if (h->tcw.enabled) TRY(tc_set_weights(h, h->tcw));
+  if (h->have_form) {
+    k_seedcoef<<<1, 256>>>(h->r_u, h->ostd, h->c, h->seed_a2, h->seed_b2);
+    CU(cudaDeviceSynchronize());
+  }
   h->have_model = true;
   h->have_mean = false;
   h->gen++;
@@ -720,6 +735,8 @@ int sdn_set_tracking(sdn_handle* h, const float* c, double q0) {
   CU(cudaMemcpy(h->c, c, (size_t)h->r_u * 4, cudaMemcpyHostToDevice));
   h->q0 = q0;
   h->have_form = true;
+  k_seedcoef<<<1, 256>>>(h->r_u, h->ostd, h->c, h->seed_a2, h->seed_b2);
+  CU(cudaDeviceSynchronize());
   h->have_mean = false;
   h->gen++;
   return SDN_OK;
@@ -845,8 +862,10 @@ static int refine_window(sdn_handle* h, const sdn_risk* risk, bool dec, int qg, 
 // (all, n_all): the evaluation's risks, whose t values travel with z (graph
 // parameters); slot: this forward's risk among them
 static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, double* stats_dev,
-                        bool store_D, const sdn_risk* all = nullptr, int n_all = 0, int slot = 0) {
+                        bool store_D, const sdn_risk* all = nullptr, int n_all = 0, int slot = 0,
+                        bool fuse_seed = false) {
   if (!all) { all = risk; n_all = 1; slot = 0; }
+  h->seed_fused = false;
   if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
   if (risk->qoi == SDN_QOI_REDUCED && !h->have_form) return fail(SDN_ERR_STATE, "set_tracking first");
   if (risk->qoi == SDN_QOI_DECODED && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
@@ -871,7 +890,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   CHECK_LAUNCH(h);
   if (h->n > 0) {
     TRY(run_forward(h, h->n, h->MR, h->r_m, h->r_m, h->W[0], h->r_m, h->zb, store_D, h->Y,
-                    h->tcw.enabled ? &h->tcw.mr : nullptr));
+                    h->tcw.enabled ? &h->tcw.mr : nullptr, nullptr, false, fuse_seed && !dec && store_D));
     if (dec) {
       TRY((gemm<false, true>(h, h->n, nullptr, h->r_u, h->r_u, h->Y, h->r_u, h->Kg, h->r_u,
                              EpiStore{h->KPhi, (int64_t)h->r_u})));
@@ -1057,13 +1076,15 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
     return SDN_OK;
   }
   const bool tcs = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
-  { ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
+  if (!(dense && h->seed_fused && tcs && h->sw == &h->sw0)) {   // else: written by the output layer
+  ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * h->r_u);
   const int sg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nmax, 8), 4 * h->num_sms));
   k_seed<<<sg, 256, 0, h->stream>>>(nmax, nact, rowidx, h->r_u, h->Y, dec ? h->KPhi : nullptr,
                                     dec ? h->cdec : h->c, h->ostd, nullptr, nullptr, RISK_UNIT, 0.0, 0.0, 1.0,
-                                    0.0, 0.0, sw.E, tcs ? sw.seed.hi : nullptr, tcs ? sw.seed.lo : nullptr); }
+                                    0.0, 0.0, sw.E, tcs ? sw.seed.hi : nullptr, tcs ? sw.seed.lo : nullptr);
   h->launches++;
   CHECK_LAUNCH(h);
+  }
   const int64_t tplane = cdiv(sw.rows, 128) * 4 * h->maxw;
   SweepSum ssum;
   ssum.W = sw.W;
@@ -1254,8 +1275,9 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     n_exact += risks[i].kind == SDN_RISK_CVAR_EXACT;
     dense |= risks[i].kind == SDN_RISK_MEAN || risks[i].kind == SDN_RISK_MEANVAR;
   }
+  // a dense sweep over all rows: the output layer writes its unit seeds
   TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad, risks, n_risks,
-                   smooth >= 0 ? smooth : 0));
+                   smooth >= 0 ? smooth : 0, dense && any_grad));
   std::vector<const uint8_t*> masks(n_risks, nullptr);
   auto select_all = [&]() -> int {
     for (int i = 0, e = 0; i < n_risks; ++i) {

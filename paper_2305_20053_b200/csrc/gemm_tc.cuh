@@ -74,6 +74,30 @@ struct TcEpiSplit {
   }
 };
 
+// output layer fused with the sweep's unit seeds (reduced frame, dense sweep):
+// phi = shift + scale (acc + bias) -> C (fp32); seed = 2 sigma (phi + c) =
+// a2 phi + b2 -> bf16x3 split (the reverse sweep's first A operand)
+struct EpiAffineSeed {
+  EpiAffine base;
+  const float* a2;
+  const float* b2;
+  TcEpiSplit seed;
+  SDN_DEV void operator()(int64_t r, int c, float4 v) const {
+    float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float y = x[j] + (base.bias ? base.bias[c + j] : 0.0f);
+      if (base.scale) y *= base.scale[c + j];
+      if (base.shift) y += base.shift[c + j];
+      x[j] = y;
+    }
+    *reinterpret_cast<float4*>(base.C + r * base.ldc + c) = make_float4(x[0], x[1], x[2], x[3]);
+    seed.store(r, c, make_float4(fmaf(a2[c], x[0], b2[c]), fmaf(a2[c + 1], x[1], b2[c + 1]),
+                                 fmaf(a2[c + 2], x[2], b2[c + 2]), fmaf(a2[c + 3], x[3], b2[c + 3])));
+  }
+  SDN_DEV void col(int64_t, int, float) const {}   // r_u is a multiple of 4
+};
+
 template <class Epi>
 struct TcChain {
   Epi base;
@@ -519,6 +543,45 @@ struct TileEpi<EpiAffine> {
   }
 };
 
+template <>
+struct TileEpi<EpiAffineSeed> {
+  using Pre = PreAff;
+  static SDN_DEV void load(const EpiAffineSeed& e, const TileRows& tr, int c0, int N, int lane, Pre& p) {
+    TileEpi<EpiAffine>::load(e.base, tr, c0, N, lane, p);
+  }
+  static SDN_DEV void chunk(const EpiAffineSeed& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
+                            const uint32_t (&v)[16], const Pre& pre) {
+    float x[16], sd[16];
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      const float4 b = pre.b[j / 4], sc = pre.s[j / 4];
+      x[j] = fmaf(sc.x, __uint_as_float(v[j]), b.x);
+      x[j + 1] = fmaf(sc.y, __uint_as_float(v[j + 1]), b.y);
+      x[j + 2] = fmaf(sc.z, __uint_as_float(v[j + 2]), b.z);
+      x[j + 3] = fmaf(sc.w, __uint_as_float(v[j + 3]), b.w);
+      const int c = min(c0 + j, N - 4);
+      const float4 a2 = __ldg(reinterpret_cast<const float4*>(e.a2 + c));
+      const float4 b2 = __ldg(reinterpret_cast<const float4*>(e.b2 + c));
+      sd[j] = fmaf(a2.x, x[j], b2.x);
+      sd[j + 1] = fmaf(a2.y, x[j + 1], b2.y);
+      sd[j + 2] = fmaf(a2.z, x[j + 2], b2.z);
+      sd[j + 3] = fmaf(a2.w, x[j + 3], b2.w);
+    }
+    epi_reclaim(s, lane);
+    row_put(s.f0, lane, x);
+    row_put_split(s.h, s.l, lane, sd);
+    if (s.om) {
+      epi_issue(s, lane, tr.r0, c0, true, false, true, true);
+      return;
+    }
+    __syncwarp();
+    tile_out(s.f0, e.base.C, e.base.ldc, tr, c0, N, lane);
+    tile_out_h(s.h, e.seed.hi, e.seed.ld, tr, c0, N, lane);
+    tile_out_h(s.l, e.seed.lo, e.seed.ld, tr, c0, N, lane);
+    __syncwarp();
+  }
+};
+
 // hidden layer forward: H = [prev +] act(acc + b), D = act'(.), split(H).
 // In a tensor-core chain prev comes from the previous layer's bf16 split
 // (ch.prev) and the fp32 H is not written (e.H == nullptr).
@@ -929,6 +992,16 @@ template <>
 struct EpiOut<EpiAffine> {
   static int build(TcWeights& t, const EpiAffine& e, int64_t M, int N, TcOutMaps& om) {
     return tc_out_map(t, e.C, false, M, N, e.ldc, &om.m[0]) == 0 ? 1 : 0;
+  }
+};
+template <>
+struct EpiOut<EpiAffineSeed> {
+  static int build(TcWeights& t, const EpiAffineSeed& e, int64_t M, int N, TcOutMaps& om) {
+    if (tc_out_map(t, e.base.C, false, M, N, e.base.ldc, &om.m[0])) return 0;
+    if (tc_out_map(t, e.seed.hi, true, M, N, e.seed.ld, &om.m[2]) ||
+        tc_out_map(t, e.seed.lo, true, M, N, e.seed.ld, &om.m[3]))
+      return 0;
+    return 1;
   }
 };
 template <>

@@ -33,6 +33,16 @@ k_zbias(int h1, int d_z, const double* __restrict__ Pz, const double* __restrict
   }
 }
 
+// unit-seed coefficients of the fused output-layer epilogue (reduced frame):
+// seed = 2 sigma (phi + c) = a2 phi + b2
+__global__ void k_seedcoef(int r_u, const float* __restrict__ ostd, const float* __restrict__ c,
+                           float* __restrict__ a2, float* __restrict__ b2) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < r_u; j += gridDim.x * blockDim.x) {
+    a2[j] = (float)(2.0 * (double)ostd[j]);
+    b2[j] = (float)(2.0 * (double)ostd[j] * (double)c[j]);
+  }
+}
+
 // X = [m_r, z_row, 0-pad]  (forward_batch / jacobian rows with per-row z)
 __global__ void k_build_x(int64_t n, int r_m, int d_z, int ldx, const float* __restrict__ mr,
                           const float* __restrict__ z, float* __restrict__ X) {
