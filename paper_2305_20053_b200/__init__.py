@@ -7,10 +7,10 @@ from .api import (Decoder, NetworkSpec, OptResult, ReducedTrackingForm, RiskSpec
                   SurrogateEvaluator, SurrogateModel, build_tracking_form, init_model,
                   mc_cvar, mc_var, minimize, saa_objective, splus, splus_d1)
 from .engine import Engine, EvalResult
-from . import workloads
+from . import fileio, workloads
 
 __version__ = "0.1.0"
 
 __all__ = ["Decoder", "Engine", "EvalResult", "NetworkSpec", "OptResult", "ReducedTrackingForm", "RiskSpec", "minimize",
            "SAAProblem", "SurrogateEvaluator", "SurrogateModel", "build_tracking_form", "init_model",
-           "mc_cvar", "mc_var", "saa_objective", "splus", "splus_d1", "workloads"]
+           "mc_cvar", "mc_var", "saa_objective", "splus", "splus_d1", "fileio", "workloads"]
