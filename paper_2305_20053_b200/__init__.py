@@ -3,14 +3,14 @@
 surface (ouukit/__init__.py:5-22); the compute runs in libsaadino.so
 (hand-written sm_100a CUDA, include/saadino.h)."""
 
-from .api import (Decoder, NetworkSpec, OptResult, ReducedTrackingForm, RiskSpec, SAAProblem,
-                  SurrogateEvaluator, SurrogateModel, build_tracking_form, init_model,
+from .api import (Decoder, NetworkSpec, OptResult, ReducedTrackingForm, RiskSpec, SAAProblem, SurrogateErrors,
+                  SurrogateEvaluator, SurrogateModel, build_tracking_form, evaluate_errors, init_model,
                   mc_cvar, mc_var, minimize, saa_objective, splus, splus_d1)
 from .engine import Engine, EvalResult
 from . import fileio, workloads
 
 __version__ = "0.1.0"
 
-__all__ = ["Decoder", "Engine", "EvalResult", "NetworkSpec", "OptResult", "ReducedTrackingForm", "RiskSpec", "minimize",
+__all__ = ["SurrogateErrors", "evaluate_errors", "Decoder", "Engine", "EvalResult", "NetworkSpec", "OptResult", "ReducedTrackingForm", "RiskSpec", "minimize",
            "SAAProblem", "SurrogateEvaluator", "SurrogateModel", "build_tracking_form", "init_model",
            "mc_cvar", "mc_var", "saa_objective", "splus", "splus_d1", "fileio", "workloads"]

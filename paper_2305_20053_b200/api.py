@@ -137,6 +137,47 @@ def init_model(spec: NetworkSpec, seed: int, input_scale=None, output_mean=None,
 
 
 # ---------------------------------------------------------------------------
+# surrogate error metrics (surrogate.py:411-448), forward and z-Jacobian on the GPU
+
+
+@dataclass(frozen=True)
+class SurrogateErrors:
+    state_rel_l2: float     # full-space relative M-norm error (mean over the set)
+    jac_rel_hs: float       # mean relative Frobenius error of the z-Jacobian
+    reduced_rel_l2: float   # reduced-frame part alone (lower bound on the state error)
+
+
+def evaluate_errors(model: SurrogateModel, test, chunk: int = 4096) -> SurrogateErrors:
+    """Mean relative state and Jacobian errors over a test set (a
+    fileio.TrainingDataset or any object with m_r, z, u_r, j_r, state_norm_sq,
+    trunc_norm_sq).  The forward and forward-mode z-Jacobian of every test
+    sample run batched on the device (chunks of `chunk` samples); the per-sample
+    norms are combined in float64 exactly as the reference does."""
+    n = int(np.asarray(test.m_r).shape[0])
+    if n == 0:
+        raise ValueError("empty test set")
+    if getattr(test, "j_r", None) is None:
+        raise ValueError("test set must carry Jacobian data")
+    if test.state_norm_sq is None or test.trunc_norm_sq is None:
+        raise ValueError("test set must carry per-sample state/truncation norms")
+    red_sq = np.empty(n)
+    jac_rel = np.empty(n)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        pred = model.forward_batch(test.m_r[a:b], test.z[a:b])
+        red_sq[a:b] = np.sum((pred - test.u_r[a:b]) ** 2, axis=1)
+        jac = model.z_jacobian_batch(test.m_r[a:b], test.z[a:b])
+        jt = np.asarray(test.j_r[a:b], float).reshape(b - a, -1)
+        num = np.linalg.norm(jac.reshape(b - a, -1) - jt, axis=1)
+        jac_rel[a:b] = num / np.maximum(np.linalg.norm(jt, axis=1), 1e-300)
+    denom = np.sqrt(np.maximum(np.asarray(test.state_norm_sq, float), 1e-300))
+    state_rel = np.sqrt(red_sq + np.asarray(test.trunc_norm_sq, float)) / denom
+    reduced_rel = np.sqrt(red_sq) / denom
+    return SurrogateErrors(state_rel_l2=float(state_rel.mean()), jac_rel_hs=float(jac_rel.mean()),
+                           reduced_rel_l2=float(reduced_rel.mean()))
+
+
+# ---------------------------------------------------------------------------
 # QoI forms (pod.py:46-62, 104-110)
 
 

@@ -16,7 +16,7 @@ REF = os.environ.get("OUUKIT_REF", "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 
 from ouukit.fileio import save_basis, save_dataset, save_model  # noqa: E402
-from ouukit.surrogate import NetworkSpec, TrainingDataset, init_model  # noqa: E402
+from ouukit.surrogate import NetworkSpec, TrainingDataset, evaluate_errors, init_model  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
 
@@ -56,6 +56,18 @@ def main():
         basis_ids={"kle": "k0"})), np.uint8)
     out["ds_m_r"], out["ds_z"], out["ds_u_r"], out["ds_j_r"] = ds.m_r, ds.z, ds.u_r, ds.j_r
     out["ds_state_norm_sq"] = ds.state_norm_sq
+    # evaluate_errors (surrogate.py:419-448) on a test set around the model's
+    # own predictions (so the relative errors are O(1e-2))
+    nt = 24
+    tm, tz = g.normal(size=(nt, 8)), g.uniform(-2, 2, size=(nt, 4))
+    tu = model.forward_batch(tm, tz) + 0.05 * g.normal(size=(nt, 8))
+    tj = model.z_jacobian_batch(tm, tz) + 0.02 * g.normal(size=(nt, 8, 4))
+    test = TrainingDataset(m_r=tm, z=tz, u_r=tu, j_r=tj, state_norm_sq=g.uniform(5, 10, nt),
+                           trunc_norm_sq=g.uniform(0, 0.1, nt))
+    errs = evaluate_errors(model, test)
+    out["err_m_r"], out["err_z"], out["err_u_r"], out["err_j_r"] = tm, tz, tu, tj
+    out["err_state_norm_sq"], out["err_trunc_norm_sq"] = test.state_norm_sq, test.trunc_norm_sq
+    out["err_values"] = np.array([errs.state_rel_l2, errs.jac_rel_hs, errs.reduced_rel_l2])
     np.savez(os.path.join(OUT, "ref_files.npz"), **out)
     print("wrote", sorted(out))
 

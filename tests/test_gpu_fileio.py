@@ -42,3 +42,17 @@ def test_engine_from_files_encodes_with_the_kle_basis():
     m_r = ref.encode(fields, kle["modes"][:, :model.spec.r_m].astype(np.float32), mass, 0.25)
     Qo, _ = ref.evaluate_reverse(ref.as_oracle(model), m_r, z, form=ref.ReducedForm(c.astype(np.float64), 0.5))
     assert _rel(Q, Qo) <= 1e-5
+
+
+def test_evaluate_errors_matches_reference():
+    """surrogate.py:419-448 on the reference-written model and a test set;
+    the reference's own SurrogateErrors are stored in the fixture."""
+    from paper_2305_20053_b200 import evaluate_errors
+    gf = dict(np.load(os.path.join(GOLD, "ref_files.npz")))
+    model, _ = fio.load_model(os.path.join(GOLD, "ref_model.bin"))
+    test = fio.TrainingDataset(m_r=gf["err_m_r"], z=gf["err_z"], u_r=gf["err_u_r"], j_r=gf["err_j_r"],
+                               state_norm_sq=gf["err_state_norm_sq"], trunc_norm_sq=gf["err_trunc_norm_sq"])
+    e = evaluate_errors(model, test, chunk=10)            # ragged chunks
+    np.testing.assert_allclose([e.state_rel_l2, e.jac_rel_hs, e.reduced_rel_l2], gf["err_values"], rtol=1e-4)
+    with pytest.raises(ValueError):
+        evaluate_errors(model, fio.TrainingDataset(m_r=gf["err_m_r"], z=gf["err_z"], u_r=gf["err_u_r"]))
