@@ -50,6 +50,7 @@ extern "C" {
 #define SDN_ACT_SOFTPLUS 2
 #define SDN_ACT_SIGMOID 3
 #define SDN_ACT_ELU 4
+#define SDN_ACT_SOFTMAX 5   /* per-layer vector softmax (surrogate.py:65-66, 175-177); SIMT chains */
 
 /* risk kinds: mean / smoothed CVaR as RiskSpec (riskopt.py:204-216), plus
  * mean + beta*variance and exact CVaR by device selection (BASELINE) */

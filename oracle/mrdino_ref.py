@@ -35,7 +35,15 @@ def _sigmoid(x):
     return 0.5 * (1.0 + np.tanh(0.5 * x))
 
 
+def _softmax_rows(s: np.ndarray) -> np.ndarray:
+    """surrogate.py:175-177: per-layer vector softmax over the units (rows)."""
+    e = np.exp(s - s.max(axis=-1, keepdims=True))
+    return e / e.sum(axis=-1, keepdims=True)
+
+
 def act_value(name: str, s: np.ndarray) -> np.ndarray:
+    if name == "softmax":
+        return _softmax_rows(s)
     if name == "tanh":
         return np.tanh(s)
     if name == "softplus":
@@ -188,7 +196,11 @@ def z_jacobian_batch(model: OracleModel, m_r: np.ndarray, z: np.ndarray) -> np.n
             h, T = S, U
         else:
             a = act_value(model.activation, S)
-            dT = act_deriv(model.activation, S)[:, None, :] * U
+            if model.activation == "softmax":      # surrogate.py:214-217
+                dot = np.einsum("bn,bkn->bk", a, U)
+                dT = a[:, None, :] * (U - dot[:, :, None])
+            else:
+                dT = act_deriv(model.activation, S)[:, None, :] * U
             if _is_residual(model, l):
                 h, T = h + a, T + dT
             else:
@@ -412,7 +424,11 @@ def _reverse_input_grad(model: OracleModel, caches, seed_y: np.ndarray) -> np.nd
             gS = g
             g = gS @ W
         else:
-            gS = act_deriv(model.activation, S) * g
+            if model.activation == "softmax":      # d softmax^T g = a (g - a.g)
+                a = _softmax_rows(S)
+                gS = a * (g - np.sum(a * g, axis=1, keepdims=True))
+            else:
+                gS = act_deriv(model.activation, S) * g
             g = gS @ W + (g if _is_residual(model, l) else 0.0)
     return g
 

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsaadino.so")
 
 SDN_OK = 0
-ACT = {"identity": 0, "tanh": 1, "softplus": 2, "sigmoid": 3, "elu": 4}
+ACT = {"identity": 0, "tanh": 1, "softplus": 2, "sigmoid": 3, "elu": 4, "softmax": 5}
 RISK = {"mean": 0, "cvar": 1, "meanvar": 2, "cvar_exact": 3}
 QOI = {"reduced": 0, "decoded": 1}
 GEMM = {"auto": 0, "simt": 1, "tc": 2}

@@ -27,7 +27,7 @@ import numpy as np
 from .engine import Engine
 from . import workloads as _wl
 
-_ACTS = ("tanh", "softplus", "sigmoid", "identity", "elu")
+_ACTS = ("tanh", "softplus", "sigmoid", "identity", "elu", "softmax")   # softmax: per-layer vector (surrogate.py:65-66)
 
 
 # ---------------------------------------------------------------------------

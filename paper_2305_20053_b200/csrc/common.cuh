@@ -10,7 +10,8 @@ namespace sdn {
 
 // ---------------------------------------------------------------------------
 // activations (reference: ouukit surrogate.py:42-63; ELU is the BASELINE gap)
-enum Act : int { ACT_IDENTITY = 0, ACT_TANH = 1, ACT_SOFTPLUS = 2, ACT_SIGMOID = 3, ACT_ELU = 4 };
+enum Act : int { ACT_IDENTITY = 0, ACT_TANH = 1, ACT_SOFTPLUS = 2, ACT_SIGMOID = 3, ACT_ELU = 4,
+                 ACT_SOFTMAX = 5 /* per-layer vector softmax: row kernels, not elementwise */ };
 
 // value and derivative of the activation at pre-activation s
 SDN_DEV void act_eval(int act, float s, float& a, float& d) {

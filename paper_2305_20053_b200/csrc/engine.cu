@@ -341,7 +341,8 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
 // chain is routed as one unit so that intermediates only the SIMT path reads
 // (fp32 H for residuals, fp32 U) are skipped when every GEMM is tcgen05.
 static bool chain_tc(sdn_handle* h, int64_t rows) {
-  if (!h->tcw.enabled || h->gemm == SDN_GEMM_SIMT || rows < 1) return false;
+  // softmax layers run SIMT chains (row kernels between the GEMMs)
+  if (!h->tcw.enabled || h->gemm == SDN_GEMM_SIMT || rows < 1 || h->act == ACT_SOFTMAX) return false;
   for (int l = 0; l < h->L; ++l) {
     const int n_out = h->w[l + 1], n_in = (l == 0) ? h->r_m : h->w[l];
     if (!tc_gemm_supported(rows, n_out, n_in) || n_in % 8 || n_out % 8) return false;
@@ -390,6 +391,19 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
       }
     } else {
       float* out = Hb[(l == 0) ? 0 : 1 - cur];
+      if (h->act == ACT_SOFTMAX) {                // S + b, then the row softmax (SIMT chain)
+        EpiFwdHidden e{bl, nullptr, out, nullptr, (int64_t)n_out, ACT_IDENTITY};
+        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, nullptr, nullptr, 0)));
+        k_softmax_rows<<<(unsigned)cdiv(nrows, 8), 256, 0, h->stream>>>(nrows, n_out, out,
+                                                                      store_D ? h->D[l] : nullptr,
+                                                                      h->res[l] ? in : nullptr);
+        h->launches++;
+        CHECK_LAUNCH(h);
+        cur = (l == 0) ? 0 : 1 - cur;
+        in = out;
+        ldin = n_out;
+        continue;
+      }
       // in a tensor-core chain the residual is read from the bf16 split of the
       // layer input (the A operand), and the fp32 H is never needed
       const bool split_prev = tc && h->res[l];
@@ -453,11 +467,18 @@ static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const
       return SDN_OK;
     }
     const bool last = (l == 1);
-    EpiBwd e{resid, h->res[l - 1] ? h->sw->G : nullptr, h->D[l - 1], (int64_t)N, rowidx,
+    const bool smax = h->act == ACT_SOFTMAX;     // derivative applied by a row kernel below
+    EpiBwd e{resid, h->res[l - 1] ? h->sw->G : nullptr, smax ? nullptr : h->D[l - 1], (int64_t)N, rowidx,
              (!tcc || last) ? h->sw->Ub[1 - cur] : nullptr, (int64_t)N};
     TcEpiSplit split = (tcc && !last) ? TcEpiSplit{&h->sw->act[1 - cur]} : TcEpiSplit{nullptr};
     TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, TcChain<EpiBwd>{e, split}, tB, tA,
                             route)));
+    if (smax) {
+      k_softmax_bwd<<<(unsigned)cdiv(nmax, 8), 256, 0, h->stream>>>(nmax, n_act_dev, rowidx, N, h->D[l - 1],
+                                                                    h->sw->Ub[1 - cur]);
+      h->launches++;
+      CHECK_LAUNCH(h);
+    }
     cur = 1 - cur;
   }
   *u0_out = h->sw->Ub[cur];
@@ -479,7 +500,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
     if (cfg->widths[i] < 1) return fail(SDN_ERR_ARG, "all widths must be positive");
   if (cfg->r_m < 1 || cfg->d_z < 1 || cfg->r_m >= cfg->widths[0])
     return fail(SDN_ERR_ARG, "need 1 <= r_m < widths[0] and d_z >= 1");
-  if (cfg->activation < 0 || cfg->activation > 4) return fail(SDN_ERR_ARG, "unknown activation");
+  if (cfg->activation < 0 || cfg->activation > 5) return fail(SDN_ERR_ARG, "unknown activation");
   if (cfg->max_samples < 1) return fail(SDN_ERR_ARG, "max_samples must be >= 1");
   for (int i = 1; i <= cfg->n_layers; ++i)
     if (cfg->widths[i] % 4 != 0) return fail(SDN_ERR_ARG, "layer output widths must be multiples of 4");
@@ -820,6 +841,7 @@ static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, 
   a.r_u = h->r_u; a.c32 = h->c; a.K64 = dec ? h->K64 : nullptr; a.c64 = dec ? h->c64dec : nullptr;
   a.q0 = dec ? h->q0dec : h->q0; a.Q = Qt ? Qt : h->Q; a.mask = mask;
   a.k = k; a.ghist = h->ref_ghist; a.gmm = h->ref_gmm; a.refine = do_refine ? 1 : 0;
+  a.softmax = h->act == ACT_SOFTMAX ? 1 : 0;
   void* args[] = {&a};
   ProfScope ps(h, k > 0 ? PC_SELECT : PC_REFINE, 0.0, k > 0 ? 8.0 * 8.0 * h->n : 0.0);
   if (h->ref_trace) {
@@ -1745,13 +1767,24 @@ int sdn_jacobian_batch(sdn_handle* h, const float* m_r, const float* z, int64_t 
     if (L == 1) {
       // linear model: tangent of y is the constant Pz (w[1] = r_u)
       k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, nullptr, h->Pz32t, Tc);
+    } else if (h->act == ACT_SOFTMAX) {          // T = a (U - a.U), U = (W1_z V_z^T)_k
+      k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, nullptr, h->Pz32t, Tc);
+      k_softmax_tangent<<<(unsigned)cdiv(rows, 8), 256, 0, h->stream>>>(rows, d_z, h->h1, h->D[0], Tc, nullptr);
+      h->launches++;
     } else {
       k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, h->D[0], h->Pz32t, Tc);
     }
     h->launches++;
     for (int l = 1; l < L - 1 && rc == SDN_OK; ++l) {
-      EpiTangent e{h->D[l], (int64_t)h->w[l + 1], d_z, h->res[l] ? Tc : nullptr, Tn, (int64_t)h->w[l + 1]};
+      const bool smax = h->act == ACT_SOFTMAX;
+      EpiTangent e{smax ? nullptr : h->D[l], (int64_t)h->w[l + 1], d_z, (h->res[l] && !smax) ? Tc : nullptr, Tn,
+                   (int64_t)h->w[l + 1]};
       rc = gemm<false, true>(h, rows, nullptr, h->w[l + 1], h->w[l], Tc, h->w[l], h->W[l], h->w[l], e);
+      if (smax && rc == SDN_OK) {
+        k_softmax_tangent<<<(unsigned)cdiv(rows, 8), 256, 0, h->stream>>>(rows, d_z, h->w[l + 1], h->D[l], Tn,
+                                                                          h->res[l] ? Tc : nullptr);
+        h->launches++;
+      }
       std::swap(Tc, Tn);
     }
     if (rc) break;

@@ -223,7 +223,8 @@ struct EpiBwd {
     }
     if (G) *reinterpret_cast<float4*>(G + r * ld + c) = make_float4(g[0], g[1], g[2], g[3]);
     int64_t rd = rowidx ? (int64_t)rowidx[r] : r;
-    float4 d = *reinterpret_cast<const float4*>(D + rd * ldD + c);
+    // D null: the derivative is applied after the GEMM (softmax: a (g - a.g))
+    float4 d = D ? *reinterpret_cast<const float4*>(D + rd * ldD + c) : make_float4(1.f, 1.f, 1.f, 1.f);
     float4 u = make_float4(d.x * g[0], d.y * g[1], d.z * g[2], d.w * g[3]);
     if (U) *reinterpret_cast<float4*>(U + r * ld + c) = u;
     return u;
@@ -237,7 +238,7 @@ struct EpiBwd {
 struct EpiTangent {
   const float* D; int64_t ldD; int rowdiv; const float* tin; float* tout; int64_t ld;
   SDN_DEV void operator()(int64_t r, int c, float4 v) const {
-    float4 d = *reinterpret_cast<const float4*>(D + (r / rowdiv) * ldD + c);
+    float4 d = D ? *reinterpret_cast<const float4*>(D + (r / rowdiv) * ldD + c) : make_float4(1.f, 1.f, 1.f, 1.f);
     float4 o = make_float4(d.x * v.x, d.y * v.y, d.z * v.z, d.w * v.w);
     if (tin) {
       float4 p = *reinterpret_cast<const float4*>(tin + r * ld + c);

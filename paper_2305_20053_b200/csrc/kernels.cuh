@@ -704,7 +704,63 @@ __global__ void k_tangent_seed(int64_t rows, int d_z, int h1, const float* __res
   if (r >= rows) return;
   int64_t i = r / d_z; int k = (int)(r % d_z);
   for (int c = threadIdx.x; c < h1; c += blockDim.x)
-    T[r * h1 + c] = D0[i * h1 + c] * Pz32t[(int64_t)k * h1 + c];
+    T[r * h1 + c] = (D0 ? D0[i * h1 + c] : 1.0f) * Pz32t[(int64_t)k * h1 + c];
+}
+
+// ---- per-layer vector softmax (surrogate.py:175-177, 214-217), SIMT chains
+// One warp per row, fp64 row reductions (fixed lane order), widths <= any.
+// forward: a = softmax(S) over the row; H = [prev +] a; D = a (for the sweep)
+__global__ void __launch_bounds__(256)
+k_softmax_rows(int64_t n, int w, float* __restrict__ H, float* __restrict__ D, const float* __restrict__ prev) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  float* h = H + r * w;
+  float mx = -INFINITY;
+  for (int c = lane; c < w; c += 32) mx = fmaxf(mx, h[c]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double sum = 0.0;
+  for (int c = lane; c < w; c += 32) sum += exp((double)h[c] - (double)mx);
+  sum = warp_sum(sum);
+  for (int c = lane; c < w; c += 32) {
+    const float a = (float)(exp((double)h[c] - (double)mx) / sum);
+    if (D) D[r * w + c] = a;
+    h[c] = prev ? prev[r * w + c] + a : a;
+  }
+}
+
+// reverse: u = a (g - a.g) in place on U (rows r < *n_dev; a = D[rowidx[r]])
+__global__ void __launch_bounds__(256)
+k_softmax_bwd(int64_t n, const int* __restrict__ n_dev, const int* __restrict__ rowidx, int w,
+              const float* __restrict__ D, float* __restrict__ U) {
+  const int64_t nr = n_dev ? (int64_t)*n_dev : n;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= nr) return;
+  const float* a = D + (rowidx ? (int64_t)rowidx[r] : r) * w;
+  float* u = U + r * w;
+  double dot = 0.0;
+  for (int c = lane; c < w; c += 32) dot += (double)a[c] * (double)u[c];
+  dot = warp_sum(dot);
+  for (int c = lane; c < w; c += 32) u[c] = (float)((double)a[c] * ((double)u[c] - dot));
+}
+
+// tangent rows (sample i = r / rowdiv): T = a (U - a.U) [+ Tin]
+__global__ void __launch_bounds__(256)
+k_softmax_tangent(int64_t rows, int rowdiv, int w, const float* __restrict__ D, float* __restrict__ U,
+                  const float* __restrict__ tin) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* a = D + (r / rowdiv) * w;
+  float* u = U + r * w;
+  double dot = 0.0;
+  for (int c = lane; c < w; c += 32) dot += (double)a[c] * (double)u[c];
+  dot = warp_sum(dot);
+  for (int c = lane; c < w; c += 32) {
+    const float t = (float)((double)a[c] * ((double)u[c] - dot));
+    u[c] = tin ? tin[r * w + c] + t : t;
+  }
 }
 
 }  // namespace sdn

@@ -66,6 +66,7 @@ struct RefineArgs {
   unsigned* ghist;              // 2 x gridDim.x x 256 scratch
   unsigned long long* gmm;      // 2 x gridDim.x scratch (min / max keys)
   int refine;                   // 0: selection only
+  int softmax;                  // hidden layers are per-row softmax (a row pass after each layer)
   unsigned long long* trace;    // optional phase timestamps (block 0, %globaltimer)
 };
 
@@ -467,6 +468,8 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
           double o;
           if (last) {
             o = (double)a.omean[c] + (double)a.ostd[c] * S;
+          } else if (a.softmax) {
+            o = S;                                        // normalised by the row pass below
           } else {
             o = act64(a.act, S);
             if (ly.resid) o += xs[j * REF_KC + c];       // resid: K == N
@@ -481,6 +484,22 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     REF_STAMP(13 + 2 * l);
     grid_barrier(a.bar, gen);
     REF_STAMP(14 + 2 * l);
+    if (a.softmax && !last) {                      // per-row softmax (+ residual), one warp per row
+      for (int r = gw; r < m; r += nw) {
+        double* o = out + (int64_t)r * N;
+        double mx = -INFINITY;
+        for (int c = lane; c < N; c += 32) mx = fmax(mx, __ldcg(o + c));
+        for (int q = 16; q > 0; q >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, q));
+        double sum = 0.0;
+        for (int c = lane; c < N; c += 32) sum += exp(__ldcg(o + c) - mx);
+        sum = warp_sum(sum);
+        for (int c = lane; c < N; c += 32) {
+          const double v = exp(__ldcg(o + c) - mx) / sum;
+          o[c] = ly.resid ? __ldcg(in64 + (int64_t)r * K + c) + v : v;
+        }
+      }
+      grid_barrier(a.bar, gen);
+    }
   }
 
   // ---- 3. QoI of the band rows -> Q (reduced: phi.(phi + 2c); decoded: phi.(K phi + 2c))

@@ -29,7 +29,7 @@ def main():
     out = {}
 
     # --- networks: forward_batch / z_jacobian_batch per activation (surrogate.py:187-233)
-    for act in ("tanh", "softplus", "sigmoid", "identity"):
+    for act in ("tanh", "softplus", "sigmoid", "identity", "softmax"):
         spec = NetworkSpec(r_m=3, d_z=4, r_u=5, hidden=(8, 6), activation=act)
         model = init_model(spec, seed=3, input_scale=g.uniform(0.5, 2, 3),
                            output_mean=g.normal(size=5), output_std=g.uniform(0.5, 2, 5))

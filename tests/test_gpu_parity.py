@@ -305,3 +305,39 @@ def test_smoothed_cvar_graph_replay_tracks_t():
         assert abs(r.value - o[0]) <= RTOL * abs(o[0])
         assert _rel(r.grad_z, o[1]) <= RTOL
         assert abs(r.grad_t - o[2]) <= 1e-6
+
+
+@pytest.mark.parametrize("residual", [False, True])
+def test_softmax_network_forward_jacobian_and_risks(residual):
+    """The reference's per-layer vector softmax (surrogate.py:65-66, 175-177,
+    214-217): forward, z-Jacobian and risk gradients (SIMT chains with row
+    kernels; fp64 refinement with a row pass) vs the float64 oracle."""
+    from paper_2305_20053_b200.api import NetworkSpec, init_model
+    g = np.random.default_rng(11)
+    spec = NetworkSpec(r_m=16, d_z=8, r_u=16, hidden=(64, 64, 64), activation="softmax", residual=residual)
+    model = init_model(spec, seed=4, input_scale=g.uniform(0.5, 2, 16), output_mean=g.normal(size=16),
+                       output_std=g.uniform(0.5, 2, 16))
+    for b in model.biases:
+        b[:] = 0.3 * g.normal(size=b.shape)
+    n = 600
+    m_r = g.normal(size=(n, 16)).astype(np.float32)
+    z = g.uniform(-1, 1, 8)
+    c = g.normal(size=16).astype(np.float32)
+    om = ref.as_oracle(model)
+    Zb = np.broadcast_to(z, (n, 8))
+    assert _rel(model.forward_batch(m_r[:50], Zb[:50]), ref.forward_batch(om, m_r[:50], Zb[:50])) <= 1e-5
+    assert _rel(model.z_jacobian_batch(m_r[:50], Zb[:50]), ref.z_jacobian_batch(om, m_r[:50], Zb[:50])) <= 1e-5
+    eng = Engine(model, max_samples=n)
+    eng.set_tracking(c, 1.5)
+    eng.set_samples(m_r)
+    form = ref.ReducedForm(c.astype(np.float64), 1.5)
+    Qo, Go = ref.evaluate_reverse(om, m_r, z, form=form)
+    Q, G = eng.eval_samples(z)
+    assert _rel(Q, Qo) <= 1e-5 and _rel(G, Go) <= 1e-4
+    for kind, beta in (("meanvar", 1.0), ("cvar_exact", 0.9)):
+        r = eng.eval(z, kind, beta=beta, alpha=1e-2)
+        o = ref.saa_objective(Qo, Go, z, ref.Risk(kind, beta=beta, alpha=1e-2))
+        assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+        assert _rel(r.grad_z, o[1]) <= RTOL
+        if kind == "cvar_exact":
+            np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qo, beta)))
