@@ -19,7 +19,7 @@ from ouukit.pod import ReducedTrackingForm, build_tracking_form, PODBasis  # noq
 from ouukit.randfield import MaternSpec, build_kle, sample_field  # noqa: E402
 from ouukit.riskopt import (RiskSpec, SAAProblem, SurrogateEvaluator, mc_cvar,  # noqa: E402
                             mc_var, saa_objective, splus, splus_d1)
-from ouukit.surrogate import NetworkSpec, init_model  # noqa: E402
+from ouukit.surrogate import NetworkSpec, TrainConfig, TrainingDataset, init_model, loss_and_grad, train  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden", "ref_golden.npz")
 
@@ -108,6 +108,38 @@ def main():
                tf_full=np.array([((basis.lift(p) - target) @ (M @ (basis.lift(p) - target))) for p in phis]))
 
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    # --- H1 training (surrogate.py:263-405): loss_and_grad and a short Adam run
+    for act in ("tanh", "softplus"):
+        spec = NetworkSpec(r_m=5, d_z=3, r_u=4, hidden=(12, 10), activation=act)
+        model = init_model(spec, seed=6, input_scale=g.uniform(0.5, 2, 5), output_mean=g.normal(size=4),
+                           output_std=g.uniform(0.5, 2, 4))
+        for b in model.biases:
+            b[:] = 0.1 * g.normal(size=b.shape)
+        ds = TrainingDataset(m_r=g.normal(size=(9, 5)), z=g.uniform(-2, 2, size=(9, 3)),
+                             u_r=g.normal(size=(9, 4)), j_r=g.normal(size=(9, 4, 3)))
+        pre = f"h1_{act}_"
+        for l, (W, b) in enumerate(zip(model.weights, model.biases)):
+            out[pre + f"W{l}"], out[pre + f"b{l}"] = W.copy(), b.copy()
+        out[pre + "in_scale"], out[pre + "out_mean"], out[pre + "out_std"] = (
+            model.input_scale, model.output_mean, model.output_std)
+        out[pre + "m_r"], out[pre + "z"], out[pre + "u_r"], out[pre + "j_r"] = ds.m_r, ds.z, ds.u_r, ds.j_r
+        for lam in (0.0, 0.7):
+            loss, gW, gb = loss_and_grad(model, ds, lam)
+            out[pre + f"loss_{lam}"] = np.array(loss)
+            for l in range(len(gW)):
+                out[pre + f"gW{l}_{lam}"], out[pre + f"gb{l}_{lam}"] = gW[l], gb[l]
+    spec = NetworkSpec(r_m=5, d_z=3, r_u=4, hidden=(12, 10), activation="tanh")
+    ds = TrainingDataset(m_r=g.normal(size=(24, 5)), z=g.uniform(-2, 2, size=(24, 3)),
+                         u_r=g.normal(size=(24, 4)), j_r=g.normal(size=(24, 4, 3)))
+    cfg = TrainConfig(epochs=3, batch_size=8, lr=3e-3, lr_drop_factor=0.5, lr_drop_epoch=2, jacobian_weight=0.5,
+                      seed=13)
+    model, hist = train(ds, spec, cfg)
+    out["train_m_r"], out["train_z"], out["train_u_r"], out["train_j_r"] = ds.m_r, ds.z, ds.u_r, ds.j_r
+    out["train_history"] = np.asarray(hist)
+    for l, (W, b) in enumerate(zip(model.weights, model.biases)):
+        out[f"train_W{l}"], out[f"train_b{l}"] = W, b
+    out["train_in_scale"], out["train_out_mean"], out["train_out_std"] = (
+        model.input_scale, model.output_mean, model.output_std)
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays, {os.path.getsize(OUT)} bytes")
 
