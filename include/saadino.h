@@ -218,6 +218,24 @@ int sdn_last_q(sdn_handle* h, const double** q_dev, int64_t* n);
  * no exact selection ran since the last forward. */
 int sdn_last_qsel(sdn_handle* h, const double** q_dev, int64_t* n);
 
+/* H1 (derivative-informed) training on the device (reference
+ * surrogate.py:263-405).  The handle's network shape and
+ * activation define the model (elementwise activations, no residual blocks,
+ * V_z = I, as the reference's network).  The dataset is resident on the device
+ * (j_r: n x r_u x d_z, may be null for jacobian_weight = 0); parameters are fp64
+ * masters in the reference layout (W_l: n_out x n_in over the full [m | z]
+ * input, b_l); sdn_train_step computes loss_and_grad over the batch idx and,
+ * when lr > 0, applies one Adam step (0.9, 0.999, 1e-8; step = 1-based count). */
+int sdn_train_setup(sdn_handle* h, const float* m_r, const float* z, const float* u_r, const float* j_r,
+                    int64_t n, int32_t batch_cap);
+int sdn_train_set_params(sdn_handle* h, const double* const* W, const double* const* b, const double* in_scale,
+                         const double* out_mean, const double* out_std);
+int sdn_train_set_mask(sdn_handle* h, const double* const* mW, const double* const* mb);   /* 0 = frozen entry */
+int sdn_train_get_params(sdn_handle* h, double* const* W, double* const* b);
+int sdn_train_get_grad(sdn_handle* h, double* const* gW, double* const* gb);
+int sdn_train_step(sdn_handle* h, const int64_t* idx, int32_t B, double jacobian_weight, double lr, int64_t step,
+                   double* loss);
+
 /* Instrumentation.  sdn_profile(h, 1) starts CUDA-event timing of every
  * launch by kernel class (0 fwd GEMM, 1 reverse GEMM, 2 QoI+moments,
  * 3 top-k select, 4 compaction, 5 seeds, 6 column sums, 7 finalise,

@@ -8,9 +8,10 @@ from .api import (Decoder, NetworkSpec, OptResult, ReducedTrackingForm, RiskSpec
                   mc_cvar, mc_var, minimize, saa_objective, splus, splus_d1)
 from .engine import Engine, EvalResult
 from . import fileio, workloads
+from .training import TrainConfig, TrainingDivergedError, loss_and_grad, train
 
 __version__ = "0.1.0"
 
-__all__ = ["SurrogateErrors", "evaluate_errors", "Decoder", "Engine", "EvalResult", "NetworkSpec", "OptResult", "ReducedTrackingForm", "RiskSpec", "minimize",
+__all__ = ["TrainConfig", "TrainingDivergedError", "loss_and_grad", "train", "SurrogateErrors", "evaluate_errors", "Decoder", "Engine", "EvalResult", "NetworkSpec", "OptResult", "ReducedTrackingForm", "RiskSpec", "minimize",
            "SAAProblem", "SurrogateEvaluator", "SurrogateModel", "build_tracking_form", "init_model",
            "mc_cvar", "mc_var", "saa_objective", "splus", "splus_d1", "fileio", "workloads"]

@@ -70,6 +70,12 @@ SIGNATURES = {
     "sdn_eval_select": (C.c_int, [_P, _P, C.c_int32, C.c_int64]),
     "sdn_eval_refine_band": (C.c_int, [_P]),
     "sdn_eval_keep_selection": (C.c_int, [_P, C.c_int32]),
+    "sdn_train_setup": (C.c_int, [_P, _F, _F, _F, _F, C.c_int64, C.c_int32]),
+    "sdn_train_set_params": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D), _D, _D, _D]),
+    "sdn_train_set_mask": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D)]),
+    "sdn_train_get_params": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D)]),
+    "sdn_train_get_grad": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D)]),
+    "sdn_train_step": (C.c_int, [_P, _I64, C.c_int32, C.c_double, C.c_double, C.c_int64, _D]),
     "sdn_eval_backward_multi": (C.c_int, [_P, C.POINTER(Risk), C.c_int32, _P, _P]),
     "sdn_eval_backward": (C.c_int, [_P, _P, _P]),
     "sdn_eval_set_risk": (C.c_int, [_P, C.POINTER(Risk)]),

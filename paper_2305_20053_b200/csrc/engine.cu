@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
 #include "refine.cuh"
+#include "train.cuh"
 
 // SMs left to side-stream work (the exact-CVaR selections) while the main
 // stream's persistent GEMMs run (sdn_eval_multi).  20 keeps the c2 sweep GEMMs
@@ -215,6 +216,26 @@ struct sdn_handle {
   double* c64dec = nullptr;
   bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
   bool ref_trace = false;       // env SDN_REFINE_TRACE=1
+  // H1 training state (sdn_train_*), allocated on first use
+  struct Train {
+    bool ready = false;
+    int64_t n = 0;
+    int bcap = 0;
+    float *dm = nullptr, *dz = nullptr, *du = nullptr, *dj = nullptr;
+    std::vector<int64_t> woff, boff;   // parameter offsets (W_l, b_l), reference layout
+    int64_t count = 0;
+    double *P = nullptr, *G = nullptr, *M = nullptr, *V = nullptr;
+    double* mask = nullptr;            // optional (padded networks)
+    float* P32 = nullptr;
+    float *scale = nullptr, *mu = nullptr, *sig = nullptr;
+    int* idx = nullptr;
+    float *Y = nullptr, *Jt = nullptr, *GA = nullptr, *GT = nullptr, *GS = nullptr, *GU = nullptr;
+    float *GA2 = nullptr, *GT2 = nullptr;
+    std::vector<float*> A, S, T, U;  // per layer (A[0] = X, T[0] = tangent seed)
+    double* part = nullptr;
+    double* hloss = nullptr;           // pinned
+    std::vector<void*> allocs;
+  } tr;
   // CUDA graph of the last evaluation configuration (sdn_eval_multi)
   bool use_graphs = true;       // env SDN_NO_GRAPH=1 disables
   cudaGraphExec_t gexec = nullptr;
@@ -660,6 +681,8 @@ int sdn_destroy(sdn_handle* h) {
   if (h->hidx) cudaFreeHost(h->hidx);
   tc_free(h->tcw);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (void* p : h->tr.allocs) cudaFree(p);
+  if (h->tr.hloss) cudaFreeHost(h->tr.hloss);
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->ev_fwd) cudaEventDestroy(h->ev_fwd);
   if (h->ev_side) cudaEventDestroy(h->ev_side);
@@ -2089,3 +2112,252 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   ms[0] = t / std::max(reps, 1);
   return SDN_OK;
 }
+
+
+// ---------------------------------------------------------------------------
+// H1 training (reference surrogate.py:263-405), SIMT
+// chains with fp64 gradients and fp64 master parameters (train.cuh)
+
+static int tr_alloc(sdn_handle* h, void** p, size_t bytes) {
+  CU(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+  h->tr.allocs.push_back(*p);
+  return SDN_OK;
+}
+
+extern "C" {
+
+int sdn_train_setup(sdn_handle* h, const float* m_r, const float* z, const float* u_r, const float* j_r, int64_t n,
+                    int32_t batch_cap) {
+  if (!h || !m_r || !z || !u_r || n < 1 || batch_cap < 1) return fail(SDN_ERR_ARG, "bad argument");
+  if (h->act == ACT_SOFTMAX || h->residual) return fail(SDN_ERR_ARG, "device training supports elementwise activations without residual blocks");
+  if (h->r_z != h->d_z) return fail(SDN_ERR_ARG, "device training needs V_z = I (the reference network)");
+  CU(cudaSetDevice(h->device));
+  auto& t = h->tr;
+  for (void* p : t.allocs) cudaFree(p);
+  t = sdn_handle::Train{};
+  const int L = h->L, d_z = h->d_z, r_m = h->r_m, r_u = h->r_u, B = batch_cap;
+  const int n0 = h->w[0];
+  t.n = n;
+  t.bcap = B;
+  TRY(tr_alloc(h, (void**)&t.dm, sizeof(float) * n * r_m));
+  TRY(tr_alloc(h, (void**)&t.dz, sizeof(float) * n * d_z));
+  TRY(tr_alloc(h, (void**)&t.du, sizeof(float) * n * r_u));
+  CU(cudaMemcpy(t.dm, m_r, sizeof(float) * n * r_m, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(t.dz, z, sizeof(float) * n * d_z, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(t.du, u_r, sizeof(float) * n * r_u, cudaMemcpyHostToDevice));
+  if (j_r) {
+    TRY(tr_alloc(h, (void**)&t.dj, sizeof(float) * n * r_u * d_z));
+    CU(cudaMemcpy(t.dj, j_r, sizeof(float) * n * r_u * d_z, cudaMemcpyHostToDevice));
+  }
+  int64_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    t.woff.push_back(off);
+    off += (int64_t)h->w[l + 1] * h->w[l];
+    t.boff.push_back(off);
+    off += h->w[l + 1];
+  }
+  t.count = off;
+  for (double** q : {&t.P, &t.G, &t.M, &t.V}) TRY(tr_alloc(h, (void**)q, sizeof(double) * off));
+  TRY(tr_alloc(h, (void**)&t.P32, sizeof(float) * off));
+  TRY(tr_alloc(h, (void**)&t.scale, sizeof(float) * r_m));
+  TRY(tr_alloc(h, (void**)&t.mu, sizeof(float) * r_u));
+  TRY(tr_alloc(h, (void**)&t.sig, sizeof(float) * r_u));
+  TRY(tr_alloc(h, (void**)&t.idx, sizeof(int) * B));
+  const int mw = std::max(h->maxw, n0);
+  TRY(tr_alloc(h, (void**)&t.Y, sizeof(float) * B * r_u));
+  TRY(tr_alloc(h, (void**)&t.Jt, sizeof(float) * B * d_z * r_u));
+  for (float** q : {&t.GA, &t.GS, &t.GA2}) TRY(tr_alloc(h, (void**)q, sizeof(float) * B * mw));
+  for (float** q : {&t.GT, &t.GU, &t.GT2}) TRY(tr_alloc(h, (void**)q, sizeof(float) * B * d_z * mw));
+  t.A.assign(L + 1, nullptr);
+  t.T.assign(L + 1, nullptr);
+  t.S.assign(L, nullptr);
+  t.U.assign(L, nullptr);
+  for (int l = 0; l <= L; ++l) {
+    TRY(tr_alloc(h, (void**)&t.A[l], sizeof(float) * B * h->w[l]));
+    TRY(tr_alloc(h, (void**)&t.T[l], sizeof(float) * B * d_z * h->w[l]));
+  }
+  for (int l = 0; l < L; ++l) {
+    TRY(tr_alloc(h, (void**)&t.S[l], sizeof(float) * B * h->w[l + 1]));
+    TRY(tr_alloc(h, (void**)&t.U[l], sizeof(float) * B * d_z * h->w[l + 1]));
+  }
+  TRY(tr_alloc(h, (void**)&t.part, sizeof(double) * 2 * 64));
+  if (!t.hloss) CU(cudaHostAlloc((void**)&t.hloss, sizeof(double) * 2, 0));
+  t.ready = true;
+  return SDN_OK;
+}
+
+// parameters in the reference layout (W_l: n_out x n_in incl. the full first
+// layer [m | z] columns), fp64; resets the Adam state
+int sdn_train_set_params(sdn_handle* h, const double* const* W, const double* const* b, const double* in_scale,
+                         const double* out_mean, const double* out_std) {
+  if (!h || !W || !b || !in_scale || !out_mean || !out_std) return fail(SDN_ERR_ARG, "null argument");
+  auto& t = h->tr;
+  if (!t.ready) return fail(SDN_ERR_STATE, "sdn_train_setup first");
+  CU(cudaSetDevice(h->device));
+  std::vector<double> P(t.count);
+  for (int l = 0; l < h->L; ++l) {
+    std::memcpy(&P[t.woff[l]], W[l], sizeof(double) * h->w[l + 1] * h->w[l]);
+    std::memcpy(&P[t.boff[l]], b[l], sizeof(double) * h->w[l + 1]);
+  }
+  CU(cudaMemcpy(t.P, P.data(), sizeof(double) * t.count, cudaMemcpyHostToDevice));
+  CU(cudaMemset(t.M, 0, sizeof(double) * t.count));
+  CU(cudaMemset(t.V, 0, sizeof(double) * t.count));
+  k_tr_f64_to_f32<<<256, 256, 0, h->stream>>>(t.count, t.P, t.P32);
+  std::vector<float> f(std::max(h->r_m, h->r_u));
+  for (int j = 0; j < h->r_m; ++j) f[j] = (float)in_scale[j];
+  CU(cudaMemcpy(t.scale, f.data(), sizeof(float) * h->r_m, cudaMemcpyHostToDevice));
+  for (int j = 0; j < h->r_u; ++j) f[j] = (float)out_mean[j];
+  CU(cudaMemcpy(t.mu, f.data(), sizeof(float) * h->r_u, cudaMemcpyHostToDevice));
+  for (int j = 0; j < h->r_u; ++j) f[j] = (float)out_std[j];
+  CU(cudaMemcpy(t.sig, f.data(), sizeof(float) * h->r_u, cudaMemcpyHostToDevice));
+  CU(cudaStreamSynchronize(h->stream));
+  return SDN_OK;
+}
+
+// per-parameter update mask (same layout as the parameters; 0 freezes an entry)
+int sdn_train_set_mask(sdn_handle* h, const double* const* mW, const double* const* mb) {
+  if (!h || !mW || !mb) return fail(SDN_ERR_ARG, "null argument");
+  auto& t = h->tr;
+  if (!t.ready) return fail(SDN_ERR_STATE, "sdn_train_setup first");
+  CU(cudaSetDevice(h->device));
+  if (!t.mask) TRY(tr_alloc(h, (void**)&t.mask, sizeof(double) * t.count));
+  std::vector<double> m(t.count);
+  for (int l = 0; l < h->L; ++l) {
+    std::memcpy(&m[t.woff[l]], mW[l], sizeof(double) * h->w[l + 1] * h->w[l]);
+    std::memcpy(&m[t.boff[l]], mb[l], sizeof(double) * h->w[l + 1]);
+  }
+  CU(cudaMemcpy(t.mask, m.data(), sizeof(double) * t.count, cudaMemcpyHostToDevice));
+  return SDN_OK;
+}
+
+int sdn_train_get_params(sdn_handle* h, double* const* W, double* const* b) {
+  if (!h || !W || !b) return fail(SDN_ERR_ARG, "null argument");
+  auto& t = h->tr;
+  if (!t.ready) return fail(SDN_ERR_STATE, "sdn_train_setup first");
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  std::vector<double> P(t.count);
+  CU(cudaMemcpy(P.data(), t.P, sizeof(double) * t.count, cudaMemcpyDeviceToHost));
+  for (int l = 0; l < h->L; ++l) {
+    std::memcpy(W[l], &P[t.woff[l]], sizeof(double) * h->w[l + 1] * h->w[l]);
+    std::memcpy(b[l], &P[t.boff[l]], sizeof(double) * h->w[l + 1]);
+  }
+  return SDN_OK;
+}
+
+// gradient of the last sdn_train_step (fp64, reference layout)
+int sdn_train_get_grad(sdn_handle* h, double* const* gW, double* const* gb) {
+  if (!h || !gW || !gb) return fail(SDN_ERR_ARG, "null argument");
+  auto& t = h->tr;
+  if (!t.ready) return fail(SDN_ERR_STATE, "sdn_train_setup first");
+  CU(cudaSetDevice(h->device));
+  CU(cudaStreamSynchronize(h->stream));
+  std::vector<double> G(t.count);
+  CU(cudaMemcpy(G.data(), t.G, sizeof(double) * t.count, cudaMemcpyDeviceToHost));
+  for (int l = 0; l < h->L; ++l) {
+    std::memcpy(gW[l], &G[t.woff[l]], sizeof(double) * h->w[l + 1] * h->w[l]);
+    std::memcpy(gb[l], &G[t.boff[l]], sizeof(double) * h->w[l + 1]);
+  }
+  return SDN_OK;
+}
+
+// one loss_and_grad over the batch idx (B records) and, when lr > 0, one Adam
+// step (step = 1-based update count for the bias corrections); *loss = the
+// batch loss (surrogate.py:263-335, 382-403)
+int sdn_train_step(sdn_handle* h, const int64_t* idx, int32_t B, double lam, double lr, int64_t step,
+                   double* loss) {
+  if (!h || !idx || !loss || B < 1) return fail(SDN_ERR_ARG, "bad argument");
+  auto& t = h->tr;
+  if (!t.ready) return fail(SDN_ERR_STATE, "sdn_train_setup first");
+  if (B > t.bcap) return fail(SDN_ERR_ARG, "batch exceeds the setup capacity");
+  if (lam > 0.0 && !t.dj) return fail(SDN_ERR_ARG, "jacobian_weight > 0 requires Jacobian data");
+  CU(cudaSetDevice(h->device));
+  const int L = h->L, d_z = h->d_z, r_u = h->r_u;
+  const bool tan = lam > 0.0;
+  const int64_t BT = (int64_t)B * d_z;
+  std::vector<int> ih(B);
+  for (int b = 0; b < B; ++b) {
+    if (idx[b] < 0 || idx[b] >= t.n) return fail(SDN_ERR_ARG, "record index out of range");
+    ih[b] = (int)idx[b];
+  }
+  CU(cudaMemcpyAsync(t.idx, ih.data(), sizeof(int) * B, cudaMemcpyHostToDevice, h->stream));
+  k_tr_gather<<<B, 128, 0, h->stream>>>(B, t.idx, t.dm, t.dz, t.du, t.dj, h->r_m, d_z, r_u, t.scale, t.mu, t.sig,
+                                        t.A[0], t.Y, tan ? t.Jt : nullptr, tan ? t.T[0] : nullptr);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  // forward with tangents
+  for (int l = 0; l < L; ++l) {
+    const int n_in = h->w[l], n_out = h->w[l + 1];
+    const float* W = t.P32 + t.woff[l];
+    const float* bb = t.P32 + t.boff[l];
+    const bool last = l == L - 1;
+    float* Sout = last ? t.A[L] : t.S[l];
+    float* Uout = last ? t.T[L] : t.U[l];
+    TRY((gemm<false, true>(h, B, nullptr, n_out, n_in, t.A[l], n_in, W, n_in,
+                           EpiAffine{bb, nullptr, nullptr, Sout, (int64_t)n_out}, nullptr, nullptr, 0)));
+    if (tan)
+      TRY((gemm<false, true>(h, BT, nullptr, n_out, n_in, t.T[l], n_in, W, n_in, EpiStore{Uout, (int64_t)n_out},
+                             nullptr, nullptr, 0)));
+    if (!last) {
+      k_tr_act<<<B, 128, 0, h->stream>>>(B, d_z, n_out, h->act, t.S[l], tan ? t.U[l] : nullptr, t.A[l + 1],
+                                         tan ? t.T[l + 1] : nullptr);
+      h->launches++;
+    }
+  }
+  // loss and output seeds
+  const int lg = 32;
+  k_tr_loss<<<lg, 256, 0, h->stream>>>(B, d_z, r_u, lam, t.A[L], t.Y, tan ? t.T[L] : nullptr, t.Jt, t.GA, t.GT,
+                                       t.part);
+  k_sum_rows<<<1, 256, 0, h->stream>>>(lg, 2, t.part, t.part + 2 * lg);
+  h->launches += 2;
+  CHECK_LAUNCH(h);
+  // reverse: GA/GT hold dLoss/d(layer outputs); gradients into G (fp64)
+  CU(cudaMemsetAsync(t.G, 0, sizeof(double) * t.count, h->stream));
+  float *GA = t.GA, *GT = t.GT, *GAn = t.GA2, *GTn = t.GT2;
+  for (int l = L - 1; l >= 0; --l) {
+    const int n_in = h->w[l], n_out = h->w[l + 1];
+    const float* W = t.P32 + t.woff[l];
+    const float *GS, *GU;
+    if (l == L - 1) {
+      GS = GA;
+      GU = GT;
+    } else {
+      k_tr_bwd<<<B, 128, 0, h->stream>>>(B, d_z, n_out, h->act, t.S[l], tan ? t.U[l] : nullptr, GA,
+                                         tan ? GT : nullptr, t.GS, t.GU);
+      h->launches++;
+      GS = t.GS;
+      GU = t.GU;
+    }
+    // gW = GS^T A_l (+ GU^T T_l), gb = colsum(GS)
+    TRY((gemm<true, false>(h, n_out, nullptr, n_in, B, GS, n_out, t.A[l], n_in,
+                           EpiAccum64{t.G + t.woff[l], (int64_t)n_in}, nullptr, nullptr, 0)));
+    if (tan)
+      TRY((gemm<true, false>(h, n_out, nullptr, n_in, (int)BT, GU, n_out, t.T[l], n_in,
+                             EpiAccum64{t.G + t.woff[l], (int64_t)n_in}, nullptr, nullptr, 0)));
+    k_tr_colsum<<<(unsigned)cdiv(n_out, 128), 128, 0, h->stream>>>(B, n_out, GS, t.G + t.boff[l]);
+    h->launches++;
+    if (l > 0) {                                 // GA = GS W, GT = GU W
+      TRY((gemm<false, false>(h, B, nullptr, n_in, n_out, GS, n_out, W, n_in, EpiStore{GAn, (int64_t)n_in},
+                              nullptr, nullptr, 0)));
+      if (tan)
+        TRY((gemm<false, false>(h, BT, nullptr, n_in, n_out, GU, n_out, W, n_in, EpiStore{GTn, (int64_t)n_in},
+                                nullptr, nullptr, 0)));
+      std::swap(GA, GAn);
+      std::swap(GT, GTn);
+    }
+  }
+  CHECK_LAUNCH(h);
+  CU(cudaMemcpyAsync(t.hloss, t.part + 2 * lg, sizeof(double) * 2, cudaMemcpyDeviceToHost, h->stream));
+  if (lr > 0.0) {
+    const double b1 = 0.9, b2 = 0.999;
+    const double c1 = 1.0 - std::pow(b1, (double)step), c2 = 1.0 - std::pow(b2, (double)step);
+    k_tr_adam<<<(unsigned)std::min<int64_t>(cdiv(t.count, 256), 4 * h->num_sms), 256, 0, h->stream>>>(
+        t.count, t.P, t.G, t.M, t.V, t.P32, lr, b1, b2, 1e-8, c1, c2, t.mask);
+    h->launches++;
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  *loss = (t.hloss[0] + lam * t.hloss[1]) / (double)B;
+  return SDN_OK;
+}
+
+}  // extern "C"

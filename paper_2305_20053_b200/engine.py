@@ -21,6 +21,19 @@ def _f32(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
 
 
+def _p4(x: int) -> int:
+    return (int(x) + 3) // 4 * 4
+
+
+def _padcols(a, width: int, fill=0.0):
+    a = np.asarray(a)
+    if a.shape[-1] == width:
+        return a
+    out = np.full(a.shape[:-1] + (width,), fill, dtype=a.dtype)
+    out[..., :a.shape[-1]] = a
+    return out
+
+
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
@@ -53,9 +66,20 @@ class Engine:
         self.r_u = w[-1]
         self.device = int(device)
         self.max_samples = int(max_samples)
-        self._widths_c = (C.c_int32 * len(w))(*w)
+        # the device kernels want r_m and every layer width in multiples of 4:
+        # other widths run zero-padded (zero weights into and out of the extra
+        # units, zero output scale), which leaves every real output unchanged
+        self.activation = model.activation
+        self.r_m4 = _p4(self.r_m)
+        self.pw = [self.r_m4 + (w[0] - self.r_m)] + [_p4(x) for x in w[1:]]
+        self.padded = self.pw != w or self.r_m4 != self.r_m
+        if bool(model.residual) and any(w[l] != w[l + 1] and self.pw[l] == self.pw[l + 1]
+                                        for l in range(1, len(w) - 2)):
+            raise ValueError("residual blocks between unequal widths that pad to the same size are not supported")
+        self.r_u4 = self.pw[-1]
+        self._widths_c = (C.c_int32 * len(w))(*self.pw)
         self._multi_cache = {}
-        cfg = _lib.Config(n_layers=len(model.weights), widths=self._widths_c, r_m=self.r_m, d_z=self.d_z,
+        cfg = _lib.Config(n_layers=len(model.weights), widths=self._widths_c, r_m=self.r_m4, d_z=self.d_z,
                           activation=_lib.ACT[model.activation], residual=int(bool(model.residual)),
                           gemm=_lib.GEMM[gemm], device=self.device, max_samples=self.max_samples)
         h = C.c_void_p()
@@ -88,23 +112,65 @@ class Engine:
         check(lib.sdn_set_stream(self.h, C.c_void_p(stream_handle)), "sdn_set_stream")
 
     # -- setup -------------------------------------------------------------------
+    def padded_params(self, model):
+        """The model's (weights, biases, input_scale, output_mean, output_std)
+        in the device's padded widths (float64; identity when unpadded)."""
+        Ws, bs = [np.asarray(W, float) for W in model.weights], [np.asarray(b, float) for b in model.biases]
+        scale = np.asarray(model.input_scale, float)
+        mean, std = np.asarray(model.output_mean, float), np.asarray(model.output_std, float)
+        if not self.padded:
+            return Ws, bs, scale, mean, std
+        pw, L = self.pw, len(Ws)
+        Wp, bp = [], []
+        for l in range(L):
+            W = np.zeros((pw[l + 1], pw[l]))
+            if l == 0:                                   # [m (r_m -> r_m4) | z] columns
+                W[:Ws[0].shape[0], :self.r_m] = Ws[0][:, :self.r_m]
+                W[:Ws[0].shape[0], self.r_m4:] = Ws[0][:, self.r_m:]
+            else:
+                W[:Ws[l].shape[0], :Ws[l].shape[1]] = Ws[l]
+            b = np.zeros(pw[l + 1])
+            if self.activation == "softmax" and l < L - 1:
+                b[:] = -np.inf                           # padded units take no softmax mass
+            b[:bs[l].size] = bs[l]
+            Wp.append(W)
+            bp.append(b)
+        return (Wp, bp, _padcols(scale, self.r_m4, 1.0), _padcols(mean, self.r_u4), _padcols(std, self.r_u4))
+
     def set_model(self, model):
-        Ws = [_f32(W) for W in model.weights]
-        bs = [_f32(b) for b in model.biases]
+        Wd, bd, scale, mean, std = self.padded_params(model)
+        Ws = [_f32(W) for W in Wd]
+        bs = [_f32(b) for b in bd]
         self._keep = (Ws, bs)
         Wp = (_lib._F * len(Ws))(*[fptr(W) for W in Ws])
         bp = (_lib._F * len(bs))(*[fptr(b) for b in bs])
         Vz = getattr(model, "Vz", None)
         vz = _f32(Vz) if Vz is not None else None
-        check(lib.sdn_set_model(self.h, Wp, bp, fptr(_f32(model.input_scale)), fptr(_f32(model.output_mean)),
-                                fptr(_f32(model.output_std)), fptr(vz) if vz is not None else None),
-              "sdn_set_model")
+        check(lib.sdn_set_model(self.h, Wp, bp, fptr(_f32(scale)), fptr(_f32(mean)), fptr(_f32(std)),
+                                fptr(vz) if vz is not None else None), "sdn_set_model")
+
+    def unpad_params(self, Wp, bp):
+        """Inverse of padded_params for (weights, biases) lists."""
+        if not self.padded:
+            return Wp, bp
+        w, L = self.widths, len(Wp)
+        Ws, bs = [], []
+        for l in range(L):
+            W = Wp[l][:w[l + 1]]
+            if l == 0:
+                W = np.concatenate([W[:, :self.r_m], W[:, self.r_m4:]], axis=1)
+            else:
+                W = W[:, :w[l]]
+            Ws.append(np.ascontiguousarray(W))
+            bs.append(np.ascontiguousarray(bp[l][:w[l + 1]]))
+        return Ws, bs
 
     def set_tracking(self, c, q0: float):
-        check(lib.sdn_set_tracking(self.h, fptr(_f32(c)), float(q0)), "sdn_set_tracking")
+        check(lib.sdn_set_tracking(self.h, fptr(_f32(_padcols(np.asarray(c, float), self.r_u4))), float(q0)),
+              "sdn_set_tracking")
 
     def set_decoder(self, U, ubias, Mdiag, u_target):
-        U = _f32(U)
+        U = _f32(_padcols(np.asarray(U, np.float32), self.r_u4))
         self.d_u = U.shape[0]
         check(lib.sdn_set_decoder(self.h, U.shape[0], fptr(U), fptr(_f32(ubias)), fptr(_f32(Mdiag)),
                                   fptr(_f32(u_target))), "sdn_set_decoder")
@@ -113,12 +179,16 @@ class Engine:
         """m_r: (n, r_m) numpy array, or a torch CUDA tensor on this device."""
         if hasattr(m_r, "data_ptr") and getattr(m_r, "is_cuda", False):
             t = m_r.contiguous().float()
+            if t.shape[1] != self.r_m4:
+                import torch.nn.functional as F
+                t = F.pad(t, (0, self.r_m4 - t.shape[1])).contiguous()
             n = t.shape[0]
             check(lib.sdn_set_samples(self.h, C.c_void_p(t.data_ptr()), n, int(global_offset), 1), "sdn_set_samples")
         else:
             a = _f32(m_r)
             if a.ndim != 2 or a.shape[1] != self.r_m:
                 raise ValueError("samples must be (n, r_m)")
+            a = _f32(_padcols(a, self.r_m4))
             n = a.shape[0]
             check(lib.sdn_set_samples(self.h, a.ctypes.data_as(C.c_void_p), n, int(global_offset), 0),
                   "sdn_set_samples")
@@ -127,7 +197,8 @@ class Engine:
 
     def encode_fields(self, m, Vm, Mdiag, m_mean: float, global_offset: int = 0):
         a = _f32(m)
-        check(lib.sdn_encode_fields(self.h, a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1], fptr(_f32(Vm)),
+        Vm = _f32(_padcols(np.asarray(Vm, np.float32), self.r_m4))
+        check(lib.sdn_encode_fields(self.h, a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1], fptr(Vm),
                                     fptr(_f32(Mdiag)), float(m_mean), int(global_offset), 0), "sdn_encode_fields")
         self.n = a.shape[0]
         self.global_offset = int(global_offset)
@@ -176,25 +247,27 @@ class Engine:
         if m_r.shape[1] != self.r_m or z.shape[1] != self.d_z:
             raise ValueError("input widths do not match the network spec")
         z = _f32(np.broadcast_to(z, (m_r.shape[0], self.d_z)))
-        phi = np.empty((m_r.shape[0], self.r_u), np.float32)
+        m_r = _f32(_padcols(m_r, self.r_m4))
+        phi = np.empty((m_r.shape[0], self.r_u4), np.float32)
         check(lib.sdn_forward_batch(self.h, fptr(m_r), fptr(z), m_r.shape[0], fptr(phi)), "sdn_forward_batch")
-        return phi
+        return phi[:, :self.r_u] if self.r_u4 != self.r_u else phi
 
     def jacobian_batch(self, m_r, z, decoded: bool = False) -> np.ndarray:
         m_r = np.atleast_2d(_f32(m_r))
         z = _f32(np.broadcast_to(np.atleast_2d(_f32(z)), (m_r.shape[0], self.d_z)))
         if m_r.shape[1] != self.r_m:
             raise ValueError("input widths do not match the network spec")
-        outw = self.d_u if decoded else self.r_u
+        outw = self.d_u if decoded else self.r_u4
         if decoded and self.d_u is None:
             raise RuntimeError("set_decoder first")
+        m_r = _f32(_padcols(m_r, self.r_m4))
         J = np.empty((m_r.shape[0], outw, self.d_z), np.float32)
         check(lib.sdn_jacobian_batch(self.h, fptr(m_r), fptr(z), m_r.shape[0], int(decoded), fptr(J)),
               "sdn_jacobian_batch")
-        return J
+        return J if decoded or self.r_u4 == self.r_u else np.ascontiguousarray(J[:, :self.r_u, :])
 
     def lift(self, phi) -> np.ndarray:
-        phi = np.atleast_2d(_f32(phi))
+        phi = np.atleast_2d(_f32(_padcols(np.atleast_2d(np.asarray(phi, np.float32)), self.r_u4)))
         u = np.empty((phi.shape[0], self.d_u), np.float32)
         check(lib.sdn_lift(self.h, fptr(phi), phi.shape[0], fptr(u)), "sdn_lift")
         return u

@@ -341,3 +341,40 @@ def test_softmax_network_forward_jacobian_and_risks(residual):
         assert _rel(r.grad_z, o[1]) <= RTOL
         if kind == "cvar_exact":
             np.testing.assert_array_equal(np.sort(r.idx), np.sort(ref.cvar_select(Qo, beta)))
+
+
+@pytest.mark.parametrize("act", ["tanh", "softplus", "softmax"])
+def test_odd_widths_run_zero_padded(act, golden):
+    """The reference's own small test networks (odd widths, e.g. 3 -> 8, 6 ->
+    5): the engine pads to multiples of 4 with inert units; forward,
+    z-Jacobian and risk gradients match the oracle, and the reference's golden
+    forward outputs."""
+    from paper_2305_20053_b200.api import NetworkSpec, SurrogateModel
+    if act != "softmax":
+        p = f"net_{act}_"
+        spec = NetworkSpec(r_m=3, d_z=4, r_u=5, hidden=(8, 6), activation=act)
+        model = SurrogateModel(spec=spec, weights=[golden[p + f"W{l}"] for l in range(3)],
+                               biases=[golden[p + f"b{l}"] for l in range(3)], input_scale=golden[p + "in_scale"],
+                               output_mean=golden[p + "out_mean"], output_std=golden[p + "out_std"])
+        assert _rel(model.forward_batch(golden[p + "m_r"], golden[p + "Z"]), golden[p + "phi"]) <= 1e-5
+        assert _rel(model.z_jacobian_batch(golden[p + "m_r"], golden[p + "Z"]), golden[p + "jac"]) <= 1e-5
+    g = np.random.default_rng(2)
+    from paper_2305_20053_b200.api import init_model
+    spec = NetworkSpec(r_m=7, d_z=3, r_u=5, hidden=(10, 9), activation=act)
+    model = init_model(spec, seed=1, input_scale=g.uniform(0.5, 2, 7), output_mean=g.normal(size=5),
+                       output_std=g.uniform(0.5, 2, 5))
+    n = 301
+    m_r = g.normal(size=(n, 7)).astype(np.float32)
+    z = g.uniform(-1, 1, 3)
+    c = g.normal(size=5).astype(np.float32)
+    eng = Engine(model, max_samples=n)
+    assert eng.padded
+    eng.set_tracking(c, 0.25)
+    eng.set_samples(m_r)
+    form = ref.ReducedForm(c.astype(np.float64), 0.25)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(model), m_r, z, form=form)
+    for kind, beta in (("meanvar", 0.5), ("cvar_exact", 0.9)):
+        r = eng.eval(z, kind, beta=beta)
+        o = ref.saa_objective(Qo, Go, z, ref.Risk(kind, beta=beta))
+        assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+        assert _rel(r.grad_z, o[1]) <= RTOL
