@@ -378,3 +378,25 @@ def test_odd_widths_run_zero_padded(act, golden):
         o = ref.saa_objective(Qo, Go, z, ref.Risk(kind, beta=beta))
         assert abs(r.value - o[0]) <= RTOL * abs(o[0])
         assert _rel(r.grad_z, o[1]) <= RTOL
+
+
+@pytest.mark.parametrize("gemm", ["simt", "tc"])
+def test_decoded_frame_cvar_risks(gemm):
+    """Full-frame QoI (riskopt.py:103-108, Gram form on the device) with both
+    CVaR risks: the fp64 refinement evaluates the decoded QoI with the fp64
+    Gram matrix; exact selection and smoothed weights vs the oracle."""
+    p = _problem("c1", 1024, with_decoder=True, seed=3)
+    eng = _engine(p, gemm)
+    eng.set_decoder(p.U, p.ubias, p.Mdiag_u, p.u_target)
+    dec = (p.U, p.ubias, p.Mdiag_u, p.u_target)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, "decoded", decoded=dec)
+    r = eng.eval(p.z, "cvar_exact", beta=0.95, qoi="decoded")
+    sel = ref.cvar_select(Qo, 0.95)
+    np.testing.assert_array_equal(np.sort(r.idx), np.sort(sel))
+    assert abs(r.value - Qo[sel].mean()) <= RTOL * abs(Qo[sel].mean())
+    assert _rel(r.grad_z, Go[sel].mean(0)) <= RTOL
+    t = ref.mc_var(Qo, 0.9)
+    r = eng.eval(p.z, "cvar", beta=0.9, eps=1e-3, t=t, qoi="decoded")
+    o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar", beta=0.9, eps=1e-3), t)
+    assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+    assert _rel(r.grad_z, o[1]) <= RTOL
