@@ -2065,15 +2065,17 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   // modes 3..6 drop parts of the fused epilogue: 3 no D, 4 no split, 5 no
   // residual input, 6 only the fp32 H store
   const bool keepD = mode < 3 || (mode != 3 && mode < 6), keepS = mode < 4 || (mode != 4 && mode < 6);
-  const bool keepP = mode < 5, keepH = mode != 7 && mode != 8 && mode != 9;
+  const bool keepP = mode < 5, keepH = mode != 7 && mode < 8;
   // mode 8: the production tensor-core chain epilogue (no fp32 H, residual
   // read from the input's bf16 split, D + split outputs)
-  // mode 9: the chain epilogue with the identity activation (arithmetic share of ELU)
-  const bool chainm = mode == 8 || mode == 9;
+  // mode 9: the chain epilogue with the identity activation (arithmetic share of ELU);
+  // 10 / 11 / 12: the chain epilogue without the act' store / the split store / the residual input
+  const bool chainm = mode == 8 || mode >= 9;
   EpiFwdHidden e{h->b[1], (h->res[1] && keepP && !chainm) ? h->H[0] : nullptr, keepH ? h->H[1] : nullptr,
-                 (keepD || chainm) ? h->D[1] : nullptr, (int64_t)N, mode == 9 ? (int)ACT_IDENTITY : h->act};
-  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{(keepS || chainm) ? &h->tcw.act[1] : nullptr},
-                           TcEpiSplit{(chainm && h->res[1]) ? &h->tcw.act[0] : nullptr}};
+                 ((keepD || chainm) && mode != 10) ? h->D[1] : nullptr, (int64_t)N,
+                 mode == 9 ? (int)ACT_IDENTITY : h->act};
+  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{((keepS || chainm) && mode != 11) ? &h->tcw.act[1] : nullptr},
+                           TcEpiSplit{(chainm && h->res[1] && mode != 12) ? &h->tcw.act[0] : nullptr}};
   h->tcw.act[0].rows = M;
   int rc = 0;
   for (int it = 0; it <= reps && rc == 0; ++it) {
