@@ -231,6 +231,8 @@ struct sdn_handle {
     int* idx = nullptr;
     float *Y = nullptr, *Jt = nullptr, *GA = nullptr, *GT = nullptr, *GS = nullptr, *GU = nullptr;
     float *GA2 = nullptr, *GT2 = nullptr;
+    float *GSt = nullptr, *GUt = nullptr, *zpart = nullptr;   // split-K weight-gradient scratch
+    int zmax = 8;
     std::vector<float*> A, S, T, U;  // per layer (A[0] = X, T[0] = tangent seed)
     double* part = nullptr;
     double* hloss = nullptr;           // pinned
@@ -2120,6 +2122,32 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
 // H1 training (reference surrogate.py:263-405), SIMT
 // chains with fp64 gradients and fp64 master parameters (train.cuh)
 
+// G64 (n_out x n_in) += X^T Y, X: K x n_out, Y: K x n_in (row-major), K large:
+// transpose X to n_out x K, split K over gridDim.z so the small output fills
+// the GPU, reduce the fp32 partials in a fixed order into fp64
+static int tr_wgrad(sdn_handle* h, int n_out, int n_in, int64_t K, const float* X, const float* Y, double* G64) {
+  auto& t = h->tr;
+  float* Xt = K <= t.bcap ? t.GSt : t.GUt;
+  k_tr_transpose<<<dim3((unsigned)cdiv(n_out, 32), (unsigned)cdiv(K, 32)), dim3(32, 8), 0, h->stream>>>(K, n_out, X, Xt);
+  const int64_t tiles = cdiv(n_out, 64) * cdiv(n_in, 64);
+  int Z = (int)std::min<int64_t>({(int64_t)t.zmax, std::max<int64_t>(1, cdiv(2 * h->num_sms, tiles)),
+                                  std::max<int64_t>(1, K / 128)});
+  const bool vec = (K % 4 == 0) && (n_in % 4 == 0);
+  dim3 grid((unsigned)cdiv(n_out, 64), (unsigned)cdiv(n_in, 64), (unsigned)Z);
+  EpiStoreZ e{t.zpart, (int64_t)n_in, (int64_t)n_out * n_in};
+  if (vec)
+    gemm_simt_kernel<64, 64, 16, 4, 4, false, false, true, EpiStoreZ><<<grid, 256, 0, h->stream>>>(
+        n_out, nullptr, n_in, (int)K, Xt, K, Y, n_in, e);
+  else
+    gemm_simt_kernel<64, 64, 16, 4, 4, false, false, false, EpiStoreZ><<<grid, 256, 0, h->stream>>>(
+        n_out, nullptr, n_in, (int)K, Xt, K, Y, n_in, e);
+  k_tr_sum_z<<<(unsigned)std::min<int64_t>(cdiv((int64_t)n_out * n_in, 256), 4 * h->num_sms), 256, 0, h->stream>>>(
+      (int64_t)n_out * n_in, Z, t.zpart, G64);
+  h->launches += 3;
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
 static int tr_alloc(sdn_handle* h, void** p, size_t bytes) {
   CU(cudaMalloc(p, std::max<size_t>(bytes, 16)));
   h->tr.allocs.push_back(*p);
@@ -2170,6 +2198,9 @@ int sdn_train_setup(sdn_handle* h, const float* m_r, const float* z, const float
   TRY(tr_alloc(h, (void**)&t.Jt, sizeof(float) * B * d_z * r_u));
   for (float** q : {&t.GA, &t.GS, &t.GA2}) TRY(tr_alloc(h, (void**)q, sizeof(float) * B * mw));
   for (float** q : {&t.GT, &t.GU, &t.GT2}) TRY(tr_alloc(h, (void**)q, sizeof(float) * B * d_z * mw));
+  TRY(tr_alloc(h, (void**)&t.GSt, sizeof(float) * B * mw));
+  TRY(tr_alloc(h, (void**)&t.GUt, sizeof(float) * B * d_z * mw));
+  TRY(tr_alloc(h, (void**)&t.zpart, sizeof(float) * t.zmax * mw * mw));
   t.A.assign(L + 1, nullptr);
   t.T.assign(L + 1, nullptr);
   t.S.assign(L, nullptr);
@@ -2301,7 +2332,8 @@ int sdn_train_step(sdn_handle* h, const int64_t* idx, int32_t B, double lam, dou
       TRY((gemm<false, true>(h, BT, nullptr, n_out, n_in, t.T[l], n_in, W, n_in, EpiStore{Uout, (int64_t)n_out},
                              nullptr, nullptr, 0)));
     if (!last) {
-      k_tr_act<<<B, 128, 0, h->stream>>>(B, d_z, n_out, h->act, t.S[l], tan ? t.U[l] : nullptr, t.A[l + 1],
+      k_tr_act<<<dim3(B, (unsigned)cdiv(n_out, 128)), 128, 0, h->stream>>>(B, d_z, n_out, h->act, t.S[l],
+                                                                         tan ? t.U[l] : nullptr, t.A[l + 1],
                                          tan ? t.T[l + 1] : nullptr);
       h->launches++;
     }
@@ -2324,18 +2356,17 @@ int sdn_train_step(sdn_handle* h, const int64_t* idx, int32_t B, double lam, dou
       GS = GA;
       GU = GT;
     } else {
-      k_tr_bwd<<<B, 128, 0, h->stream>>>(B, d_z, n_out, h->act, t.S[l], tan ? t.U[l] : nullptr, GA,
+      k_tr_bwd<<<dim3(B, (unsigned)cdiv(n_out, 128)), 128, 0, h->stream>>>(B, d_z, n_out, h->act, t.S[l],
+                                                                         tan ? t.U[l] : nullptr, GA,
                                          tan ? GT : nullptr, t.GS, t.GU);
       h->launches++;
       GS = t.GS;
       GU = t.GU;
     }
-    // gW = GS^T A_l (+ GU^T T_l), gb = colsum(GS)
-    TRY((gemm<true, false>(h, n_out, nullptr, n_in, B, GS, n_out, t.A[l], n_in,
-                           EpiAccum64{t.G + t.woff[l], (int64_t)n_in}, nullptr, nullptr, 0)));
-    if (tan)
-      TRY((gemm<true, false>(h, n_out, nullptr, n_in, (int)BT, GU, n_out, t.T[l], n_in,
-                             EpiAccum64{t.G + t.woff[l], (int64_t)n_in}, nullptr, nullptr, 0)));
+    // gW = GS^T A_l (+ GU^T T_l): K-contiguous transposes, split-K SIMT GEMMs
+    // into fp32 partials, fixed-order fp64 reduction; gb = colsum(GS)
+    TRY(tr_wgrad(h, n_out, n_in, B, GS, t.A[l], t.G + t.woff[l]));
+    if (tan) TRY(tr_wgrad(h, n_out, n_in, BT, GU, t.T[l], t.G + t.woff[l]));
     k_tr_colsum<<<(unsigned)cdiv(n_out, 128), 128, 0, h->stream>>>(B, n_out, GS, t.G + t.boff[l]);
     h->launches++;
     if (l > 0) {                                 // GA = GS W, GT = GU W

@@ -44,7 +44,15 @@ gemm_simt_kernel(int64_t M, const int* __restrict__ Mdev, int N, int K, const fl
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
 
-  for (int k0 = 0; k0 < K; k0 += BK) {
+  // split-K over gridDim.z (default 1): this block's K range [kb, K) in
+  // BK-aligned slices; the epilogue writes one partial per z (EpiStoreZ)
+  int kb = 0;
+  if (gridDim.z > 1) {
+    const int kz = ((K + (int)gridDim.z - 1) / (int)gridDim.z + BK - 1) / BK * BK;
+    kb = (int)blockIdx.z * kz;
+    K = min(K, kb + kz);
+  }
+  for (int k0 = kb; k0 < K; k0 += BK) {
     // ---- A tile -> As[k][m]
     if (!AT) {
       if (VEC) {
@@ -149,6 +157,17 @@ struct EpiStore {
     else { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
   }
   SDN_DEV void col(int64_t r, int c, float v) const { C[r * ldc + c] = v; }
+};
+
+// split-K partial store: C + blockIdx.z * zstride (reduced by k_sum_z)
+struct EpiStoreZ {
+  float* C; int64_t ldc; int64_t zstride;
+  SDN_DEV void operator()(int64_t r, int c, float4 v) const {
+    float* p = C + blockIdx.z * zstride + r * ldc + c;
+    if ((ldc & 3) == 0) *reinterpret_cast<float4*>(p) = v;
+    else { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
+  }
+  SDN_DEV void col(int64_t r, int c, float v) const { C[blockIdx.z * zstride + r * ldc + c] = v; }
 };
 
 // fp64 accumulate (split-K setup GEMMs): C64[r, c] += acc

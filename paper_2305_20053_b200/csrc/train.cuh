@@ -68,7 +68,7 @@ __global__ void k_tr_act(int B, int d_z, int n, int act, const float* __restrict
                          float* __restrict__ A, float* __restrict__ T) {
   const int b = blockIdx.x;
   if (b >= B) return;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < n; c += gridDim.y * blockDim.x) {
     float a, d;
     act_eval(act, S[(int64_t)b * n + c], a, d);
     A[(int64_t)b * n + c] = a;
@@ -117,7 +117,7 @@ __global__ void k_tr_bwd(int B, int d_z, int n, int act, const float* __restrict
                          float* __restrict__ GU) {
   const int b = blockIdx.x;
   if (b >= B) return;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < n; c += gridDim.y * blockDim.x) {
     double d1, d2;
     act_d12(act, (double)S[(int64_t)b * n + c], d1, d2);
     double ut = 0.0;
@@ -154,6 +154,33 @@ __global__ void k_tr_adam(int64_t count, double* __restrict__ P, const double* _
     const double p = P[i] - lr * (m / c1) / (sqrt(v / c2) + eps);
     P[i] = p;
     P32[i] = (float)p;
+  }
+}
+
+// out (cols x rows) = in (rows x cols)^T, 32 x 32 smem tiles
+__global__ void k_tr_transpose(int64_t rows, int cols, const float* __restrict__ in, float* __restrict__ out) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32;
+  const int c0 = blockIdx.x * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y;
+    const int c = c0 + threadIdx.x;
+    t[y][threadIdx.x] = (r < rows && c < cols) ? in[r * cols + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int c = c0 + y;
+    const int64_t r = r0 + threadIdx.x;
+    if (c < cols && r < rows) out[(int64_t)c * rows + r] = t[threadIdx.x][y];
+  }
+}
+
+// G64 += sum_z part[z] (fixed z order)
+__global__ void k_tr_sum_z(int64_t count, int Z, const float* __restrict__ part, double* __restrict__ G) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < Z; ++z) s += (double)part[(int64_t)z * count + i];
+    G[i] += s;
   }
 }
 
