@@ -192,6 +192,7 @@ struct sdn_handle {
   bool qr_valid = false;
   double* wpart = nullptr;      // k_weights block partials (qgrid x 2 SDN_RMAX)
   double* vsum = nullptr;       // 2 SDN_RMAX: per-risk sum_{w != 0} Q, count
+  int* red_counter = nullptr;   // last-block reduction counters (k_qoi, k_weights), self re-arming
   unsigned* ref_bar = nullptr;  // k_refine grid barrier
   int ref_grid = 0;
   bool ref_ok = false;          // every layer input width <= REF_KC
@@ -622,6 +623,8 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->seed_b2, h->r_u))) return bail(rc);
   if ((rc = dalloc(h, &h->wpart, (size_t)h->qgrid * 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->vsum, 2 * SDN_RMAX))) return bail(rc);
+  if ((rc = dalloc(h, &h->red_counter, 4))) return bail(rc);
+  if (cudaMemset(h->red_counter, 0, 4 * sizeof(int)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
   if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);
   if (cudaMemset(h->ref_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
   for (int i = 0; i < 2; ++i)
@@ -947,9 +950,8 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   { ProfScope ps(h, PC_QOI, 4.0 * h->n * h->r_u, 4.0 * h->n * h->r_u * (dec ? 2 : 1) + 8.0 * h->n);
   k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
                                    h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
-                                   h->Q, h->qpart, tp);
-  k_sum_rows<<<(unsigned)cdiv(STATS_LEN, 8), 256, 0, h->stream>>>(qg, STATS_LEN, h->qpart, stats_dev); }
-  h->launches += 2;
+                                   h->Q, h->qpart, tp, h->red_counter, stats_dev); }
+  h->launches += 1;
   CHECK_LAUNCH(h);
   TRY(refine_window(h, risk, dec, qg, stats_dev, tp));
   h->fwd_done = true;
@@ -1106,9 +1108,9 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   const int wg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(nmax, 1), 256), h->qgrid));
   auto weights = [&]() -> int {
     ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * (1 + R));
-    k_weights<<<wg, 256, 0, h->stream>>>(nmax, nact, rowidx, rs, h->Q, stats_dev, h->shift, sw.W, h->wpart);
-    k_sum_rows<<<(unsigned)cdiv(2 * SDN_RMAX, 8), 256, 0, h->stream>>>(wg, 2 * SDN_RMAX, h->wpart, h->vsum);
-    h->launches += 2;
+    k_weights<<<wg, 256, 0, h->stream>>>(nmax, nact, rowidx, rs, h->Q, stats_dev, h->shift, sw.W, h->wpart,
+                                         h->red_counter + 1, h->vsum);
+    h->launches += 1;
     CHECK_LAUNCH(h);
     return SDN_OK;
   };

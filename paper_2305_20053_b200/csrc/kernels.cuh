@@ -16,6 +16,31 @@ enum RiskKind : int { RISK_MEAN = 0, RISK_CVAR_SMOOTH = 1, RISK_MEANVAR = 2, RIS
 
 constexpr int STATS_LEN = 8;   // [n, sum q~, sum q~^2, sum splus, sum d1, n_active, 0, 0]
 
+// Last-block reduction (fuses the k_sum_rows pass into the producing kernel):
+// every block has written its w-wide partial row; the last block to finish
+// sums the nb rows in a fixed order into out and re-arms the counter.  All
+// threads of every block must call it.
+SDN_DEV void last_block_sum(int* counter, int nb, int w, const double* part, double* out) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(counter, 1) == nb - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // one warp per field, lanes stride the rows, fixed butterfly (as k_sum_rows)
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int f = threadIdx.x >> 5; f < w; f += nw) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(part + (int64_t)b * w + f);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[f] = s;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+}
+
 // zb = b1 + Pz z  (first-layer control contribution, W1_z V_z^T z, shared by
 // every sample of the evaluation -- SURVEY 2.2 K2)
 // one warp per output c, lanes over k (row c of Pz is contiguous)
@@ -63,7 +88,8 @@ __global__ void k_build_x(int64_t n, int r_m, int d_z, int ldx, const float* __r
 __global__ void __launch_bounds__(256)
 k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict__ kphi,
       const float* __restrict__ c, double q0, double shift, double t, double eps,
-      double* __restrict__ Q, double* __restrict__ part, const double* __restrict__ tp = nullptr) {
+      double* __restrict__ Q, double* __restrict__ part, const double* __restrict__ tp = nullptr,
+      int* __restrict__ counter = nullptr, double* __restrict__ out = nullptr) {
   if (tp) t = *tp;                     // device-side t (graph replay)
   __shared__ double sp[8][6];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -95,6 +121,7 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
     part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = s;
   }
   if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;
+  if (counter) last_block_sum(counter, gridDim.x, STATS_LEN, part, out);
 }
 
 // fixed-order sum of nb rows of width w (fp64) -> out (w): one warp per
@@ -327,7 +354,7 @@ k_union_compact(int64_t n, RiskSet rs, const double* __restrict__ Q, const int* 
 __global__ void __launch_bounds__(256)
 k_weights(int64_t nsw, const int* __restrict__ n_act_dev, const int* __restrict__ rowidx, RiskSet rs,
           const double* __restrict__ Q, const double* __restrict__ st, double shift, double* __restrict__ W,
-          double* __restrict__ part) {
+          double* __restrict__ part, int* __restrict__ counter = nullptr, double* __restrict__ out = nullptr) {
   __shared__ double sp[8][2 * SDN_RMAX];
   const int64_t nr = n_act_dev ? (int64_t)*n_act_dev : nsw;
   double acc[2 * SDN_RMAX];
@@ -357,6 +384,7 @@ k_weights(int64_t nsw, const int* __restrict__ n_act_dev, const int* __restrict_
     for (int w = 0; w < 8; ++w) s += sp[w][threadIdx.x];
     part[(int64_t)blockIdx.x * 2 * SDN_RMAX + threadIdx.x] = s;
   }
+  if (counter) last_block_sum(counter, gridDim.x, 2 * SDN_RMAX, part, out);
 }
 
 // weighted column sums of U (n_act x w): part[r][by][c] = sum_rows W[row][r] U[row][c]
