@@ -268,6 +268,10 @@ constexpr int TC_BM = 128;
 static unsigned long long* g_tc_trace = nullptr;
 // tuning switch: thread-issued coalesced stores instead of TMA stores
 static bool g_tc_thread_stores = getenv("SDN_TC_THREAD_STORES") != nullptr;
+// programmatic dependent launch between consecutive GEMMs: measured slower at
+// c2 (early-resident dependent CTAs take the SMs the side stream needs), so
+// opt-in only (SDN_PDL=1)
+static bool g_tc_pdl = getenv("SDN_PDL") != nullptr;
 constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 
 // per epilogue warp: two fp32 32x16 tiles + two bf16 32x16 tiles (6 KB)
@@ -797,13 +801,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  if (Mdev) M = min(M, (int64_t)*Mdev);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tiles = (int)((M + TC_BM - 1) / TC_BM);
-  const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
-  const int kblocks = (K + TC_BK - 1) / TC_BK;
-
   if (threadIdx.x == 0) {
     tcx::prefetch_tmap(&tAh); tcx::prefetch_tmap(&tAl);
     tcx::prefetch_tmap(&tBh); tcx::prefetch_tmap(&tBl);
@@ -819,6 +817,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   __syncthreads();
   tcx::fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM,
+  // descriptor prefetch) overlaps the previous grid's tail; every global
+  // access (operands, epilogue inputs and outputs, *Mdev) comes after it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (Mdev) M = min(M, (int64_t)*Mdev);
+  const int m_tiles = (int)((M + TC_BM - 1) / TC_BM);
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = (K + TC_BK - 1) / TC_BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1050,9 +1058,21 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   TcOutMaps om;
   memset(&om, 0, sizeof(om));
   const int use_om = g_tc_thread_stores ? 0 : EpiOut<Epi>::build(t, epi, std::max<int64_t>(M, 1), N, om);
-  tc_gemm_kernel<BN, Epi><<<grid, TC_THREADS, TcCfg<BN>::SMEM, st>>>(ah, al, bh, bl, M, Mdev, N, K, epi, om, use_om,
-                                                                     g_tc_trace);
-  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+  // optional programmatic stream serialization (PDL, SDN_PDL=1): the kernel
+  // may start while the previous one drains; griddepcontrol.wait orders it
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = TcCfg<BN>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_tc_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ah, al, bh, bl, M, Mdev, N, K, epi, om,
+                                           use_om, g_tc_trace);
+  return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -3;
 }
 
 template <class Epi>
