@@ -339,6 +339,7 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
     if (tiles < h->num_sms / 2) use_tc = false;
   }
   if (use_tc) {
+    g_tc_pdl_now = h->sm_avail == h->num_sms;   // no PDL while SMs are reserved for the side stream
     int rc = tc_gemm(h->tcw, h->stream, h->sm_avail, M, Mdev, N, K, *tcA, *tcB, epi, rows);
     h->launches++;
     if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");

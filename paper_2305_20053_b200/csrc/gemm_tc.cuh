@@ -268,10 +268,13 @@ constexpr int TC_BM = 128;
 static unsigned long long* g_tc_trace = nullptr;
 // tuning switch: thread-issued coalesced stores instead of TMA stores
 static bool g_tc_thread_stores = getenv("SDN_TC_THREAD_STORES") != nullptr;
-// programmatic dependent launch between consecutive GEMMs: measured slower at
-// c2 (early-resident dependent CTAs take the SMs the side stream needs), so
-// opt-in only (SDN_PDL=1)
-static bool g_tc_pdl = getenv("SDN_PDL") != nullptr;
+// programmatic dependent launch between consecutive GEMMs (the next GEMM's
+// prologue and launch overlap the previous one's tail).  Not while SMs are
+// reserved for the side stream: early-resident dependent CTAs would take them
+// (measured: slower there, faster and steadier everywhere else).  SDN_NO_PDL=1
+// disables it.
+static bool g_tc_pdl = getenv("SDN_NO_PDL") == nullptr;
+static bool g_tc_pdl_now = true;      // cleared by the engine while side-stream work needs free SMs
 constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 
 // per epilogue warp: two fp32 32x16 tiles + two bf16 32x16 tiles (6 KB)
@@ -1058,8 +1061,8 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   TcOutMaps om;
   memset(&om, 0, sizeof(om));
   const int use_om = g_tc_thread_stores ? 0 : EpiOut<Epi>::build(t, epi, std::max<int64_t>(M, 1), N, om);
-  // optional programmatic stream serialization (PDL, SDN_PDL=1): the kernel
-  // may start while the previous one drains; griddepcontrol.wait orders it
+  // programmatic stream serialization (PDL): the kernel may start while the
+  // previous one drains; griddepcontrol.wait orders it
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(TC_THREADS);
@@ -1067,7 +1070,7 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_tc_pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ah, al, bh, bl, M, Mdev, N, K, epi, om,
