@@ -193,6 +193,8 @@ struct sdn_handle {
   double* wpart = nullptr;      // k_weights block partials (qgrid x 2 SDN_RMAX)
   double* vsum = nullptr;       // 2 SDN_RMAX: per-risk sum_{w != 0} Q, count
   int* red_counter = nullptr;   // last-block reduction counters (k_qoi, k_weights), self re-arming
+  int* fwdflags = nullptr;      // forward chain row-block readiness (L x fwd_mtiles)
+  int fwd_mtiles = 0;
   unsigned* ref_bar = nullptr;  // k_refine grid barrier
   int ref_grid = 0;
   bool ref_ok = false;          // every layer input width <= REF_KC
@@ -323,7 +325,7 @@ static void launch_simt(sdn_handle* h, int64_t M, const int* Mdev, int N, int K,
 template <bool AT, bool BT, class Epi>
 static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const float* A, int64_t lda,
                 const float* B, int64_t ldb, Epi epi, const TcOperand* tcB = nullptr,
-                const TcOperand* tcA = nullptr, int route = -1) {
+                const TcOperand* tcA = nullptr, int route = -1, TcFlags fl = TcFlags{}) {
   if (M <= 0 || N <= 0) return SDN_OK;
   const int64_t rows = h->prows ? h->prows : M;
   h->prows = 0;
@@ -340,7 +342,7 @@ static int gemm(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const f
   }
   if (use_tc) {
     g_tc_pdl_now = h->sm_avail == h->num_sms;   // no PDL while SMs are reserved for the side stream
-    int rc = tc_gemm(h->tcw, h->stream, h->sm_avail, M, Mdev, N, K, *tcA, *tcB, epi, rows);
+    int rc = tc_gemm(h->tcw, h->stream, h->sm_avail, M, Mdev, N, K, *tcA, *tcB, epi, rows, fl);
     h->launches++;
     if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 GEMM launch failed (" + std::to_string(rc) + ")");
     CHECK_LAUNCH(h);
@@ -391,6 +393,19 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
   const int L = h->L;
   const bool tcc = !simt && chain_tc(h, nrows);
   float* const* Hb = Hs ? Hs : h->H;
+  // row-block readiness flags between the chain's GEMMs (PDL early start)
+  static const bool no_rflags = getenv("SDN_NO_RFLAGS") != nullptr;
+  const bool rflags = tcc && !Hs && nrows <= h->cap && !no_rflags;
+  if (rflags) {
+    CU(cudaMemsetAsync(h->fwdflags, 0, sizeof(int) * (size_t)L * h->fwd_mtiles, h->stream));
+  }
+  auto flags_of = [&](int l) -> TcFlags {
+    TcFlags f;
+    if (!rflags) return f;
+    if (l >= 1 && (l > 1 || tcX0)) f.in = h->fwdflags + (size_t)(l - 1) * h->fwd_mtiles;
+    if (l < L - 1) f.out = h->fwdflags + (size_t)l * h->fwd_mtiles;
+    return f;
+  };
   int cur = 0;
   const float* in = X;
   int64_t ldin = ld0;
@@ -409,10 +424,11 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
       EpiAffine e{bl, h->ostd, h->omean, phi_out, (int64_t)n_out};
       if (fuse_seed && tc && L > 1) {      // + the reverse sweep's unit seeds (bf16x3 split)
         EpiAffineSeed es{e, h->seed_a2, h->seed_b2, TcEpiSplit{&h->sw->seed}};
-        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, es, tB, tA, 1)));
+        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, es, tB, tA, 1, flags_of(l))));
         h->seed_fused = true;
       } else {
-        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA, tc ? 1 : 0)));
+        TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, e, tB, tA, tc ? 1 : 0,
+                               tc ? flags_of(l) : TcFlags{})));
       }
     } else {
       float* out = Hb[(l == 0) ? 0 : 1 - cur];
@@ -437,7 +453,8 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
       TcEpiSplit split = tcc ? TcEpiSplit{&h->tcw.act[(l == 0) ? 0 : 1 - cur]} : TcEpiSplit{nullptr};
       TcEpiSplit prev = split_prev ? TcEpiSplit{&h->tcw.act[cur]} : TcEpiSplit{nullptr};
       TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW,
-                             TcChain<EpiFwdHidden>{e, split, prev}, tB, tA, tc ? 1 : 0)));
+                             TcChain<EpiFwdHidden>{e, split, prev}, tB, tA, tc ? 1 : 0,
+                             tc ? flags_of(l) : TcFlags{})));
       cur = (l == 0) ? 0 : 1 - cur;
       in = out;
       ldin = n_out;
@@ -625,6 +642,8 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->wpart, (size_t)h->qgrid * 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->vsum, 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->red_counter, 4))) return bail(rc);
+  h->fwd_mtiles = (int)cdiv(cap, 128);
+  if ((rc = dalloc(h, &h->fwdflags, (size_t)h->L * h->fwd_mtiles))) return bail(rc);
   if (cudaMemset(h->red_counter, 0, 4 * sizeof(int)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
   if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);
   if (cudaMemset(h->ref_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));

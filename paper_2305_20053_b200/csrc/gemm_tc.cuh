@@ -191,6 +191,15 @@ SDN_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "mem
 SDN_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 SDN_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 SDN_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+SDN_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+SDN_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SDN_DEV void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 SDN_DEV void tmem_alloc(uint32_t* dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
                : "memory");
@@ -787,12 +796,23 @@ struct TileEpi<EpiBwdSum> {
   }
 };
 
+// Row-block readiness between consecutive chain GEMMs (with PDL): the
+// producing GEMM adds, per 128-row block, 32 x the columns each epilogue warp
+// finished once its TMA stores are complete (release); a consuming GEMM
+// waits (acquire) until its A row block reached 128 x K before loading it --
+// so CTAs that become resident on SMs the previous GEMM's last wave left idle
+// start on row blocks already done instead of waiting for the whole grid.
+struct TcFlags {
+  const int* in = nullptr;   // readiness of this GEMM's A operand rows (null: whole-grid dependency)
+  int* out = nullptr;        // readiness of this GEMM's outputs
+};
+
 template <int BN, class Epi>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
                const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
-               int use_om, unsigned long long* __restrict__ trace = nullptr) {
+               int use_om, unsigned long long* __restrict__ trace = nullptr, TcFlags flags = TcFlags{}) {
   using C = TcCfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -823,7 +843,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   // programmatic dependent launch: the prologue above (barriers, TMEM,
   // descriptor prefetch) overlaps the previous grid's tail; every global
   // access (operands, epilogue inputs and outputs, *Mdev) comes after it
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!flags.in) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (Mdev) M = min(M, (int64_t)*Mdev);
   const int m_tiles = (int)((M + TC_BM - 1) / TC_BM);
@@ -838,6 +858,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       if (trace && blockIdx.x == 0) trace[0] = clock64();
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int mb = tile / n_tiles, nb = tile % n_tiles;
+        if (flags.in) {                          // this row block of A written and visible
+          const int need = TC_BM * K;
+          while (tcx::ld_acquire(flags.in + mb) < need) __nanosleep(64);
+          tcx::fence_proxy_async_global();
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           tcx::mbar_wait(&empty[stage], phase ^ 1);
           if (trace && blockIdx.x == 0 && tile == (int)blockIdx.x && kb < 4) trace[1 + kb] = clock64();
@@ -919,6 +944,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (flags.out) {                           // publish this warp's part of the row block
+        if (!use_om) __threadfence();            // thread stores of all lanes
+        __syncwarp();
+        if (lane == 0) {
+          int cols = 0;
+          for (int c0 = 16 * third; c0 < BN && nb * BN + c0 < N; c0 += 48) cols += 16;
+          if (use_om) tcx::bulk_wait0();         // this warp's TMA stores complete
+          tcx::fence_proxy_async_global();
+          tcx::red_release_add(flags.out + mb, 32 * cols);
+        }
+      }
     }
     if (use_om && lane == 0) tcx::bulk_wait0();    // this warp's TMA stores are complete
   }
@@ -1046,7 +1082,7 @@ inline bool tc_gemm_supported(int64_t M, int N, int K) {
 
 template <int BN, class Epi>
 static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const int* Mdev, int N, int K,
-                     const TcOperand& A, const TcOperand& B, Epi epi) {
+                     const TcOperand& A, const TcOperand& B, Epi epi, TcFlags fl = TcFlags{}) {
   CUtensorMap ah, al, bh, bl;
   if (tc_map(t, A.hi, std::max<int64_t>(M, 1), K, A.ld, TC_BM, &ah) || tc_map(t, A.lo, std::max<int64_t>(M, 1), K, A.ld, TC_BM, &al) ||
       tc_map(t, B.hi, N, K, B.ld, BN, &bh) || tc_map(t, B.lo, N, K, B.ld, BN, &bl))
@@ -1073,23 +1109,26 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (!(g_tc_pdl && g_tc_pdl_now)) fl.in = nullptr;   // row flags only pay off with early (PDL) launch
   const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ah, al, bh, bl, M, Mdev, N, K, epi, om,
-                                           use_om, g_tc_trace);
+                                           use_om, g_tc_trace, fl);
   return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -3;
 }
 
 template <class Epi>
 static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const int* Mdev, int N, int K,
-                   const TcOperand& A, const TcOperand& B, Epi epi, int64_t rows_est = -1) {
+                   const TcOperand& A, const TcOperand& B, Epi epi, int64_t rows_est = -1, TcFlags fl = TcFlags{}) {
   // widest N tile that still gives every SM work; narrower tiles for the
   // short compacted sweeps (CVaR tails) and small shards
   const int64_t mt = ((rows_est > 0 ? rows_est : M) + TC_BM - 1) / TC_BM;
   static const int bn_force = getenv("SDN_TC_BN") ? atoi(getenv("SDN_TC_BN")) : 0;   // tuning override
-  if (bn_force == 64) return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
-  if (bn_force == 128) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
-  if (N > 128 && mt * ((N + 255) / 256) >= num_sms / 2) return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
-  if (N > 64 && mt * ((N + 127) / 128) >= num_sms / 4) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
-  return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi);
+  if (bn_force == 64) return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
+  if (bn_force == 128) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
+  if (N > 128 && mt * ((N + 255) / 256) >= num_sms / 2)
+    return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
+  if (N > 64 && mt * ((N + 127) / 128) >= num_sms / 4)
+    return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
+  return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
 }
 
 // allocation / refresh of the split operands -------------------------------
