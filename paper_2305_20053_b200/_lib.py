@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsaadino.so")
+# SDN_LIB_VARIANT=name loads libsaadino_<name>.so (build-variant A/B studies)
+LIB_PATH = os.path.join(_HERE, "libsaadino" + (("_" + os.environ["SDN_LIB_VARIANT"]) if os.environ.get("SDN_LIB_VARIANT") else "") + ".so")
 
 SDN_OK = 0
 ACT = {"identity": 0, "tanh": 1, "softplus": 2, "sigmoid": 3, "elu": 4, "softmax": 5}

@@ -2094,12 +2094,21 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   // read from the input's bf16 split, D + split outputs)
   // mode 9: the chain epilogue with the identity activation (arithmetic share of ELU);
   // 10 / 11 / 12: the chain epilogue without the act' store / the split store / the residual input
+  // 13 / 14: the chain epilogue with the MMAs skipped / MMAs and TMA loads
+  // skipped (epilogue pace alone)
+  // composite study modes: base | 256 skip MMAs | 512 skip TMA loads | 1024 no act' store |
+  // 2048 no split store | 4096 no residual input
+  const int flags = mode & ~255;
+  mode &= 255;
+  int skip = mode == 13 ? 1 : mode == 14 ? 3 : (flags >> 8) & 3;
+  cudaMemcpyToSymbol(g_tc_dbg_skip, &skip, sizeof(int));
   const bool chainm = mode == 8 || mode >= 9;
+  const bool noD = mode == 10 || (flags & 1024), noS = mode == 11 || (flags & 2048), noP = mode == 12 || (flags & 4096);
   EpiFwdHidden e{h->b[1], (h->res[1] && keepP && !chainm) ? h->H[0] : nullptr, keepH ? h->H[1] : nullptr,
-                 ((keepD || chainm) && mode != 10) ? h->D[1] : nullptr, (int64_t)N,
+                 ((keepD || chainm) && !noD) ? h->D[1] : nullptr, (int64_t)N,
                  mode == 9 ? (int)ACT_IDENTITY : h->act};
-  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{((keepS || chainm) && mode != 11) ? &h->tcw.act[1] : nullptr},
-                           TcEpiSplit{(chainm && h->res[1] && mode != 12) ? &h->tcw.act[0] : nullptr}};
+  TcChain<EpiFwdHidden> ch{e, TcEpiSplit{((keepS || chainm) && !noS) ? &h->tcw.act[1] : nullptr},
+                           TcEpiSplit{(chainm && h->res[1] && !noP) ? &h->tcw.act[0] : nullptr}};
   h->tcw.act[0].rows = M;
   int rc = 0;
   for (int it = 0; it <= reps && rc == 0; ++it) {
@@ -2113,14 +2122,14 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   if (getenv("SDN_TRACE") && mode != 2 && rc == 0) {
     // one more launch with per-phase clock64 stamps of CTA 0 (stderr)
     unsigned long long* tr = nullptr;
-    cudaMalloc(&tr, 64 * sizeof(unsigned long long));
-    cudaMemset(tr, 0, 64 * sizeof(unsigned long long));
+    cudaMalloc(&tr, 128 * sizeof(unsigned long long));
+    cudaMemset(tr, 0, 128 * sizeof(unsigned long long));
     g_tc_trace = tr;
     if (mode == 0) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], EpiNull{});
     else rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], ch);
     g_tc_trace = nullptr;
     cudaStreamSynchronize(h->stream);
-    unsigned long long ht[64];
+    unsigned long long ht[128];
     cudaMemcpy(ht, tr, sizeof(ht), cudaMemcpyDeviceToHost);
     cudaFree(tr);
     fprintf(stderr, "trace mode %d M %lld: tma[kb0..3] %lld %lld %lld %lld | mma_done %lld | epi_start %lld |", mode,
@@ -2130,6 +2139,8 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
       if (ht[9 + 2 * i]) fprintf(stderr, " c%d[%lld,%lld]", i, (long long)(ht[9 + 2 * i] - ht[0]), (long long)(ht[10 + 2 * i] - ht[0]));
     fprintf(stderr, "\n");
   }
+  skip = 0;
+  cudaMemcpyToSymbol(g_tc_dbg_skip, &skip, sizeof(int));
   float t = 0.f;
   cudaEventElapsedTime(&t, a, b);
   cudaEventDestroy(a);

@@ -1,3 +1,4 @@
+#include <type_traits>
 // gemm_tc.cuh -- tcgen05 GEMM back end (sm_100a): TMA -> SMEM (128B swizzle)
 // -> tcgen05.mma.kind::f16 (bf16 x bf16 -> fp32 in TMEM) -> tcgen05.ld
 // epilogue with the same fused functors as the SIMT kernel.
@@ -272,6 +273,9 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 
 }  // namespace tcx
 
+#ifndef SDN_ST256
+#define SDN_ST256 3
+#endif
 constexpr int TC_BM = 128;
 // optional device trace buffer (sdn_debug_gemm): per-phase clock64 stamps of CTA 0
 static unsigned long long* g_tc_trace = nullptr;
@@ -284,6 +288,8 @@ static bool g_tc_thread_stores = getenv("SDN_TC_THREAD_STORES") != nullptr;
 // disables it.
 static bool g_tc_pdl = getenv("SDN_NO_PDL") == nullptr;
 static bool g_tc_pdl_now = true;      // cleared by the engine while side-stream work needs free SMs
+// sdn_debug_gemm study switch (device): bit 0 skips the MMAs, bit 1 also the TMA loads
+__device__ int g_tc_dbg_skip = 0;
 constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 
 // per epilogue warp: two fp32 32x16 tiles + two bf16 32x16 tiles (6 KB)
@@ -291,14 +297,25 @@ constexpr uint32_t TC_EPI_WARP_BYTES = 6144;
 constexpr int TC_EPI_WARPS = 12;               // three per TMEM lane quarter
 constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
 
-template <int BN>
+// RING > 0: the asynchronous-input epilogue (epi_ring): per warp RING
+// 2-KB slots that TMA-load the epilogue's input tile ahead of use and then
+// stage its bf16 split output, a 2-KB fp32 output tile, and a shared 4-KB
+// bias copy; the mainloop ring gets whatever shared memory is left (2-4 stages)
+constexpr uint32_t TC_SMEM_MAX = 232448;      // 227 KB opt-in per block
+constexpr uint32_t TC_BAR_BYTES = 1024;       // mbarriers + TMEM slot
+// (reverse-sweep rings, BWD: 4-KB slots holding the residual-gradient and
+// act' input tiles, reused for the G and split outputs; no bias)
+template <int BN, int RING = 0, bool BWD = false>
 struct TcCfg {
   static constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;
   static constexpr uint32_t B_BYTES = BN * TC_BK * 2;
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 3 : 4;
-  static constexpr uint32_t EPI_BYTES = TC_EPI_WARPS * TC_EPI_WARP_BYTES;
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t EPI_WARP =
+      !RING ? TC_EPI_WARP_BYTES : BWD ? (uint32_t)RING * 4096u : (uint32_t)RING * 2048u + 2048u;
+  static constexpr uint32_t EPI_BYTES = TC_EPI_WARPS * EPI_WARP + ((RING && !BWD) ? 4096u : 0u);
+  static constexpr int STAGES_FIT = (int)((TC_SMEM_MAX - EPI_BYTES - 1024 - TC_BAR_BYTES) / STAGE_BYTES);
+  static constexpr int STAGES = RING ? (STAGES_FIT > 4 ? 4 : STAGES_FIT) : ((BN == 256) ? SDN_ST256 : 4);
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + TC_BAR_BYTES;
 };
 
 // ---------------------------------------------------------------------------
@@ -454,7 +471,7 @@ SDN_DEV void row_put_split(uint32_t* bh, uint32_t* bl, int lane, const float (&x
 // output tensor maps of a TMA-store epilogue (slot meaning per epilogue:
 // fwd hidden H, D, hi, lo; reverse G, U, hi, lo; affine C)
 struct TcOutMaps {
-  CUtensorMap m[4];
+  CUtensorMap m[6];      // m[4], m[5]: ring-epilogue input tiles (hi, lo or fp32 pair)
 };
 
 struct EpiSmem {
@@ -598,6 +615,34 @@ struct TileEpi<EpiAffineSeed> {
   }
 };
 
+// hidden-layer activation of one 16-column row chunk: a = [a +] act(v + b),
+// d = act'(v + b)
+SDN_DEV void fwd_act16(int act, const uint32_t (&v)[16], const float (&bias)[16], bool has_prev, float (&a)[16],
+                       float (&d)[16]) {
+  if (act == ACT_ELU) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      // branch-free (selects only) so the 16 elements interleave
+      const float x = __uint_as_float(v[j]) + bias[j];
+      const float xn = x > 0.0f ? 0.0f : x;     // (not fminf: a NaN must propagate, as in the oracle)
+      const float ex = __expf(xn);
+      // e^x - 1 without cancellation near 0 (Taylor to x^5 on (-1/16, 0])
+      const float pm = xn * (1.0f + xn * (0.5f + xn * (0.16666667f + xn * (0.041666668f + xn * 0.008333334f))));
+      const float y = x > 0.0f ? x : (xn > -0.0625f ? pm : ex - 1.0f);
+      a[j] = has_prev ? a[j] + y : y;
+      d[j] = x > 0.0f ? 1.0f : ex;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float y, dy;
+      act_eval(act, __uint_as_float(v[j]) + bias[j], y, dy);
+      a[j] = has_prev ? a[j] + y : y;
+      d[j] = dy;
+    }
+  }
+}
+
 // hidden layer forward: H = [prev +] act(acc + b), D = act'(.), split(H).
 // In a tensor-core chain prev comes from the previous layer's bf16 split
 // (ch.prev) and the fp32 H is not written (e.H == nullptr).
@@ -636,28 +681,7 @@ struct TileEpi<TcChain<EpiFwdHidden>> {
       const float4 b4 = pre.c[j / 4];
       bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
     }
-    if (e.act == ACT_ELU) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        // branch-free (selects only) so the 16 elements interleave
-        const float x = __uint_as_float(v[j]) + bias[j];
-        const float xn = x > 0.0f ? 0.0f : x;     // (not fminf: a NaN must propagate, as in the oracle)
-        const float ex = __expf(xn);
-        // e^x - 1 without cancellation near 0 (Taylor to x^5 on (-1/16, 0])
-        const float pm = xn * (1.0f + xn * (0.5f + xn * (0.16666667f + xn * (0.041666668f + xn * 0.008333334f))));
-        const float y = x > 0.0f ? x : (xn > -0.0625f ? pm : ex - 1.0f);
-        a[j] = has_prev ? a[j] + y : y;
-        d[j] = x > 0.0f ? 1.0f : ex;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float y, dy;
-        act_eval(e.act, __uint_as_float(v[j]) + bias[j], y, dy);
-        a[j] = has_prev ? a[j] + y : y;
-        d[j] = dy;
-      }
-    }
+    fwd_act16(e.act, v, bias, has_prev, a, d);
     __syncwarp();
     if (e.H) row_put(s.f0, lane, a);
     if (e.D) row_put(s.f1, lane, d);
@@ -807,13 +831,301 @@ struct TcFlags {
   int* out = nullptr;        // readiness of this GEMM's outputs
 };
 
-template <int BN, class Epi>
+// ---------------------------------------------------------------------------
+// asynchronous-input epilogue for the forward chain (RING slots per warp).
+// The epilogue used to prefetch its residual input through registers one
+// chunk ahead; the loads were then still in flight at the proxy fence before
+// the TMA stores (MEMBAR), so every chunk paid a full global latency.  Here
+// the residual tiles (the previous layer's bf16 split, 32 rows x 16 columns)
+// are TMA-loaded RING-1 chunks ahead into per-warp slots (async proxy,
+// mbarrier completion, no registers held), the chunk's split output is
+// staged in the slot it was read from, and the bias comes from a per-CTA
+// shared copy.  The chunk order per warp runs across the CTA's tiles, so the
+// next tile's first residual tiles load during the current tile's last chunks.
+template <int BN, int RING>
+SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, uint8_t* epi_base, uint64_t* rbar_all,
+                          uint64_t* tfull, uint64_t* tempty, uint32_t tmem, int warp, int lane, int num_tiles,
+                          int n_tiles, int N, int K, const TcFlags& flags) {
+  constexpr uint32_t WB = (uint32_t)RING * 2048u + 2048u;
+  const int w = warp - 4, q = warp & 3, third = w >> 2, first_c = 16 * third;
+  uint8_t* wb = epi_base + w * WB;
+  float* Dst = reinterpret_cast<float*>(wb + RING * 2048);
+  float* bias_s = reinterpret_cast<float*>(epi_base + TC_EPI_WARPS * WB);
+  uint64_t* rbar = rbar_all + w * RING;
+  const EpiFwdHidden& e = ch.base;
+  const bool has_prev = ch.prev.hi != nullptr, has_split = ch.split.hi != nullptr, has_D = e.D != nullptr;
+  const bool bias_smem = N <= 1024;
+  if (bias_smem)
+    for (int i = (int)threadIdx.x - 128; i < N; i += 32 * TC_EPI_WARPS) bias_s[i] = __ldg(e.bias + i);
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS) : "memory");
+
+  // load cursor (tile lt, column lc), RING-1 chunks ahead of the compute cursor
+  int lt = blockIdx.x, lc = first_c, jl = 0, last_mb = -1;
+  auto lnorm = [&]() {
+    while (lt < num_tiles && !(lc < BN && (lt % n_tiles) * BN + lc < N)) { lt += gridDim.x; lc = first_c; }
+  };
+  auto issue = [&]() {
+    if (lt >= num_tiles) return;
+    if (has_prev) {
+      const int mb = lt / n_tiles, s = jl % RING;
+      if (lane == 0) {
+        if (flags.in && mb != last_mb) {          // rows of the previous layer written and visible
+          while (tcx::ld_acquire(flags.in + mb) < TC_BM * K) __nanosleep(64);
+          tcx::fence_proxy_async_global();
+        }
+        tcx::mbar_expect_tx(&rbar[s], 2048);
+        const int x = (lt % n_tiles) * BN + lc, y = mb * TC_BM + q * 32;
+        tcx::tma_load_2d(wb + s * 2048, &om.m[4], &rbar[s], x, y);
+        tcx::tma_load_2d(wb + s * 2048 + 1024, &om.m[5], &rbar[s], x, y);
+      }
+      last_mb = mb;
+    }
+    ++jl;
+    lc += 48;
+    lnorm();
+  };
+  lnorm();
+  for (int k = 0; k < RING - 1; ++k) issue();
+
+  int acc = 0, jc = 0;
+  uint32_t acc_phase = 0;
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const int mb = tile / n_tiles, nb = tile % n_tiles;
+    const int r0 = mb * TC_BM + q * 32;
+    int nch = 0;
+    for (int c = first_c; c < BN && nb * BN + c < N; c += 48) ++nch;
+    tcx::mbar_wait(&tfull[acc], acc_phase);
+    tcx::fence_after();
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+    if (nch == 0) {
+      tcx::fence_before();
+      __syncwarp();
+      if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+    }
+#pragma unroll 1
+    for (int ci = 0; ci < nch; ++ci, ++jc) {
+      const int c0 = first_c + 48 * ci, col = nb * BN + c0, s = jc % RING;
+      uint32_t* sh = reinterpret_cast<uint32_t*>(wb + s * 2048);
+      uint32_t* sl = sh + 256;
+      uint32_t v[16];
+      tcx::tmem_ld16(tbase + c0, v);
+      if (has_prev) tcx::mbar_wait(&rbar[s], (uint32_t)(jc / RING) & 1u);
+      tcx::tmem_ld_wait();
+      if (ci == nch - 1) {                        // accumulator drained: the MMA may reuse it
+        tcx::fence_before();
+        __syncwarp();
+        if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+      }
+      float a[16], d[16], bias[16];
+      if (has_prev) row_get_split(sh, sl, lane, a);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 b4 = bias_smem ? *reinterpret_cast<const float4*>(bias_s + col + j)
+                                    : __ldg(reinterpret_cast<const float4*>(e.bias + col + j));
+        bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
+      }
+      fwd_act16(e.act, v, bias, has_prev, a, d);
+      // the previous chunk's stores have read the output tile and its slot:
+      // refill that slot RING-1 chunks ahead
+      if (lane == 0) tcx::bulk_wait_read0();
+      __syncwarp();
+      issue();
+      if (has_D) row_put(Dst, lane, d);
+      if (has_split) row_put_split(sh, sl, lane, a);
+      tcx::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (has_D) tcx::tma_store_2d(&om.m[1], Dst, col, r0);
+        if (has_split) {
+          tcx::tma_store_2d(&om.m[2], sh, col, r0);
+          tcx::tma_store_2d(&om.m[3], sl, col, r0);
+        }
+        tcx::bulk_commit();
+      }
+    }
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    if (flags.out) {                              // publish this warp's part of the row block
+      __syncwarp();
+      if (lane == 0) {
+        tcx::bulk_wait0();
+        tcx::fence_proxy_async_global();
+        tcx::red_release_add(flags.out + mb, 32 * 16 * nch);
+      }
+    }
+  }
+  if (lane == 0) tcx::bulk_wait0();
+}
+
+// asynchronous-input epilogue for the dense reverse sweep (no row gather):
+// per chunk the residual-gradient tile (fp32, optional) and the act' tile
+// (fp32) are TMA-loaded RING-1 chunks ahead into one 4-KB slot; the chain
+// step stages G in the residual half and the bf16 split of u = D g in the
+// act' half for its TMA stores; the summing step (EpiBwdSum) stages u and
+// the per-row risk weights there for its fixed-order fp64 column sums.
+template <class Epi>
+struct BwdRingView;
+template <>
+struct BwdRingView<TcChain<EpiBwd>> {
+  static constexpr bool SUM = false;
+  static SDN_DEV const float* resid(const TcChain<EpiBwd>& c) { return c.base.resid; }
+};
+template <>
+struct BwdRingView<EpiBwdSum> {
+  static constexpr bool SUM = true;
+  static SDN_DEV const float* resid(const EpiBwdSum& e) { return e.resid; }
+};
+
+template <int BN, int RING, class Epi>
+SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base, uint64_t* rbar_all,
+                          uint64_t* tfull, uint64_t* tempty, uint32_t tmem, int warp, int lane, int num_tiles,
+                          int n_tiles, int64_t M, int N) {
+  constexpr bool SUM = BwdRingView<Epi>::SUM;
+  constexpr uint32_t WB = (uint32_t)RING * 4096u;
+  const int w = warp - 4, q = warp & 3, third = w >> 2, first_c = 16 * third;
+  uint8_t* wb = epi_base + w * WB;
+  uint64_t* rbar = rbar_all + w * RING;
+  const bool has_resid = BwdRingView<Epi>::resid(ep) != nullptr;
+  const uint32_t tx = has_resid ? 4096u : 2048u;
+
+  int lt = blockIdx.x, lc = first_c, jl = 0;
+  auto lnorm = [&]() {
+    while (lt < num_tiles && !(lc < BN && (lt % n_tiles) * BN + lc < N)) { lt += gridDim.x; lc = first_c; }
+  };
+  auto issue = [&]() {
+    if (lt >= num_tiles) return;
+    const int s = jl % RING;
+    if (lane == 0) {
+      const int x = (lt % n_tiles) * BN + lc, y = (lt / n_tiles) * TC_BM + q * 32;
+      tcx::mbar_expect_tx(&rbar[s], tx);
+      if (has_resid) tcx::tma_load_2d(wb + s * 4096, &om.m[4], &rbar[s], x, y);
+      tcx::tma_load_2d(wb + s * 4096 + 2048, &om.m[5], &rbar[s], x, y);
+    }
+    ++jl;
+    lc += 48;
+    lnorm();
+  };
+  lnorm();
+  for (int k = 0; k < RING - 1; ++k) issue();
+
+  int acc = 0, jc = 0;
+  uint32_t acc_phase = 0;
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const int mb = tile / n_tiles, nb = tile % n_tiles;
+    const int64_t r0 = (int64_t)mb * TC_BM + q * 32;
+    int nch = 0;
+    for (int c = first_c; c < BN && nb * BN + c < N; c += 48) ++nch;
+    tcx::mbar_wait(&tfull[acc], acc_phase);
+    tcx::fence_after();
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+    if (nch == 0) {
+      tcx::fence_before();
+      __syncwarp();
+      if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+    }
+#pragma unroll 1
+    for (int ci = 0; ci < nch; ++ci, ++jc) {
+      const int c0 = first_c + 48 * ci, col = nb * BN + c0, s = jc % RING;
+      float* Rs = reinterpret_cast<float*>(wb + s * 4096);
+      float* Ds = Rs + 512;
+      uint32_t v[16];
+      tcx::tmem_ld16(tbase + c0, v);
+      tcx::mbar_wait(&rbar[s], (uint32_t)(jc / RING) & 1u);
+      tcx::tmem_ld_wait();
+      if (ci == nch - 1) {
+        tcx::fence_before();
+        __syncwarp();
+        if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+      }
+      float g[16], dd[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) g[j] = __uint_as_float(v[j]);
+      if (has_resid) {
+        float r[16];
+        row_get(Rs, lane, r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) g[j] += r[j];
+      }
+      row_get(Ds, lane, dd);
+      if constexpr (SUM) {
+        const EpiBwdSum& e = ep;
+        const bool live = r0 + lane < M;           // rows past M hold stale operand data
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dd[j] = live ? dd[j] * g[j] : 0.0f;
+        __syncwarp();
+        row_put(Ds, lane, dd);
+        double* ws = reinterpret_cast<double*>(Rs);   // per-row risk weights (fp64)
+        if (e.W)
+          for (int qq = 0; qq < e.R; ++qq) ws[qq * 32 + lane] = live ? e.W[(r0 + lane) * e.R + qq] : 0.0;
+        __syncwarp();
+        const int64_t prow = (r0 >> 7) * 4 + ((r0 >> 5) & 3);
+        const int j = lane & 15;
+        if (!e.W) {
+          if (lane < 16 && col + j < N) {
+            double a = 0.0;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) a += (double)Ds[sw_f(r, j >> 2) + (j & 3)];
+            e.part[prow * e.ldp + col + j] = a;
+          }
+        } else if (col + j < N) {
+          for (int qq = lane >> 4; qq < e.R; qq += 2) {
+            double a = 0.0;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) a += ws[qq * 32 + r] * (double)Ds[sw_f(r, j >> 2) + (j & 3)];
+            e.part[qq * e.plane + prow * e.ldp + col + j] = a;
+          }
+        }
+        // this slot's generic reads before the async refill of the previous one
+        tcx::fence_proxy_async();
+        __syncwarp();
+        issue();
+      } else {
+        const TcChain<EpiBwd>& ch = ep;
+        const bool has_G = ch.base.G != nullptr, has_split = ch.split.hi != nullptr;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dd[j] *= g[j];
+        if (lane == 0) tcx::bulk_wait_read0();   // previous chunk's stores have read their slot
+        __syncwarp();
+        issue();
+        if (has_G) row_put(Rs, lane, g);
+        uint32_t* sh = reinterpret_cast<uint32_t*>(Ds);
+        if (has_split) row_put_split(sh, sh + 256, lane, dd);
+        tcx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if (has_G) tcx::tma_store_2d(&om.m[0], Rs, col, (int)r0);
+          if (has_split) {
+            tcx::tma_store_2d(&om.m[2], sh, col, (int)r0);
+            tcx::tma_store_2d(&om.m[3], sh + 256, col, (int)r0);
+          }
+          tcx::bulk_commit();
+        }
+      }
+    }
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+  if (!SUM && lane == 0) tcx::bulk_wait0();
+}
+
+template <class Epi>
+struct RingKind {
+  static constexpr bool BWD = false;
+};
+template <>
+struct RingKind<TcChain<EpiBwd>> {
+  static constexpr bool BWD = true;
+};
+template <>
+struct RingKind<EpiBwdSum> {
+  static constexpr bool BWD = true;
+};
+
+template <int BN, class Epi, int RING = 0>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
                const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
                int use_om, unsigned long long* __restrict__ trace = nullptr, TcFlags flags = TcFlags{}) {
-  using C = TcCfg<BN>;
+  using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment by offset arithmetic keeps the pointer in the shared window
@@ -822,7 +1134,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;                   // RING slots per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + (RING ? RING * TC_EPI_WARPS : 0));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -830,6 +1143,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
     tcx::prefetch_tmap(&tBh); tcx::prefetch_tmap(&tBl);
     for (int s = 0; s < STAGES; ++s) { tcx::mbar_init(&full[s], 1); tcx::mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], TC_EPI_WARPS); }
+    for (int i = 0; i < RING * TC_EPI_WARPS; ++i) tcx::mbar_init(&rbar[i], 1);
     tcx::fence_barrier_init();
   }
   if (warp == 2) {
@@ -855,6 +1169,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const bool skip_loads = (g_tc_dbg_skip & 2) != 0;
       if (trace && blockIdx.x == 0) trace[0] = clock64();
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int mb = tile / n_tiles, nb = tile % n_tiles;
@@ -867,6 +1182,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
           tcx::mbar_wait(&empty[stage], phase ^ 1);
           if (trace && blockIdx.x == 0 && tile == (int)blockIdx.x && kb < 4) trace[1 + kb] = clock64();
           uint8_t* st = smem + stage * C::STAGE_BYTES;
+          if (skip_loads) {
+            tcx::mbar_arrive(&full[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           tcx::tma_load_2d(st, &tAh, &full[stage], kb * TC_BK, mb * TC_BM);
           tcx::tma_load_2d(st + C::A_BYTES, &tAl, &full[stage], kb * TC_BK, mb * TC_BM);
@@ -881,6 +1201,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       constexpr uint32_t idesc = tcx::idesc_bf16(TC_BM, BN);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
+      const bool skip_mma = (g_tc_dbg_skip & 1) != 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tcx::fence_after();
@@ -890,7 +1211,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
           tcx::fence_after();
           const uint32_t base = tcx::smem_u32(smem + stage * C::STAGE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+          for (int kk = 0; kk < (skip_mma ? 0 : TC_BK / 16); ++kk) {
             const uint64_t ah = tcx::sdesc_k64(base + kk * 32);
             const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
             const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
@@ -907,6 +1228,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (RING > 0 && warp >= 4) {
+    if constexpr (RING > 0 && RingKind<Epi>::BWD)
+      epi_bwd_ring<BN, RING>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
+                             num_tiles, n_tiles, M, N);
+    else if constexpr (RING > 0)
+      epi_fwd_ring<BN, RING>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
+                             num_tiles, n_tiles, N, K, flags);
   } else if (warp >= 4) {
     const int q = warp & 3;                      // TMEM lane quarter of this warp
     const int third = (warp - 4) >> 2;           // which 16-column chunks (mod 3)
@@ -1030,7 +1358,8 @@ static int tc_out_map(TcWeights& t, const void* base, bool bf16, int64_t rows, i
 }
 
 // which epilogues store through TMA, and their output maps (slot order as in
-// TcOutMaps); returns 1 when every output got a map
+// TcOutMaps); returns bit 1 when every output got a map, bit 2 when the
+// ring epilogue's input maps (m[4], m[5]) were built too
 template <class Epi>
 struct EpiOut {
   static int build(TcWeights&, const Epi&, int64_t, int, TcOutMaps&) { return 0; }
@@ -1060,7 +1389,11 @@ struct EpiOut<TcChain<EpiFwdHidden>> {
     if (ch.split.hi && (tc_out_map(t, ch.split.hi, true, M, N, ch.split.ld, &om.m[2]) ||
                         tc_out_map(t, ch.split.lo, true, M, N, ch.split.ld, &om.m[3])))
       return 0;
-    return 1;
+    // residual input tiles for the ring epilogue (same 32 x 16 boxes, loaded): bit 2
+    if (ch.prev.hi && (tc_out_map(t, ch.prev.hi, true, M, N, ch.prev.ld, &om.m[4]) ||
+                       tc_out_map(t, ch.prev.lo, true, M, N, ch.prev.ld, &om.m[5])))
+      return 1;
+    return 3;
   }
 };
 template <>
@@ -1072,12 +1405,79 @@ struct EpiOut<TcChain<EpiBwd>> {
     if (ch.split.hi && (tc_out_map(t, ch.split.hi, true, M, N, ch.split.ld, &om.m[2]) ||
                         tc_out_map(t, ch.split.lo, true, M, N, ch.split.ld, &om.m[3])))
       return 0;
-    return 1;
+    // ring-epilogue input tiles (dense sweeps only: no row gather): bit 2
+    if (e.rowidx || !e.D) return 1;
+    if (e.resid && tc_out_map(t, e.resid, false, M, N, e.ld, &om.m[4])) return 1;
+    if (tc_out_map(t, e.D, false, M, N, e.ldD, &om.m[5])) return 1;
+    return 3;
+  }
+};
+// the summing reverse step stores nothing through TMA: its maps are the
+// ring-epilogue inputs only (bit 2)
+template <>
+struct EpiOut<EpiBwdSum> {
+  static int build(TcWeights& t, const EpiBwdSum& e, int64_t M, int N, TcOutMaps& om) {
+    if (e.rowidx || !e.D) return 0;
+    if (e.resid && tc_out_map(t, e.resid, false, M, N, e.ld, &om.m[4])) return 0;
+    if (tc_out_map(t, e.D, false, M, N, e.ldD, &om.m[5])) return 0;
+    return 2;
   }
 };
 
 inline bool tc_gemm_supported(int64_t M, int N, int K) {
   return M >= 1 && K >= 8 && K % 8 == 0 && N >= 16 && N % 16 == 0 && tc_encode_fn() != nullptr;
+}
+
+// ring epilogue depth for the forward chain (0 = register-prefetch epilogue);
+// SDN_EPI_RING=0/2/3 overrides
+static int g_tc_ring = getenv("SDN_EPI_RING") ? atoi(getenv("SDN_EPI_RING")) : 3;
+
+template <class Epi>
+struct RingOk {
+  static bool ok(const Epi&, int) { return false; }
+};
+template <>
+struct RingOk<TcChain<EpiFwdHidden>> {
+  static bool ok(const TcChain<EpiFwdHidden>& ch, int) { return !ch.base.H && !ch.base.prev; }
+};
+template <>
+struct RingOk<TcChain<EpiBwd>> {
+  static bool ok(const TcChain<EpiBwd>& ch, int) { return !ch.base.rowidx && ch.base.D && !ch.base.U; }
+};
+template <>
+struct RingOk<EpiBwdSum> {
+  static bool ok(const EpiBwdSum& e, int) { return !e.rowidx && e.D; }
+};
+// reverse-sweep ring depth (0 = register-prefetch epilogue); SDN_BWD_RING overrides
+static int g_tc_bwd_ring = getenv("SDN_BWD_RING") ? atoi(getenv("SDN_BWD_RING")) : 2;
+
+template <int BN, class Epi, int RING>
+static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, int N, int K, const CUtensorMap& ah,
+                       const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl, const Epi& epi,
+                       const TcOutMaps& om, int use_om, TcFlags fl) {
+  using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
+  static_assert(C::STAGES >= 2 && C::SMEM <= TC_SMEM_MAX, "shared memory budget");
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr_set = true;
+  }
+  // programmatic stream serialization (PDL): the kernel may start while the
+  // previous one drains; griddepcontrol.wait orders it
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (!(g_tc_pdl && g_tc_pdl_now)) fl.in = nullptr;   // row flags only pay off with early (PDL) launch
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, RING>, ah, al, bh, bl, M, Mdev, N, K, epi,
+                                           om, use_om, g_tc_trace, fl);
+  return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -3;
 }
 
 template <int BN, class Epi>
@@ -1087,32 +1487,26 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   if (tc_map(t, A.hi, std::max<int64_t>(M, 1), K, A.ld, TC_BM, &ah) || tc_map(t, A.lo, std::max<int64_t>(M, 1), K, A.ld, TC_BM, &al) ||
       tc_map(t, B.hi, N, K, B.ld, BN, &bh) || tc_map(t, B.lo, N, K, B.ld, BN, &bl))
     return -1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<BN>::SMEM);
-    attr_set = true;
-  }
   const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
   TcOutMaps om;
   memset(&om, 0, sizeof(om));
-  const int use_om = g_tc_thread_stores ? 0 : EpiOut<Epi>::build(t, epi, std::max<int64_t>(M, 1), N, om);
-  // programmatic stream serialization (PDL): the kernel may start while the
-  // previous one drains; griddepcontrol.wait orders it
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = TcCfg<BN>::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (!(g_tc_pdl && g_tc_pdl_now)) fl.in = nullptr;   // row flags only pay off with early (PDL) launch
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ah, al, bh, bl, M, Mdev, N, K, epi, om,
-                                           use_om, g_tc_trace, fl);
-  return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -3;
+  const int ob = g_tc_thread_stores ? 0 : EpiOut<Epi>::build(t, epi, std::max<int64_t>(M, 1), N, om);
+  const int use_om = ob & 1;
+  if constexpr (std::is_same<Epi, TcChain<EpiFwdHidden>>::value) {
+    if ((ob & 2) && g_tc_ring > 0 && !g_tc_trace && RingOk<Epi>::ok(epi, N)) {
+      if (g_tc_ring == 2) return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+      return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+    }
+  }
+  if constexpr (RingKind<Epi>::BWD) {
+    if ((ob & 2) && !Mdev && g_tc_bwd_ring > 0 && !g_tc_trace && RingOk<Epi>::ok(epi, N)) {
+      if constexpr (TcCfg<BN, 3, true>::STAGES_FIT >= 2)
+        if (g_tc_bwd_ring == 3) return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+      return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+    }
+  }
+  return tc_launch_k<BN, Epi, 0>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
 }
 
 template <class Epi>

@@ -9,9 +9,9 @@ from paper_2305_20053_b200 import Engine, workloads as wl, _lib
 
 MODES = {0: "tc-null-epi", 1: "tc-fused-epi", 2: "simt-fused-epi", 3: "tc-no-D", 4: "tc-no-split", 7: "tc-no-stores", 8: "tc-chain-epi",
          5: "tc-no-residual", 6: "tc-H-only", 9: "tc-chain-identity", 10: "chain-no-D", 11: "chain-no-split",
-         12: "chain-no-prev"}
+         12: "chain-no-prev", 13: "chain-no-mma", 14: "chain-no-mma-no-tma"}
 names = [a for a in sys.argv[1:] if not a.startswith("-")] or ["c2"]
-modes = [0, 8, 9, 10, 11, 12, 1, 6, 7] + ([2] if "--simt" in sys.argv else [])
+modes = [0, 8, 13, 14, 9, 10, 11, 12] + ([2] if "--simt" in sys.argv else [])
 for name in names:
     cfg = wl.WORKLOADS[name]
     p = wl.make_problem(cfg.with_samples(256), seed=0, count=256)
