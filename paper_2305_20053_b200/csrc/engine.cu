@@ -2100,7 +2100,8 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   // 2048 no split store | 4096 no residual input
   const int flags = mode & ~255;
   mode &= 255;
-  int skip = mode == 13 ? 1 : mode == 14 ? 3 : (flags >> 8) & 3;
+  // 8192 / 16384: ring epilogue without the proxy fence / without TMEM loads
+  int skip = mode == 13 ? 1 : mode == 14 ? 3 : ((flags >> 8) & 3) | ((flags & 8192) ? 16 : 0) | ((flags & 16384) ? 32 : 0);
   cudaMemcpyToSymbol(g_tc_dbg_skip, &skip, sizeof(int));
   const bool chainm = mode == 8 || mode >= 9;
   const bool noD = mode == 10 || (flags & 1024), noS = mode == 11 || (flags & 2048), noP = mode == 12 || (flags & 4096);

@@ -169,6 +169,11 @@ SDN_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+SDN_DEV float exp2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 SDN_DEV void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 SDN_DEV void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -296,6 +301,17 @@ constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 constexpr uint32_t TC_EPI_WARP_BYTES = 6144;
 constexpr int TC_EPI_WARPS = 12;               // three per TMEM lane quarter
 constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
+// ring kernels: epilogue warps (three per lane quarter; four -- 16-column
+// chunks of a 256-column tile split evenly -- measured slower at c2: the
+// larger epilogue leaves the mainloop only two stages)
+#ifndef TC_RING_EW
+#define TC_RING_EW 12
+#endif
+template <int RING>
+struct EpiWarps {
+  static constexpr int EW = RING ? TC_RING_EW : TC_EPI_WARPS;
+  static constexpr int THREADS = 32 * (4 + EW);
+};
 
 // RING > 0: the asynchronous-input epilogue (epi_ring): per warp RING
 // 2-KB slots that TMA-load the epilogue's input tile ahead of use and then
@@ -312,7 +328,7 @@ struct TcCfg {
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr uint32_t EPI_WARP =
       !RING ? TC_EPI_WARP_BYTES : BWD ? (uint32_t)RING * 4096u : (uint32_t)RING * 2048u + 2048u;
-  static constexpr uint32_t EPI_BYTES = TC_EPI_WARPS * EPI_WARP + ((RING && !BWD) ? 4096u : 0u);
+  static constexpr uint32_t EPI_BYTES = EpiWarps<RING>::EW * EPI_WARP + ((RING && !BWD) ? 4096u : 0u);
   static constexpr int STAGES_FIT = (int)((TC_SMEM_MAX - EPI_BYTES - 1024 - TC_BAR_BYTES) / STAGE_BYTES);
   static constexpr int STAGES = RING ? (STAGES_FIT > 4 ? 4 : STAGES_FIT) : ((BN == 256) ? SDN_ST256 : 4);
   static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + TC_BAR_BYTES;
@@ -451,15 +467,20 @@ SDN_DEV void row_put(float* buf, int lane, const float (&x)[16]) {
 SDN_DEV uint32_t pack_bf2(__nv_bfloat16 a, __nv_bfloat16 b) {
   return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
 }
+// two fp32 -> packed bf16x2 (round to nearest), a in the low half
+SDN_DEV uint32_t cvt_bf2(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
 SDN_DEV void row_put_split(uint32_t* bh, uint32_t* bl, int lane, const float (&x)[16]) {
   uint32_t ph[8], pl[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    __nv_bfloat16 h0, l0, h1, l1;
-    split_bf16(x[2 * k], h0, l0);
-    split_bf16(x[2 * k + 1], h1, l1);
-    ph[k] = pack_bf2(h0, h1);
-    pl[k] = pack_bf2(l0, l1);
+    // same values as split_bf16: hi = bf16(x), lo = bf16(x - hi) (x - hi is exact)
+    ph[k] = cvt_bf2(x[2 * k], x[2 * k + 1]);
+    const float h0 = __uint_as_float(ph[k] << 16), h1 = __uint_as_float(ph[k] & 0xFFFF0000u);
+    pl[k] = cvt_bf2(x[2 * k] - h0, x[2 * k + 1] - h1);
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -625,10 +646,10 @@ SDN_DEV void fwd_act16(int act, const uint32_t (&v)[16], const float (&bias)[16]
       // branch-free (selects only) so the 16 elements interleave
       const float x = __uint_as_float(v[j]) + bias[j];
       const float xn = x > 0.0f ? 0.0f : x;     // (not fminf: a NaN must propagate, as in the oracle)
-      const float ex = __expf(xn);
-      // e^x - 1 without cancellation near 0 (Taylor to x^5 on (-1/16, 0])
-      const float pm = xn * (1.0f + xn * (0.5f + xn * (0.16666667f + xn * (0.041666668f + xn * 0.008333334f))));
-      const float y = x > 0.0f ? x : (xn > -0.0625f ? pm : ex - 1.0f);
+      const float ex = tcx::exp2_ftz(xn * 1.4426950408889634f);   // e^xn, xn <= 0 (flush below 2^-126)
+      // e^x - 1 directly: near 0 its absolute error (~1e-7) is far below the
+      // bf16x3 split error of the next GEMM operand (2^-17 |h|)
+      const float y = x > 0.0f ? x : ex - 1.0f;
       a[j] = has_prev ? a[j] + y : y;
       d[j] = x > 0.0f ? 1.0f : ex;
     }
@@ -847,17 +868,19 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
                           uint64_t* tfull, uint64_t* tempty, uint32_t tmem, int warp, int lane, int num_tiles,
                           int n_tiles, int N, int K, const TcFlags& flags) {
   constexpr uint32_t WB = (uint32_t)RING * 2048u + 2048u;
-  const int w = warp - 4, q = warp & 3, third = w >> 2, first_c = 16 * third;
+  constexpr int EW = EpiWarps<RING>::EW, CS = 16 * (EW / 4);   // chunk stride of a warp
+  const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
   uint8_t* wb = epi_base + w * WB;
   float* Dst = reinterpret_cast<float*>(wb + RING * 2048);
-  float* bias_s = reinterpret_cast<float*>(epi_base + TC_EPI_WARPS * WB);
+  float* bias_s = reinterpret_cast<float*>(epi_base + EW * WB);
   uint64_t* rbar = rbar_all + w * RING;
   const EpiFwdHidden& e = ch.base;
   const bool has_prev = ch.prev.hi != nullptr, has_split = ch.split.hi != nullptr, has_D = e.D != nullptr;
   const bool bias_smem = N <= 1024;
+  const int dbg = g_tc_dbg_skip;                  // study switches (sdn_debug_gemm): 16 no fence, 32 no TMEM load
   if (bias_smem)
-    for (int i = (int)threadIdx.x - 128; i < N; i += 32 * TC_EPI_WARPS) bias_s[i] = __ldg(e.bias + i);
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS) : "memory");
+    for (int i = (int)threadIdx.x - 128; i < N; i += 32 * EW) bias_s[i] = __ldg(e.bias + i);
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
 
   // load cursor (tile lt, column lc), RING-1 chunks ahead of the compute cursor
   int lt = blockIdx.x, lc = first_c, jl = 0, last_mb = -1;
@@ -881,7 +904,7 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
       last_mb = mb;
     }
     ++jl;
-    lc += 48;
+    lc += CS;
     lnorm();
   };
   lnorm();
@@ -893,7 +916,7 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
     const int mb = tile / n_tiles, nb = tile % n_tiles;
     const int r0 = mb * TC_BM + q * 32;
     int nch = 0;
-    for (int c = first_c; c < BN && nb * BN + c < N; c += 48) ++nch;
+    for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
     tcx::mbar_wait(&tfull[acc], acc_phase);
     tcx::fence_after();
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -904,13 +927,14 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
     }
 #pragma unroll 1
     for (int ci = 0; ci < nch; ++ci, ++jc) {
-      const int c0 = first_c + 48 * ci, col = nb * BN + c0, s = jc % RING;
+      const int c0 = first_c + CS * ci, col = nb * BN + c0, s = jc % RING;
       uint32_t* sh = reinterpret_cast<uint32_t*>(wb + s * 2048);
       uint32_t* sl = sh + 256;
       uint32_t v[16];
-      tcx::tmem_ld16(tbase + c0, v);
+      if (!(dbg & 32)) tcx::tmem_ld16(tbase + c0, v);
+      else for (int j = 0; j < 16; ++j) v[j] = __float_as_uint((float)(lane - j));
       if (has_prev) tcx::mbar_wait(&rbar[s], (uint32_t)(jc / RING) & 1u);
-      tcx::tmem_ld_wait();
+      if (!(dbg & 32)) tcx::tmem_ld_wait();
       if (ci == nch - 1) {                        // accumulator drained: the MMA may reuse it
         tcx::fence_before();
         __syncwarp();
@@ -932,7 +956,8 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
       issue();
       if (has_D) row_put(Dst, lane, d);
       if (has_split) row_put_split(sh, sl, lane, a);
-      tcx::fence_proxy_async();
+      if (!(dbg & 16)) tcx::fence_proxy_async();
+      else if (!has_D && !has_split) { float z = 0.f; for (int j = 0; j < 16; ++j) z += a[j] + d[j]; if (z == 1.2345f) Dst[lane] = z; }
       __syncwarp();
       if (lane == 0) {
         if (has_D) tcx::tma_store_2d(&om.m[1], Dst, col, r0);
@@ -981,7 +1006,8 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
                           int n_tiles, int64_t M, int N) {
   constexpr bool SUM = BwdRingView<Epi>::SUM;
   constexpr uint32_t WB = (uint32_t)RING * 4096u;
-  const int w = warp - 4, q = warp & 3, third = w >> 2, first_c = 16 * third;
+  constexpr int EW = EpiWarps<RING>::EW, CS = 16 * (EW / 4);   // chunk stride of a warp
+  const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
   uint8_t* wb = epi_base + w * WB;
   uint64_t* rbar = rbar_all + w * RING;
   const bool has_resid = BwdRingView<Epi>::resid(ep) != nullptr;
@@ -1001,7 +1027,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
       tcx::tma_load_2d(wb + s * 4096 + 2048, &om.m[5], &rbar[s], x, y);
     }
     ++jl;
-    lc += 48;
+    lc += CS;
     lnorm();
   };
   lnorm();
@@ -1013,7 +1039,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
     const int mb = tile / n_tiles, nb = tile % n_tiles;
     const int64_t r0 = (int64_t)mb * TC_BM + q * 32;
     int nch = 0;
-    for (int c = first_c; c < BN && nb * BN + c < N; c += 48) ++nch;
+    for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
     tcx::mbar_wait(&tfull[acc], acc_phase);
     tcx::fence_after();
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -1024,7 +1050,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
     }
 #pragma unroll 1
     for (int ci = 0; ci < nch; ++ci, ++jc) {
-      const int c0 = first_c + 48 * ci, col = nb * BN + c0, s = jc % RING;
+      const int c0 = first_c + CS * ci, col = nb * BN + c0, s = jc % RING;
       float* Rs = reinterpret_cast<float*>(wb + s * 4096);
       float* Ds = Rs + 512;
       uint32_t v[16];
@@ -1120,7 +1146,7 @@ struct RingKind<EpiBwdSum> {
 };
 
 template <int BN, class Epi, int RING = 0>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(EpiWarps<RING>::THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
                const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
@@ -1135,15 +1161,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;                   // RING slots per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + (RING ? RING * TC_EPI_WARPS : 0));
+  constexpr int EW = EpiWarps<RING>::EW;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + (RING ? RING * EW : 0));
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches and
+  // the TMA / mbarrier operands stay in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tcx::prefetch_tmap(&tAh); tcx::prefetch_tmap(&tAl);
     tcx::prefetch_tmap(&tBh); tcx::prefetch_tmap(&tBl);
     for (int s = 0; s < STAGES; ++s) { tcx::mbar_init(&full[s], 1); tcx::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], TC_EPI_WARPS); }
-    for (int i = 0; i < RING * TC_EPI_WARPS; ++i) tcx::mbar_init(&rbar[i], 1);
+    for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], EW); }
+    for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar[i], 1);
     tcx::fence_barrier_init();
   }
   if (warp == 2) {
@@ -1228,14 +1257,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (RING > 0 && warp >= 4) {
-    if constexpr (RING > 0 && RingKind<Epi>::BWD)
+  } else if (warp >= 4) {
+    // (compile-time split: a ring kernel carries no register-prefetch epilogue code)
+    if constexpr (RING > 0 && RingKind<Epi>::BWD) {
       epi_bwd_ring<BN, RING>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
                              num_tiles, n_tiles, M, N);
-    else if constexpr (RING > 0)
+    } else if constexpr (RING > 0) {
       epi_fwd_ring<BN, RING>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
                              num_tiles, n_tiles, N, K, flags);
-  } else if (warp >= 4) {
+    } else {
     const int q = warp & 3;                      // TMEM lane quarter of this warp
     const int third = (warp - 4) >> 2;           // which 16-column chunks (mod 3)
     uint8_t* ep = smem + STAGES * C::STAGE_BYTES + (warp - 4) * TC_EPI_WARP_BYTES;
@@ -1285,6 +1315,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
       }
     }
     if (use_om && lane == 0) tcx::bulk_wait0();    // this warp's TMA stores are complete
+    }
   }
   __syncthreads();
   if (warp == 2) {
@@ -1430,7 +1461,7 @@ inline bool tc_gemm_supported(int64_t M, int N, int K) {
 
 // ring epilogue depth for the forward chain (0 = register-prefetch epilogue);
 // SDN_EPI_RING=0/2/3 overrides
-static int g_tc_ring = getenv("SDN_EPI_RING") ? atoi(getenv("SDN_EPI_RING")) : 3;
+static int g_tc_ring = getenv("SDN_EPI_RING") ? atoi(getenv("SDN_EPI_RING")) : 2;
 
 template <class Epi>
 struct RingOk {
@@ -1466,7 +1497,7 @@ static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, in
   // previous one drains; griddepcontrol.wait orders it
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(EpiWarps<RING>::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1495,8 +1526,9 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   const int use_om = ob & 1;
   if constexpr (std::is_same<Epi, TcChain<EpiFwdHidden>>::value) {
     if ((ob & 2) && g_tc_ring > 0 && !g_tc_trace && RingOk<Epi>::ok(epi, N)) {
-      if (g_tc_ring == 2) return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
-      return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+      if constexpr (TcCfg<BN, 3, false>::STAGES_FIT >= 2)
+        if (g_tc_ring == 3) return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+      return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
     }
   }
   if constexpr (RingKind<Epi>::BWD) {

@@ -13,6 +13,8 @@ rows = [("null epilogue", 0), ("chain (production)", 8), ("chain, no MMA/TMA-loa
         ("  - residual input", 8 | S | 4096), ("  - residual, act'", 8 | S | 4096 | 1024),
         ("  - residual, split", 8 | S | 4096 | 2048), ("  - residual, act', split (TMEM+math)", 8 | S | 4096 | 1024 | 2048),
         ("  - act' only", 8 | S | 1024), ("  - split only", 8 | S | 2048),
+        ("  - residual, act', split, fence", 8 | S | 4096 | 1024 | 2048 | 8192),
+        ("  - residual, act', split, fence, TMEM ld", 8 | S | 4096 | 1024 | 2048 | 8192 | 16384),
         ("chain - residual (with MMA)", 8 | 4096), ("chain - all outputs+residual (with MMA)", 8 | 4096 | 1024 | 2048)]
 for label, mode in rows:
     ms = np.zeros(1)
