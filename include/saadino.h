@@ -246,6 +246,11 @@ int sdn_profile(sdn_handle* h, int32_t enable);
 int sdn_profile_read(sdn_handle* h, int32_t n_cls, double* ms, double* flops, double* bytes,
                      int64_t* count);
 
+/* Device time (CUDA events on the handle's stream, ms) of the last
+ * sdn_eval_multi: from its first enqueued operation to its last (graph
+ * replay included), host staging and result post-processing excluded. */
+int sdn_last_device_ms(sdn_handle* h, double* ms);
+
 /* Kernel tuning: average ms of one layer-1 forward GEMM over M rows
  * (mode 0 tcgen05 + null epilogue, 1 tcgen05 + fused epilogue, 2 SIMT). */
 int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t reps, double* ms);

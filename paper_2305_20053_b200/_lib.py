@@ -87,6 +87,7 @@ SIGNATURES = {
     "sdn_profile": (C.c_int, [_P, C.c_int32]),
     "sdn_debug_gemm": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _D]),
     "sdn_profile_read": (C.c_int, [_P, C.c_int32, _D, _D, _D, _I64]),
+    "sdn_last_device_ms": (C.c_int, [_P, _D]),
 }
 
 

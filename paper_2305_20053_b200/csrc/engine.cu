@@ -244,6 +244,8 @@ struct sdn_handle {
   // CUDA graph of the last evaluation configuration (sdn_eval_multi)
   bool use_graphs = true;       // env SDN_NO_GRAPH=1 disables
   cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t dev_ev[2] = {nullptr, nullptr};   // device span of the last sdn_eval_multi
+  double last_dev_ms = 0.0;
   std::vector<double> gkey;
   int64_t glaunches = 0;
   int64_t gen = 0;              // bumped by every set_* call (invalidates the graph)
@@ -684,6 +686,8 @@ int sdn_destroy(sdn_handle* h) {
   if (!h) return SDN_OK;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  for (cudaEvent_t e : h->dev_ev)
+    if (e) cudaEventDestroy(e);
   for (void* p : h->allocs) cudaFree(p);
   if (h->U) cudaFree(h->U);
   if (h->ub) cudaFree(h->ub);
@@ -1476,6 +1480,10 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     h->band_cap = n_risks + 1;
   }
   TRY(ensure_xsel(h, n_exact));
+  if (!h->dev_ev[0]) {
+    CU(cudaEventCreate(&h->dev_ev[0]));
+    CU(cudaEventCreate(&h->dev_ev[1]));
+  }
   if (dense && n_exact > 0) TRY(ensure_side(h));
   TRY(ensure_sweep(h, *h->sw, n_risks));
   // graph path (z and every risk's t are per-call graph parameters, staged
@@ -1509,12 +1517,20 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       h->fwd_done = true;
       h->qr_valid = n_exact > 0;
     }
+    CU(cudaEventRecord(h->dev_ev[0], h->stream));
     CU(cudaGraphLaunch(h->gexec, h->stream));
+    CU(cudaEventRecord(h->dev_ev[1], h->stream));
     h->launches += h->glaunches;
   } else {
+    CU(cudaEventRecord(h->dev_ev[0], h->stream));
     TRY(enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0));
+    CU(cudaEventRecord(h->dev_ev[1], h->stream));
   }
   CU(cudaStreamSynchronize(h->stream));
+  {
+    float t = 0.f;
+    h->last_dev_ms = cudaEventElapsedTime(&t, h->dev_ev[0], h->dev_ev[1]) == cudaSuccess ? (double)t : -1.0;
+  }
   for (int i = 0; i < n_risks; ++i) {
     TRY(finish_host(h, risks[i], h->hstats, h->hpart_multi + (size_t)i * plen, &res[i],
                     grads ? grads + (size_t)i * h->d_z : nullptr));
@@ -1522,6 +1538,12 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   }
   if (cvar_idx)
     for (int64_t j = 0; j < ktot; ++j) cvar_idx[j] = h->goff + h->hidx[j];
+  return SDN_OK;
+}
+
+int sdn_last_device_ms(sdn_handle* h, double* ms) {
+  if (!h || !ms) return fail(SDN_ERR_ARG, "null argument");
+  *ms = h->last_dev_ms;
   return SDN_OK;
 }
 
@@ -2112,8 +2134,27 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
                            TcEpiSplit{(chainm && h->res[1] && !noP) ? &h->tcw.act[0] : nullptr}};
   h->tcw.act[0].rows = M;
   int rc = 0;
+  // 20 / 21: the dense reverse-sweep chain step (layer 2) / the summing last
+  // step (layer 1) on the sweep buffers of a previous evaluation (flags as above:
+  // 1024 no G store, 2048 no split store, 4096 no residual-gradient input)
+  if ((mode == 20 || mode == 21) && (!h->sw || h->sw->rows < M || h->sw->planes < 1 || h->L < 4))
+    return fail(SDN_ERR_STATE, "debug reverse GEMM: run a multi-risk evaluation first (L >= 4)");
   for (int it = 0; it <= reps && rc == 0; ++it) {
     if (it == 1) cudaEventRecord(a, h->stream);
+    if (mode == 20) {
+      SweepBufs& sw = *h->sw;
+      EpiBwd e{noP ? nullptr : sw.G, noD ? nullptr : sw.G, h->D[1], (int64_t)h->w[2], nullptr, nullptr, (int64_t)h->w[2]};
+      TcChain<EpiBwd> cb{e, TcEpiSplit{noS ? nullptr : &sw.act[1]}};
+      rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, h->w[2], h->w[3], sw.act[0], h->tcw.bwd[2], cb);
+      continue;
+    }
+    if (mode == 21) {
+      SweepBufs& sw = *h->sw;
+      EpiBwdSum e{noP ? nullptr : sw.G, h->D[0], (int64_t)h->w[1], nullptr, (int64_t)h->w[1], sw.tsum, (int64_t)h->w[1]};
+      e.W = sw.W; e.R = sw.planes; e.plane = cdiv(sw.rows, 128) * 4 * h->maxw;
+      rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, h->w[1], h->w[2], sw.act[0], h->tcw.bwd[1], e);
+      continue;
+    }
     if (mode == 0) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], EpiNull{});
     else if (mode != 2) rc = tc_gemm(h->tcw, h->stream, h->num_sms, M, nullptr, N, K, h->tcw.act[0], h->tcw.fwd[1], ch);
     else { launch_simt<128, 128, 8, 8, false, true>(h, M, nullptr, N, K, h->H[0], K, h->W[1], K, ch, true); }

@@ -307,9 +307,12 @@ constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
 #ifndef TC_RING_EW
 #define TC_RING_EW 12
 #endif
-template <int RING>
+#ifndef TC_RING_EW_BWD
+#define TC_RING_EW_BWD 8
+#endif
+template <int RING, bool BWD = false>
 struct EpiWarps {
-  static constexpr int EW = RING ? TC_RING_EW : TC_EPI_WARPS;
+  static constexpr int EW = !RING ? TC_EPI_WARPS : BWD ? TC_RING_EW_BWD : TC_RING_EW;
   static constexpr int THREADS = 32 * (4 + EW);
 };
 
@@ -328,7 +331,7 @@ struct TcCfg {
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr uint32_t EPI_WARP =
       !RING ? TC_EPI_WARP_BYTES : BWD ? (uint32_t)RING * 4096u : (uint32_t)RING * 2048u + 2048u;
-  static constexpr uint32_t EPI_BYTES = EpiWarps<RING>::EW * EPI_WARP + ((RING && !BWD) ? 4096u : 0u);
+  static constexpr uint32_t EPI_BYTES = EpiWarps<RING, BWD>::EW * EPI_WARP + ((RING && !BWD) ? 4096u : 0u);
   static constexpr int STAGES_FIT = (int)((TC_SMEM_MAX - EPI_BYTES - 1024 - TC_BAR_BYTES) / STAGE_BYTES);
   static constexpr int STAGES = RING ? (STAGES_FIT > 4 ? 4 : STAGES_FIT) : ((BN == 256) ? SDN_ST256 : 4);
   static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + TC_BAR_BYTES;
@@ -1006,7 +1009,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
                           int n_tiles, int64_t M, int N) {
   constexpr bool SUM = BwdRingView<Epi>::SUM;
   constexpr uint32_t WB = (uint32_t)RING * 4096u;
-  constexpr int EW = EpiWarps<RING>::EW, CS = 16 * (EW / 4);   // chunk stride of a warp
+  constexpr int EW = EpiWarps<RING, true>::EW, CS = 16 * (EW / 4);   // chunk stride of a warp
   const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
   uint8_t* wb = epi_base + w * WB;
   uint64_t* rbar = rbar_all + w * RING;
@@ -1146,7 +1149,7 @@ struct RingKind<EpiBwdSum> {
 };
 
 template <int BN, class Epi, int RING = 0>
-__global__ void __launch_bounds__(EpiWarps<RING>::THREADS, 1)
+__global__ void __launch_bounds__((EpiWarps<RING, RingKind<Epi>::BWD>::THREADS), 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
                const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
                const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
@@ -1161,7 +1164,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;                   // RING slots per epilogue warp
-  constexpr int EW = EpiWarps<RING>::EW;
+  constexpr int EW = EpiWarps<RING, RingKind<Epi>::BWD>::EW;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + (RING ? RING * EW : 0));
 
   // warp index through a shuffle: provably warp-uniform, so role branches and
@@ -1497,7 +1500,7 @@ static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, in
   // previous one drains; griddepcontrol.wait orders it
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(EpiWarps<RING>::THREADS);
+  cfg.blockDim = dim3(EpiWarps<RING, RingKind<Epi>::BWD>::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1540,6 +1543,7 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   }
   return tc_launch_k<BN, Epi, 0>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
 }
+
 
 template <class Epi>
 static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const int* Mdev, int N, int K,

@@ -325,6 +325,12 @@ class Engine:
     def profile(self, enable: bool = True):
         check(lib.sdn_profile(self.h, int(bool(enable))), "sdn_profile")
 
+    def last_device_ms(self) -> float:
+        """Device time (CUDA events on the handle's stream) of the last eval_multi."""
+        ms = np.zeros(1)
+        check(lib.sdn_last_device_ms(self.h, dptr(ms)), "sdn_last_device_ms")
+        return float(ms[0])
+
     def profile_read(self) -> dict:
         n = len(_lib.PROF_CLASSES)
         ms, fl, by = np.zeros(n), np.zeros(n), np.zeros(n)
