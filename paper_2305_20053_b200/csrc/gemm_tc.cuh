@@ -1554,6 +1554,11 @@ static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const 
   static const int bn_force = getenv("SDN_TC_BN") ? atoi(getenv("SDN_TC_BN")) : 0;   // tuning override
   if (bn_force == 64) return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
   if (bn_force == 128) return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
+  // dense reverse-sweep ring GEMMs: 128-column tiles leave the mainloop four
+  // stages next to the 4-KB-slot epilogue ring (256: two); measured faster at c2
+  if constexpr (RingKind<Epi>::BWD)
+    if (!Mdev && !bn_force && N > 128 && mt * ((N + 127) / 128) >= num_sms && g_tc_bwd_ring > 0)
+      return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
   if (N > 128 && mt * ((N + 255) / 256) >= num_sms / 2)
     return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
   if (N > 64 && mt * ((N + 127) / 128) >= num_sms / 4)
