@@ -564,8 +564,12 @@ struct TileEpi<EpiNull> {
 // output layer: phi = shift + scale * (acc + bias)
 template <>
 struct TileEpi<EpiAffine> {
-  using Pre = PreAff;
-  static SDN_DEV void load(const EpiAffine& e, const TileRows&, int c0, int N, int, Pre& p) {
+  // the folded bias / scale are read at use (lane-uniform, L1-resident): a
+  // prefetched load still in flight at the proxy fence before the TMA stores
+  // would be waited on there (MEMBAR), serialising every chunk on a global latency
+  using Pre = PreNone;
+  static SDN_DEV void load(const EpiAffine&, const TileRows&, int, int, int, Pre&) {}
+  static SDN_DEV void fold(const EpiAffine& e, int c0, int N, PreAff& p) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f), o = make_float4(1.f, 1.f, 1.f, 1.f);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -578,7 +582,9 @@ struct TileEpi<EpiAffine> {
     }
   }
   static SDN_DEV void chunk(const EpiAffine& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const Pre& pre) {
+                            const uint32_t (&v)[16], const Pre&) {
+    PreAff pre;
+    fold(e, c0, N, pre);
     float x[16];
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
@@ -602,12 +608,12 @@ struct TileEpi<EpiAffine> {
 
 template <>
 struct TileEpi<EpiAffineSeed> {
-  using Pre = PreAff;
-  static SDN_DEV void load(const EpiAffineSeed& e, const TileRows& tr, int c0, int N, int lane, Pre& p) {
-    TileEpi<EpiAffine>::load(e.base, tr, c0, N, lane, p);
-  }
+  using Pre = PreNone;
+  static SDN_DEV void load(const EpiAffineSeed&, const TileRows&, int, int, int, Pre&) {}
   static SDN_DEV void chunk(const EpiAffineSeed& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
-                            const uint32_t (&v)[16], const Pre& pre) {
+                            const uint32_t (&v)[16], const Pre&) {
+    PreAff pre;
+    TileEpi<EpiAffine>::fold(e.base, c0, N, pre);
     float x[16], sd[16];
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
