@@ -1049,6 +1049,15 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
     const int64_t r0 = (int64_t)mb * TC_BM + q * 32;
     int nch = 0;
     for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
+    // summing step: this lane's row weights (up to 4 risks) once per tile, not per chunk
+    double wreg[4] = {0.0, 0.0, 0.0, 0.0};
+    if constexpr (SUM) {
+      const EpiBwdSum& e = ep;
+      if (e.W && r0 + lane < M)
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+          if (qq < e.R) wreg[qq] = e.W[(r0 + lane) * e.R + qq];
+    }
     tcx::mbar_wait(&tfull[acc], acc_phase);
     tcx::fence_after();
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -1089,8 +1098,12 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
         __syncwarp();
         row_put(Ds, lane, dd);
         double* ws = reinterpret_cast<double*>(Rs);   // per-row risk weights (fp64)
-        if (e.W)
-          for (int qq = 0; qq < e.R; ++qq) ws[qq * 32 + lane] = live ? e.W[(r0 + lane) * e.R + qq] : 0.0;
+        if (e.W) {
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            if (qq < e.R) ws[qq * 32 + lane] = wreg[qq];
+          for (int qq = 4; qq < e.R; ++qq) ws[qq * 32 + lane] = live ? e.W[(r0 + lane) * e.R + qq] : 0.0;
+        }
         __syncwarp();
         const int64_t prow = (r0 >> 7) * 4 + ((r0 >> 5) & 3);
         const int j = lane & 15;
