@@ -2122,8 +2122,18 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   // 2048 no split store | 4096 no residual input
   const int flags = mode & ~255;
   mode &= 255;
-  // 8192 / 16384: ring epilogue without the proxy fence / without TMEM loads
-  int skip = mode == 13 ? 1 : mode == 14 ? 3 : ((flags >> 8) & 3) | ((flags & 8192) ? 16 : 0) | ((flags & 16384) ? 32 : 0);
+  // 8192 / 16384: ring epilogue without the proxy fence / without TMEM loads;
+  // SDN_EPI_TRACE: ring-epilogue phase stamps of one warp printed after the timing
+  // 32768: the mainloop TMA-loads only the hi halves (timing study; results wrong)
+  int skip = mode == 13 ? 1 : mode == 14 ? 3 : ((flags >> 8) & 3) | ((flags & 8192) ? 16 : 0) | ((flags & 16384) ? 32 : 0) |
+             ((flags & 32768) ? 128 : 0);
+  unsigned long long* eptr = nullptr;
+  if (getenv("SDN_EPI_TRACE")) {
+    cudaMalloc(&eptr, 96 * sizeof(unsigned long long));
+    cudaMemset(eptr, 0, 96 * sizeof(unsigned long long));
+    cudaMemcpyToSymbol(g_tc_eptr, &eptr, sizeof(eptr));
+    skip |= 64;
+  }
   cudaMemcpyToSymbol(g_tc_dbg_skip, &skip, sizeof(int));
   const bool chainm = mode == 8 || mode >= 9;
   const bool noD = mode == 10 || (flags & 1024), noS = mode == 11 || (flags & 2048), noP = mode == 12 || (flags & 4096);
@@ -2183,6 +2193,18 @@ extern "C" int sdn_debug_gemm(sdn_handle* h, int64_t M, int32_t mode, int32_t re
   }
   skip = 0;
   cudaMemcpyToSymbol(g_tc_dbg_skip, &skip, sizeof(int));
+  if (eptr) {
+    unsigned long long et[96];
+    cudaMemcpy(et, eptr, sizeof(et), cudaMemcpyDeviceToHost);
+    cudaFree(eptr);
+    fprintf(stderr, "ring epilogue phases (cycles from chunk start: rbar, tmem, math, reclaim, issue, staged+fenced, stored)\n");
+    for (int c = 0; c < 12; ++c) {
+      if (!et[c * 8]) continue;
+      fprintf(stderr, "  tile %d chunk %d @%lld:", c / 6, c % 6, (long long)(et[c * 8] - et[0]));
+      for (int k = 1; k < 8; ++k) fprintf(stderr, " %lld", (long long)(et[c * 8 + k] - et[c * 8]));
+      fprintf(stderr, "\n");
+    }
+  }
   float t = 0.f;
   cudaEventElapsedTime(&t, a, b);
   cudaEventDestroy(a);

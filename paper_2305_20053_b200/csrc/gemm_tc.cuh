@@ -185,6 +185,21 @@ SDN_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// 3-D variants: the split operands keep hi and lo in one allocation (lo at a
+// fixed offset), a 3rd box dimension of 2 moves both halves in one instruction
+SDN_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+SDN_DEV void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
 // TMA store smem tile -> global (bulk-group completion); the staging layout
 // must match the map's swizzle (64B for 16 fp32, 32B for 16 bf16 per row)
 SDN_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
@@ -295,6 +310,9 @@ static bool g_tc_pdl = getenv("SDN_NO_PDL") == nullptr;
 static bool g_tc_pdl_now = true;      // cleared by the engine while side-stream work needs free SMs
 // sdn_debug_gemm study switch (device): bit 0 skips the MMAs, bit 1 also the TMA loads
 __device__ int g_tc_dbg_skip = 0;
+// ring-epilogue phase trace (sdn_debug_gemm, SDN_EPI_TRACE): CTA 0 / warp 4 /
+// lane 0, first two tiles, six chunks each, eight stamps per chunk
+__device__ unsigned long long* g_tc_eptr = nullptr;
 constexpr int TC_BK = 32;   // 32 bf16 = one 64-byte swizzle row (3-4 deep ring)
 
 // per epilogue warp: two fp32 32x16 tiles + two bf16 32x16 tiles (6 KB)
@@ -513,8 +531,7 @@ SDN_DEV void epi_issue(const EpiSmem& s, int lane, int64_t r0, int c0, bool s0, 
   if (lane == 0) {
     if (s0) tcx::tma_store_2d(&s.om->m[0], s.f0, c0, (int)r0);
     if (s1) tcx::tma_store_2d(&s.om->m[1], s.f1, c0, (int)r0);
-    if (s2) tcx::tma_store_2d(&s.om->m[2], s.h, c0, (int)r0);
-    if (s3) tcx::tma_store_2d(&s.om->m[3], s.l, c0, (int)r0);
+    if (s2 || s3) tcx::tma_store_3d(&s.om->m[2], s.h, c0, (int)r0, 0);   // hi and lo (s.l = s.h + 1 KB)
     tcx::bulk_commit();
   }
 }
@@ -887,6 +904,9 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
   const bool has_prev = ch.prev.hi != nullptr, has_split = ch.split.hi != nullptr, has_D = e.D != nullptr;
   const bool bias_smem = N <= 1024;
   const int dbg = g_tc_dbg_skip;                  // study switches (sdn_debug_gemm): 16 no fence, 32 no TMEM load
+  unsigned long long* etr = (dbg & 64) && blockIdx.x == 0 && warp == 4 && lane == 0 ? g_tc_eptr : nullptr;
+  int ti = 0;
+#define EPI_STAMP(k) if (etr && ti < 2 && ci < 6) etr[(ti * 6 + ci) * 8 + (k)] = clock64()
   if (bias_smem)
     for (int i = (int)threadIdx.x - 128; i < N; i += 32 * EW) bias_s[i] = __ldg(e.bias + i);
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
@@ -907,8 +927,7 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
         }
         tcx::mbar_expect_tx(&rbar[s], 2048);
         const int x = (lt % n_tiles) * BN + lc, y = mb * TC_BM + q * 32;
-        tcx::tma_load_2d(wb + s * 2048, &om.m[4], &rbar[s], x, y);
-        tcx::tma_load_2d(wb + s * 2048 + 1024, &om.m[5], &rbar[s], x, y);
+        tcx::tma_load_3d(wb + s * 2048, &om.m[4], &rbar[s], x, y, 0);   // hi then lo (+1 KB)
       }
       last_mb = mb;
     }
@@ -940,10 +959,13 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
       uint32_t* sh = reinterpret_cast<uint32_t*>(wb + s * 2048);
       uint32_t* sl = sh + 256;
       uint32_t v[16];
+      EPI_STAMP(0);
       if (!(dbg & 32)) tcx::tmem_ld16(tbase + c0, v);
       else for (int j = 0; j < 16; ++j) v[j] = __float_as_uint((float)(lane - j));
       if (has_prev) tcx::mbar_wait(&rbar[s], (uint32_t)(jc / RING) & 1u);
+      EPI_STAMP(1);
       if (!(dbg & 32)) tcx::tmem_ld_wait();
+      EPI_STAMP(2);
       if (ci == nch - 1) {                        // accumulator drained: the MMA may reuse it
         tcx::fence_before();
         __syncwarp();
@@ -958,25 +980,30 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
         bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
       }
       fwd_act16(e.act, v, bias, has_prev, a, d);
+      EPI_STAMP(3);
       // the previous chunk's stores have read the output tile and its slot:
       // refill that slot RING-1 chunks ahead
       if (lane == 0) tcx::bulk_wait_read0();
       __syncwarp();
+      EPI_STAMP(4);
       issue();
+      EPI_STAMP(5);
       if (has_D) row_put(Dst, lane, d);
       if (has_split) row_put_split(sh, sl, lane, a);
       if (!(dbg & 16)) tcx::fence_proxy_async();
       else if (!has_D && !has_split) { float z = 0.f; for (int j = 0; j < 16; ++j) z += a[j] + d[j]; if (z == 1.2345f) Dst[lane] = z; }
       __syncwarp();
+      EPI_STAMP(6);
       if (lane == 0) {
         if (has_D) tcx::tma_store_2d(&om.m[1], Dst, col, r0);
         if (has_split) {
-          tcx::tma_store_2d(&om.m[2], sh, col, r0);
-          tcx::tma_store_2d(&om.m[3], sl, col, r0);
+          tcx::tma_store_3d(&om.m[2], sh, col, r0, 0);                  // hi, lo (sl = sh + 1 KB)
         }
         tcx::bulk_commit();
       }
+      EPI_STAMP(7);
     }
+    ++ti;
     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     if (flags.out) {                              // publish this warp's part of the row block
       __syncwarp();
@@ -988,6 +1015,7 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
     }
   }
   if (lane == 0) tcx::bulk_wait0();
+#undef EPI_STAMP
 }
 
 // asynchronous-input epilogue for the dense reverse sweep (no row gather):
@@ -1142,8 +1170,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
         if (lane == 0) {
           if (has_G) tcx::tma_store_2d(&om.m[0], Rs, col, (int)r0);
           if (has_split) {
-            tcx::tma_store_2d(&om.m[2], sh, col, (int)r0);
-            tcx::tma_store_2d(&om.m[3], sh + 256, col, (int)r0);
+            tcx::tma_store_3d(&om.m[2], sh, col, (int)r0, 0);           // hi, lo (+1 KB)
           }
           tcx::bulk_commit();
         }
@@ -1169,8 +1196,7 @@ struct RingKind<EpiBwdSum> {
 
 template <int BN, class Epi, int RING = 0>
 __global__ void __launch_bounds__((EpiWarps<RING, RingKind<Epi>::BWD>::THREADS), 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
-               const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl, int64_t M,
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, int64_t M,
                const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
                int use_om, unsigned long long* __restrict__ trace = nullptr, TcFlags flags = TcFlags{}) {
   using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
@@ -1190,8 +1216,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
   // the TMA / mbarrier operands stay in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    tcx::prefetch_tmap(&tAh); tcx::prefetch_tmap(&tAl);
-    tcx::prefetch_tmap(&tBh); tcx::prefetch_tmap(&tBl);
+    tcx::prefetch_tmap(&tA);
+    tcx::prefetch_tmap(&tB);
     for (int s = 0; s < STAGES; ++s) { tcx::mbar_init(&full[s], 1); tcx::mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], EW); }
     for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar[i], 1);
@@ -1239,10 +1265,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ 
             continue;
           }
           tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tcx::tma_load_2d(st, &tAh, &full[stage], kb * TC_BK, mb * TC_BM);
-          tcx::tma_load_2d(st + C::A_BYTES, &tAl, &full[stage], kb * TC_BK, mb * TC_BM);
-          tcx::tma_load_2d(st + 2 * C::A_BYTES, &tBh, &full[stage], kb * TC_BK, nb * BN);
-          tcx::tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &tBl, &full[stage], kb * TC_BK, nb * BN);
+          // A hi + lo, then B hi + lo: one 3-D TMA load each (pair maps)
+          tcx::tma_load_3d(st, &tA, &full[stage], kb * TC_BK, mb * TC_BM, 0);
+          tcx::tma_load_3d(st + 2 * C::A_BYTES, &tB, &full[stage], kb * TC_BK, nb * BN, 0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1361,20 +1386,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
   return fn;
 }
 
-// 2-D bf16 map over (rows x cols) with row pitch ld elements; box = box_rows x 64
-static int tc_map(TcWeights& t, const __nv_bfloat16* base, int64_t rows, int cols, int ld, int box_rows,
-                  CUtensorMap* out) {
-  auto key = std::make_tuple((const void*)base, rows, cols * 65536 + box_rows, ld);
+// 3-D bf16 pair map over a split operand: (cols x rows x {hi, lo}) with row
+// pitch ld elements and lo at a fixed offset from hi; box = 32 x box_rows x 2
+// (64 B swizzle): one TMA load brings a k-block's hi and lo tiles
+static int tc_map(TcWeights& t, const TcOperand& op, int64_t rows, int cols, int box_rows, CUtensorMap* out) {
+  const __nv_bfloat16* base = op.hi;
+  const int ld = op.ld;
+  const int64_t pair = (int64_t)((const char*)op.lo - (const char*)op.hi);
+  auto key = std::make_tuple((const void*)base, rows, cols * 65536 + box_rows, (int)ld);
   auto it = t.maps.find(key);
   if (it != t.maps.end()) { *out = it->second; return 0; }
   auto fn = tc_encode_fn();
   if (!fn) return -1;
+  if (pair <= 0 || pair % 16) return -4;
   CUtensorMap m;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(base), dims, strides, box,
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)pair};
+  cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(base), dims, strides, box,
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -2;
@@ -1410,6 +1440,31 @@ static int tc_out_map(TcWeights& t, const void* base, bool bf16, int64_t rows, i
   return 0;
 }
 
+// epilogue pair map of a split operand (hi, lo at a fixed offset): box
+// 16 columns x 32 rows x 2, 32 B swizzle (the sw_h staging of hi, then lo +1 KB)
+static int tc_out_map_pair(TcWeights& t, const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t rows, int cols,
+                           int64_t ld, CUtensorMap* out) {
+  const int64_t pair = (int64_t)((const char*)lo - (const char*)hi);
+  auto key = std::make_tuple((const void*)hi, rows, (int64_t)cols * 2 + 1 + (pair << 20), ld + (1ll << 40));
+  auto it = t.omaps.find(key);
+  if (it != t.omaps.end()) { *out = it->second; return 0; }
+  auto fn = tc_encode_fn();
+  if (!fn) return -1;
+  if (((uintptr_t)hi & 15) || (ld * 2) % 16 || pair <= 0 || pair % 16) return -2;
+  CUtensorMap m;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)std::max<int64_t>(rows, 1), 2};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)pair};
+  cuuint32_t box[3] = {16, 32, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(hi), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -3;
+  t.omaps[key] = m;
+  *out = m;
+  return 0;
+}
+
 // which epilogues store through TMA, and their output maps (slot order as in
 // TcOutMaps); returns bit 1 when every output got a map, bit 2 when the
 // ring epilogue's input maps (m[4], m[5]) were built too
@@ -1427,9 +1482,7 @@ template <>
 struct EpiOut<EpiAffineSeed> {
   static int build(TcWeights& t, const EpiAffineSeed& e, int64_t M, int N, TcOutMaps& om) {
     if (tc_out_map(t, e.base.C, false, M, N, e.base.ldc, &om.m[0])) return 0;
-    if (tc_out_map(t, e.seed.hi, true, M, N, e.seed.ld, &om.m[2]) ||
-        tc_out_map(t, e.seed.lo, true, M, N, e.seed.ld, &om.m[3]))
-      return 0;
+    if (tc_out_map_pair(t, e.seed.hi, e.seed.lo, M, N, e.seed.ld, &om.m[2])) return 0;
     return 1;
   }
 };
@@ -1439,13 +1492,9 @@ struct EpiOut<TcChain<EpiFwdHidden>> {
     const EpiFwdHidden& e = ch.base;
     if (e.H && tc_out_map(t, e.H, false, M, N, e.ld, &om.m[0])) return 0;
     if (e.D && tc_out_map(t, e.D, false, M, N, e.ld, &om.m[1])) return 0;
-    if (ch.split.hi && (tc_out_map(t, ch.split.hi, true, M, N, ch.split.ld, &om.m[2]) ||
-                        tc_out_map(t, ch.split.lo, true, M, N, ch.split.ld, &om.m[3])))
-      return 0;
+    if (ch.split.hi && tc_out_map_pair(t, ch.split.hi, ch.split.lo, M, N, ch.split.ld, &om.m[2])) return 0;
     // residual input tiles for the ring epilogue (same 32 x 16 boxes, loaded): bit 2
-    if (ch.prev.hi && (tc_out_map(t, ch.prev.hi, true, M, N, ch.prev.ld, &om.m[4]) ||
-                       tc_out_map(t, ch.prev.lo, true, M, N, ch.prev.ld, &om.m[5])))
-      return 1;
+    if (ch.prev.hi && tc_out_map_pair(t, ch.prev.hi, ch.prev.lo, M, N, ch.prev.ld, &om.m[4])) return 1;
     return 3;
   }
 };
@@ -1455,9 +1504,7 @@ struct EpiOut<TcChain<EpiBwd>> {
     const EpiBwd& e = ch.base;
     if (e.G && tc_out_map(t, e.G, false, M, N, e.ld, &om.m[0])) return 0;
     if (e.U && tc_out_map(t, e.U, false, M, N, e.ld, &om.m[1])) return 0;
-    if (ch.split.hi && (tc_out_map(t, ch.split.hi, true, M, N, ch.split.ld, &om.m[2]) ||
-                        tc_out_map(t, ch.split.lo, true, M, N, ch.split.ld, &om.m[3])))
-      return 0;
+    if (ch.split.hi && tc_out_map_pair(t, ch.split.hi, ch.split.lo, M, N, ch.split.ld, &om.m[2])) return 0;
     // ring-epilogue input tiles (dense sweeps only: no row gather): bit 2
     if (e.rowidx || !e.D) return 1;
     if (e.resid && tc_out_map(t, e.resid, false, M, N, e.ld, &om.m[4])) return 1;
@@ -1505,9 +1552,8 @@ struct RingOk<EpiBwdSum> {
 static int g_tc_bwd_ring = getenv("SDN_BWD_RING") ? atoi(getenv("SDN_BWD_RING")) : 2;
 
 template <int BN, class Epi, int RING>
-static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, int N, int K, const CUtensorMap& ah,
-                       const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl, const Epi& epi,
-                       const TcOutMaps& om, int use_om, TcFlags fl) {
+static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, int N, int K, const CUtensorMap& am,
+                       const CUtensorMap& bm, const Epi& epi, const TcOutMaps& om, int use_om, TcFlags fl) {
   using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
   static_assert(C::STAGES >= 2 && C::SMEM <= TC_SMEM_MAX, "shared memory budget");
   static bool attr_set = false;
@@ -1528,18 +1574,16 @@ static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, in
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!(g_tc_pdl && g_tc_pdl_now)) fl.in = nullptr;   // row flags only pay off with early (PDL) launch
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, RING>, ah, al, bh, bl, M, Mdev, N, K, epi,
-                                           om, use_om, g_tc_trace, fl);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, RING>, am, bm, M, Mdev, N, K, epi, om,
+                                           use_om, g_tc_trace, fl);
   return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -3;
 }
 
 template <int BN, class Epi>
 static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const int* Mdev, int N, int K,
                      const TcOperand& A, const TcOperand& B, Epi epi, TcFlags fl = TcFlags{}) {
-  CUtensorMap ah, al, bh, bl;
-  if (tc_map(t, A.hi, std::max<int64_t>(M, 1), K, A.ld, TC_BM, &ah) || tc_map(t, A.lo, std::max<int64_t>(M, 1), K, A.ld, TC_BM, &al) ||
-      tc_map(t, B.hi, N, K, B.ld, BN, &bh) || tc_map(t, B.lo, N, K, B.ld, BN, &bl))
-    return -1;
+  CUtensorMap am, bm;
+  if (tc_map(t, A, std::max<int64_t>(M, 1), K, TC_BM, &am) || tc_map(t, B, N, K, BN, &bm)) return -1;
   const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
   TcOutMaps om;
@@ -1549,18 +1593,18 @@ static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, cons
   if constexpr (std::is_same<Epi, TcChain<EpiFwdHidden>>::value) {
     if ((ob & 2) && g_tc_ring > 0 && !g_tc_trace && RingOk<Epi>::ok(epi, N)) {
       if constexpr (TcCfg<BN, 3, false>::STAGES_FIT >= 2)
-        if (g_tc_ring == 3) return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
-      return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+        if (g_tc_ring == 3) return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, am, bm, epi, om, use_om, fl);
+      return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, am, bm, epi, om, use_om, fl);
     }
   }
   if constexpr (RingKind<Epi>::BWD) {
     if ((ob & 2) && !Mdev && g_tc_bwd_ring > 0 && !g_tc_trace && RingOk<Epi>::ok(epi, N)) {
       if constexpr (TcCfg<BN, 3, true>::STAGES_FIT >= 2)
-        if (g_tc_bwd_ring == 3) return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
-      return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+        if (g_tc_bwd_ring == 3) return tc_launch_k<BN, Epi, 3>(st, grid, M, Mdev, N, K, am, bm, epi, om, use_om, fl);
+      return tc_launch_k<BN, Epi, 2>(st, grid, M, Mdev, N, K, am, bm, epi, om, use_om, fl);
     }
   }
-  return tc_launch_k<BN, Epi, 0>(st, grid, M, Mdev, N, K, ah, al, bh, bl, epi, om, use_om, fl);
+  return tc_launch_k<BN, Epi, 0>(st, grid, M, Mdev, N, K, am, bm, epi, om, use_om, fl);
 }
 
 
@@ -1592,11 +1636,12 @@ static int tc_buf(H* h, TcWeights& t, TcOperand& op, int64_t rows, int ld) {
   op.rows = rows;
   op.ld = ld;
   size_t n = (size_t)std::max<int64_t>(rows, 1) * ld;
-  if (cudaMalloc(&op.hi, n * 2) != cudaSuccess || cudaMalloc(&op.lo, n * 2) != cudaSuccess) return -1;
-  cudaMemset(op.hi, 0, n * 2);
-  cudaMemset(op.lo, 0, n * 2);
+  // hi and lo in one allocation, lo at +n elements: the TMA pair maps move both
+  // halves of a tile with one instruction
+  if (cudaMalloc(&op.hi, n * 4) != cudaSuccess) return -1;
+  op.lo = op.hi + n;
+  cudaMemset(op.hi, 0, n * 4);
   t.allocs.push_back(op.hi);
-  t.allocs.push_back(op.lo);
   return 0;
 }
 
