@@ -1496,7 +1496,13 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       drop_graph(h);
       const int64_t l0 = h->launches;
       CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
-      int rc = enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0);
+      // the device span events are nodes of the graph itself (first and last):
+      // the span excludes any host delay in submitting the replay
+      cudaError_t ee = cudaEventRecordWithFlags(h->dev_ev[0], h->stream, cudaEventRecordExternal);
+      int rc = ee == cudaSuccess ? enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0)
+                                 : fail(SDN_ERR_CUDA, "event record node");
+      if (rc == SDN_OK && cudaEventRecordWithFlags(h->dev_ev[1], h->stream, cudaEventRecordExternal) != cudaSuccess)
+        rc = fail(SDN_ERR_CUDA, "event record node");
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
       if (rc != SDN_OK) { if (g) cudaGraphDestroy(g); return rc; }
@@ -1517,9 +1523,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       h->fwd_done = true;
       h->qr_valid = n_exact > 0;
     }
-    CU(cudaEventRecord(h->dev_ev[0], h->stream));
     CU(cudaGraphLaunch(h->gexec, h->stream));
-    CU(cudaEventRecord(h->dev_ev[1], h->stream));
     h->launches += h->glaunches;
   } else {
     CU(cudaEventRecord(h->dev_ev[0], h->stream));
