@@ -21,10 +21,12 @@
 #include "refine.cuh"
 #include "train.cuh"
 
-// SMs left to side-stream work (the exact-CVaR selections) while the main
-// stream's persistent GEMMs run (sdn_eval_multi).  20 keeps the c2 sweep GEMMs
-// (256 tiles) at two full waves on the other 128.
-constexpr int SDN_SIDE_SMS_DEFAULT = 20;
+// SMs left to side-stream work (the exact-CVaR selection + fp64 band
+// refinement, a cooperative kernel on this many blocks) while the main stream's
+// persistent sweep GEMMs run (sdn_eval_multi).  The selection is the critical
+// path of the c2 step: measured 0.408 ms at 20, 0.397 at 24, 0.382-0.386 at 32,
+// 0.386 at 40, 0.403 at 48 (the 128-column reverse tiles lose little to fewer SMs).
+constexpr int SDN_SIDE_SMS_DEFAULT = 32;
 
 #include <algorithm>
 #include <cmath>
@@ -208,7 +210,7 @@ struct sdn_handle {
   std::vector<uint8_t*> x_mask;
   std::vector<int64_t> x_k;     // k of each kept selection (multi-rank phases)
   int sm_avail = 0;             // SMs the persistent GEMMs may use
-  int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS
+  int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS (default clamped to a quarter of the SMs)
   bool no_overlap = false;               // env SDN_NO_OVERLAP=1
   SweepBufs sw0;                // sweep buffers
   SweepBufs* sw = &sw0;
@@ -663,6 +665,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   { const char* e = getenv("SDN_NO_OVERLAP"); h->no_overlap = e && e[0] == '1'; }
   { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
+  h->side_sms = std::max(1, std::min(SDN_SIDE_SMS_DEFAULT, h->num_sms / 4));
   { const char* e = getenv("SDN_SIDE_SMS");
     if (e) h->side_sms = std::max(1, std::min(atoi(e), h->num_sms / 2)); }
   h->tcw.enabled = false;
