@@ -23,10 +23,10 @@
 
 // SMs left to side-stream work (the exact-CVaR selection + fp64 band
 // refinement, a cooperative kernel on this many blocks) while the main stream's
-// persistent sweep GEMMs run (sdn_eval_multi).  The selection is the critical
-// path of the c2 step: measured 0.408 ms at 20, 0.397 at 24, 0.382-0.386 at 32,
-// 0.386 at 40, 0.403 at 48 (the 128-column reverse tiles lose little to fewer SMs).
-constexpr int SDN_SIDE_SMS_DEFAULT = 32;
+// persistent sweep GEMMs run (sdn_eval_multi).  Balances the two paths of the
+// c2 step: with the width-templated refinement, 0.394 ms at 20, 0.385 at 24-28,
+// 0.387 at 32 (before it: the selection was the critical path up to 32 SMs).
+constexpr int SDN_SIDE_SMS_DEFAULT = 28;
 
 #include <algorithm>
 #include <cmath>

@@ -121,20 +121,23 @@ SDN_DEV int block_excl(int* s_w, int warp, int lane, int v, int& total) {
 
 // one W row slice into registers: unconditional loads at clamped addresses so
 // all are in flight at once (a branch per load would serialise the round trips)
-SDN_DEV void ref_load_w(const float* w, int K, int lane, float (&wf)[REF_KC / 32]) {
+// (KC: the layer's input width rounded up to 128/256/512/1024 -- no loads or
+// registers for columns past it)
+template <int KC>
+SDN_DEV void ref_load_w(const float* w, int K, int lane, float (&wf)[KC / 32]) {
 #pragma unroll
-  for (int u = 0; u < REF_KC / 32; ++u) wf[u] = __ldg(w + min(lane + 32 * u, K - 1));
+  for (int u = 0; u < KC / 32; ++u) wf[u] = __ldg(w + min(lane + 32 * u, K - 1));
 }
 
 // dot products of RB staged rows with one W row; transposed butterfly so that
 // lanes 4j..4j+3 end with row j's total (9 double shuffles instead of 8 x 5)
-template <int RB>
-SDN_DEV double ref_column(const double* xs, const float (&wf)[REF_KC / 32], int K, int lane) {
+template <int RB, int KC>
+SDN_DEV double ref_column(const double* xs, const float (&wf)[KC / 32], int K, int lane) {
   double acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.0;
 #pragma unroll
-  for (int u = 0; u < REF_KC / 32; ++u) {
+  for (int u = 0; u < KC / 32; ++u) {
     if (lane + 32 * u < K) {
       const double wk = (double)wf[u];
 #pragma unroll
@@ -157,6 +160,69 @@ SDN_DEV double ref_column(const double* xs, const float (&wf)[REF_KC / 32], int 
   d += __shfl_xor_sync(0xffffffffu, d, 2);
   d += __shfl_xor_sync(0xffffffffu, d, 1);
   return d;                                      // total of row (lane >> 2)
+}
+
+// one pass of up to REF_RB band rows through layer ly (stage the rows in
+// shared memory, then this warp's output columns)
+template <int KC>
+SDN_DEV void ref_rows(const RefineArgs& a, const RefineLayer& ly, double* xs, int warp, int lane, int gw, int nw,
+                      int r0, int rb, bool first, bool last, const double* in64, double* out) {
+  const int K = ly.K, N = ly.N;
+  {                                          // warp j stages row r0 + j (clamped)
+    const int rj = r0 + min(warp, rb - 1);
+    if (first) {                              // x = m_r * in_scale (exact in fp64, as the oracle)
+      const float* src = a.MR + (int64_t)__ldcg(a.rowidx + rj) * K;
+      float v[KC / 32], sc[KC / 32];
+#pragma unroll
+      for (int u = 0; u < KC / 32; ++u) {
+        v[u] = __ldg(src + min(lane + 32 * u, K - 1));
+        sc[u] = __ldg(a.iscale + min(lane + 32 * u, K - 1));
+      }
+#pragma unroll
+      for (int u = 0; u < KC / 32; ++u)
+        if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = (double)v[u] * (double)sc[u];
+    } else {
+      const double* src = in64 + (int64_t)rj * K;
+      double v[KC / 32];
+#pragma unroll
+      for (int u = 0; u < KC / 32; ++u) v[u] = __ldcg(src + min(lane + 32 * u, K - 1));
+#pragma unroll
+      for (int u = 0; u < KC / 32; ++u)
+        if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = v[u];
+    }
+  }
+  __syncthreads();
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && r0 == 0) a.trace[first ? 30 : (last ? 31 : 32)] = gtime();
+  // columns of this warp: c = gw, gw + nw, ...; the next column's W row is
+  // loaded while the current one is reduced (software pipeline)
+  float wf[KC / 32];
+  int c = gw;
+  if (c < N) ref_load_w<KC>(ly.W + (int64_t)c * K, K, lane, wf);
+  for (; c < N; c += nw) {
+    float wn[KC / 32];
+    if (c + nw < N) ref_load_w<KC>(ly.W + (int64_t)(c + nw) * K, K, lane, wn);
+    double v;
+    if (rb <= 2) v = ref_column<2, KC>(xs, wf, K, lane);
+    else if (rb <= 4) v = ref_column<4, KC>(xs, wf, K, lane);
+    else v = ref_column<8, KC>(xs, wf, K, lane);
+    const int j = lane >> 2;                 // row whose total this lane holds
+    if ((lane & 3) == 0 && j < rb) {
+      const double S = v + (first ? a.zb64[c] : (double)ly.b[c]);
+      double o;
+      if (last) {
+        o = (double)a.omean[c] + (double)a.ostd[c] * S;
+      } else if (a.softmax) {
+        o = S;                                        // normalised by the row pass below
+      } else {
+        o = act64(a.act, S);
+        if (ly.resid) o += xs[j * REF_KC + c];       // resid: K == N
+      }
+      out[(int64_t)(r0 + j) * N + c] = o;
+    }
+#pragma unroll
+    for (int u = 0; u < KC / 32; ++u) wf[u] = wn[u];
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
@@ -426,60 +492,10 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     double* out = a.buf[l & 1];
     for (int r0 = 0; r0 < m; r0 += REF_RB) {
       const int rb = min(REF_RB, m - r0);
-      {                                          // warp j stages row r0 + j (clamped)
-        const int rj = r0 + min(warp, rb - 1);
-        if (first) {                              // x = m_r * in_scale (exact in fp64, as the oracle)
-          const float* src = a.MR + (int64_t)__ldcg(a.rowidx + rj) * K;
-          float v[REF_KC / 32], sc[REF_KC / 32];
-#pragma unroll
-          for (int u = 0; u < REF_KC / 32; ++u) {
-            v[u] = __ldg(src + min(lane + 32 * u, K - 1));
-            sc[u] = __ldg(a.iscale + min(lane + 32 * u, K - 1));
-          }
-#pragma unroll
-          for (int u = 0; u < REF_KC / 32; ++u)
-            if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = (double)v[u] * (double)sc[u];
-        } else {
-          const double* src = in64 + (int64_t)rj * K;
-          double v[REF_KC / 32];
-#pragma unroll
-          for (int u = 0; u < REF_KC / 32; ++u) v[u] = __ldcg(src + min(lane + 32 * u, K - 1));
-#pragma unroll
-          for (int u = 0; u < REF_KC / 32; ++u)
-            if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = v[u];
-        }
-      }
-      __syncthreads();
-      // columns of this warp: c = gw, gw + nw, ...; the next column's W row is
-      // loaded while the current one is reduced (software pipeline)
-      float wf[REF_KC / 32];
-      int c = gw;
-      if (c < N) ref_load_w(ly.W + (int64_t)c * K, K, lane, wf);
-      for (; c < N; c += nw) {
-        float wn[REF_KC / 32];
-        if (c + nw < N) ref_load_w(ly.W + (int64_t)(c + nw) * K, K, lane, wn);
-        double v;
-        if (rb <= 2) v = ref_column<2>(xs, wf, K, lane);
-        else if (rb <= 4) v = ref_column<4>(xs, wf, K, lane);
-        else v = ref_column<8>(xs, wf, K, lane);
-        const int j = lane >> 2;                 // row whose total this lane holds
-        if ((lane & 3) == 0 && j < rb) {
-          const double S = v + (first ? a.zb64[c] : (double)ly.b[c]);
-          double o;
-          if (last) {
-            o = (double)a.omean[c] + (double)a.ostd[c] * S;
-          } else if (a.softmax) {
-            o = S;                                        // normalised by the row pass below
-          } else {
-            o = act64(a.act, S);
-            if (ly.resid) o += xs[j * REF_KC + c];       // resid: K == N
-          }
-          out[(int64_t)(r0 + j) * N + c] = o;
-        }
-#pragma unroll
-        for (int u = 0; u < REF_KC / 32; ++u) wf[u] = wn[u];
-      }
-      __syncthreads();
+      if (K <= 128) ref_rows<128>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
+      else if (K <= 256) ref_rows<256>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
+      else if (K <= 512) ref_rows<512>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
+      else ref_rows<1024>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
     }
     REF_STAMP(13 + 2 * l);
     grid_barrier(a.bar, gen);
