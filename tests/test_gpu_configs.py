@@ -114,3 +114,24 @@ def test_c4_full_n_properties():
     Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), p.m_r[sl], p.z,
                                  form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
     assert _rel(Q[sl], Qo) <= 2e-5
+
+
+def test_c5_full_n_jacobian_ties_to_reverse_gradient():
+    """c5 at BASELINE size (16384 samples): the forward-mode control Jacobians
+    (surrogate.py:195-233) match the float64 oracle on a random subset, and,
+    contracted with dQ/dphi = 2 (phi + c) and averaged over all samples, equal
+    the reverse-mode mean-risk gradient of the same engine (size-independent
+    tie-out between the c5 Jacobian path and the SAA gradient path)."""
+    cfg = wl.WORKLOADS["c5"]
+    n = cfg.n_samples
+    p, eng = _setup("c5", n)
+    Z = np.broadcast_to(p.z, (n, cfg.d_z))
+    J = eng.jacobian_batch(p.m_r, Z)
+    assert J.shape == (n, cfg.r_u, cfg.d_z) and np.isfinite(J).all()
+    sub = np.random.default_rng(5).choice(n, 96, replace=False)
+    Jo = ref.z_jacobian_batch(ref.as_oracle(p), p.m_r[sub], Z[sub])
+    assert _rel(J[sub], Jo) <= RTOL
+    phi = eng.forward_batch(p.m_r, Z).astype(np.float64)
+    g_fwd = np.einsum("iu,iuk->k", 2.0 * (phi + p.c.astype(np.float64)), J.astype(np.float64)) / n
+    r = eng.eval(p.z, "mean", alpha=0.0)
+    assert _rel(g_fwd, r.grad_z) <= RTOL
