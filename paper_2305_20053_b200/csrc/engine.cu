@@ -1019,10 +1019,12 @@ static int compact_rows(sdn_handle* h, int kind, double t, double eps, const dou
 static int launch_topk(sdn_handle* h, int64_t n, int64_t k, const double* vals, const double* gidx, uint8_t* mask,
                        double* thr = nullptr) {
   if (n <= TOPK_SMEM_MAX) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned attr = 0;                      // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr & (1u << (dev & 31)))) {
       cudaFuncSetAttribute(k_topk_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TOPK_SMEM_BYTES);
-      attr = true;
+      attr |= 1u << (dev & 31);
     }
     k_topk_select_smem<<<1, 1024, TOPK_SMEM_BYTES, h->stream>>>((int)n, k, vals, gidx, mask, thr);
   } else {

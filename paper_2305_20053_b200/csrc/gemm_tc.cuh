@@ -1556,10 +1556,12 @@ static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, in
                        const CUtensorMap& bm, const Epi& epi, const TcOutMaps& om, int use_om, TcFlags fl) {
   using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
   static_assert(C::STAGES >= 2 && C::SMEM <= TC_SMEM_MAX, "shared memory budget");
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned attr_set = 0;                    // per device: the attribute is a per-context setting
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set & (1u << (dev & 31)))) {
     cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr_set = true;
+    attr_set |= 1u << (dev & 31);
   }
   // programmatic stream serialization (PDL): the kernel may start while the
   // previous one drains; griddepcontrol.wait orders it
