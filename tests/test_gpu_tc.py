@@ -93,3 +93,40 @@ def test_tc_wide_layers_c3_shapes():
                           form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
     assert abs(r.value - o["value"]) <= RTOL * abs(o["value"])
     assert _rel(r.grad_z, o["grad_z"]) <= RTOL
+
+
+_RING_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[2])
+from paper_2305_20053_b200 import Engine, workloads as wl
+cfg = wl.WORKLOADS["c2"].with_samples(8192)
+p = wl.make_problem(cfg, seed=3, count=8192)
+eng = Engine(p, max_samples=8192, gemm="tc")
+eng.set_tracking(p.c, p.q0)
+eng.set_samples(p.m_r)
+risks = [dict(kind="meanvar", beta=1.0, alpha=1e-2), dict(kind="cvar_exact", beta=0.95, alpha=1e-2)]
+out = eng.eval_multi(p.z, risks)
+np.savez(sys.argv[1], q=eng.last_q(), g0=out[0].grad_z, g1=out[1].grad_z, v=[o.value for o in out],
+         idx=np.sort(out[1].idx))
+"""
+
+
+def test_ring_epilogues_bit_identical_to_register_prefetch_path(tmp_path):
+    """The asynchronous-input ring epilogues (forward chain, dense reverse sweep)
+    compute exactly what the register-prefetch epilogues compute: same Q, risk
+    values, gradients and CVaR indices, bit for bit (the switches are read once
+    per process, so each variant runs in its own interpreter)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "ring.py"
+    script.write_text(_RING_SCRIPT)
+    outs = []
+    for env_extra in ({}, {"SDN_EPI_RING": "0", "SDN_BWD_RING": "0"}):
+        out = tmp_path / f"r{len(outs)}.npz"
+        env = dict(os.environ, **env_extra)
+        subprocess.run([sys.executable, str(script), str(out), root], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    for k in ("q", "g0", "g1", "v", "idx"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
