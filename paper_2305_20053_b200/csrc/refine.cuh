@@ -86,19 +86,23 @@ SDN_DEV int warp_sum_i(int v) {
 }
 
 // grid-wide barrier (all blocks co-resident: cooperative launch)
+// (release on arrival, acquire on the generation flag: orders this block's
+// prior writes before the release and everyone's after the acquire, without
+// two full fences per block)
 SDN_DEV void grid_barrier(unsigned* bar, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned arrived = atomicAdd(&bar[0], 1u);
+    unsigned arrived;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
     if (arrived == gridDim.x - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicExch(&bar[1], gen + 1u);
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1u) : "memory");
     } else {
-      while (*(volatile unsigned*)&bar[1] == gen) __nanosleep(20);
+      unsigned g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      } while (g == gen);
     }
-    __threadfence();
   }
   ++gen;
   __syncthreads();
