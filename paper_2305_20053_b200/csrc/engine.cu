@@ -156,7 +156,7 @@ struct sdn_handle {
   uint8_t* cand_mask = nullptr;
   int64_t cand_cap = 0;
   // pinned staging
-  double* hz = nullptr;         // d_z
+  double* hz = nullptr;         // d_z + SDN_RMAX (z, then each risk's t)
   double* hstats = nullptr;     // STATS_LEN
   double* hpart = nullptr;      // partial len
 
@@ -247,6 +247,11 @@ struct sdn_handle {
   bool use_graphs = true;       // env SDN_NO_GRAPH=1 disables
   cudaGraphExec_t gexec = nullptr;
   cudaEvent_t dev_ev[2] = {nullptr, nullptr};   // device span of the last sdn_eval_multi
+  // stage timeline inside the evaluation graph (env SDN_TIMELINE=1: event
+  // record nodes at stage boundaries, printed after each sdn_eval_multi)
+  bool tl_on = false;
+  cudaEvent_t tl[12] = {};
+  bool tl_hit[12] = {};
   double last_dev_ms = 0.0;
   std::vector<double> gkey;
   int64_t glaunches = 0;
@@ -307,6 +312,18 @@ struct ProfScope {
 // GEMM dispatch
 
 static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// stage boundary mark (SDN_TIMELINE=1): an event record node on `st`
+static inline void tl_mark(sdn_handle* h, int i, cudaStream_t st = nullptr) {
+  if (!h->tl_on) return;
+  if (!h->tl[i]) cudaEventCreate(&h->tl[i]);
+  cudaEventRecordWithFlags(h->tl[i], st ? st : h->stream, cudaEventRecordExternal);
+  h->tl_hit[i] = true;
+}
+static const char* const TL_NAMES[12] = {"start", "z-bias", "forward GEMMs", "QoI+moments", "side: start",
+                                          "side: selection+refine+compaction", "reverse chain (pre-join)",
+                                          "join wait", "sweep weights", "last reverse GEMM + sums",
+                                          "column sums + finalize", "end"};
 
 template <int BM, int BN, int TM, int TN, bool AT, bool BT, class Epi>
 static void launch_simt(sdn_handle* h, int64_t M, const int* Mdev, int N, int K, const float* A,
@@ -655,16 +672,17 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
     if ((rc = dalloc(h, &h->ref64[i], (size_t)h->ref_rows * h->maxw))) return bail(rc);
   h->band_cap = 8;
   if ((rc = dalloc(h, &h->band_log, h->band_cap))) return bail(rc);
-  if (cudaHostAlloc((void**)&h->hband, sizeof(int) * h->band_cap, 0) != cudaSuccess)
+  if (cudaHostAlloc((void**)&h->hband, sizeof(int) * h->band_cap, cudaHostAllocMapped) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
   if (cudaHostAlloc((void**)&h->hz, sizeof(double) * (h->d_z + SDN_RMAX), 0) != cudaSuccess ||
-      cudaHostAlloc((void**)&h->hstats, sizeof(double) * STATS_LEN, 0) != cudaSuccess ||
-      cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), 0) != cudaSuccess)
+      cudaHostAlloc((void**)&h->hstats, sizeof(double) * STATS_LEN, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), cudaHostAllocMapped) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
   { const char* e = getenv("SDN_NO_REFINE"); h->no_refine = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_OVERLAP"); h->no_overlap = e && e[0] == '1'; }
   { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
+  { const char* e = getenv("SDN_TIMELINE"); h->tl_on = e && e[0] == '1'; }
   h->side_sms = std::max(1, std::min(SDN_SIDE_SMS_DEFAULT, h->num_sms / 4));
   { const char* e = getenv("SDN_SIDE_SMS");
     if (e) h->side_sms = std::max(1, std::min(atoi(e), h->num_sms / 2)); }
@@ -690,6 +708,8 @@ int sdn_destroy(sdn_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (cudaEvent_t e : h->dev_ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->tl)
     if (e) cudaEventDestroy(e);
   for (void* p : h->allocs) cudaFree(p);
   if (h->U) cudaFree(h->U);
@@ -861,6 +881,8 @@ static void stage_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n
   for (int r = 0; r < SDN_RMAX; ++r) h->hz[h->d_z + r] = r < n_risks ? risks[r].t : 0.0;
   h->hzz = zz;
 }
+// (a copy node from the pinned staging buffer: measured faster than having
+// every k_zbias block read z from host-mapped memory)
 static int upload_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks) {
   stage_z(h, z, risks, n_risks);
   CU(cudaMemcpyAsync(h->zdev, h->hz, sizeof(double) * (h->d_z + SDN_RMAX), cudaMemcpyHostToDevice, h->stream));
@@ -963,11 +985,13 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
   k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb,
                                                              h->zb64); }
+  tl_mark(h, 1);
   h->launches++;
   CHECK_LAUNCH(h);
   if (h->n > 0) {
     TRY(run_forward(h, h->n, h->MR, h->r_m, h->r_m, h->W[0], h->r_m, h->zb, store_D, h->Y,
                     h->tcw.enabled ? &h->tcw.mr : nullptr, nullptr, false, fuse_seed && !dec && store_D));
+    tl_mark(h, 2);
     if (dec) {
       TRY((gemm<false, true>(h, h->n, nullptr, h->r_u, h->r_u, h->Y, h->r_u, h->Kg, h->r_u,
                              EpiStore{h->KPhi, (int64_t)h->r_u})));
@@ -978,6 +1002,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
                                    h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
                                    h->Q, h->qpart, tp, h->red_counter, stats_dev); }
+  tl_mark(h, 3);
   h->launches += 1;
   CHECK_LAUNCH(h);
   TRY(refine_window(h, risk, dec, qg, stats_dev, tp));
@@ -1169,12 +1194,17 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   ssum.R = R;
   ssum.plane = tplane;
   ssum.before_last = [&]() -> int {
+    tl_mark(h, 6);
     if (dense && join) TRY(join());
-    return weights();
+    tl_mark(h, 7);
+    const int rc = weights();
+    tl_mark(h, 8);
+    return rc;
   };
   float* u0 = nullptr;
   int64_t nrb = 0;
   TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint, false, &nrb, &ssum));
+  tl_mark(h, 9);
   const double* part;
   int nrb_fin;
   int64_t plane;
@@ -1313,9 +1343,17 @@ static int64_t refined_count(sdn_handle* h, const sdn_risk& r, int exact_slot) {
 
 static int eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
                        double* grad_z, int exact_slot = -1) {
-  CU(cudaMemcpyAsync(h->hstats, stats_dev, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaMemcpyAsync(h->hpart, partial_dev, sizeof(double) * h->plen(), cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaMemcpyAsync(h->hband, h->band_log, sizeof(int) * 2, cudaMemcpyDeviceToHost, h->stream));
+  {                                   // results -> host-mapped memory (one kernel, no copy nodes)
+    double *dst_s = nullptr, *dst_p = nullptr;
+    int* dst_b = nullptr;
+    CU(cudaHostGetDevicePointer((void**)&dst_s, h->hstats, 0));
+    CU(cudaHostGetDevicePointer((void**)&dst_p, h->hpart, 0));
+    CU(cudaHostGetDevicePointer((void**)&dst_b, h->hband, 0));
+    k_export<<<1, 256, 0, h->stream>>>(stats_dev, dst_s, STATS_LEN, partial_dev, dst_p, h->plen(), h->band_log,
+                                       dst_b, 2);
+    h->launches++;
+    CHECK_LAUNCH(h);
+  }
   CU(cudaStreamSynchronize(h->stream));
   TRY(finish_host(h, h->risk, h->hstats, h->hpart, res, grad_z));
   res->n_refined = refined_count(h, h->risk, exact_slot);
@@ -1382,10 +1420,12 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   if (overlap) {
     CU(cudaEventRecord(h->ev_fwd, h->stream));
     CU(cudaStreamWaitEvent(h->side, h->ev_fwd, 0));
+    tl_mark(h, 4, h->side);
     {
       SideScope ss(h);
       TRY(select_all());
     }
+    tl_mark(h, 5, h->side);
     CU(cudaEventRecord(h->ev_side, h->side));
     h->sm_avail = h->num_sms - h->side_sms;
     join = [h]() -> int {
@@ -1401,10 +1441,17 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
                           h->zdev + h->d_z);
   h->sm_avail = h->num_sms;
   if (rc) return rc;
-  CU(cudaMemcpyAsync(h->hstats, h->stats_loc, sizeof(double) * STATS_LEN, cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaMemcpyAsync(h->hpart_multi, h->partial_multi, sizeof(double) * n_risks * plen, cudaMemcpyDeviceToHost,
-                     h->stream));
-  CU(cudaMemcpyAsync(h->hband, h->band_log, sizeof(int) * (n_risks + 1), cudaMemcpyDeviceToHost, h->stream));
+  {                                   // results -> host-mapped memory (one kernel, no copy nodes)
+    double *dst_s = nullptr, *dst_p = nullptr;
+    int* dst_b = nullptr;
+    CU(cudaHostGetDevicePointer((void**)&dst_s, h->hstats, 0));
+    CU(cudaHostGetDevicePointer((void**)&dst_p, h->hpart_multi, 0));
+    CU(cudaHostGetDevicePointer((void**)&dst_b, h->hband, 0));
+    k_export<<<1, 256, 0, h->stream>>>(h->stats_loc, dst_s, STATS_LEN, h->partial_multi, dst_p, n_risks * plen,
+                                       h->band_log, dst_b, n_risks + 1);
+    h->launches++;
+    CHECK_LAUNCH(h);
+  }
   return SDN_OK;
 }
 
@@ -1469,7 +1516,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     h->multi_cap = std::max(n_risks, 4);
     h->hidx_cap = std::max<int64_t>(ktot, 1);
     CU(cudaMalloc(&h->partial_multi, sizeof(double) * h->multi_cap * plen));
-    CU(cudaHostAlloc((void**)&h->hpart_multi, sizeof(double) * h->multi_cap * plen, 0));
+    CU(cudaHostAlloc((void**)&h->hpart_multi, sizeof(double) * h->multi_cap * plen, cudaHostAllocMapped));
     CU(cudaHostAlloc((void**)&h->hidx, sizeof(int) * h->hidx_cap, 0));
   }
   if (n_risks + 1 > h->band_cap) {
@@ -1477,7 +1524,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     int* bl = nullptr;
     int* hb = nullptr;
     CU(cudaMalloc(&bl, sizeof(int) * (n_risks + 1)));
-    CU(cudaHostAlloc((void**)&hb, sizeof(int) * (n_risks + 1), 0));
+    CU(cudaHostAlloc((void**)&hb, sizeof(int) * (n_risks + 1), cudaHostAllocMapped));
     h->allocs.push_back(bl);
     if (h->hband) cudaFreeHost(h->hband);
     h->band_log = bl;                // (the old block stays in allocs until destroy)
@@ -1504,8 +1551,10 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
       // the device span events are nodes of the graph itself (first and last):
       // the span excludes any host delay in submitting the replay
       cudaError_t ee = cudaEventRecordWithFlags(h->dev_ev[0], h->stream, cudaEventRecordExternal);
+      tl_mark(h, 0);
       int rc = ee == cudaSuccess ? enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0)
                                  : fail(SDN_ERR_CUDA, "event record node");
+      tl_mark(h, 11);
       if (rc == SDN_OK && cudaEventRecordWithFlags(h->dev_ev[1], h->stream, cudaEventRecordExternal) != cudaSuccess)
         rc = fail(SDN_ERR_CUDA, "event record node");
       cudaGraph_t g = nullptr;
@@ -1539,6 +1588,15 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   {
     float t = 0.f;
     h->last_dev_ms = cudaEventElapsedTime(&t, h->dev_ev[0], h->dev_ev[1]) == cudaSuccess ? (double)t : -1.0;
+  }
+  if (h->tl_on && h->tl_hit[0] && h->tl_hit[11]) {      // stage timeline (us from the graph's first node)
+    fprintf(stderr, "timeline:");
+    for (int i = 1; i < 12; ++i) {
+      float t = 0.f;
+      if (h->tl_hit[i] && cudaEventElapsedTime(&t, h->tl[0], h->tl[i]) == cudaSuccess)
+        fprintf(stderr, " | %s %.1f", TL_NAMES[i], 1e3 * t);
+    }
+    fprintf(stderr, "\n");
   }
   for (int i = 0; i < n_risks; ++i) {
     TRY(finish_host(h, risks[i], h->hstats, h->hpart_multi + (size_t)i * plen, &res[i],

@@ -178,6 +178,16 @@ k_moments(int64_t n, const double* __restrict__ Q, double shift, double t, doubl
   if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;
 }
 
+// results of an evaluation straight into host-mapped pinned memory (zero
+// copy): one small kernel instead of three device-to-host copy nodes
+__global__ void __launch_bounds__(256)
+k_export(const double* __restrict__ stats, double* __restrict__ hstats, int nstats, const double* __restrict__ part,
+         double* __restrict__ hpart, int npart, const int* __restrict__ band, int* __restrict__ hband, int nband) {
+  for (int i = threadIdx.x; i < nstats; i += blockDim.x) hstats[i] = stats[i];
+  for (int i = threadIdx.x; i < npart; i += blockDim.x) hpart[i] = part[i];
+  for (int i = threadIdx.x; i < nband; i += blockDim.x) hband[i] = band[i];
+}
+
 // sample weight w_i of the risk functional:
 //   mean: 1/n; meanvar: (1 + 2 beta (Q_i - Qbar))/n; smoothed CVaR (riskopt.py:238-241):
 //   splus'(Q_i - t)/(n (1-beta)); exact CVaR: 1/k on the selection; unit: 1.
