@@ -400,3 +400,26 @@ def test_decoded_frame_cvar_risks(gemm):
     o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar", beta=0.9, eps=1e-3), t)
     assert abs(r.value - o[0]) <= RTOL * abs(o[0])
     assert _rel(r.grad_z, o[1]) <= RTOL
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_bench_step_at_full_size_matches_oracle(seed):
+    """The benchmarked evaluation itself (BASELINE config 2, 16384 samples: mean +
+    variance and exact CVaR_0.95 with control cost, one forward and one sweep,
+    CUDA-graph replay) against the float64 oracle: values and gradients within
+    1e-4, the CVaR index set bit-exact; the second replay with a new z too."""
+    cfg = wl.WORKLOADS["c2"]
+    p = wl.make_problem(cfg, seed=seed)
+    eng = _engine(p)
+    risks = [dict(kind="meanvar", beta=1.0, alpha=cfg.alpha), dict(kind="cvar_exact", beta=0.95, alpha=cfg.alpha)]
+    form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    m = ref.as_oracle(p)
+    rng = np.random.default_rng(100 + seed)
+    for z in (p.z, np.clip(p.z + 0.5 * rng.standard_normal(cfg.d_z), -4.0, 4.0)):
+        out = eng.eval_multi(z, risks)
+        o_mv = ref.risk_and_grad(m, p.m_r, z, ref.Risk("meanvar", beta=1.0, alpha=cfg.alpha), form=form)
+        o_cv = ref.risk_and_grad(m, p.m_r, z, ref.Risk("cvar_exact", beta=0.95, alpha=cfg.alpha), form=form)
+        for r, o in zip(out, (o_mv, o_cv)):
+            assert abs(r.value - o["value"]) <= RTOL * abs(o["value"])
+            assert _rel(r.grad_z, o["grad_z"]) <= RTOL
+        np.testing.assert_array_equal(np.sort(out[1].idx), np.sort(o_cv["idx"]))
