@@ -59,7 +59,7 @@ def test_c3_smoothed_cvar_simt_exact_fp32():
     assert abs(r.grad_t - o[2]) <= 1e-6
 
 
-@pytest.mark.parametrize("n", [2048, 8192])
+@pytest.mark.parametrize("n", [2048, 8192, 65536])   # 65536 = BASELINE config 3 (full size)
 def test_c3_smoothed_cvar_tc_refined(n):
     """Same risk on the default tensor-core chain: the rows whose bf16x3 Q
     lies within error of the splus' window are re-evaluated in exact fp32
