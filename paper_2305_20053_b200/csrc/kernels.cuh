@@ -383,21 +383,18 @@ k_weights(int64_t nsw, const int* __restrict__ n_act_dev, const int* __restrict_
       }
     }
   }
-  // fixed-order block reduction: lanes (butterfly), then warps in order --
-  // only the 2R fields in use (partials packed with stride 2R)
-  const int nf = 2 * rs.R;
+  // fixed-order block reduction: lanes (butterfly), then warps in order
 #pragma unroll
-  for (int f = 0; f < 2 * SDN_RMAX; ++f)
-    if (f < nf) acc[f] = warp_sum(acc[f]);
+  for (int f = 0; f < 2 * SDN_RMAX; ++f) acc[f] = warp_sum(acc[f]);
   if (lane == 0)
-    for (int f = 0; f < nf; ++f) sp[warp][f] = acc[f];
+    for (int f = 0; f < 2 * SDN_RMAX; ++f) sp[warp][f] = acc[f];
   __syncthreads();
-  if (threadIdx.x < nf) {
+  if (threadIdx.x < 2 * SDN_RMAX) {
     double s = 0.0;
     for (int w = 0; w < 8; ++w) s += sp[w][threadIdx.x];
-    part[(int64_t)blockIdx.x * nf + threadIdx.x] = s;
+    part[(int64_t)blockIdx.x * 2 * SDN_RMAX + threadIdx.x] = s;
   }
-  if (counter) last_block_sum(counter, gridDim.x, nf, part, out);
+  if (counter) last_block_sum(counter, gridDim.x, 2 * SDN_RMAX, part, out);
 }
 
 // weighted column sums of U (n_act x w): part[r][by][c] = sum_rows W[row][r] U[row][c]
