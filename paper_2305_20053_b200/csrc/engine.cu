@@ -24,9 +24,9 @@
 // SMs left to side-stream work (the exact-CVaR selection + fp64 band
 // refinement, a cooperative kernel on this many blocks) while the main stream's
 // persistent sweep GEMMs run (sdn_eval_multi).  Balances the two paths of the
-// c2 step: with the width-templated refinement, 0.394 ms at 20, 0.385 at 24-28,
-// 0.387 at 32 (before it: the selection was the critical path up to 32 SMs).
-constexpr int SDN_SIDE_SMS_DEFAULT = 28;
+// c2 step; re-measured after each change to either path (latest, with the
+// depth-3 reverse ring: 0.370 ms at 24-28, 0.358-0.367 at 32-44).
+constexpr int SDN_SIDE_SMS_DEFAULT = 36;
 
 #include <algorithm>
 #include <cmath>
