@@ -326,7 +326,7 @@ constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
 #define TC_RING_EW 12
 #endif
 #ifndef TC_RING_EW_BWD
-#define TC_RING_EW_BWD 8
+#define TC_RING_EW_BWD 8      // reverse rings (4-KB slots, depth 3): 8 warps keep four mainloop stages
 #endif
 template <int RING, bool BWD = false>
 struct EpiWarps {
