@@ -5,10 +5,14 @@ elliptic 2D 129x129, MLP 228->512x4->128 (ELU, residual), N=16384 samples
 per GPU, one step = mean+variance AND exact CVaR_0.95 risk + gradient.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--config c1..c4] [--scaling weak|strong]
 
-One process per GPU (torchrun for N>1, NCCL); per-GPU work fixed (weak
-scaling); `value` = all ranks' samples / max-over-ranks device time.
-See DESIGN.md section "Measurement" for every field.
+One process per GPU (torchrun for N>1, NCCL).  c1/c2: per-GPU work fixed
+(weak scaling, the config's N per GPU); c3/c4: the config's global N is
+sharded over the GPUs (strong scaling, as BASELINE specifies them).
+`value` = all ranks' samples / max-over-ranks device time, the same outer
+CUDA-event timer at every GPU count.  See DESIGN.md section "Measurement"
+for every field.
 """
 
 from __future__ import annotations
@@ -41,8 +45,41 @@ def parse():
     ap.add_argument("--gemm", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-samples", type=int, default=8192, help="bounded CPU-baseline sample (~10-20 s)")
+    ap.add_argument("--ref-samples", type=int, default=1024,
+                    help="--impl reference: samples per timed step (a bounded sample of the workload)")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="weak: the config's N per GPU; strong: the config's N over all GPUs "
+                         "(auto: strong for c3/c4, which BASELINE specifies sharded over 8 GPUs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
+
+
+DTYPE = "f32 (bf16x3 tensor-core products, fp32 accumulate; fp64 QoI, moments and reductions)"
+
+
+def scaling_mode(args):
+    if args.scaling != "auto":
+        return args.scaling
+    return "strong" if args.config in ("c3", "c4") else "weak"
+
+
+def shard_of(cfg, mode, world, rank):
+    """(n_global, start, count) of this rank's contiguous sample shard."""
+    from paper_2305_20053_b200.distributed import shard_range
+    if mode == "weak":
+        n_global = cfg.n_samples * world
+        return n_global, rank * cfg.n_samples, cfg.n_samples
+    a, b = shard_range(cfg.n_samples, world, rank)
+    return cfg.n_samples, a, b - a
+
+
+def config_block(cfg, mode, world, risks):
+    """The workload description; identical for both arms (--impl ours / reference)."""
+    n_global = cfg.n_samples * world if mode == "weak" else cfg.n_samples
+    return {"workload": cfg.name, "description": cfg.description, "global_samples": n_global,
+            "samples_per_gpu": n_global // world if n_global % world == 0 else n_global / world,
+            "risks": [f"{r['kind']}(beta={r['beta']})" for r in risks], "alpha": cfg.alpha,
+            "parallelism": f"dp{world} sample shards", "scaling": mode}
 
 
 def risks_for(cfg):
@@ -151,19 +188,28 @@ def cpu_cores():
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the reference's own CPU algorithm (oracle port)."""
+    """--impl reference: the reference's own CPU algorithm -- the forward-mode
+    chunked SurrogateEvaluator loop + saa_objective (riskopt.py:163-243),
+    restated in oracle/ (fp64 numpy, all BLAS threads) because the reference
+    package cannot travel to the GPU box -- on this workload.  Each step is a
+    bounded sample (--ref-samples) of the workload's samples; its cost is
+    linear in N, so samples/s is the workload's rate.  Rank 0 only."""
     if rank != 0:
         return
-    n_step = 256
+    mode = scaling_mode(args)
+    n_step = min(args.ref_samples, cfg.n_samples)
     from oracle import mrdino_ref as ref
     from paper_2305_20053_b200 import workloads as wl
     p = wl.make_problem(cfg.with_samples(n_step), seed=args.seed, count=n_step)
     m = ref.as_oracle(p)
     form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
     z = p.z.astype(np.float64)
+    chunk = 512
 
     def step():
-        Q, G = ref.evaluate_forward_mode(m, p.m_r, z, form)
+        parts = [ref.evaluate_forward_mode(m, p.m_r[a:a + chunk], z, form) for a in range(0, n_step, chunk)]
+        Q = np.concatenate([q for q, _ in parts])
+        G = np.concatenate([g for _, g in parts])
         for r in cfg.risks:
             ref.saa_objective(Q, G, z, ref.Risk(r.kind, beta=r.beta, eps=r.eps, alpha=cfg.alpha),
                               t=float(np.quantile(Q, r.beta)) if r.kind == "cvar" else None)
@@ -175,13 +221,16 @@ def run_reference(args, cfg, rank, world):
         step()
     dt = time.perf_counter() - t0
     value = n_step * args.steps / dt
-    sample = f"{n_step} samples of {cfg.name} per step (forward-mode z-Jacobian, fp64, numpy BLAS threads)"
+    sample = (f"{n_step} of the workload's {cfg.n_samples} samples per step, in the reference evaluator's "
+              f"{chunk}-sample chunks (forward-mode z-Jacobian, fp64 numpy BLAS, {cpu_cores()} threads); "
+              f"cost is linear in N")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": mode, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": cfg.name, "description": cfg.description, "n_samples_per_step": n_step},
+        "config": config_block(cfg, mode, world, risks_for(cfg)),
+        "samples_per_timed_step": n_step,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -211,13 +260,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     from paper_2305_20053_b200 import Engine
-    n_loc = cfg.n_samples
-    p = wl.make_problem(cfg, seed=args.seed, start=rank * n_loc, count=n_loc)
+    mode = scaling_mode(args)
+    n_global, start, n_loc = shard_of(cfg, mode, world, rank)
+    p = wl.make_problem(cfg, seed=args.seed, start=start, count=n_loc)
     eng = Engine(p, max_samples=n_loc, device=local_rank, gemm=args.gemm)
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     eng.set_tracking(p.c, p.q0)
-    eng.set_samples(torch.from_numpy(p.m_r).cuda(), global_offset=rank * n_loc)   # resident in HBM
+    eng.set_samples(torch.from_numpy(p.m_r).cuda(), global_offset=start)   # resident in HBM
     risks = risks_for(cfg)
     z = p.z.astype(np.float64)
     for d in risks:
@@ -233,7 +283,7 @@ def main():
     sharded = None
     if world > 1:
         from paper_2305_20053_b200.distributed import ShardedObjective, TorchComm
-        sharded = ShardedObjective(eng, TorchComm(dist), n_global=n_loc * world)
+        sharded = ShardedObjective(eng, TorchComm(dist), n_global=n_global)
 
     def step():
         if sharded is not None:
@@ -269,11 +319,11 @@ def main():
         barrier()
     launches = eng.kernel_launches() - launches0
     per_step_outer = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    # N = 1: the engine's own CUDA events on the launch stream around the
-    # evaluation graph (device work only; the outer events also hold the host
-    # staging / post-processing gaps between the graph and the event records).
-    # N > 1: the outer events, which include the NCCL exchanges of the step.
-    per_step = dev_steps if sharded is None else per_step_outer
+    # the same timer at every GPU count: CUDA events on the launch stream
+    # around each step call (device work, NCCL exchanges and the host's
+    # staging / result gaps between them).  N = 1 also reports the engine's
+    # in-graph device span (graph's first to last node) beside it.
+    per_step = per_step_outer
     ms = sum(per_step)
     if os.environ.get("SDN_BENCH_STEPS_DUMP"):
         print("per-step ms:", " ".join(f"{x:.4f}" for x in per_step), file=sys.stderr)
@@ -282,7 +332,7 @@ def main():
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_total = float(t_local.item())
     ms_step = ms_total / args.steps
-    value = n_loc * world * args.steps / (ms_total / 1e3)
+    value = n_global * args.steps / (ms_total / 1e3)
 
     # ---- profiled pass (same steps, per-launch events by kernel class)
     eng.profile(True)
@@ -306,17 +356,22 @@ def main():
     t_e2e = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = n_loc * world * args.steps / float(t_e2e.item())
-    kmax = sum(max(int(np.ceil((1 - r["beta"]) * n_loc * world - 1e-9)), 1) for r in risks
+    e2e_value = n_global * args.steps / float(t_e2e.item())
+    kmax = sum(max(int(np.ceil((1 - r["beta"]) * n_global - 1e-9)), 1) for r in risks
                if r["kind"] == "cvar_exact")
     h2d = 8 * cfg.d_z
-    d2h = len(risks) * 8 * (_lib.STATS_LEN + eng.partial_len()) + 4 * kmax
+    # results read back per step: moments + each risk's partials (fp64), and
+    # the exact-CVaR selection (int32 local indices on one GPU; the merged
+    # global candidate set, fp64 global index + mask byte, when sharded)
+    idx_bytes = 4 * kmax if world == 1 else 9 * world * kmax
+    d2h = len(risks) * 8 * (_lib.STATS_LEN + eng.partial_len()) + idx_bytes
 
     # ---- roofline of the dominant kernel class
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
-    peak_src = "measured bf16 sustained (MEASURED_PEAKS.json)" if peaks else "fallback"
+    # the timed loop is short (K steps of well under a second): the burst peak applies
+    peak_tf = peaks.get("bf16_tflops", 1590.0)
+    peak_src = "of measured bf16 burst (MEASURED_PEAKS.json)" if peaks else "of fallback (B200_PROFILING.md)"
     dom = max(prof, key=lambda k: prof[k]["ms"])
     d = prof[dom]
     step_ms_prof = sum(v["ms"] for v in prof.values())
@@ -326,7 +381,10 @@ def main():
                 "frac": achieved / peak_tf, "traffic": None, "kernel": dom,
                 "launches": d["launches"], "avg_launch_us": 1e3 * d["ms"] / max(d["launches"], 1),
                 "share_of_step": d["ms"] / step_ms_prof, "peak_source": peak_src,
-                "frac_of_bf16x3_effective": achieved / (peak_tf / 3.0)}
+                "frac_of_bf16x3_effective": achieved / (peak_tf / 3.0),
+                "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", peak_tf),
+                "note": "achieved = algorithmic flops (2 per MAC, no bf16x3 factor) / class time; every "
+                        "product issues 3 bf16 MMAs, so the attainable ceiling is peak/3"}
     else:
         bw = d["bytes"] / (d["ms"] / 1e3) / 1e9
         peak_bw = peaks.get("hbm_gbs", 6650.0)
@@ -355,16 +413,12 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
-            "timing": ("engine device span: CUDA events on the launch stream around each evaluation graph"
-                       if world == 1 else "CUDA events around each sharded step (NCCL included), max over ranks"),
-            "ms_per_step_outer_events": sum(per_step_outer) / args.steps,
+            "timing": "CUDA events on the launch stream around each step call (every N), max over ranks",
+            "ms_per_step_device_span": (sum(dev_steps) / args.steps) if dev_steps else None,
             "ms_per_step_median": float(np.median(per_step)),
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.name, "description": cfg.description, "n_samples_per_gpu": n_loc,
-                       "global_samples": n_loc * world,
-                       "risks": [f"{r['kind']}(beta={r['beta']})" for r in risks], "alpha": cfg.alpha,
-                       "gemm": args.gemm, "l2": "flushed between steps (256 MiB write, untimed)",
-                       "parallelism": f"dp{world} sample shards"},
+            "scaling": mode, "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+            "config": config_block(cfg, mode, world, risks),
+            "gemm": args.gemm, "l2": "flushed between steps (256 MiB write, untimed)",
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "Engine.eval_multi (host z in, host value/grad/indices out)"},
             "gpu_launches": int(launches),

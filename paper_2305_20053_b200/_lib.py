@@ -1,7 +1,11 @@
 """ctypes binding of libsaadino.so (the C ABI in include/saadino.h).
 
-The product path has no CPU fallback: if the shared library is missing this
-module raises at import, naming the build command.
+The library is mapped on first use (the first call through `lib`), not at
+import: the package's host-side modules (workloads, fileio, the reference-
+facing API types) import without the CUDA engine, so e.g. bench.py's CPU
+reference arm never maps it.  The product path has no CPU fallback: the
+first engine call raises ImportError, naming the build command, when the
+shared library is missing.
 """
 
 from __future__ import annotations
@@ -108,7 +112,22 @@ def _load():
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """Proxy that CDLLs libsaadino.so on first attribute access."""
+
+    _lib = None
+
+    def __getattr__(self, name):
+        if _LazyLib._lib is None:
+            _LazyLib._lib = _load()
+        return getattr(_LazyLib._lib, name)
+
+    @staticmethod
+    def loaded() -> bool:
+        return _LazyLib._lib is not None
+
+
+lib = _LazyLib()
 
 
 def check(rc: int, what: str = ""):

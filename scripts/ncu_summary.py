@@ -7,8 +7,24 @@ usage: python scripts/ncu_summary.py report.ncu-rep out.json
 import csv
 import io
 import json
+import re
 import subprocess
 import sys
+
+# tcgen05.mma kind::f16 M=128: 8192 bf16 flops per SM cycle (dense), i.e.
+# N/2 cycles per 128 x N x 16 instruction; its SS operands are 128 x 16 (A)
+# and N x 16 (B) bf16 = 32 + N/4 tensor-pipe SMEM wavefronts of 128 B
+def tc_busy_pct(name, wavefronts, cycles):
+    """Tensor-pipe busy share of the SM cycles, in the SM clock domain:
+    (MMAs per SM x N/2 cycles) / sm__cycles_elapsed.avg, with the MMA count
+    recovered from the tensor pipe's SMEM operand wavefronts and the kernel's
+    N tile (tc_gemm_kernel<BN, ...>)."""
+    m = re.search(r"tc_gemm_kernel<(\d+)", name)
+    if not m or not wavefronts or not cycles:
+        return None
+    bn = int(m.group(1))
+    n_mma = wavefronts / (32 + bn / 4)
+    return round(100.0 * n_mma * (bn / 2) / (148 * cycles), 2)
 
 
 def _f(x):
@@ -34,7 +50,7 @@ def summarise(rep):
         us = get(r, "gpu__time_duration.sum")
         unit = units[col["gpu__time_duration.sum"]]
         us = us / 1e3 if unit == "nsecond" else (us * 1e3 if unit == "msecond" else us)
-        hm = get(r, "TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg")
+        wf = get(r, "l1tex__data_pipe_tc_wavefronts_mem_shared.sum")
         cyc = get(r, "sm__cycles_elapsed.avg")
         name = r[col["Kernel Name"]]
         out.append({
@@ -45,7 +61,8 @@ def summarise(rep):
             "dram_read_MB": get(r, "dram__bytes_read.sum"),
             "dram_write_MB": get(r, "dram__bytes_write.sum"),
             "lts_pct": get(r, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
-            "tensor_active_pct": round(100.0 * hm / cyc, 2) if hm and cyc else None,
+            "tensor_busy_pct": tc_busy_pct(name, wf, cyc),
+            "tc_smem_operand_pct": get(r, "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
             "issue_active_pct": get(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "sm_clock_ghz": round(cyc / (us * 1e3), 3) if cyc and us else None,
         })
