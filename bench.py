@@ -285,10 +285,18 @@ def main():
         from paper_2305_20053_b200.distributed import ShardedObjective, TorchComm
         sharded = ShardedObjective(eng, TorchComm(dist), n_global=n_global)
 
-    def step():
+    def step(end_event=None):
+        """One evaluation; end_event (if given) is recorded on the stream right
+        after the device work is enqueued, before the host reads the results."""
         if sharded is not None:
-            return sharded.eval_multi(z, risks)
-        return eng.eval_multi(z, risks)
+            res = sharded.eval_multi(z, risks)
+            if end_event is not None:
+                end_event.record(stream)
+            return res
+        eng.eval_multi_launch(z, risks)
+        if end_event is not None:
+            end_event.record(stream)
+        return eng.eval_multi_wait()
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
 
@@ -312,17 +320,18 @@ def main():
         for i in range(args.steps):
             flush.zero_()                     # L2 flush between steps (untimed)
             starts[i].record(stream)
-            res = step()
-            ends[i].record(stream)
+            res = step(ends[i])
             if sharded is None:
                 dev_steps.append(eng.last_device_ms())
         barrier()
     launches = eng.kernel_launches() - launches0
     per_step_outer = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     # the same timer at every GPU count: CUDA events on the launch stream
-    # around each step call (device work, NCCL exchanges and the host's
-    # staging / result gaps between them).  N = 1 also reports the engine's
-    # in-graph device span (graph's first to last node) beside it.
+    # around each step (device work, NCCL exchanges and any host staging gaps
+    # between them; the end event is enqueued behind the step's last device
+    # work, so the host's wake-up to read the results is not in it).  N = 1
+    # also reports the engine's in-graph device span (graph's first to last
+    # node) beside it.
     per_step = per_step_outer
     ms = sum(per_step)
     if os.environ.get("SDN_BENCH_STEPS_DUMP"):
@@ -413,7 +422,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
-            "timing": "CUDA events on the launch stream around each step call (every N), max over ranks",
+            "timing": "CUDA events on the launch stream: start before each step's host staging, end enqueued behind its last device work (every N; N>1 includes the exchanges and host phase gaps), max over ranks",
             "ms_per_step_device_span": (sum(dev_steps) / args.steps) if dev_steps else None,
             "ms_per_step_median": float(np.median(per_step)),
             "scaling": mode, "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",

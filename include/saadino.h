@@ -98,8 +98,9 @@ typedef struct sdn_result {
   int64_t n_samples;         /* global sample count */
   int64_t n_selected;        /* CVaR exact: k; smoothed: active samples */
   double q_mean, q_var;      /* sample moments of Q (for reporting) */
-  int64_t n_refined;         /* rows of this rank re-evaluated in exact fp32
-                                (smoothed CVaR on tensor-core chains) */
+  int64_t n_refined;         /* rows of this rank re-evaluated in fp64 at the
+                                risk's decision boundary (smoothed-CVaR window,
+                                exact-CVaR threshold band); never skipped */
 } sdn_result;
 
 const char* sdn_last_error(void);
@@ -150,6 +151,14 @@ int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* r
  * NULL; cvar_idx receives each exact-CVaR selection in order, or NULL. */
 int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks,
                    sdn_result* res, double* grads, int64_t* cvar_idx);
+/* sdn_eval_multi in two halves: _launch enqueues the evaluation on the
+ * handle's stream (one CUDA-graph replay) and returns at once; _wait blocks
+ * until it is done and reads the results (same arguments as sdn_eval_multi;
+ * cvar_idx only if want_idx was set at launch).  Lets a caller record its own
+ * stream events around the device work, or overlap host work with it. */
+int sdn_eval_multi_launch(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks,
+                          int32_t want_idx);
+int sdn_eval_multi_wait(sdn_handle* h, sdn_result* res, double* grads, int64_t* cvar_idx);
 
 /* Per-sample evaluator protocol: Q (n) and G (n x d_z) as float64 host arrays. */
 int sdn_eval_samples(sdn_handle* h, const double* z, int32_t qoi, double* Q, double* G);
@@ -202,6 +211,12 @@ int sdn_eval_refine_band(sdn_handle* h);
  * together; finish each risk with sdn_eval_set_risk + sdn_eval_finish on its
  * slice.  (sdn_eval_multi does the same on one handle.) */
 int sdn_eval_keep_selection(sdn_handle* h, int32_t slot);
+/* The kept selection of `slot` as k ascending GLOBAL sample indices (host
+ * buffer idx_out, k = the risk's ceil-count over the global N).  Every rank
+ * holds the same merged selection, so every rank returns the same indices --
+ * the sharded counterpart of sdn_eval's cvar_idx (riskopt.py:73-82: the
+ * samples mc_cvar averages, ordered by index). */
+int sdn_eval_selection(sdn_handle* h, int32_t slot, int64_t k, int64_t* idx_out);
 int sdn_eval_backward_multi(sdn_handle* h, const sdn_risk* risks, int32_t n_risks, const double* stats_dev,
                             double* partials_dev);
 int sdn_eval_backward(sdn_handle* h, const double* stats_dev, double* partial_dev);

@@ -64,6 +64,8 @@ SIGNATURES = {
     "sdn_encode_fields": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _F, _F, C.c_float, C.c_int64, C.c_int32]),
     "sdn_eval": (C.c_int, [_P, _D, C.POINTER(Risk), C.POINTER(Result), _D, _I64]),
     "sdn_eval_multi": (C.c_int, [_P, _D, C.POINTER(Risk), C.c_int32, C.POINTER(Result), _D, _I64]),
+    "sdn_eval_multi_launch": (C.c_int, [_P, _D, C.POINTER(Risk), C.c_int32, C.c_int32]),
+    "sdn_eval_multi_wait": (C.c_int, [_P, C.POINTER(Result), _D, _I64]),
     "sdn_eval_samples": (C.c_int, [_P, _D, C.c_int32, _D, _D]),
     "sdn_forward_batch": (C.c_int, [_P, _F, _F, C.c_int64, _F]),
     "sdn_jacobian_batch": (C.c_int, [_P, _F, _F, C.c_int64, C.c_int32, _F]),
@@ -75,6 +77,7 @@ SIGNATURES = {
     "sdn_eval_select": (C.c_int, [_P, _P, C.c_int32, C.c_int64]),
     "sdn_eval_refine_band": (C.c_int, [_P]),
     "sdn_eval_keep_selection": (C.c_int, [_P, C.c_int32]),
+    "sdn_eval_selection": (C.c_int, [_P, C.c_int32, C.c_int64, _I64]),
     "sdn_train_setup": (C.c_int, [_P, _F, _F, _F, _F, C.c_int64, C.c_int32]),
     "sdn_train_set_params": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D), _D, _D, _D]),
     "sdn_train_set_mask": (C.c_int, [_P, C.POINTER(_D), C.POINTER(_D)]),

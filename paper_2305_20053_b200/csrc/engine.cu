@@ -154,6 +154,12 @@ struct sdn_handle {
   double* cand_vals = nullptr;  // candidate scratch (exact CVaR, multi-rank)
   double* cand_gidx = nullptr;
   uint8_t* cand_mask = nullptr;
+  int64_t n_cand = 0;           // candidates of the last sdn_eval_select
+  // sdn_eval_multi_launch -> sdn_eval_multi_wait
+  bool pending = false;
+  std::vector<sdn_risk> pend_risks;
+  int64_t pend_ktot = 0;
+  bool pend_idx = false;
   int64_t cand_cap = 0;
   // pinned staging
   double* hz = nullptr;         // d_z + SDN_RMAX (z, then each risk's t)
@@ -199,7 +205,7 @@ struct sdn_handle {
   int fwd_mtiles = 0;
   unsigned* ref_bar = nullptr;  // k_refine grid barrier
   int ref_grid = 0;
-  bool ref_ok = false;          // every layer input width <= REF_KC
+  bool ref_ok = false;          // the fp64 refinement can run (L <= REF_MAX_LAYERS)
   const double* ref_tp = nullptr;  // device-side t of the refinement window (set by refine_window)
   // side stream (overlapped exact-CVaR selection in sdn_eval_multi)
   cudaStream_t side = nullptr;
@@ -209,6 +215,8 @@ struct sdn_handle {
   std::vector<int*> x_rowidx, x_nact;
   std::vector<uint8_t*> x_mask;
   std::vector<int64_t> x_k;     // k of each kept selection (multi-rank phases)
+  std::vector<int64_t*> x_gidx; // global indices of each kept selection (ascending)
+  std::vector<int64_t> x_gcap;
   int sm_avail = 0;             // SMs the persistent GEMMs may use
   int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS (default clamped to a quarter of the SMs)
   bool no_overlap = false;               // env SDN_NO_OVERLAP=1
@@ -650,8 +658,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, REF_THREADS, sizeof(double) * REF_RB * REF_KC);
     h->ref_grid = h->num_sms;                     // one block per SM, all co-resident
-    h->ref_ok = per_sm >= 1 && h->L <= REF_MAX_LAYERS && h->r_m <= REF_KC;
-    for (int l = 1; l < h->L; ++l) h->ref_ok = h->ref_ok && h->w[l] <= REF_KC;
+    h->ref_ok = per_sm >= 1 && h->L <= REF_MAX_LAYERS;   // any width (K chunks), any band size (row chunks)
   }
   if ((rc = dalloc(h, &h->ref_blockcnt, h->num_sms))) return bail(rc);
   if ((rc = dalloc(h, &h->ref_rowidx, cap))) return bail(rc);
@@ -898,8 +905,8 @@ static int compact_rows(sdn_handle* h, int kind, double t, double eps, const dou
 // threshold (RISK_BAND_EXACT, value in thr_dev) -- are compacted and
 // re-evaluated by an fp64 chain on the same fp32 weights (the oracle's
 // arithmetic), and their Q replaced in place.  No host round trip: the band
-// count stays on the device (*count); more than ref_rows band rows skips the
-// refinement for that evaluation (reported as a negative n_refined).
+// count stays on the device (*count); bands of more than ref_rows rows run in
+// row chunks, and a large exact-CVaR band is reselected cooperatively.
 static int refine_band(sdn_handle* h, int kind, double t, double eps, bool dec, int* count,
                        uint8_t* mask = nullptr, double* Qt = nullptr, int64_t k = 0, bool do_refine = true) {
   do_refine = do_refine && h->ref_ok;
@@ -969,6 +976,11 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   if (risk->qoi == SDN_QOI_REDUCED && !h->have_form) return fail(SDN_ERR_STATE, "set_tracking first");
   if (risk->qoi == SDN_QOI_DECODED && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
   TRY(check_risk(risk));
+  // CVaR decisions need the fp64 boundary refinement: never
+  // return a possibly wrong selection silently
+  for (int i = 0; i < n_all; ++i)
+    if ((all[i].kind == SDN_RISK_CVAR_SMOOTH || all[i].kind == SDN_RISK_CVAR_EXACT) && !h->ref_ok && !h->no_refine)
+      return fail(SDN_ERR_STATE, "CVaR risks need the fp64 boundary refinement, which supports at most 16 layers");
   CU(cudaSetDevice(h->device));
   h->risk = *risk;
   h->fwd_risk = *risk;
@@ -1332,13 +1344,13 @@ struct SideScope {
 
 // refined-row count of a risk from the band log (read back with the
 // results): smoothed CVaR -> the forward window (slot 0), exact CVaR -> its
-// threshold band (exact_slot, -1 = none); > ref_rows means skipped (negative)
+// threshold band (exact_slot, -1 = none)
 static int64_t refined_count(sdn_handle* h, const sdn_risk& r, int exact_slot) {
   if (h->no_refine || !h->ref_ok) return 0;
   int64_t v = 0;
   if (r.kind == SDN_RISK_CVAR_SMOOTH) v = h->hband[0];
   else if (r.kind == SDN_RISK_CVAR_EXACT && exact_slot > 0) v = h->hband[exact_slot];
-  return v > h->ref_rows ? -v : v;
+  return v;
 }
 
 static int eval_finish(sdn_handle* h, const double* stats_dev, const double* partial_dev, sdn_result* res,
@@ -1474,9 +1486,9 @@ static void drop_graph(sdn_handle* h) {
   h->gkey.clear();
 }
 
-int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks, sdn_result* res,
-                   double* grads, int64_t* cvar_idx) {
-  if (!h || !z || !risks || n_risks < 1 || !res) return fail(SDN_ERR_ARG, "null argument");
+int sdn_eval_multi_launch(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks, int32_t want_idx_i) {
+  if (!h || !z || !risks || n_risks < 1) return fail(SDN_ERR_ARG, "null argument");
+  h->pending = false;
   if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
   if (n_risks > SDN_RMAX) return fail(SDN_ERR_ARG, "at most 8 risks per evaluation");
   int smooth = -1, any_grad = 0;
@@ -1541,7 +1553,7 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   // graph path (z and every risk's t are per-call graph parameters, staged
   // in pinned memory); not when profiling / tracing (host timers and syncs)
   const bool use_graph = h->use_graphs && !h->prof && !h->ref_trace;
-  const bool want_idx = cvar_idx != nullptr;
+  const bool want_idx = want_idx_i != 0;
   if (use_graph) {
     const std::vector<double> key = graph_key(h, risks, n_risks, want_idx);
     if (!h->gexec || key != h->gkey) {
@@ -1584,6 +1596,24 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
     TRY(enqueue_multi(h, z, risks, n_risks, want_idx, kks, koff, smooth, any_grad != 0));
     CU(cudaEventRecord(h->dev_ev[1], h->stream));
   }
+  h->pend_risks.assign(risks, risks + n_risks);
+  h->pend_ktot = ktot;
+  h->pend_idx = want_idx;
+  h->pending = true;
+  return SDN_OK;
+}
+
+// wait for the evaluation sdn_eval_multi_launch enqueued and read its results
+int sdn_eval_multi_wait(sdn_handle* h, sdn_result* res, double* grads, int64_t* cvar_idx) {
+  if (!h || !res) return fail(SDN_ERR_ARG, "null argument");
+  if (!h->pending) return fail(SDN_ERR_STATE, "sdn_eval_multi_launch first");
+  if (cvar_idx && !h->pend_idx) return fail(SDN_ERR_ARG, "indices were not requested at launch");
+  h->pending = false;
+  CU(cudaSetDevice(h->device));
+  const int n_risks = (int)h->pend_risks.size();
+  const sdn_risk* risks = h->pend_risks.data();
+  const int64_t ktot = h->pend_ktot;
+  const int plen = h->plen();
   CU(cudaStreamSynchronize(h->stream));
   {
     float t = 0.f;
@@ -1606,6 +1636,13 @@ int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_
   if (cvar_idx)
     for (int64_t j = 0; j < ktot; ++j) cvar_idx[j] = h->goff + h->hidx[j];
   return SDN_OK;
+}
+
+int sdn_eval_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int32_t n_risks, sdn_result* res,
+                   double* grads, int64_t* cvar_idx) {
+  if (!h || !z || !risks || n_risks < 1 || !res) return fail(SDN_ERR_ARG, "null argument");
+  TRY(sdn_eval_multi_launch(h, z, risks, n_risks, cvar_idx != nullptr));
+  return sdn_eval_multi_wait(h, res, grads, cvar_idx);
 }
 
 int sdn_last_device_ms(sdn_handle* h, double* ms) {
@@ -1677,6 +1714,7 @@ int sdn_eval_select(sdn_handle* h, const double* all_cand_dev, int32_t n_ranks, 
   k_unpack_candidates<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(n_ranks, k, all_cand_dev, h->cand_vals,
                                                                       h->cand_gidx);
   TRY(launch_topk(h, nc, k, h->cand_vals, h->cand_gidx, h->cand_mask, h->thr_dev));
+  h->n_cand = nc;
   CU(cudaMemsetAsync(h->sel, 0, std::max<int64_t>(h->n, 1), h->stream));
   k_scatter_selection<<<(unsigned)cdiv(nc, 256), 256, 0, h->stream>>>(nc, h->cand_mask, h->cand_gidx, h->goff,
                                                                       h->n, h->sel);
@@ -1713,6 +1751,28 @@ int sdn_eval_keep_selection(sdn_handle* h, int32_t slot) {
   if ((int)h->x_k.size() < slot + 1) h->x_k.resize(slot + 1, 0);
   CU(cudaMemcpyAsync(h->x_mask[slot], h->sel, std::max<int64_t>(h->n, 1), cudaMemcpyDeviceToDevice, h->stream));
   h->x_k[slot] = h->kk;
+  // the global selection (identical on every rank) as ascending global indices
+  if ((int)h->x_gidx.size() < slot + 1) { h->x_gidx.resize(slot + 1, nullptr); h->x_gcap.resize(slot + 1, 0); }
+  if (h->x_gcap[slot] < h->kk) {
+    int rc;
+    if ((rc = dalloc(h, &h->x_gidx[slot], h->kk))) return rc;
+    h->x_gcap[slot] = h->kk;
+  }
+  k_selection_gidx<<<1, 1024, 0, h->stream>>>(h->n_cand, h->cand_mask, h->cand_gidx, h->kk, h->x_gidx[slot]);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  return SDN_OK;
+}
+
+// multi-rank: the kept exact-CVaR selection of `slot` as k ascending GLOBAL
+// sample indices (host buffer; every rank returns the same set)
+int sdn_eval_selection(sdn_handle* h, int32_t slot, int64_t k, int64_t* idx_out) {
+  if (!h || !idx_out || slot < 0) return fail(SDN_ERR_ARG, "bad argument");
+  if (slot >= (int)h->x_gidx.size() || !h->x_gidx[slot]) return fail(SDN_ERR_STATE, "eval_keep_selection first");
+  if (k != h->x_k[slot]) return fail(SDN_ERR_ARG, "k does not match the kept selection");
+  CU(cudaSetDevice(h->device));
+  CU(cudaMemcpyAsync(idx_out, h->x_gidx[slot], sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
   return SDN_OK;
 }
 

@@ -140,7 +140,7 @@ k_sum_rows(int nb, int w, const double* __restrict__ part, double* __restrict__ 
 // REFINE_REL bounds the chain's Q error with ~6x margin over the largest
 // measured (1.7e-5 relative at c3).
 constexpr double REFINE_REL = 1e-4;
-constexpr int REFINE_ROWS = 4096;     // band rows per evaluation (k_refine reselect: <= 16 x 256)
+constexpr int REFINE_ROWS = 4096;     // band rows per k_refine row chunk (larger bands run in several chunks)
 SDN_DEV bool in_band(double q, double t, double eps) {       // smoothed CVaR window
   double d = REFINE_REL * fabs(q) + 1e-300;
   double x = q - t;
@@ -711,6 +711,32 @@ __global__ void k_unpack_candidates(int n_ranks, int64_t k, const double* __rest
     vals[e] = all[r * 2 * k + j];
     gidx[e] = all[r * 2 * k + k + j];
   }
+}
+
+// global selection over the gathered candidates -> its global indices in
+// ascending order.  Candidates arrive rank-major and, within a rank, in
+// ascending local row order (ordered compaction), so an ordered compaction of
+// the mask is already sorted.  One block of 1024 threads.
+__global__ void __launch_bounds__(1024)
+k_selection_gidx(int64_t ncand, const uint8_t* __restrict__ cmask, const double* __restrict__ gidx,
+                 int64_t k, int64_t* __restrict__ out) {
+  __shared__ int s_w[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t base_out = 0;
+  for (int64_t base = 0; base < ncand; base += 1024) {
+    const int64_t e = base + tid;
+    const bool f = e < ncand && cmask[e] && gidx[e] >= 0.0;
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_w[warp] = __popc(b);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) { const int c = s_w[w]; before += (w < warp) ? c : 0; tot += c; }
+    const int64_t pos = base_out + before + __popc(b & ((1u << lane) - 1u));
+    if (f && pos < k) out[pos] = (int64_t)gidx[e];
+    base_out += tot;
+    __syncthreads();
+  }
+  for (int64_t p = base_out + tid; p < k; p += 1024) out[p] = -1;   // (never: the merge selects k)
 }
 
 // global selection mask over candidates -> local selection mask

@@ -19,9 +19,10 @@
 namespace sdn {
 
 constexpr int REF_RB = 8;             // rows per pass (= warps per block: warp j stages row j)
-constexpr int REF_KC = 1024;          // max layer input width on the fused path
+constexpr int REF_KC = 1024;          // layer input width per K chunk (wider layers run in chunks)
 constexpr int REF_THREADS = 256;
 constexpr int REF_MAX_LAYERS = 16;
+constexpr int REF_RESELECT_SMALL = 256;   // band rows up to which one block ranks them O(m^2)
 
 struct RefineLayer {
   const float* W;     // N x K (layer 0: W1[:, :r_m] unscaled)
@@ -168,31 +169,38 @@ SDN_DEV double ref_column(const double* xs, const float (&wf)[KC / 32], int K, i
 
 // one pass of up to REF_RB band rows through layer ly (stage the rows in
 // shared memory, then this warp's output columns)
+// Layers wider than REF_KC run in K chunks [k0, k0 + Kc): each chunk's
+// partial dot products are accumulated in `out` (fp64; the same lane owns the
+// same (row, column) entry in every chunk), the epilogue runs on the last.
+// ridx: the band rows of the current row chunk (ordered compaction).
 template <int KC>
 SDN_DEV void ref_rows(const RefineArgs& a, const RefineLayer& ly, double* xs, int warp, int lane, int gw, int nw,
-                      int r0, int rb, bool first, bool last, const double* in64, double* out) {
+                      const int* ridx, int r0, int rb, bool first, bool last, const double* in64, double* out,
+                      int k0 = 0, int Kc = -1) {
   const int K = ly.K, N = ly.N;
+  if (Kc < 0) Kc = K;
+  const bool kfirst = k0 == 0, klast = k0 + Kc >= K;
   {                                          // warp j stages row r0 + j (clamped)
     const int rj = r0 + min(warp, rb - 1);
     if (first) {                              // x = m_r * in_scale (exact in fp64, as the oracle)
-      const float* src = a.MR + (int64_t)__ldcg(a.rowidx + rj) * K;
+      const float* src = a.MR + (int64_t)__ldcg(ridx + rj) * K + k0;
       float v[KC / 32], sc[KC / 32];
 #pragma unroll
       for (int u = 0; u < KC / 32; ++u) {
-        v[u] = __ldg(src + min(lane + 32 * u, K - 1));
-        sc[u] = __ldg(a.iscale + min(lane + 32 * u, K - 1));
+        v[u] = __ldg(src + min(lane + 32 * u, Kc - 1));
+        sc[u] = __ldg(a.iscale + k0 + min(lane + 32 * u, Kc - 1));
       }
 #pragma unroll
       for (int u = 0; u < KC / 32; ++u)
-        if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = (double)v[u] * (double)sc[u];
+        if (lane + 32 * u < Kc) xs[warp * REF_KC + lane + 32 * u] = (double)v[u] * (double)sc[u];
     } else {
-      const double* src = in64 + (int64_t)rj * K;
+      const double* src = in64 + (int64_t)rj * K + k0;
       double v[KC / 32];
 #pragma unroll
-      for (int u = 0; u < KC / 32; ++u) v[u] = __ldcg(src + min(lane + 32 * u, K - 1));
+      for (int u = 0; u < KC / 32; ++u) v[u] = __ldcg(src + min(lane + 32 * u, Kc - 1));
 #pragma unroll
       for (int u = 0; u < KC / 32; ++u)
-        if (lane + 32 * u < K) xs[warp * REF_KC + lane + 32 * u] = v[u];
+        if (lane + 32 * u < Kc) xs[warp * REF_KC + lane + 32 * u] = v[u];
     }
   }
   __syncthreads();
@@ -201,27 +209,34 @@ SDN_DEV void ref_rows(const RefineArgs& a, const RefineLayer& ly, double* xs, in
   // loaded while the current one is reduced (software pipeline)
   float wf[KC / 32];
   int c = gw;
-  if (c < N) ref_load_w<KC>(ly.W + (int64_t)c * K, K, lane, wf);
+  if (c < N) ref_load_w<KC>(ly.W + (int64_t)c * K + k0, Kc, lane, wf);
   for (; c < N; c += nw) {
     float wn[KC / 32];
-    if (c + nw < N) ref_load_w<KC>(ly.W + (int64_t)(c + nw) * K, K, lane, wn);
+    if (c + nw < N) ref_load_w<KC>(ly.W + (int64_t)(c + nw) * K + k0, Kc, lane, wn);
     double v;
-    if (rb <= 2) v = ref_column<2, KC>(xs, wf, K, lane);
-    else if (rb <= 4) v = ref_column<4, KC>(xs, wf, K, lane);
-    else v = ref_column<8, KC>(xs, wf, K, lane);
+    if (rb <= 2) v = ref_column<2, KC>(xs, wf, Kc, lane);
+    else if (rb <= 4) v = ref_column<4, KC>(xs, wf, Kc, lane);
+    else v = ref_column<8, KC>(xs, wf, Kc, lane);
     const int j = lane >> 2;                 // row whose total this lane holds
     if ((lane & 3) == 0 && j < rb) {
-      const double S = v + (first ? a.zb64[c] : (double)ly.b[c]);
-      double o;
-      if (last) {
-        o = (double)a.omean[c] + (double)a.ostd[c] * S;
-      } else if (a.softmax) {
-        o = S;                                        // normalised by the row pass below
+      double* dst = out + (int64_t)(r0 + j) * N + c;
+      if (!kfirst) v += *dst;                  // earlier K chunks (written by this lane)
+      if (!klast) {
+        *dst = v;
       } else {
-        o = act64(a.act, S);
-        if (ly.resid) o += xs[j * REF_KC + c];       // resid: K == N
+        const double S = v + (first ? a.zb64[c] : (double)ly.b[c]);
+        double o;
+        if (last) {
+          o = (double)a.omean[c] + (double)a.ostd[c] * S;
+        } else if (a.softmax) {
+          o = S;                                        // normalised by the row pass below
+        } else {
+          o = act64(a.act, S);
+          if (ly.resid)                                 // resid: K == N
+            o += (kfirst && c < Kc) ? xs[j * REF_KC + c] : __ldcg(in64 + (int64_t)(r0 + j) * K + c);
+        }
+        *dst = o;
       }
-      out[(int64_t)(r0 + j) * N + c] = o;
     }
 #pragma unroll
     for (int u = 0; u < KC / 32; ++u) wf[u] = wn[u];
@@ -229,24 +244,228 @@ SDN_DEV void ref_rows(const RefineArgs& a, const RefineLayer& ly, double* xs, in
   __syncthreads();
 }
 
+struct RefShared {
+  int w[REF_THREADS / 32], m[REF_THREADS / 32];
+  unsigned gen;
+  int need;
+  unsigned hist[256];
+  unsigned long long prefix;
+  long long krem;
+  unsigned long long mm[2][REF_THREADS / 32];
+};
+
+// Cooperative exact top-k over n items (value desc, position asc): MSD radix
+// select on order-preserving keys, from the first byte in which the keys
+// differ; per-block 256-bin histograms summed by every block (identical
+// decisions), ties taken in position order via per-block counts of
+// threshold-equal keys.  key(i) -> dkey, set(i, selected).  Returns the
+// threshold value (the k-th largest), also written to *thr_out if given.
+// With trailing = false the caller must barrier before reusing blockcnt.
+// grid scratch of the cooperative select (a few pointers: passing the whole
+// RefineArgs by reference to a non-inlined function would copy it to the stack)
+struct SelScratch {
+  unsigned* bar;
+  unsigned* ghist;
+  unsigned long long* gmm;
+  int* blockcnt;
+  unsigned long long* trace;
+};
+
+template <class KeyF, class SetF>
+__device__ __noinline__ double coop_select(SelScratch a, RefShared& S, unsigned& gen, int64_t n, int64_t k, KeyF key,
+                                           SetF set, double* thr_out, bool trailing) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t per = (n + G - 1) / G;            // contiguous slice per block (position order)
+  const int64_t lo = min((int64_t)blockIdx.x * per, n), hi = min(lo + per, n);
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
+    const unsigned long long kk = key(i);
+    kmin = min(kmin, kk);
+    kmax = max(kmax, kk);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) { S.mm[0][warp] = kmin; S.mm[1][warp] = kmax; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < REF_THREADS / 32; ++w) { kmin = min(kmin, S.mm[0][w]); kmax = max(kmax, S.mm[1][w]); }
+    a.gmm[blockIdx.x] = kmin;
+    a.gmm[G + blockIdx.x] = kmax;
+  }
+  grid_barrier(a.bar, gen);
+  REF_STAMP(1);
+  {                                                // parallel loads, warp reductions
+    unsigned long long x = ~0ull, y = 0ull;
+    for (unsigned b = tid; b < G; b += REF_THREADS) { x = min(x, __ldcg(a.gmm + b)); y = max(y, __ldcg(a.gmm + G + b)); }
+    for (int o = 16; o > 0; o >>= 1) {
+      x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+      y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
+    }
+    __syncthreads();
+    if (lane == 0) { S.mm[0][warp] = x; S.mm[1][warp] = y; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    unsigned long long x = S.mm[0][0], y = S.mm[1][0];
+    for (int w = 1; w < REF_THREADS / 32; ++w) { x = min(x, S.mm[0][w]); y = max(y, S.mm[1][w]); }
+    const int cp = (x == y) ? 8 : __clzll((long long)(x ^ y)) / 8;
+    S.w[0] = cp;
+    S.prefix = (cp == 0) ? 0ull : (cp >= 8 ? x : (x & (~0ull << (64 - 8 * cp))));
+    S.krem = k;
+  }
+  __syncthreads();
+  const int first = S.w[0];
+  unsigned long long himask = (first == 0) ? 0ull : (first >= 8 ? ~0ull : (~0ull << (64 - 8 * first)));
+  bool early = false;
+  unsigned long long tmin = 0ull;
+  if (tid == 0) S.need = 0;
+  __syncthreads();
+  for (int pass = first; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    const unsigned long long prefix = S.prefix;
+    for (int d = tid; d < 256; d += REF_THREADS) S.hist[d] = 0;
+    __syncthreads();
+    for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
+      const unsigned long long kk = key(i);
+      if ((kk & himask) == prefix) atomicAdd(&S.hist[(unsigned)(kk >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    unsigned* gh = a.ghist + (size_t)(pass & 1) * G * 256;
+    for (int d = tid; d < 256; d += REF_THREADS) gh[blockIdx.x * 256 + d] = S.hist[d];
+    grid_barrier(a.bar, gen);
+    for (int d = tid; d < 256; d += REF_THREADS) {
+      unsigned c = 0;
+#pragma unroll 16
+      for (unsigned b = 0; b < G; ++b) c += __ldcg(gh + b * 256 + d);   // unrolled: loads in flight
+      S.hist[d] = c;
+    }
+    __syncthreads();
+    if (warp == 0) {                               // lane l owns digits 255-8l .. 248-8l
+      unsigned c[8], t8 = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { c[q] = S.hist[255 - 8 * lane - q]; t8 += c[q]; }
+      unsigned incl = t8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const long long krem = S.krem;
+      const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= krem);
+      const int L = hit ? __ffs(hit) - 1 : 31;
+      if (lane == L) {
+        long long cum = (long long)(incl - t8);
+        int d = 255 - 8 * lane;
+        for (int q = 0; q < 8; ++q) {
+          d = 255 - 8 * lane - q;
+          if (cum + (long long)c[q] >= krem || q == 7) break;
+          cum += c[q];
+        }
+        S.krem = krem - cum;
+        S.prefix = prefix | ((unsigned long long)d << shift);
+        S.need = (krem - cum == (long long)c[(255 - 8 * lane) - d]) ? 1 : 0;   // whole bucket taken
+      }
+    }
+    himask |= (0xFFull << shift);
+    __syncthreads();
+    REF_STAMP(2 + pass);
+    if (S.need && pass < 7) {
+      // early exit: the k-th falls at the bottom of a bucket that is taken
+      // whole, so the selection is {key >= Tlow}; the threshold value (the
+      // band centre) is the smallest selected key
+      const unsigned long long Tlow = S.prefix;
+      unsigned long long mn = ~0ull;
+      for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
+        const unsigned long long kk = key(i);
+        set(i, kk >= Tlow);
+        if (kk >= Tlow) mn = min(mn, kk);
+      }
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      __syncthreads();
+      if (lane == 0) S.mm[0][warp] = mn;
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < REF_THREADS / 32; ++w) mn = min(mn, S.mm[0][w]);
+        a.gmm[blockIdx.x] = mn;
+      }
+      grid_barrier(a.bar, gen);
+      mn = ~0ull;
+      for (unsigned b = tid; b < G; b += REF_THREADS) mn = min(mn, __ldcg(a.gmm + b));
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      __syncthreads();
+      if (lane == 0) S.mm[0][warp] = mn;
+      __syncthreads();
+      for (int w = 0; w < REF_THREADS / 32; ++w) mn = min(mn, S.mm[0][w]);
+      early = true;
+      tmin = mn;
+      break;
+    }
+  }
+  double thr;
+  if (early) {
+    thr = dkey_inv(tmin);
+    if (thr_out && blockIdx.x == 0 && tid == 0) *thr_out = thr;
+    REF_STAMP(10);
+    return thr;                                    // (blockcnt untouched on this path)
+  }
+  const unsigned long long T = S.prefix;
+  const long long need = S.krem;                   // threshold-equal keys to take, lowest position first
+  thr = dkey_inv(T);
+  if (thr_out && blockIdx.x == 0 && tid == 0) *thr_out = thr;
+  int eq = 0;
+  for (int64_t i = lo + tid; i < hi; i += REF_THREADS) eq += (key(i) == T) ? 1 : 0;
+  eq = warp_sum_i(eq);
+  if (lane == 0) S.w[warp] = eq;
+  __syncthreads();
+  if (tid == 0) {
+    int e = 0;
+    for (int w = 0; w < REF_THREADS / 32; ++w) e += S.w[w];
+    a.blockcnt[blockIdx.x] = e;
+  }
+  grid_barrier(a.bar, gen);
+  long long run = 0;                               // threshold-equal keys in earlier blocks
+  {
+    int pr = 0;
+    for (unsigned b = tid; b < blockIdx.x; b += REF_THREADS) pr += __ldcg(a.blockcnt + b);
+    pr = warp_sum_i(pr);
+    __syncthreads();
+    if (lane == 0) S.w[warp] = pr;
+    __syncthreads();
+    for (int w = 0; w < REF_THREADS / 32; ++w) run += S.w[w];
+    __syncthreads();
+  }
+  for (int64_t base = lo; base < hi; base += REF_THREADS) {
+    const int64_t i = base + tid;
+    const unsigned long long kk = i < hi ? key(i) : 0ull;
+    const bool e = i < hi && kk == T;
+    const unsigned bal = __ballot_sync(0xffffffffu, e);
+    int t2;
+    const int wb = block_excl(S.w, warp, lane, __popc(bal), t2);
+    const long long rank = run + wb + __popc(bal & ((1u << lane) - 1u));
+    if (i < hi) set(i, kk > T || (e && rank < need));
+    run += t2;
+  }
+  REF_STAMP(10);
+  if (trailing) grid_barrier(a.bar, gen);          // blockcnt is reused by the caller
+  return thr;
+}
+
 __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   extern __shared__ double xs[];                  // REF_RB x REF_KC
-  __shared__ int s_w[REF_THREADS / 32], s_m[REF_THREADS / 32];
-  __shared__ unsigned s_gen;
-  __shared__ int s_need;
-  __shared__ unsigned s_hist[256];
-  __shared__ unsigned long long s_prefix;
-  __shared__ long long s_krem;
-  __shared__ unsigned long long s_mm[2][REF_THREADS / 32];
+  __shared__ RefShared S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned G = gridDim.x;
   REF_STAMP(0);
-  if (tid == 0) s_gen = *(volatile unsigned*)&a.bar[1];
+  if (tid == 0) S.gen = *(volatile unsigned*)&a.bar[1];
   __syncthreads();
-  unsigned gen = s_gen;
+  unsigned gen = S.gen;
   const int64_t per = (a.n + G - 1) / G;          // contiguous slice per block (index order)
   const int64_t lo = min((int64_t)blockIdx.x * per, a.n), hi = min(lo + per, a.n);
   const int gw = blockIdx.x * (REF_THREADS / 32) + warp, nw = G * (REF_THREADS / 32);
+  const SelScratch sc{a.bar, a.ghist, a.gmm, a.blockcnt, a.trace};
   if (a.refine) {                                 // W rows of every layer -> L2 now (overlaps phases 0-1)
     for (int l = 0; l < a.L; ++l) {
       const RefineLayer& ly = a.layer[l];
@@ -258,185 +477,14 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     }
   }
 
-  // ---- 0. exact top-k (k > 0): cooperative MSD radix select on order-
-  // preserving keys, from the first byte in which the keys differ; per-block
-  // 256-bin histograms summed by every block (identical decisions), ties
-  // taken in index order via per-block counts of threshold-equal keys
+  // ---- 0. exact top-k (k > 0) over Q -> mask and the threshold (*tdev)
   double thr = 0.0;
   if (a.k > 0) {
-    unsigned long long kmin = ~0ull, kmax = 0ull;
-    for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
-      const unsigned long long key = dkey(a.Q[i]);
-      kmin = min(kmin, key);
-      kmax = max(kmax, key);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if (lane == 0) { s_mm[0][warp] = kmin; s_mm[1][warp] = kmax; }
-    __syncthreads();
-    if (tid == 0) {
-      for (int w = 1; w < REF_THREADS / 32; ++w) { kmin = min(kmin, s_mm[0][w]); kmax = max(kmax, s_mm[1][w]); }
-      a.gmm[blockIdx.x] = kmin;
-      a.gmm[G + blockIdx.x] = kmax;
-    }
-    grid_barrier(a.bar, gen);
-    REF_STAMP(1);
-    {                                              // parallel loads, warp reductions
-      unsigned long long x = ~0ull, y = 0ull;
-      for (unsigned b = tid; b < G; b += REF_THREADS) { x = min(x, __ldcg(a.gmm + b)); y = max(y, __ldcg(a.gmm + G + b)); }
-      for (int o = 16; o > 0; o >>= 1) {
-        x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
-        y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
-      }
-      __syncthreads();
-      if (lane == 0) { s_mm[0][warp] = x; s_mm[1][warp] = y; }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      unsigned long long x = s_mm[0][0], y = s_mm[1][0];
-      for (int w = 1; w < REF_THREADS / 32; ++w) { x = min(x, s_mm[0][w]); y = max(y, s_mm[1][w]); }
-      const int cp = (x == y) ? 8 : __clzll((long long)(x ^ y)) / 8;
-      s_w[0] = cp;
-      s_prefix = (cp == 0) ? 0ull : (cp >= 8 ? x : (x & (~0ull << (64 - 8 * cp))));
-      s_krem = a.k;
-    }
-    __syncthreads();
-    const int first = s_w[0];
-    unsigned long long himask = (first == 0) ? 0ull : (first >= 8 ? ~0ull : (~0ull << (64 - 8 * first)));
-    bool early = false;
-    unsigned long long tmin = 0ull;
-    if (tid == 0) s_need = 0;
-    __syncthreads();
-    for (int pass = first; pass < 8; ++pass) {
-      const int shift = 56 - 8 * pass;
-      const unsigned long long prefix = s_prefix;
-      for (int d = tid; d < 256; d += REF_THREADS) s_hist[d] = 0;
-      __syncthreads();
-      for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
-        const unsigned long long key = dkey(a.Q[i]);
-        if ((key & himask) == prefix) atomicAdd(&s_hist[(unsigned)(key >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      unsigned* gh = a.ghist + (size_t)(pass & 1) * G * 256;
-      for (int d = tid; d < 256; d += REF_THREADS) gh[blockIdx.x * 256 + d] = s_hist[d];
-      grid_barrier(a.bar, gen);
-      for (int d = tid; d < 256; d += REF_THREADS) {
-        unsigned c = 0;
-#pragma unroll 16
-        for (unsigned b = 0; b < G; ++b) c += __ldcg(gh + b * 256 + d);   // unrolled: loads in flight
-        s_hist[d] = c;
-      }
-      __syncthreads();
-      if (warp == 0) {                             // lane l owns digits 255-8l .. 248-8l
-        unsigned c[8], t8 = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) { c[i] = s_hist[255 - 8 * lane - i]; t8 += c[i]; }
-        unsigned incl = t8;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const long long krem = s_krem;
-        const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= krem);
-        const int L = hit ? __ffs(hit) - 1 : 31;
-        if (lane == L) {
-          long long cum = (long long)(incl - t8);
-          int d = 255 - 8 * lane;
-          for (int i = 0; i < 8; ++i) {
-            d = 255 - 8 * lane - i;
-            if (cum + (long long)c[i] >= krem || i == 7) break;
-            cum += c[i];
-          }
-          s_krem = krem - cum;
-          s_prefix = prefix | ((unsigned long long)d << shift);
-          s_need = (krem - cum == (long long)c[(255 - 8 * lane) - d]) ? 1 : 0;   // whole bucket taken
-        }
-      }
-      himask |= (0xFFull << shift);
-      __syncthreads();
-      REF_STAMP(2 + pass);
-      if (s_need && pass < 7) {
-        // early exit: the k-th falls at the bottom of a bucket that is taken
-        // whole, so the selection is {key >= Tlow}; the threshold value (the
-        // band centre) is the smallest selected key
-        const unsigned long long Tlow = s_prefix;
-        unsigned long long mn = ~0ull;
-        for (int64_t i = lo + tid; i < hi; i += REF_THREADS) {
-          const unsigned long long key = dkey(a.Q[i]);
-          a.mask[i] = key >= Tlow ? 1 : 0;
-          if (key >= Tlow) mn = min(mn, key);
-        }
-        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        __syncthreads();
-        if (lane == 0) s_mm[0][warp] = mn;
-        __syncthreads();
-        if (tid == 0) {
-          for (int w = 1; w < REF_THREADS / 32; ++w) mn = min(mn, s_mm[0][w]);
-          a.gmm[blockIdx.x] = mn;
-        }
-        grid_barrier(a.bar, gen);
-        mn = ~0ull;
-        for (unsigned b = tid; b < G; b += REF_THREADS) mn = min(mn, __ldcg(a.gmm + b));
-        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        __syncthreads();
-        if (lane == 0) s_mm[0][warp] = mn;
-        __syncthreads();
-        for (int w = 0; w < REF_THREADS / 32; ++w) mn = min(mn, s_mm[0][w]);
-        early = true;
-        tmin = mn;
-        break;
-      }
-    }
-    if (early) {
-      thr = dkey_inv(tmin);
-      if (blockIdx.x == 0 && tid == 0) *const_cast<double*>(a.tdev) = thr;
-      REF_STAMP(10);
-      if (!a.refine) return;
-    } else {
-    const unsigned long long T = s_prefix;
-    const long long need = s_krem;                 // threshold-equal keys to take, lowest index first
-    thr = dkey_inv(T);
-    if (blockIdx.x == 0 && tid == 0) *const_cast<double*>(a.tdev) = thr;
-    int eq = 0;
-    for (int64_t i = lo + tid; i < hi; i += REF_THREADS) eq += (dkey(a.Q[i]) == T) ? 1 : 0;
-    eq = warp_sum_i(eq);
-    if (lane == 0) s_w[warp] = eq;
-    __syncthreads();
-    if (tid == 0) {
-      int e = 0;
-      for (int w = 0; w < REF_THREADS / 32; ++w) e += s_w[w];
-      a.blockcnt[blockIdx.x] = e;
-    }
-    grid_barrier(a.bar, gen);
-    long long run = 0;                             // threshold-equal keys in earlier blocks
-    {
-      int pr = 0;
-      for (unsigned b = tid; b < blockIdx.x; b += REF_THREADS) pr += __ldcg(a.blockcnt + b);
-      pr = warp_sum_i(pr);
-      __syncthreads();
-      if (lane == 0) s_w[warp] = pr;
-      __syncthreads();
-      for (int w = 0; w < REF_THREADS / 32; ++w) run += s_w[w];
-      __syncthreads();
-    }
-    for (int64_t base = lo; base < hi; base += REF_THREADS) {
-      const int64_t i = base + tid;
-      const unsigned long long key = i < hi ? dkey(a.Q[i]) : 0ull;
-      const bool e = i < hi && key == T;
-      const unsigned bal = __ballot_sync(0xffffffffu, e);
-      int t2;
-      const int wb = block_excl(s_w, warp, lane, __popc(bal), t2);
-      const long long rank = run + wb + __popc(bal & ((1u << lane) - 1u));
-      if (i < hi) a.mask[i] = (key > T || (e && rank < need)) ? 1 : 0;
-      run += t2;
-    }
-    REF_STAMP(10);
+    const double* Qp = a.Q;
+    uint8_t* mk = a.mask;
+    thr = coop_select(sc, S, gen, a.n, a.k, [&](int64_t i) { return (unsigned long long)dkey(Qp[i]); },
+                      [&](int64_t i, bool v) { mk[i] = v ? 1 : 0; }, const_cast<double*>(a.tdev), a.refine != 0);
     if (!a.refine) return;
-    grid_barrier(a.bar, gen);                      // blockcnt is reused below
-    }
   }
 
   // ---- 1. band flags and ordered compaction
@@ -453,7 +501,7 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     mine += (lane == 0) ? __popc(b) : 0;
   }
   int tot;
-  (void)block_excl(s_w, warp, lane, mine, tot);
+  (void)block_excl(S.w, warp, lane, mine, tot);
   if (tid == 0) a.blockcnt[blockIdx.x] = tot;
   grid_barrier(a.bar, gen);
   int off = 0, m = 0;
@@ -467,9 +515,9 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     po = warp_sum_i(po);
     pm = warp_sum_i(pm);
     __syncthreads();
-    if (lane == 0) { s_w[warp] = po; s_m[warp] = pm; }
+    if (lane == 0) { S.w[warp] = po; S.m[warp] = pm; }
     __syncthreads();
-    for (int w = 0; w < REF_THREADS / 32; ++w) { off += s_w[w]; m += s_m[w]; }
+    for (int w = 0; w < REF_THREADS / 32; ++w) { off += S.w[w]; m += S.m[w]; }
     __syncthreads();
   }
   for (int64_t base = lo; base < hi; base += REF_THREADS) {
@@ -477,68 +525,76 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     const bool f = i < hi && band(i);
     const unsigned b = __ballot_sync(0xffffffffu, f);
     int t2;
-    const int wb = block_excl(s_w, warp, lane, __popc(b), t2);
+    const int wb = block_excl(S.w, warp, lane, __popc(b), t2);
     if (f) a.rowidx[off + wb + __popc(b & ((1u << lane) - 1u))] = (int)i;
     off += t2;
   }
   if (blockIdx.x == 0 && tid == 0) *a.count = m;
   REF_STAMP(11);
-  if (m == 0 || m > a.cap_rows) return;          // uniform: every block computed the same m
+  if (m == 0) return;                            // uniform: every block computed the same m
   grid_barrier(a.bar, gen);
   REF_STAMP(12);
 
-  // ---- 2. fp64 chain over the m band rows
-  for (int l = 0; l < a.L; ++l) {
-    const RefineLayer& ly = a.layer[l];
-    const int K = ly.K, N = ly.N;
-    const bool first = l == 0, last = l == a.L - 1;
-    const double* in64 = first ? nullptr : a.buf[(l - 1) & 1];
-    double* out = a.buf[l & 1];
-    for (int r0 = 0; r0 < m; r0 += REF_RB) {
-      const int rb = min(REF_RB, m - r0);
-      if (K <= 128) ref_rows<128>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
-      else if (K <= 256) ref_rows<256>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
-      else if (K <= 512) ref_rows<512>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
-      else ref_rows<1024>(a, ly, xs, warp, lane, gw, nw, r0, rb, first, last, in64, out);
-    }
-    REF_STAMP(13 + 2 * l);
-    grid_barrier(a.bar, gen);
-    REF_STAMP(14 + 2 * l);
-    if (a.softmax && !last) {                      // per-row softmax (+ residual), one warp per row
-      for (int r = gw; r < m; r += nw) {
-        double* o = out + (int64_t)r * N;
-        double mx = -INFINITY;
-        for (int c = lane; c < N; c += 32) mx = fmax(mx, __ldcg(o + c));
-        for (int q = 16; q > 0; q >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, q));
-        double sum = 0.0;
-        for (int c = lane; c < N; c += 32) sum += exp(__ldcg(o + c) - mx);
-        sum = warp_sum(sum);
-        for (int c = lane; c < N; c += 32) {
-          const double v = exp(__ldcg(o + c) - mx) / sum;
-          o[c] = ly.resid ? __ldcg(in64 + (int64_t)r * K + c) + v : v;
-        }
+  // ---- 2./3. fp64 chain + QoI over the m band rows, in row chunks of
+  // cap_rows (the ping-pong buffers' size); layers wider than REF_KC in K chunks
+  for (int c0 = 0; c0 < m; c0 += a.cap_rows) {
+    const int mc = min(a.cap_rows, m - c0);
+    const int* ridx = a.rowidx + c0;
+    if (c0 > 0) grid_barrier(a.bar, gen);          // the previous chunk's QoI has read buf
+    for (int l = 0; l < a.L; ++l) {
+      const RefineLayer& ly = a.layer[l];
+      const int K = ly.K, N = ly.N;
+      const bool first = l == 0, last = l == a.L - 1;
+      const double* in64 = first ? nullptr : a.buf[(l - 1) & 1];
+      double* out = a.buf[l & 1];
+      for (int r0 = 0; r0 < mc; r0 += REF_RB) {
+        const int rb = min(REF_RB, mc - r0);
+        if (K <= 128) ref_rows<128>(a, ly, xs, warp, lane, gw, nw, ridx, r0, rb, first, last, in64, out);
+        else if (K <= 256) ref_rows<256>(a, ly, xs, warp, lane, gw, nw, ridx, r0, rb, first, last, in64, out);
+        else if (K <= 512) ref_rows<512>(a, ly, xs, warp, lane, gw, nw, ridx, r0, rb, first, last, in64, out);
+        else                                     // (one call site: K <= REF_KC is one chunk)
+          for (int k0 = 0; k0 < K; k0 += REF_KC)
+            ref_rows<REF_KC>(a, ly, xs, warp, lane, gw, nw, ridx, r0, rb, first, last, in64, out, k0,
+                             min(REF_KC, K - k0));
       }
+      REF_STAMP(13 + 2 * l);
       grid_barrier(a.bar, gen);
-    }
-  }
-
-  // ---- 3. QoI of the band rows -> Q (reduced: phi.(phi + 2c); decoded: phi.(K phi + 2c))
-  const double* phi = a.buf[(a.L - 1) & 1];
-  for (int r = gw; r < m; r += nw) {
-    const double* p = phi + (int64_t)r * a.r_u;
-    double s = 0.0;
-    for (int j = lane; j < a.r_u; j += 32) {
-      double kp;
-      if (a.K64) {
-        kp = 2.0 * a.c64[j];
-        for (int q = 0; q < a.r_u; ++q) kp = fma(a.K64[(int64_t)j * a.r_u + q], __ldcg(p + q), kp);
-      } else {
-        kp = __ldcg(p + j) + 2.0 * (double)a.c32[j];
+      REF_STAMP(14 + 2 * l);
+      if (a.softmax && !last) {                    // per-row softmax (+ residual), one warp per row
+        for (int r = gw; r < mc; r += nw) {
+          double* o = out + (int64_t)r * N;
+          double mx = -INFINITY;
+          for (int c = lane; c < N; c += 32) mx = fmax(mx, __ldcg(o + c));
+          for (int q = 16; q > 0; q >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, q));
+          double sum = 0.0;
+          for (int c = lane; c < N; c += 32) sum += exp(__ldcg(o + c) - mx);
+          sum = warp_sum(sum);
+          for (int c = lane; c < N; c += 32) {
+            const double v = exp(__ldcg(o + c) - mx) / sum;
+            o[c] = ly.resid ? __ldcg(in64 + (int64_t)r * K + c) + v : v;
+          }
+        }
+        grid_barrier(a.bar, gen);
       }
-      s = fma(__ldcg(p + j), kp, s);
     }
-    s = warp_sum(s);
-    if (lane == 0) a.Q[__ldcg(a.rowidx + r)] = s + a.q0;
+    // QoI of the chunk's rows -> Q (reduced: phi.(phi + 2c); decoded: phi.(K phi + 2c))
+    const double* phi = a.buf[(a.L - 1) & 1];
+    for (int r = gw; r < mc; r += nw) {
+      const double* p = phi + (int64_t)r * a.r_u;
+      double s = 0.0;
+      for (int j = lane; j < a.r_u; j += 32) {
+        double kp;
+        if (a.K64) {
+          kp = 2.0 * a.c64[j];
+          for (int q = 0; q < a.r_u; ++q) kp = fma(a.K64[(int64_t)j * a.r_u + q], __ldcg(p + q), kp);
+        } else {
+          kp = __ldcg(p + j) + 2.0 * (double)a.c32[j];
+        }
+        s = fma(__ldcg(p + j), kp, s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) a.Q[__ldcg(ridx + r)] = s + a.q0;
+    }
   }
   REF_STAMP(40);
   if (!a.mask) return;
@@ -547,18 +603,58 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
 
   // ---- 4. exact CVaR: the band holds `need` selected rows (rows outside keep
   // their side of the threshold); take the top `need` band rows by
-  // (Q desc, position asc).  One block; m <= cap_rows <= 16 * REF_THREADS.
+  // (refined Q desc, position asc -- positions are in index order).
+  if (m > REF_RESELECT_SMALL) {                  // large band: cooperative radix select over the band
+    int cnt = 0;
+    for (int64_t r = (int64_t)blockIdx.x * REF_THREADS + tid; r < m; r += (int64_t)G * REF_THREADS)
+      cnt += __ldcg(a.mask + __ldcg(a.rowidx + r)) ? 1 : 0;
+    cnt = warp_sum_i(cnt);
+    if (lane == 0) S.w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      int e = 0;
+      for (int w = 0; w < REF_THREADS / 32; ++w) e += S.w[w];
+      a.blockcnt[blockIdx.x] = e;
+    }
+    grid_barrier(a.bar, gen);
+    long long need = 0;
+    {
+      int pr = 0;
+      for (unsigned b = tid; b < G; b += REF_THREADS) pr += __ldcg(a.blockcnt + b);
+      pr = warp_sum_i(pr);
+      __syncthreads();
+      if (lane == 0) S.w[warp] = pr;
+      __syncthreads();
+      for (int w = 0; w < REF_THREADS / 32; ++w) need += S.w[w];
+      __syncthreads();
+    }
+    grid_barrier(a.bar, gen);                      // blockcnt is reused by the select
+    if (need == 0) {
+      for (int64_t r = (int64_t)blockIdx.x * REF_THREADS + tid; r < m; r += (int64_t)G * REF_THREADS)
+        a.mask[__ldcg(a.rowidx + r)] = 0;
+    } else {
+      const int* ri = a.rowidx;
+      const double* Qp = a.Q;
+      uint8_t* mk = a.mask;
+      (void)coop_select(sc, S, gen, (int64_t)m, need,
+                        [&](int64_t r) { return (unsigned long long)dkey(__ldcg(Qp + __ldcg(ri + r))); },
+                        [&](int64_t r, bool v) { mk[__ldcg(ri + r)] = v ? 1 : 0; }, nullptr, false);
+    }
+    REF_STAMP(42);
+    return;
+  }
+  // small band: one block ranks every band row against the others
   if (blockIdx.x != 0) return;
-  if (tid == 0) s_need = 0;
+  if (tid == 0) S.need = 0;
   __syncthreads();
   int cnt = 0;
   for (int r = tid; r < m; r += REF_THREADS) cnt += __ldcg(a.mask + __ldcg(a.rowidx + r)) ? 1 : 0;
-  atomicAdd(&s_need, cnt);
+  atomicAdd(&S.need, cnt);
   __syncthreads();
-  const int need = s_need;
-  bool selr[16];
+  const int need = S.need;
+  bool selr[REF_RESELECT_SMALL / REF_THREADS];
   int t = 0;
-  for (int r = tid; r < m && t < 16; r += REF_THREADS, ++t) {
+  for (int r = tid; r < m; r += REF_THREADS, ++t) {
     const int ri = __ldcg(a.rowidx + r);
     const uint64_t ki = dkey(__ldcg(a.Q + ri));
     int rank = 0;
@@ -571,7 +667,7 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
   }
   __syncthreads();                               // every rank computed from the pre-update mask
   t = 0;
-  for (int r = tid; r < m && t < 16; r += REF_THREADS, ++t) a.mask[__ldcg(a.rowidx + r)] = selr[t] ? 1 : 0;
+  for (int r = tid; r < m; r += REF_THREADS, ++t) a.mask[__ldcg(a.rowidx + r)] = selr[t] ? 1 : 0;
   REF_STAMP(42);
 }
 

@@ -9,6 +9,9 @@ only exchanges are small float64 buffers:
                every rank merges them identically (value desc, index asc)
   backward  -> all-reduce the d_z-long weighted gradient (+ CVaR sums)
 
+Every rank returns the merged exact-CVaR selection as ascending global
+sample indices (bit-exact with the single-handle selection).
+
 so every rank returns bit-identical values for 1/2/4/8 GPUs up to the
 float64 summation order of the collective.  The phase sequence is written
 once (`ShardedObjective`) over a `backend` (libsaadino Engine, or the test
@@ -16,6 +19,7 @@ oracle backend) and a `comm`:
 
   TorchComm   torch.distributed collectives (NCCL on device buffers, gloo on
               host buffers)
+  HostStagedComm  gloo collectives on device buffers staged through the host
   ThreadComm  virtual ranks as threads of one process (several handles on
               one GPU, exchanges through host barriers, no kernel ever waits
               on another) -- the single-GPU test harness for this module.
@@ -57,6 +61,34 @@ class TorchComm:
         parts = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(parts, t, group=self.group)
         return torch.stack(parts)
+
+
+class HostStagedComm(TorchComm):
+    """torch.distributed over a host-only backend (gloo) for device buffers:
+    each collective copies the (KB-sized) exchange buffer to the host, runs
+    there, and copies the result back.  Lets several processes share one GPU
+    (each its own handle; no kernel waits on another process).  `sync`
+    waits for the handle's stream (the engine writes the buffers there, not
+    on torch's current stream)."""
+
+    def __init__(self, dist, group=None, sync=None):
+        super().__init__(dist, group)
+        self.sync = sync or (lambda: None)
+
+    def allreduce_(self, t):
+        self.sync()
+        h = t.cpu()
+        self.dist.all_reduce(h, group=self.group)
+        t.copy_(h)
+        return t
+
+    def allgather(self, t):
+        import torch
+        self.sync()
+        h = t.cpu()
+        parts = [torch.empty_like(h) for _ in range(self.world)]
+        self.dist.all_gather(parts, h, group=self.group)
+        return torch.stack(parts).to(t.device)
 
 
 class ThreadComm:
@@ -136,7 +168,8 @@ class ShardedObjective:
         # the fp64 refinement of the band around the global threshold), kept
         # in slots; then ONE sweep for all risks and ONE all-reduce
         slot = 0
-        for r, rr in zip(risks, rs):
+        kept = {}                                 # risk position -> (slot, k)
+        for i, (r, rr) in enumerate(zip(risks, rs)):
             if r["kind"] != "cvar_exact":
                 continue
             self.b.phase_set_risk(rr)
@@ -149,6 +182,7 @@ class ShardedObjective:
                 if rnd == 0:
                     self.b.phase_refine_band()
             self.b.phase_keep_selection(slot)
+            kept[i] = (slot, k)
             slot += 1
         plen = self.b.partial_len()
         partials = self.b.new_buffer(plen * len(rs))
@@ -158,8 +192,9 @@ class ShardedObjective:
         for i, (r, rr) in enumerate(zip(risks, rs)):
             self.b.phase_set_risk(rr)
             res, grad = self.b.phase_finish(stats, partials[i * plen:(i + 1) * plen])
+            idx = self.b.phase_selection(*kept[i]) if i in kept else None
             out.append(EvalResult(value=res.value, grad_z=grad if r.get("need_grad", True) else None,
-                                  grad_t=res.grad_t if r["kind"] == "cvar" else None, idx=None,
+                                  grad_t=res.grad_t if r["kind"] == "cvar" else None, idx=idx,
                                   n_samples=int(res.n_samples), n_selected=int(res.n_selected),
                                   q_mean=res.q_mean, q_var=res.q_var))
         return out

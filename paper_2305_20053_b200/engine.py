@@ -48,7 +48,7 @@ class EvalResult:
     n_selected: int
     q_mean: float
     q_var: float
-    n_refined: int = 0             # rows re-evaluated in exact fp32 (smoothed CVaR, TC chains)
+    n_refined: int = 0             # rows re-evaluated in fp64 at the decision boundary (CVaR)
 
 
 class Engine:
@@ -282,6 +282,12 @@ class Engine:
     def eval_multi(self, z, risks) -> list:
         """Several risks from one forward pass.  risks: list of dicts with
         keys of `eval` (kind, beta, eps, t, alpha, qoi, need_grad)."""
+        self.eval_multi_launch(z, risks)
+        return self.eval_multi_wait()
+
+    def eval_multi_launch(self, z, risks):
+        """Enqueue eval_multi on the handle's stream and return at once;
+        eval_multi_wait() blocks and returns the results."""
         # the ctypes argument blocks of a risk configuration are built once and
         # reused (repeated calls replay one device graph; keep the host side lean)
         key = (self.n, tuple(tuple(sorted((k, v) for k, v in r.items() if k != "t")) for r in risks))
@@ -307,7 +313,13 @@ class Engine:
         z = _f64(z)
         if z.shape != (self.d_z,):
             raise ValueError(f"control must have shape ({self.d_z},)")
-        check(lib.sdn_eval_multi(self.h, dptr(z), arr, len(risks), res, gptr, iptr), "sdn_eval_multi")
+        check(lib.sdn_eval_multi_launch(self.h, dptr(z), arr, len(risks), 1), "sdn_eval_multi_launch")
+        self._pending = (risks, cached)
+
+    def eval_multi_wait(self) -> list:
+        risks, (arr, res, grads, ks, idx, gptr, iptr) = self._pending
+        self._pending = None
+        check(lib.sdn_eval_multi_wait(self.h, res, gptr, iptr), "sdn_eval_multi_wait")
         out, off = [], 0
         for i, r in enumerate(risks):
             sel = None
@@ -362,6 +374,12 @@ class Engine:
 
     def phase_keep_selection(self, slot: int):
         check(lib.sdn_eval_keep_selection(self.h, int(slot)), "sdn_eval_keep_selection")
+
+    def phase_selection(self, slot: int, k: int) -> np.ndarray:
+        """The kept exact-CVaR selection of `slot`: k ascending global indices."""
+        idx = np.zeros(int(k), np.int64)
+        check(lib.sdn_eval_selection(self.h, int(slot), int(k), i64ptr(idx)), "sdn_eval_selection")
+        return idx
 
     def phase_backward_multi(self, risks, stats_dev, partials_dev):
         arr = (_lib.Risk * len(risks))(*risks)

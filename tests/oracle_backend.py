@@ -69,7 +69,9 @@ class OracleBackend:
         vals, gidx = a[:, :k].ravel(), a[:, k:].ravel()
         ok = gidx >= 0
         vals, gidx = vals[ok], gidx[ok]
-        top = gidx[self._order(vals, gidx)[:k]].astype(np.int64) - self.goff
+        gtop = gidx[self._order(vals, gidx)[:k]].astype(np.int64)
+        self.gsel = np.sort(gtop)
+        top = gtop - self.goff
         self.sel = np.sort(top[(top >= 0) & (top < self.n)])
         self.k = k
 
@@ -80,6 +82,13 @@ class OracleBackend:
         if not hasattr(self, "kept"):
             self.kept = {}
         self.kept[slot] = (self.sel.copy(), self.k)
+        if not hasattr(self, "kept_global"):
+            self.kept_global = {}
+        self.kept_global[slot] = self.gsel.copy()
+
+    def phase_selection(self, slot, k):
+        assert len(self.kept_global[slot]) == k
+        return self.kept_global[slot].copy()
 
     def phase_backward_multi(self, risks, stats, partials):
         """One call for all risks: the i-th exact risk uses kept slot i."""

@@ -37,6 +37,7 @@ def _worker(rank, port, out_path, risks):
     so = ShardedObjective(OracleBackend(p, start), TorchComm(dist), n_global=N)
     res = so.eval_multi(p.z, risks)
     np.save(f"{out_path}.{rank}.npy", np.array([[r.value] + list(r.grad_z) for r in res]))
+    np.save(f"{out_path}.{rank}.idx.npy", np.concatenate([r.idx for r in res if r.idx is not None]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -45,15 +46,20 @@ def _run(tmp_path, risks):
     import torch.multiprocessing as mp
     out = str(tmp_path / "res")
     mp.spawn(_worker, args=(_free_port(), out, risks), nprocs=WORLD, join=True)
-    return [np.load(f"{out}.{r}.npy") for r in range(WORLD)]
+    return [np.load(f"{out}.{r}.npy") for r in range(WORLD)], [np.load(f"{out}.{r}.idx.npy") for r in range(WORLD)]
 
 
 def test_gloo_world2_matches_single_process(tmp_path):
-    got = _run(tmp_path, RISKS)
+    got, idx = _run(tmp_path, RISKS)
     np.testing.assert_array_equal(got[0], got[1])          # every rank agrees
+    np.testing.assert_array_equal(idx[0], idx[1])
     cfg = wl.WORKLOADS["c1"].with_samples(N)
     p = wl.make_problem(cfg, seed=3, count=N)
     form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
+    # merged exact-CVaR selections == the single-process selection rule on the whole Q
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=form)
+    want = np.concatenate([np.sort(ref.cvar_select(Qo, r["beta"])) for r in RISKS if r["kind"] == "cvar_exact"])
+    np.testing.assert_array_equal(idx[0], want)
     for row, r in zip(got[0], RISKS):
         o = ref.risk_and_grad(ref.as_oracle(p), p.m_r, p.z,
                               ref.Risk(r["kind"], beta=r.get("beta", 0.95), alpha=r.get("alpha", 0.0)), form=form)

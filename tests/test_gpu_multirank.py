@@ -45,17 +45,13 @@ def _sharded(cfg, n, world, risks, seed=0, gemm="auto"):
     return out
 
 
-@pytest.mark.parametrize("gemm", ["simt", "tc"])
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_virtual_ranks_match_single_handle(world, gemm):
-    n = 8192 + 37
-    cfg = wl.WORKLOADS["c2"].with_samples(n)
-    p = wl.make_problem(cfg, seed=0, count=n)
+def _check_against_single(cfg, n, world, risks, gemm, seed=0):
+    p = wl.make_problem(cfg, seed=seed, count=n)
     eng = Engine(p, max_samples=n, gemm=gemm)     # same GEMM path on both sides
     eng.set_tracking(p.c, p.q0)
     eng.set_samples(p.m_r)
-    single = eng.eval_multi(p.z, RISKS)
-    sharded = _sharded(cfg, n, world, RISKS, gemm=gemm)
+    single = eng.eval_multi(p.z, risks)
+    sharded = _sharded(cfg, n, world, risks, seed=seed, gemm=gemm)
     for rank_res in sharded:
         for a, b in zip(rank_res, single):
             assert a.value == pytest.approx(b.value, rel=1e-12)
@@ -65,6 +61,31 @@ def test_virtual_ranks_match_single_handle(world, gemm):
         for a, b in zip(rank_res, sharded[0]):
             assert a.value == b.value
             np.testing.assert_array_equal(a.grad_z, b.grad_z)
+    # exact-CVaR indices: sharded (every rank) == single handle == the float64
+    # oracle's selection rule on the oracle's Q (riskopt.py:73-82)
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    for i, spec in enumerate(risks):
+        if spec["kind"] != "cvar_exact":
+            continue
+        want = np.sort(ref.cvar_select(Qo, spec["beta"]))
+        np.testing.assert_array_equal(single[i].idx, want)
+        for rank_res in sharded:
+            np.testing.assert_array_equal(rank_res[i].idx, want)
+
+
+@pytest.mark.parametrize("gemm", ["simt", "tc"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_virtual_ranks_match_single_handle(world, gemm):
+    n = 8192 + 37
+    _check_against_single(wl.WORKLOADS["c2"].with_samples(n), n, world, RISKS, gemm)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_virtual_ranks_c4_shapes_exact_cvar_099(world):
+    """c4 network shapes (416 -> 1024 x 6 -> 400) and its CVaR_0.99, sharded."""
+    n = 16384 + 5
+    risks = [dict(kind="cvar_exact", beta=0.99, alpha=1e-2), dict(kind="mean")]
+    _check_against_single(wl.WORKLOADS["c4"].with_samples(n), n, world, risks, "tc", seed=1)
 
 
 def test_virtual_ranks_match_oracle():
