@@ -264,7 +264,10 @@ def main():
     n_global, start, n_loc = shard_of(cfg, mode, world, rank)
     p = wl.make_problem(cfg, seed=args.seed, start=start, count=n_loc)
     eng = Engine(p, max_samples=n_loc, device=local_rank, gemm=args.gemm)
-    stream = torch.cuda.current_stream()
+    # one non-default stream for the engine, the L2 flush, the timing events
+    # and (N > 1) NCCL: events on it order with the engine's graph launches
+    stream = torch.cuda.Stream(device=local_rank)
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     eng.set_tracking(p.c, p.q0)
     eng.set_samples(torch.from_numpy(p.m_r).cuda(), global_offset=start)   # resident in HBM

@@ -266,6 +266,60 @@ SDN_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 SDN_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---- CTA pairs (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256-row tile; each CTA holds 128 rows of A and half of B's rows in its own
+// shared memory, the leader (rank 0) issues the MMAs for both, and each CTA's
+// TMEM receives its own 128 accumulator rows.  Shared-window addresses with
+// bit 24 cleared name the leader's copy of a barrier.
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;
+SDN_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SDN_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's shared memory, completion counted on the LEADER's barrier
+SDN_DEV void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+// arrive on the leader's copy of a barrier (release at cluster scope)
+SDN_DEV void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK)
+               : "memory");
+}
+SDN_DEV void tmem_alloc_pair(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+}
+SDN_DEV void tmem_relinquish_pair() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+SDN_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// completion of the leader's MMAs -> the barrier at this offset in BOTH CTAs
+SDN_DEV void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+SDN_DEV void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms of
 // 1024 B (SBO), version 1 (sm_100), LBO unused for swizzled K-major (= 16 B)
 // K-major, 64B swizzle (32 bf16 per row), 8-row atoms of 512 B (SBO)
@@ -342,10 +396,10 @@ constexpr uint32_t TC_SMEM_MAX = 232448;      // 227 KB opt-in per block
 constexpr uint32_t TC_BAR_BYTES = 1024;       // mbarriers + TMEM slot
 // (reverse-sweep rings, BWD: 4-KB slots holding the residual-gradient and
 // act' input tiles, reused for the G and split outputs; no bias)
-template <int BN, int RING = 0, bool BWD = false>
+template <int BN, int RING = 0, bool BWD = false, int CG = 1>
 struct TcCfg {
   static constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr uint32_t B_BYTES = BN * TC_BK * 2;
+  static constexpr uint32_t B_BYTES = (BN / CG) * TC_BK * 2;   // CTA pairs: each CTA holds half of B's rows
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr uint32_t EPI_WARP =
       !RING ? TC_EPI_WARP_BYTES : BWD ? (uint32_t)RING * 4096u : (uint32_t)RING * 2048u + 2048u;
@@ -878,6 +932,18 @@ struct TcFlags {
   int* out = nullptr;        // readiness of this GEMM's outputs
 };
 
+// persistent tile walk of one CTA: tiles t0, t0 + ts, ...; a tile covers
+// TC_BM * CG rows, of which this CTA's epilogue owns the 128 at row_off
+struct TileWalk {
+  int t0, ts, row_off;
+};
+// accumulator drained: tell the MMA issuer (the leader's barrier for pairs)
+template <int CG>
+SDN_DEV void tmem_release(uint64_t* tempty) {
+  if constexpr (CG == 1) tcx::mbar_arrive(tempty);
+  else tcx::mbar_arrive_leader(tempty);
+}
+
 // ---------------------------------------------------------------------------
 // asynchronous-input epilogue for the forward chain (RING slots per warp).
 // The epilogue used to prefetch its residual input through registers one
@@ -889,10 +955,11 @@ struct TcFlags {
 // staged in the slot it was read from, and the bias comes from a per-CTA
 // shared copy.  The chunk order per warp runs across the CTA's tiles, so the
 // next tile's first residual tiles load during the current tile's last chunks.
-template <int BN, int RING>
+template <int BN, int RING, int CG>
 SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, uint8_t* epi_base, uint64_t* rbar_all,
                           uint64_t* tfull, uint64_t* tempty, uint32_t tmem, int warp, int lane, int num_tiles,
-                          int n_tiles, int N, int K, const TcFlags& flags) {
+                          int n_tiles, int N, int K, const TcFlags& flags, const TileWalk tw) {
+  constexpr int BMT = TC_BM * CG;
   constexpr uint32_t WB = (uint32_t)RING * 2048u + 2048u;
   constexpr int EW = EpiWarps<RING>::EW, CS = 16 * (EW / 4);   // chunk stride of a warp
   const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
@@ -912,14 +979,14 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
 
   // load cursor (tile lt, column lc), RING-1 chunks ahead of the compute cursor
-  int lt = blockIdx.x, lc = first_c, jl = 0, last_mb = -1;
+  int lt = tw.t0, lc = first_c, jl = 0, last_mb = -1;
   auto lnorm = [&]() {
-    while (lt < num_tiles && !(lc < BN && (lt % n_tiles) * BN + lc < N)) { lt += gridDim.x; lc = first_c; }
+    while (lt < num_tiles && !(lc < BN && (lt % n_tiles) * BN + lc < N)) { lt += tw.ts; lc = first_c; }
   };
   auto issue = [&]() {
     if (lt >= num_tiles) return;
     if (has_prev) {
-      const int mb = lt / n_tiles, s = jl % RING;
+      const int mb = (lt / n_tiles) * CG + tw.row_off / TC_BM, s = jl % RING;   // 128-row block
       if (lane == 0) {
         if (flags.in && mb != last_mb) {          // rows of the previous layer written and visible
           while (tcx::ld_acquire(flags.in + mb) < TC_BM * K) __nanosleep(64);
@@ -940,8 +1007,8 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
 
   int acc = 0, jc = 0;
   uint32_t acc_phase = 0;
-  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-    const int mb = tile / n_tiles, nb = tile % n_tiles;
+  for (int tile = tw.t0; tile < num_tiles; tile += tw.ts) {
+    const int mb = (tile / n_tiles) * CG + tw.row_off / TC_BM, nb = tile % n_tiles;   // 128-row block
     const int r0 = mb * TC_BM + q * 32;
     int nch = 0;
     for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
@@ -951,7 +1018,7 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
     if (nch == 0) {
       tcx::fence_before();
       __syncwarp();
-      if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) tmem_release<CG>(&tempty[acc]);
     }
 #pragma unroll 1
     for (int ci = 0; ci < nch; ++ci, ++jc) {
@@ -969,7 +1036,7 @@ SDN_DEV void epi_fwd_ring(const TcChain<EpiFwdHidden>& ch, const TcOutMaps& om, 
       if (ci == nch - 1) {                        // accumulator drained: the MMA may reuse it
         tcx::fence_before();
         __syncwarp();
-        if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+        if (lane == 0) tmem_release<CG>(&tempty[acc]);
       }
       float a[16], d[16], bias[16];
       if (has_prev) row_get_split(sh, sl, lane, a);
@@ -1037,10 +1104,11 @@ struct BwdRingView<EpiBwdSum> {
   static SDN_DEV const float* resid(const EpiBwdSum& e) { return e.resid; }
 };
 
-template <int BN, int RING, class Epi>
+template <int BN, int RING, int CG, class Epi>
 SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base, uint64_t* rbar_all,
                           uint64_t* tfull, uint64_t* tempty, uint32_t tmem, int warp, int lane, int num_tiles,
-                          int n_tiles, int64_t M, int N) {
+                          int n_tiles, int64_t M, int N, const TileWalk tw) {
+  constexpr int BMT = TC_BM * CG;
   constexpr bool SUM = BwdRingView<Epi>::SUM;
   constexpr uint32_t WB = (uint32_t)RING * 4096u;
   constexpr int EW = EpiWarps<RING, true>::EW, CS = 16 * (EW / 4);   // chunk stride of a warp
@@ -1050,15 +1118,15 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
   const bool has_resid = BwdRingView<Epi>::resid(ep) != nullptr;
   const uint32_t tx = has_resid ? 4096u : 2048u;
 
-  int lt = blockIdx.x, lc = first_c, jl = 0;
+  int lt = tw.t0, lc = first_c, jl = 0;
   auto lnorm = [&]() {
-    while (lt < num_tiles && !(lc < BN && (lt % n_tiles) * BN + lc < N)) { lt += gridDim.x; lc = first_c; }
+    while (lt < num_tiles && !(lc < BN && (lt % n_tiles) * BN + lc < N)) { lt += tw.ts; lc = first_c; }
   };
   auto issue = [&]() {
     if (lt >= num_tiles) return;
     const int s = jl % RING;
     if (lane == 0) {
-      const int x = (lt % n_tiles) * BN + lc, y = (lt / n_tiles) * TC_BM + q * 32;
+      const int x = (lt % n_tiles) * BN + lc, y = (lt / n_tiles) * BMT + tw.row_off + q * 32;
       tcx::mbar_expect_tx(&rbar[s], tx);
       if (has_resid) tcx::tma_load_2d(wb + s * 4096, &om.m[4], &rbar[s], x, y);
       tcx::tma_load_2d(wb + s * 4096 + 2048, &om.m[5], &rbar[s], x, y);
@@ -1072,9 +1140,9 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
 
   int acc = 0, jc = 0;
   uint32_t acc_phase = 0;
-  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+  for (int tile = tw.t0; tile < num_tiles; tile += tw.ts) {
     const int mb = tile / n_tiles, nb = tile % n_tiles;
-    const int64_t r0 = (int64_t)mb * TC_BM + q * 32;
+    const int64_t r0 = (int64_t)mb * BMT + tw.row_off + q * 32;
     int nch = 0;
     for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
     // summing step: this lane's row weights (up to 4 risks) once per tile, not per chunk
@@ -1092,7 +1160,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
     if (nch == 0) {
       tcx::fence_before();
       __syncwarp();
-      if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) tmem_release<CG>(&tempty[acc]);
     }
 #pragma unroll 1
     for (int ci = 0; ci < nch; ++ci, ++jc) {
@@ -1106,7 +1174,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
       if (ci == nch - 1) {
         tcx::fence_before();
         __syncwarp();
-        if (lane == 0) tcx::mbar_arrive(&tempty[acc]);
+        if (lane == 0) tmem_release<CG>(&tempty[acc]);
       }
       float g[16], dd[16];
 #pragma unroll
@@ -1194,12 +1262,16 @@ struct RingKind<EpiBwdSum> {
   static constexpr bool BWD = true;
 };
 
-template <int BN, class Epi, int RING = 0>
+// CG = 2: CTA pairs (cluster of two, cta_group::2 MMAs on 256-row tiles;
+// ring epilogues only).  CG = 1: one CTA per 128-row tile.
+template <int BN, class Epi, int RING = 0, int CG = 1>
 __global__ void __launch_bounds__((EpiWarps<RING, RingKind<Epi>::BWD>::THREADS), 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, int64_t M,
                const int* __restrict__ Mdev, int N, int K, Epi epi, const __grid_constant__ TcOutMaps om,
                int use_om, unsigned long long* __restrict__ trace = nullptr, TcFlags flags = TcFlags{}) {
-  using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
+  static_assert(CG == 1 || (CG == 2 && RING > 0), "CTA pairs run the ring epilogues only");
+  using C = TcCfg<BN, RING, RingKind<Epi>::BWD, CG>;
+  constexpr int BMT = TC_BM * CG;                // rows per tile
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment by offset arithmetic keeps the pointer in the shared window
@@ -1215,20 +1287,28 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
   // warp index through a shuffle: provably warp-uniform, so role branches and
   // the TMA / mbarrier operands stay in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int rank = CG == 1 ? 0 : (int)tcx::cluster_rank();
   if (threadIdx.x == 0) {
     tcx::prefetch_tmap(&tA);
     tcx::prefetch_tmap(&tB);
     for (int s = 0; s < STAGES; ++s) { tcx::mbar_init(&full[s], 1); tcx::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], EW); }
+    // (pairs: the leader's tempty counts the epilogue warps of both CTAs)
+    for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], CG * EW); }
     for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar[i], 1);
     tcx::fence_barrier_init();
   }
   if (warp == 2) {
-    tcx::tmem_alloc(tmem_slot, 2 * BN);
-    tcx::tmem_relinquish();
+    if constexpr (CG == 1) {
+      tcx::tmem_alloc(tmem_slot, 2 * BN);
+      tcx::tmem_relinquish();
+    } else {
+      tcx::tmem_alloc_pair(tmem_slot, 2 * BN);
+      tcx::tmem_relinquish_pair();
+    }
   }
   tcx::fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads();
+  else tcx::cluster_sync();                      // peer barriers initialised before any remote arrive
   tcx::fence_after();
   const uint32_t tmem = *tmem_slot;
   // programmatic dependent launch: the prologue above (barriers, TMEM,
@@ -1237,7 +1317,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
   if (!flags.in) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (Mdev) M = min(M, (int64_t)*Mdev);
-  const int m_tiles = (int)((M + TC_BM - 1) / TC_BM);
+  const int m_tiles = (int)((M + BMT - 1) / BMT);
+  const TileWalk tw{(int)blockIdx.x / CG, (int)gridDim.x / CG, rank * TC_BM};
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int kblocks = (K + TC_BK - 1) / TC_BK;
@@ -1248,11 +1329,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
       uint32_t phase = 0;
       const bool skip_loads = (g_tc_dbg_skip & 2) != 0;
       if (trace && blockIdx.x == 0) trace[0] = clock64();
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tw.t0; tile < num_tiles; tile += tw.ts) {
         const int mb = tile / n_tiles, nb = tile % n_tiles;
+        const int arow = mb * BMT + tw.row_off;  // this CTA's 128 rows of A
         if (flags.in) {                          // this row block of A written and visible
           const int need = TC_BM * K;
-          while (tcx::ld_acquire(flags.in + mb) < need) __nanosleep(64);
+          while (tcx::ld_acquire(flags.in + arow / TC_BM) < need) __nanosleep(64);
           tcx::fence_proxy_async_global();
         }
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -1264,21 +1346,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
-          tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           // A hi + lo, then B hi + lo: one 3-D TMA load each (pair maps)
-          tcx::tma_load_3d(st, &tA, &full[stage], kb * TC_BK, mb * TC_BM, 0);
-          tcx::tma_load_3d(st + 2 * C::A_BYTES, &tB, &full[stage], kb * TC_BK, nb * BN, 0);
+          if constexpr (CG == 1) {
+            tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tcx::tma_load_3d(st, &tA, &full[stage], kb * TC_BK, arow, 0);
+            tcx::tma_load_3d(st + 2 * C::A_BYTES, &tB, &full[stage], kb * TC_BK, nb * BN, 0);
+          } else {                               // both CTAs' bytes complete on the leader's barrier
+            if (rank == 0) tcx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tcx::tma_load_3d_pair(st, &tA, &full[stage], kb * TC_BK, arow, 0);
+            tcx::tma_load_3d_pair(st + 2 * C::A_BYTES, &tB, &full[stage], kb * TC_BK, nb * BN + rank * (BN / 2), 0);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = tcx::idesc_bf16(TC_BM, BN);
+    if (lane == 0 && rank == 0) {                // (pairs: the leader issues for both CTAs)
+      constexpr uint32_t idesc = tcx::idesc_bf16(BMT, BN);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       const bool skip_mma = (g_tc_dbg_skip & 1) != 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tw.t0; tile < num_tiles; tile += tw.ts) {
         tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tcx::fence_after();
         const uint32_t d = tmem + acc * BN;
@@ -1292,26 +1380,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
             const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
             const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
             const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
-            tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
-            tcx::mma_bf16(d, ah, bl, idesc, 1);
-            tcx::mma_bf16(d, al, bh, idesc, 1);
+            if constexpr (CG == 1) {
+              tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
+              tcx::mma_bf16(d, ah, bl, idesc, 1);
+              tcx::mma_bf16(d, al, bh, idesc, 1);
+            } else {
+              tcx::mma_bf16_pair(d, ah, bh, idesc, (kb | kk) != 0);
+              tcx::mma_bf16_pair(d, ah, bl, idesc, 1);
+              tcx::mma_bf16_pair(d, al, bh, idesc, 1);
+            }
           }
-          tcx::commit(&empty[stage]);            // frees the smem slot when these MMAs finish
+          // frees the smem slot (both CTAs' for pairs) when these MMAs finish
+          if constexpr (CG == 1) tcx::commit(&empty[stage]);
+          else tcx::commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         if (trace && blockIdx.x == 0 && tile == (int)blockIdx.x) trace[5] = clock64();
-        tcx::commit(&tfull[acc]);                // accumulator ready for the epilogue
+        // accumulator ready for the epilogue (both CTAs' for pairs)
+        if constexpr (CG == 1) tcx::commit(&tfull[acc]);
+        else tcx::commit_pair(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
     // (compile-time split: a ring kernel carries no register-prefetch epilogue code)
     if constexpr (RING > 0 && RingKind<Epi>::BWD) {
-      epi_bwd_ring<BN, RING>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
-                             num_tiles, n_tiles, M, N);
+      epi_bwd_ring<BN, RING, CG>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
+                                 num_tiles, n_tiles, M, N, tw);
     } else if constexpr (RING > 0) {
-      epi_fwd_ring<BN, RING>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
-                             num_tiles, n_tiles, N, K, flags);
+      epi_fwd_ring<BN, RING, CG>(epi, om, smem + STAGES * C::STAGE_BYTES, rbar, tfull, tempty, tmem, warp, lane,
+                                 num_tiles, n_tiles, N, K, flags, tw);
     } else {
     const int q = warp & 3;                      // TMEM lane quarter of this warp
     const int third = (warp - 4) >> 2;           // which 16-column chunks (mod 3)
@@ -1364,10 +1462,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
     if (use_om && lane == 0) tcx::bulk_wait0();    // this warp's TMA stores are complete
     }
   }
-  __syncthreads();
+  // (pairs: neither CTA leaves while the other may still arrive on its
+  // barriers or the leader's MMAs may still write its TMEM)
+  if constexpr (CG == 1) __syncthreads();
+  else tcx::cluster_sync();
   if (warp == 2) {
     tcx::fence_after();
-    tcx::tmem_dealloc(tmem, 2 * BN);
+    if constexpr (CG == 1) tcx::tmem_dealloc(tmem, 2 * BN);
+    else tcx::tmem_dealloc_pair(tmem, 2 * BN);
   }
 }
 
@@ -1553,16 +1655,17 @@ struct RingOk<EpiBwdSum> {
 // 0.185 -> 0.171 ms per c2 step against depth 2 with four stages
 static int g_tc_bwd_ring = getenv("SDN_BWD_RING") ? atoi(getenv("SDN_BWD_RING")) : 3;
 
-template <int BN, class Epi, int RING>
+template <int BN, class Epi, int RING, int CG = 1>
 static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, int N, int K, const CUtensorMap& am,
                        const CUtensorMap& bm, const Epi& epi, const TcOutMaps& om, int use_om, TcFlags fl) {
-  using C = TcCfg<BN, RING, RingKind<Epi>::BWD>;
+  using C = TcCfg<BN, RING, RingKind<Epi>::BWD, CG>;
   static_assert(C::STAGES >= 2 && C::SMEM <= TC_SMEM_MAX, "shared memory budget");
   static unsigned attr_set = 0;                    // per device: the attribute is a per-context setting
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1u << (dev & 31)))) {
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, RING, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
     attr_set |= 1u << (dev & 31);
   }
   // programmatic stream serialization (PDL): the kernel may start while the
@@ -1572,28 +1675,62 @@ static int tc_launch_k(cudaStream_t st, int grid, int64_t M, const int* Mdev, in
   cfg.blockDim = dim3(EpiWarps<RING, RingKind<Epi>::BWD>::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;   // CTA pairs on one TPC
+  attr[1].val.clusterDim.x = CG;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = CG > 1 ? 2 : 1;
   if (!(g_tc_pdl && g_tc_pdl_now)) fl.in = nullptr;   // row flags only pay off with early (PDL) launch
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, RING>, am, bm, M, Mdev, N, K, epi, om,
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, RING, CG>, am, bm, M, Mdev, N, K, epi, om,
                                            use_om, g_tc_trace, fl);
   return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -3;
+}
+
+// CTA pairs (cta_group::2, 256-row tiles) for the ring GEMMs with a host-
+// known row count: each SM then loads half of every weight k-block.  Measured
+// neutral at c2 (forward 182.7 vs 180.9, reverse 168.7 vs 172.2 us per step:
+// the epilogue, not the mainloop's L2 traffic, paces these GEMMs), so off by
+// default; SDN_TC_PAIRS=1 enables them
+static bool g_tc_pairs = getenv("SDN_TC_PAIRS") && getenv("SDN_TC_PAIRS")[0] == '1';
+
+template <int BN, class Epi>
+static int tc_launch_pairs(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, int N, int K, const TcOperand& A,
+                           const TcOperand& B, const Epi& epi, const TcOutMaps& om, int use_om, TcFlags fl) {
+  constexpr bool BWD = RingKind<Epi>::BWD;
+  constexpr int RING_BWD = 3;
+  CUtensorMap am, bm;
+  if (tc_map(t, A, std::max<int64_t>(M, 1), K, TC_BM, &am) || tc_map(t, B, N, K, BN / 2, &bm)) return -1;
+  const int64_t tiles = ((M + 2 * TC_BM - 1) / (2 * TC_BM)) * ((N + BN - 1) / BN);
+  const int grid = 2 * (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms / 2));
+  if constexpr (BWD) {
+    if constexpr (TcCfg<BN, RING_BWD, true, 2>::STAGES_FIT >= 2)
+      return tc_launch_k<BN, Epi, RING_BWD, 2>(st, grid, M, nullptr, N, K, am, bm, epi, om, use_om, fl);
+    return -5;
+  } else {
+    return tc_launch_k<BN, Epi, 2, 2>(st, grid, M, nullptr, N, K, am, bm, epi, om, use_om, fl);
+  }
 }
 
 template <int BN, class Epi>
 static int tc_launch(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const int* Mdev, int N, int K,
                      const TcOperand& A, const TcOperand& B, Epi epi, TcFlags fl = TcFlags{}) {
-  CUtensorMap am, bm;
-  if (tc_map(t, A, std::max<int64_t>(M, 1), K, TC_BM, &am) || tc_map(t, B, N, K, BN, &bm)) return -1;
-  const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
   TcOutMaps om;
   memset(&om, 0, sizeof(om));
   const int ob = g_tc_thread_stores ? 0 : EpiOut<Epi>::build(t, epi, std::max<int64_t>(M, 1), N, om);
   const int use_om = ob & 1;
+  if constexpr (BN == 256 && (std::is_same<Epi, TcChain<EpiFwdHidden>>::value || RingKind<Epi>::BWD)) {
+    const bool ring = std::is_same<Epi, TcChain<EpiFwdHidden>>::value ? g_tc_ring > 0 : g_tc_bwd_ring > 0;
+    if (g_tc_pairs && !Mdev && (ob & 2) && ring && !g_tc_trace && RingOk<Epi>::ok(epi, N) && num_sms >= 2)
+      return tc_launch_pairs<BN>(t, st, num_sms, M, N, K, A, B, epi, om, use_om, fl);
+  }
+  CUtensorMap am, bm;
+  if (tc_map(t, A, std::max<int64_t>(M, 1), K, TC_BM, &am) || tc_map(t, B, N, K, BN, &bm)) return -1;
+  const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms));
   if constexpr (std::is_same<Epi, TcChain<EpiFwdHidden>>::value) {
     if ((ob & 2) && g_tc_ring > 0 && !g_tc_trace && RingOk<Epi>::ok(epi, N)) {
       if constexpr (TcCfg<BN, 3, false>::STAGES_FIT >= 2)
@@ -1624,7 +1761,7 @@ static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const 
   // dense reverse-sweep ring GEMMs: 128-column tiles leave the mainloop four
   // stages next to the 4-KB-slot epilogue ring (256: two); measured faster at c2
   if constexpr (RingKind<Epi>::BWD)
-    if (!Mdev && !bn_force && N > 128 && mt * ((N + 127) / 128) >= num_sms && g_tc_bwd_ring > 0)
+    if (!Mdev && !bn_force && N > 128 && mt * ((N + 127) / 128) >= num_sms && g_tc_bwd_ring > 0 && !g_tc_pairs)
       return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
   if (N > 128 && mt * ((N + 255) / 256) >= num_sms / 2)
     return tc_launch<256>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
