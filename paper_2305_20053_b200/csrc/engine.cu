@@ -438,7 +438,48 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
   int cur = 0;
   const float* in = X;
   int64_t ldin = ld0;
-  for (int l = 0; l < L; ++l) {
+  int l_start = 0;
+  // persistent chain: the hidden layers (equal widths, tensor-core operands
+  // from layer 0 on) in one launch; the output layer follows as its own GEMM
+  {
+    const int NH = L - 1, Nw = h->w[1];
+    bool ok = tcc && rflags && tcX0 && g_tc_chain && NH >= 2 && NH <= SDN_CHAIN_MAX && h->act != ACT_SOFTMAX &&
+              h->tcw.enabled && Nw % 16 == 0 && Nw > 128 && tcX0->ld % 8 == 0 && K0 % 8 == 0;
+    for (int l = 1; l < NH && ok; ++l) ok = h->w[l + 1] == Nw && h->res[l];
+    if (ok) {
+      std::vector<FwdChainLayerHost> ls;
+      int c = 0;
+      for (int l = 0; l < NH; ++l) {
+        FwdChainLayerHost x{};
+        const TcFlags f = flags_of(l);
+        x.A = l == 0 ? tcX0 : &h->tcw.act[c];
+        x.B = &h->tcw.fwd[l];
+        x.S = &h->tcw.act[l == 0 ? 0 : 1 - c];
+        x.P = l == 0 ? nullptr : &h->tcw.act[c];
+        x.D = store_D ? h->D[l] : nullptr;
+        x.bias = l == 0 ? bias0 : h->b[l];
+        x.K = l == 0 ? K0 : h->w[l];
+        x.fl = f;
+        ls.push_back(x);
+        c = l == 0 ? 0 : 1 - c;
+      }
+      double fl_sum = 0.0;
+      for (int l = 0; l < NH; ++l) fl_sum += 2.0 * nrows * Nw * (l == 0 ? K0 : h->w[l]);
+      ProfScope ps(h, PC_FWD_GEMM, fl_sum, 0.0);
+      g_tc_pdl_now = h->sm_avail == h->num_sms;
+      const int64_t tiles = cdiv(nrows, 128) * cdiv(Nw, 256) * NH;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, h->sm_avail));
+      const int rc = tc_fwd_chain(h->tcw, h->stream, grid, nrows, Nw, h->act, ls);
+      h->launches++;
+      if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 forward chain launch failed (" + std::to_string(rc) + ")");
+      CHECK_LAUNCH(h);
+      cur = c;
+      l_start = NH;
+      in = nullptr;
+      ldin = Nw;
+    }
+  }
+  for (int l = l_start; l < L; ++l) {
     const int n_in = h->w[l], n_out = h->w[l + 1];
     const float* Wl = (l == 0) ? W0 : h->W[l];
     const int64_t ldW = (l == 0) ? ldW0 : n_in;
@@ -670,7 +711,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->wpart, (size_t)h->qgrid * 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->vsum, 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->red_counter, 4))) return bail(rc);
-  h->fwd_mtiles = (int)cdiv(cap, 128);
+  h->fwd_mtiles = 2 * (int)cdiv(cap, 256);        // 128-row blocks, whole 256-row pair tiles
   if ((rc = dalloc(h, &h->fwdflags, (size_t)h->L * h->fwd_mtiles))) return bail(rc);
   if (cudaMemset(h->red_counter, 0, 4 * sizeof(int)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
   if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);

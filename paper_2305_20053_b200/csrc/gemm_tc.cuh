@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -394,6 +395,7 @@ struct EpiWarps {
 // bias copy; the mainloop ring gets whatever shared memory is left (2-4 stages)
 constexpr uint32_t TC_SMEM_MAX = 232448;      // 227 KB opt-in per block
 constexpr uint32_t TC_BAR_BYTES = 1024;       // mbarriers + TMEM slot
+constexpr uint32_t SDN_CHAIN_BIAS_BYTES = 4096;  // persistent forward chain: room for every layer's bias (8 KB with the ring's 4 KB)
 // (reverse-sweep rings, BWD: 4-KB slots holding the residual-gradient and
 // act' input tiles, reused for the G and split outputs; no bias)
 template <int BN, int RING = 0, bool BWD = false, int CG = 1>
@@ -1474,6 +1476,293 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
 }
 
 // ---------------------------------------------------------------------------
+// Persistent forward chain: the hidden layers of the MLP forward in ONE
+// launch.  The CTA walks a global tile list (layer-major; tile g of layer
+// g / tpl) with the per-layer row-block flags as the only dependency: a
+// layer-l tile starts once the layer-(l-1) rows it reads are published, so a
+// layer's wave tail overlaps the next layer's first tiles on the same SM (the
+// accumulator double buffer lets tile g+1's MMAs run under tile g's
+// epilogue), and the prologue (barriers, TMEM) is paid once.  Buffer reuse is
+// safe: layer l+1 writes the ping-pong split that layer l read, but only on
+// rows whose layer-l outputs -- hence all layer-l reads of them -- are complete.
+// The epilogue prefetches residual tiles only within its current tile (never
+// across a flag wait that could depend on the tile it has not yet published).
+constexpr int SDN_CHAIN_MAX = 8;
+// study switch (SDN_CHAIN_TRACE=1, non-graph runs): per CTA and tile,
+// %globaltimer stamps {producer waits, producer starts, MMA starts, MMA done,
+// epilogue (warp 4) starts, epilogue published}, 32 tiles per CTA
+constexpr int CHAIN_TR_TILES = 32;
+__device__ unsigned long long* g_chain_trace = nullptr;
+SDN_DEV void chain_stamp(int tile_i, int k) {
+  if (g_chain_trace && tile_i < CHAIN_TR_TILES) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_chain_trace[((size_t)blockIdx.x * CHAIN_TR_TILES + tile_i) * 8 + k] = t;
+  }
+}
+struct FwdChainLayer {
+  const float* bias;
+  const int* fin;      // readiness of this layer's input rows (null: ready at launch)
+  int* fout;           // this layer's row-block flags (null: not published)
+  int K, has_prev, has_D, has_split;
+};
+struct FwdChainArgs {
+  int L, N, n_tiles, m_tiles, act, bias_smem;
+
+
+  int64_t M;
+  FwdChainLayer ly[SDN_CHAIN_MAX];
+  CUtensorMap a[SDN_CHAIN_MAX], b[SDN_CHAIN_MAX];          // mainloop operands
+  CUtensorMap dmap[SDN_CHAIN_MAX], smap[SDN_CHAIN_MAX];    // D, split outputs
+  CUtensorMap pmap[SDN_CHAIN_MAX];                         // residual input (split of the layer input)
+};
+
+// shared-memory plan of the chain kernel: STAGES mainloop stages, EW
+// epilogue warps with RING 2-KB slots + a 2-KB D tile each, every layer's bias
+template <int BN, int RING, int CG, int EW>
+struct ChainCfg {
+  static_assert(EW % 4 == 0 && EW >= 4, "epilogue warps come in lane-quarter groups of four");
+  using C = TcCfg<BN, RING, false, CG>;
+  static constexpr uint32_t WB = (uint32_t)RING * 2048u + 2048u;
+  static constexpr uint32_t EPI_BYTES = EW * WB;
+  static constexpr uint32_t BIAS_BYTES = 4096u + SDN_CHAIN_BIAS_BYTES;
+  static constexpr int FIT = (int)((TC_SMEM_MAX - EPI_BYTES - BIAS_BYTES - 1024 - TC_BAR_BYTES) / C::STAGE_BYTES);
+  static constexpr int STAGES = FIT > 4 ? 4 : FIT;
+  static constexpr uint32_t SMEM = STAGES * C::STAGE_BYTES + EPI_BYTES + BIAS_BYTES + 1024 + TC_BAR_BYTES;
+  static constexpr int THREADS = 32 * (4 + EW);
+};
+
+template <int BN, int RING, int CG, int EW>
+__global__ void __launch_bounds__(ChainCfg<BN, RING, CG, EW>::THREADS, 1)
+tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
+  using CC = ChainCfg<BN, RING, CG, EW>;
+  using C = typename CC::C;
+  constexpr int BMT = TC_BM * CG;
+  constexpr int STAGES = CC::STAGES;
+  constexpr int CS = 16 * (EW / 4);
+  constexpr uint32_t WB = CC::WB;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tcx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* epi_base = smem + STAGES * C::STAGE_BYTES;
+  // (the bias copies of every layer follow the epilogue slots when they fit)
+  float* bias_all = reinterpret_cast<float*>(epi_base + EW * WB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_base + CC::EPI_BYTES + CC::BIAS_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar_all = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar_all + RING * EW);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int rank = CG == 1 ? 0 : (int)tcx::cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int l = 0; l < ca.L; ++l) {
+      tcx::prefetch_tmap(&ca.a[l]);
+      tcx::prefetch_tmap(&ca.b[l]);
+    }
+    for (int s2 = 0; s2 < STAGES; ++s2) { tcx::mbar_init(&full[s2], 1); tcx::mbar_init(&empty[s2], 1); }
+    for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], CG * EW); }
+    for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar_all[i], 1);
+    tcx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    if constexpr (CG == 1) {
+      tcx::tmem_alloc(tmem_slot, 2 * BN);
+      tcx::tmem_relinquish();
+    } else {
+      tcx::tmem_alloc_pair(tmem_slot, 2 * BN);
+      tcx::tmem_relinquish_pair();
+    }
+  }
+  tcx::fence_before();
+  if constexpr (CG == 1) __syncthreads();
+  else tcx::cluster_sync();
+  tcx::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");      // inputs of the first layer (MR split, z-bias)
+  asm volatile("griddepcontrol.launch_dependents;");
+  // (pairs: m_tiles counts 256-row tiles; the CTA of rank r owns rows 128 r .. 128 r + 127 of each)
+  const int n_tiles = ca.n_tiles, tpl = ca.m_tiles * n_tiles, total = ca.L * tpl, N = ca.N;
+  const int t0 = (int)blockIdx.x / CG, ts = (int)gridDim.x / CG;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
+        const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+        const int mb = mbt * CG + rank;          // this CTA's 128-row block
+        const FwdChainLayer& ly = ca.ly[l];
+        chain_stamp(ti, 0);
+        if (ly.fin) {                            // input rows of this layer written and visible
+          while (tcx::ld_acquire(ly.fin + mb) < TC_BM * ly.K) __nanosleep(64);
+          tcx::fence_proxy_async_global();
+        }
+        chain_stamp(ti, 1);
+        const int kblocks = (ly.K + TC_BK - 1) / TC_BK;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          tcx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * C::STAGE_BYTES;
+          if constexpr (CG == 1) {
+            tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tcx::tma_load_3d(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
+            tcx::tma_load_3d(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN, 0);
+          } else {
+            if (rank == 0) tcx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tcx::tma_load_3d_pair(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
+            tcx::tma_load_3d_pair(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN + rank * (BN / 2), 0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = tcx::idesc_bf16(BMT, BN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
+        const int l = g / tpl;
+        const int kblocks = (ca.ly[l].K + TC_BK - 1) / TC_BK;
+        tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tcx::fence_after();
+        chain_stamp(ti, 2);
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          tcx::mbar_wait(&full[stage], phase);
+          tcx::fence_after();
+          const uint32_t base = tcx::smem_u32(smem + stage * C::STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 16; ++kk) {
+            const uint64_t ah = tcx::sdesc_k64(base + kk * 32);
+            const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
+            const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
+            const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
+            if constexpr (CG == 1) {
+              tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
+              tcx::mma_bf16(d, ah, bl, idesc, 1);
+              tcx::mma_bf16(d, al, bh, idesc, 1);
+            } else {
+              tcx::mma_bf16_pair(d, ah, bh, idesc, (kb | kk) != 0);
+              tcx::mma_bf16_pair(d, ah, bl, idesc, 1);
+              tcx::mma_bf16_pair(d, al, bh, idesc, 1);
+            }
+          }
+          if constexpr (CG == 1) tcx::commit(&empty[stage]);
+          else tcx::commit_pair(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if constexpr (CG == 1) tcx::commit(&tfull[acc]);
+        else tcx::commit_pair(&tfull[acc]);
+        chain_stamp(ti, 3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
+    uint8_t* wb = epi_base + w * WB;
+    int ti = 0;
+    float* Dst = reinterpret_cast<float*>(wb + RING * 2048);
+    uint64_t* rbar = rbar_all + w * RING;
+    if (ca.bias_smem)
+      for (int i = (int)threadIdx.x - 128; i < ca.L * N; i += 32 * EW) bias_all[i] = __ldg(ca.ly[i / N].bias + i % N);
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+    int acc = 0, jt = 0;                          // jt: chunks before this tile (ring slot of chunk ci = (jt + ci) % RING)
+    uint32_t acc_phase = 0, rphase = 0;          // rphase: parity bit per ring slot
+    for (int g = t0; g < total; g += ts) {
+      const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+      const int mbl = mbt * CG + rank;            // this CTA's 128-row block
+      const FwdChainLayer& ly = ca.ly[l];
+      const bool has_prev = ly.has_prev, has_split = ly.has_split, has_D = ly.has_D;
+      const int r0 = mbl * TC_BM + q * 32;
+      int nch = 0;
+      for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
+      // this tile's residual tiles, RING-1 chunks ahead (within the tile)
+      if (has_prev && lane == 0 && nch > 0 && ly.fin) {
+        while (tcx::ld_acquire(ly.fin + mbl) < TC_BM * ly.K) __nanosleep(64);
+        tcx::fence_proxy_async_global();
+      }
+      auto issue = [&](int ci) {
+        if (has_prev && ci < nch && lane == 0) {
+          const int s2 = (jt + ci) % RING;
+          tcx::mbar_expect_tx(&rbar[s2], 2048);
+          tcx::tma_load_3d(wb + s2 * 2048, &ca.pmap[l], &rbar[s2], nb * BN + first_c + CS * ci, r0, 0);
+        }
+      };
+      for (int k = 0; k < RING - 1; ++k) issue(k);
+      tcx::mbar_wait(&tfull[acc], acc_phase);
+      tcx::fence_after();
+      if (warp == 4 && lane == 0) chain_stamp(ti, 4);
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (nch == 0) {
+        tcx::fence_before();
+        __syncwarp();
+        if (lane == 0) tmem_release<CG>(&tempty[acc]);
+      }
+      const float* bias_l = ca.bias_smem ? bias_all + l * N : nullptr;
+#pragma unroll 1
+      for (int ci = 0; ci < nch; ++ci) {
+        const int c0 = first_c + CS * ci, col = nb * BN + c0, s2 = (jt + ci) % RING;
+        uint32_t* sh = reinterpret_cast<uint32_t*>(wb + s2 * 2048);
+        uint32_t* sl = sh + 256;
+        uint32_t v[16];
+        tcx::tmem_ld16(tbase + c0, v);
+        if (has_prev) {
+          tcx::mbar_wait(&rbar[s2], (rphase >> s2) & 1u);
+          rphase ^= 1u << s2;
+        }
+        tcx::tmem_ld_wait();
+        if (ci == nch - 1) {
+          tcx::fence_before();
+          __syncwarp();
+          if (lane == 0) tmem_release<CG>(&tempty[acc]);
+        }
+        float a[16], d[16], bias[16];
+        if (has_prev) row_get_split(sh, sl, lane, a);
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          const float4 b4 = bias_l ? *reinterpret_cast<const float4*>(bias_l + col + j)
+                                   : __ldg(reinterpret_cast<const float4*>(ly.bias + col + j));
+          bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
+        }
+        fwd_act16(ca.act, v, bias, has_prev, a, d);
+        if (lane == 0) tcx::bulk_wait_read0();   // previous chunk's stores have read their staging
+        __syncwarp();
+        issue(ci + RING - 1);
+        if (has_D) row_put(Dst, lane, d);
+        if (has_split) row_put_split(sh, sl, lane, a);
+        tcx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if (has_D) tcx::tma_store_2d(&ca.dmap[l], Dst, col, r0);
+          if (has_split) tcx::tma_store_3d(&ca.smap[l], sh, col, r0, 0);
+          tcx::bulk_commit();
+        }
+      }
+      jt += nch;
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (ly.fout) {                              // publish this warp's part of the row block
+        __syncwarp();
+        if (lane == 0) {
+          tcx::bulk_wait0();
+          tcx::fence_proxy_async_global();
+          tcx::red_release_add(ly.fout + mbl, 32 * 16 * nch);
+        }
+      }
+      if (warp == 4 && lane == 0) chain_stamp(ti, 5);
+      ++ti;
+    }
+    if (lane == 0) tcx::bulk_wait0();
+  }
+  if constexpr (CG == 1) __syncthreads();
+  else tcx::cluster_sync();
+  if (warp == 2) {
+    tcx::fence_after();
+    if constexpr (CG == 1) tcx::tmem_dealloc(tmem, 2 * BN);
+    else tcx::tmem_dealloc_pair(tmem, 2 * BN);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
@@ -1768,6 +2057,113 @@ static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const 
   if (N > 64 && mt * ((N + 127) / 128) >= num_sms / 4)
     return tc_launch<128>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
   return tc_launch<64>(t, st, num_sms, M, Mdev, N, K, A, B, epi, fl);
+}
+
+// persistent forward chain launch (see tc_fwd_chain_kernel).  Layer l reads
+// A[l] and writes its split to S[l] (the next layer's A) and act' to D[l];
+// P[l] (may be null) is its residual input.  Returns 0 on launch.
+struct FwdChainLayerHost {
+  const TcOperand* A;
+  const TcOperand* B;
+  const TcOperand* S;
+  const TcOperand* P;
+  float* D;
+  const float* bias;
+  int K;
+  TcFlags fl;
+};
+static bool g_tc_chain = !(getenv("SDN_NO_CHAIN") && getenv("SDN_NO_CHAIN")[0] == '1');
+template <int CG, int EW>
+static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N, int act,
+                          const std::vector<FwdChainLayerHost>& ls) {
+  constexpr int BN = 256, RING = 2;
+  using CC = ChainCfg<BN, RING, CG, EW>;
+  constexpr uint32_t SMEM = CC::SMEM;
+  static_assert(CC::STAGES >= 2 && SMEM <= TC_SMEM_MAX, "chain shared memory budget");
+  grid = CG * std::max(1, grid / CG);
+  const int L = (int)ls.size();
+  if (L < 1 || L > SDN_CHAIN_MAX || N % 16) return -1;
+  FwdChainArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  ca.L = L; ca.N = N; ca.M = M; ca.act = act;
+  ca.n_tiles = (N + BN - 1) / BN;
+  ca.m_tiles = (int)((M + TC_BM * CG - 1) / (TC_BM * CG));
+  ca.bias_smem = (uint32_t)L * N * 4 <= CC::BIAS_BYTES ? 1 : 0;
+  for (int l = 0; l < L; ++l) {
+    const FwdChainLayerHost& x = ls[l];
+    FwdChainLayer& y = ca.ly[l];
+    if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l]) ||
+        tc_map(t, *x.B, N, x.K, BN / CG, &ca.b[l]))
+      return -2;
+    if (x.D && tc_out_map(t, x.D, false, M, N, N, &ca.dmap[l])) return -3;
+    if (x.S && tc_out_map_pair(t, x.S->hi, x.S->lo, M, N, x.S->ld, &ca.smap[l])) return -3;
+    if (x.P && tc_out_map_pair(t, x.P->hi, x.P->lo, M, N, x.P->ld, &ca.pmap[l])) return -3;
+    y.bias = x.bias; y.K = x.K; y.fin = x.fl.in; y.fout = x.fl.out;
+    y.has_prev = x.P != nullptr; y.has_D = x.D != nullptr; y.has_split = x.S != nullptr;
+
+  }
+
+  static unsigned attr_set = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set & (1u << (dev & 31)))) {
+    cudaFuncSetAttribute(tc_fwd_chain_kernel<BN, RING, CG, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SMEM);
+    attr_set |= 1u << (dev & 31);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CC::THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CG;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CG > 1 ? 2 : 1;
+  static const bool trace = getenv("SDN_CHAIN_TRACE") != nullptr;
+  static unsigned long long* tbuf = nullptr;
+  const size_t tn = (size_t)grid * CHAIN_TR_TILES * 8;
+  if (trace) {
+    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 148 * 2 * CHAIN_TR_TILES * 8);
+    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * tn, st);
+    cudaMemcpyToSymbolAsync(g_chain_trace, &tbuf, sizeof(tbuf), 0, cudaMemcpyHostToDevice, st);
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_fwd_chain_kernel<BN, RING, CG, EW>, ca);
+  if (trace) {                                    // dump: grid, tiles per layer, then stamps
+    std::vector<unsigned long long> hb(tn);
+    cudaMemcpyAsync(hb.data(), tbuf, sizeof(unsigned long long) * tn, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long* z = nullptr;
+    cudaMemcpyToSymbol(g_chain_trace, &z, sizeof(z));
+    FILE* f = fopen(getenv("SDN_CHAIN_TRACE"), "ab");
+    if (f) {
+      const long long hdr[3] = {grid, (long long)ca.m_tiles * ca.n_tiles, L};
+      fwrite(hdr, sizeof(hdr), 1, f);
+      fwrite(hb.data(), sizeof(unsigned long long), tn, f);
+      fclose(f);
+    }
+  }
+  return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -4;
+}
+// CTA pairs for the persistent chain (SDN_CHAIN_PAIRS=0 disables)
+static bool g_chain_pairs = !(getenv("SDN_CHAIN_PAIRS") && getenv("SDN_CHAIN_PAIRS")[0] == '0');
+// epilogue warps of the chain (SDN_CHAIN_EW=12 / 16): 12 measured faster at
+// c2 (forward GEMMs 148 vs 153 us per step), though 16 split a 256-column tile
+// into four chunks per warp exactly (12: five or six)
+static int g_chain_ew = getenv("SDN_CHAIN_EW") ? atoi(getenv("SDN_CHAIN_EW")) : 12;
+static int tc_fwd_chain(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N, int act,
+                        const std::vector<FwdChainLayerHost>& ls) {
+  if (g_chain_pairs && grid >= 2) {
+    if (g_chain_ew == 12) return tc_fwd_chain_k<2, 12>(t, st, grid, M, N, act, ls);
+    return tc_fwd_chain_k<2, 16>(t, st, grid, M, N, act, ls);
+  }
+  if (g_chain_ew == 16) return tc_fwd_chain_k<1, 16>(t, st, grid, M, N, act, ls);
+  return tc_fwd_chain_k<1, 12>(t, st, grid, M, N, act, ls);
 }
 
 // allocation / refresh of the split operands -------------------------------
