@@ -32,6 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SAA samples/sec for risk+grad_risk(z)"
+JAC_METRIC = "batched control-Jacobian samples/sec (dq/dz decoded to d_u x d_z)"
 UNIT = "samples/s"
 
 
@@ -200,13 +201,18 @@ def run_reference(args, cfg, rank, world):
     n_step = min(args.ref_samples, cfg.n_samples)
     from oracle import mrdino_ref as ref
     from paper_2305_20053_b200 import workloads as wl
-    p = wl.make_problem(cfg.with_samples(n_step), seed=args.seed, count=n_step)
+    p = wl.make_problem(cfg.with_samples(n_step), seed=args.seed, count=n_step, with_decoder=cfg.jacobian)
     m = ref.as_oracle(p)
     form = ref.ReducedForm(p.c.astype(np.float64), p.q0)
     z = p.z.astype(np.float64)
     chunk = 512
 
     def step():
+        if cfg.jacobian:                   # c5: z_jacobian_batch + decode (test_acceptance.py:326)
+            Z = np.broadcast_to(z, (n_step, cfg.d_z))
+            for a in range(0, n_step, 256):
+                np.einsum("du,iuk->idk", p.U.astype(np.float64), ref.z_jacobian_batch(m, p.m_r[a:a + 256], Z[a:a + 256]))
+            return
         parts = [ref.evaluate_forward_mode(m, p.m_r[a:a + chunk], z, form) for a in range(0, n_step, chunk)]
         Q = np.concatenate([q for q, _ in parts])
         G = np.concatenate([g for _, g in parts])
@@ -225,7 +231,7 @@ def run_reference(args, cfg, rank, world):
               f"{chunk}-sample chunks (forward-mode z-Jacobian, fp64 numpy BLAS, {cpu_cores()} threads); "
               f"cost is linear in N")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": JAC_METRIC if cfg.jacobian else METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
         "scaling": mode, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
@@ -238,6 +244,149 @@ def run_reference(args, cfg, rank, world):
 
 
 # ---------------------------------------------------------------------------
+# BASELINE config 5: batched control Jacobian decoded to d_u x d_z
+
+
+def cpu_jacobian_rate(cfg, seed, n_cpu):
+    """The reference's z_jacobian_batch (surrogate.py:195-233, forward mode,
+    restated in oracle/, fp64 numpy BLAS) + the decode modes @ J
+    (test_acceptance.py:326) on n_cpu samples."""
+    from oracle import mrdino_ref as ref
+    from paper_2305_20053_b200 import workloads as wl
+    p = wl.make_problem(cfg.with_samples(n_cpu), seed=seed, count=n_cpu, with_decoder=True)
+    m = ref.as_oracle(p)
+    Z = np.broadcast_to(p.z.astype(np.float64), (n_cpu, cfg.d_z))
+    U = p.U.astype(np.float64)
+    t0 = time.perf_counter()
+    for a in range(0, n_cpu, 256):
+        J = ref.z_jacobian_batch(m, p.m_r[a:a + 256], Z[a:a + 256])
+        np.einsum("du,iuk->idk", U, J)
+    dt = time.perf_counter() - t0
+    return n_cpu / dt, dt
+
+
+def run_jacobian(args, cfg, rank, world, local_rank, dist):
+    """c5: one step = the decoded control Jacobians of this rank's samples at
+    the control z, written to a device buffer (sdn_jacobian_samples).  The
+    dominant cost is writing n x d_u x d_z fp32 (HBM-write bound)."""
+    import torch
+    from paper_2305_20053_b200 import Engine, workloads as wl
+    mode = scaling_mode(args)
+    n_global, start, n_loc = shard_of(cfg, mode, world, rank)
+    p = wl.make_problem(cfg, seed=args.seed, start=start, count=n_loc, with_decoder=True)
+    eng = Engine(p, max_samples=n_loc, device=local_rank, gemm=args.gemm)
+    stream = torch.cuda.Stream(device=local_rank)
+    torch.cuda.set_stream(stream)
+    eng.set_stream(stream.cuda_stream)
+    eng.set_tracking(p.c, p.q0)
+    eng.set_decoder(p.U, p.ubias, p.Mdiag_u, p.u_target)
+    eng.set_samples(torch.from_numpy(p.m_r).cuda(), global_offset=start)
+    z = p.z.astype(np.float64)
+    J = torch.empty((n_loc, cfg.d_u, cfg.d_z), dtype=torch.float32, device="cuda")   # 1.78 GB at c5 (> L2)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        eng.jacobian_samples(z, decoded=True, out=J)
+    barrier()
+    launches0 = eng.kernel_launches()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for i in range(args.steps):
+            starts[i].record(stream)
+            eng.jacobian_samples(z, decoded=True, out=J)   # output 1.78 GB > L2: no flush needed
+            ends[i].record(stream)
+        barrier()
+    launches = eng.kernel_launches() - launches0
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    value = n_global * args.steps / (ms_total / 1e3)
+    out_bytes = n_loc * cfg.d_u * cfg.d_z * 4
+
+    # per-class profile (tangent GEMMs, decode GEMM)
+    eng.profile(True)
+    for _ in range(args.steps):
+        eng.jacobian_samples(z, decoded=True, out=J)
+    torch.cuda.synchronize()
+    prof = eng.profile_read()
+    eng.profile(False)
+
+    # e2e: the reference-facing batch API with host buffers (m_r, z rows up;
+    # the decoded Jacobians down into pinned host memory)
+    Jh = torch.empty((n_loc, cfg.d_u, cfg.d_z), dtype=torch.float32).pin_memory().numpy()
+    Z = np.ascontiguousarray(np.broadcast_to(p.z, (n_loc, cfg.d_z)).astype(np.float32))
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        Jh[...] = eng.jacobian_batch(p.m_r, Z, decoded=True)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n_global * e2e_steps / float(te.item())
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_bw = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "of measured HBM copy (MEASURED_PEAKS.json)" if peaks else "of fallback (B200_PROFILING.md)"
+    step_gbps = out_bytes * args.steps / (ms / 1e3) / 1e9
+    dec = prof.get("decode_gemm", {"ms": 0.0, "launches": 0})
+    step_ms_prof = sum(v["ms"] for v in prof.values())
+    if dec["launches"]:
+        achieved = out_bytes * args.steps / (dec["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak_bw, "unit": "GB/s", "frac": achieved / peak_bw,
+                "traffic": None, "kernel": "decode_gemm (tcgen05, scatter epilogue into J[i, u, k])",
+                "launches": dec["launches"], "avg_launch_us": 1e3 * dec["ms"] / dec["launches"],
+                "share_of_step": dec["ms"] / step_ms_prof, "algorithmic_bytes_per_launch": out_bytes,
+                "peak_source": peak_src, "whole_step_GBps": step_gbps,
+                "note": "achieved = decoded Jacobian bytes written (n x d_u x d_z x 4 = 108,900 B/sample) / the "
+                        "decoder GEMM's launch time; whole_step_GBps divides by the whole step"}
+    else:
+        roof = {"bound": "hbm", "achieved": step_gbps, "peak": peak_bw, "unit": "GB/s",
+                "frac": step_gbps / peak_bw, "traffic": None, "kernel": "whole Jacobian step",
+                "algorithmic_bytes_per_step": out_bytes, "peak_source": peak_src}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_cpu = min(args.cpu_samples, 1024)
+        rate, secs = cpu_jacobian_rate(cfg, args.seed, n_cpu)
+        cpu = {"value": rate, "unit": "samples/s", "cores": cpu_cores(), "kind": "port",
+               "sample": f"{n_cpu} samples of c5: forward-mode z_jacobian_batch in 256-sample chunks + decode "
+                         f"(oracle port, fp64 numpy BLAS) ({secs:.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": JAC_METRIC, "value": value,
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "timing": "CUDA events on the launch stream around each step, max over ranks",
+            "scaling": mode, "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+            "config": {"workload": cfg.name, "description": cfg.description, "global_samples": n_global,
+                       "samples_per_gpu": n_loc, "output_bytes_per_gpu": out_bytes,
+                       "parallelism": f"dp{world} sample shards", "scaling": mode},
+            "l2": "output (1.78 GB per step) larger than L2",
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(p.m_r.nbytes + Z.nbytes),
+                    "d2h_bytes_per_step": int(out_bytes),
+                    "api": "Engine.jacobian_batch (host m_r, z rows in; decoded Jacobians to pinned host memory)"},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps}
+                               for k, v in prof.items() if v["launches"]},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():
@@ -258,6 +407,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    if cfg.jacobian:
+        run_jacobian(args, cfg, rank, world, local_rank, dist)
+        return
 
     from paper_2305_20053_b200 import Engine
     mode = scaling_mode(args)

@@ -171,6 +171,14 @@ int sdn_forward_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n
                       float* phi);
 int sdn_jacobian_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n,
                        int32_t decoded, float* J);
+/* Batched control Jacobian of the handle's resident samples (sdn_set_samples)
+ * at one control z (host, d_z float64) -- BASELINE config 5: dq/dz per
+ * sample, J_dev a DEVICE buffer of n x r_u x d_z floats, or decoded
+ * U (std . dq/dz) of n x d_u x d_z (test_acceptance.py:326), same layout as
+ * z_jacobian_batch (surrogate.py:195-233).  Enqueued on the handle's stream;
+ * returns without waiting (sdn_synchronize).  Multi-GPU: each rank passes its
+ * shard's buffer (no exchange). */
+int sdn_jacobian_samples(sdn_handle* h, const double* z, int32_t decoded, float* J_dev);
 
 /* Decoded states u = U phi + b for the rows' phi (n x r_u) -> (n x d_u). */
 int sdn_lift(sdn_handle* h, const float* phi, int64_t n, float* u);
@@ -256,7 +264,7 @@ int sdn_train_step(sdn_handle* h, const int64_t* idx, int32_t B, double jacobian
  * 3 top-k select, 4 compaction, 5 seeds, 6 column sums, 7 finalise,
  * 8 zbias, 9 other, 10 fp64 Q refinement); sdn_profile_read returns per-class device ms,
  * algorithmic flops and bytes, and launch counts. */
-#define SDN_PROF_CLASSES 11
+#define SDN_PROF_CLASSES 13
 int sdn_profile(sdn_handle* h, int32_t enable);
 int sdn_profile_read(sdn_handle* h, int32_t n_cls, double* ms, double* flops, double* bytes,
                      int64_t* count);

@@ -24,7 +24,7 @@ QOI = {"reduced": 0, "decoded": 1}
 GEMM = {"auto": 0, "simt": 1, "tc": 2}
 STATS_LEN = 8
 PROF_CLASSES = ["fwd_gemm", "bwd_gemm", "qoi", "select", "compact", "seed", "colsum", "finalize", "zbias",
-                "other", "refine"]
+                "other", "refine", "tangent_gemm", "decode_gemm"]
 
 
 class Config(C.Structure):
@@ -69,6 +69,7 @@ SIGNATURES = {
     "sdn_eval_samples": (C.c_int, [_P, _D, C.c_int32, _D, _D]),
     "sdn_forward_batch": (C.c_int, [_P, _F, _F, C.c_int64, _F]),
     "sdn_jacobian_batch": (C.c_int, [_P, _F, _F, C.c_int64, C.c_int32, _F]),
+    "sdn_jacobian_samples": (C.c_int, [_P, _D, C.c_int32, _P]),
     "sdn_lift": (C.c_int, [_P, _F, C.c_int64, _F]),
     "sdn_select_topk": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int32, _I64]),
     "sdn_partial_len": (C.c_int, [_P]),

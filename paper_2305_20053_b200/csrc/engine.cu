@@ -227,6 +227,17 @@ struct sdn_handle {
   int band_cap = 0;
   double* K64 = nullptr;        // decoded-frame Gram / c in fp64
   double* c64dec = nullptr;
+  // batched control Jacobian (c5): scratch kept across calls (no per-call
+  // allocation); tensor-core chains hold the tangents as bf16x3 splits
+  int64_t jac_rows = 0;         // tangent-row capacity of the scratch below
+  TcOperand jtan[2];            // tangent split ping-pong (rows x maxw)
+  TcOperand jjr;                // std . dy/dz split (rows x r_u), the decoder GEMM's A
+  TcOperand usplit;             // decoder basis split (d_u16 x r_u)
+  int64_t d_u16 = 0;
+  float* jT[2] = {nullptr, nullptr};   // SIMT tangents (rows x maxw)
+  float* jJt = nullptr;         // SIMT std . dy/dz (rows x r_u)
+  int64_t jin_cap = 0;          // host-input scratch (sdn_jacobian_batch): samples
+  float *jmr = nullptr, *jz = nullptr, *jX = nullptr, *jJ = nullptr;
   bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
   bool ref_trace = false;       // env SDN_REFINE_TRACE=1
   // H1 training state (sdn_train_*), allocated on first use
@@ -289,7 +300,7 @@ static int dalloc(sdn_handle* h, T** p, size_t count) {
 // profiling: events bracket each launch on the handle's stream
 
 enum ProfClass { PC_FWD_GEMM = 0, PC_BWD_GEMM, PC_QOI, PC_SELECT, PC_COMPACT, PC_SEED, PC_COLSUM, PC_FINAL,
-                 PC_ZBIAS, PC_OTHER, PC_REFINE, PC_N };
+                 PC_ZBIAS, PC_OTHER, PC_REFINE, PC_TANGENT, PC_DECODE, PC_N };
 
 static cudaEvent_t prof_event(sdn_handle* h) {
   if (h->pool_used == h->pool.size()) {
@@ -1966,167 +1977,260 @@ int sdn_forward_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n
 
 // forward-mode control Jacobian (surrogate.py:195-233) on the device:
 // tangent rows (i*d_z + k) through the chain; decoded: U (std . J)
+// (test_acceptance.py:326).  The tangent GEMMs run on the tensor cores
+// (bf16x3, act' gathered per sample in the epilogue, tangents kept only as
+// the next GEMM's split) whenever the forward chain does; the output is
+// scattered straight into J[i, u, k] by the last GEMM's epilogue (a warp's
+// 32 rows are consecutive k of one or two samples: coalesced).
+
+static bool jac_tc(sdn_handle* h) {
+  return h->tcw.enabled && h->gemm != SDN_GEMM_SIMT && h->L >= 2 && h->act != ACT_SOFTMAX;
+}
+
+// scratch for `rows` tangent rows (grown, never shrunk; freed at destroy)
+static int jac_scratch(sdn_handle* h, int64_t rows, bool decoded) {
+  if (rows <= h->jac_rows && (!decoded || h->jjr.hi || !jac_tc(h))) return SDN_OK;
+  const int64_t cap = std::max(rows, h->jac_rows);
+  const int wmax = std::max(h->maxw, h->r_u);
+  int rc;
+  if (jac_tc(h)) {
+    for (int i = 0; i < 2; ++i)
+      if (tc_buf(h, h->tcw, h->jtan[i], cap, wmax)) return fail(SDN_ERR_NOMEM, "jacobian scratch");
+    if (decoded && tc_buf(h, h->tcw, h->jjr, cap, h->r_u)) return fail(SDN_ERR_NOMEM, "jacobian scratch");
+  } else {
+    for (int i = 0; i < 2; ++i)
+      if ((rc = dalloc(h, &h->jT[i], (size_t)cap * wmax))) return rc;
+    if ((rc = dalloc(h, &h->jJt, (size_t)cap * h->r_u))) return rc;
+  }
+  h->jac_rows = cap;
+  return SDN_OK;
+}
+
+// tangent-row budget of one chunk (~1.5 GB of scratch)
+static int64_t jac_chunk_samples(sdn_handle* h, bool decoded) {
+  const int64_t per_row = 4ll * (2 * std::max(h->maxw, h->r_u) + (decoded ? h->r_u : 0));
+  const int64_t rows = std::max<int64_t>(h->d_z, (1536ll << 20) / per_row);
+  return std::max<int64_t>(1, std::min<int64_t>(h->cap, rows / h->d_z));
+}
+
+// Jacobians of m samples whose forward (act' in D[l] rows dro .. dro + m)
+// is done, into J (device, m x outw x d_z)
+static int jac_rows(sdn_handle* h, int64_t dro, int64_t m, bool decoded, float* J) {
+  const int d_z = h->d_z, L = h->L;
+  const int64_t rows = m * d_z;
+  TRY(jac_scratch(h, rows, decoded));
+  const float* D0 = h->act == ACT_SOFTMAX ? nullptr : h->D[0] + dro * h->w[1];
+  if (jac_tc(h)) {
+    // seed (the tangent of x_z = V_z^T z through W1_z is the constant Pz), as a split
+    TcOperand* Tc = &h->jtan[0];
+    TcOperand* Tn = &h->jtan[1];
+    { ProfScope ps(h, PC_SEED, 0.0, 4.0 * rows * Tc->ld);
+      k_tangent_seed_split<<<(unsigned)std::min<int64_t>(cdiv(rows, 8), 32ll * h->num_sms), 256, 0, h->stream>>>(
+          rows, d_z, h->h1, Tc->ld, D0, h->Pz32t, Tc->hi, Tc->lo); }
+    h->launches++;
+    CHECK_LAUNCH(h);
+    for (int l = 1; l < L - 1; ++l) {
+      TcChain<EpiTanTc> e{EpiTanTc{h->D[l] + dro * h->w[l + 1], (int64_t)h->w[l + 1], d_z}, TcEpiSplit{Tn},
+                          TcEpiSplit{h->res[l] ? Tc : nullptr}};
+      ProfScope ps(h, PC_TANGENT, 2.0 * rows * h->w[l + 1] * h->w[l], 0.0);
+      const int rc = tc_gemm(h->tcw, h->stream, h->sm_avail, rows, nullptr, h->w[l + 1], h->w[l], *Tc,
+                             h->tcw.fwd[l], e, rows);
+      h->launches++;
+      if (rc) return fail(SDN_ERR_CUDA, "tangent GEMM launch failed (" + std::to_string(rc) + ")");
+      CHECK_LAUNCH(h);
+      std::swap(Tc, Tn);
+    }
+    const int Kl = h->w[L - 1];
+    int rc;
+    if (!decoded) {
+      ProfScope ps(h, PC_TANGENT, 2.0 * rows * h->r_u * Kl, 4.0 * rows * h->r_u);
+      rc = tc_gemm(h->tcw, h->stream, h->sm_avail, rows, nullptr, h->r_u, Kl, *Tc, h->tcw.fwd[L - 1],
+                   EpiJacScatter{h->ostd, J, d_z, (int64_t)h->r_u}, rows);
+    } else {
+      { ProfScope ps(h, PC_TANGENT, 2.0 * rows * h->r_u * Kl, 0.0);
+        rc = tc_gemm(h->tcw, h->stream, h->sm_avail, rows, nullptr, h->r_u, Kl, *Tc, h->tcw.fwd[L - 1],
+                     EpiScaleSplit{h->ostd, TcEpiSplit{&h->jjr}}, rows); }
+      h->launches++;
+      // decoder GEMM: HBM-write bound (4 d_u bytes per tangent row)
+      ProfScope ps(h, PC_DECODE, 0.0, 4.0 * rows * h->d_u);
+      if (rc == 0)
+        rc = tc_gemm(h->tcw, h->stream, h->sm_avail, rows, nullptr, (int)h->d_u16, h->r_u, h->jjr, h->usplit,
+                     EpiJacScatter{nullptr, J, d_z, h->d_u, h->d_u}, rows);
+    }
+    h->launches++;
+    if (rc) return fail(SDN_ERR_CUDA, "jacobian GEMM launch failed (" + std::to_string(rc) + ")");
+    CHECK_LAUNCH(h);
+    return SDN_OK;
+  }
+  // SIMT chains (small widths / softmax / SDN_GEMM_SIMT)
+  float* Tc = h->jT[0];
+  float* Tn = h->jT[1];
+  k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, L == 1 ? nullptr : D0, h->Pz32t, Tc);
+  h->launches++;
+  if (L > 1 && h->act == ACT_SOFTMAX) {          // T = a (U - a.U), U = (W1_z V_z^T)_k
+    k_softmax_tangent<<<(unsigned)cdiv(rows, 8), 256, 0, h->stream>>>(rows, d_z, h->h1, h->D[0] + dro * h->w[1],
+                                                                      Tc, nullptr);
+    h->launches++;
+  }
+  for (int l = 1; l < L - 1; ++l) {
+    const bool smax = h->act == ACT_SOFTMAX;
+    EpiTangent e{smax ? nullptr : h->D[l] + dro * h->w[l + 1], (int64_t)h->w[l + 1], d_z,
+                 (h->res[l] && !smax) ? Tc : nullptr, Tn, (int64_t)h->w[l + 1]};
+    TRY((gemm<false, true>(h, rows, nullptr, h->w[l + 1], h->w[l], Tc, h->w[l], h->W[l], h->w[l], e, nullptr,
+                           nullptr, 0)));
+    if (smax) {
+      k_softmax_tangent<<<(unsigned)cdiv(rows, 8), 256, 0, h->stream>>>(rows, d_z, h->w[l + 1],
+                                                                        h->D[l] + dro * h->w[l + 1], Tn,
+                                                                        h->res[l] ? Tc : nullptr);
+      h->launches++;
+    }
+    std::swap(Tc, Tn);
+  }
+  if (L >= 2) {
+    if (!decoded) {
+      EpiJacScatter e{h->ostd, J, d_z, (int64_t)h->r_u};
+      TRY((gemm<false, true>(h, rows, nullptr, h->r_u, h->w[L - 1], Tc, h->w[L - 1], h->W[L - 1], h->w[L - 1], e,
+                             nullptr, nullptr, 0)));
+      return SDN_OK;
+    }
+    EpiAffine e{nullptr, h->ostd, nullptr, h->jJt, (int64_t)h->r_u};
+    TRY((gemm<false, true>(h, rows, nullptr, h->r_u, h->w[L - 1], Tc, h->w[L - 1], h->W[L - 1], h->w[L - 1], e,
+                           nullptr, nullptr, 0)));
+  } else {                                       // linear model: dy/dz rows are the seed (w[1] = r_u)
+    k_scale_cols<<<(unsigned)cdiv(rows * h->r_u, 256), 256, 0, h->stream>>>(rows, h->r_u, h->ostd, Tc,
+                                                                            decoded ? h->jJt : nullptr, J, d_z);
+    h->launches++;
+    if (!decoded) return SDN_OK;
+  }
+  EpiJacScatter e{nullptr, J, d_z, h->d_u};
+  TRY((gemm<false, true>(h, rows, nullptr, (int)h->d_u, h->r_u, h->jJt, h->r_u, h->U, h->r_u, e, nullptr, nullptr,
+                         0)));
+  return SDN_OK;
+}
+
 int sdn_jacobian_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n, int32_t decoded, float* J) {
   if (!h || !m_r || !z || !J) return fail(SDN_ERR_ARG, "null argument");
   if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
   if (decoded && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  if (n < 0) return fail(SDN_ERR_ARG, "negative row count");
   CU(cudaSetDevice(h->device));
-  const int d_z = h->d_z, L = h->L;
+  const int d_z = h->d_z;
   const int64_t outw = decoded ? h->d_u : h->r_u;
-  const int64_t row_budget = std::max<int64_t>(d_z, (int64_t)(256ll << 20) / (4ll * std::max(h->maxw, h->r_u)));
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(h->cap, row_budget / d_z));
-  const int64_t trows = chunk * d_z;
-  float *mr = nullptr, *zz = nullptr, *X = nullptr, *T0 = nullptr, *T1 = nullptr, *Jt = nullptr, *Jd = nullptr;
-  int rc = SDN_OK;
-  auto cleanup = [&]() {
-    cudaStreamSynchronize(h->stream);
-    cudaFree(mr); cudaFree(zz); cudaFree(X); cudaFree(T0); cudaFree(T1); cudaFree(Jt); cudaFree(Jd);
-  };
-  if (cudaMalloc(&mr, sizeof(float) * chunk * h->r_m + 16) || cudaMalloc(&zz, sizeof(float) * chunk * d_z + 16) ||
-      cudaMalloc(&X, sizeof(float) * chunk * h->ldx + 16) ||
-      cudaMalloc(&T0, sizeof(float) * trows * std::max(h->maxw, h->r_u) + 16) ||
-      cudaMalloc(&T1, sizeof(float) * trows * std::max(h->maxw, h->r_u) + 16) ||
-      cudaMalloc(&Jt, sizeof(float) * trows * h->r_u + 16) ||
-      cudaMalloc(&Jd, sizeof(float) * chunk * outw * d_z + 16)) {
-    cleanup();
-    return fail(SDN_ERR_NOMEM, "jacobian scratch allocation failed");
+  const int64_t chunk = jac_chunk_samples(h, decoded != 0);
+  if (chunk > h->jin_cap) {
+    int rc;
+    if ((rc = dalloc(h, &h->jmr, (size_t)chunk * h->r_m)) || (rc = dalloc(h, &h->jz, (size_t)chunk * d_z)) ||
+        (rc = dalloc(h, &h->jX, (size_t)chunk * h->ldx)) ||
+        (rc = dalloc(h, &h->jJ, (size_t)chunk * std::max<int64_t>(h->d_u, h->r_u) * d_z)))
+      return rc;
+    h->jin_cap = chunk;
   }
-  for (int64_t s = 0; s < n && rc == SDN_OK; s += chunk) {
-    const int64_t m = std::min(chunk, n - s), rows = m * d_z;
-    if (cudaMemcpyAsync(mr, m_r + s * h->r_m, sizeof(float) * m * h->r_m, cudaMemcpyHostToDevice, h->stream) ||
-        cudaMemcpyAsync(zz, z + s * d_z, sizeof(float) * m * d_z, cudaMemcpyHostToDevice, h->stream)) {
-      rc = fail(SDN_ERR_CUDA, "upload failed");
-      break;
-    }
-    if ((rc = forward_rows(h, mr, zz, m, X, true, h->Y))) break;
-    float* Tc = T0;
-    float* Tn = T1;
-    if (L == 1) {
-      // linear model: tangent of y is the constant Pz (w[1] = r_u)
-      k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, nullptr, h->Pz32t, Tc);
-    } else if (h->act == ACT_SOFTMAX) {          // T = a (U - a.U), U = (W1_z V_z^T)_k
-      k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, nullptr, h->Pz32t, Tc);
-      k_softmax_tangent<<<(unsigned)cdiv(rows, 8), 256, 0, h->stream>>>(rows, d_z, h->h1, h->D[0], Tc, nullptr);
-      h->launches++;
-    } else {
-      k_tangent_seed<<<(unsigned)rows, 128, 0, h->stream>>>(rows, d_z, h->h1, h->D[0], h->Pz32t, Tc);
-    }
-    h->launches++;
-    for (int l = 1; l < L - 1 && rc == SDN_OK; ++l) {
-      const bool smax = h->act == ACT_SOFTMAX;
-      EpiTangent e{smax ? nullptr : h->D[l], (int64_t)h->w[l + 1], d_z, (h->res[l] && !smax) ? Tc : nullptr, Tn,
-                   (int64_t)h->w[l + 1]};
-      rc = gemm<false, true>(h, rows, nullptr, h->w[l + 1], h->w[l], Tc, h->w[l], h->W[l], h->w[l], e);
-      if (smax && rc == SDN_OK) {
-        k_softmax_tangent<<<(unsigned)cdiv(rows, 8), 256, 0, h->stream>>>(rows, d_z, h->w[l + 1], h->D[l], Tn,
-                                                                          h->res[l] ? Tc : nullptr);
-        h->launches++;
-      }
-      std::swap(Tc, Tn);
-    }
-    if (rc) break;
-    if (L >= 2) {
-      if (!decoded) {
-        EpiJacScatter e{h->ostd, Jd, d_z, (int64_t)h->r_u};
-        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->w[L - 1], Tc, h->w[L - 1], h->W[L - 1], h->w[L - 1], e);
-      } else {
-        EpiAffine e{nullptr, h->ostd, nullptr, Jt, (int64_t)h->r_u};
-        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->w[L - 1], Tc, h->w[L - 1], h->W[L - 1], h->w[L - 1], e);
-      }
-    } else {
-      if (!decoded) {
-        // Tc rows already hold dy/dz; scale by std and scatter via a unit GEMM
-        EpiJacScatter e{h->ostd, Jd, d_z, (int64_t)h->r_u};
-        std::vector<float> eye((size_t)h->r_u * h->r_u, 0.0f);
-        for (int i = 0; i < h->r_u; ++i) eye[(size_t)i * h->r_u + i] = 1.0f;
-        float* I = nullptr;
-        cudaMalloc(&I, sizeof(float) * eye.size());
-        cudaMemcpy(I, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice);
-        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->r_u, Tc, h->r_u, I, h->r_u, e);
-        cudaStreamSynchronize(h->stream);
-        cudaFree(I);
-      } else {
-        EpiAffine e{nullptr, h->ostd, nullptr, Jt, (int64_t)h->r_u};
-        std::vector<float> eye((size_t)h->r_u * h->r_u, 0.0f);
-        for (int i = 0; i < h->r_u; ++i) eye[(size_t)i * h->r_u + i] = 1.0f;
-        float* I = nullptr;
-        cudaMalloc(&I, sizeof(float) * eye.size());
-        cudaMemcpy(I, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice);
-        rc = gemm<false, true>(h, rows, nullptr, h->r_u, h->r_u, Tc, h->r_u, I, h->r_u, e);
-        cudaStreamSynchronize(h->stream);
-        cudaFree(I);
-      }
-    }
-    if (rc) break;
-    if (decoded) {
-      EpiJacScatter e{nullptr, Jd, d_z, (int64_t)h->d_u};
-      if ((rc = gemm<false, true>(h, rows, nullptr, (int)h->d_u, h->r_u, Jt, h->r_u, h->U, h->r_u, e))) break;
-    }
-    if (cudaMemcpyAsync(J + s * outw * d_z, Jd, sizeof(float) * m * outw * d_z, cudaMemcpyDeviceToHost,
-                        h->stream) ||
-        cudaStreamSynchronize(h->stream))
-      rc = fail(SDN_ERR_CUDA, "download failed");
+  for (int64_t s = 0; s < n; s += chunk) {
+    const int64_t m = std::min(chunk, n - s);
+    CU(cudaMemcpyAsync(h->jmr, m_r + s * h->r_m, sizeof(float) * m * h->r_m, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(h->jz, z + s * d_z, sizeof(float) * m * d_z, cudaMemcpyHostToDevice, h->stream));
+    TRY(forward_rows(h, h->jmr, h->jz, m, h->jX, true, h->Y));
+    TRY(jac_rows(h, 0, m, decoded != 0, h->jJ));
+    CU(cudaMemcpyAsync(J + s * outw * d_z, h->jJ, sizeof(float) * m * outw * d_z, cudaMemcpyDeviceToHost, h->stream));
   }
-  cleanup();
-  return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  return SDN_OK;
+}
+
+// the resident samples (sdn_set_samples) at one control z: J_dev (device,
+// n x outw x d_z) -- the benchmarked c5 path: no host transfer but z
+int sdn_jacobian_samples(sdn_handle* h, const double* z, int32_t decoded, float* J_dev) {
+  if (!h || !z || !J_dev) return fail(SDN_ERR_ARG, "null argument");
+  if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
+  if (decoded && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  if (h->n < 1) return fail(SDN_ERR_ARG, "empty sample set");
+  CU(cudaSetDevice(h->device));
+  const int64_t outw = decoded ? h->d_u : h->r_u;
+  sdn_risk r{};
+  r.kind = SDN_RISK_MEAN;
+  TRY(upload_z(h, z, &r, 1));
+  k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb, h->zb64);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  TRY(run_forward(h, h->n, h->MR, h->r_m, h->r_m, h->W[0], h->r_m, h->zb, true, h->Y,
+                  h->tcw.enabled ? &h->tcw.mr : nullptr));
+  const int64_t chunk = jac_chunk_samples(h, decoded != 0);
+  for (int64_t s = 0; s < h->n; s += chunk) {
+    const int64_t m = std::min(chunk, h->n - s);
+    TRY(jac_rows(h, s, m, decoded != 0, J_dev + s * outw * h->d_z));
+  }
+  return SDN_OK;
 }
 
 // decoder: Gram K = U^T M U (split-K fp64), c = U^T M (b - u_t), q0 (host fp64)
 int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubias, const float* Mdiag,
                     const float* u_target) {
   if (!h || !U || !ubias || !Mdiag || !u_target || d_u < 1) return fail(SDN_ERR_ARG, "bad argument");
-  if (d_u % 4 != 0 && false) return fail(SDN_ERR_ARG, "d_u");
   CU(cudaSetDevice(h->device));
   const int r_u = h->r_u;
-  std::vector<double> cd(r_u, 0.0);
-  double q0 = 0.0;
-  std::vector<float> um((size_t)d_u * r_u);
-  for (int64_t d = 0; d < d_u; ++d) {
-    const double s = (double)ubias[d] - (double)u_target[d];
-    const double ms = (double)Mdiag[d] * s;
-    q0 += s * ms;
-    for (int j = 0; j < r_u; ++j) {
-      cd[j] += (double)U[d * r_u + j] * ms;
-      um[(size_t)d * r_u + j] = (float)((double)Mdiag[d] * (double)U[d * r_u + j]);
-    }
-  }
+  // everything on the device: Um = diag(M) U, c and q0 (fixed-order fp64
+  // block sums), the Gram K = Um^T U (split-K fp64 GEMM); one read-back of q0
   if (h->U) { cudaFree(h->U); h->U = nullptr; }
   if (h->ub) { cudaFree(h->ub); h->ub = nullptr; }
   if (!h->Kg) CU(cudaMalloc(&h->Kg, sizeof(float) * r_u * r_u));
   if (!h->cdec) CU(cudaMalloc(&h->cdec, sizeof(float) * r_u));
   if (!h->KPhi) CU(cudaMalloc(&h->KPhi, sizeof(float) * h->cap * r_u));
+  if (!h->c64dec) CU(cudaMalloc(&h->c64dec, sizeof(double) * r_u));
   CU(cudaMalloc(&h->U, sizeof(float) * d_u * r_u));
   CU(cudaMalloc(&h->ub, sizeof(float) * d_u));
-  CU(cudaMemcpy(h->U, U, sizeof(float) * d_u * r_u, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(h->ub, ubias, sizeof(float) * d_u, cudaMemcpyHostToDevice));
-  float* Um = nullptr;
-  double* K64 = nullptr;
-  CU(cudaMalloc(&Um, sizeof(float) * d_u * r_u));
-  CU(cudaMalloc(&K64, sizeof(double) * r_u * r_u));
-  CU(cudaMemcpy(Um, um.data(), sizeof(float) * um.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemset(K64, 0, sizeof(double) * r_u * r_u));
-  const int64_t kc = 2048;
+  float *Um = nullptr, *Md = nullptr, *ut = nullptr;
+  double *K64 = nullptr, *q0d = nullptr;
+  auto cleanup = [&]() { cudaFree(Um); cudaFree(Md); cudaFree(ut); cudaFree(q0d); };
+  if (cudaMalloc(&Um, sizeof(float) * d_u * r_u) || cudaMalloc(&Md, sizeof(float) * d_u) ||
+      cudaMalloc(&ut, sizeof(float) * d_u) || cudaMalloc(&q0d, sizeof(double)) ||
+      cudaMalloc(&K64, sizeof(double) * r_u * r_u)) {
+    cleanup();
+    return fail(SDN_ERR_NOMEM, "decoder scratch allocation failed");
+  }
   int rc = SDN_OK;
-  for (int64_t k0 = 0; k0 < d_u && rc == SDN_OK; k0 += kc) {
-    const int kl = (int)std::min(kc, d_u - k0);
-    // K += (Um[k0:k0+kl])^T U[k0:k0+kl]  (A stored K x M: AT)
-    rc = gemm<true, false>(h, r_u, nullptr, r_u, kl, Um + k0 * r_u, r_u, h->U + k0 * r_u, r_u,
-                           EpiAccum64{K64, (int64_t)r_u});
-  }
-  std::vector<double> k64((size_t)r_u * r_u);
-  std::vector<float> k32((size_t)r_u * r_u);
+  if (cudaMemcpyAsync(h->U, U, sizeof(float) * d_u * r_u, cudaMemcpyHostToDevice, h->stream) ||
+      cudaMemcpyAsync(h->ub, ubias, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream) ||
+      cudaMemcpyAsync(Md, Mdiag, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream) ||
+      cudaMemcpyAsync(ut, u_target, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream) ||
+      cudaMemsetAsync(K64, 0, sizeof(double) * r_u * r_u, h->stream))
+    rc = fail(SDN_ERR_CUDA, "decoder upload failed");
   if (rc == SDN_OK) {
-    cudaStreamSynchronize(h->stream);
-    cudaMemcpy(k64.data(), K64, sizeof(double) * k64.size(), cudaMemcpyDeviceToHost);
-    for (size_t i = 0; i < k64.size(); ++i) k32[i] = (float)k64[i];
-    cudaMemcpy(h->Kg, k32.data(), sizeof(float) * k32.size(), cudaMemcpyHostToDevice);
-    std::vector<float> c32(r_u);
-    for (int j = 0; j < r_u; ++j) c32[j] = (float)cd[j];
-    cudaMemcpy(h->cdec, c32.data(), sizeof(float) * r_u, cudaMemcpyHostToDevice);
-    if (!h->c64dec) CU(cudaMalloc(&h->c64dec, sizeof(double) * r_u));
-    cudaMemcpy(h->c64dec, cd.data(), sizeof(double) * r_u, cudaMemcpyHostToDevice);
+    k_dec_scale<<<(unsigned)std::min<int64_t>(cdiv(d_u * r_u, 256), 4096), 256, 0, h->stream>>>(d_u, r_u, h->U, Md, Um);
+    k_dec_c<<<(unsigned)(r_u + 1), 256, 0, h->stream>>>(d_u, r_u, h->U, h->ub, Md, ut, h->c64dec, q0d);
+    k_f64_to_f32<<<1, 256, 0, h->stream>>>(r_u, h->c64dec, h->cdec);
+    h->launches += 3;
+    const int64_t kc = 2048;
+    for (int64_t k0 = 0; k0 < d_u && rc == SDN_OK; k0 += kc) {
+      const int kl = (int)std::min(kc, d_u - k0);
+      // K += (Um[k0:k0+kl])^T U[k0:k0+kl]  (A stored K x M: AT)
+      rc = gemm<true, false>(h, r_u, nullptr, r_u, kl, Um + k0 * r_u, r_u, h->U + k0 * r_u, r_u,
+                             EpiAccum64{K64, (int64_t)r_u});
+    }
   }
-  cudaFree(Um);
+  double q0 = 0.0;
+  if (rc == SDN_OK) {
+    k_f64_to_f32<<<(unsigned)cdiv(r_u * r_u, 256), 256, 0, h->stream>>>((int64_t)r_u * r_u, K64, h->Kg);
+    h->launches++;
+    if (cudaMemcpyAsync(&q0, q0d, sizeof(double), cudaMemcpyDeviceToHost, h->stream) ||
+        cudaStreamSynchronize(h->stream))
+      rc = fail(SDN_ERR_CUDA, "decoder set-up failed");
+  }
+  // the decoder basis as a tensor-core operand (rows padded to 16) for the
+  // decoded Jacobian GEMM
+  if (rc == SDN_OK && h->tcw.enabled) {
+    const int64_t d16 = (d_u + 15) / 16 * 16;
+    if (!h->usplit.hi || h->usplit.rows < d16) {
+      if (tc_buf(h, h->tcw, h->usplit, d16, r_u)) rc = fail(SDN_ERR_NOMEM, "decoder operand allocation failed");
+    }
+    if (rc == SDN_OK) {
+      cudaMemsetAsync(h->usplit.hi, 0, sizeof(__nv_bfloat16) * 2 * h->usplit.rows * r_u, h->stream);
+      k_split<<<(unsigned)std::min<int64_t>(cdiv(d_u * r_u, 256), 4096), 256, 0, h->stream>>>(
+          d_u, nullptr, r_u, r_u, h->U, r_u, h->usplit.hi, h->usplit.lo);
+      h->launches++;
+      h->d_u16 = d16;
+    }
+  }
+  cleanup();
   if (h->K64) cudaFree(h->K64);
   h->K64 = K64;                 // kept (fp64) for the refinement chain's decoded QoI
   if (rc) return rc;

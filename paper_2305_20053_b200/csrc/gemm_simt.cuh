@@ -270,18 +270,21 @@ struct EpiTangent {
 
 // Jacobian scatter: tangent row (i*d_z + k), column u -> J[i, u, k] * scale[u]
 // (surrogate.py:232-233: out_std * T^T).  ncol = r_u (or d_u when decoding).
+// (nvalid: columns past it are GEMM padding and not written; 0 = ncol)
 struct EpiJacScatter {
-  const float* scale; float* J; int d_z; int64_t ncol;
+  const float* scale; float* J; int d_z; int64_t ncol; int64_t nvalid = 0;
   SDN_DEV void operator()(int64_t r, int c, float4 v) const {
     int64_t i = r / d_z; int k = (int)(r % d_z);
     float x[4] = {v.x, v.y, v.z, v.w};
     float* base = J + i * ncol * d_z + k;
+    const int64_t nv = nvalid ? nvalid : ncol;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) base[(int64_t)(c + j) * d_z] = scale ? x[j] * scale[c + j] : x[j];
+    for (int j = 0; j < 4; ++j)
+      if (c + j < nv) base[(int64_t)(c + j) * d_z] = scale ? x[j] * scale[c + j] : x[j];
   }
   SDN_DEV void col(int64_t r, int c, float v) const {
     int64_t i = r / d_z; int k = (int)(r % d_z);
-    J[i * ncol * d_z + (int64_t)c * d_z + k] = scale ? v * scale[c] : v;
+    if (c < (nvalid ? nvalid : ncol)) J[i * ncol * d_z + (int64_t)c * d_z + k] = scale ? v * scale[c] : v;
   }
 };
 

@@ -426,7 +426,8 @@ SDN_DEV int sw_h(int r, int h) { return r * 8 + ((h ^ ((r >> 2) & 1)) << 2); }
 struct TileRows {
   int64_t r0, M;          // first row of the warp's 32, valid-row bound
   const int* gather;      // optional row map for gathered inputs
-  SDN_DEV int64_t src(int64_t r) const { return gather ? (int64_t)gather[r] : r; }
+  int rowdiv = 1;         // gathered inputs without a map: row r reads row r / rowdiv (tangent rows -> sample)
+  SDN_DEV int64_t src(int64_t r) const { return gather ? (int64_t)gather[r] : r / rowdiv; }
 };
 
 // coalesced global -> smem (swizzled) for 32 rows x 16 fp32 columns
@@ -850,6 +851,128 @@ struct TileEpi<TcChain<EpiBwd>> {
       tile_out_h(s.h, ch.split.hi, ch.split.ld, tr, c0, N, lane);
       tile_out_h(s.l, ch.split.lo, ch.split.ld, tr, c0, N, lane);
     }
+    __syncwarp();
+  }
+};
+
+// forward-mode tangent step on the tensor cores (surrogate.py:208-223, with
+// the residual): T_out = D[row / rowdiv] * acc [+ T_in].  Tangent rows are
+// (sample i, control k) = i * d_z + k, so rowdiv = d_z gathers the sample's
+// act' row.  T_in is read from the split of the layer input (the A operand,
+// ch.prev) and T_out is written only as the next GEMM's split (ch.split).
+struct EpiTanTc {
+  const float* D;
+  int64_t ldD;
+  int rowdiv;
+  SDN_DEV void operator()(int64_t, int, float4) const {}
+  SDN_DEV void col(int64_t, int, float) const {}
+};
+struct PreTan {
+  float4 d[4];           // gathered act'
+  uint4 u[4];            // T_in split: hi[0..1] / lo[2..3]
+};
+template <>
+struct TileEpi<TcChain<EpiTanTc>> {
+  using Pre = PreTan;
+  static SDN_DEV void load(const TcChain<EpiTanTc>& ch, const TileRows& tr, int c0, int N, int lane, Pre& p) {
+    TileRows tg = tr;
+    tg.gather = nullptr;
+    tg.rowdiv = ch.base.rowdiv;
+    tile_fetch(p.d, ch.base.D, ch.base.ldD, tg, true, c0, N, lane);
+    if (ch.prev.hi) {
+      tile_fetch_h(p.u, ch.prev.hi, ch.prev.ld, tr, c0, N, lane);
+      tile_fetch_h(p.u + 2, ch.prev.lo, ch.prev.ld, tr, c0, N, lane);
+    }
+  }
+  static SDN_DEV void chunk(const TcChain<EpiTanTc>& ch, const EpiSmem& s, const TileRows& tr, int c0, int N,
+                            int lane, const uint32_t (&v)[16], const Pre& pre) {
+    epi_reclaim(s, lane);
+    tile_stash(s.f1, pre.d, lane);
+    if (ch.prev.hi) {
+      tile_stash_h(s.h, pre.u, lane);
+      tile_stash_h(s.l, pre.u + 2, lane);
+    }
+    __syncwarp();
+    float t[16], dd[16];
+    row_get(s.f1, lane, dd);
+    if (ch.prev.hi) row_get_split(s.h, s.l, lane, t);
+    else
+#pragma unroll
+      for (int j = 0; j < 16; ++j) t[j] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = fmaf(dd[j], __uint_as_float(v[j]), t[j]);
+    __syncwarp();
+    row_put_split(s.h, s.l, lane, t);
+    if (s.om) {
+      epi_issue(s, lane, tr.r0, c0, false, false, true, true);
+      return;
+    }
+    __syncwarp();
+    tile_out_h(s.h, ch.split.hi, ch.split.ld, tr, c0, N, lane);
+    tile_out_h(s.l, ch.split.lo, ch.split.ld, tr, c0, N, lane);
+    __syncwarp();
+  }
+};
+
+// Jacobian scatter on the tensor-core path: row r = i d_z + k, column u ->
+// J[i, u, k] (* scale[u]).  A warp's 32 rows are consecutive k of one or two
+// samples, so each column's store is one or two contiguous runs; (i, k) is
+// computed once per chunk in 32-bit arithmetic.
+template <>
+struct TileEpi<EpiJacScatter> {
+  using Pre = PreNone;
+  static SDN_DEV void load(const EpiJacScatter&, const TileRows&, int, int, int, Pre&) {}
+  static SDN_DEV void chunk(const EpiJacScatter& e, const EpiSmem&, const TileRows& tr, int c0, int N, int lane,
+                            const uint32_t (&v)[16], const Pre&) {
+    const int64_t row = tr.r0 + lane;
+    if (row >= tr.M) return;
+    const unsigned rr = (unsigned)row, dz = (unsigned)e.d_z;
+    const unsigned i = rr / dz, k = rr - i * dz;
+    float* base = e.J + (int64_t)i * e.ncol * e.d_z + k;
+    const int nv = (int)(e.nvalid ? e.nvalid : e.ncol);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = c0 + j;
+      if (c < nv) {
+        const float x = __uint_as_float(v[j]);
+        __stcs(base + (int64_t)c * e.d_z, e.scale ? x * __ldg(e.scale + c) : x);   // streaming: written once
+      }
+    }
+  }
+};
+
+// scale * acc -> bf16x3 split only (the Jacobian's output layer when it is
+// decoded next: std . (T W^T) feeds the decoder GEMM)
+struct EpiScaleSplit {
+  const float* scale;
+  TcEpiSplit split;
+  SDN_DEV void operator()(int64_t, int, float4) const {}
+  SDN_DEV void col(int64_t, int, float) const {}
+};
+template <>
+struct TileEpi<EpiScaleSplit> {
+  using Pre = PreNone;
+  static SDN_DEV void load(const EpiScaleSplit&, const TileRows&, int, int, int, Pre&) {}
+  static SDN_DEV void chunk(const EpiScaleSplit& e, const EpiSmem& s, const TileRows& tr, int c0, int N, int lane,
+                            const uint32_t (&v)[16], const Pre&) {
+    float x[16];
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      const float4 sc = __ldg(reinterpret_cast<const float4*>(e.scale + min(c0 + j, N - 4)));
+      x[j] = sc.x * __uint_as_float(v[j]);
+      x[j + 1] = sc.y * __uint_as_float(v[j + 1]);
+      x[j + 2] = sc.z * __uint_as_float(v[j + 2]);
+      x[j + 3] = sc.w * __uint_as_float(v[j + 3]);
+    }
+    epi_reclaim(s, lane);
+    row_put_split(s.h, s.l, lane, x);
+    if (s.om) {
+      epi_issue(s, lane, tr.r0, c0, false, false, true, true);
+      return;
+    }
+    __syncwarp();
+    tile_out_h(s.h, e.split.hi, e.split.ld, tr, c0, N, lane);
+    tile_out_h(s.l, e.split.lo, e.split.ld, tr, c0, N, lane);
     __syncwarp();
   }
 };
@@ -1901,6 +2024,18 @@ struct EpiOut<TcChain<EpiBwd>> {
     if (e.resid && tc_out_map(t, e.resid, false, M, N, e.ld, &om.m[4])) return 1;
     if (tc_out_map(t, e.D, false, M, N, e.ldD, &om.m[5])) return 1;
     return 3;
+  }
+};
+template <>
+struct EpiOut<TcChain<EpiTanTc>> {
+  static int build(TcWeights& t, const TcChain<EpiTanTc>& ch, int64_t M, int N, TcOutMaps& om) {
+    return tc_out_map_pair(t, ch.split.hi, ch.split.lo, M, N, ch.split.ld, &om.m[2]) == 0 ? 1 : 0;
+  }
+};
+template <>
+struct EpiOut<EpiScaleSplit> {
+  static int build(TcWeights& t, const EpiScaleSplit& e, int64_t M, int N, TcOutMaps& om) {
+    return tc_out_map_pair(t, e.split.hi, e.split.lo, M, N, e.split.ld, &om.m[2]) == 0 ? 1 : 0;
   }
 };
 // the summing reverse step stores nothing through TMA: its maps are the

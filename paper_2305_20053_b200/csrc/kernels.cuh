@@ -771,6 +771,79 @@ __global__ void k_tangent_seed(int64_t rows, int d_z, int h1, const float* __res
     T[r * h1 + c] = (D0 ? D0[i * h1 + c] : 1.0f) * Pz32t[(int64_t)k * h1 + c];
 }
 
+// the same seed written as the first tangent GEMM's bf16x3 split operand
+// (rows x ld, columns [h1, ld) zero): T[(i,k), c] = D0[i, c] Pz[k, c]
+__global__ void __launch_bounds__(256)
+k_tangent_seed_split(int64_t rows, int d_z, int h1, int ld, const float* __restrict__ D0,
+                     const float* __restrict__ Pz32t, __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+  // one warp per tangent row (8 rows per block, grid-strided), lanes over column pairs
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * 8) {
+    const unsigned i = (unsigned)(r / d_z), k = (unsigned)(r - (int64_t)i * d_z);
+    const float* dr = D0 ? D0 + (int64_t)i * h1 : nullptr;
+    const float* pr = Pz32t + (int64_t)k * h1;
+    __nv_bfloat162* ph = reinterpret_cast<__nv_bfloat162*>(hi + r * ld);
+    __nv_bfloat162* pl = reinterpret_cast<__nv_bfloat162*>(lo + r * ld);
+    for (int c = 2 * lane; c < ld; c += 64) {
+      float x0 = 0.0f, x1 = 0.0f;
+      if (c < h1) x0 = (dr ? __ldg(dr + c) : 1.0f) * __ldg(pr + c);
+      if (c + 1 < h1) x1 = (dr ? __ldg(dr + c + 1) : 1.0f) * __ldg(pr + c + 1);
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1b = __float2bfloat16_rn(x1);
+      ph[c / 2] = __halves2bfloat162(h0, h1b);
+      pl[c / 2] = __halves2bfloat162(__float2bfloat16_rn(x0 - __bfloat162float(h0)),
+                                     __float2bfloat16_rn(x1 - __bfloat162float(h1b)));
+    }
+  }
+}
+
+// linear model Jacobian (one layer): dy/dz rows are the seed; scale by the
+// output std into Jt (rows x r_u, decoded next) or scatter into J[i, u, k]
+__global__ void k_scale_cols(int64_t rows, int r_u, const float* __restrict__ scale, const float* __restrict__ T,
+                             float* __restrict__ Jt, float* __restrict__ J, int d_z) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * r_u;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / r_u;
+    const int u = (int)(e % r_u);
+    const float v = scale[u] * T[e];
+    if (Jt) Jt[e] = v;
+    else J[((r / d_z) * r_u + u) * d_z + r % d_z] = v;
+  }
+}
+
+// decoder set-up on the device (pod.py:104-110): Um = diag(M) U (fp32 of the
+// fp64 product, the Gram GEMM's A), and per block j < r_u the fixed-order fp64
+// c_j = sum_d U[d, j] M[d] (b[d] - u_t[d]); block r_u: q0 = sum_d M s^2
+__global__ void k_dec_scale(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restrict__ Mdiag,
+                            float* __restrict__ Um) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < d_u * r_u;
+       e += (int64_t)gridDim.x * blockDim.x)
+    Um[e] = (float)((double)Mdiag[e / r_u] * (double)U[e]);
+}
+__global__ void __launch_bounds__(256)
+k_dec_c(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restrict__ ub,
+        const float* __restrict__ Mdiag, const float* __restrict__ ut, double* __restrict__ c, double* __restrict__ q0) {
+  __shared__ double sw[8];
+  const int j = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t d = threadIdx.x; d < d_u; d += blockDim.x) {
+    const double sd = (double)ub[d] - (double)ut[d], ms = (double)Mdiag[d] * sd;
+    acc += j < r_u ? (double)U[d * r_u + j] * ms : sd * ms;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sw[w];
+    if (j < r_u) c[j] = t;
+    else *q0 = t;
+  }
+}
+__global__ void k_f64_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    b[e] = (float)a[e];
+}
+
 // ---- per-layer vector softmax (surrogate.py:175-177, 214-217), SIMT chains
 // One warp per row, fp64 row reductions (fixed lane order), widths <= any.
 // forward: a = softmax(S) over the row; H = [prev +] a; D = a (for the sweep)

@@ -266,6 +266,29 @@ class Engine:
               "sdn_jacobian_batch")
         return J if decoded or self.r_u4 == self.r_u else np.ascontiguousarray(J[:, :self.r_u, :])
 
+    def jacobian_samples(self, z, decoded: bool = False, out=None):
+        """Control Jacobians of the resident samples at control z (BASELINE
+        config 5), computed into a device buffer: a torch CUDA tensor of
+        shape (n, r_u, d_z), or (n, d_u, d_z) decoded.  `out` may pass a
+        preallocated tensor of that shape (float32, contiguous)."""
+        import torch
+        z = _f64(z)
+        if z.shape != (self.d_z,):
+            raise ValueError(f"control must have shape ({self.d_z},)")
+        if decoded and self.d_u is None:
+            raise RuntimeError("set_decoder first")
+        outw = self.d_u if decoded else self.r_u4
+        shape = (self.n, outw, self.d_z)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=f"cuda:{self.device}")
+        elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous float32 tensor of shape {shape}")
+        check(lib.sdn_jacobian_samples(self.h, dptr(z), int(bool(decoded)), C.c_void_p(out.data_ptr())),
+              "sdn_jacobian_samples")
+        if not decoded and self.r_u4 != self.r_u:
+            return out[:, :self.r_u, :]
+        return out
+
     def lift(self, phi) -> np.ndarray:
         phi = np.atleast_2d(_f32(_padcols(np.atleast_2d(np.asarray(phi, np.float32)), self.r_u4)))
         u = np.empty((phi.shape[0], self.d_u), np.float32)

@@ -155,3 +155,38 @@ def test_c4_full_size_exact_cvar_matches_oracle():
     o = ref.saa_objective(Qo, Go, p.z, ref.Risk("cvar_exact", beta=0.99, alpha=cfg.alpha))
     assert abs(r.value - o[0]) <= RTOL * abs(o[0])
     assert _rel(r.grad_z, o[1]) <= RTOL
+
+
+def test_c5_full_n_decoded_jacobian_on_device():
+    """c5 at BASELINE size through the device path (sdn_jacobian_samples):
+    16384 samples decoded to d_u x d_z = 1089 x 25 (1.78 GB written to a device
+    buffer, no host copy).  A random subset matches the float64 oracle's
+    decoded Jacobian U J (test_acceptance.py:326); at full size the decoded
+    output equals U applied to the same path's reduced Jacobian (float64 on
+    the GPU), and the reduced Jacobian equals the host-API batch path."""
+    import torch
+    cfg = wl.WORKLOADS["c5"]
+    n = cfg.n_samples
+    p = wl.make_problem(cfg, seed=0, count=n, with_decoder=True)
+    eng = Engine(p, max_samples=n)
+    eng.set_tracking(p.c, p.q0)
+    eng.set_decoder(p.U, p.ubias, p.Mdiag_u, p.u_target)
+    eng.set_samples(p.m_r)
+    Jd = eng.jacobian_samples(p.z, decoded=True)
+    Jr = eng.jacobian_samples(p.z, decoded=False)
+    eng.synchronize()
+    assert tuple(Jd.shape) == (n, cfg.d_u, cfg.d_z) and bool(torch.isfinite(Jd).all())
+    sub = np.random.default_rng(7).choice(n, 48, replace=False)
+    Z = np.broadcast_to(p.z, (n, cfg.d_z))
+    Jo = ref.z_jacobian_batch(ref.as_oracle(p), p.m_r[sub], Z[sub])
+    Jdo = np.einsum("du,iuk->idk", p.U.astype(np.float64), Jo)
+    assert _rel(Jd[sub].cpu().numpy(), Jdo) <= RTOL
+    assert _rel(Jr[sub].cpu().numpy(), Jo) <= RTOL
+    U = torch.from_numpy(p.U.astype(np.float64)).cuda()
+    for a in range(0, n, 4096):                      # full size: decode == U (reduced), float64
+        ref_d = torch.einsum("du,iuk->idk", U, Jr[a:a + 4096].double())
+        err = (Jd[a:a + 4096].double() - ref_d).norm() / ref_d.norm()
+        assert float(err) <= 1e-5
+    Jh = eng.jacobian_batch(p.m_r[:1024], Z[:1024])
+    # (the host API's forward takes z per row, so its act' differs in the last bits)
+    assert _rel(Jr[:1024].cpu().numpy(), Jh) <= 1e-5
