@@ -22,6 +22,8 @@ import math
 from dataclasses import dataclass, field
 from typing import Optional
 
+import hashlib
+
 import numpy as np
 
 from .engine import Engine
@@ -90,13 +92,29 @@ class SurrogateModel:
         if eng is None or eng.max_samples < min(rows, 1 << 16):
             eng = Engine(self, max_samples=max(min(rows, 1 << 16), 256), device=self.device)
             object.__setattr__(self, "_eng", eng)
+            object.__setattr__(self, "_eng_digest", self._digest())
         return eng
 
+    def _digest(self) -> bytes:
+        h = hashlib.blake2b(digest_size=16)
+        for a in (*self.weights, *self.biases, self.input_scale, self.output_mean, self.output_std, self.Vz):
+            if a is not None:
+                a = np.ascontiguousarray(a)
+                h.update(str(a.dtype).encode() + str(a.shape).encode())
+                h.update(memoryview(a).cast("B"))
+        return h.digest()
+
     def refresh(self):
-        """Push modified weights to the device (after in-place edits)."""
+        """Push the weights to the device if they changed since the last
+        upload (in-place edits included: the check is a digest of every
+        parameter's bytes, far cheaper than re-uploading and re-splitting)."""
         eng = getattr(self, "_eng", None)
-        if eng is not None:
+        if eng is None:
+            return
+        d = self._digest()
+        if d != getattr(self, "_eng_digest", None):
             eng.set_model(self)
+            object.__setattr__(self, "_eng_digest", d)
 
     def _check(self, m_r, z):
         if np.shape(m_r)[-1] != self.spec.r_m or np.shape(z)[-1] != self.spec.d_z:
@@ -109,8 +127,9 @@ class SurrogateModel:
         """phi = out_mean + out_std * net(x), (B, r_u) float64 (surrogate.py:187-191)."""
         self._check(m_r, z)
         m_r = np.atleast_2d(m_r)
+        eng = self._engine(m_r.shape[0])
         self.refresh()
-        return self._engine(m_r.shape[0]).forward_batch(m_r, z).astype(np.float64)
+        return eng.forward_batch(m_r, z).astype(np.float64)
 
     def z_jacobian(self, m_r, z) -> np.ndarray:
         return self.z_jacobian_batch(np.asarray(m_r)[None, :], np.asarray(z)[None, :])[0]
@@ -119,8 +138,9 @@ class SurrogateModel:
         """d(phi)/d(z), (B, r_u, d_z) (surrogate.py:229-233), forward mode on the GPU."""
         self._check(m_r, z)
         m_r = np.atleast_2d(m_r)
+        eng = self._engine(m_r.shape[0])
         self.refresh()
-        return self._engine(m_r.shape[0]).jacobian_batch(m_r, z).astype(np.float64)
+        return eng.jacobian_batch(m_r, z).astype(np.float64)
 
 
 def init_model(spec: NetworkSpec, seed: int, input_scale=None, output_mean=None, output_std=None,
@@ -421,6 +441,20 @@ def minimize(prob: SAAProblem, z0, t0: Optional[float] = None, max_iter: int = 5
         v, gz, _ = saa_objective(prob, xv)
         return float(v), np.asarray(gz, float)
 
+    # Armijo trials on the fused device path ask for the value only (forward,
+    # QoI, risk; no reverse sweep); the gradient is evaluated once a step is
+    # accepted.  The iterates are the reference's: it computes (f, g) per trial
+    # (riskopt.py:335-344) but uses g only at the accepted point.  Other
+    # evaluators (the duck-typed protocol) return Q and G together anyway.
+    fused = isinstance(prob.evaluator, SurrogateEvaluator)
+
+    def f_only(xv):
+        if not fused:
+            return fg(xv)
+        r = prob.evaluator.risk_and_grad(xv[:-1] if use_t else xv, prob.risk, xv[-1] if use_t else None,
+                                         need_grad=False)
+        return float(r.value), None
+
     f, g = fg(x)
     pairs: list = []
     history, pg_history = [f], []
@@ -442,7 +476,7 @@ def minimize(prob: SAAProblem, z0, t0: Optional[float] = None, max_iter: int = 5
             dx = x_new - x
             if not np.any(dx):
                 break
-            f_new, g_new = fg(x_new)
+            f_new, g_new = f_only(x_new)
             if np.isfinite(f_new) and f_new <= f + 1e-4 * float(g @ dx):
                 accepted = True
                 break
@@ -450,6 +484,8 @@ def minimize(prob: SAAProblem, z0, t0: Optional[float] = None, max_iter: int = 5
         if not accepted:
             ls_failed = True
             break
+        if g_new is None:
+            f_new, g_new = fg(x_new)
         s_vec, y_vec = x_new - x, g_new - g
         sy = float(s_vec @ y_vec)
         if sy > 1e-12 * np.linalg.norm(s_vec) * np.linalg.norm(y_vec):

@@ -237,6 +237,11 @@ struct sdn_handle {
   float* jT[2] = {nullptr, nullptr};   // SIMT tangents (rows x maxw)
   float* jJt = nullptr;         // SIMT std . dy/dz (rows x r_u)
   int64_t jin_cap = 0;          // host-input scratch (sdn_jacobian_batch): samples
+  // grow-only device scratch for the host-facing entry points (no per-call
+  // cudaMalloc/cudaFree; freed at destroy)
+  void* scr[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t scr_bytes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  TcOperand lift_in;            // lift: phi split (rows x r_u)
   float *jmr = nullptr, *jz = nullptr, *jX = nullptr, *jJ = nullptr;
   bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
   bool ref_trace = false;       // env SDN_REFINE_TRACE=1
@@ -293,6 +298,26 @@ static int dalloc(sdn_handle* h, T** p, size_t count) {
   if (e != cudaSuccess) return fail(SDN_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   h->allocs.push_back(q);
   *p = reinterpret_cast<T*>(q);
+  return SDN_OK;
+}
+
+// grow-only scratch slot (stream-ordered reuse: callers are serialised on the
+// handle's stream; a grown buffer is freed after a stream sync)
+enum ScratchSlot { SCR_A = 0, SCR_B, SCR_C, SCR_D, SCR_E, SCR_F };
+template <class T>
+static int scratch(sdn_handle* h, int slot, size_t count, T** p) {
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  if (bytes > h->scr_bytes[slot]) {
+    if (h->scr[slot]) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(h->scr[slot]);
+      h->scr[slot] = nullptr;
+      h->scr_bytes[slot] = 0;
+    }
+    if (cudaMalloc(&h->scr[slot], bytes) != cudaSuccess) return fail(SDN_ERR_NOMEM, "scratch allocation failed");
+    h->scr_bytes[slot] = bytes;
+  }
+  *p = reinterpret_cast<T*>(h->scr[slot]);
   return SDN_OK;
 }
 
@@ -771,6 +796,8 @@ int sdn_destroy(sdn_handle* h) {
   for (cudaEvent_t e : h->tl)
     if (e) cudaEventDestroy(e);
   for (void* p : h->allocs) cudaFree(p);
+  for (void* p : h->scr)
+    if (p) cudaFree(p);
   if (h->U) cudaFree(h->U);
   if (h->ub) cudaFree(h->ub);
   if (h->Kg) cudaFree(h->Kg);
@@ -1951,9 +1978,9 @@ int sdn_forward_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n
   CU(cudaSetDevice(h->device));
   const int64_t chunk = h->cap;
   float *mr = nullptr, *zz = nullptr, *X = nullptr;
-  CU(cudaMalloc(&mr, sizeof(float) * chunk * h->r_m + 16));
-  CU(cudaMalloc(&zz, sizeof(float) * chunk * h->d_z + 16));
-  CU(cudaMalloc(&X, sizeof(float) * chunk * h->ldx + 16));
+  TRY(scratch(h, SCR_A, (size_t)chunk * h->r_m, &mr));
+  TRY(scratch(h, SCR_B, (size_t)chunk * h->d_z, &zz));
+  TRY(scratch(h, SCR_C, (size_t)chunk * h->ldx, &X));
   int rc = SDN_OK;
   for (int64_t s = 0; s < n && rc == SDN_OK; s += chunk) {
     const int64_t m = std::min(chunk, n - s);
@@ -1969,9 +1996,6 @@ int sdn_forward_batch(sdn_handle* h, const float* m_r, const float* z, int64_t n
       rc = fail(SDN_ERR_CUDA, "download failed");
   }
   cudaStreamSynchronize(h->stream);
-  cudaFree(mr);
-  cudaFree(zz);
-  cudaFree(X);
   return rc;
 }
 
@@ -2176,8 +2200,10 @@ int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubi
   if (!h->cdec) CU(cudaMalloc(&h->cdec, sizeof(float) * r_u));
   if (!h->KPhi) CU(cudaMalloc(&h->KPhi, sizeof(float) * h->cap * r_u));
   if (!h->c64dec) CU(cudaMalloc(&h->c64dec, sizeof(double) * r_u));
+  const int64_t d16 = (d_u + 15) / 16 * 16;
   CU(cudaMalloc(&h->U, sizeof(float) * d_u * r_u));
-  CU(cudaMalloc(&h->ub, sizeof(float) * d_u));
+  CU(cudaMalloc(&h->ub, sizeof(float) * d16));      // zero-padded to the tensor-core operand's rows
+  CU(cudaMemsetAsync(h->ub, 0, sizeof(float) * d16, h->stream));
   float *Um = nullptr, *Md = nullptr, *ut = nullptr;
   double *K64 = nullptr, *q0d = nullptr;
   auto cleanup = [&]() { cudaFree(Um); cudaFree(Md); cudaFree(ut); cudaFree(q0d); };
@@ -2218,7 +2244,6 @@ int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubi
   // the decoder basis as a tensor-core operand (rows padded to 16) for the
   // decoded Jacobian GEMM
   if (rc == SDN_OK && h->tcw.enabled) {
-    const int64_t d16 = (d_u + 15) / 16 * 16;
     if (!h->usplit.hi || h->usplit.rows < d16) {
       if (tc_buf(h, h->tcw, h->usplit, d16, r_u)) rc = fail(SDN_ERR_NOMEM, "decoder operand allocation failed");
     }
@@ -2247,26 +2272,42 @@ int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubi
 int sdn_lift(sdn_handle* h, const float* phi, int64_t n, float* u) {
   if (!h || !phi || !u) return fail(SDN_ERR_ARG, "null argument");
   if (!h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
+  if (n < 0) return fail(SDN_ERR_ARG, "negative row count");
   CU(cudaSetDevice(h->device));
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(512ll << 20) / (4 * h->d_u)));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(512ll << 20) / (4 * h->d_u)));
   float *p = nullptr, *o = nullptr;
-  CU(cudaMalloc(&p, sizeof(float) * chunk * h->r_u + 16));
-  CU(cudaMalloc(&o, sizeof(float) * chunk * h->d_u + 16));
-  int rc = SDN_OK;
-  for (int64_t s = 0; s < n && rc == SDN_OK; s += chunk) {
-    const int64_t m = std::min(chunk, n - s);
-    cudaMemcpyAsync(p, phi + s * h->r_u, sizeof(float) * m * h->r_u, cudaMemcpyHostToDevice, h->stream);
-    rc = gemm<false, true>(h, m, nullptr, (int)h->d_u, h->r_u, p, h->r_u, h->U, h->r_u,
-                           EpiAffine{h->ub, nullptr, nullptr, o, h->d_u});
-    if (rc == SDN_OK && (cudaMemcpyAsync(u + s * h->d_u, o, sizeof(float) * m * h->d_u, cudaMemcpyDeviceToHost,
-                                         h->stream) ||
-                         cudaStreamSynchronize(h->stream)))
-      rc = fail(SDN_ERR_CUDA, "download failed");
+  const int64_t ldo = std::max<int64_t>(h->d_u16, h->d_u);   // padded rows on the tensor-core path
+  TRY(scratch(h, SCR_D, (size_t)chunk * h->r_u, &p));
+  TRY(scratch(h, SCR_E, (size_t)chunk * ldo, &o));
+  // tensor cores when the decoder operand exists and the chunk fills the GPU
+  const bool tc = h->tcw.enabled && h->usplit.hi && h->gemm != SDN_GEMM_SIMT && chunk >= 128ll * h->num_sms / 4;
+  if (tc && (!h->lift_in.hi || h->lift_in.rows < chunk)) {
+    if (tc_buf(h, h->tcw, h->lift_in, chunk, h->r_u)) return fail(SDN_ERR_NOMEM, "lift operand allocation failed");
   }
-  cudaStreamSynchronize(h->stream);
-  cudaFree(p);
-  cudaFree(o);
-  return rc;
+  for (int64_t s = 0; s < n; s += chunk) {
+    const int64_t m = std::min(chunk, n - s);
+    CU(cudaMemcpyAsync(p, phi + s * h->r_u, sizeof(float) * m * h->r_u, cudaMemcpyHostToDevice, h->stream));
+    if (tc) {
+      // u = U phi + b (pod.py:36-40): phi split, then one tcgen05 GEMM against the split U
+      k_split<<<(unsigned)std::min<int64_t>(cdiv(m * h->r_u, 256), 4096), 256, 0, h->stream>>>(
+          m, nullptr, h->r_u, h->r_u, p, h->r_u, h->lift_in.hi, h->lift_in.lo);
+      h->launches++;
+      ProfScope ps(h, PC_DECODE, 2.0 * m * h->d_u * h->r_u, 4.0 * m * h->d_u);
+      // (TMA-store epilogue into rows padded to d_u16; the padding is dropped by the 2-D copy out)
+      const int rc = tc_gemm(h->tcw, h->stream, h->sm_avail, m, nullptr, (int)h->d_u16, h->r_u, h->lift_in,
+                             h->usplit, EpiAffine{h->ub, nullptr, nullptr, o, ldo}, m);
+      h->launches++;
+      if (rc) return fail(SDN_ERR_CUDA, "lift GEMM launch failed (" + std::to_string(rc) + ")");
+      CHECK_LAUNCH(h);
+    } else {
+      TRY((gemm<false, true>(h, m, nullptr, (int)h->d_u, h->r_u, p, h->r_u, h->U, h->r_u,
+                             EpiAffine{h->ub, nullptr, nullptr, o, ldo})));
+    }
+    CU(cudaMemcpy2DAsync(u + s * h->d_u, sizeof(float) * h->d_u, o, sizeof(float) * ldo, sizeof(float) * h->d_u, m,
+                         cudaMemcpyDeviceToHost, h->stream));
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  return SDN_OK;
 }
 
 // encoder K1: m_r = (m - mean) diag(M) V_m, split-K in fp64 (randfield.py:67-72)
@@ -2276,55 +2317,47 @@ int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, con
   if (n > h->cap) return fail(SDN_ERR_ARG, "sample count exceeds the handle capacity");
   CU(cudaSetDevice(h->device));
   const int r_m = h->r_m;
-  std::vector<float> vmm((size_t)d_m * r_m);
-  std::vector<double> bias(r_m, 0.0);
-  for (int64_t d = 0; d < d_m; ++d)
-    for (int j = 0; j < r_m; ++j) {
-      const double v = (double)Mdiag[d] * (double)Vm[d * r_m + j];
-      vmm[(size_t)d * r_m + j] = (float)v;
-      bias[j] -= (double)m_mean * v;
-    }
-  float *V = nullptr, *mb = nullptr;
+  // everything on the device: Vmm = diag(M) V_m (fp32 of the fp64 product),
+  // bias_j = -m_mean sum_d Vmm[d, j] (fixed-order fp64), the split-K product
+  // accumulated in fp64, then MR = float(acc + bias).  (The products stay on
+  // the FMA pipe in fp32: the input whitening 1/sqrt(lambda_j) amplifies the
+  // encoder's error by up to ~6500x at c4's highest mode, which a bf16x3
+  // product error of ~2^-16 cannot absorb -- DESIGN.md section 3.)
+  const int64_t rows_chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1ll << 30) / (4 * d_m)));
+  float *V = nullptr, *Vraw = nullptr, *Md = nullptr, *mb = nullptr;
   double *acc = nullptr, *bd = nullptr;
-  int rc = SDN_OK;
-  const int64_t rows_chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(1ll << 30) / (4 * d_m)));
-  CU(cudaMalloc(&V, sizeof(float) * vmm.size()));
-  CU(cudaMalloc(&acc, sizeof(double) * std::max<int64_t>(n, 1) * r_m));
-  CU(cudaMalloc(&bd, sizeof(double) * r_m));
-  if (!on_device) CU(cudaMalloc(&mb, sizeof(float) * rows_chunk * d_m));
-  CU(cudaMemcpy(V, vmm.data(), sizeof(float) * vmm.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(bd, bias.data(), sizeof(double) * r_m, cudaMemcpyHostToDevice));
+  TRY(scratch(h, SCR_A, (size_t)d_m * r_m, &V));
+  TRY(scratch(h, SCR_B, (size_t)d_m * r_m, &Vraw));
+  TRY(scratch(h, SCR_C, (size_t)d_m, &Md));
+  TRY(scratch(h, SCR_D, (size_t)std::max<int64_t>(n, 1) * r_m, &acc));
+  TRY(scratch(h, SCR_E, (size_t)r_m, &bd));
+  if (!on_device) TRY(scratch(h, SCR_F, (size_t)rows_chunk * d_m, &mb));
+  CU(cudaMemcpyAsync(Vraw, Vm, sizeof(float) * d_m * r_m, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Md, Mdiag, sizeof(float) * d_m, cudaMemcpyHostToDevice, h->stream));
+  k_dec_scale<<<(unsigned)std::min<int64_t>(cdiv(d_m * r_m, 256), 4096), 256, 0, h->stream>>>(d_m, r_m, Vraw, Md, V);
+  k_enc_bias<<<(unsigned)r_m, 256, 0, h->stream>>>(d_m, r_m, V, (double)m_mean, bd);
+  h->launches += 2;
   CU(cudaMemsetAsync(acc, 0, sizeof(double) * std::max<int64_t>(n, 1) * r_m, h->stream));
   const int64_t kc = 1024;
-  for (int64_t s = 0; s < n && rc == SDN_OK; s += rows_chunk) {
+  for (int64_t s = 0; s < n; s += rows_chunk) {
     const int64_t rows = std::min(rows_chunk, n - s);
     const float* src = m + s * d_m;
     if (!on_device) {
-      cudaMemcpyAsync(mb, src, sizeof(float) * rows * d_m, cudaMemcpyHostToDevice, h->stream);
+      CU(cudaMemcpyAsync(mb, src, sizeof(float) * rows * d_m, cudaMemcpyHostToDevice, h->stream));
       src = mb;
     }
-    for (int64_t k0 = 0; k0 < d_m && rc == SDN_OK; k0 += kc) {
+    ProfScope ps(h, PC_OTHER, 2.0 * rows * r_m * d_m, 4.0 * rows * d_m);
+    for (int64_t k0 = 0; k0 < d_m; k0 += kc) {
       const int kl = (int)std::min(kc, d_m - k0);
-      rc = gemm<false, false>(h, rows, nullptr, r_m, kl, src + k0, d_m, V + k0 * r_m, r_m,
-                              EpiAccum64{acc + s * r_m, (int64_t)r_m});
+      TRY((gemm<false, false>(h, rows, nullptr, r_m, kl, src + k0, d_m, V + k0 * r_m, r_m,
+                              EpiAccum64{acc + s * r_m, (int64_t)r_m})));
     }
   }
-  if (rc == SDN_OK && n > 0) {
-    // MR = (float)(acc + bias)
-    std::vector<double> hacc((size_t)n * r_m);
-    cudaStreamSynchronize(h->stream);
-    cudaMemcpy(hacc.data(), acc, sizeof(double) * hacc.size(), cudaMemcpyDeviceToHost);
-    std::vector<float> mr((size_t)n * r_m);
-    for (int64_t i = 0; i < n; ++i)
-      for (int j = 0; j < r_m; ++j) mr[(size_t)i * r_m + j] = (float)(hacc[(size_t)i * r_m + j] + bias[j]);
-    cudaMemcpy(h->MR, mr.data(), sizeof(float) * mr.size(), cudaMemcpyHostToDevice);
+  if (n > 0) {
+    k_enc_finish<<<(unsigned)std::min<int64_t>(cdiv(n * r_m, 256), 4096), 256, 0, h->stream>>>(n, r_m, acc, bd, h->MR);
+    h->launches++;
   }
-  cudaStreamSynchronize(h->stream);
-  cudaFree(V);
-  cudaFree(acc);
-  cudaFree(bd);
-  if (mb) cudaFree(mb);
-  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
   CU(cudaGetLastError());
   h->n = n;
   h->goff = global_offset;
@@ -2343,15 +2376,15 @@ int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k, i
   uint8_t* mask = nullptr;
   int *cnt = nullptr, *offs = nullptr, *na = nullptr, *ri = nullptr;
   const int nb = (int)cdiv(n, 1024);
-  CU(cudaMalloc(&v, sizeof(double) * n));
-  CU(cudaMalloc(&mask, n));
-  CU(cudaMalloc(&cnt, sizeof(int) * nb));
-  CU(cudaMalloc(&offs, sizeof(int) * nb));
-  CU(cudaMalloc(&na, sizeof(int)));
-  CU(cudaMalloc(&ri, sizeof(int) * k));
+  TRY(scratch(h, SCR_A, (size_t)n, &v));
+  TRY(scratch(h, SCR_B, (size_t)n, &mask));
+  TRY(scratch(h, SCR_C, (size_t)2 * nb + 1, &cnt));
+  TRY(scratch(h, SCR_D, (size_t)k, &ri));
+  offs = cnt + nb;
+  na = cnt + 2 * nb;
   CU(cudaMemcpyAsync(v, values, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                      h->stream));
-  if (int rc = launch_topk(h, n, k, v, nullptr, mask)) { cudaFree(v); cudaFree(mask); return rc; }
+  TRY(launch_topk(h, n, k, v, nullptr, mask));
   k_flag_count<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, nullptr, cnt);
   k_scan_counts<<<1, 32, 0, h->stream>>>(nb, cnt, offs, na);
   k_compact<<<nb, 1024, 0, h->stream>>>(n, RISK_CVAR_EXACT, v, mask, 0.0, 1.0, nullptr, offs, ri);
@@ -2359,7 +2392,6 @@ int sdn_select_topk(sdn_handle* h, const double* values, int64_t n, int64_t k, i
   std::vector<int> hi(k);
   cudaError_t e = cudaMemcpyAsync(hi.data(), ri, sizeof(int) * k, cudaMemcpyDeviceToHost, h->stream);
   cudaError_t e2 = cudaStreamSynchronize(h->stream);
-  cudaFree(v); cudaFree(mask); cudaFree(cnt); cudaFree(offs); cudaFree(na); cudaFree(ri);
   if (e != cudaSuccess || e2 != cudaSuccess) return fail(SDN_ERR_CUDA, "top-k failed");
   for (int64_t i = 0; i < k; ++i) idx[i] = hi[i];
   return SDN_OK;

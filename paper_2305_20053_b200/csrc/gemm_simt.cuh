@@ -180,6 +180,21 @@ struct EpiAccum64 {
   SDN_DEV void col(int64_t r, int c, float v) const { C[r * ldc + c] += v; }
 };
 
+// C = acc + bias with a column bound (GEMMs whose N is padded past the real
+// width, e.g. the decoder operand's rows padded to 16): columns >= nvalid dropped
+struct EpiAffineN {
+  const float* bias; float* C; int64_t ldc; int64_t nvalid;
+  SDN_DEV void operator()(int64_t r, int c, float4 v) const {
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (c + j < nvalid) C[r * ldc + c + j] = x[j] + (bias ? bias[c + j] : 0.0f);
+  }
+  SDN_DEV void col(int64_t r, int c, float v) const {
+    if (c < nvalid) C[r * ldc + c] = v + (bias ? bias[c] : 0.0f);
+  }
+};
+
 // store with bias add and an optional per-column scale/shift:
 // C = shift + scale * (acc + bias)   (scale/shift may be null)
 struct EpiAffine {

@@ -839,6 +839,28 @@ k_dec_c(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restri
     else *q0 = t;
   }
 }
+// encoder: bias_j = -m_mean sum_d Vmm[d, j] (fixed-order fp64, one block per j)
+__global__ void __launch_bounds__(256)
+k_enc_bias(int64_t d_m, int r_m, const float* __restrict__ Vmm, double m_mean, double* __restrict__ bias) {
+  __shared__ double sw[8];
+  const int j = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t d = threadIdx.x; d < d_m; d += blockDim.x) acc += (double)Vmm[d * r_m + j];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sw[w];
+    bias[j] = -m_mean * t;
+  }
+}
+// MR = float(acc + bias)
+__global__ void k_enc_finish(int64_t n, int r_m, const double* __restrict__ acc, const double* __restrict__ bias,
+                             float* __restrict__ MR) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * r_m; e += (int64_t)gridDim.x * blockDim.x)
+    MR[e] = (float)(acc[e] + bias[e % r_m]);
+}
 __global__ void k_f64_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     b[e] = (float)a[e];
