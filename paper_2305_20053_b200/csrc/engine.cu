@@ -26,7 +26,7 @@
 // persistent sweep GEMMs run (sdn_eval_multi).  Balances the two paths of the
 // c2 step; re-measured after each change to either path (latest, with the
 // depth-3 reverse ring: 0.370 ms at 24-28, 0.358-0.367 at 32-44).
-constexpr int SDN_SIDE_SMS_DEFAULT = 36;
+constexpr int SDN_SIDE_SMS_DEFAULT = 16;   // the exact-CVaR selections are off the critical path (deferred sums)
 
 #include <algorithm>
 #include <cmath>
@@ -202,6 +202,7 @@ struct sdn_handle {
   double* vsum = nullptr;       // 2 SDN_RMAX: per-risk sum_{w != 0} Q, count
   int* red_counter = nullptr;   // last-block reduction counters (k_qoi, k_weights), self re-arming
   int* fwdflags = nullptr;      // forward chain row-block readiness (L x fwd_mtiles)
+  int* bwdflags = nullptr;      // reverse chain row-block readiness (L x fwd_mtiles)
   int fwd_mtiles = 0;
   unsigned* ref_bar = nullptr;  // k_refine grid barrier
   int ref_grid = 0;
@@ -577,6 +578,7 @@ struct SweepSum {
   int R = 1;
   int64_t plane = 0;
   std::function<int()> before_last;
+  float* U0 = nullptr;          // store u = dL/dS_0 too (deferred exact-CVaR sums)
 };
 
 // reverse sweep over `nmax` (device count n_act_dev) compacted rows from the
@@ -596,7 +598,48 @@ static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const
   const bool tcc = chain_tc(h, rows_hint >= 0 ? rows_hint : nmax);
   const int route = tcc ? 1 : 0;
   int cur = 0;
-  for (int l = L - 1; l >= 1; --l) {
+  int l_top = L - 1;
+  // persistent reverse chain: the dense sweep's steps l = L-1 .. 2 (equal
+  // widths) in one launch; the summing step (l = 1) follows as its own GEMM
+  {
+    const int NW = h->w[1];
+    bool ok = tcc && g_bwd_chain && ss && !want_u0 && !rowidx && !n_act_dev && L >= 4 && L - 2 <= SDN_CHAIN_MAX &&
+              h->act != ACT_SOFTMAX && NW % 16 == 0 && NW > 128 && nmax <= h->cap;
+    for (int l = 1; l < L && ok; ++l) ok = h->w[l] == NW;
+    if (ok) {
+      std::vector<BwdChainLayerHost> ls;
+      CU(cudaMemsetAsync(h->bwdflags, 0, sizeof(int) * (size_t)L * h->fwd_mtiles, h->stream));
+      double fl_sum = 0.0;
+      int c = 0, step = 0;
+      for (int l = L - 1; l >= 2; --l, ++step) {
+        BwdChainLayerHost x{};
+        x.A = (l == L - 1) ? &h->sw->seed : &h->sw->act[c];
+        x.B = &h->tcw.bwd[l];
+        x.S = &h->sw->act[1 - c];
+        x.R = (l < L - 1 && h->res[l]) ? h->sw->G : nullptr;
+        x.G = h->res[l - 1] ? h->sw->G : nullptr;
+        x.D = h->D[l - 1];
+        x.ldD = NW;
+        x.K = h->w[l + 1];
+        x.fl.in = step > 0 ? h->bwdflags + (size_t)(step - 1) * h->fwd_mtiles : nullptr;
+        x.fl.out = h->bwdflags + (size_t)step * h->fwd_mtiles;
+        fl_sum += 2.0 * nmax * NW * x.K;
+        ls.push_back(x);
+        c = 1 - c;
+      }
+      ProfScope ps(h, PC_BWD_GEMM, fl_sum, 0.0);
+      g_tc_pdl_now = h->sm_avail == h->num_sms;
+      const int64_t tiles = cdiv(nmax, 128) * cdiv(NW, 256) * (int64_t)ls.size();
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, h->sm_avail));
+      const int rc = tc_bwd_chain(h->tcw, h->stream, grid, nmax, NW, ls);
+      h->launches++;
+      if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 reverse chain launch failed (" + std::to_string(rc) + ")");
+      CHECK_LAUNCH(h);
+      cur = c;
+      l_top = 1;
+    }
+  }
+  for (int l = l_top; l >= 1; --l) {
     // GEMM l: g_{l-1} = (res[l] ? g_l : 0) + u_l W_l, u_{l-1} = D_{l-1} g_{l-1}
     const int K = h->w[l + 1], N = h->w[l];
     const float* A = (l == L - 1) ? h->sw->E : h->sw->Ub[cur];
@@ -608,7 +651,7 @@ static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const
     h->prows = rows_hint;
     if (l == 1 && tcc && !want_u0) {
       EpiBwdSum e{resid, h->D[0], (int64_t)N, rowidx, (int64_t)N, h->sw->tsum, (int64_t)N};
-      if (ss) { e.W = ss->W; e.R = ss->R; e.plane = ss->plane; }
+      if (ss) { e.W = ss->W; e.R = ss->R; e.plane = ss->plane; e.U0 = ss->U0; }
       TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, e, tB, tA, route)));
       *u0_out = nullptr;
       if (nrb) *nrb = cdiv(nmax, 128) * 4;
@@ -749,6 +792,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->red_counter, 4))) return bail(rc);
   h->fwd_mtiles = 2 * (int)cdiv(cap, 256);        // 128-row blocks, whole 256-row pair tiles
   if ((rc = dalloc(h, &h->fwdflags, (size_t)h->L * h->fwd_mtiles))) return bail(rc);
+  if ((rc = dalloc(h, &h->bwdflags, (size_t)h->L * h->fwd_mtiles))) return bail(rc);
   if (cudaMemset(h->red_counter, 0, 4 * sizeof(int)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
   if ((rc = dalloc(h, &h->ref_bar, 2))) return bail(rc);
   if (cudaMemset(h->ref_bar, 0, 2 * sizeof(unsigned)) != cudaSuccess) return bail(fail(SDN_ERR_CUDA, "memset"));
@@ -1203,7 +1247,8 @@ static int ensure_sweep(sdn_handle* h, SweepBufs& b, int R) {
 // right before the last GEMM, so the selections overlap the sweep.
 static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uint8_t* const* masks,
                           const int64_t* ks, const double* stats_dev, double* partials,
-                          const std::function<int()>& join = {}, const double* tdev = nullptr) {
+                          const std::function<int()>& join = {}, const double* tdev = nullptr,
+                          const int* const* sel_rows = nullptr) {
   if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
   if (R < 1 || R > SDN_RMAX) return fail(SDN_ERR_ARG, "1..8 risks per sweep");
   RiskSet rs{};
@@ -1251,9 +1296,20 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   if (nmax > sw.rows) return fail(SDN_ERR_STATE, "sweep buffers too small");
   // weights + value partials (the first read of the masks and of Q)
   const int wg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(nmax, 1), 256), h->qgrid));
+  // deferred exact CVaR (dense sweep overlapped with the selections): the
+  // last reverse GEMM runs without waiting for them -- dense risks' weights
+  // are known after the forward moments -- and also stores u = dL/dS_0; once
+  // the selections join, each exact risk's sums are taken over its k selected
+  // rows of u (k_sel_colsum).  The masks are then never on the sweep's path.
+  const bool defer = join && dense && sel_rows && !rowidx && h->n > 0 &&
+                     chain_tc(h, nmax) && h->sw == &h->sw0 && h->L >= 2;
+  RiskSet rs_w = rs;
+  if (defer)
+    for (int r = 0; r < R; ++r)
+      if (rs.kind[r] == SDN_RISK_CVAR_EXACT) rs_w.mask[r] = nullptr;
   auto weights = [&]() -> int {
     ProfScope ps(h, PC_SEED, 0.0, 0.0, rows_hint, 8.0 * (1 + R));
-    k_weights<<<wg, 256, 0, h->stream>>>(nmax, nact, rowidx, rs, h->Q, stats_dev, h->shift, sw.W, h->wpart,
+    k_weights<<<wg, 256, 0, h->stream>>>(nmax, nact, rowidx, rs_w, h->Q, stats_dev, h->shift, sw.W, h->wpart,
                                          h->red_counter + 1, h->vsum);
     h->launches += 1;
     CHECK_LAUNCH(h);
@@ -1286,12 +1342,13 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   ssum.plane = tplane;
   ssum.before_last = [&]() -> int {
     tl_mark(h, 6);
-    if (dense && join) TRY(join());
+    if (dense && join && !defer) TRY(join());
     tl_mark(h, 7);
     const int rc = weights();
     tl_mark(h, 8);
     return rc;
   };
+  if (defer) ssum.U0 = sw.Ub[0];
   float* u0 = nullptr;
   int64_t nrb = 0;
   TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint, false, &nrb, &ssum));
@@ -1316,6 +1373,18 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   }
   h->launches++;
   CHECK_LAUNCH(h);
+  if (defer) {
+    TRY(join());
+    for (int r = 0; r < R; ++r) {
+      if (rs.kind[r] != SDN_RISK_CVAR_EXACT) continue;
+      ProfScope ps(h, PC_COLSUM, 0.0, 4.0 * ks[r] * h->h1);
+      k_sel_colsum<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>(
+          ks[r], sel_rows[r], h->h1, sw.Ub[0], h->h1, rs.kinv[r], h->Q, sw.csum + (int64_t)r * h->h1,
+          h->vsum + 2 * r);
+      h->launches++;
+      CHECK_LAUNCH(h);
+    }
+  }
   { ProfScope ps(h, PC_FINAL, 0.0, 8.0 * nrb_fin * h->h1 * R);
   k_finalize_multi<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(
       nrb_fin, plane, h->h1, h->d_z, part, h->PzT, h->vsum, h->plen(), partials); }
@@ -1486,12 +1555,14 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad, risks, n_risks,
                    smooth >= 0 ? smooth : 0, dense && any_grad));
   std::vector<const uint8_t*> masks(n_risks, nullptr);
+  std::vector<const int*> sel_rows(n_risks, nullptr);
   auto select_all = [&]() -> int {
     for (int i = 0, e = 0; i < n_risks; ++i) {
       if (risks[i].kind != SDN_RISK_CVAR_EXACT) continue;
       h->risk = risks[i];
       TRY(select_local(h, kks[i], h->band_log + 1 + i, h->x_mask[e], h->x_rowidx[e], h->x_nact[e]));
       masks[i] = h->x_mask[e];
+      sel_rows[i] = h->x_rowidx[e];
       if (want_idx)
         CU(cudaMemcpyAsync(h->hidx + koff[i], h->x_rowidx[e], sizeof(int) * kks[i], cudaMemcpyDeviceToHost,
                            h->stream));
@@ -1529,7 +1600,7 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   }
   h->risk = risks[0];
   int rc = backward_multi(h, risks, n_risks, masks.data(), kks.data(), h->stats_loc, h->partial_multi, join,
-                          h->zdev + h->d_z);
+                          h->zdev + h->d_z, sel_rows.data());
   h->sm_avail = h->num_sms;
   if (rc) return rc;
   {                                   // results -> host-mapped memory (one kernel, no copy nodes)

@@ -986,6 +986,9 @@ struct EpiBwdSum {
   // unified sweep: per-row risk weights W[row * R + r] (sweep rows), one
   // partial plane per risk (plane stride); W null = unit weights, R = 1
   const double* W = nullptr; int R = 1; int64_t plane = 0;
+  // optional: u = D g itself stored (fp32, ld) through TMA by the ring
+  // epilogue, for sums whose row weights are known only later (exact CVaR)
+  float* U0 = nullptr;
   SDN_DEV void operator()(int64_t, int, float4) const {}
   SDN_DEV void col(int64_t, int, float) const {}
 };
@@ -1018,6 +1021,10 @@ struct TileEpi<EpiBwdSum> {
     for (int j = 0; j < 16; ++j) dd[j] = live ? dd[j] * g[j] : 0.0f;
     __syncwarp();
     row_put(s.f1, lane, dd);
+    if (e.U0) {                                   // u itself for deferred sums (coalesced thread stores)
+      __syncwarp();
+      tile_out(s.f1, e.U0, e.ld, tr, c0, N, lane);
+    }
     // unified sweep: each lane stages its row's risk weights (fp64) in the
     // residual staging buffer, free at this point
     double* ws = reinterpret_cast<double*>(s.f0);
@@ -1343,10 +1350,25 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
             e.part[qq * e.plane + prow * e.ldp + col + j] = a;
           }
         }
-        // this slot's generic reads before the async refill of the previous one
-        tcx::fence_proxy_async();
-        __syncwarp();
-        issue();
+        if (e.U0) {
+          // u itself for the deferred (exact-CVaR) sums: TMA-stored from the
+          // staging tile; the refill below targets the previous chunk's slot,
+          // whose u store must have read it first
+          if (lane == 0) tcx::bulk_wait_read0();
+          __syncwarp();
+          issue();
+          tcx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tcx::tma_store_2d(&om.m[1], Ds, col, (int)r0);
+            tcx::bulk_commit();
+          }
+        } else {
+          // this slot's generic reads before the async refill of the previous one
+          tcx::fence_proxy_async();
+          __syncwarp();
+          issue();
+        }
       } else {
         const TcChain<EpiBwd>& ch = ep;
         const bool has_G = ch.base.G != nullptr, has_split = ch.split.hi != nullptr;
@@ -1371,7 +1393,7 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
     }
     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
   }
-  if (!SUM && lane == 0) tcx::bulk_wait0();
+  if (lane == 0) tcx::bulk_wait0();
 }
 
 template <class Epi>
@@ -1640,6 +1662,86 @@ struct FwdChainArgs {
   CUtensorMap pmap[SDN_CHAIN_MAX];                         // residual input (split of the layer input)
 };
 
+// the chain kernels' producer (TMA) and MMA-issuer loops over the global
+// tile list (identical for the forward and the reverse chain; Args holds the
+// per-layer operand maps a[l], b[l], K and input flags fin)
+template <int BN, int CG, int STAGES, class C, class Args>
+SDN_DEV void chain_produce(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* empty, int rank, int t0, int ts,
+                           int tpl, int total, int n_tiles) {
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
+    const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+    const int mb = mbt * CG + rank;          // this CTA's 128-row block
+    const auto& ly = ca.ly[l];
+    chain_stamp(ti, 0);
+    if (ly.fin) {                            // input rows of this layer written and visible
+      while (tcx::ld_acquire(ly.fin + mb) < TC_BM * ly.K) __nanosleep(64);
+      tcx::fence_proxy_async_global();
+    }
+    chain_stamp(ti, 1);
+    const int kblocks = (ly.K + TC_BK - 1) / TC_BK;
+    for (int kb = 0; kb < kblocks; ++kb) {
+      tcx::mbar_wait(&empty[stage], phase ^ 1);
+      uint8_t* st = smem + stage * C::STAGE_BYTES;
+      if constexpr (CG == 1) {
+        tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+        tcx::tma_load_3d(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
+        tcx::tma_load_3d(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN, 0);
+      } else {
+        if (rank == 0) tcx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+        tcx::tma_load_3d_pair(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
+        tcx::tma_load_3d_pair(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN + rank * (BN / 2), 0);
+      }
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+  }
+}
+template <int BN, int CG, int STAGES, class C, class Args>
+SDN_DEV void chain_mma(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* tfull,
+                       uint64_t* tempty, uint32_t tmem, int t0, int ts, int tpl, int total) {
+  constexpr int BMT = TC_BM * CG;
+  constexpr uint32_t idesc = tcx::idesc_bf16(BMT, BN);
+  int stage = 0, acc = 0;
+  uint32_t phase = 0, acc_phase = 0;
+  for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
+    const int l = g / tpl;
+    const int kblocks = (ca.ly[l].K + TC_BK - 1) / TC_BK;
+    tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+    tcx::fence_after();
+    chain_stamp(ti, 2);
+    const uint32_t d = tmem + acc * BN;
+    for (int kb = 0; kb < kblocks; ++kb) {
+      tcx::mbar_wait(&full[stage], phase);
+      tcx::fence_after();
+      const uint32_t base = tcx::smem_u32(smem + stage * C::STAGE_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < TC_BK / 16; ++kk) {
+        const uint64_t ah = tcx::sdesc_k64(base + kk * 32);
+        const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
+        const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
+        const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
+        if constexpr (CG == 1) {
+          tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
+          tcx::mma_bf16(d, ah, bl, idesc, 1);
+          tcx::mma_bf16(d, al, bh, idesc, 1);
+        } else {
+          tcx::mma_bf16_pair(d, ah, bh, idesc, (kb | kk) != 0);
+          tcx::mma_bf16_pair(d, ah, bl, idesc, 1);
+          tcx::mma_bf16_pair(d, al, bh, idesc, 1);
+        }
+      }
+      if constexpr (CG == 1) tcx::commit(&empty[stage]);
+      else tcx::commit_pair(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+    if constexpr (CG == 1) tcx::commit(&tfull[acc]);
+    else tcx::commit_pair(&tfull[acc]);
+    chain_stamp(ti, 3);
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+}
+
 // shared-memory plan of the chain kernel: STAGES mainloop stages, EW
 // epilogue warps with RING 2-KB slots + a 2-KB D tile each, every layer's bias
 template <int BN, int RING, int CG, int EW>
@@ -1708,78 +1810,9 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
   const int t0 = (int)blockIdx.x / CG, ts = (int)gridDim.x / CG;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
-        const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
-        const int mb = mbt * CG + rank;          // this CTA's 128-row block
-        const FwdChainLayer& ly = ca.ly[l];
-        chain_stamp(ti, 0);
-        if (ly.fin) {                            // input rows of this layer written and visible
-          while (tcx::ld_acquire(ly.fin + mb) < TC_BM * ly.K) __nanosleep(64);
-          tcx::fence_proxy_async_global();
-        }
-        chain_stamp(ti, 1);
-        const int kblocks = (ly.K + TC_BK - 1) / TC_BK;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          tcx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* st = smem + stage * C::STAGE_BYTES;
-          if constexpr (CG == 1) {
-            tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-            tcx::tma_load_3d(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
-            tcx::tma_load_3d(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN, 0);
-          } else {
-            if (rank == 0) tcx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-            tcx::tma_load_3d_pair(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
-            tcx::tma_load_3d_pair(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN + rank * (BN / 2), 0);
-          }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
+    if (lane == 0) chain_produce<BN, CG, STAGES, C>(ca, smem, full, empty, rank, t0, ts, tpl, total, n_tiles);
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = tcx::idesc_bf16(BMT, BN);
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
-        const int l = g / tpl;
-        const int kblocks = (ca.ly[l].K + TC_BK - 1) / TC_BK;
-        tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tcx::fence_after();
-        chain_stamp(ti, 2);
-        const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          tcx::mbar_wait(&full[stage], phase);
-          tcx::fence_after();
-          const uint32_t base = tcx::smem_u32(smem + stage * C::STAGE_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk) {
-            const uint64_t ah = tcx::sdesc_k64(base + kk * 32);
-            const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
-            const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
-            const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
-            if constexpr (CG == 1) {
-              tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
-              tcx::mma_bf16(d, ah, bl, idesc, 1);
-              tcx::mma_bf16(d, al, bh, idesc, 1);
-            } else {
-              tcx::mma_bf16_pair(d, ah, bh, idesc, (kb | kk) != 0);
-              tcx::mma_bf16_pair(d, ah, bl, idesc, 1);
-              tcx::mma_bf16_pair(d, al, bh, idesc, 1);
-            }
-          }
-          if constexpr (CG == 1) tcx::commit(&empty[stage]);
-          else tcx::commit_pair(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        if constexpr (CG == 1) tcx::commit(&tfull[acc]);
-        else tcx::commit_pair(&tfull[acc]);
-        chain_stamp(ti, 3);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
+    if (lane == 0 && rank == 0) chain_mma<BN, CG, STAGES, C>(ca, smem, full, empty, tfull, tempty, tmem, t0, ts, tpl, total);
   } else if (warp >= 4) {
     const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
     uint8_t* wb = epi_base + w * WB;
@@ -1873,6 +1906,190 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
       }
       if (warp == 4 && lane == 0) chain_stamp(ti, 5);
       ++ti;
+    }
+    if (lane == 0) tcx::bulk_wait0();
+  }
+  if constexpr (CG == 1) __syncthreads();
+  else tcx::cluster_sync();
+  if (warp == 2) {
+    tcx::fence_after();
+    if constexpr (CG == 1) tcx::tmem_dealloc(tmem, 2 * BN);
+    else tcx::tmem_dealloc_pair(tmem, 2 * BN);
+  }
+}
+
+// Persistent reverse chain: the dense sweep's chain steps (every reverse
+// GEMM but the last, summing one) in ONE launch, the forward chain's scheme
+// with the reverse ring epilogue: per chunk the residual gradient G and the
+// act' tile are TMA-loaded RING-1 chunks ahead into one 4-KB slot, g = acc
+// [+ G], u = D g, G written back in place (same rows, same columns: the tile
+// that reads a G element is the one that rewrites it) and u's split stored
+// as the next step's A operand.  Layer l-1 overwrites the split that layer l
+// read only on rows whose layer-l outputs are published (row-block flags).
+struct BwdChainLayer {
+  const int* fin;
+  int* fout;
+  int K, has_resid, has_G;
+};
+struct BwdChainArgs {
+  int L, N, n_tiles, m_tiles;
+  int64_t M;
+  BwdChainLayer ly[SDN_CHAIN_MAX];
+  CUtensorMap a[SDN_CHAIN_MAX], b[SDN_CHAIN_MAX];          // mainloop operands
+  CUtensorMap rmap[SDN_CHAIN_MAX], dmap[SDN_CHAIN_MAX];    // residual gradient, act' inputs
+  CUtensorMap gmap[SDN_CHAIN_MAX], smap[SDN_CHAIN_MAX];    // G and split(u) outputs
+};
+template <int BN, int RING, int CG, int EW>
+struct BwdChainCfg {
+  static_assert(EW % 4 == 0 && EW >= 4, "epilogue warps come in lane-quarter groups of four");
+  using C = TcCfg<BN, RING, true, CG>;
+  static constexpr uint32_t WB = (uint32_t)RING * 4096u;
+  static constexpr uint32_t EPI_BYTES = EW * WB;
+  static constexpr int FIT = (int)((TC_SMEM_MAX - EPI_BYTES - 1024 - TC_BAR_BYTES) / C::STAGE_BYTES);
+  static constexpr int STAGES = FIT > 4 ? 4 : FIT;
+  static constexpr uint32_t SMEM = STAGES * C::STAGE_BYTES + EPI_BYTES + 1024 + TC_BAR_BYTES;
+  static constexpr int THREADS = 32 * (4 + EW);
+};
+
+template <int BN, int RING, int CG, int EW>
+__global__ void __launch_bounds__(BwdChainCfg<BN, RING, CG, EW>::THREADS, 1)
+tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
+  using CC = BwdChainCfg<BN, RING, CG, EW>;
+  using C = typename CC::C;
+  constexpr int STAGES = CC::STAGES;
+  constexpr int CS = 16 * (EW / 4);
+  constexpr uint32_t WB = CC::WB;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tcx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* epi_base = smem + STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_base + CC::EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar_all = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar_all + RING * EW);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int rank = CG == 1 ? 0 : (int)tcx::cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int l = 0; l < ca.L; ++l) {
+      tcx::prefetch_tmap(&ca.a[l]);
+      tcx::prefetch_tmap(&ca.b[l]);
+    }
+    for (int s2 = 0; s2 < STAGES; ++s2) { tcx::mbar_init(&full[s2], 1); tcx::mbar_init(&empty[s2], 1); }
+    for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], CG * EW); }
+    for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar_all[i], 1);
+    tcx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    if constexpr (CG == 1) {
+      tcx::tmem_alloc(tmem_slot, 2 * BN);
+      tcx::tmem_relinquish();
+    } else {
+      tcx::tmem_alloc_pair(tmem_slot, 2 * BN);
+      tcx::tmem_relinquish_pair();
+    }
+  }
+  tcx::fence_before();
+  if constexpr (CG == 1) __syncthreads();
+  else tcx::cluster_sync();
+  tcx::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");      // the seeds' split (forward output layer)
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int n_tiles = ca.n_tiles, tpl = ca.m_tiles * n_tiles, total = ca.L * tpl, N = ca.N;
+  const int t0 = (int)blockIdx.x / CG, ts = (int)gridDim.x / CG;
+
+  if (warp == 0) {
+    if (lane == 0) chain_produce<BN, CG, STAGES, C>(ca, smem, full, empty, rank, t0, ts, tpl, total, n_tiles);
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) chain_mma<BN, CG, STAGES, C>(ca, smem, full, empty, tfull, tempty, tmem, t0, ts, tpl, total);
+  } else if (warp >= 4) {
+    const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
+    uint8_t* wb = epi_base + w * WB;
+    uint64_t* rbar = rbar_all + w * RING;
+    int acc = 0, jt = 0;
+    uint32_t acc_phase = 0, rphase = 0;
+    for (int g = t0; g < total; g += ts) {
+      const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+      const int mbl = mbt * CG + rank;
+      const BwdChainLayer& ly = ca.ly[l];
+      const bool has_resid = ly.has_resid, has_G = ly.has_G;
+      const int r0 = mbl * TC_BM + q * 32;
+      int nch = 0;
+      for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
+      if (lane == 0 && nch > 0 && ly.fin) {       // this step's inputs (G rows) published
+        while (tcx::ld_acquire(ly.fin + mbl) < TC_BM * ly.K) __nanosleep(64);
+        tcx::fence_proxy_async_global();
+      }
+      auto issue = [&](int ci) {
+        if (ci < nch && lane == 0) {
+          const int s2 = (jt + ci) % RING;
+          const int x = nb * BN + first_c + CS * ci;
+          tcx::mbar_expect_tx(&rbar[s2], has_resid ? 4096u : 2048u);
+          if (has_resid) tcx::tma_load_2d(wb + s2 * 4096, &ca.rmap[l], &rbar[s2], x, r0);
+          tcx::tma_load_2d(wb + s2 * 4096 + 2048, &ca.dmap[l], &rbar[s2], x, r0);
+        }
+      };
+      for (int k = 0; k < RING - 1; ++k) issue(k);
+      tcx::mbar_wait(&tfull[acc], acc_phase);
+      tcx::fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (nch == 0) {
+        tcx::fence_before();
+        __syncwarp();
+        if (lane == 0) tmem_release<CG>(&tempty[acc]);
+      }
+#pragma unroll 1
+      for (int ci = 0; ci < nch; ++ci) {
+        const int c0 = first_c + CS * ci, col = nb * BN + c0, s2 = (jt + ci) % RING;
+        float* Rs = reinterpret_cast<float*>(wb + s2 * 4096);
+        float* Ds = Rs + 512;
+        uint32_t v[16];
+        tcx::tmem_ld16(tbase + c0, v);
+        tcx::mbar_wait(&rbar[s2], (rphase >> s2) & 1u);
+        rphase ^= 1u << s2;
+        tcx::tmem_ld_wait();
+        if (ci == nch - 1) {
+          tcx::fence_before();
+          __syncwarp();
+          if (lane == 0) tmem_release<CG>(&tempty[acc]);
+        }
+        float gv[16], dd[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) gv[j] = __uint_as_float(v[j]);
+        if (has_resid) {
+          float r[16];
+          row_get(Rs, lane, r);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) gv[j] += r[j];
+        }
+        row_get(Ds, lane, dd);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dd[j] *= gv[j];
+        if (lane == 0) tcx::bulk_wait_read0();   // previous chunk's stores have read their slot
+        __syncwarp();
+        issue(ci + RING - 1);
+        if (has_G) row_put(Rs, lane, gv);
+        uint32_t* sh = reinterpret_cast<uint32_t*>(Ds);
+        row_put_split(sh, sh + 256, lane, dd);
+        tcx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if (has_G) tcx::tma_store_2d(&ca.gmap[l], Rs, col, r0);
+          tcx::tma_store_3d(&ca.smap[l], sh, col, r0, 0);      // hi, lo (+1 KB)
+          tcx::bulk_commit();
+        }
+      }
+      jt += nch;
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (ly.fout) {
+        __syncwarp();
+        if (lane == 0) {
+          tcx::bulk_wait0();
+          tcx::fence_proxy_async_global();
+          tcx::red_release_add(ly.fout + mbl, 32 * 16 * nch);
+        }
+      }
     }
     if (lane == 0) tcx::bulk_wait0();
   }
@@ -2046,6 +2263,7 @@ struct EpiOut<EpiBwdSum> {
     if (e.rowidx || !e.D) return 0;
     if (e.resid && tc_out_map(t, e.resid, false, M, N, e.ld, &om.m[4])) return 0;
     if (tc_out_map(t, e.D, false, M, N, e.ldD, &om.m[5])) return 0;
+    if (e.U0 && tc_out_map(t, e.U0, false, M, N, e.ld, &om.m[1])) return 0;
     return 2;
   }
 };
@@ -2299,6 +2517,79 @@ static int tc_fwd_chain(TcWeights& t, cudaStream_t st, int grid, int64_t M, int 
   }
   if (g_chain_ew == 16) return tc_fwd_chain_k<1, 16>(t, st, grid, M, N, act, ls);
   return tc_fwd_chain_k<1, 12>(t, st, grid, M, N, act, ls);
+}
+
+// persistent reverse chain launch (see tc_bwd_chain_kernel).  Step l reads
+// A[l] (the previous step's split of u), the residual gradient R[l] (may be
+// null) and act' D[l]; writes G[l] (may be null; in place of R) and split(u).
+struct BwdChainLayerHost {
+  const TcOperand* A;
+  const TcOperand* B;
+  const TcOperand* S;
+  const float* R;
+  float* G;
+  const float* D;
+  int64_t ldD;
+  int K;
+  TcFlags fl;
+};
+template <int CG>
+static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N,
+                          const std::vector<BwdChainLayerHost>& ls) {
+  constexpr int BN = 256, RING = 3, EW = 8;
+  using CC = BwdChainCfg<BN, RING, CG, EW>;
+  static_assert(CC::STAGES >= 2 && CC::SMEM <= TC_SMEM_MAX, "reverse chain shared memory budget");
+  grid = CG * std::max(1, grid / CG);
+  const int L = (int)ls.size();
+  if (L < 1 || L > SDN_CHAIN_MAX || N % 16) return -1;
+  BwdChainArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  ca.L = L; ca.N = N; ca.M = M;
+  ca.n_tiles = (N + BN - 1) / BN;
+  ca.m_tiles = (int)((M + TC_BM * CG - 1) / (TC_BM * CG));
+  for (int l = 0; l < L; ++l) {
+    const BwdChainLayerHost& x = ls[l];
+    BwdChainLayer& y = ca.ly[l];
+    if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l]) ||
+        tc_map(t, *x.B, N, x.K, BN / CG, &ca.b[l]))
+      return -2;
+    if (x.R && tc_out_map(t, x.R, false, M, N, N, &ca.rmap[l])) return -3;
+    if (tc_out_map(t, x.D, false, M, N, x.ldD, &ca.dmap[l])) return -3;
+    if (x.G && tc_out_map(t, x.G, false, M, N, N, &ca.gmap[l])) return -3;
+    if (tc_out_map_pair(t, x.S->hi, x.S->lo, M, N, x.S->ld, &ca.smap[l])) return -3;
+    y.K = x.K; y.fin = x.fl.in; y.fout = x.fl.out;
+    y.has_resid = x.R != nullptr; y.has_G = x.G != nullptr;
+  }
+  static unsigned attr_set = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set & (1u << (dev & 31)))) {
+    cudaFuncSetAttribute(tc_bwd_chain_kernel<BN, RING, CG, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)CC::SMEM);
+    attr_set |= 1u << (dev & 31);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CC::THREADS);
+  cfg.dynamicSmemBytes = CC::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (g_tc_pdl && g_tc_pdl_now) ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CG;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CG > 1 ? 2 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_chain_kernel<BN, RING, CG, EW>, ca);
+  return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -4;
+}
+static bool g_bwd_chain = !(getenv("SDN_NO_BWD_CHAIN") && getenv("SDN_NO_BWD_CHAIN")[0] == '1');
+static int tc_bwd_chain(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N,
+                        const std::vector<BwdChainLayerHost>& ls) {
+  if (g_chain_pairs && grid >= 2) return tc_bwd_chain_k<2>(t, st, grid, M, N, ls);
+  return tc_bwd_chain_k<1>(t, st, grid, M, N, ls);
 }
 
 // allocation / refresh of the split operands -------------------------------

@@ -309,7 +309,9 @@ struct RiskSet {
 SDN_DEV double risk_t(const RiskSet& rs, int r) { return rs.tdev ? rs.tdev[r] : rs.t[r]; }
 
 SDN_DEV double risk_weight(const RiskSet& rs, int r, int64_t i, double q, const double* st, double shift) {
-  if (rs.kind[r] == RISK_CVAR_EXACT) return rs.mask[r][i] ? rs.kinv[r] : 0.0;
+  // (an exact-CVaR risk without a mask is deferred: its sums are taken later
+  // over the selected rows' stored u, k_sel_colsum)
+  if (rs.kind[r] == RISK_CVAR_EXACT) return (rs.mask[r] && rs.mask[r][i]) ? rs.kinv[r] : 0.0;
   return sample_weight(rs.kind[r], q, st, shift, rs.beta[r], rs.eps[r], risk_t(rs, r), 0.0);
 }
 
@@ -448,6 +450,35 @@ k_finalize_multi(int nrb, int64_t plane, int h1, int d_z, const double* __restri
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     o[d_z] = vsum[2 * r];
     o[d_z + 1] = vsum[2 * r + 1];
+  }
+}
+
+// deferred exact-CVaR sums: out[c] = kinv * sum_{j < k} u[rows[j], c] (fp64,
+// fixed order: thread rows j = y, y + 32, ..., then the 32 row groups in
+// order) and the value partials vs = (sum_j Q[rows[j]], k)
+__global__ void __launch_bounds__(1024)
+k_sel_colsum(int64_t k, const int* __restrict__ rows, int w, const float* __restrict__ u, int64_t ld, double kinv,
+             const double* __restrict__ Q, double* __restrict__ out, double* __restrict__ vs) {
+  __shared__ double s[32][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  double acc = 0.0;
+  if (c < w)
+    for (int64_t j = threadIdx.y; j < k; j += 32) acc += (double)u[(int64_t)rows[j] * ld + c];
+  s[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < w) {
+    double t = 0.0;
+    for (int y = 0; y < 32; ++y) t += s[y][threadIdx.x];
+    out[c] = kinv * t;
+  }
+  if (blockIdx.x == 0 && threadIdx.y == 1) {       // one warp: lane-strided, fixed butterfly
+    double qs = 0.0;
+    for (int64_t j = threadIdx.x; j < k; j += 32) qs += Q[rows[j]];
+    qs = warp_sum(qs);
+    if (threadIdx.x == 0) {
+      vs[0] = qs;
+      vs[1] = (double)k;
+    }
   }
 }
 
