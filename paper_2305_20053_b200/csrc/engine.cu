@@ -579,6 +579,12 @@ struct SweepSum {
   int64_t plane = 0;
   std::function<int()> before_last;
   float* U0 = nullptr;          // store u = dL/dS_0 too (deferred exact-CVaR sums)
+  // weights computed in the last GEMM's epilogue (wfun) from Q and the moments
+  int wfun = 0;
+  RiskSet rs{};
+  const double* Q = nullptr;
+  const double* st = nullptr;
+  double shift = 0.0;
 };
 
 // reverse sweep over `nmax` (device count n_act_dev) compacted rows from the
@@ -651,7 +657,10 @@ static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const
     h->prows = rows_hint;
     if (l == 1 && tcc && !want_u0) {
       EpiBwdSum e{resid, h->D[0], (int64_t)N, rowidx, (int64_t)N, h->sw->tsum, (int64_t)N};
-      if (ss) { e.W = ss->W; e.R = ss->R; e.plane = ss->plane; e.U0 = ss->U0; }
+      if (ss) {
+        e.W = ss->W; e.R = ss->R; e.plane = ss->plane; e.U0 = ss->U0;
+        if (ss->wfun) { e.W = nullptr; e.wfun = 1; e.rs = ss->rs; e.Q = ss->Q; e.st = ss->st; e.shift = ss->shift; }
+      }
       TRY((gemm<false, false>(h, nmax, n_act_dev, N, K, A, K, h->W[l], N, e, tB, tA, route)));
       *u0_out = nullptr;
       if (nrb) *nrb = cdiv(nmax, 128) * 4;
@@ -790,6 +799,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->wpart, (size_t)h->qgrid * 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->vsum, 2 * SDN_RMAX))) return bail(rc);
   if ((rc = dalloc(h, &h->red_counter, 4))) return bail(rc);
+
   h->fwd_mtiles = 2 * (int)cdiv(cap, 256);        // 128-row blocks, whole 256-row pair tiles
   if ((rc = dalloc(h, &h->fwdflags, (size_t)h->L * h->fwd_mtiles))) return bail(rc);
   if ((rc = dalloc(h, &h->bwdflags, (size_t)h->L * h->fwd_mtiles))) return bail(rc);
@@ -1344,11 +1354,18 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
     tl_mark(h, 6);
     if (dense && join && !defer) TRY(join());
     tl_mark(h, 7);
-    const int rc = weights();
+    const int rc = defer ? SDN_OK : weights();   // deferred: the last GEMM weighs its rows itself
     tl_mark(h, 8);
     return rc;
   };
-  if (defer) ssum.U0 = sw.Ub[0];
+  if (defer) {
+    ssum.U0 = sw.Ub[0];
+    ssum.wfun = 1;
+    ssum.rs = rs_w;
+    ssum.Q = h->Q;
+    ssum.st = stats_dev;
+    ssum.shift = h->shift;
+  }
   float* u0 = nullptr;
   int64_t nrb = 0;
   TRY(run_backward(h, nmax, nact, rowidx, &u0, rows_hint, false, &nrb, &ssum));

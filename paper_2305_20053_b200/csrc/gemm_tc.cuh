@@ -989,6 +989,17 @@ struct EpiBwdSum {
   // optional: u = D g itself stored (fp32, ld) through TMA by the ring
   // epilogue, for sums whose row weights are known only later (exact CVaR)
   float* U0 = nullptr;
+  // weights computed in the epilogue from Q and the moments (wfun != 0)
+  // instead of read from W: no weights kernel ahead of this GEMM
+  int wfun = 0;
+  RiskSet rs{};
+  const double* Q = nullptr;
+  const double* st = nullptr;
+  double shift = 0.0;
+  SDN_DEV bool has_w() const { return W != nullptr || wfun != 0; }
+  SDN_DEV double weight(int64_t row, int q) const {
+    return wfun ? risk_weight(rs, q, row, Q[row], st, shift) : W[row * R + q];
+  }
   SDN_DEV void operator()(int64_t, int, float4) const {}
   SDN_DEV void col(int64_t, int, float) const {}
 };
@@ -1028,12 +1039,12 @@ struct TileEpi<EpiBwdSum> {
     // unified sweep: each lane stages its row's risk weights (fp64) in the
     // residual staging buffer, free at this point
     double* ws = reinterpret_cast<double*>(s.f0);
-    if (e.W)
-      for (int q = 0; q < e.R; ++q) ws[q * 32 + lane] = live ? e.W[(tr.r0 + lane) * e.R + q] : 0.0;
+    if (e.has_w())
+      for (int q = 0; q < e.R; ++q) ws[q * 32 + lane] = live ? e.weight(tr.r0 + lane, q) : 0.0;
     __syncwarp();
     const int64_t prow = (tr.r0 >> 7) * 4 + ((tr.r0 >> 5) & 3);
     const int j = lane & 15;                      // column of the chunk
-    if (!e.W) {
+    if (!e.has_w()) {
       if (lane < 16 && c0 + j < N) {
         double acc = 0.0;
 #pragma unroll 8
@@ -1281,10 +1292,10 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
     double wreg[4] = {0.0, 0.0, 0.0, 0.0};
     if constexpr (SUM) {
       const EpiBwdSum& e = ep;
-      if (e.W && r0 + lane < M)
+      if (e.has_w() && r0 + lane < M)
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq)
-          if (qq < e.R) wreg[qq] = e.W[(r0 + lane) * e.R + qq];
+          if (qq < e.R) wreg[qq] = e.weight(r0 + lane, qq);
     }
     tcx::mbar_wait(&tfull[acc], acc_phase);
     tcx::fence_after();
@@ -1326,16 +1337,16 @@ SDN_DEV void epi_bwd_ring(const Epi& ep, const TcOutMaps& om, uint8_t* epi_base,
         __syncwarp();
         row_put(Ds, lane, dd);
         double* ws = reinterpret_cast<double*>(Rs);   // per-row risk weights (fp64)
-        if (e.W) {
+        if (e.has_w()) {
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq)
             if (qq < e.R) ws[qq * 32 + lane] = wreg[qq];
-          for (int qq = 4; qq < e.R; ++qq) ws[qq * 32 + lane] = live ? e.W[(r0 + lane) * e.R + qq] : 0.0;
+          for (int qq = 4; qq < e.R; ++qq) ws[qq * 32 + lane] = live ? e.weight(r0 + lane, qq) : 0.0;
         }
         __syncwarp();
         const int64_t prow = (r0 >> 7) * 4 + ((r0 >> 5) & 3);
         const int j = lane & 15;
-        if (!e.W) {
+        if (!e.has_w()) {
           if (lane < 16 && col + j < N) {
             double a = 0.0;
 #pragma unroll 8

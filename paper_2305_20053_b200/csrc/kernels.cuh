@@ -462,8 +462,10 @@ k_sel_colsum(int64_t k, const int* __restrict__ rows, int w, const float* __rest
   __shared__ double s[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
   double acc = 0.0;
-  if (c < w)
-    for (int64_t j = threadIdx.y; j < k; j += 32) acc += (double)u[(int64_t)rows[j] * ld + c];
+  if (c < w) {
+#pragma unroll 4
+    for (int64_t j = threadIdx.y; j < k; j += 32) acc += (double)u[(int64_t)__ldg(rows + j) * ld + c];
+  }
   s[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && c < w) {
