@@ -480,8 +480,12 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
   // from layer 0 on) in one launch; the output layer follows as its own GEMM
   {
     const int NH = L - 1, Nw = h->w[1];
+    // (only when a layer's 128 x 256 tiles fill at least half the GPU, as
+    // tc_gemm's 256-column rule: small batches (c1) keep the per-layer GEMMs'
+    // narrower tiles, which spread over more SMs)
     bool ok = tcc && rflags && tcX0 && g_tc_chain && NH >= 2 && NH <= SDN_CHAIN_MAX && h->act != ACT_SOFTMAX &&
-              h->tcw.enabled && Nw % 16 == 0 && Nw > 128 && tcX0->ld % 8 == 0 && K0 % 8 == 0;
+              h->tcw.enabled && Nw % 16 == 0 && Nw > 128 && tcX0->ld % 8 == 0 && K0 % 8 == 0 &&
+              cdiv(nrows, 128) * cdiv(Nw, 256) >= h->num_sms / 2;
     for (int l = 1; l < NH && ok; ++l) ok = h->w[l + 1] == Nw && h->res[l];
     if (ok) {
       std::vector<FwdChainLayerHost> ls;
@@ -610,7 +614,8 @@ static int run_backward(sdn_handle* h, int64_t nmax, const int* n_act_dev, const
   {
     const int NW = h->w[1];
     bool ok = tcc && g_bwd_chain && ss && !want_u0 && !rowidx && !n_act_dev && L >= 4 && L - 2 <= SDN_CHAIN_MAX &&
-              h->act != ACT_SOFTMAX && NW % 16 == 0 && NW > 128 && nmax <= h->cap;
+              h->act != ACT_SOFTMAX && NW % 16 == 0 && NW > 128 && nmax <= h->cap &&
+              cdiv(nmax, 128) * cdiv(NW, 256) >= h->num_sms / 2;
     for (int l = 1; l < L && ok; ++l) ok = h->w[l] == NW;
     if (ok) {
       std::vector<BwdChainLayerHost> ls;
