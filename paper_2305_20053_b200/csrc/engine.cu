@@ -210,7 +210,7 @@ struct sdn_handle {
   const double* ref_tp = nullptr;  // device-side t of the refinement window (set by refine_window)
   // side stream (overlapped exact-CVaR selection in sdn_eval_multi)
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fwd = nullptr, ev_side = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_side = nullptr, ev_qoi = nullptr;
   int* x_counts = nullptr;
   int* x_offs = nullptr;
   std::vector<int*> x_rowidx, x_nact;
@@ -883,6 +883,7 @@ int sdn_destroy(sdn_handle* h) {
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->ev_fwd) cudaEventDestroy(h->ev_fwd);
   if (h->ev_side) cudaEventDestroy(h->ev_side);
+  if (h->ev_qoi) cudaEventDestroy(h->ev_qoi);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return SDN_OK;
@@ -1105,9 +1106,13 @@ static int refine_window(sdn_handle* h, const sdn_risk* risk, bool dec, int qg, 
 // phase 1: forward over the shard; local moments -> stats_dev (device)
 // (all, n_all): the evaluation's risks, whose t values travel with z (graph
 // parameters); slot: this forward's risk among them
+static int launch_qoi(sdn_handle* h, const sdn_risk* risk, double* stats_dev, const double* tp);
+
+// (defer_qoi: the caller launches the QoI itself, launch_qoi -- sdn_eval_multi
+// puts it on the side stream so the reverse sweep starts right after the forward)
 static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, double* stats_dev,
                         bool store_D, const sdn_risk* all = nullptr, int n_all = 0, int slot = 0,
-                        bool fuse_seed = false) {
+                        bool fuse_seed = false, bool defer_qoi = false) {
   if (!all) { all = risk; n_all = 1; slot = 0; }
   h->seed_fused = false;
   if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
@@ -1147,16 +1152,24 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
                              EpiStore{h->KPhi, (int64_t)h->r_u})));
     }
   }
+  h->fwd_done = true;
+  if (!defer_qoi) TRY(launch_qoi(h, risk, stats_dev, tp));
+  return SDN_OK;
+}
+
+// per-sample QoI + moments (and the smoothed-CVaR window refinement) on h->stream
+static int launch_qoi(sdn_handle* h, const sdn_risk* risk, double* stats_dev, const double* tp) {
+  const bool dec = risk->qoi == SDN_QOI_DECODED;
+  const double q0 = dec ? h->q0dec : h->q0;
   const int qg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(h->n, 1), 8), h->qgrid));
   { ProfScope ps(h, PC_QOI, 4.0 * h->n * h->r_u, 4.0 * h->n * h->r_u * (dec ? 2 : 1) + 8.0 * h->n);
   k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
                                    h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
                                    h->Q, h->qpart, tp, h->red_counter, stats_dev); }
-  tl_mark(h, 3);
+  tl_mark(h, 3, h->stream);
   h->launches += 1;
   CHECK_LAUNCH(h);
   TRY(refine_window(h, risk, dec, qg, stats_dev, tp));
-  h->fwd_done = true;
   return SDN_OK;
 }
 
@@ -1263,7 +1276,7 @@ static int ensure_sweep(sdn_handle* h, SweepBufs& b, int R) {
 static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uint8_t* const* masks,
                           const int64_t* ks, const double* stats_dev, double* partials,
                           const std::function<int()>& join = {}, const double* tdev = nullptr,
-                          const int* const* sel_rows = nullptr) {
+                          const int* const* sel_rows = nullptr, const std::function<int()>& qjoin = {}) {
   if (!h->fwd_done) return fail(SDN_ERR_STATE, "eval_forward first");
   if (R < 1 || R > SDN_RMAX) return fail(SDN_ERR_ARG, "1..8 risks per sweep");
   RiskSet rs{};
@@ -1357,6 +1370,7 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   ssum.plane = tplane;
   ssum.before_last = [&]() -> int {
     tl_mark(h, 6);
+    if (qjoin) TRY(qjoin());                      // Q and the moments (QoI on the side stream)
     if (dense && join && !defer) TRY(join());
     tl_mark(h, 7);
     const int rc = defer ? SDN_OK : weights();   // deferred: the last GEMM weighs its rows itself
@@ -1484,6 +1498,7 @@ static int ensure_side(sdn_handle* h) {
   CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_qoi, cudaEventDisableTiming));
   const int nb1024 = (int)cdiv(h->cap, 1024);
   int rc;
   if ((rc = dalloc(h, &h->x_counts, nb1024))) return rc;
@@ -1574,8 +1589,13 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     dense |= risks[i].kind == SDN_RISK_MEAN || risks[i].kind == SDN_RISK_MEANVAR;
   }
   // a dense sweep over all rows: the output layer writes its unit seeds
+  // Overlap (a dense risk present, see below): the QoI runs first on the side
+  // stream -- the sweep's unit seeds never read Q, so the reverse chain starts
+  // right behind the forward; Q and the moments join before the last GEMM
+  const bool overlap = dense && n_exact > 0 && !h->prof && !h->no_overlap;
+  const bool qoi_side = overlap && smooth < 0 && any_grad && h->tcw.enabled;
   TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad, risks, n_risks,
-                   smooth >= 0 ? smooth : 0, dense && any_grad));
+                   smooth >= 0 ? smooth : 0, dense && any_grad, qoi_side));
   std::vector<const uint8_t*> masks(n_risks, nullptr);
   std::vector<const int*> sel_rows(n_risks, nullptr);
   auto select_all = [&]() -> int {
@@ -1599,14 +1619,21 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   // stream seeds and runs the first L-2 sweep GEMMs.  The sweep's seeds are
   // unit weights (no Q read), so the in-place refinement of Q cannot race.
   // (Profiling runs serialise: its class timers are stream-ordered.)
-  const bool overlap = dense && n_exact > 0 && !h->prof && !h->no_overlap;
-  std::function<int()> join;
+  std::function<int()> join, qjoin;
   if (overlap) {
     CU(cudaEventRecord(h->ev_fwd, h->stream));
     CU(cudaStreamWaitEvent(h->side, h->ev_fwd, 0));
     tl_mark(h, 4, h->side);
     {
       SideScope ss(h);
+      if (qoi_side) {
+        TRY(launch_qoi(h, &risks[0], h->stats_loc, h->zdev + h->d_z));
+        CU(cudaEventRecord(h->ev_qoi, h->side));
+        qjoin = [h]() -> int {
+          CU(cudaStreamWaitEvent(h->stream, h->ev_qoi, 0));
+          return SDN_OK;
+        };
+      }
       TRY(select_all());
     }
     tl_mark(h, 5, h->side);
@@ -1622,7 +1649,7 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   }
   h->risk = risks[0];
   int rc = backward_multi(h, risks, n_risks, masks.data(), kks.data(), h->stats_loc, h->partial_multi, join,
-                          h->zdev + h->d_z, sel_rows.data());
+                          h->zdev + h->d_z, sel_rows.data(), qjoin);
   h->sm_avail = h->num_sms;
   if (rc) return rc;
   {                                   // results -> host-mapped memory (one kernel, no copy nodes)
