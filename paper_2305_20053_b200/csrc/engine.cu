@@ -504,8 +504,35 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
         ls.push_back(x);
         c = l == 0 ? 0 : 1 - c;
       }
+      // optionally the output layer too (phi = mu + sigma (acc + b), and the
+      // reverse sweep's unit seeds when fused) as the chain's last layer:
+      // measured slower at c2 (device span 0.330 -> 0.342 ms: its 128-column
+      // layer on 256-column tiles at the end of every CTA's list), so off by
+      // default; SDN_CHAIN_OUT=1 enables it
+      static const bool chain_out = getenv("SDN_CHAIN_OUT") && getenv("SDN_CHAIN_OUT")[0] == '1';
+      const bool out_in_chain = chain_out && h->r_u % 16 == 0 && h->r_u >= 16;
+      if (out_in_chain) {
+        FwdChainLayerHost x{};
+        x.A = &h->tcw.act[c];
+        x.B = &h->tcw.fwd[L - 1];
+        const bool seeds = fuse_seed && L > 1;
+        x.S = seeds ? &h->sw->seed : nullptr;
+        x.D = phi_out;
+        x.bias = h->b[L - 1];
+        x.K = h->w[L - 1];
+        x.fl = flags_of(L - 1);
+        x.N = h->r_u;
+        x.kind = 1;
+        x.scale = h->ostd;
+        x.shift = h->omean;
+        x.a2 = h->seed_a2;
+        x.b2 = h->seed_b2;
+        ls.push_back(x);
+        if (seeds) h->seed_fused = true;
+      }
       double fl_sum = 0.0;
       for (int l = 0; l < NH; ++l) fl_sum += 2.0 * nrows * Nw * (l == 0 ? K0 : h->w[l]);
+      if (out_in_chain) fl_sum += 2.0 * nrows * h->r_u * h->w[L - 1];
       ProfScope ps(h, PC_FWD_GEMM, fl_sum, 0.0);
       g_tc_pdl_now = h->sm_avail == h->num_sms;
       const int64_t tiles = cdiv(nrows, 128) * cdiv(Nw, 256) * NH;
@@ -515,7 +542,7 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
       if (rc != 0) return fail(SDN_ERR_CUDA, "tcgen05 forward chain launch failed (" + std::to_string(rc) + ")");
       CHECK_LAUNCH(h);
       cur = c;
-      l_start = NH;
+      l_start = out_in_chain ? L : NH;
       in = nullptr;
       ldin = Nw;
     }

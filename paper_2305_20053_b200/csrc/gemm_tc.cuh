@@ -1661,9 +1661,19 @@ struct FwdChainLayer {
   const int* fin;      // readiness of this layer's input rows (null: ready at launch)
   int* fout;           // this layer's row-block flags (null: not published)
   int K, has_prev, has_D, has_split;
+  int N, nt;           // output width, column tiles
+  int boff;            // this layer's bias offset in the shared-memory copy
+  // kind 1: the output layer -- phi = shift + scale (acc + bias) stored fp32
+  // (dmap) and the reverse sweep's unit seeds a2 phi + b2 as a split (smap)
+  int kind;
+  const float* scale;
+  const float* shift;
+  const float* a2;
+  const float* b2;
 };
 struct FwdChainArgs {
   int L, N, n_tiles, m_tiles, act, bias_smem;
+  int lstart[SDN_CHAIN_MAX + 1];                           // first global tile of each layer
 
 
   int64_t M;
@@ -1676,13 +1686,24 @@ struct FwdChainArgs {
 // the chain kernels' producer (TMA) and MMA-issuer loops over the global
 // tile list (identical for the forward and the reverse chain; Args holds the
 // per-layer operand maps a[l], b[l], K and input flags fin)
+// global tile g -> (layer, 256-row tile, column tile); layers may differ in width
+template <class Args>
+SDN_DEV void chain_tile(const Args& ca, int g, int& l, int& mbt, int& nb) {
+  l = 0;
+  while (l + 1 < ca.L && g >= ca.lstart[l + 1]) ++l;
+  const int t = g - ca.lstart[l], nt = ca.ly[l].nt;
+  mbt = t / nt;
+  nb = t - mbt * nt;
+}
+
 template <int BN, int CG, int STAGES, class C, class Args>
 SDN_DEV void chain_produce(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* empty, int rank, int t0, int ts,
                            int tpl, int total, int n_tiles) {
   int stage = 0;
   uint32_t phase = 0;
   for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
-    const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+    int l, mbt, nb;
+    chain_tile(ca, g, l, mbt, nb);
     const int mb = mbt * CG + rank;          // this CTA's 128-row block
     const auto& ly = ca.ly[l];
     chain_stamp(ti, 0);
@@ -1716,7 +1737,8 @@ SDN_DEV void chain_mma(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* 
   int stage = 0, acc = 0;
   uint32_t phase = 0, acc_phase = 0;
   for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
-    const int l = g / tpl;
+    int l, mbt, nb;
+    chain_tile(ca, g, l, mbt, nb);
     const int kblocks = (ca.ly[l].K + TC_BK - 1) / TC_BK;
     tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
     tcx::fence_after();
@@ -1817,7 +1839,7 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
   asm volatile("griddepcontrol.wait;" ::: "memory");      // inputs of the first layer (MR split, z-bias)
   asm volatile("griddepcontrol.launch_dependents;");
   // (pairs: m_tiles counts 256-row tiles; the CTA of rank r owns rows 128 r .. 128 r + 127 of each)
-  const int n_tiles = ca.n_tiles, tpl = ca.m_tiles * n_tiles, total = ca.L * tpl, N = ca.N;
+  const int n_tiles = ca.n_tiles, tpl = ca.m_tiles * n_tiles, total = ca.lstart[ca.L];
   const int t0 = (int)blockIdx.x / CG, ts = (int)gridDim.x / CG;
 
   if (warp == 0) {
@@ -1831,15 +1853,19 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
     float* Dst = reinterpret_cast<float*>(wb + RING * 2048);
     uint64_t* rbar = rbar_all + w * RING;
     if (ca.bias_smem)
-      for (int i = (int)threadIdx.x - 128; i < ca.L * N; i += 32 * EW) bias_all[i] = __ldg(ca.ly[i / N].bias + i % N);
+      for (int l = 0; l < ca.L; ++l)
+        for (int i = (int)threadIdx.x - 128; i < ca.ly[l].N; i += 32 * EW)
+          bias_all[ca.ly[l].boff + i] = __ldg(ca.ly[l].bias + i);
     asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
     int acc = 0, jt = 0;                          // jt: chunks before this tile (ring slot of chunk ci = (jt + ci) % RING)
     uint32_t acc_phase = 0, rphase = 0;          // rphase: parity bit per ring slot
     for (int g = t0; g < total; g += ts) {
-      const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+      int l, mbt, nb;
+      chain_tile(ca, g, l, mbt, nb);
       const int mbl = mbt * CG + rank;            // this CTA's 128-row block
       const FwdChainLayer& ly = ca.ly[l];
-      const bool has_prev = ly.has_prev, has_split = ly.has_split, has_D = ly.has_D;
+      const int N = ly.N;
+      const bool has_prev = ly.has_prev, has_split = ly.has_split, has_D = ly.has_D, outl = ly.kind == 1;
       const int r0 = mbl * TC_BM + q * 32;
       int nch = 0;
       for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
@@ -1865,7 +1891,7 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
         __syncwarp();
         if (lane == 0) tmem_release<CG>(&tempty[acc]);
       }
-      const float* bias_l = ca.bias_smem ? bias_all + l * N : nullptr;
+      const float* bias_l = ca.bias_smem ? bias_all + ly.boff : nullptr;
 #pragma unroll 1
       for (int ci = 0; ci < nch; ++ci) {
         const int c0 = first_c + CS * ci, col = nb * BN + c0, s2 = (jt + ci) % RING;
@@ -1891,7 +1917,24 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
                                    : __ldg(reinterpret_cast<const float4*>(ly.bias + col + j));
           bias[j] = b4.x; bias[j + 1] = b4.y; bias[j + 2] = b4.z; bias[j + 3] = b4.w;
         }
-        fwd_act16(ca.act, v, bias, has_prev, a, d);
+        if (outl) {                               // phi = shift + scale (acc + b) -> d; seeds a2 phi + b2 -> a
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            const float4 sc = __ldg(reinterpret_cast<const float4*>(ly.scale + col + j));
+            const float4 sf = __ldg(reinterpret_cast<const float4*>(ly.shift + col + j));
+            const float4 aa = __ldg(reinterpret_cast<const float4*>(ly.a2 + col + j));
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(ly.b2 + col + j));
+            const float scs[4] = {sc.x, sc.y, sc.z, sc.w}, sfs[4] = {sf.x, sf.y, sf.z, sf.w};
+            const float as[4] = {aa.x, aa.y, aa.z, aa.w}, bs[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              d[j + k] = fmaf(scs[k], __uint_as_float(v[j + k]) + bias[j + k], sfs[k]);
+              a[j + k] = fmaf(as[k], d[j + k], bs[k]);
+            }
+          }
+        } else {
+          fwd_act16(ca.act, v, bias, has_prev, a, d);
+        }
         if (lane == 0) tcx::bulk_wait_read0();   // previous chunk's stores have read their staging
         __syncwarp();
         issue(ci + RING - 1);
@@ -1941,9 +1984,11 @@ struct BwdChainLayer {
   const int* fin;
   int* fout;
   int K, has_resid, has_G;
+  int N, nt;
 };
 struct BwdChainArgs {
   int L, N, n_tiles, m_tiles;
+  int lstart[SDN_CHAIN_MAX + 1];
   int64_t M;
   BwdChainLayer ly[SDN_CHAIN_MAX];
   CUtensorMap a[SDN_CHAIN_MAX], b[SDN_CHAIN_MAX];          // mainloop operands
@@ -2007,7 +2052,7 @@ tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
   const uint32_t tmem = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");      // the seeds' split (forward output layer)
   asm volatile("griddepcontrol.launch_dependents;");
-  const int n_tiles = ca.n_tiles, tpl = ca.m_tiles * n_tiles, total = ca.L * tpl, N = ca.N;
+  const int n_tiles = ca.n_tiles, tpl = ca.m_tiles * n_tiles, total = ca.lstart[ca.L];
   const int t0 = (int)blockIdx.x / CG, ts = (int)gridDim.x / CG;
 
   if (warp == 0) {
@@ -2021,9 +2066,11 @@ tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
     int acc = 0, jt = 0;
     uint32_t acc_phase = 0, rphase = 0;
     for (int g = t0; g < total; g += ts) {
-      const int l = g / tpl, t = g - l * tpl, mbt = t / n_tiles, nb = t - mbt * n_tiles;
+      int l, mbt, nb;
+      chain_tile(ca, g, l, mbt, nb);
       const int mbl = mbt * CG + rank;
       const BwdChainLayer& ly = ca.ly[l];
+      const int N = ly.N;
       const bool has_resid = ly.has_resid, has_G = ly.has_G;
       const int r0 = mbl * TC_BM + q * 32;
       int nch = 0;
@@ -2435,6 +2482,12 @@ struct FwdChainLayerHost {
   const float* bias;
   int K;
   TcFlags fl;
+  int N = 0;           // 0: the chain's N
+  int kind = 0;        // 1: output layer (phi to D, seeds to S)
+  const float* scale = nullptr;
+  const float* shift = nullptr;
+  const float* a2 = nullptr;
+  const float* b2 = nullptr;
 };
 static bool g_tc_chain = !(getenv("SDN_NO_CHAIN") && getenv("SDN_NO_CHAIN")[0] == '1');
 template <int CG, int EW>
@@ -2452,20 +2505,27 @@ static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
   ca.L = L; ca.N = N; ca.M = M; ca.act = act;
   ca.n_tiles = (N + BN - 1) / BN;
   ca.m_tiles = (int)((M + TC_BM * CG - 1) / (TC_BM * CG));
-  ca.bias_smem = (uint32_t)L * N * 4 <= CC::BIAS_BYTES ? 1 : 0;
+  int boff = 0, tiles = 0;
   for (int l = 0; l < L; ++l) {
     const FwdChainLayerHost& x = ls[l];
     FwdChainLayer& y = ca.ly[l];
+    const int Nl = x.N ? x.N : N;
+    if (Nl % 16) return -1;
     if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l]) ||
-        tc_map(t, *x.B, N, x.K, BN / CG, &ca.b[l]))
+        tc_map(t, *x.B, Nl, x.K, BN / CG, &ca.b[l]))
       return -2;
-    if (x.D && tc_out_map(t, x.D, false, M, N, N, &ca.dmap[l])) return -3;
-    if (x.S && tc_out_map_pair(t, x.S->hi, x.S->lo, M, N, x.S->ld, &ca.smap[l])) return -3;
-    if (x.P && tc_out_map_pair(t, x.P->hi, x.P->lo, M, N, x.P->ld, &ca.pmap[l])) return -3;
+    if (x.D && tc_out_map(t, x.D, false, M, Nl, Nl, &ca.dmap[l])) return -3;
+    if (x.S && tc_out_map_pair(t, x.S->hi, x.S->lo, M, Nl, x.S->ld, &ca.smap[l])) return -3;
+    if (x.P && tc_out_map_pair(t, x.P->hi, x.P->lo, M, Nl, x.P->ld, &ca.pmap[l])) return -3;
     y.bias = x.bias; y.K = x.K; y.fin = x.fl.in; y.fout = x.fl.out;
     y.has_prev = x.P != nullptr; y.has_D = x.D != nullptr; y.has_split = x.S != nullptr;
-
+    y.N = Nl; y.nt = (Nl + BN - 1) / BN; y.boff = boff; boff += Nl;
+    y.kind = x.kind; y.scale = x.scale; y.shift = x.shift; y.a2 = x.a2; y.b2 = x.b2;
+    ca.lstart[l] = tiles;
+    tiles += ca.m_tiles * y.nt;
   }
+  ca.lstart[L] = tiles;
+  ca.bias_smem = (uint32_t)boff * 4 <= CC::BIAS_BYTES ? 1 : 0;
 
   static unsigned attr_set = 0;
   int dev = 0;
@@ -2570,7 +2630,10 @@ static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
     if (tc_out_map_pair(t, x.S->hi, x.S->lo, M, N, x.S->ld, &ca.smap[l])) return -3;
     y.K = x.K; y.fin = x.fl.in; y.fout = x.fl.out;
     y.has_resid = x.R != nullptr; y.has_G = x.G != nullptr;
+    y.N = N; y.nt = ca.n_tiles;
+    ca.lstart[l] = l * ca.m_tiles * ca.n_tiles;
   }
+  ca.lstart[L] = L * ca.m_tiles * ca.n_tiles;
   static unsigned attr_set = 0;
   int dev = 0;
   cudaGetDevice(&dev);
