@@ -218,6 +218,13 @@ struct sdn_handle {
   std::vector<int64_t> x_k;     // k of each kept selection (multi-rank phases)
   std::vector<int64_t*> x_gidx; // global indices of each kept selection (ascending)
   std::vector<int64_t> x_gcap;
+  // short tail (k_sel_colsum_sl + k_finalize_export): sliced selected-row sums, finalise + export in one launch
+  bool tail_fuse = false;       // env SDN_TAIL_FUSE=1 enables (measured: no gain at c2, profiles/README.md)
+  bool tail_export = false;     // env SDN_TAIL_EXPORT=1: the finalise kernel's last block also exports (measured slower)
+  bool exp_want = false, exp_done = false;   // enqueue_multi asks the tail to export; the tail says it did
+  double *exp_s = nullptr, *exp_p = nullptr; // host-mapped destinations (stats, partials)
+  int* exp_b = nullptr;                      // ... band log
+  int exp_np = 0, exp_nb = 0;
   int sm_avail = 0;             // SMs the persistent GEMMs may use
   int side_sms = SDN_SIDE_SMS_DEFAULT;   // env SDN_SIDE_SMS (default clamped to a quarter of the SMs)
   bool no_overlap = false;               // env SDN_NO_OVERLAP=1
@@ -853,6 +860,8 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
   { const char* e = getenv("SDN_TIMELINE"); h->tl_on = e && e[0] == '1'; }
+  h->tail_fuse = getenv("SDN_TAIL_FUSE") && getenv("SDN_TAIL_FUSE")[0] == '1';
+  h->tail_export = getenv("SDN_TAIL_EXPORT") && getenv("SDN_TAIL_EXPORT")[0] == '1';
   h->side_sms = std::max(1, std::min(SDN_SIDE_SMS_DEFAULT, h->num_sms / 4));
   { const char* e = getenv("SDN_SIDE_SMS");
     if (e) h->side_sms = std::max(1, std::min(atoi(e), h->num_sms / 2)); }
@@ -1436,21 +1445,46 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   }
   h->launches++;
   CHECK_LAUNCH(h);
+  // short tail: sliced sums over the selected rows, one finalise + export launch
+  const int S = std::max(1, std::min(8, h->crb));
+  const bool short_tail = h->tail_fuse && !h->prof && !u0;
+  FinArgs fa{};
+  for (int r = 0; r < R; ++r) fa.risk[r] = FinRisk{part + (int64_t)r * plane, nrb_fin, 1.0};
   if (defer) {
     TRY(join());
     for (int r = 0; r < R; ++r) {
       if (rs.kind[r] != SDN_RISK_CVAR_EXACT) continue;
       ProfScope ps(h, PC_COLSUM, 0.0, 4.0 * ks[r] * h->h1);
-      k_sel_colsum<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>(
-          ks[r], sel_rows[r], h->h1, sw.Ub[0], h->h1, rs.kinv[r], h->Q, sw.csum + (int64_t)r * h->h1,
-          h->vsum + 2 * r);
+      if (short_tail) {
+        // (cpart: the SIMT sweep's partial planes, idle here: R x crb x maxw >= R x S x h1)
+        double* sl = sw.cpart + (int64_t)r * h->crb * h->maxw;
+        k_sel_colsum_sl<<<dim3((unsigned)cdiv(h->h1, 32), S), dim3(32, 32), 0, h->stream>>>(
+            ks[r], sel_rows[r], h->h1, sw.Ub[0], h->h1, h->Q, sl, h->vsum + 2 * r);
+        fa.risk[r] = FinRisk{sl, S, rs.kinv[r]};
+      } else {
+        k_sel_colsum<<<(unsigned)cdiv(h->h1, 32), dim3(32, 32), 0, h->stream>>>(
+            ks[r], sel_rows[r], h->h1, sw.Ub[0], h->h1, rs.kinv[r], h->Q, sw.csum + (int64_t)r * h->h1,
+            h->vsum + 2 * r);
+      }
       h->launches++;
       CHECK_LAUNCH(h);
     }
   }
   { ProfScope ps(h, PC_FINAL, 0.0, 8.0 * nrb_fin * h->h1 * R);
-  k_finalize_multi<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(
-      nrb_fin, plane, h->h1, h->d_z, part, h->PzT, h->vsum, h->plen(), partials); }
+  if (short_tail) {
+    fa.h1 = h->h1; fa.d_z = h->d_z; fa.plen = h->plen();
+    fa.PzT = h->PzT; fa.vsum = h->vsum; fa.out = partials; fa.counter = h->red_counter + 2;
+    if (h->tail_export && h->exp_want && partials == h->partial_multi) {
+      fa.stats = stats_dev; fa.hstats = h->exp_s; fa.nstats = STATS_LEN;
+      fa.hpart = h->exp_p; fa.npart = h->exp_np;
+      fa.band = h->band_log; fa.hband = h->exp_b; fa.nband = h->exp_nb;
+      h->exp_done = true;
+    }
+    k_finalize_export<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(fa);
+  } else {
+    k_finalize_multi<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(
+        nrb_fin, plane, h->h1, h->d_z, part, h->PzT, h->vsum, h->plen(), partials);
+  } }
   h->launches++;
   CHECK_LAUNCH(h);
   return SDN_OK;
@@ -1675,16 +1709,23 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     TRY(select_all());
   }
   h->risk = risks[0];
+  // results -> host-mapped memory: by the sweep's fused tail when it runs,
+  // else by one export kernel (no copy nodes either way)
+  double *dst_s = nullptr, *dst_p = nullptr;
+  int* dst_b = nullptr;
+  CU(cudaHostGetDevicePointer((void**)&dst_s, h->hstats, 0));
+  CU(cudaHostGetDevicePointer((void**)&dst_p, h->hpart_multi, 0));
+  CU(cudaHostGetDevicePointer((void**)&dst_b, h->hband, 0));
+  h->exp_want = true;
+  h->exp_done = false;
+  h->exp_s = dst_s; h->exp_p = dst_p; h->exp_b = dst_b;
+  h->exp_np = n_risks * plen; h->exp_nb = n_risks + 1;
   int rc = backward_multi(h, risks, n_risks, masks.data(), kks.data(), h->stats_loc, h->partial_multi, join,
                           h->zdev + h->d_z, sel_rows.data(), qjoin);
   h->sm_avail = h->num_sms;
+  h->exp_want = false;
   if (rc) return rc;
-  {                                   // results -> host-mapped memory (one kernel, no copy nodes)
-    double *dst_s = nullptr, *dst_p = nullptr;
-    int* dst_b = nullptr;
-    CU(cudaHostGetDevicePointer((void**)&dst_s, h->hstats, 0));
-    CU(cudaHostGetDevicePointer((void**)&dst_p, h->hpart_multi, 0));
-    CU(cudaHostGetDevicePointer((void**)&dst_b, h->hband, 0));
+  if (!h->exp_done) {
     k_export<<<1, 256, 0, h->stream>>>(h->stats_loc, dst_s, STATS_LEN, h->partial_multi, dst_p, n_risks * plen,
                                        h->band_log, dst_b, n_risks + 1);
     h->launches++;

@@ -219,6 +219,15 @@ SDN_DEV int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// CTA-local progress counter in shared memory (chain publisher hand-off)
+SDN_DEV void red_release_cta_smem(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+SDN_DEV uint32_t ld_acquire_cta_smem(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
 SDN_DEV void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -289,10 +298,14 @@ SDN_DEV void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
-// arrive on the leader's copy of a barrier (release at cluster scope)
+// arrive on the leader's copy of a barrier.  The arrivals on these barriers
+// hand TMEM accumulators back to the MMA issuer: the tcgen05 fences on both
+// sides order the TMEM accesses, no generic-proxy memory is published, so the
+// default (cta-scope) release is enough -- a cluster-scope release compiles
+// to MEMBAR.ALL.GPU + ERRBAR, ~11% of an epilogue warp's time in the chains
+// (profiles/r02g_fwd_chain_stalls.txt)
 SDN_DEV void mbar_arrive_leader(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK) : "memory");
 }
 SDN_DEV void tmem_alloc_pair(uint32_t* dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
@@ -1775,6 +1788,35 @@ SDN_DEV void chain_mma(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* 
   }
 }
 
+// the chain kernels' publisher (warp 3, one thread): the gpu-scope release of
+// a row block's flag costs MEMBAR.ALL.GPU + CCTL.IVALL (~10% of an epilogue
+// warp's time when each warp published its own part,
+// profiles/r02g_fwd_chain_stalls.txt).  The epilogue warps instead count
+// "my stores of tile i are complete" on a CTA-local shared counter
+// (release.cta after cp.async.bulk.wait_group + the proxy fence), and this
+// otherwise idle thread turns EW counts into one red.release.gpu on the flag.
+// Four rotating counters: a warp can run at most two tiles ahead of another
+// (the accumulator double buffer), so tile i never shares a counter with a
+// tile still in flight.
+template <int BN, int CG, int EW, class Args>
+SDN_DEV void chain_publish(const Args& ca, uint32_t* pubc, int rank, int t0, int ts, int total) {
+  uint64_t want = 0;                               // 4 x 16-bit expected counts (no local array)
+  int ti = 0;
+  for (int g = t0; g < total; g += ts, ++ti) {
+    int l, mbt, nb;
+    chain_tile(ca, g, l, mbt, nb);
+    const auto& ly = ca.ly[l];
+    if (!ly.fout) continue;
+    const int sh = 16 * (ti & 3);
+    want += (uint64_t)EW << sh;
+    const uint32_t need = (uint32_t)(want >> sh) & 0xFFFFu;
+    int nchunks = 0;                               // 16-column chunks of this tile, all column groups
+    for (int c = 0; c < BN && nb * BN + c < ly.N; c += 16) ++nchunks;
+    while (tcx::ld_acquire_cta_smem(&pubc[ti & 3]) < need) __nanosleep(32);
+    tcx::red_release_add(ly.fout + (mbt * CG + rank), TC_BM * 16 * nchunks);
+  }
+}
+
 // shared-memory plan of the chain kernel: STAGES mainloop stages, EW
 // epilogue warps with RING 2-KB slots + a 2-KB D tile each, every layer's bias
 template <int BN, int RING, int CG, int EW>
@@ -1810,6 +1852,7 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar_all = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar_all + RING * EW);
+  uint32_t* pubc = tmem_slot + 2;                 // 4 rotating tile-done counters (publisher hand-off)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int rank = CG == 1 ? 0 : (int)tcx::cluster_rank();
   if (threadIdx.x == 0) {
@@ -1820,6 +1863,7 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
     for (int s2 = 0; s2 < STAGES; ++s2) { tcx::mbar_init(&full[s2], 1); tcx::mbar_init(&empty[s2], 1); }
     for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], CG * EW); }
     for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar_all[i], 1);
+    for (int i = 0; i < 4; ++i) pubc[i] = 0;
     tcx::fence_barrier_init();
   }
   if (warp == 2) {
@@ -1846,8 +1890,10 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
     if (lane == 0) chain_produce<BN, CG, STAGES, C>(ca, smem, full, empty, rank, t0, ts, tpl, total, n_tiles);
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) chain_mma<BN, CG, STAGES, C>(ca, smem, full, empty, tfull, tempty, tmem, t0, ts, tpl, total);
+  } else if (warp == 3) {
+    if (lane == 0) chain_publish<BN, CG, EW>(ca, pubc, rank, t0, ts, total);
   } else if (warp >= 4) {
-    const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
+    const int w = warp - 4, q = warp & 3;
     uint8_t* wb = epi_base + w * WB;
     int ti = 0;
     float* Dst = reinterpret_cast<float*>(wb + RING * 2048);
@@ -1867,6 +1913,10 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
       const int N = ly.N;
       const bool has_prev = ly.has_prev, has_split = ly.has_split, has_D = ly.has_D, outl = ly.kind == 1;
       const int r0 = mbl * TC_BM + q * 32;
+      // the warp's column group rotates with the tile: a 256-column tile is 16
+      // chunks, i.e. 6 + 5 + 5 over three groups -- rotating evens the warps out
+      // over consecutive tiles (they only meet at the accumulator hand-back)
+      const int first_c = 16 * (((w >> 2) + ti) % (EW / 4));
       int nch = 0;
       for (int c = first_c; c < BN && nb * BN + c < N; c += CS) ++nch;
       // this tile's residual tiles, RING-1 chunks ahead (within the tile)
@@ -1950,12 +2000,12 @@ tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
       }
       jt += nch;
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      if (ly.fout) {                              // publish this warp's part of the row block
+      if (ly.fout) {                              // this warp's part of the row block is written: tell the publisher
         __syncwarp();
         if (lane == 0) {
           tcx::bulk_wait0();
           tcx::fence_proxy_async_global();
-          tcx::red_release_add(ly.fout + mbl, 32 * 16 * nch);
+          tcx::red_release_cta_smem(&pubc[ti & 3], 1u);
         }
       }
       if (warp == 4 && lane == 0) chain_stamp(ti, 5);
@@ -2024,6 +2074,7 @@ tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar_all = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar_all + RING * EW);
+  uint32_t* pubc = tmem_slot + 2;                 // 4 rotating tile-done counters (publisher hand-off)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int rank = CG == 1 ? 0 : (int)tcx::cluster_rank();
   if (threadIdx.x == 0) {
@@ -2034,6 +2085,7 @@ tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
     for (int s2 = 0; s2 < STAGES; ++s2) { tcx::mbar_init(&full[s2], 1); tcx::mbar_init(&empty[s2], 1); }
     for (int a = 0; a < 2; ++a) { tcx::mbar_init(&tfull[a], 1); tcx::mbar_init(&tempty[a], CG * EW); }
     for (int i = 0; i < RING * EW; ++i) tcx::mbar_init(&rbar_all[i], 1);
+    for (int i = 0; i < 4; ++i) pubc[i] = 0;
     tcx::fence_barrier_init();
   }
   if (warp == 2) {
@@ -2059,13 +2111,15 @@ tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
     if (lane == 0) chain_produce<BN, CG, STAGES, C>(ca, smem, full, empty, rank, t0, ts, tpl, total, n_tiles);
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) chain_mma<BN, CG, STAGES, C>(ca, smem, full, empty, tfull, tempty, tmem, t0, ts, tpl, total);
+  } else if (warp == 3) {
+    if (lane == 0) chain_publish<BN, CG, EW>(ca, pubc, rank, t0, ts, total);
   } else if (warp >= 4) {
     const int w = warp - 4, q = warp & 3, first_c = 16 * (w >> 2);
     uint8_t* wb = epi_base + w * WB;
     uint64_t* rbar = rbar_all + w * RING;
-    int acc = 0, jt = 0;
+    int acc = 0, jt = 0, ti = 0;
     uint32_t acc_phase = 0, rphase = 0;
-    for (int g = t0; g < total; g += ts) {
+    for (int g = t0; g < total; g += ts, ++ti) {
       int l, mbt, nb;
       chain_tile(ca, g, l, mbt, nb);
       const int mbl = mbt * CG + rank;
@@ -2140,12 +2194,12 @@ tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
       }
       jt += nch;
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      if (ly.fout) {
+      if (ly.fout) {                              // this warp's stores of the tile are complete: tell the publisher
         __syncwarp();
         if (lane == 0) {
           tcx::bulk_wait0();
           tcx::fence_proxy_async_global();
-          tcx::red_release_add(ly.fout + mbl, 32 * 16 * nch);
+          tcx::red_release_cta_smem(&pubc[ti & 3], 1u);
         }
       }
     }
@@ -2473,6 +2527,25 @@ static int tc_gemm(TcWeights& t, cudaStream_t st, int num_sms, int64_t M, const 
 // persistent forward chain launch (see tc_fwd_chain_kernel).  Layer l reads
 // A[l] and writes its split to S[l] (the next layer's A) and act' to D[l];
 // P[l] (may be null) is its residual input.  Returns 0 on launch.
+// CTA (pair) slots of a persistent chain.  Slot c walks the layer-major tile
+// list with stride S; a layer-(l+1) tile depends on the layer-l tiles of its
+// rows, T = tiles per layer earlier in the list, i.e. T/S rounds back.  With
+// T >= 2 S every dependency was published at least two rounds ago, so a tile's
+// MMAs always run under the previous tile's epilogue.  With T < 2 S the slots
+// c >= T - S depend on tiles of the round just before theirs: their MMAs cannot
+// start until that round's epilogues are done, every round -- the c2 forward
+// chain on 74 pair slots (T = 128) ran 7 rounds of epilogue + exposed MMA
+// (122 us) where 64 slots run 8 rounds of epilogue alone.  Cost model:
+// epilogue 2, exposed MMA 1 per round (SDN_CHAIN_SLOTS=n overrides).
+static int chain_slots(int slots_max, int T, int total) {
+  static const int forced = getenv("SDN_CHAIN_SLOTS") ? atoi(getenv("SDN_CHAIN_SLOTS")) : 0;
+  if (forced > 0) return std::min(forced, slots_max);
+  const int alt = T / 2;
+  if (alt < 1 || alt >= slots_max) return slots_max;
+  auto cost = [&](int S) { return ((total + S - 1) / S) * (2 + (T < 2 * S ? 1 : 0)) + 1; };
+  return cost(alt) < cost(slots_max) ? alt : slots_max;
+}
+
 struct FwdChainLayerHost {
   const TcOperand* A;
   const TcOperand* B;
@@ -2526,6 +2599,11 @@ static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
   }
   ca.lstart[L] = tiles;
   ca.bias_smem = (uint32_t)boff * 4 <= CC::BIAS_BYTES ? 1 : 0;
+  if (L > 1) {
+    int T = tiles;
+    for (int l = 0; l + 1 < L; ++l) T = std::min(T, ca.m_tiles * ca.ly[l].nt);
+    grid = CG * chain_slots(grid / CG, T, tiles);
+  }
 
   static unsigned attr_set = 0;
   int dev = 0;
@@ -2634,6 +2712,7 @@ static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
     ca.lstart[l] = l * ca.m_tiles * ca.n_tiles;
   }
   ca.lstart[L] = L * ca.m_tiles * ca.n_tiles;
+  if (L > 1) grid = CG * chain_slots(grid / CG, ca.m_tiles * ca.n_tiles, ca.lstart[L]);
   static unsigned attr_set = 0;
   int dev = 0;
   cudaGetDevice(&dev);

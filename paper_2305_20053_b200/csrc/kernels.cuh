@@ -84,7 +84,9 @@ __global__ void k_build_x(int64_t n, int r_m, int d_z, int ldx, const float* __r
 //   reduced: Q = phi.phi + 2 phi.c + q0
 //   gram   : Q = phi.(K phi) + 2 phi.c + q0  (decoded frame, K = U^T M U)
 // accumulated in fp64; plus per-block fp64 partial moments.
-// One warp per row, grid-stride; block partials in fixed order.
+// One warp per row, grid-stride, four rows in flight per warp (their 16-byte
+// loads are issued before the first fp64 reduction); block partials in fixed
+// order (rows of a warp are accumulated in ascending order).
 __global__ void __launch_bounds__(256)
 k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict__ kphi,
       const float* __restrict__ c, double q0, double shift, double t, double eps,
@@ -94,22 +96,57 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
   __shared__ double sp[8][6];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
-    const float* p = phi + i * r_u;
-    const float* kp = kphi ? kphi + i * r_u : p;
-    double s = 0.0;
-    for (int j = lane; j < r_u; j += 32) {
-      double pj = p[j];
-      s += pj * ((double)kp[j] + 2.0 * (double)c[j]);
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  const bool vec = (r_u & 3) == 0;     // rows start 16-byte aligned (cudaMalloc base, r_u % 4 == 0)
+  for (int64_t i0 = (int64_t)blockIdx.x * 8 + warp; i0 < n; i0 += 4 * stride) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (vec) {
+      for (int j = 4 * lane; j < r_u; j += 128) {
+        const float4 c4 = __ldg(reinterpret_cast<const float4*>(c + j));
+        float4 p4[4], k4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + u * stride;
+          p4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (i < n) p4[u] = __ldg(reinterpret_cast<const float4*>(phi + i * r_u + j));
+          k4[u] = p4[u];
+          if (kphi && i < n) k4[u] = __ldg(reinterpret_cast<const float4*>(kphi + i * r_u + j));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s[u] += (double)p4[u].x * ((double)k4[u].x + 2.0 * (double)c4.x);
+          s[u] += (double)p4[u].y * ((double)k4[u].y + 2.0 * (double)c4.y);
+          s[u] += (double)p4[u].z * ((double)k4[u].z + 2.0 * (double)c4.z);
+          s[u] += (double)p4[u].w * ((double)k4[u].w + 2.0 * (double)c4.w);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= n) break;
+        const float* p = phi + i * r_u;
+        const float* kp = kphi ? kphi + i * r_u : p;
+        for (int j = lane; j < r_u; j += 32) {
+          double pj = p[j];
+          s[u] += pj * ((double)kp[j] + 2.0 * (double)c[j]);
+        }
+      }
     }
-    s = warp_sum(s);
-    double q = s + q0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = warp_sum(s[u]);
     if (lane == 0) {
-      Q[i] = q;
-      double qs = q - shift, x = q - t;
-      double d1 = splus_d1_d(x, eps);
-      acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
-      acc[3] += splus_d(x, eps); acc[4] += d1; acc[5] += (d1 > 0.0) ? 1.0 : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= n) break;
+        const double q = s[u] + q0;
+        Q[i] = q;
+        double qs = q - shift, x = q - t;
+        double d1 = splus_d1_d(x, eps);
+        acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
+        acc[3] += splus_d(x, eps); acc[4] += d1; acc[5] += (d1 > 0.0) ? 1.0 : 0.0;
+      }
     }
   }
   if (lane == 0)
@@ -506,6 +543,105 @@ k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __re
     for (int y = 0; y < 32; ++y) t += s[y][threadIdx.x];
     out[c] = t;
   }
+}
+
+// ---- short tail of an evaluation (graph path).  The deferred exact-CVaR
+// sums over the k selected rows of the stored u are taken by row slices
+// (k_sel_colsum_sl: S x w/32 blocks instead of w/32; 13.7 -> ~4 us at c2), and
+// one kernel finalises every risk from its own list of partial rows and --
+// its last block -- writes the results to host-mapped memory (k_finalize_export:
+// what k_finalize_multi + k_export did in two dependent launches).  A variant
+// that did all of it in one launch with a single finishing block was slower
+// (the 2 x d_z projections of length h1 on one SM: +14 us), profiles/README.md.
+// out[s][c] = sum over slice s of the selected rows of u[rows[j], c] (fp64,
+// fixed order: thread rows j = lo + y, lo + y + 32, ..., then the 32 row groups
+// in order); the value partials vs = (sum_j Q[rows[j]], k) by block (0, 0)
+__global__ void __launch_bounds__(1024)
+k_sel_colsum_sl(int64_t k, const int* __restrict__ rows, int w, const float* __restrict__ u, int64_t ld,
+                const double* __restrict__ Q, double* __restrict__ out, double* __restrict__ vs) {
+  __shared__ double s[32][33];
+  const int c = blockIdx.x * 32 + threadIdx.x, S = gridDim.y, sl = blockIdx.y;
+  const int64_t per = (k + S - 1) / S, lo = sl * per, hi = min(k, lo + per);
+  double acc = 0.0;
+  if (c < w) {
+#pragma unroll 4
+    for (int64_t j = lo + threadIdx.y; j < hi; j += 32) acc += (double)u[(int64_t)__ldg(rows + j) * ld + c];
+  }
+  s[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < w) {
+    double t = 0.0;
+    for (int y = 0; y < 32; ++y) t += s[y][threadIdx.x];
+    out[(int64_t)sl * w + c] = t;
+  }
+  if (blockIdx.x == 0 && sl == 0 && threadIdx.y == 1) {       // one warp: lane-strided, fixed butterfly
+    double qs = 0.0;
+    for (int64_t j = threadIdx.x; j < k; j += 32) qs += Q[rows[j]];
+    qs = warp_sum(qs);
+    if (threadIdx.x == 0) {
+      vs[0] = qs;
+      vs[1] = (double)k;
+    }
+  }
+}
+struct FinRisk {
+  const double* part;    // nrb partial rows of h1 (null: zero gradient)
+  int nrb;
+  double scale;          // applied to the summed rows (1/k for the deferred exact-CVaR sums)
+};
+struct FinArgs {
+  int h1, d_z, plen;
+  FinRisk risk[SDN_RMAX];
+  const double* PzT;
+  const double* vsum;
+  double* out;           // [R][plen]
+  int* counter;          // last-block export (self re-arming)
+  const double* stats; double* hstats; int nstats;      // export (hstats null: none)
+  double* hpart; int npart;
+  const int* band; int* hband; int nband;
+};
+// per-risk finalisation (blockIdx.y = risk): A = scale * sum_b part[b][:];
+// out_r[k] = sum_c PzT[k][c] A[c]; out_r[d_z], out_r[d_z+1] = vsum[2r], vsum[2r+1];
+// then the last block exports stats / partials / band log
+__global__ void __launch_bounds__(256)
+k_finalize_export(const FinArgs a) {
+  extern __shared__ double A[];
+  __shared__ bool s_last;
+  const int r = blockIdx.y, h1 = a.h1, d_z = a.d_z;
+  const FinRisk& fr = a.risk[r];
+  for (int c = threadIdx.x; c < h1; c += blockDim.x) {
+    double s = 0.0;
+    if (fr.part)
+      for (int b = 0; b < fr.nrb; ++b) s += fr.part[(int64_t)b * h1 + c];
+    A[c] = fr.scale * s;
+  }
+  __syncthreads();
+  double* o = a.out + (int64_t)r * a.plen;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k = blockIdx.x * nw + warp; k < d_z; k += gridDim.x * nw) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = lane; c < h1; c += 32) s += __ldg(a.PzT + (int64_t)k * h1 + c) * A[c];
+    s = warp_sum(s);
+    if (lane == 0) o[k] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    o[d_z] = a.vsum[2 * r];
+    o[d_z + 1] = a.vsum[2 * r + 1];
+  }
+  if (!a.hstats) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.counter, 1) == (int)(gridDim.x * gridDim.y) - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < a.nstats; i += blockDim.x) a.hstats[i] = a.stats[i];
+  for (int i = threadIdx.x; i < a.npart; i += blockDim.x) a.hpart[i] = __ldcg(a.out + i);
+  for (int i = threadIdx.x; i < a.nband; i += blockDim.x) a.hband[i] = a.band[i];
+  if (threadIdx.x == 0) *a.counter = 0;
 }
 
 // histogram increment (plain shared atomics measured faster than warp
