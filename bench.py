@@ -188,6 +188,17 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def cpu_model():
+    """CPU model name of the host the CPU legs ran on (BASELINE.md section 4 asks for it)."""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the reference's own CPU algorithm -- the forward-mode
     chunked SurrogateEvaluator loop + saa_objective (riskopt.py:163-243),
@@ -237,7 +248,7 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference",
         "config": config_block(cfg, mode, world, risks_for(cfg)),
         "samples_per_timed_step": n_step,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "cpu_model": cpu_model(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -359,7 +370,7 @@ def run_jacobian(args, cfg, rank, world, local_rank, dist):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cpu = min(args.cpu_samples, 1024)
         rate, secs = cpu_jacobian_rate(cfg, args.seed, n_cpu)
-        cpu = {"value": rate, "unit": "samples/s", "cores": cpu_cores(), "kind": "port",
+        cpu = {"value": rate, "unit": "samples/s", "cores": cpu_cores(), "cpu_model": cpu_model(), "kind": "port",
                "sample": f"{n_cpu} samples of c5: forward-mode z_jacobian_batch in 256-sample chunks + decode "
                          f"(oracle port, fp64 numpy BLAS) ({secs:.1f} s)"}
     if rank == 0:
@@ -389,8 +400,92 @@ def run_jacobian(args, cfg, rank, world, local_rank, dist):
         dist.destroy_process_group()
 
 
+ENC_METRIC = "KLE encoder fields/sec (m_r = V_m^T M (m - mean))"
+
+
+def run_encoder(args, rank, world, local_rank):
+    """--config enc: the cold encoder (randfield.py:67-72) on the
+    c4 field shapes (d_m = 35937, r_m = 256) over a bounded number of fields --
+    setup work, once per SAA sample set.  value: fields already in HBM; e2e:
+    host fields in (pinned) through the public call.  Roofline: the fields are
+    read once (4 d_m bytes each), so the HBM figure is the algorithmic bound;
+    the kernel itself runs fp32 products with fp64 accumulation on the FMA pipe
+    (tensor-core products cannot hold the precision the
+    input whitening needs), which is what bounds it."""
+    import torch
+    from paper_2305_20053_b200 import Engine, workloads as wl
+    cfg = wl.WORKLOADS["c4"]
+    n = 4096
+    p = wl.make_problem(cfg.with_samples(n), seed=args.seed)
+    psi, lam, mdiag = wl.kl_modes(cfg, args.seed)
+    Vm = np.ascontiguousarray(psi[:, :cfg.r_m], dtype=np.float32)
+    eng = Engine(p, max_samples=n, device=local_rank, gemm=args.gemm)
+    stream = torch.cuda.Stream(device=local_rank)
+    torch.cuda.set_stream(stream)
+    eng.set_stream(stream.cuda_stream)
+    g = torch.Generator(device="cuda").manual_seed(args.seed)
+    # synthetic fields with the KL law's scale: mean + unit-variance nodal noise (values do not change the cost)
+    F = (wl.M_MEAN + torch.randn((n, cfg.d_m), generator=g, device="cuda", dtype=torch.float32)).contiguous()
+    in_bytes = n * cfg.d_m * 4                     # 589 MB > L2
+    for _ in range(max(args.warmup, 3)):
+        eng.encode_fields(F, Vm, mdiag, wl.M_MEAN)
+    steps = max(1, min(args.steps, 10))
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    launches0 = eng.kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        for i in range(steps):
+            starts[i].record(stream)
+            eng.encode_fields(F, Vm, mdiag, wl.M_MEAN)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = eng.kernel_launches() - launches0
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    value = n * steps / (ms / 1e3)
+    Fh = F.cpu().pin_memory().numpy()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        eng.encode_fields(Fh, Vm, mdiag, wl.M_MEAN)
+    e2e_value = n * 2 / (time.perf_counter() - t0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_bw = peaks.get("hbm_gbs", 6650.0)
+    gbps = in_bytes * steps / (ms / 1e3) / 1e9
+    flops = 2.0 * n * cfg.d_m * cfg.r_m
+    line = {
+        "metric": ENC_METRIC, "value": value, "unit": "fields/s", "n_gpus": world, "steps": steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / steps, "higher_is_better": True,
+        "timing": "CUDA events on the launch stream around each encode call", "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 products, f64 accumulation (FMA pipe)", "data": "synthetic",
+        "config": {"workload": "enc", "description": f"cold KLE encoder on c4 field shapes: d_m={cfg.d_m}, "
+                   f"r_m={cfg.r_m}, {n} fields per step ({in_bytes / 1e6:.0f} MB > L2; c4's full set is 18.8 GB)",
+                   "fields_per_step": n, "parallelism": "dp1"},
+        "l2": "inputs larger than L2 (589 MB per step)",
+        "e2e": {"value": e2e_value, "unit": "fields/s", "h2d_bytes_per_step": in_bytes,
+                "d2h_bytes_per_step": 0, "api": "Engine.encode_fields (host fields in; m_r stays on the device)"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak_bw, "unit": "GB/s", "frac": gbps / peak_bw,
+                     "traffic": None, "kernel": "gemm_simt_kernel<EpiAccum64> (split-K over d_m)",
+                     "algorithmic_bytes_per_step": in_bytes,
+                     "fp32_tflops": flops * steps / (ms / 1e3) / 1e12,
+                     "note": "algorithmic bytes = the fields read once; the kernel is FMA-pipe bound "
+                             "(2 n d_m r_m flops), not HBM bound"},
+        "cpu_baseline": None, "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def main():
     args = parse()
+    if args.config == "enc":
+        if args.impl == "reference" or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            print(json.dumps({"impl": args.impl, "unavailable": "enc is a single-GPU setup benchmark of this repo only"}))
+            return
+        import torch
+        torch.cuda.set_device(0)
+        run_encoder(args, 0, 1, 0)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -567,7 +662,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, secs = cpu_reference_rate(cfg, args.seed, args.cpu_samples, reps=1)
-        cpu = {"value": rate, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+        cpu = {"value": rate, "unit": UNIT, "cores": cpu_cores(), "cpu_model": cpu_model(), "kind": "port",
                "sample": f"{args.cpu_samples} samples of {cfg.name} in the reference evaluator's 512-sample "
                          f"chunks, forward-mode z-Jacobian (oracle port, fp64 numpy BLAS), all of the "
                          f"workload's risks ({secs:.1f} s)"}

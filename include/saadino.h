@@ -128,6 +128,14 @@ int sdn_set_tracking(sdn_handle* h, const float* c, double q0);
 int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubias,
                     const float* Mdiag, const float* u_target);
 
+/* The same with a general sparse state mass M in CSR (indptr: d_u + 1 int64,
+ * indices: nnz int32 columns, data: nnz values; host pointers) -- the
+ * reference's q_tracking takes any scipy sparse target.M (riskopt.py:103-108),
+ * e.g. the consistent P1 mass of fem.py:119-126 with lumped=False. */
+int sdn_set_decoder_csr(sdn_handle* h, int64_t d_u, const float* U, const float* ubias,
+                        const int64_t* indptr, const int32_t* indices, const float* data,
+                        const float* u_target);
+
 /* Encoded samples m_r (n x r_m row-major).  on_device != 0: device pointer.
  * global_offset = index of row 0 in the global sample set (CVaR tie-break). */
 int sdn_set_samples(sdn_handle* h, const float* m_r, int64_t n, int64_t global_offset,

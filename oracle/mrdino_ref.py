@@ -230,9 +230,16 @@ def tracking_form(U: np.ndarray, ubias: np.ndarray, Mdiag: np.ndarray,
     """pod.py:104-110 for a diagonal (lumped) mass: c = U^T M (b - u_t),
     q0 = ||b - u_t||_M^2.  Exact only when U^T M U = I (pod.py:46-48)."""
     shift = np.asarray(ubias, np.float64) - np.asarray(u_target, np.float64)
-    Mdiag = np.asarray(Mdiag, np.float64)
-    return ReducedForm(c=np.asarray(U, np.float64).T @ (Mdiag * shift),
-                       q0=float(shift @ (Mdiag * shift)))
+    ms = _mass_apply(Mdiag, shift)
+    return ReducedForm(c=np.asarray(U, np.float64).T @ ms, q0=float(shift @ ms))
+
+
+def _mass_apply(M, x: np.ndarray) -> np.ndarray:
+    """x M for rows x (M symmetric): M a 1-D lumped diagonal or a scipy sparse
+    matrix (the reference's target.M, riskopt.py:103-108)."""
+    if hasattr(M, "tocsr"):
+        return np.asarray((M.tocsr().astype(np.float64) @ np.atleast_2d(x).T).T).reshape(np.shape(x))
+    return x * np.asarray(M, np.float64)
 
 
 def decoded_qoi(phi: np.ndarray, U: np.ndarray, ubias: np.ndarray, Mdiag: np.ndarray,
@@ -242,7 +249,7 @@ def decoded_qoi(phi: np.ndarray, U: np.ndarray, ubias: np.ndarray, Mdiag: np.nda
     phi = np.atleast_2d(np.asarray(phi, np.float64))
     U = np.asarray(U, np.float64)
     diff = phi @ U.T + np.asarray(ubias, np.float64) - np.asarray(u_target, np.float64)
-    mdiff = diff * np.asarray(Mdiag, np.float64)
+    mdiff = _mass_apply(Mdiag, diff)
     return np.sum(diff * mdiff, axis=1), 2.0 * (mdiff @ U)
 
 

@@ -60,6 +60,7 @@ SIGNATURES = {
     "sdn_set_model": (C.c_int, [_P, C.POINTER(_F), C.POINTER(_F), _F, _F, _F, _F]),
     "sdn_set_tracking": (C.c_int, [_P, _F, C.c_double]),
     "sdn_set_decoder": (C.c_int, [_P, C.c_int64, _F, _F, _F, _F]),
+    "sdn_set_decoder_csr": (C.c_int, [_P, C.c_int64, _F, _F, C.POINTER(C.c_int64), C.POINTER(C.c_int32), _F, _F]),
     "sdn_set_samples": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int32]),
     "sdn_encode_fields": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _F, _F, C.c_float, C.c_int64, C.c_int32]),
     "sdn_eval": (C.c_int, [_P, _D, C.POINTER(Risk), C.POINTER(Result), _D, _I64]),

@@ -238,10 +238,12 @@ def build_tracking_form(basis, u_target) -> ReducedTrackingForm:
 @dataclass(frozen=True)
 class Decoder:
     """Full-frame tracking target (riskopt.py:89-109 + pod.py:36-40):
-    u = U phi + bias, Q = (u - u_target)^T diag(M) (u - u_target)."""
+    u = U phi + bias, Q = (u - u_target)^T M (u - u_target).  Mdiag: the
+    lumped mass diagonal (d_u,), or the mass as any scipy sparse matrix
+    (d_u, d_u) -- the reference's TrackingTarget.M."""
     U: np.ndarray
     bias: np.ndarray
-    Mdiag: np.ndarray
+    Mdiag: object
     u_target: np.ndarray
 
 

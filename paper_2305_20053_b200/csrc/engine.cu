@@ -210,7 +210,7 @@ struct sdn_handle {
   const double* ref_tp = nullptr;  // device-side t of the refinement window (set by refine_window)
   // side stream (overlapped exact-CVaR selection in sdn_eval_multi)
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fwd = nullptr, ev_side = nullptr, ev_qoi = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_side = nullptr, ev_qoi = nullptr, ev_idx = nullptr;
   int* x_counts = nullptr;
   int* x_offs = nullptr;
   std::vector<int*> x_rowidx, x_nact;
@@ -920,6 +920,7 @@ int sdn_destroy(sdn_handle* h) {
   if (h->ev_fwd) cudaEventDestroy(h->ev_fwd);
   if (h->ev_side) cudaEventDestroy(h->ev_side);
   if (h->ev_qoi) cudaEventDestroy(h->ev_qoi);
+  if (h->ev_idx) cudaEventDestroy(h->ev_idx);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return SDN_OK;
@@ -1228,6 +1229,14 @@ static int compact_rows(sdn_handle* h, int kind, double t, double eps, const dou
   const int nb = (int)cdiv(std::max<int64_t>(h->n, 1), 1024);
   if (!sel) sel = h->sel;
   ProfScope ps(h, PC_COMPACT, 0.0, 2.0 * (8.0 + 1.0) * h->n);
+  if (kind == RISK_CVAR_EXACT && h->n <= COMPACT1_MAX) {     // a mask, few rows: one block, one launch
+    k_compact_mask1<<<1, 1024, 0, h->stream>>>(h->n, sel, rowidx_out ? rowidx_out : h->rowidx,
+                                               count_out ? count_out : h->n_act_dev);
+    h->launches += 1;
+    CHECK_LAUNCH(h);
+    if (!rowidx_out) h->compacted = true;
+    return SDN_OK;
+  }
   k_flag_count<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, sel, t, eps, tdev, h->counts);
   k_scan_counts<<<1, 32, 0, h->stream>>>(nb, h->counts, h->offs, count_out ? count_out : h->n_act_dev);
   k_compact<<<nb, 1024, 0, h->stream>>>(h->n, kind, h->Q, sel, t, eps, tdev, h->offs,
@@ -1560,6 +1569,7 @@ static int ensure_side(sdn_handle* h) {
   CU(cudaEventCreateWithFlags(&h->ev_fwd, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_qoi, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_idx, cudaEventDisableTiming));
   const int nb1024 = (int)cdiv(h->cap, 1024);
   int rc;
   if ((rc = dalloc(h, &h->x_counts, nb1024))) return rc;
@@ -1666,9 +1676,17 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
       TRY(select_local(h, kks[i], h->band_log + 1 + i, h->x_mask[e], h->x_rowidx[e], h->x_nact[e]));
       masks[i] = h->x_mask[e];
       sel_rows[i] = h->x_rowidx[e];
-      if (want_idx)
-        CU(cudaMemcpyAsync(h->hidx + koff[i], h->x_rowidx[e], sizeof(int) * kks[i], cudaMemcpyDeviceToHost,
-                           h->stream));
+      ++e;
+    }
+    return SDN_OK;
+  };
+  // the selections' indices -> host (on the stream that made them)
+  auto copy_idx = [&]() -> int {
+    if (!want_idx) return SDN_OK;
+    for (int i = 0, e = 0; i < n_risks; ++i) {
+      if (risks[i].kind != SDN_RISK_CVAR_EXACT) continue;
+      CU(cudaMemcpyAsync(h->hidx + koff[i], h->x_rowidx[e], sizeof(int) * kks[i], cudaMemcpyDeviceToHost,
+                         h->stream));
       ++e;
     }
     return SDN_OK;
@@ -1699,6 +1717,11 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     }
     tl_mark(h, 5, h->side);
     CU(cudaEventRecord(h->ev_side, h->side));
+    {                                 // the index copies stay off the path the tail waits for
+      SideScope ss(h);
+      TRY(copy_idx());
+    }
+    CU(cudaEventRecord(h->ev_idx, h->side));
     h->sm_avail = h->num_sms - h->side_sms;
     join = [h]() -> int {
       h->sm_avail = h->num_sms;
@@ -1707,6 +1730,7 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
     };
   } else {
     TRY(select_all());
+    TRY(copy_idx());
   }
   h->risk = risks[0];
   // results -> host-mapped memory: by the sweep's fused tail when it runs,
@@ -1725,6 +1749,7 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   h->sm_avail = h->num_sms;
   h->exp_want = false;
   if (rc) return rc;
+  if (overlap) CU(cudaStreamWaitEvent(h->stream, h->ev_idx, 0));   // the side stream rejoins (index copies done)
   if (!h->exp_done) {
     k_export<<<1, 256, 0, h->stream>>>(h->stats_loc, dst_s, STATS_LEN, h->partial_multi, dst_p, n_risks * plen,
                                        h->band_log, dst_b, n_risks + 1);
@@ -2375,9 +2400,32 @@ int sdn_jacobian_samples(sdn_handle* h, const double* z, int32_t decoded, float*
 }
 
 // decoder: Gram K = U^T M U (split-K fp64), c = U^T M (b - u_t), q0 (host fp64)
+static int set_decoder_impl(sdn_handle* h, int64_t d_u, const float* U, const float* ubias, const float* Mdiag,
+                            const int64_t* indptr, const int32_t* indices, const float* data, const float* u_target);
+
 int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubias, const float* Mdiag,
                     const float* u_target) {
   if (!h || !U || !ubias || !Mdiag || !u_target || d_u < 1) return fail(SDN_ERR_ARG, "bad argument");
+  return set_decoder_impl(h, d_u, U, ubias, Mdiag, nullptr, nullptr, nullptr, u_target);
+}
+
+// general sparse (CSR) state mass, e.g. the consistent P1 mass: the reduced
+// tracking form only needs M U, M (b - u_t): one SpMM and one SpMV at set-up
+int sdn_set_decoder_csr(sdn_handle* h, int64_t d_u, const float* U, const float* ubias, const int64_t* indptr,
+                        const int32_t* indices, const float* data, const float* u_target) {
+  if (!h || !U || !ubias || !indptr || !indices || !data || !u_target || d_u < 1)
+    return fail(SDN_ERR_ARG, "bad argument");
+  if (indptr[0] != 0) return fail(SDN_ERR_ARG, "CSR indptr must start at 0");
+  for (int64_t d = 0; d < d_u; ++d)
+    if (indptr[d + 1] < indptr[d]) return fail(SDN_ERR_ARG, "CSR indptr must be non-decreasing");
+  const int64_t nnz = indptr[d_u];
+  for (int64_t e = 0; e < nnz; ++e)
+    if (indices[e] < 0 || indices[e] >= d_u) return fail(SDN_ERR_ARG, "CSR column index out of range");
+  return set_decoder_impl(h, d_u, U, ubias, nullptr, indptr, indices, data, u_target);
+}
+
+static int set_decoder_impl(sdn_handle* h, int64_t d_u, const float* U, const float* ubias, const float* Mdiag,
+                            const int64_t* indptr, const int32_t* indices, const float* data, const float* u_target) {
   CU(cudaSetDevice(h->device));
   const int r_u = h->r_u;
   // everything on the device: Um = diag(M) U, c and q0 (fixed-order fp64
@@ -2392,25 +2440,44 @@ int sdn_set_decoder(sdn_handle* h, int64_t d_u, const float* U, const float* ubi
   CU(cudaMalloc(&h->U, sizeof(float) * d_u * r_u));
   CU(cudaMalloc(&h->ub, sizeof(float) * d16));      // zero-padded to the tensor-core operand's rows
   CU(cudaMemsetAsync(h->ub, 0, sizeof(float) * d16, h->stream));
-  float *Um = nullptr, *Md = nullptr, *ut = nullptr;
-  double *K64 = nullptr, *q0d = nullptr;
-  auto cleanup = [&]() { cudaFree(Um); cudaFree(Md); cudaFree(ut); cudaFree(q0d); };
-  if (cudaMalloc(&Um, sizeof(float) * d_u * r_u) || cudaMalloc(&Md, sizeof(float) * d_u) ||
-      cudaMalloc(&ut, sizeof(float) * d_u) || cudaMalloc(&q0d, sizeof(double)) ||
-      cudaMalloc(&K64, sizeof(double) * r_u * r_u)) {
+  float *Um = nullptr, *Md = nullptr, *ut = nullptr, *cdat = nullptr;
+  double *K64 = nullptr, *q0d = nullptr, *msv = nullptr;
+  int64_t* cptr = nullptr;
+  int32_t* cidx = nullptr;
+  const int64_t nnz = indptr ? indptr[d_u] : 0;
+  auto cleanup = [&]() {
+    cudaFree(Um); cudaFree(Md); cudaFree(ut); cudaFree(q0d); cudaFree(msv); cudaFree(cptr); cudaFree(cidx);
+    cudaFree(cdat);
+  };
+  if (cudaMalloc(&Um, sizeof(float) * d_u * r_u) || cudaMalloc(&ut, sizeof(float) * d_u) ||
+      cudaMalloc(&q0d, sizeof(double)) || cudaMalloc(&msv, sizeof(double) * d_u) ||
+      cudaMalloc(&K64, sizeof(double) * r_u * r_u) ||
+      (Mdiag ? cudaMalloc(&Md, sizeof(float) * d_u)
+             : (cudaMalloc(&cptr, sizeof(int64_t) * (d_u + 1)) ||
+                cudaMalloc(&cidx, sizeof(int32_t) * std::max<int64_t>(nnz, 1)) ||
+                cudaMalloc(&cdat, sizeof(float) * std::max<int64_t>(nnz, 1))))) {
     cleanup();
     return fail(SDN_ERR_NOMEM, "decoder scratch allocation failed");
   }
   int rc = SDN_OK;
   if (cudaMemcpyAsync(h->U, U, sizeof(float) * d_u * r_u, cudaMemcpyHostToDevice, h->stream) ||
       cudaMemcpyAsync(h->ub, ubias, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream) ||
-      cudaMemcpyAsync(Md, Mdiag, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream) ||
       cudaMemcpyAsync(ut, u_target, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream) ||
-      cudaMemsetAsync(K64, 0, sizeof(double) * r_u * r_u, h->stream))
+      cudaMemsetAsync(K64, 0, sizeof(double) * r_u * r_u, h->stream) ||
+      (Mdiag ? cudaMemcpyAsync(Md, Mdiag, sizeof(float) * d_u, cudaMemcpyHostToDevice, h->stream)
+             : (cudaMemcpyAsync(cptr, indptr, sizeof(int64_t) * (d_u + 1), cudaMemcpyHostToDevice, h->stream) ||
+                cudaMemcpyAsync(cidx, indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, h->stream) ||
+                cudaMemcpyAsync(cdat, data, sizeof(float) * nnz, cudaMemcpyHostToDevice, h->stream))))
     rc = fail(SDN_ERR_CUDA, "decoder upload failed");
   if (rc == SDN_OK) {
-    k_dec_scale<<<(unsigned)std::min<int64_t>(cdiv(d_u * r_u, 256), 4096), 256, 0, h->stream>>>(d_u, r_u, h->U, Md, Um);
-    k_dec_c<<<(unsigned)(r_u + 1), 256, 0, h->stream>>>(d_u, r_u, h->U, h->ub, Md, ut, h->c64dec, q0d);
+    const unsigned rg = (unsigned)std::min<int64_t>(cdiv(d_u, 8), 4096);
+    if (Mdiag)
+      k_dec_scale<<<(unsigned)std::min<int64_t>(cdiv(d_u * r_u, 256), 4096), 256, 0, h->stream>>>(d_u, r_u, h->U, Md, Um);
+    else
+      k_dec_spmm<<<rg, 256, 0, h->stream>>>(d_u, r_u, h->U, cptr, cidx, cdat, Um);
+    k_dec_ms<<<rg, 256, 0, h->stream>>>(d_u, h->ub, ut, Md, cptr, cidx, cdat, msv);
+    h->launches++;
+    k_dec_c<<<(unsigned)(r_u + 1), 256, 0, h->stream>>>(d_u, r_u, h->U, h->ub, msv, ut, h->c64dec, q0d);
     k_f64_to_f32<<<1, 256, 0, h->stream>>>(r_u, h->c64dec, h->cdec);
     h->launches += 3;
     const int64_t kc = 2048;

@@ -270,6 +270,44 @@ k_flag_count(int64_t n, int kind, const double* __restrict__ Q, const uint8_t* _
   }
 }
 
+// ordered compaction of a selection mask in ONE block (n up to 64 K rows):
+// thread t owns the rows [t per, (t + 1) per), counts, a block-wide exclusive
+// scan, then writes its rows' indices in order; total -> *n_act.  Replaces the
+// count / scan / compact chain (three dependent launches) behind the exact-CVaR
+// selection, which sits on the evaluation's critical path at c2.
+constexpr int64_t COMPACT1_MAX = 65536;
+__global__ void __launch_bounds__(1024)
+k_compact_mask1(int64_t n, const uint8_t* __restrict__ sel, int* __restrict__ rowidx, int* __restrict__ n_act) {
+  __shared__ int wsum[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int per = (int)((n + 1023) / 1024);
+  const int64_t lo = min((int64_t)t * per, n), hi = min(lo + per, n);
+  int c = 0;
+  for (int64_t i = lo; i < hi; ++i) c += sel[i] != 0;
+  int inc = c;                                     // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = wsum[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    wsum[lane] = wi - w;                           // exclusive warp offsets
+    if (lane == 31) *n_act = wi;
+  }
+  __syncthreads();
+  int off = wsum[warp] + inc - c;
+  for (int64_t i = lo; i < hi; ++i)
+    if (sel[i] != 0) rowidx[off++] = (int)i;
+}
+
 // exclusive scan of nb block counts (single block); total -> *n_act
 __global__ void k_scan_counts(int nb, const int* __restrict__ counts, int* __restrict__ offs,
                               int* __restrict__ n_act) {
@@ -981,21 +1019,61 @@ __global__ void k_scale_cols(int64_t rows, int r_u, const float* __restrict__ sc
 
 // decoder set-up on the device (pod.py:104-110): Um = diag(M) U (fp32 of the
 // fp64 product, the Gram GEMM's A), and per block j < r_u the fixed-order fp64
-// c_j = sum_d U[d, j] M[d] (b[d] - u_t[d]); block r_u: q0 = sum_d M s^2
+// c_j = sum_d U[d, j] (M s)[d] with s = b - u_t; block r_u: q0 = s.(M s)
 __global__ void k_dec_scale(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restrict__ Mdiag,
                             float* __restrict__ Um) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < d_u * r_u;
        e += (int64_t)gridDim.x * blockDim.x)
     Um[e] = (float)((double)Mdiag[e / r_u] * (double)U[e]);
 }
+// ms = M (b - u_t) in fp64: lumped mass (Mdiag) or a general sparse mass in
+// CSR (riskopt.py:103-108 takes any scipy sparse M; one warp per row, the
+// row's entries in stored order, fixed butterfly)
+__global__ void __launch_bounds__(256)
+k_dec_ms(int64_t d_u, const float* __restrict__ ub, const float* __restrict__ ut, const float* __restrict__ Mdiag,
+         const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, const float* __restrict__ data,
+         double* __restrict__ ms) {
+  if (Mdiag) {
+    for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < d_u; d += (int64_t)gridDim.x * blockDim.x)
+      ms[d] = (double)Mdiag[d] * ((double)ub[d] - (double)ut[d]);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int64_t d = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); d < d_u;
+       d += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    double acc = 0.0;
+    for (int64_t e = indptr[d] + lane; e < indptr[d + 1]; e += 32) {
+      const int32_t q = indices[e];
+      acc += (double)data[e] * ((double)ub[q] - (double)ut[q]);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) ms[d] = acc;
+  }
+}
+// Um = M U for a CSR mass (fp32 of the fp64 row sums): one warp per row, lanes
+// over the r_u columns, the row's entries in stored order
+__global__ void __launch_bounds__(256)
+k_dec_spmm(int64_t d_u, int r_u, const float* __restrict__ U, const int64_t* __restrict__ indptr,
+           const int32_t* __restrict__ indices, const float* __restrict__ data, float* __restrict__ Um) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t d = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); d < d_u;
+       d += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t e0 = indptr[d], e1 = indptr[d + 1];
+    for (int j = lane; j < r_u; j += 32) {
+      double acc = 0.0;
+      for (int64_t e = e0; e < e1; ++e) acc += (double)data[e] * (double)U[(int64_t)indices[e] * r_u + j];
+      Um[d * r_u + j] = (float)acc;
+    }
+  }
+}
 __global__ void __launch_bounds__(256)
 k_dec_c(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restrict__ ub,
-        const float* __restrict__ Mdiag, const float* __restrict__ ut, double* __restrict__ c, double* __restrict__ q0) {
+        const double* __restrict__ msv, const float* __restrict__ ut, double* __restrict__ c, double* __restrict__ q0) {
   __shared__ double sw[8];
   const int j = blockIdx.x;
   double acc = 0.0;
   for (int64_t d = threadIdx.x; d < d_u; d += blockDim.x) {
-    const double sd = (double)ub[d] - (double)ut[d], ms = (double)Mdiag[d] * sd;
+    const double sd = (double)ub[d] - (double)ut[d], ms = msv[d];
     acc += j < r_u ? (double)U[d * r_u + j] * ms : sd * ms;
   }
   acc = warp_sum(acc);

@@ -169,10 +169,28 @@ class Engine:
         check(lib.sdn_set_tracking(self.h, fptr(_f32(_padcols(np.asarray(c, float), self.r_u4))), float(q0)),
               "sdn_set_tracking")
 
-    def set_decoder(self, U, ubias, Mdiag, u_target):
+    def set_decoder(self, U, ubias, M, u_target):
+        """M: the state mass -- a 1-D array (lumped / diagonal mass) or any scipy
+        sparse matrix (the reference's TrackingTarget.M, riskopt.py:89-109)."""
         U = _f32(_padcols(np.asarray(U, np.float32), self.r_u4))
         self.d_u = U.shape[0]
-        check(lib.sdn_set_decoder(self.h, U.shape[0], fptr(U), fptr(_f32(ubias)), fptr(_f32(Mdiag)),
+        if hasattr(M, "tocsr"):
+            A = M.tocsr()
+            if A.shape != (self.d_u, self.d_u):
+                raise ValueError("mass matrix must be (d_u, d_u)")
+            A.sort_indices()
+            ip = np.ascontiguousarray(A.indptr, dtype=np.int64)
+            ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+            dv = _f32(A.data)
+            check(lib.sdn_set_decoder_csr(self.h, self.d_u, fptr(U), fptr(_f32(ubias)),
+                                          ip.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          ix.ctypes.data_as(C.POINTER(C.c_int32)), fptr(dv),
+                                          fptr(_f32(u_target))), "sdn_set_decoder_csr")
+            return
+        Mdiag = _f32(M)
+        if Mdiag.ndim != 1 or Mdiag.shape[0] != self.d_u:
+            raise ValueError("a dense mass must be the (d_u,) diagonal; pass a scipy sparse matrix otherwise")
+        check(lib.sdn_set_decoder(self.h, U.shape[0], fptr(U), fptr(_f32(ubias)), fptr(Mdiag),
                                   fptr(_f32(u_target))), "sdn_set_decoder")
 
     def set_samples(self, m_r, global_offset: int = 0):
@@ -196,11 +214,18 @@ class Engine:
         self.global_offset = int(global_offset)
 
     def encode_fields(self, m, Vm, Mdiag, m_mean: float, global_offset: int = 0):
-        a = _f32(m)
+        """m: (n, d_m) nodal fields -- a numpy array, or a torch CUDA tensor on
+        this device (fields already resident in HBM); Vm, Mdiag: host arrays."""
         Vm = _f32(_padcols(np.asarray(Vm, np.float32), self.r_m4))
-        check(lib.sdn_encode_fields(self.h, a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1], fptr(Vm),
-                                    fptr(_f32(Mdiag)), float(m_mean), int(global_offset), 0), "sdn_encode_fields")
-        self.n = a.shape[0]
+        if hasattr(m, "data_ptr") and getattr(m, "is_cuda", False):
+            t = m.contiguous().float()
+            n, d_m, ptr, dev = t.shape[0], t.shape[1], C.c_void_p(t.data_ptr()), 1
+        else:
+            a = _f32(m)
+            n, d_m, ptr, dev = a.shape[0], a.shape[1], a.ctypes.data_as(C.c_void_p), 0
+        check(lib.sdn_encode_fields(self.h, ptr, n, d_m, fptr(Vm), fptr(_f32(Mdiag)), float(m_mean),
+                                    int(global_offset), dev), "sdn_encode_fields")
+        self.n = n
         self.global_offset = int(global_offset)
 
     # -- evaluation ----------------------------------------------------------------

@@ -144,6 +144,25 @@ def grid_lumped_mass(nx: int, ny: int) -> np.ndarray:
     return (count.ravel() * (0.5 / (nx * ny)) / 3.0)
 
 
+def grid_consistent_mass(nx: int, ny: int):
+    """Consistent (non-lumped) P1 mass on the same mesh as a scipy CSR matrix
+    (fem.py:119-126 with lumped=False): per triangle |T|/12 (1 + delta_ab).
+    The full-frame QoI accepts it through Engine.set_decoder (a sparse M)."""
+    import scipy.sparse as sp
+    n00 = (np.arange(ny)[:, None] * (nx + 1) + np.arange(nx)[None, :]).ravel()
+    n10, n01, n11 = n00 + 1, n00 + nx + 1, n00 + nx + 2
+    tris = np.concatenate([np.stack([n00, n10, n11], 1), np.stack([n00, n11, n01], 1)])   # (2 nx ny, 3)
+    loc = (0.5 / (nx * ny)) / 12.0 * (np.ones((3, 3)) + np.eye(3))
+    rows = np.repeat(tris, 3, axis=1).ravel()
+    cols = np.tile(tris, (1, 3)).ravel()
+    vals = np.tile(loc.ravel(), tris.shape[0])
+    n = (nx + 1) * (ny + 1)
+    M = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    M.sum_duplicates()
+    M.sort_indices()
+    return M
+
+
 def grid_coords(nx: int, ny: int) -> np.ndarray:
     xs = np.linspace(0.0, 1.0, nx + 1)
     ys = np.linspace(0.0, 1.0, ny + 1)

@@ -140,6 +140,19 @@ def main():
         out[f"train_W{l}"], out[f"train_b{l}"] = W, b
     out["train_in_scale"], out["train_out_mean"], out["train_out_std"] = (
         model.input_scale, model.output_mean, model.output_std)
+    # --- full-frame tracking with a general sparse mass (riskopt.py:89-109): the
+    # consistent P1 mass (fem.py:119-126, lumped=False).  Drawn last so that every
+    # earlier vector keeps its value.
+    from ouukit.riskopt import TrackingTarget, q_tracking
+    mesh8 = build_mesh(8, 6)
+    Mc = assemble_mass(mesh8, lumped=False).tocsr()
+    Mc.sort_indices()
+    tgt = g.normal(size=mesh8.d)
+    us = g.normal(size=(4, mesh8.d))
+    vals, grads = zip(*(q_tracking(u, TrackingTarget(u_target=tgt, M=Mc)) for u in us))
+    out.update(cm_indptr=Mc.indptr.astype(np.int64), cm_indices=Mc.indices.astype(np.int32), cm_data=Mc.data,
+               cm_target=tgt, cm_states=us, cm_values=np.array(vals), cm_grads=np.array(grads),
+               cm_shape=np.array([8, 6]))
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays, {os.path.getsize(OUT)} bytes")
 

@@ -113,6 +113,38 @@ def test_forward_batch_and_jacobian_rowwise_z(act, residual):
     assert _rel(J, Jo) <= RTOL
 
 
+@pytest.mark.parametrize("gemm", ["simt", "tc"])
+def test_decoded_frame_sparse_consistent_mass(gemm):
+    """Full-frame QoI with a general sparse mass (riskopt.py:103-108 takes any
+    scipy sparse target.M): the consistent P1 mass instead of the lumped
+    diagonal -- value, gradient and exact-CVaR indices vs the float64 oracle."""
+    p = _problem("c1", 256, with_decoder=True)
+    M = wl.grid_consistent_mass(32, 32)
+    assert M.shape[0] == p.U.shape[0] and (M != M.T).nnz == 0 and M.nnz > 5 * M.shape[0]
+    M32 = M.astype(np.float32)
+    eng = _engine(p, gemm)
+    eng.set_decoder(p.U, p.ubias, M32, p.u_target)
+    m = ref.as_oracle(p)
+    dec = (p.U, p.ubias, M32, p.u_target)
+    for risk, kw in ((ref.Risk("meanvar", beta=0.5, alpha=1e-2), dict(kind="meanvar", beta=0.5)),
+                     (ref.Risk("cvar_exact", beta=0.9, alpha=1e-2), dict(kind="cvar_exact", beta=0.9))):
+        o = ref.risk_and_grad(m, p.m_r, p.z, risk, decoded=dec)
+        r = eng.eval(p.z, alpha=1e-2, qoi="decoded", **kw)
+        assert abs(r.value - o["value"]) <= RTOL * abs(o["value"])
+        assert _rel(r.grad_z, o["grad_z"]) <= RTOL
+        if risk.kind == "cvar_exact":
+            assert np.array_equal(np.sort(r.idx), np.sort(o["idx"]))
+    # the lumped mass gives a different answer: the sparse path is really used
+    eng.set_decoder(p.U, p.ubias, np.asarray(M.sum(axis=1)).ravel().astype(np.float32), p.u_target)
+    r_l = eng.eval(p.z, "meanvar", beta=0.5, alpha=1e-2, qoi="decoded")
+    o_c = ref.risk_and_grad(m, p.m_r, p.z, ref.Risk("meanvar", beta=0.5, alpha=1e-2), decoded=dec)
+    assert abs(r_l.value - o_c["value"]) > 10 * RTOL * abs(o_c["value"])
+    # malformed CSR is refused
+    import scipy.sparse as sp
+    with pytest.raises(ValueError):
+        eng.set_decoder(p.U, p.ubias, sp.identity(7, format="csr"), p.u_target)
+
+
 def test_decoded_frame_and_jacobian():
     p = _problem("c1", 128, with_decoder=True)
     eng = _engine(p)
