@@ -20,6 +20,7 @@
 #include "gemm_tc.cuh"
 #include "refine.cuh"
 #include "train.cuh"
+#include "small.cuh"
 
 // SMs left to side-stream work (the exact-CVaR selection + fp64 band
 // refinement, a cooperative kernel on this many blocks) while the main stream's
@@ -252,6 +253,11 @@ struct sdn_handle {
   TcOperand lift_in;            // lift: phi split (rows x r_u)
   float *jmr = nullptr, *jz = nullptr, *jX = nullptr, *jJ = nullptr;
   bool no_refine = false;       // env SDN_NO_REFINE=1 (precision studies)
+  // small sample sets: the whole evaluation in one launch (small.cuh)
+  bool no_small = false;        // env SDN_NO_SMALL=1
+  std::vector<float*> WT;       // transposed fp32 weights (w[l] x w[l+1]) of the one-launch path
+  double* small_part = nullptr; // per-CTA partials
+  int64_t small_gen = -1;       // handle generation the transposes were taken at
   bool ref_trace = false;       // env SDN_REFINE_TRACE=1
   // H1 training state (sdn_train_*), allocated on first use
   struct Train {
@@ -856,6 +862,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
       cudaHostAlloc((void**)&h->hpart, sizeof(double) * h->plen(), cudaHostAllocMapped) != cudaSuccess)
     return bail(fail(SDN_ERR_NOMEM, "cudaHostAlloc failed"));
   { const char* e = getenv("SDN_NO_REFINE"); h->no_refine = e && e[0] == '1'; }
+  { const char* e = getenv("SDN_NO_SMALL"); h->no_small = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_OVERLAP"); h->no_overlap = e && e[0] == '1'; }
   { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
@@ -1639,6 +1646,124 @@ int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* r
   return sdn_eval_multi(h, z, risk, 1, res, grad_z, risk->kind == SDN_RISK_CVAR_EXACT ? cvar_idx : nullptr);
 }
 
+// ---- small sample sets (BASELINE config 1): one launch per evaluation (small.cuh)
+constexpr int64_t SMALL_MAX_ROWS = 1024;
+__global__ void k_transpose32(int rows, int cols, const float* __restrict__ A, float* __restrict__ AT) {
+  __shared__ float tile[32][33];
+  const int x = blockIdx.x * 32 + threadIdx.x, y0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8)
+    if (x < cols && y0 + j < rows) tile[j][threadIdx.x] = A[(int64_t)(y0 + j) * cols + x];
+  __syncthreads();
+  const int tx = blockIdx.y * 32 + threadIdx.x, ty0 = blockIdx.x * 32;
+  for (int j = threadIdx.y; j < 32; j += 8)
+    if (tx < rows && ty0 + j < cols) AT[(int64_t)(ty0 + j) * rows + tx] = tile[threadIdx.x][j];
+}
+// rows per CTA: 4 (more CTAs, shorter FFMA chains: measured faster) or 8 (SDN_SMALL_RB=8)
+static int small_rb() {
+  static const int rb = getenv("SDN_SMALL_RB") && atoi(getenv("SDN_SMALL_RB")) == 8 ? 8 : 4;
+  return rb;
+}
+static bool small_eligible(const sdn_handle* h, const sdn_risk* risks, int n_risks) {
+  if (h->no_small || h->prof || h->gemm != SDN_GEMM_AUTO || h->n < 1 || h->n > SMALL_MAX_ROWS) return false;
+  if (h->L < 1 || h->L > SM_MAXL || h->act == ACT_SOFTMAX || h->r_m > SM_MAXW) return false;
+  for (int l = 0; l < h->L; ++l)
+    if (h->w[l + 1] > SM_MAXW) return false;
+  if (small_smem_bytes(small_rb(), h->L - 1) > TC_SMEM_MAX - 2048) return false;
+  for (int i = 0; i < n_risks; ++i) {
+    if (risks[i].kind != SDN_RISK_MEAN && risks[i].kind != SDN_RISK_MEANVAR) return false;
+    if (risks[i].qoi != SDN_QOI_REDUCED) return false;
+  }
+  return h->have_form;
+}
+// buffers and weight transposes (outside any graph capture)
+static int ensure_small(sdn_handle* h) {
+  int rc;
+  if (!h->small_part) {
+    if ((rc = dalloc(h, &h->small_part, (size_t)cdiv(std::max<int64_t>(h->cap, 1), 4) * (2 * h->h1 + 4)))) return rc;
+  }
+  if ((int)h->WT.size() < h->L) {
+    h->WT.resize(h->L, nullptr);
+    for (int l = 0; l < h->L; ++l) {
+      const int K = l == 0 ? h->r_m : h->w[l];
+      if ((rc = dalloc(h, &h->WT[l], (size_t)K * h->w[l + 1]))) return rc;
+    }
+    h->small_gen = -1;
+  }
+  if (h->small_gen != h->gen) {
+    for (int l = 0; l < h->L; ++l) {
+      const int K = l == 0 ? h->r_m : h->w[l], N = h->w[l + 1];
+      k_transpose32<<<dim3((unsigned)cdiv(K, 32), (unsigned)cdiv(N, 32)), dim3(32, 8), 0, h->stream>>>(N, K, h->W[l],
+                                                                                                h->WT[l]);
+    }
+    h->launches += h->L;
+    CHECK_LAUNCH(h);
+    h->small_gen = h->gen;
+    static unsigned attr = 0;                      // per device
+    if (!(attr & (1u << (h->device & 31)))) {
+      CU(cudaFuncSetAttribute(k_small_eval<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::min<size_t>(small_smem_bytes(4, SM_MAXL - 1), TC_SMEM_MAX - 2048)));
+      CU(cudaFuncSetAttribute(k_small_eval<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::min<size_t>(small_smem_bytes(8, SM_MAXL - 1), TC_SMEM_MAX - 2048)));
+      attr |= 1u << (h->device & 31);
+    }
+  }
+  return SDN_OK;
+}
+static int enqueue_small(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks) {
+  CU(cudaSetDevice(h->device));
+  h->risk = risks[0];
+  h->fwd_risk = risks[0];
+  h->seed_fused = false;
+  h->selected = false;
+  h->compacted = false;
+  h->qr_valid = false;
+  h->fwd_done = false;                             // the layer buffers are not written on this path
+  h->shift = h->q0;
+  TRY(upload_z(h, z, risks, n_risks));
+  SmallArgs a{};
+  a.L = h->L; a.n = (int)h->n; a.r_m = h->r_m; a.d_z = h->d_z; a.r_u = h->r_u; a.h1 = h->h1; a.act = h->act;
+  a.R = n_risks; a.plen = h->plen();
+  a.w[0] = h->r_m;
+  for (int l = 0; l < h->L; ++l) {
+    a.w[l + 1] = h->w[l + 1];
+    a.res[l] = (l > 0 && l < h->L - 1 && h->res[l]) ? 1 : 0;
+    a.W[l] = h->W[l]; a.WT[l] = h->WT[l]; a.b[l] = h->b[l];
+  }
+  a.MR = h->MR; a.Pz = h->Pz; a.z = h->zdev; a.omean = h->omean; a.ostd = h->ostd; a.c = h->c;
+  a.q0 = h->q0; a.shift = h->shift;
+  for (int i = 0; i < n_risks; ++i) { a.kind[i] = risks[i].kind; a.beta[i] = risks[i].beta; }
+  a.Q = h->Q; a.part = h->small_part; a.PzT = h->PzT; a.stats = h->stats_loc; a.out = h->partial_multi;
+  a.counter = h->red_counter + 3;
+  CU(cudaHostGetDevicePointer((void**)&a.hstats, h->hstats, 0));
+  CU(cudaHostGetDevicePointer((void**)&a.hpart, h->hpart_multi, 0));
+  CU(cudaHostGetDevicePointer((void**)&a.hband, h->hband, 0));
+  a.nband = n_risks + 1;
+  static const bool trace = getenv("SDN_SMALL_TRACE") != nullptr;     // study switch: phase stamps, printed per call
+  static unsigned long long* tbuf = nullptr;
+  if (trace) {
+    if (!tbuf) CU(cudaMalloc(&tbuf, 16 * sizeof(unsigned long long)));
+    a.trace = tbuf;
+  }
+  const int rb = small_rb();
+  tl_mark(h, 1);
+  if (rb == 8)
+    k_small_eval<8><<<(unsigned)cdiv(h->n, 8), SM_THREADS, small_smem_bytes(8, h->L - 1), h->stream>>>(a);
+  else
+    k_small_eval<4><<<(unsigned)cdiv(h->n, 4), SM_THREADS, small_smem_bytes(4, h->L - 1), h->stream>>>(a);
+  h->launches++;
+  CHECK_LAUNCH(h);
+  if (trace && !h->use_graphs) {
+    unsigned long long hb[9];
+    CU(cudaMemcpyAsync(hb, tbuf, sizeof(hb), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    fprintf(stderr, "k_small_eval: CTA 0 [start 0 | inputs %.1f | forward %.1f | Q+seeds %.1f | sweep %.1f | partials %.1f] "
+            "last CTA [ticket %.1f | combined %.1f | end %.1f] us\n", (hb[1] - hb[0]) / 1e3, (hb[2] - hb[0]) / 1e3,
+            (hb[3] - hb[0]) / 1e3, (hb[4] - hb[0]) / 1e3, (hb[5] - hb[0]) / 1e3, (hb[6] - hb[0]) / 1e3,
+            (hb[7] - hb[0]) / 1e3, (hb[8] - hb[0]) / 1e3);
+  }
+  return SDN_OK;
+}
+
 // several risk functionals from ONE forward pass and ONE reverse sweep (e.g.
 // c2: mean+variance and exact CVaR).  At most one smoothed-CVaR entry (its
 // t/eps feed the forward-time moments and window refinement).
@@ -1652,6 +1777,7 @@ int sdn_eval(sdn_handle* h, const double* z, const sdn_risk* risk, sdn_result* r
 static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks, bool want_idx,
                          const std::vector<int64_t>& kks, const std::vector<int64_t>& koff, int smooth,
                          bool any_grad) {
+  if (small_eligible(h, risks, n_risks)) return enqueue_small(h, z, risks, n_risks);
   const int plen = h->plen();
   int n_exact = 0;
   bool dense = false;
@@ -1842,6 +1968,7 @@ int sdn_eval_multi_launch(sdn_handle* h, const double* z, const sdn_risk* risks,
   }
   if (dense && n_exact > 0) TRY(ensure_side(h));
   TRY(ensure_sweep(h, *h->sw, n_risks));
+  if (small_eligible(h, risks, n_risks)) TRY(ensure_small(h));
   // graph path (z and every risk's t are per-call graph parameters, staged
   // in pinned memory); not when profiling / tracing (host timers and syncs)
   const bool use_graph = h->use_graphs && !h->prof && !h->ref_trace;

@@ -412,6 +412,55 @@ def test_odd_widths_run_zero_padded(act, golden):
         assert _rel(r.grad_z, o[1]) <= RTOL
 
 
+@pytest.mark.parametrize("act,residual,hidden", [("elu", True, (256, 256, 256)), ("tanh", False, (64, 96)),
+                                                  ("softplus", True, (40, 40)), ("identity", False, ())])
+def test_small_set_one_launch_path(act, residual, hidden):
+    """Small sample sets with mean / mean + beta var risks run the whole
+    evaluation in ONE launch (csrc/small.cuh): value, gradient and per-sample Q
+    vs the float64 oracle and vs the layer-by-layer SIMT path, for a sample
+    count that does not fill the last CTA, several risks at once, and a second
+    control through the same graph."""
+    from paper_2305_20053_b200.api import NetworkSpec, init_model
+    g = np.random.default_rng(11)
+    spec = NetworkSpec(r_m=64, d_z=25, r_u=64, hidden=hidden, activation=act, residual=residual)
+    model = init_model(spec, seed=4, input_scale=g.uniform(0.5, 2, 64), output_mean=g.normal(size=64),
+                       output_std=g.uniform(0.5, 2, 64))
+    for b in model.biases:
+        b[:] = 0.1 * g.normal(size=b.shape)
+    n = 251
+    m_r = g.normal(size=(n, 64)).astype(np.float32)
+    c = g.normal(size=64).astype(np.float32)
+    form = ref.ReducedForm(c.astype(np.float64), 1.5)
+    risks = [dict(kind="mean", alpha=1e-2), dict(kind="meanvar", beta=0.5, alpha=1e-2),
+             dict(kind="meanvar", beta=2.0, alpha=0.0)]
+    engs = {}
+    for gemm in ("auto", "simt"):
+        e = Engine(model, max_samples=n, gemm=gemm)
+        e.set_tracking(c, 1.5)
+        e.set_samples(m_r)
+        engs[gemm] = e
+    for z in (g.uniform(-1, 1, 25), g.uniform(-2, 2, 25)):
+        Qo, Go = ref.evaluate_reverse(ref.as_oracle(model), m_r, z, form=form)
+        l0 = engs["auto"].kernel_launches()
+        out = engs["auto"].eval_multi(z, risks)
+        assert engs["auto"].kernel_launches() - l0 <= 1 + len(model.weights)   # (first call: + the weight transposes)
+        slow = engs["simt"].eval_multi(z, risks)
+        for r, s, d in zip(out, slow, risks):
+            o = ref.saa_objective(Qo, Go, z, ref.Risk(d["kind"], beta=d.get("beta", 0.95), alpha=d["alpha"]))
+            assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+            assert _rel(r.grad_z, o[1]) <= RTOL
+            assert abs(r.value - s.value) <= 1e-5 * abs(s.value) and _rel(r.grad_z, s.grad_z) <= 1e-4
+            assert r.n_samples == n
+        np.testing.assert_allclose(engs["auto"].last_q(), Qo, rtol=1e-4)
+    # one launch per evaluation once the graph exists; the forced paths and CVaR risks take the general route
+    l0 = engs["auto"].kernel_launches()
+    engs["auto"].eval_multi(z, risks)
+    assert engs["auto"].kernel_launches() - l0 == 1
+    r = engs["auto"].eval(z, "cvar_exact", beta=0.9)
+    o = ref.saa_objective(Qo, Go, z, ref.Risk("cvar_exact", beta=0.9))
+    assert abs(r.value - o[0]) <= RTOL * abs(o[0]) and np.array_equal(np.sort(r.idx), np.sort(o[3]))
+
+
 @pytest.mark.parametrize("gemm", ["simt", "tc"])
 def test_decoded_frame_cvar_risks(gemm):
     """Full-frame QoI (riskopt.py:103-108, Gram form on the device) with both
