@@ -220,8 +220,8 @@ struct sdn_handle {
   std::vector<int64_t*> x_gidx; // global indices of each kept selection (ascending)
   std::vector<int64_t> x_gcap;
   // short tail (k_sel_colsum_sl + k_finalize_export): sliced selected-row sums, finalise + export in one launch
-  bool tail_fuse = false;       // env SDN_TAIL_FUSE=1 enables (measured: no gain at c2, profiles/README.md)
-  bool tail_export = false;     // env SDN_TAIL_EXPORT=1: the finalise kernel's last block also exports (measured slower)
+  bool tail_fuse = true;        // env SDN_NO_TAIL_FUSE=1 disables (c2: 0.3117 -> 0.3086 ms with the direct host writes)
+  bool tail_export = false;     // env SDN_TAIL_EXPORT=1: the finalise kernel writes the host results itself (no export launch)
   bool exp_want = false, exp_done = false;   // enqueue_multi asks the tail to export; the tail says it did
   double *exp_s = nullptr, *exp_p = nullptr; // host-mapped destinations (stats, partials)
   int* exp_b = nullptr;                      // ... band log
@@ -867,7 +867,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   { const char* e = getenv("SDN_REFINE_TRACE"); h->ref_trace = e && e[0] == '1'; }
   { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
   { const char* e = getenv("SDN_TIMELINE"); h->tl_on = e && e[0] == '1'; }
-  h->tail_fuse = getenv("SDN_TAIL_FUSE") && getenv("SDN_TAIL_FUSE")[0] == '1';
+  h->tail_fuse = !(getenv("SDN_NO_TAIL_FUSE") && getenv("SDN_NO_TAIL_FUSE")[0] == '1');
   h->tail_export = getenv("SDN_TAIL_EXPORT") && getenv("SDN_TAIL_EXPORT")[0] == '1';
   h->side_sms = std::max(1, std::min(SDN_SIDE_SMS_DEFAULT, h->num_sms / 4));
   { const char* e = getenv("SDN_SIDE_SMS");
@@ -1463,7 +1463,8 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   CHECK_LAUNCH(h);
   // short tail: sliced sums over the selected rows, one finalise + export launch
   const int S = std::max(1, std::min(8, h->crb));
-  const bool short_tail = h->tail_fuse && !h->prof && !u0;
+  const bool short_tail = h->tail_fuse && !h->prof && !u0;      // sliced selected-row sums
+  const bool fin_export = (h->tail_export || short_tail) && !h->prof && !u0;   // finalise writes the host results itself
   FinArgs fa{};
   for (int r = 0; r < R; ++r) fa.risk[r] = FinRisk{part + (int64_t)r * plane, nrb_fin, 1.0};
   if (defer) {
@@ -1487,10 +1488,10 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
     }
   }
   { ProfScope ps(h, PC_FINAL, 0.0, 8.0 * nrb_fin * h->h1 * R);
-  if (short_tail) {
+  if (fin_export) {
     fa.h1 = h->h1; fa.d_z = h->d_z; fa.plen = h->plen();
     fa.PzT = h->PzT; fa.vsum = h->vsum; fa.out = partials; fa.counter = h->red_counter + 2;
-    if (h->tail_export && h->exp_want && partials == h->partial_multi) {
+    if (h->exp_want && partials == h->partial_multi) {
       fa.stats = stats_dev; fa.hstats = h->exp_s; fa.nstats = STATS_LEN;
       fa.hpart = h->exp_p; fa.npart = h->exp_np;
       fa.band = h->band_log; fa.hband = h->exp_b; fa.nband = h->exp_nb;
@@ -1790,7 +1791,8 @@ static int enqueue_multi(sdn_handle* h, const double* z, const sdn_risk* risks, 
   // stream -- the sweep's unit seeds never read Q, so the reverse chain starts
   // right behind the forward; Q and the moments join before the last GEMM
   const bool overlap = dense && n_exact > 0 && !h->prof && !h->no_overlap;
-  const bool qoi_side = overlap && smooth < 0 && any_grad && h->tcw.enabled;
+  static const bool qoi_main = getenv("SDN_QOI_MAIN") && getenv("SDN_QOI_MAIN")[0] == '1';   // study switch
+  const bool qoi_side = overlap && smooth < 0 && any_grad && h->tcw.enabled && !qoi_main;
   TRY(eval_forward(h, z, &risks[smooth >= 0 ? smooth : 0], h->stats_loc, any_grad, risks, n_risks,
                    smooth >= 0 ? smooth : 0, dense && any_grad, qoi_side));
   std::vector<const uint8_t*> masks(n_risks, nullptr);

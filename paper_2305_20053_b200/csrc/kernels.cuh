@@ -84,6 +84,16 @@ __global__ void k_build_x(int64_t n, int r_m, int d_z, int ldx, const float* __r
 //   reduced: Q = phi.phi + 2 phi.c + q0
 //   gram   : Q = phi.(K phi) + 2 phi.c + q0  (decoded frame, K = U^T M U)
 // accumulated in fp64; plus per-block fp64 partial moments.
+// the warp's moments: lanes 0..3 each accumulated every fourth row of the
+// warp; added in lane order (k_qoi and k_moments share this order)
+SDN_DEV void qoi_lane_combine(const double (&acc)[6], double* dst, int lane) {
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const double a1 = __shfl_sync(0xffffffffu, acc[f], 1), a2 = __shfl_sync(0xffffffffu, acc[f], 2),
+                 a3 = __shfl_sync(0xffffffffu, acc[f], 3);
+    if (lane == 0) dst[f] = ((acc[f] + a1) + a2) + a3;
+  }
+}
 // One warp per row, grid-stride, four rows in flight per warp (their 16-byte
 // loads are issued before the first fp64 reduction); block partials in fixed
 // order (rows of a warp are accumulated in ascending order).
@@ -135,12 +145,10 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) s[u] = warp_sum(s[u]);
-    if (lane == 0) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + u * stride;
-        if (i >= n) break;
-        const double q = s[u] + q0;
+    if (lane < 4) {                      // lane u finishes row u (the smoothed-plus terms are fp64 exp/log work)
+      const int64_t i = i0 + lane * stride;
+      if (i < n) {
+        const double q = (lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3]) + q0;
         Q[i] = q;
         double qs = q - shift, x = q - t;
         double d1 = splus_d1_d(x, eps);
@@ -149,8 +157,7 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
       }
     }
   }
-  if (lane == 0)
-    for (int f = 0; f < 6; ++f) sp[warp][f] = acc[f];
+  qoi_lane_combine(acc, sp[warp], lane);
   __syncthreads();
   if (threadIdx.x < 6) {
     double s = 0.0;
@@ -195,17 +202,18 @@ k_moments(int64_t n, const double* __restrict__ Q, double shift, double t, doubl
   __shared__ double sp[8][6];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  // same row -> (block, warp) assignment and per-lane-0 order as k_qoi
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
-    if (lane == 0) {
+  // same row -> (block, warp, lane) assignment and order as k_qoi
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t i0 = (int64_t)blockIdx.x * 8 + warp; i0 < n; i0 += 4 * stride) {
+    const int64_t i = i0 + lane * stride;
+    if (lane < 4 && i < n) {
       double q = Q[i], qs = q - shift, x = q - t;
       double d1 = splus_d1_d(x, eps);
       acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
       acc[3] += splus_d(x, eps); acc[4] += d1; acc[5] += (d1 > 0.0) ? 1.0 : 0.0;
     }
   }
-  if (lane == 0)
-    for (int f = 0; f < 6; ++f) sp[warp][f] = acc[f];
+  qoi_lane_combine(acc, sp[warp], lane);
   __syncthreads();
   if (threadIdx.x < 6) {
     double s = 0.0;
@@ -587,10 +595,10 @@ k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __re
 // sums over the k selected rows of the stored u are taken by row slices
 // (k_sel_colsum_sl: S x w/32 blocks instead of w/32; 13.7 -> ~4 us at c2), and
 // one kernel finalises every risk from its own list of partial rows and --
-// its last block -- writes the results to host-mapped memory (k_finalize_export:
-// what k_finalize_multi + k_export did in two dependent launches).  A variant
-// that did all of it in one launch with a single finishing block was slower
-// (the 2 x d_z projections of length h1 on one SM: +14 us), profiles/README.md.
+// every block writing its own outputs -- puts the results in host-mapped memory
+// (k_finalize_export: what k_finalize_multi + k_export did in two dependent
+// launches).  Variants that finished in ONE block (all projections, or only
+// the export behind an atomic ticket) were slower, profiles/README.md.
 // out[s][c] = sum over slice s of the selected rows of u[rows[j], c] (fp64,
 // fixed order: thread rows j = lo + y, lo + y + 32, ..., then the 32 row groups
 // in order); the value partials vs = (sum_j Q[rows[j]], k) by block (0, 0)
@@ -633,18 +641,19 @@ struct FinArgs {
   const double* PzT;
   const double* vsum;
   double* out;           // [R][plen]
-  int* counter;          // last-block export (self re-arming)
-  const double* stats; double* hstats; int nstats;      // export (hstats null: none)
+  int* counter;          // (unused)
+  const double* stats; double* hstats; int nstats;      // export to host-mapped memory (hstats null: none)
   double* hpart; int npart;
   const int* band; int* hband; int nband;
 };
 // per-risk finalisation (blockIdx.y = risk): A = scale * sum_b part[b][:];
-// out_r[k] = sum_c PzT[k][c] A[c]; out_r[d_z], out_r[d_z+1] = vsum[2r], vsum[2r+1];
-// then the last block exports stats / partials / band log
+// out_r[k] = sum_c PzT[k][c] A[c]; out_r[d_z], out_r[d_z+1] = vsum[2r], vsum[2r+1].
+// With hstats set every block also writes its outputs straight to the
+// host-mapped result buffers (block (0, 0): the moments and the band log too),
+// so no export kernel follows and no block waits for another.
 __global__ void __launch_bounds__(256)
 k_finalize_export(const FinArgs a) {
   extern __shared__ double A[];
-  __shared__ bool s_last;
   const int r = blockIdx.y, h1 = a.h1, d_z = a.d_z;
   const FinRisk& fr = a.risk[r];
   for (int c = threadIdx.x; c < h1; c += blockDim.x) {
@@ -655,31 +664,28 @@ k_finalize_export(const FinArgs a) {
   }
   __syncthreads();
   double* o = a.out + (int64_t)r * a.plen;
+  double* ho = a.hstats ? a.hpart + (int64_t)r * a.plen : nullptr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int k = blockIdx.x * nw + warp; k < d_z; k += gridDim.x * nw) {
     double s = 0.0;
 #pragma unroll 8
     for (int c = lane; c < h1; c += 32) s += __ldg(a.PzT + (int64_t)k * h1 + c) * A[c];
     s = warp_sum(s);
-    if (lane == 0) o[k] = s;
+    if (lane == 0) {
+      o[k] = s;
+      if (ho) ho[k] = s;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    o[d_z] = a.vsum[2 * r];
-    o[d_z + 1] = a.vsum[2 * r + 1];
+    const double v0 = a.vsum[2 * r], v1 = a.vsum[2 * r + 1];
+    o[d_z] = v0;
+    o[d_z + 1] = v1;
+    if (ho) { ho[d_z] = v0; ho[d_z + 1] = v1; }
   }
-  if (!a.hstats) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(a.counter, 1) == (int)(gridDim.x * gridDim.y) - 1;
+  if (a.hstats && blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int i = threadIdx.x; i < a.nstats; i += blockDim.x) a.hstats[i] = a.stats[i];
+    for (int i = threadIdx.x; i < a.nband; i += blockDim.x) a.hband[i] = a.band[i];
   }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int i = threadIdx.x; i < a.nstats; i += blockDim.x) a.hstats[i] = a.stats[i];
-  for (int i = threadIdx.x; i < a.npart; i += blockDim.x) a.hpart[i] = __ldcg(a.out + i);
-  for (int i = threadIdx.x; i < a.nband; i += blockDim.x) a.hband[i] = a.band[i];
-  if (threadIdx.x == 0) *a.counter = 0;
 }
 
 // histogram increment (plain shared atomics measured faster than warp
