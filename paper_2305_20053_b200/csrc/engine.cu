@@ -1294,10 +1294,18 @@ static int select_local(sdn_handle* h, int64_t k, int* band_count = nullptr, uin
   const bool refine = band_count && !h->no_refine;
   if (!mask) mask = h->sel;
   double* Qs = sel_q(h);
+  // study switch SDN_TOPK_SMEM=1: the top-k by the single-CTA shared-memory radix select (no grid
+  // barriers), then the cooperative kernel only for the band refinement and the reselection
+  static const bool topk_smem = getenv("SDN_TOPK_SMEM") && getenv("SDN_TOPK_SMEM")[0] == '1';
+  if (topk_smem && h->n <= TOPK_SMEM_MAX && refine && h->ref_ok) {
+    TRY(launch_topk(h, h->n, k, Qs, nullptr, mask, h->thr_dev));
+    TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, band_count, mask, Qs, 0, true));
+  } else {
   // one cooperative launch: top-k, then (refine) the fp64 threshold band and
   // the reselection among it
   TRY(refine_band(h, RISK_BAND_EXACT, 0.0, 0.0, h->risk.qoi == SDN_QOI_DECODED, band_count, mask, Qs, k,
                   refine));
+  }
   TRY(compact_rows(h, RISK_CVAR_EXACT, 0.0, 1.0, nullptr, count_out, mask, rowidx_out));
   h->selected = true;
   return SDN_OK;

@@ -399,6 +399,7 @@ constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
 template <int RING, bool BWD = false>
 struct EpiWarps {
   static constexpr int EW = !RING ? TC_EPI_WARPS : BWD ? TC_RING_EW_BWD : TC_RING_EW;
+  static_assert(EW % 4 == 0 && EW >= 4, "epilogue warps come in lane-quarter groups of four (CS = 16 EW / 4)");
   static constexpr int THREADS = 32 * (4 + EW);
 };
 
@@ -411,10 +412,13 @@ constexpr uint32_t TC_BAR_BYTES = 1024;       // mbarriers + TMEM slot
 constexpr uint32_t SDN_CHAIN_BIAS_BYTES = 4096;  // persistent forward chain: room for every layer's bias (8 KB with the ring's 4 KB)
 // (reverse-sweep rings, BWD: 4-KB slots holding the residual-gradient and
 // act' input tiles, reused for the G and split outputs; no bias)
-template <int BN, int RING = 0, bool BWD = false, int CG = 1>
+// (BK: K columns per mainloop stage -- 32 = 64-byte swizzle rows, the default;
+// 64 = 128-byte swizzle rows, chain kernels only, SDN_CHAIN_BK=64)
+template <int BN, int RING = 0, bool BWD = false, int CG = 1, int BK = TC_BK>
 struct TcCfg {
-  static constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr uint32_t B_BYTES = (BN / CG) * TC_BK * 2;   // CTA pairs: each CTA holds half of B's rows
+  static constexpr int BK_ = BK;
+  static constexpr uint32_t A_BYTES = TC_BM * BK * 2;
+  static constexpr uint32_t B_BYTES = (BN / CG) * BK * 2;   // CTA pairs: each CTA holds half of B's rows
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr uint32_t EPI_WARP =
       !RING ? TC_EPI_WARP_BYTES : BWD ? (uint32_t)RING * 4096u : (uint32_t)RING * 2048u + 2048u;
@@ -1709,6 +1713,12 @@ SDN_DEV void chain_tile(const Args& ca, int g, int& l, int& mbt, int& nb) {
   nb = t - mbt * nt;
 }
 
+// K-major operand descriptor for a stage of BK columns: 64-byte (BK = 32) or 128-byte (BK = 64) swizzle rows
+template <int BK>
+SDN_DEV uint64_t sdesc_bk(uint32_t saddr) {
+  if constexpr (BK == 64) return tcx::sdesc_k128(saddr);
+  else return tcx::sdesc_k64(saddr);
+}
 template <int BN, int CG, int STAGES, class C, class Args>
 SDN_DEV void chain_produce(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* empty, int rank, int t0, int ts,
                            int tpl, int total, int n_tiles) {
@@ -1725,18 +1735,18 @@ SDN_DEV void chain_produce(const Args& ca, uint8_t* smem, uint64_t* full, uint64
       tcx::fence_proxy_async_global();
     }
     chain_stamp(ti, 1);
-    const int kblocks = (ly.K + TC_BK - 1) / TC_BK;
+    const int kblocks = (ly.K + C::BK_ - 1) / C::BK_;
     for (int kb = 0; kb < kblocks; ++kb) {
       tcx::mbar_wait(&empty[stage], phase ^ 1);
       uint8_t* st = smem + stage * C::STAGE_BYTES;
       if constexpr (CG == 1) {
         tcx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-        tcx::tma_load_3d(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
-        tcx::tma_load_3d(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN, 0);
+        tcx::tma_load_3d(st, &ca.a[l], &full[stage], kb * C::BK_, mb * TC_BM, 0);
+        tcx::tma_load_3d(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * C::BK_, nb * BN, 0);
       } else {
         if (rank == 0) tcx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-        tcx::tma_load_3d_pair(st, &ca.a[l], &full[stage], kb * TC_BK, mb * TC_BM, 0);
-        tcx::tma_load_3d_pair(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * TC_BK, nb * BN + rank * (BN / 2), 0);
+        tcx::tma_load_3d_pair(st, &ca.a[l], &full[stage], kb * C::BK_, mb * TC_BM, 0);
+        tcx::tma_load_3d_pair(st + 2 * C::A_BYTES, &ca.b[l], &full[stage], kb * C::BK_, nb * BN + rank * (BN / 2), 0);
       }
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
@@ -1752,7 +1762,7 @@ SDN_DEV void chain_mma(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* 
   for (int g = t0, ti = 0; g < total; g += ts, ++ti) {
     int l, mbt, nb;
     chain_tile(ca, g, l, mbt, nb);
-    const int kblocks = (ca.ly[l].K + TC_BK - 1) / TC_BK;
+    const int kblocks = (ca.ly[l].K + C::BK_ - 1) / C::BK_;
     tcx::mbar_wait(&tempty[acc], acc_phase ^ 1);
     tcx::fence_after();
     chain_stamp(ti, 2);
@@ -1762,11 +1772,11 @@ SDN_DEV void chain_mma(const Args& ca, uint8_t* smem, uint64_t* full, uint64_t* 
       tcx::fence_after();
       const uint32_t base = tcx::smem_u32(smem + stage * C::STAGE_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < TC_BK / 16; ++kk) {
-        const uint64_t ah = tcx::sdesc_k64(base + kk * 32);
-        const uint64_t al = tcx::sdesc_k64(base + C::A_BYTES + kk * 32);
-        const uint64_t bh = tcx::sdesc_k64(base + 2 * C::A_BYTES + kk * 32);
-        const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
+      for (int kk = 0; kk < C::BK_ / 16; ++kk) {
+        const uint64_t ah = sdesc_bk<C::BK_>(base + kk * 32);
+        const uint64_t al = sdesc_bk<C::BK_>(base + C::A_BYTES + kk * 32);
+        const uint64_t bh = sdesc_bk<C::BK_>(base + 2 * C::A_BYTES + kk * 32);
+        const uint64_t bl = sdesc_bk<C::BK_>(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
         if constexpr (CG == 1) {
           tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
           tcx::mma_bf16(d, ah, bl, idesc, 1);
@@ -1819,10 +1829,10 @@ SDN_DEV void chain_publish(const Args& ca, uint32_t* pubc, int rank, int t0, int
 
 // shared-memory plan of the chain kernel: STAGES mainloop stages, EW
 // epilogue warps with RING 2-KB slots + a 2-KB D tile each, every layer's bias
-template <int BN, int RING, int CG, int EW>
+template <int BN, int RING, int CG, int EW, int BK = TC_BK>
 struct ChainCfg {
   static_assert(EW % 4 == 0 && EW >= 4, "epilogue warps come in lane-quarter groups of four");
-  using C = TcCfg<BN, RING, false, CG>;
+  using C = TcCfg<BN, RING, false, CG, BK>;
   static constexpr uint32_t WB = (uint32_t)RING * 2048u + 2048u;
   static constexpr uint32_t EPI_BYTES = EW * WB;
   static constexpr uint32_t BIAS_BYTES = 4096u + SDN_CHAIN_BIAS_BYTES;
@@ -1832,10 +1842,10 @@ struct ChainCfg {
   static constexpr int THREADS = 32 * (4 + EW);
 };
 
-template <int BN, int RING, int CG, int EW>
-__global__ void __launch_bounds__(ChainCfg<BN, RING, CG, EW>::THREADS, 1)
+template <int BN, int RING, int CG, int EW, int BK = TC_BK>
+__global__ void __launch_bounds__(ChainCfg<BN, RING, CG, EW, BK>::THREADS, 1)
 tc_fwd_chain_kernel(const __grid_constant__ FwdChainArgs ca) {
-  using CC = ChainCfg<BN, RING, CG, EW>;
+  using CC = ChainCfg<BN, RING, CG, EW, BK>;
   using C = typename CC::C;
   constexpr int BMT = TC_BM * CG;
   constexpr int STAGES = CC::STAGES;
@@ -2045,10 +2055,10 @@ struct BwdChainArgs {
   CUtensorMap rmap[SDN_CHAIN_MAX], dmap[SDN_CHAIN_MAX];    // residual gradient, act' inputs
   CUtensorMap gmap[SDN_CHAIN_MAX], smap[SDN_CHAIN_MAX];    // G and split(u) outputs
 };
-template <int BN, int RING, int CG, int EW>
+template <int BN, int RING, int CG, int EW, int BK = TC_BK>
 struct BwdChainCfg {
   static_assert(EW % 4 == 0 && EW >= 4, "epilogue warps come in lane-quarter groups of four");
-  using C = TcCfg<BN, RING, true, CG>;
+  using C = TcCfg<BN, RING, true, CG, BK>;
   static constexpr uint32_t WB = (uint32_t)RING * 4096u;
   static constexpr uint32_t EPI_BYTES = EW * WB;
   static constexpr int FIT = (int)((TC_SMEM_MAX - EPI_BYTES - 1024 - TC_BAR_BYTES) / C::STAGE_BYTES);
@@ -2057,10 +2067,10 @@ struct BwdChainCfg {
   static constexpr int THREADS = 32 * (4 + EW);
 };
 
-template <int BN, int RING, int CG, int EW>
-__global__ void __launch_bounds__(BwdChainCfg<BN, RING, CG, EW>::THREADS, 1)
+template <int BN, int RING, int CG, int EW, int BK = TC_BK>
+__global__ void __launch_bounds__(BwdChainCfg<BN, RING, CG, EW, BK>::THREADS, 1)
 tc_bwd_chain_kernel(const __grid_constant__ BwdChainArgs ca) {
-  using CC = BwdChainCfg<BN, RING, CG, EW>;
+  using CC = BwdChainCfg<BN, RING, CG, EW, BK>;
   using C = typename CC::C;
   constexpr int STAGES = CC::STAGES;
   constexpr int CS = 16 * (EW / 4);
@@ -2232,11 +2242,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
 // 3-D bf16 pair map over a split operand: (cols x rows x {hi, lo}) with row
 // pitch ld elements and lo at a fixed offset from hi; box = 32 x box_rows x 2
 // (64 B swizzle): one TMA load brings a k-block's hi and lo tiles
-static int tc_map(TcWeights& t, const TcOperand& op, int64_t rows, int cols, int box_rows, CUtensorMap* out) {
+static int tc_map(TcWeights& t, const TcOperand& op, int64_t rows, int cols, int box_rows, CUtensorMap* out,
+                  int bk = TC_BK) {
   const __nv_bfloat16* base = op.hi;
   const int ld = op.ld;
   const int64_t pair = (int64_t)((const char*)op.lo - (const char*)op.hi);
-  auto key = std::make_tuple((const void*)base, rows, cols * 65536 + box_rows, (int)ld);
+  auto key = std::make_tuple((const void*)base, rows, cols * 65536 + box_rows + (bk == TC_BK ? 0 : 32768), (int)ld);
   auto it = t.maps.find(key);
   if (it != t.maps.end()) { *out = it->second; return 0; }
   auto fn = tc_encode_fn();
@@ -2245,11 +2256,11 @@ static int tc_map(TcWeights& t, const TcOperand& op, int64_t rows, int cols, int
   CUtensorMap m;
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 2};
   cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)pair};
-  cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows, 2};
+  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)box_rows, 2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -2;
   t.maps[key] = m;
   *out = m;
@@ -2405,8 +2416,9 @@ struct RingOk<EpiBwdSum> {
   static bool ok(const EpiBwdSum& e, int) { return !e.rowidx && e.D; }
 };
 // reverse-sweep ring depth (0 = register-prefetch epilogue); SDN_BWD_RING overrides.
-// 3 on the 128-column reverse tiles (two mainloop stages left): reverse GEMMs
-// 0.185 -> 0.171 ms per c2 step against depth 2 with four stages
+// 3 on the 128-column reverse tiles: with 8 epilogue warps (TC_RING_EW_BWD) depths 2
+// and 3 both keep four mainloop stages; depth 3 wins on the epilogue's prefetch
+// distance (reverse GEMMs 0.185 -> 0.171 ms per c2 step)
 static int g_tc_bwd_ring = getenv("SDN_BWD_RING") ? atoi(getenv("SDN_BWD_RING")) : 3;
 
 template <int BN, class Epi, int RING, int CG = 1>
@@ -2563,11 +2575,11 @@ struct FwdChainLayerHost {
   const float* b2 = nullptr;
 };
 static bool g_tc_chain = !(getenv("SDN_NO_CHAIN") && getenv("SDN_NO_CHAIN")[0] == '1');
-template <int CG, int EW>
+template <int CG, int EW, int BK = TC_BK>
 static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N, int act,
                           const std::vector<FwdChainLayerHost>& ls) {
   constexpr int BN = 256, RING = 2;
-  using CC = ChainCfg<BN, RING, CG, EW>;
+  using CC = ChainCfg<BN, RING, CG, EW, BK>;
   constexpr uint32_t SMEM = CC::SMEM;
   static_assert(CC::STAGES >= 2 && SMEM <= TC_SMEM_MAX, "chain shared memory budget");
   grid = CG * std::max(1, grid / CG);
@@ -2584,8 +2596,8 @@ static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
     FwdChainLayer& y = ca.ly[l];
     const int Nl = x.N ? x.N : N;
     if (Nl % 16) return -1;
-    if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l]) ||
-        tc_map(t, *x.B, Nl, x.K, BN / CG, &ca.b[l]))
+    if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l], BK) ||
+        tc_map(t, *x.B, Nl, x.K, BN / CG, &ca.b[l], BK))
       return -2;
     if (x.D && tc_out_map(t, x.D, false, M, Nl, Nl, &ca.dmap[l])) return -3;
     if (x.S && tc_out_map_pair(t, x.S->hi, x.S->lo, M, Nl, x.S->ld, &ca.smap[l])) return -3;
@@ -2609,7 +2621,7 @@ static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1u << (dev & 31)))) {
-    cudaFuncSetAttribute(tc_fwd_chain_kernel<BN, RING, CG, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tc_fwd_chain_kernel<BN, RING, CG, EW, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)SMEM);
     attr_set |= 1u << (dev & 31);
   }
@@ -2635,7 +2647,7 @@ static int tc_fwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
     cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * tn, st);
     cudaMemcpyToSymbolAsync(g_chain_trace, &tbuf, sizeof(tbuf), 0, cudaMemcpyHostToDevice, st);
   }
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_fwd_chain_kernel<BN, RING, CG, EW>, ca);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_fwd_chain_kernel<BN, RING, CG, EW, BK>, ca);
   if (trace) {                                    // dump: grid, tiles per layer, then stamps
     std::vector<unsigned long long> hb(tn);
     cudaMemcpyAsync(hb.data(), tbuf, sizeof(unsigned long long) * tn, cudaMemcpyDeviceToHost, st);
@@ -2660,7 +2672,12 @@ static bool g_chain_pairs = !(getenv("SDN_CHAIN_PAIRS") && getenv("SDN_CHAIN_PAI
 static int g_chain_ew = getenv("SDN_CHAIN_EW") ? atoi(getenv("SDN_CHAIN_EW")) : 12;
 static int tc_fwd_chain(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N, int act,
                         const std::vector<FwdChainLayerHost>& ls) {
+  // 128-byte swizzle rows, 64 K columns per stage (two 64-KB stages instead of four 32-KB ones): the
+  // forward chain's TMA row requests halve -- c2 0.3081 -> 0.3024 ms, c3 +1-2% (SDN_CHAIN_BK=32: the old
+  // stages; the reverse chain measured slower with 64, SDN_BWD_CHAIN_BK=64)
+  static const bool bk64 = !(getenv("SDN_CHAIN_BK") && atoi(getenv("SDN_CHAIN_BK")) == 32);
   if (g_chain_pairs && grid >= 2) {
+    if (g_chain_ew == 12 && bk64) return tc_fwd_chain_k<2, 12, 64>(t, st, grid, M, N, act, ls);
     if (g_chain_ew == 12) return tc_fwd_chain_k<2, 12>(t, st, grid, M, N, act, ls);
     return tc_fwd_chain_k<2, 16>(t, st, grid, M, N, act, ls);
   }
@@ -2682,11 +2699,11 @@ struct BwdChainLayerHost {
   int K;
   TcFlags fl;
 };
-template <int CG>
+template <int CG, int BK = TC_BK>
 static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N,
                           const std::vector<BwdChainLayerHost>& ls) {
   constexpr int BN = 256, RING = 3, EW = 8;
-  using CC = BwdChainCfg<BN, RING, CG, EW>;
+  using CC = BwdChainCfg<BN, RING, CG, EW, BK>;
   static_assert(CC::STAGES >= 2 && CC::SMEM <= TC_SMEM_MAX, "reverse chain shared memory budget");
   grid = CG * std::max(1, grid / CG);
   const int L = (int)ls.size();
@@ -2699,8 +2716,8 @@ static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
   for (int l = 0; l < L; ++l) {
     const BwdChainLayerHost& x = ls[l];
     BwdChainLayer& y = ca.ly[l];
-    if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l]) ||
-        tc_map(t, *x.B, N, x.K, BN / CG, &ca.b[l]))
+    if (tc_map(t, *x.A, std::max<int64_t>(M, 1), x.K, TC_BM, &ca.a[l], BK) ||
+        tc_map(t, *x.B, N, x.K, BN / CG, &ca.b[l], BK))
       return -2;
     if (x.R && tc_out_map(t, x.R, false, M, N, N, &ca.rmap[l])) return -3;
     if (tc_out_map(t, x.D, false, M, N, x.ldD, &ca.dmap[l])) return -3;
@@ -2717,7 +2734,7 @@ static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_set & (1u << (dev & 31)))) {
-    cudaFuncSetAttribute(tc_bwd_chain_kernel<BN, RING, CG, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tc_bwd_chain_kernel<BN, RING, CG, EW, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)CC::SMEM);
     attr_set |= 1u << (dev & 31);
   }
@@ -2735,12 +2752,14 @@ static int tc_bwd_chain_k(TcWeights& t, cudaStream_t st, int grid, int64_t M, in
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CG > 1 ? 2 : 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_chain_kernel<BN, RING, CG, EW>, ca);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_chain_kernel<BN, RING, CG, EW, BK>, ca);
   return (e == cudaSuccess && cudaGetLastError() == cudaSuccess) ? 0 : -4;
 }
 static bool g_bwd_chain = !(getenv("SDN_NO_BWD_CHAIN") && getenv("SDN_NO_BWD_CHAIN")[0] == '1');
 static int tc_bwd_chain(TcWeights& t, cudaStream_t st, int grid, int64_t M, int N,
                         const std::vector<BwdChainLayerHost>& ls) {
+  static const bool bk64 = getenv("SDN_BWD_CHAIN_BK") && atoi(getenv("SDN_BWD_CHAIN_BK")) == 64;   // study switch
+  if (g_chain_pairs && grid >= 2 && bk64) return tc_bwd_chain_k<2, 64>(t, st, grid, M, N, ls);
   if (g_chain_pairs && grid >= 2) return tc_bwd_chain_k<2>(t, st, grid, M, N, ls);
   return tc_bwd_chain_k<1>(t, st, grid, M, N, ls);
 }
