@@ -317,7 +317,7 @@ static int dalloc(sdn_handle* h, T** p, size_t count) {
 
 // grow-only scratch slot (stream-ordered reuse: callers are serialised on the
 // handle's stream; a grown buffer is freed after a stream sync)
-enum ScratchSlot { SCR_A = 0, SCR_B, SCR_C, SCR_D, SCR_E, SCR_F };
+enum ScratchSlot { SCR_A = 0, SCR_B, SCR_C, SCR_D, SCR_E, SCR_F, SCR_G, SCR_H };
 template <class T>
 static int scratch(sdn_handle* h, int slot, size_t count, T** p) {
   const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
@@ -1498,7 +1498,7 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
   { ProfScope ps(h, PC_FINAL, 0.0, 8.0 * nrb_fin * h->h1 * R);
   if (fin_export) {
     fa.h1 = h->h1; fa.d_z = h->d_z; fa.plen = h->plen();
-    fa.PzT = h->PzT; fa.vsum = h->vsum; fa.out = partials; fa.counter = h->red_counter + 2;
+    fa.PzT = h->PzT; fa.vsum = h->vsum; fa.out = partials;
     if (h->exp_want && partials == h->partial_multi) {
       fa.stats = stats_dev; fa.hstats = h->exp_s; fa.nstats = STATS_LEN;
       fa.hpart = h->exp_p; fa.npart = h->exp_np;
@@ -2723,7 +2723,7 @@ int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, con
   TRY(scratch(h, SCR_C, (size_t)d_m, &Md));
   TRY(scratch(h, SCR_D, (size_t)std::max<int64_t>(n, 1) * r_m, &acc));
   TRY(scratch(h, SCR_E, (size_t)r_m, &bd));
-  if (!on_device) TRY(scratch(h, SCR_F, (size_t)rows_chunk * d_m, &mb));
+  if (!on_device) TRY(scratch(h, SCR_F, (size_t)std::max<int64_t>(rows_chunk, std::min<int64_t>(n, 16384)) * d_m, &mb));
   CU(cudaMemcpyAsync(Vraw, Vm, sizeof(float) * d_m * r_m, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(Md, Mdiag, sizeof(float) * d_m, cudaMemcpyHostToDevice, h->stream));
   k_dec_scale<<<(unsigned)std::min<int64_t>(cdiv(d_m * r_m, 256), 4096), 256, 0, h->stream>>>(d_m, r_m, Vraw, Md, V);
@@ -2731,14 +2731,58 @@ int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, con
   h->launches += 2;
   CU(cudaMemsetAsync(acc, 0, sizeof(double) * std::max<int64_t>(n, 1) * r_m, h->stream));
   const int64_t kc = 1024;
-  for (int64_t s = 0; s < n; s += rows_chunk) {
-    const int64_t rows = std::min(rows_chunk, n - s);
+  // Tensor cores (default when the handle has them and the shard fills a few
+  // tiles; SDN_ENC_TC=0: the FMA-pipe GEMM).  Both operands are split into
+  // three bf16 planes (24 mantissa bits); four bf16x3 passes over plane pairs,
+  //   (a0,a1)x(b0,b1), (a1,a2)x(b1,b2), (a2,0)x(b0,0), (a0,0)x(b2,0),
+  // give every product term a_i b_j with i + j <= 2 -- the fp32 product to
+  // ~2^-24, which the input whitening downstream needs --
+  // with fp32 accumulation in TMEM over a 1024-column K chunk and fp64
+  // accumulation across chunks, as on the FMA path.
+  static const bool enc_tc_off = getenv("SDN_ENC_TC") && getenv("SDN_ENC_TC")[0] == '0';
+  const bool enc_tc = !enc_tc_off && h->tcw.enabled && h->gemm != SDN_GEMM_SIMT && r_m % 16 == 0 && n >= 512 &&
+                      tc_encode_fn() != nullptr;
+  const int64_t ldk = cdiv(d_m, kc) * kc;           // plane columns (zero-padded to whole K chunks)
+  __nv_bfloat16 *PA = nullptr, *PB = nullptr;
+  int64_t tc_rows = 0;
+  if (enc_tc) {
+    tc_rows = cdiv(std::min<int64_t>(n, 16384), 128) * 128;      // up to 16384 rows per pass: 256 tiles per launch
+    TRY(scratch(h, SCR_G, (size_t)4 * tc_rows * ldk, &PA));
+    TRY(scratch(h, SCR_H, (size_t)4 * r_m * ldk, &PB));
+    const int64_t pb = (int64_t)r_m * ldk;
+    CU(cudaMemsetAsync(PB, 0, sizeof(__nv_bfloat16) * 4 * pb, h->stream));
+    CU(cudaMemsetAsync(PA + 3 * tc_rows * ldk, 0, sizeof(__nv_bfloat16) * tc_rows * ldk, h->stream));
+    k_split3_transpose<<<dim3((unsigned)cdiv(ldk, 32), (unsigned)cdiv(r_m, 32)), dim3(32, 8), 0, h->stream>>>(
+        d_m, r_m, V, ldk, PB, PB + pb, PB + 2 * pb);
+    h->launches++;
+    CHECK_LAUNCH(h);
+  }
+  for (int64_t s = 0; s < n; s += (enc_tc ? tc_rows : rows_chunk)) {
+    const int64_t rows = std::min(enc_tc ? tc_rows : rows_chunk, n - s);
     const float* src = m + s * d_m;
     if (!on_device) {
       CU(cudaMemcpyAsync(mb, src, sizeof(float) * rows * d_m, cudaMemcpyHostToDevice, h->stream));
       src = mb;
     }
     ProfScope ps(h, PC_OTHER, 2.0 * rows * r_m * d_m, 4.0 * rows * d_m);
+    if (enc_tc) {
+      const int64_t pa = tc_rows * ldk, pb = (int64_t)r_m * ldk;
+      k_split3<<<(unsigned)std::min<int64_t>(cdiv(rows * ldk, 256), 16384), 256, 0, h->stream>>>(
+          rows, (int)d_m, d_m, src, ldk, PA, PA + pa, PA + 2 * pa);
+      h->launches++;
+      CHECK_LAUNCH(h);
+      const int pass[4][4] = {{0, 1, 0, 1}, {1, 2, 1, 2}, {2, 3, 0, 3}, {0, 3, 2, 3}};   // planes: A hi, A lo, B hi, B lo
+      for (int64_t k0 = 0; k0 < ldk; k0 += kc) {
+        for (int q = 0; q < 4; ++q) {
+          TcOperand ta, tb;
+          ta.hi = PA + pass[q][0] * pa + k0; ta.lo = PA + pass[q][1] * pa + k0; ta.ld = (int)ldk; ta.rows = rows;
+          tb.hi = PB + pass[q][2] * pb + k0; tb.lo = PB + pass[q][3] * pb + k0; tb.ld = (int)ldk; tb.rows = r_m;
+          TRY((gemm<false, true>(h, rows, nullptr, r_m, (int)kc, src + k0, d_m, V + k0 * r_m, r_m,
+                                 EpiAccum64{acc + s * r_m, (int64_t)r_m}, &tb, &ta, 1)));
+        }
+      }
+      continue;
+    }
     for (int64_t k0 = 0; k0 < d_m; k0 += kc) {
       const int kl = (int)std::min(kc, d_m - k0);
       TRY((gemm<false, false>(h, rows, nullptr, r_m, kl, src + k0, d_m, V + k0 * r_m, r_m,

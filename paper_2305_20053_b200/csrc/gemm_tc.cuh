@@ -639,6 +639,38 @@ struct TileEpi {
   }
 };
 
+// fp64 accumulation of a K chunk's fp32 result (the encoder's split-K sum):
+// the row's 16 doubles are loaded together, added and stored -- one global
+// round trip per chunk (the generic functor path read-modify-writes four
+// columns at a time: four dependent round trips)
+template <>
+struct TileEpi<EpiAccum64> {
+  using Pre = PreNone;
+  static SDN_DEV void load(const EpiAccum64&, const TileRows&, int, int, int, Pre&) {}
+  static SDN_DEV void chunk(const EpiAccum64& epi, const EpiSmem&, const TileRows& tr, int c0, int N, int lane,
+                            const uint32_t (&v)[16], const Pre&) {
+    const int64_t row = tr.r0 + lane;
+    if (row >= tr.M) return;
+    double* p = epi.C + row * epi.ldc + c0;
+    if (c0 + 16 <= N) {
+      double2 d[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[j] = *reinterpret_cast<const double2*>(p + 2 * j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        d[j].x += (double)__uint_as_float(v[2 * j]);
+        d[j].y += (double)__uint_as_float(v[2 * j + 1]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) *reinterpret_cast<double2*>(p + 2 * j) = d[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < N) p[j] += (double)__uint_as_float(v[j]);
+    }
+  }
+};
+
 // no-op epilogue (mainloop timing in sdn_debug_gemm)
 struct EpiNull {
   SDN_DEV void operator()(int64_t, int, float4) const {}

@@ -641,7 +641,6 @@ struct FinArgs {
   const double* PzT;
   const double* vsum;
   double* out;           // [R][plen]
-  int* counter;          // (unused)
   const double* stats; double* hstats; int nstats;      // export to host-mapped memory (hstats null: none)
   double* hpart; int npart;
   const int* band; int* hband; int nband;
@@ -1090,6 +1089,57 @@ k_dec_c(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restri
     for (int w = 0; w < 8; ++w) t += sw[w];
     if (j < r_u) c[j] = t;
     else *q0 = t;
+  }
+}
+// ---- tensor-core encoder operands: a three-way bf16 split x = p0 + p1 + p2
+// (p0 = bf16(x), p1 = bf16(x - p0), p2 = bf16(x - p0 - p1): 24 mantissa bits,
+// every subtraction exact), planes of ldp columns (columns >= cols zero).
+// With both operands split three ways, the products p_i q_j with i + j <= 2 carry
+// the fp32 product to ~2^-24; four bf16x3 GEMM passes over plane pairs cover
+// them (engine.cu, sdn_encode_fields).
+__global__ void k_split3(int64_t rows, int cols, int64_t ld_src, const float* __restrict__ src, int64_t ldp,
+                         __nv_bfloat16* __restrict__ p0, __nv_bfloat16* __restrict__ p1,
+                         __nv_bfloat16* __restrict__ p2) {
+  const int64_t total = rows * ldp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ldp;
+    const int c = (int)(e - r * ldp);
+    const float x = c < cols ? src[r * ld_src + c] : 0.0f;
+    const __nv_bfloat16 a = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(a);
+    const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(b);
+    p0[e] = a;
+    p1[e] = b;
+    p2[e] = __float2bfloat16_rn(r2);
+  }
+}
+// the same for V (d x r, row-major) transposed: planes hold V^T (r rows of ldp columns)
+__global__ void k_split3_transpose(int64_t d, int r, const float* __restrict__ V, int64_t ldp,
+                                   __nv_bfloat16* __restrict__ p0, __nv_bfloat16* __restrict__ p1,
+                                   __nv_bfloat16* __restrict__ p2) {
+  __shared__ float tile[32][33];
+  const int64_t d0 = (int64_t)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t dd = d0 + i;
+    const int j = j0 + threadIdx.x;
+    tile[i][threadIdx.x] = (dd < d && j < r) ? V[dd * r + j] : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int j = j0 + i;
+    const int64_t dd = d0 + threadIdx.x;
+    if (j < r && dd < ldp) {
+      const float x = tile[threadIdx.x][i];
+      const __nv_bfloat16 a = __float2bfloat16_rn(x);
+      const float r1 = x - __bfloat162float(a);
+      const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+      const int64_t e = (int64_t)j * ldp + dd;
+      p0[e] = a;
+      p1[e] = b;
+      p2[e] = __float2bfloat16_rn(r1 - __bfloat162float(b));
+    }
   }
 }
 // encoder: bias_j = -m_mean sum_d Vmm[d, j] (fixed-order fp64, one block per j)

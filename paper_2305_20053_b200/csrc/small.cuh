@@ -36,7 +36,6 @@ constexpr int SM_MAXL = 8;           // weight matrices
 constexpr int SM_THREADS = 256;
 constexpr int SM_CH = 32;            // matrix rows per chunk
 constexpr int SM_STAGES = 5;         // ring depth (<= 32 KB per stage; 3 stages: 0.83 us per chunk, latency-bound)
-constexpr int SM_MAXCHUNKS = 160;    // 2 x SM_MAXL x (SM_MAXW / SM_CH) + slack
 
 struct SmallArgs {
   unsigned long long* trace;         // optional %globaltimer stamps (SDN_SMALL_TRACE=1): CTA 0 phases, then the last CTA's

@@ -232,6 +232,36 @@ def test_encoder_matches_oracle():
     np.testing.assert_allclose(Q, Qo, rtol=1e-4)
 
 
+@pytest.mark.parametrize("name,n", [("c2", 1024)])
+def test_encoder_tensor_cores_match_oracle(name, n):
+    """The tensor-core encoder (three-way bf16 split of both operands, four
+    bf16x3 passes, fp64 accumulation across K chunks): the encoded samples feed
+    the network through the input whitening 1/sqrt(lambda_j) (x1640 at c2's
+    highest mode), so the check is on the per-sample Q downstream, against the
+    float64 oracle's encode and against the FMA-pipe encoder."""
+    cfg = wl.WORKLOADS[name].with_samples(n)
+    p = wl.make_problem(cfg, seed=0, count=n)
+    psi, lam, mdiag = wl.kl_modes(cfg, 0)
+    m = wl.fields(cfg, 0, 0, n).astype(np.float32)
+    Vm, Md = psi[:, :cfg.r_m].astype(np.float32), mdiag.astype(np.float32)
+    enc = ref.encode(m, Vm, Md, wl.M_MEAN)
+    po = wl.make_problem(cfg, seed=0, count=n)
+    po.m_r = enc.astype(np.float32)
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(po), enc, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    Qs = {}
+    for gemm in ("auto", "simt"):
+        eng = Engine(p, max_samples=n, gemm=gemm)
+        eng.set_tracking(p.c, p.q0)
+        l0 = eng.kernel_launches()
+        eng.encode_fields(m, Vm, Md, wl.M_MEAN)
+        launches = eng.kernel_launches() - l0
+        Qs[gemm], _ = eng.eval_samples(p.z, need_grad=False)
+        np.testing.assert_allclose(Qs[gemm], Qo, rtol=1e-4)
+        if gemm == "auto":      # 4 passes per 1024-column K chunk (+ the splits, scale, bias, finish)
+            assert launches >= 4 * ((cfg.d_m + 1023) // 1024)
+    assert np.max(np.abs(Qs["auto"] - Qs["simt"]) / np.abs(Qs["simt"])) < 5e-5
+
+
 def test_determinism_bitwise():
     p = _problem("c2", 4096)
     eng = _engine(p)
