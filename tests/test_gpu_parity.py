@@ -491,6 +491,33 @@ def test_small_set_one_launch_path(act, residual, hidden):
     assert abs(r.value - o[0]) <= RTOL * abs(o[0]) and np.array_equal(np.sort(r.idx), np.sort(o[3]))
 
 
+@pytest.mark.parametrize("n,d_z", [(1, 5), (7, 40), (1024, 33)])
+def test_small_set_one_launch_edges(n, d_z):
+    """One-launch path at its edges: a single sample, a partly filled CTA, the
+    largest eligible set (1024), and more than 32 controls (the z-bias is summed
+    in blocks of 32 controls)."""
+    from paper_2305_20053_b200.api import NetworkSpec, init_model
+    g = np.random.default_rng(n + d_z)
+    spec = NetworkSpec(r_m=12, d_z=d_z, r_u=8, hidden=(48, 48), activation="elu", residual=True)
+    model = init_model(spec, seed=9, input_scale=g.uniform(0.5, 2, 12), output_mean=g.normal(size=8),
+                       output_std=g.uniform(0.5, 2, 8))
+    m_r = g.normal(size=(n, 12)).astype(np.float32)
+    c = g.normal(size=8).astype(np.float32)
+    z = g.uniform(-1, 1, d_z)
+    eng = Engine(model, max_samples=n)
+    eng.set_tracking(c, 0.5)
+    eng.set_samples(m_r)
+    Qo, Go = ref.evaluate_reverse(ref.as_oracle(model), m_r, z, form=ref.ReducedForm(c.astype(np.float64), 0.5))
+    eng.eval(z, "meanvar", beta=0.5)                 # (first call: weight transposes + graph capture)
+    l0 = eng.kernel_launches()
+    r = eng.eval(z, "meanvar", beta=0.5)
+    assert eng.kernel_launches() - l0 == 1
+    o = ref.saa_objective(Qo, Go, z, ref.Risk("meanvar", beta=0.5))
+    assert abs(r.value - o[0]) <= RTOL * abs(o[0])
+    assert _rel(r.grad_z, o[1]) <= RTOL
+    np.testing.assert_allclose(eng.last_q(), Qo, rtol=1e-4)
+
+
 @pytest.mark.parametrize("gemm", ["simt", "tc"])
 def test_decoded_frame_cvar_risks(gemm):
     """Full-frame QoI (riskopt.py:103-108, Gram form on the device) with both
