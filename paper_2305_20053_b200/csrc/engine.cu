@@ -2733,27 +2733,27 @@ int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, con
   const int64_t kc = 1024;
   // Tensor cores (default when the handle has them and the shard fills a few
   // tiles; SDN_ENC_TC=0: the FMA-pipe GEMM).  Both operands are split into
-  // three bf16 planes (24 mantissa bits); four bf16x3 passes over plane pairs,
-  //   (a0,a1)x(b0,b1), (a1,a2)x(b1,b2), (a2,0)x(b0,0), (a0,0)x(b2,0),
-  // give every product term a_i b_j with i + j <= 2 -- the fp32 product to
-  // ~2^-24, which the input whitening downstream needs --
-  // with fp32 accumulation in TMEM over a 1024-column K chunk and fp64
-  // accumulation across chunks, as on the FMA path.
+  // three bf16 planes (24 mantissa bits); per 1024-column K chunk two launches
+  // (k_split3's layout): pass A, a bf16x3 GEMM over the chunk's segments
+  // (a0;a1)x(b0;b1) and (a1;a2)x(b1;b2); pass B, hi-only products a2 b0 + a0 b2.
+  // Together every term a_i b_j with i + j <= 2 -- the fp32 product to ~2^-24,
+  // which the input whitening downstream needs -- with
+  // fp32 accumulation in TMEM within a launch and fp64 accumulation across
+  // launches, as on the FMA path.
   static const bool enc_tc_off = getenv("SDN_ENC_TC") && getenv("SDN_ENC_TC")[0] == '0';
   const bool enc_tc = !enc_tc_off && h->tcw.enabled && h->gemm != SDN_GEMM_SIMT && r_m % 16 == 0 && n >= 512 &&
                       tc_encode_fn() != nullptr;
-  const int64_t ldk = cdiv(d_m, kc) * kc;           // plane columns (zero-padded to whole K chunks)
-  __nv_bfloat16 *PA = nullptr, *PB = nullptr;
+  const int nch = (int)cdiv(d_m, kc);               // K chunks (planes zero-padded to whole chunks)
+  const int64_t lda = 4 * kc, ldb2 = 2 * kc;          // row pitch inside a chunk (chunk-major planes)
+  __nv_bfloat16 *PA = nullptr, *PB = nullptr, *PB2 = nullptr;
   int64_t tc_rows = 0;
   if (enc_tc) {
-    tc_rows = cdiv(std::min<int64_t>(n, 16384), 128) * 128;      // up to 16384 rows per pass: 256 tiles per launch
-    TRY(scratch(h, SCR_G, (size_t)4 * tc_rows * ldk, &PA));
-    TRY(scratch(h, SCR_H, (size_t)4 * r_m * ldk, &PB));
-    const int64_t pb = (int64_t)r_m * ldk;
-    CU(cudaMemsetAsync(PB, 0, sizeof(__nv_bfloat16) * 4 * pb, h->stream));
-    CU(cudaMemsetAsync(PA + 3 * tc_rows * ldk, 0, sizeof(__nv_bfloat16) * tc_rows * ldk, h->stream));
-    k_split3_transpose<<<dim3((unsigned)cdiv(ldk, 32), (unsigned)cdiv(r_m, 32)), dim3(32, 8), 0, h->stream>>>(
-        d_m, r_m, V, ldk, PB, PB + pb, PB + 2 * pb);
+    tc_rows = cdiv(std::min<int64_t>(n, 16384), 128) * 128;      // up to 16384 rows per pass: 128 256-column tiles per launch
+    TRY(scratch(h, SCR_G, (size_t)nch * tc_rows * lda + 2 * kc, &PA));
+    TRY(scratch(h, SCR_H, (size_t)nch * r_m * (lda + ldb2) + 2 * kc, &PB));
+    PB2 = PB + (int64_t)nch * r_m * lda;
+    k_split3_transpose<<<dim3((unsigned)cdiv((int64_t)nch * kc, 32), (unsigned)cdiv(r_m, 32)), dim3(32, 8), 0, h->stream>>>(
+        d_m, r_m, V, nch, (int)kc, PB, PB2);
     h->launches++;
     CHECK_LAUNCH(h);
   }
@@ -2766,20 +2766,25 @@ int sdn_encode_fields(sdn_handle* h, const float* m, int64_t n, int64_t d_m, con
     }
     ProfScope ps(h, PC_OTHER, 2.0 * rows * r_m * d_m, 4.0 * rows * d_m);
     if (enc_tc) {
-      const int64_t pa = tc_rows * ldk, pb = (int64_t)r_m * ldk;
-      k_split3<<<(unsigned)std::min<int64_t>(cdiv(rows * ldk, 256), 16384), 256, 0, h->stream>>>(
-          rows, (int)d_m, d_m, src, ldk, PA, PA + pa, PA + 2 * pa);
+      k_split3<<<(unsigned)std::min<int64_t>(cdiv(rows * nch * kc / 8, 256), 65536), 256, 0, h->stream>>>(
+          rows, (int)d_m, d_m, src, nch, (int)kc, tc_rows, PA);
       h->launches++;
       CHECK_LAUNCH(h);
-      const int pass[4][4] = {{0, 1, 0, 1}, {1, 2, 1, 2}, {2, 3, 0, 3}, {0, 3, 2, 3}};   // planes: A hi, A lo, B hi, B lo
-      for (int64_t k0 = 0; k0 < ldk; k0 += kc) {
-        for (int q = 0; q < 4; ++q) {
-          TcOperand ta, tb;
-          ta.hi = PA + pass[q][0] * pa + k0; ta.lo = PA + pass[q][1] * pa + k0; ta.ld = (int)ldk; ta.rows = rows;
-          tb.hi = PB + pass[q][2] * pb + k0; tb.lo = PB + pass[q][3] * pb + k0; tb.ld = (int)ldk; tb.rows = r_m;
-          TRY((gemm<false, true>(h, rows, nullptr, r_m, (int)kc, src + k0, d_m, V + k0 * r_m, r_m,
-                                 EpiAccum64{acc + s * r_m, (int64_t)r_m}, &tb, &ta, 1)));
-        }
+      for (int c = 0; c < nch; ++c) {
+        TcOperand ta, tb;
+        TcFlags fl;
+        // pass A: hi = (a0, a1), lo = (a1, a2) -- the same rows one segment on
+        ta.hi = PA + (int64_t)c * tc_rows * lda; ta.lo = ta.hi + kc; ta.ld = (int)lda; ta.rows = rows;
+        tb.hi = PB + (int64_t)c * r_m * lda; tb.lo = tb.hi + kc; tb.ld = (int)lda; tb.rows = r_m;
+        TRY((gemm<false, true>(h, rows, nullptr, r_m, (int)(2 * kc), src, d_m, V, r_m,
+                               EpiAccum64{acc + s * r_m, (int64_t)r_m}, &tb, &ta, 1, fl)));
+        // pass B: hi-only a2 b0 + a0 b2 (the lo halves are loaded and ignored)
+        // (lo = the hi rows shifted by 16 bytes: the same cache lines, never multiplied; the buffers carry slack)
+        ta.hi = PA + (int64_t)c * tc_rows * lda + 2 * kc; ta.lo = ta.hi + 8;
+        tb.hi = PB2 + (int64_t)c * r_m * ldb2; tb.lo = tb.hi + 8; tb.ld = (int)ldb2;
+        fl.hi_only = 1;
+        TRY((gemm<false, true>(h, rows, nullptr, r_m, (int)(2 * kc), src, d_m, V, r_m,
+                               EpiAccum64{acc + s * r_m, (int64_t)r_m}, &tb, &ta, 1, fl)));
       }
       continue;
     }

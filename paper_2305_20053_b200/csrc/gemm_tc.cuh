@@ -1122,6 +1122,7 @@ struct TileEpi<EpiBwdSum> {
 struct TcFlags {
   const int* in = nullptr;   // readiness of this GEMM's A operand rows (null: whole-grid dependency)
   int* out = nullptr;        // readiness of this GEMM's outputs
+  int hi_only = 0;           // issue only the hi x hi MMAs (the lo halves are loaded but ignored): encoder pass B
 };
 
 // persistent tile walk of one CTA: tiles t0, t0 + ts, ...; a tile covers
@@ -1589,8 +1590,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ C
             const uint64_t bl = tcx::sdesc_k64(base + 2 * C::A_BYTES + C::B_BYTES + kk * 32);
             if constexpr (CG == 1) {
               tcx::mma_bf16(d, ah, bh, idesc, (kb | kk) != 0);
-              tcx::mma_bf16(d, ah, bl, idesc, 1);
-              tcx::mma_bf16(d, al, bh, idesc, 1);
+              if (!flags.hi_only) {
+                tcx::mma_bf16(d, ah, bl, idesc, 1);
+                tcx::mma_bf16(d, al, bh, idesc, 1);
+              }
             } else {
               tcx::mma_bf16_pair(d, ah, bh, idesc, (kb | kk) != 0);
               tcx::mma_bf16_pair(d, ah, bl, idesc, 1);

@@ -1093,34 +1093,53 @@ k_dec_c(int64_t d_u, int r_u, const float* __restrict__ U, const float* __restri
 }
 // ---- tensor-core encoder operands: a three-way bf16 split x = p0 + p1 + p2
 // (p0 = bf16(x), p1 = bf16(x - p0), p2 = bf16(x - p0 - p1): 24 mantissa bits,
-// every subtraction exact), planes of ldp columns (columns >= cols zero).
-// With both operands split three ways, the products p_i q_j with i + j <= 2 carry
-// the fp32 product to ~2^-24; four bf16x3 GEMM passes over plane pairs cover
-// them (engine.cu, sdn_encode_fields).
-__global__ void k_split3(int64_t rows, int cols, int64_t ld_src, const float* __restrict__ src, int64_t ldp,
-                         __nv_bfloat16* __restrict__ p0, __nv_bfloat16* __restrict__ p1,
-                         __nv_bfloat16* __restrict__ p2) {
-  const int64_t total = rows * ldp;
+// every subtraction exact).  With both operands split three ways, the products
+// p_i q_j with i + j <= 2 carry the fp32 product to ~2^-24.  Layout, per K chunk
+// of kc columns and per row: segments [p0 | p1 | p2 | p0] of kc values each
+// (chunk-major, row length 4 kc), so that
+//   pass A = ONE bf16x3 GEMM over K' = 2 kc with hi = the row at +0 (p0, p1) and
+//            lo = the same row at +kc (p1, p2): (p0;p1)x(q0;q1) + (p1;p2)x(q1;q2),
+//   pass B = ONE hi-only GEMM over K' = 2 kc with A hi at +2 kc (p2, p0) and B
+//            from a second buffer [q0 | q2]: p2 q0 + p0 q2
+// (engine.cu, sdn_encode_fields).  Columns >= cols are zero.
+SDN_DEV void split3(float x, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
+  a = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(a);
+  b = __float2bfloat16_rn(r1);
+  c = __float2bfloat16_rn(r1 - __bfloat162float(b));
+}
+// (chunk-major: chunk ch of every row first -- P[ch][row][4 kc] -- so a GEMM tile's
+// rows are 8 KB apart instead of a whole plane row: DRAM pages are reused across
+// the tile's k-blocks; rows_alloc = rows of the buffer per chunk)
+__global__ void k_split3(int64_t rows, int cols, int64_t ld_src, const float* __restrict__ src, int nch, int kc,
+                         int64_t rows_alloc, __nv_bfloat16* __restrict__ P) {
+  // eight consecutive columns per thread: four 16-byte stores (kc % 8 == 0)
+  const int64_t per_row = (int64_t)nch * kc, groups = per_row / 8, total = rows * groups;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / ldp;
-    const int c = (int)(e - r * ldp);
-    const float x = c < cols ? src[r * ld_src + c] : 0.0f;
-    const __nv_bfloat16 a = __float2bfloat16_rn(x);
-    const float r1 = x - __bfloat162float(a);
-    const __nv_bfloat16 b = __float2bfloat16_rn(r1);
-    const float r2 = r1 - __bfloat162float(b);
-    p0[e] = a;
-    p1[e] = b;
-    p2[e] = __float2bfloat16_rn(r2);
+    const int64_t r = e / groups;
+    const int64_t k = (e - r * groups) * 8;
+    const int64_t ch = k / kc, kk = k - ch * kc;
+    union { __nv_bfloat16 v[8]; uint4 u; } pa, pb, pc;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float x = k + j < cols ? __ldg(src + r * ld_src + k + j) : 0.0f;
+      split3(x, pa.v[j], pb.v[j], pc.v[j]);
+    }
+    __nv_bfloat16* q = P + (ch * rows_alloc + r) * 4 * kc + kk;
+    *reinterpret_cast<uint4*>(q) = pa.u;
+    *reinterpret_cast<uint4*>(q + kc) = pb.u;
+    *reinterpret_cast<uint4*>(q + 2 * kc) = pc.u;
+    *reinterpret_cast<uint4*>(q + 3 * (int64_t)kc) = pa.u;
   }
 }
-// the same for V (d x r, row-major) transposed: planes hold V^T (r rows of ldp columns)
-__global__ void k_split3_transpose(int64_t d, int r, const float* __restrict__ V, int64_t ldp,
-                                   __nv_bfloat16* __restrict__ p0, __nv_bfloat16* __restrict__ p1,
-                                   __nv_bfloat16* __restrict__ p2) {
+// the same for V (d x r, row-major) transposed: rows of V^T in P ([q0 | q1 | q2 | q0]
+// per chunk, chunk-major) and the pass-B operand [q0 | q2] per chunk in P2 (row length 2 kc)
+__global__ void k_split3_transpose(int64_t d, int r, const float* __restrict__ V, int nch, int kc,
+                                   __nv_bfloat16* __restrict__ P, __nv_bfloat16* __restrict__ P2) {
   __shared__ float tile[32][33];
   const int64_t d0 = (int64_t)blockIdx.x * 32;
   const int j0 = blockIdx.y * 32;
+  const int64_t per_row = (int64_t)nch * kc;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int64_t dd = d0 + i;
     const int j = j0 + threadIdx.x;
@@ -1129,16 +1148,15 @@ __global__ void k_split3_transpose(int64_t d, int r, const float* __restrict__ V
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int j = j0 + i;
-    const int64_t dd = d0 + threadIdx.x;
-    if (j < r && dd < ldp) {
-      const float x = tile[threadIdx.x][i];
-      const __nv_bfloat16 a = __float2bfloat16_rn(x);
-      const float r1 = x - __bfloat162float(a);
-      const __nv_bfloat16 b = __float2bfloat16_rn(r1);
-      const int64_t e = (int64_t)j * ldp + dd;
-      p0[e] = a;
-      p1[e] = b;
-      p2[e] = __float2bfloat16_rn(r1 - __bfloat162float(b));
+    const int64_t k = d0 + threadIdx.x;
+    if (j < r && k < per_row) {
+      __nv_bfloat16 a, b, c;
+      split3(tile[threadIdx.x][i], a, b, c);
+      const int64_t ch = k / kc, kk = k - ch * kc;
+      __nv_bfloat16* q = P + (ch * r + j) * 4 * kc + kk;
+      q[0] = a; q[kc] = b; q[2 * kc] = c; q[3 * (int64_t)kc] = a;
+      __nv_bfloat16* q2 = P2 + (ch * r + j) * 2 * kc + kk;
+      q2[0] = a; q2[kc] = c;
     }
   }
 }
