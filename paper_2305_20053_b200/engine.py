@@ -79,6 +79,7 @@ class Engine:
         self.r_u4 = self.pw[-1]
         self._widths_c = (C.c_int32 * len(w))(*self.pw)
         self._multi_cache = {}
+        self._multi_last = None      # (risks list object, n, entry snapshots, cached argument block) of the last call
         cfg = _lib.Config(n_layers=len(model.weights), widths=self._widths_c, r_m=self.r_m4, d_z=self.d_z,
                           activation=_lib.ACT[model.activation], residual=int(bool(model.residual)),
                           gemm=_lib.GEMM[gemm], device=self.device, max_samples=self.max_samples)
@@ -338,8 +339,16 @@ class Engine:
         eval_multi_wait() blocks and returns the results."""
         # the ctypes argument blocks of a risk configuration are built once and
         # reused (repeated calls replay one device graph; keep the host side lean)
-        key = (self.n, tuple(tuple(sorted((k, v) for k, v in r.items() if k != "t")) for r in risks))
-        cached = self._multi_cache.get(key)
+        # (same list object with unchanged entries: skip rebuilding the key -- dict equality is cheap;
+        # entries carrying a per-call "t" take the keyed path)
+        last = self._multi_last
+        if (last is not None and last[0] is risks and last[1] == self.n and len(risks) == len(last[2])
+                and all("t" not in r and r == s for r, s in zip(risks, last[2]))):
+            cached = last[3]
+        else:
+            key = (self.n, tuple(tuple(sorted((k, v) for k, v in r.items() if k != "t")) for r in risks))
+            cached = self._multi_cache.get(key)
+            self._multi_last = None
         if cached is None:
             rs = [self.make_risk(**r) for r in risks]
             arr = (_lib.Risk * len(rs))(*rs)
@@ -352,6 +361,8 @@ class Engine:
             if len(self._multi_cache) > 16:
                 self._multi_cache.clear()
             self._multi_cache[key] = cached
+        if self._multi_last is None and not any("t" in r for r in risks):
+            self._multi_last = (risks, self.n, [dict(r) for r in risks], cached)
         arr, res, grads, ks, idx, gptr, iptr = cached
         for i, r in enumerate(risks):           # t is per call (the optimizer's auxiliary variable)
             if r["kind"] == "cvar":
