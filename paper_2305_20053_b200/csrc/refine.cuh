@@ -643,31 +643,35 @@ __global__ void __launch_bounds__(REF_THREADS, 1) k_refine(RefineArgs a) {
     REF_STAMP(42);
     return;
   }
-  // small band: one block ranks every band row against the others
+  // small band: one block ranks every band row against the others.  The band's
+  // rows, keys and old mask bits are read into shared memory once (two global
+  // round trips instead of two per pair of rows: this phase is on the c2
+  // evaluation's critical path)
   if (blockIdx.x != 0) return;
+  __shared__ unsigned long long s_key[REF_RESELECT_SMALL];
+  __shared__ int s_row[REF_RESELECT_SMALL];
   if (tid == 0) S.need = 0;
   __syncthreads();
   int cnt = 0;
-  for (int r = tid; r < m; r += REF_THREADS) cnt += __ldcg(a.mask + __ldcg(a.rowidx + r)) ? 1 : 0;
+  for (int r = tid; r < m; r += REF_THREADS) {
+    const int ri = __ldcg(a.rowidx + r);
+    s_row[r] = ri;
+    s_key[r] = (unsigned long long)dkey(__ldcg(a.Q + ri));
+    cnt += __ldcg(a.mask + ri) ? 1 : 0;
+  }
   atomicAdd(&S.need, cnt);
   __syncthreads();
   const int need = S.need;
-  bool selr[REF_RESELECT_SMALL / REF_THREADS];
-  int t = 0;
-  for (int r = tid; r < m; r += REF_THREADS, ++t) {
-    const int ri = __ldcg(a.rowidx + r);
-    const uint64_t ki = dkey(__ldcg(a.Q + ri));
+  for (int r = tid; r < m; r += REF_THREADS) {
+    const int ri = s_row[r];
+    const unsigned long long ki = s_key[r];
     int rank = 0;
     for (int u = 0; u < m; ++u) {
-      const int rj = __ldcg(a.rowidx + u);
-      const uint64_t kj = dkey(__ldcg(a.Q + rj));
-      rank += (kj > ki || (kj == ki && rj < ri)) ? 1 : 0;
+      const unsigned long long kj = s_key[u];
+      rank += (kj > ki || (kj == ki && s_row[u] < ri)) ? 1 : 0;
     }
-    selr[t] = rank < need;
+    a.mask[ri] = rank < need ? 1 : 0;            // (ranks use the shared copies only: no ordering needed)
   }
-  __syncthreads();                               // every rank computed from the pre-update mask
-  t = 0;
-  for (int r = tid; r < m; r += REF_THREADS, ++t) a.mask[__ldcg(a.rowidx + r)] = selr[t] ? 1 : 0;
   REF_STAMP(42);
 }
 
