@@ -206,10 +206,16 @@ SDN_DEV void ref_rows(const RefineArgs& a, const RefineLayer& ly, double* xs, in
   __syncthreads();
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && r0 == 0) a.trace[first ? 30 : (last ? 31 : 32)] = gtime();
   // columns of this warp: c = gw, gw + nw, ...; the next column's W row is
-  // loaded while the current one is reduced (software pipeline)
+  // loaded while the current one is reduced (software pipeline).  The fp64
+  // epilogues (bias, activation with its exp, residual, store) of up to four
+  // columns run together: after the butterfly the four lanes 4j..4j+3 all hold
+  // row j's total, so lane 4j + i finishes column i instead of lane 4j doing
+  // four activations one after another.
   float wf[KC / 32];
   int c = gw;
   if (c < N) ref_load_w<KC>(ly.W + (int64_t)c * K + k0, Kc, lane, wf);
+  double vq[4] = {0.0, 0.0, 0.0, 0.0};
+  int cq0 = gw, nq = 0;                       // queued columns: cq0 + i nw, i < nq
   for (; c < N; c += nw) {
     float wn[KC / 32];
     if (c + nw < N) ref_load_w<KC>(ly.W + (int64_t)(c + nw) * K + k0, Kc, lane, wn);
@@ -217,26 +223,34 @@ SDN_DEV void ref_rows(const RefineArgs& a, const RefineLayer& ly, double* xs, in
     if (rb <= 2) v = ref_column<2, KC>(xs, wf, Kc, lane);
     else if (rb <= 4) v = ref_column<4, KC>(xs, wf, Kc, lane);
     else v = ref_column<8, KC>(xs, wf, Kc, lane);
-    const int j = lane >> 2;                 // row whose total this lane holds
-    if ((lane & 3) == 0 && j < rb) {
-      double* dst = out + (int64_t)(r0 + j) * N + c;
-      if (!kfirst) v += *dst;                  // earlier K chunks (written by this lane)
-      if (!klast) {
-        *dst = v;
-      } else {
-        const double S = v + (first ? a.zb64[c] : (double)ly.b[c]);
-        double o;
-        if (last) {
-          o = (double)a.omean[c] + (double)a.ostd[c] * S;
-        } else if (a.softmax) {
-          o = S;                                        // normalised by the row pass below
+    if (nq == 0) cq0 = c;
+    if (nq == 0) vq[0] = v; else if (nq == 1) vq[1] = v; else if (nq == 2) vq[2] = v; else vq[3] = v;
+    ++nq;
+    if (nq == 4 || c + nw >= N) {
+      const int i = lane & 3, j = lane >> 2;   // this lane's queued column and row
+      const int ci = cq0 + i * nw;
+      double vi = i == 0 ? vq[0] : i == 1 ? vq[1] : i == 2 ? vq[2] : vq[3];
+      if (i < nq && j < rb) {
+        double* dst = out + (int64_t)(r0 + j) * N + ci;
+        if (!kfirst) vi += *dst;                 // earlier K chunks (written by this lane)
+        if (!klast) {
+          *dst = vi;
         } else {
-          o = act64(a.act, S);
-          if (ly.resid)                                 // resid: K == N
-            o += (kfirst && c < Kc) ? xs[j * REF_KC + c] : __ldcg(in64 + (int64_t)(r0 + j) * K + c);
+          const double S = vi + (first ? a.zb64[ci] : (double)ly.b[ci]);
+          double o;
+          if (last) {
+            o = (double)a.omean[ci] + (double)a.ostd[ci] * S;
+          } else if (a.softmax) {
+            o = S;                                        // normalised by the row pass below
+          } else {
+            o = act64(a.act, S);
+            if (ly.resid)                                 // resid: K == N
+              o += (kfirst && ci < Kc) ? xs[j * REF_KC + ci] : __ldcg(in64 + (int64_t)(r0 + j) * K + ci);
+          }
+          *dst = o;
         }
-        *dst = o;
       }
+      nq = 0;
     }
 #pragma unroll
     for (int u = 0; u < KC / 32; ++u) wf[u] = wn[u];
