@@ -688,12 +688,12 @@ def main():
             "kernel_classes": per_class,
             "clocks": clk.summary(),
         }
-        one_launch = (world == 1 and launches <= 2 * args.steps and args.gemm == "auto")
+        one_launch = (world == 1 and launches <= 3 * args.steps and args.gemm == "auto")
         if one_launch:
             # small sample sets run the whole evaluation in one launch (csrc/small.cuh, fp32 FFMA);
             # the per-class profile above is the layer-by-layer path (profiling disables the one-launch path)
             line["dtype"] = "f32 (FFMA; fp64 QoI, moments and reductions)"
-            line["path"] = "one launch per evaluation (k_small_eval); kernel_classes/roofline: the layer-by-layer path"
+            line["path"] = "one evaluation kernel (k_small_eval) + the z fetch per evaluation; kernel_classes/roofline: the layer-by-layer path"
             flops = cfg.flops_forward() + cfg.flops_backward() if hasattr(cfg, "flops_backward") else None
             if flops and dev_steps:
                 line["one_launch_tflops"] = flops * n_loc / (sum(dev_steps) / args.steps / 1e3) / 1e12
