@@ -220,6 +220,10 @@ struct sdn_handle {
   std::vector<int64_t*> x_gidx; // global indices of each kept selection (ascending)
   std::vector<int64_t> x_gcap;
   // short tail (k_sel_colsum_sl + k_finalize_export): sliced selected-row sums, finalise + export in one launch
+  // QoI partials written by the output layer's epilogue (cap x r_u/16 chunk planes), summed by k_qoi_part
+  double* qp = nullptr;
+  bool qoi_fuse = true;         // env SDN_NO_QOI_FUSE=1: k_qoi reads Y back instead
+  bool q_fused = false;         // the last forward wrote qp
   bool tail_fuse = true;        // env SDN_NO_TAIL_FUSE=1 disables (c2: 0.3117 -> 0.3086 ms with the direct host writes)
   bool tail_export = false;     // env SDN_TAIL_EXPORT=1: the finalise kernel writes the host results itself (no export launch)
   bool exp_want = false, exp_done = false;   // enqueue_multi asks the tail to export; the tail says it did
@@ -575,6 +579,10 @@ static int run_forward(sdn_handle* h, int64_t nrows, const float* X, int64_t ld0
       EpiAffine e{bl, h->ostd, h->omean, phi_out, (int64_t)n_out};
       if (fuse_seed && tc && L > 1) {      // + the reverse sweep's unit seeds (bf16x3 split)
         EpiAffineSeed es{e, h->seed_a2, h->seed_b2, TcEpiSplit{&h->sw->seed}};
+        if (h->qoi_fuse && n_out == h->r_u && n_out % 16 == 0 && nrows <= h->cap && phi_out == h->Y) {
+          es.cq = h->c; es.qp = h->qp; es.qld = h->cap;     // + the QoI's chunk partials (launch_qoi: k_qoi_part)
+          h->q_fused = true;
+        }
         TRY((gemm<false, true>(h, nrows, nullptr, n_out, K, in, ldin, Wl, ldW, es, tB, tA, 1, flags_of(l))));
         h->seed_fused = true;
       } else {
@@ -816,6 +824,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   if ((rc = dalloc(h, &h->n_act_dev, 1))) return bail(rc);
   h->qgrid = (int)std::min<int64_t>(cdiv(cap, 8), 2 * h->num_sms);
   if ((rc = dalloc(h, &h->qpart, (size_t)h->qgrid * STATS_LEN))) return bail(rc);
+  if ((rc = dalloc(h, &h->qp, (size_t)cap * (size_t)cdiv(h->r_u, 16)))) return bail(rc);
   h->crb = (int)std::min<int64_t>(cdiv(cap, 8), 16);
   if ((rc = dalloc(h, &h->stats_loc, STATS_LEN))) return bail(rc);
   if ((rc = dalloc(h, &h->partial_loc, h->plen()))) return bail(rc);
@@ -868,6 +877,7 @@ int sdn_create(const sdn_config* cfg, sdn_handle** out) {
   { const char* e = getenv("SDN_NO_GRAPH"); h->use_graphs = !(e && e[0] == '1'); }
   { const char* e = getenv("SDN_TIMELINE"); h->tl_on = e && e[0] == '1'; }
   h->tail_fuse = !(getenv("SDN_NO_TAIL_FUSE") && getenv("SDN_NO_TAIL_FUSE")[0] == '1');
+  h->qoi_fuse = !(getenv("SDN_NO_QOI_FUSE") && getenv("SDN_NO_QOI_FUSE")[0] == '1');
   h->tail_export = getenv("SDN_TAIL_EXPORT") && getenv("SDN_TAIL_EXPORT")[0] == '1';
   h->side_sms = std::max(1, std::min(SDN_SIDE_SMS_DEFAULT, h->num_sms / 4));
   { const char* e = getenv("SDN_SIDE_SMS");
@@ -1173,6 +1183,7 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
                         bool fuse_seed = false, bool defer_qoi = false) {
   if (!all) { all = risk; n_all = 1; slot = 0; }
   h->seed_fused = false;
+  h->q_fused = false;
   if (!h->have_model) return fail(SDN_ERR_STATE, "set_model first");
   if (risk->qoi == SDN_QOI_REDUCED && !h->have_form) return fail(SDN_ERR_STATE, "set_tracking first");
   if (risk->qoi == SDN_QOI_DECODED && !h->have_dec) return fail(SDN_ERR_STATE, "set_decoder first");
@@ -1220,10 +1231,24 @@ static int launch_qoi(sdn_handle* h, const sdn_risk* risk, double* stats_dev, co
   const bool dec = risk->qoi == SDN_QOI_DECODED;
   const double q0 = dec ? h->q0dec : h->q0;
   const int qg = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(h->n, 1), 8), h->qgrid));
+  // Q also goes to the exact-CVaR selection's copy (sel_q: no copy node ahead of the selection), unless a
+  // smoothed-CVaR window refinement is about to change Q in place
+  // (study switch SDN_Q2_WRITE=1, off: measured 1-2 us slower per c2 evaluation than the copy node)
+  static const bool q2w = getenv("SDN_Q2_WRITE") && getenv("SDN_Q2_WRITE")[0] == '1';
+  double* q2 = (q2w && risk->kind != SDN_RISK_CVAR_SMOOTH && h->Qr && h->n > 0) ? h->Qr : nullptr;
+  if (h->q_fused && !dec && h->n > 0) {             // the output layer left the row's chunk partials
+    const int nch = h->r_u / 16;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(h->n, 128), h->qgrid));
+    ProfScope ps(h, PC_QOI, 2.0 * h->n * nch, 8.0 * h->n * (nch + 1));
+    k_qoi_part<<<g, 128, 0, h->stream>>>(h->n, nch, h->qp, h->cap, q0, h->shift, risk->t,
+                                         risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0, h->Q, h->qpart, tp,
+                                         h->red_counter, stats_dev, q2);
+  } else
   { ProfScope ps(h, PC_QOI, 4.0 * h->n * h->r_u, 4.0 * h->n * h->r_u * (dec ? 2 : 1) + 8.0 * h->n);
   k_qoi<<<qg, 256, 0, h->stream>>>(h->n, h->r_u, h->Y, dec ? h->KPhi : nullptr, dec ? h->cdec : h->c, q0,
                                    h->shift, risk->t, risk->kind == SDN_RISK_CVAR_SMOOTH ? risk->eps : 1.0,
-                                   h->Q, h->qpart, tp, h->red_counter, stats_dev); }
+                                   h->Q, h->qpart, tp, h->red_counter, stats_dev, q2); }
+  if (q2) h->qr_valid = true;
   tl_mark(h, 3, h->stream);
   h->launches += 1;
   CHECK_LAUNCH(h);
@@ -1737,6 +1762,7 @@ static int enqueue_small(sdn_handle* h, const double* z, const sdn_risk* risks, 
   h->risk = risks[0];
   h->fwd_risk = risks[0];
   h->seed_fused = false;
+  h->q_fused = false;
   h->selected = false;
   h->compacted = false;
   h->qr_valid = false;

@@ -84,6 +84,12 @@ struct EpiAffineSeed {
   const float* a2;
   const float* b2;
   TcEpiSplit seed;
+  // fused QoI (reduced frame): every 16-column chunk's fp64 partial of
+  // phi . (phi + 2 c) -> qp[chunk][row] (row stride qld); k_qoi_part sums a row's
+  // chunks in order, adds q0 and takes the moments (the tensor-core tile path only)
+  const float* cq = nullptr;
+  double* qp = nullptr;
+  int64_t qld = 0;
   SDN_DEV void operator()(int64_t r, int c, float4 v) const {
     float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -752,6 +758,19 @@ struct TileEpi<EpiAffineSeed> {
       sd[j + 1] = fmaf(a2.y, x[j + 1], b2.y);
       sd[j + 2] = fmaf(a2.z, x[j + 2], b2.z);
       sd[j + 3] = fmaf(a2.w, x[j + 3], b2.w);
+    }
+    if (e.qp) {                                  // this row's QoI partial over the chunk's columns (fp64)
+      double q = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 cc = __ldg(reinterpret_cast<const float4*>(e.cq + min(c0 + j, N - 4)));
+        const double p0 = x[j], p1 = x[j + 1], p2 = x[j + 2], p3 = x[j + 3];
+        q += p0 * (p0 + 2.0 * (double)cc.x);
+        q += p1 * (p1 + 2.0 * (double)cc.y);
+        q += p2 * (p2 + 2.0 * (double)cc.z);
+        q += p3 * (p3 + 2.0 * (double)cc.w);
+      }
+      if (tr.r0 + lane < tr.M) e.qp[(int64_t)(c0 >> 4) * e.qld + tr.r0 + lane] = q;
     }
     epi_reclaim(s, lane);
     row_put(s.f0, lane, x);

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256)
 k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict__ kphi,
       const float* __restrict__ c, double q0, double shift, double t, double eps,
       double* __restrict__ Q, double* __restrict__ part, const double* __restrict__ tp = nullptr,
-      int* __restrict__ counter = nullptr, double* __restrict__ out = nullptr) {
+      int* __restrict__ counter = nullptr, double* __restrict__ out = nullptr, double* __restrict__ Q2 = nullptr) {
   if (tp) t = *tp;                     // device-side t (graph replay)
   __shared__ double sp[8][6];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -150,6 +150,7 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
       if (i < n) {
         const double q = (lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3]) + q0;
         Q[i] = q;
+        if (Q2) Q2[i] = q;             // the exact-CVaR selection's own copy (sel_q)
         double qs = q - shift, x = q - t;
         double d1 = splus_d1_d(x, eps);
         acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
@@ -162,6 +163,45 @@ k_qoi(int64_t n, int r_u, const float* __restrict__ phi, const float* __restrict
   if (threadIdx.x < 6) {
     double s = 0.0;
     for (int w = 0; w < 8; ++w) s += sp[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = s;
+  }
+  if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;
+  if (counter) last_block_sum(counter, gridDim.x, STATS_LEN, part, out);
+}
+
+// QoI from the output layer's fused chunk partials (EpiAffineSeed::qp,
+// gemm_tc.cuh): Q_i = q0 + sum over the row's 16-column chunks in order, then
+// the moments exactly as k_qoi takes them.  One thread per row (coalesced
+// chunk planes), fixed butterfly per warp, warps in order, last block sums.
+__global__ void __launch_bounds__(128)
+k_qoi_part(int64_t n, int nch, const double* __restrict__ P, int64_t ld, double q0, double shift, double t,
+           double eps, double* __restrict__ Q, double* __restrict__ part, const double* __restrict__ tp = nullptr,
+           int* __restrict__ counter = nullptr, double* __restrict__ out = nullptr, double* __restrict__ Q2 = nullptr) {
+  if (tp) t = *tp;                     // device-side t (graph replay)
+  __shared__ double sp[4][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 128) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int ch = 0; ch < nch; ++ch) s += P[(int64_t)ch * ld + i];
+    const double q = s + q0;
+    Q[i] = q;
+    if (Q2) Q2[i] = q;                 // the exact-CVaR selection's own copy (sel_q)
+    const double qs = q - shift, x = q - t;
+    const double d1 = splus_d1_d(x, eps);
+    acc[0] += 1.0; acc[1] += qs; acc[2] += qs * qs;
+    acc[3] += splus_d(x, eps); acc[4] += d1; acc[5] += (d1 > 0.0) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const double v = warp_sum(acc[f]);
+    if (lane == 0) sp[warp][f] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int w = 0; w < 4; ++w) s += sp[w][threadIdx.x];
     part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = s;
   }
   if (threadIdx.x == 6 || threadIdx.x == 7) part[(int64_t)blockIdx.x * STATS_LEN + threadIdx.x] = 0.0;

@@ -130,3 +130,28 @@ def test_ring_epilogues_bit_identical_to_register_prefetch_path(tmp_path):
         outs.append(np.load(out))
     for k in ("q", "g0", "g1", "v", "idx"):
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+def test_fused_qoi_partials_match_the_row_kernel(monkeypatch):
+    """The output layer's epilogue leaves each row's fp64 QoI partials per
+    16-column chunk (k_qoi_part sums them); SDN_NO_QOI_FUSE=1 (read when the
+    handle is created) reads phi back with k_qoi instead.  Same fp32 phi, fp64
+    sums in a different order: Q agrees to rounding, the exact-CVaR selection
+    and the risk values do not move, and the fused Q matches the oracle."""
+    n = 4096 + 77                     # a partly filled last row tile
+    risks = [dict(kind="meanvar", beta=1.0, alpha=1e-2), dict(kind="cvar_exact", beta=0.95, alpha=1e-2)]
+    res = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("SDN_NO_QOI_FUSE", "1")
+        p, eng = _setup("c2", n, "tc", seed=5)
+        out = eng.eval_multi(p.z, risks)
+        res.append((eng.last_q().copy(), out, eng.kernel_launches()))
+    (qa, oa, _), (qb, ob, _) = res
+    assert np.max(np.abs(qa - qb) / np.abs(qb)) <= 1e-14
+    assert np.array_equal(np.sort(oa[1].idx), np.sort(ob[1].idx))
+    for a, b in zip(oa, ob):
+        assert abs(a.value - b.value) <= 1e-13 * abs(b.value)
+        assert _rel(a.grad_z, b.grad_z) <= 1e-12
+    Qo, _ = ref.evaluate_reverse(ref.as_oracle(p), p.m_r, p.z, form=ref.ReducedForm(p.c.astype(np.float64), p.q0))
+    assert _rel(qa, Qo) <= 2e-5
