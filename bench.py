@@ -104,6 +104,8 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.stamps = []
+        self.t0 = None
 
     def __enter__(self):
         try:
@@ -118,7 +120,20 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
+            self.stamps.append(time.monotonic())
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout: float = 3.0):
+        """Block until nvidia-smi has delivered its first sample (its start-up --
+        NVML initialisation, device enumeration -- takes driver locks for tens of
+        milliseconds; a timed region that begins meanwhile sees launch stalls)."""
+        t_end = time.monotonic() + timeout
+        while self.proc and not self.lines and time.monotonic() < t_end:
+            time.sleep(0.01)
+
+    def mark(self):
+        """Start of the timed region: summary() uses the samples taken from here on."""
+        self.t0 = time.monotonic()
 
     def __exit__(self, *a):
         if self.proc:
@@ -135,7 +150,11 @@ class ClockSampler:
             return None
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.t0 is not None:
+            timed = [ln for ts, ln in zip(self.stamps, self.lines) if ts >= self.t0]
+            lines = timed or self.lines
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -558,16 +577,21 @@ def main():
             dist.barrier()
             torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    barrier()
-
-    # ---- timed region: device time per step (CUDA events on the engine's stream)
-    launches0 = eng.kernel_launches()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # the clock sampler starts ahead of the warm-up: nvidia-smi's start-up (NVML initialisation) holds driver locks
+    # for tens of ms, which a timed region beginning right behind it would see as launch stalls; its samples count
+    # from clk.mark() on
     with ClockSampler(local_rank) as clk:
+        for _ in range(max(args.warmup, 3)):
+            step()
         barrier()
+        clk.wait_first()
+
+        # ---- timed region: device time per step (CUDA events on the engine's stream)
+        launches0 = eng.kernel_launches()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        barrier()
+        clk.mark()
         dev_steps = []
         for i in range(args.steps):
             flush.zero_()                     # L2 flush between steps (untimed)
