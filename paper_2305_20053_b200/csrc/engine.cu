@@ -224,6 +224,7 @@ struct sdn_handle {
   double* qp = nullptr;
   bool qoi_fuse = true;         // env SDN_NO_QOI_FUSE=1: k_qoi reads Y back instead
   bool q_fused = false;         // the last forward wrote qp
+  bool z_by_kernel = false;     // upload_z used the fetch kernel (k_zbias may launch programmatically behind it)
   bool tail_fuse = true;        // env SDN_NO_TAIL_FUSE=1 disables (c2: 0.3117 -> 0.3086 ms with the direct host writes)
   bool tail_export = false;     // env SDN_TAIL_EXPORT=1: the finalise kernel writes the host results itself (no export launch)
   bool exp_want = false, exp_done = false;   // enqueue_multi asks the tail to export; the tail says it did
@@ -1084,10 +1085,12 @@ static void stage_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n
 // (z reaches the device once -- by a one-block fetch kernel or a copy node -- rather than every
 // k_zbias block reading it from host-mapped memory, which measured slower)
 __global__ void k_fetch_small(int n, const double* __restrict__ src_host, double* __restrict__ dst) {
+  asm volatile("griddepcontrol.launch_dependents;");       // k_zbias loads its Pz rows meanwhile
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src_host[i];
 }
 static int upload_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n_risks) {
   stage_z(h, z, risks, n_risks);
+  h->z_by_kernel = false;
   // one small block reads the pinned (host-mapped) staging buffer over PCIe instead of a copy node: the same
   // device span, a cheaper graph launch on the host (c2 e2e 50.2 -> 50.6 M samples/s); SDN_Z_KERNEL=0: the copy node
   static const bool zk = !(getenv("SDN_Z_KERNEL") && getenv("SDN_Z_KERNEL")[0] == '0');
@@ -1095,6 +1098,7 @@ static int upload_z(sdn_handle* h, const double* z, const sdn_risk* risks, int n
     double* src = nullptr;
     CU(cudaHostGetDevicePointer((void**)&src, h->hz, 0));
     k_fetch_small<<<1, 128, 0, h->stream>>>(h->d_z + SDN_RMAX, src, h->zdev);
+    h->z_by_kernel = true;
     h->launches++;
     CHECK_LAUNCH(h);
     return SDN_OK;
@@ -1207,8 +1211,16 @@ static int eval_forward(sdn_handle* h, const double* z, const sdn_risk* risk, do
   TRY(upload_z(h, z, all, n_all));
   const double* tp = h->zdev + h->d_z + slot;
   { ProfScope ps(h, PC_ZBIAS, 2.0 * h->h1 * h->d_z, 8.0 * h->h1 * h->d_z);
-  k_zbias<<<(unsigned)cdiv(h->h1, 8), 256, 0, h->stream>>>(h->h1, h->d_z, h->Pz, h->zdev, h->b[0], h->zb,
-                                                             h->zb64); }
+  // (behind the z fetch kernel: a programmatic dependent launch -- its blocks load their Pz rows while z arrives)
+  static const bool zpdl = !(getenv("SDN_NO_PDL") || (getenv("SDN_Z_PDL") && getenv("SDN_Z_PDL")[0] == '0'));
+  cudaLaunchConfig_t zc{};
+  zc.gridDim = dim3((unsigned)cdiv(h->h1, 8)); zc.blockDim = dim3(256); zc.dynamicSmemBytes = 0; zc.stream = h->stream;
+  cudaLaunchAttribute za[1];
+  za[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  za[0].val.programmaticStreamSerializationAllowed = (zpdl && h->z_by_kernel && !h->tl_on && !h->prof) ? 1 : 0;
+  zc.attrs = za; zc.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&zc, k_zbias, h->h1, h->d_z, (const double*)h->Pz, (const double*)h->zdev,
+                        (const float*)h->b[0], h->zb, h->zb64)); }
   tl_mark(h, 1);
   h->launches++;
   CHECK_LAUNCH(h);

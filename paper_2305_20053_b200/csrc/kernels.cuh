@@ -47,10 +47,24 @@ SDN_DEV void last_block_sum(int* counter, int nb, int w, const double* part, dou
 __global__ void __launch_bounds__(256)
 k_zbias(int h1, int d_z, const double* __restrict__ Pz, const double* __restrict__ z,
         const float* __restrict__ b1, float* __restrict__ zb, double* __restrict__ zb64 = nullptr) {
+  // programmatic dependent launch on both sides (no-ops in a plain launch): the forward chain behind this kernel
+  // may set itself up now, and -- launched behind the z fetch kernel -- this row's Pz entries (the cold HBM
+  // reads) are in registers before z is waited for
+  asm volatile("griddepcontrol.launch_dependents;");
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  double pz[4] = {0.0, 0.0, 0.0, 0.0};
+  if (c < h1) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lane + 32 * u < d_z) pz[u] = Pz[(int64_t)c * d_z + lane + 32 * u];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (c >= h1) return;
   double s = 0.0;
-  for (int k = lane; k < d_z; k += 32) s += Pz[(int64_t)c * d_z + k] * z[k];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (lane + 32 * u < d_z) s += pz[u] * z[lane + 32 * u];
+  for (int k = lane + 128; k < d_z; k += 32) s += Pz[(int64_t)c * d_z + k] * z[k];
   s = warp_sum(s);
   if (lane == 0) {
     zb[c] = (float)(s + (double)b1[c]);
