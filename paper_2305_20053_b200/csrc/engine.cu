@@ -1556,7 +1556,16 @@ static int backward_multi(sdn_handle* h, const sdn_risk* risks, int R, const uin
       fa.band = h->band_log; fa.hband = h->exp_b; fa.nband = h->exp_nb;
       h->exp_done = true;
     }
-    k_finalize_export<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(fa);
+    // (programmatic dependent launch behind the last sum kernel: its blocks prefetch their PzT rows meanwhile)
+    static const bool fpdl = !(getenv("SDN_NO_PDL") || (getenv("SDN_FIN_PDL") && getenv("SDN_FIN_PDL")[0] == '0'));
+    cudaLaunchConfig_t fc{};
+    fc.gridDim = dim3((unsigned)cdiv(h->d_z, 8), R); fc.blockDim = dim3(256); fc.dynamicSmemBytes = fsm;
+    fc.stream = h->stream;
+    cudaLaunchAttribute fat[1];
+    fat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    fat[0].val.programmaticStreamSerializationAllowed = (fpdl && !h->tl_on) ? 1 : 0;
+    fc.attrs = fat; fc.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&fc, k_finalize_export, fa));
   } else {
     k_finalize_multi<<<dim3((unsigned)cdiv(h->d_z, 8), R), 256, fsm, h->stream>>>(
         nrb_fin, plane, h->h1, h->d_z, part, h->PzT, h->vsum, h->plen(), partials);

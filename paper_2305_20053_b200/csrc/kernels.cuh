@@ -659,6 +659,7 @@ k_colsum64(int nrb, const int* __restrict__ n_act_dev, int w, const double* __re
 __global__ void __launch_bounds__(1024)
 k_sel_colsum_sl(int64_t k, const int* __restrict__ rows, int w, const float* __restrict__ u, int64_t ld,
                 const double* __restrict__ Q, double* __restrict__ out, double* __restrict__ vs) {
+  asm volatile("griddepcontrol.launch_dependents;");       // k_finalize_export prefetches its PzT rows meanwhile
   __shared__ double s[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x, S = gridDim.y, sl = blockIdx.y;
   const int64_t per = (k + S - 1) / S, lo = sl * per, hi = min(k, lo + per);
@@ -709,6 +710,12 @@ k_finalize_export(const FinArgs a) {
   extern __shared__ double A[];
   const int r = blockIdx.y, h1 = a.h1, d_z = a.d_z;
   const FinRisk& fr = a.risk[r];
+  // launched programmatically behind the last sum kernel (a no-op in a plain launch): this block's PzT rows
+  // (static, cold in L2 after the evaluation's traffic) are on their way before the sums are waited for
+  for (int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < d_z; k += gridDim.x * (blockDim.x >> 5))
+    for (int o = (threadIdx.x & 31) * 128; o < h1 * 8; o += 32 * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.PzT + (int64_t)k * h1) + o));
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int c = threadIdx.x; c < h1; c += blockDim.x) {
     double s = 0.0;
     if (fr.part)
